@@ -1,0 +1,194 @@
+/* pathgcn_b200 — C ABI of the B200-native backward-aggregation path.
+ *
+ * Drop-in for the four operator groups of the reference's C++ API
+ * (namespace pathgcn, /root/reference/proj/core/include/pathgcn/*.hpp):
+ * graph load, execution-path build, group partition, backward aggregate.
+ * Each entry point names the reference interface it replaces. Plain
+ * pointers and sizes only; device memory is owned by the opaque handles.
+ *
+ * Status codes (every function returns int): 0 ok; 2 config/shape/staleness
+ * (ConfigError, ShapeError, StalenessError — error.hpp:10-31); 3 io
+ * (IoError, error.hpp:33-35); 4 numeric (NumericError, error.hpp:37-47);
+ * 5 CUDA device/runtime failure. pg_last_error() returns the message of the
+ * calling thread's last failure.
+ *
+ * Threading (mirrors the reference's "synchronous, internally parallel"
+ * contract): build calls are synchronous; pg_backward_aggregate /
+ * pg_aggregate_pull / dense ops are asynchronous on the caller's stream and
+ * ACCUMULATE into the output like aggregate_pull (aggregate.hpp:50-55)
+ * unless PG_AGG_OVERWRITE is set (equivalent for a zeroed output). A handle
+ * is not thread-safe; distinct handles may be used concurrently. Multi-GPU:
+ * one handle set and one NCCL rank per device.
+ *
+ * There is no CPU fallback: without a CUDA device every call returns 5.
+ */
+#ifndef PATHGCN_B200_H
+#define PATHGCN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PG_OK 0
+#define PG_ERR_CONFIG 2
+#define PG_ERR_IO 3
+#define PG_ERR_NUMERIC 4
+#define PG_ERR_DEVICE 5
+
+/* WeightMode (csr_graph.hpp:13) */
+#define PG_WEIGHTS_UNIT 0
+#define PG_WEIGHTS_SYMNORM 1
+
+/* aggregation flags. CommitMode (aggregate.hpp:21): Deterministic is the
+ * default; PG_AGG_FAST selects Fast, which on the device runs the same
+ * atomic-free kernel (a valid Fast result, bit-equal to Deterministic) and
+ * reports the reference's Fast counters. */
+#define PG_AGG_FAST 1u
+#define PG_AGG_OVERWRITE 2u
+
+typedef struct pg_graph_s* pg_graph;         /* CsrGraph      csr_graph.hpp:19-38   */
+typedef struct pg_frontiers_s* pg_frontiers; /* FrontierSets  frontier.hpp:14-18    */
+typedef struct pg_path_s* pg_path;           /* ExecutionPath execution_path.hpp:16-33 */
+typedef struct pg_groups_s* pg_groups;       /* GroupedCsr    grouping.hpp:14-28    */
+
+int pg_last_error(char* buf, size_t cap);
+int pg_version(void);
+int pg_device_count(int* count);
+
+/* ---------------- graph load ---------------- */
+
+/* rmat.cpp:10-44 gen_rmat (host, same libstdc++ mt19937_64 stream):
+ * writes 2*m ids to pairs, *n_pad = padded vertex count. */
+int pg_gen_rmat(uint32_t n, uint64_t m, double a, double b, double c, double d, uint64_t seed,
+                uint32_t* pairs, uint32_t* n_pad);
+/* training_set.cpp:28-49 sample_training_set (host). *k = max(1, llround(ratio*n)). */
+int pg_training_set_size(uint32_t n, double ratio, uint64_t* k);
+int pg_sample_training_set(uint32_t n, double ratio, uint64_t seed, uint32_t* out);
+
+/* csr_graph.cpp:33-63 build_undirected_csr + :65-77 assign_edge_weights, on
+ * device. n_hint < 0: none. pairs: 2*npairs host ids. */
+int pg_graph_build(int device, int64_t n_hint, const uint32_t* pairs, uint64_t npairs,
+                   int weight_mode, pg_graph* out);
+/* Upload an existing host CsrGraph (offsets u64[n+1], neighbors u32[m],
+ * weights f64[m]); validates the CsrGraph invariants (sorted, unique,
+ * symmetric, symmetric weights) when validate != 0. */
+int pg_graph_create(int device, uint32_t n, const uint64_t* offsets, const uint32_t* neighbors,
+                    const double* weights, int validate, pg_graph* out);
+/* csr_graph.cpp:65-77 assign_edge_weights */
+int pg_graph_assign_weights(pg_graph g, int weight_mode);
+/* n, m, max_degree (csr_graph.cpp:13-17), FNV fingerprint (csr_graph.cpp:19-31) */
+int pg_graph_info(pg_graph g, uint32_t* n, uint64_t* m, uint32_t* max_degree, uint64_t* fingerprint);
+/* copy to host (any pointer may be NULL) */
+int pg_graph_export(pg_graph g, uint64_t* offsets, uint32_t* neighbors, double* weights);
+int pg_graph_destroy(pg_graph g);
+/* execution_path.cpp:17-22 path_fingerprint(g, V_t, L) */
+int pg_path_fingerprint(pg_graph g, const uint32_t* vt, uint64_t k, uint64_t layers, uint64_t* fp);
+
+/* ---------------- execution-path build ---------------- */
+
+/* frontier.cpp:7-26 compute_frontiers. vt: sorted unique host ids. */
+int pg_frontiers_compute(pg_graph g, const uint32_t* vt, uint64_t k, uint64_t layers, pg_frontiers* out);
+int pg_frontiers_size(pg_frontiers f, uint64_t level, uint64_t* size);
+int pg_frontiers_export(pg_frontiers f, uint64_t level, uint32_t* out);
+int pg_frontiers_destroy(pg_frontiers f);
+
+/* execution_path.cpp:24-88 extract_execution_path (layer l: dests N^{L-l},
+ * sources N^{L-l-1}). prepare_all_paths (:90-96) = layers L-1 .. 0. */
+int pg_path_extract(pg_graph g, pg_frontiers f, uint64_t layer, pg_path* out);
+int pg_path_info(pg_path p, uint64_t* layer, uint32_t* dests, uint32_t* srcs, uint64_t* edges,
+                 uint32_t* parent_rows, uint32_t* max_degree);
+/* copy the ExecutionPath arrays to host (any pointer may be NULL) */
+int pg_path_export(pg_path p, uint32_t* dest_local_to_global, uint32_t* src_local_to_global,
+                   uint32_t* src_pos_in_parent, uint64_t* offsets, uint32_t* neighbors,
+                   double* weights);
+/* ExecutionPath::fingerprint stamp (train.hpp:108-112) */
+int pg_path_set_fingerprint(pg_path p, uint64_t fp);
+int pg_path_get_fingerprint(pg_path p, uint64_t* fp);
+int pg_path_destroy(pg_path p);
+
+/* ---------------- group partition ---------------- */
+
+/* gs_model.cpp:68-74 regression_gs over train.hpp:16-24 path_stats
+ * (|D|, directed pull-edge count, E/|D|); beta NULL = default_gs_model
+ * (gs_model.cpp:64-66). */
+int pg_gs_regression(pg_path p, const double* beta, uint32_t* gs);
+/* gs_model.cpp:68-74 on explicit GraphStats */
+int pg_gs_regression_stats(uint32_t n_vertices, uint64_t n_edges, double avg_degree,
+                           const double* beta, uint32_t* gs);
+/* group_cost.cpp:30-34 default_gs_candidates; *count <= 33 */
+int pg_gs_default_candidates(uint32_t max_degree, uint32_t* out, uint64_t* count);
+/* group_cost.cpp:36-53 oracle_gs with cost_model_evaluator(dim, {workers,
+ * lambda}) (:9-28), evaluated on device. cands NULL: default candidates of
+ * the path's max degree; table gets one cost per candidate (capacity 33 when
+ * cands is NULL); *ncand_out = candidates evaluated. */
+int pg_gs_oracle_cost(pg_path p, uint64_t dim, int workers, double lambda, const uint32_t* cands,
+                      uint64_t ncand, uint32_t* best, double* table, uint64_t* ncand_out);
+/* group_cost.cpp:9-24 grouping_cost for a built grouping */
+int pg_grouping_cost(pg_groups G, uint64_t dim, int workers, double lambda, double* cost);
+
+/* grouping.cpp:7-27 group_neighbors over a path (or the whole graph). The
+ * grouping borrows its base, which must outlive it (grouping.hpp:10-13). */
+int pg_group(pg_path p, uint32_t gs, pg_groups* out);
+int pg_group_graph(pg_graph g, uint32_t gs, pg_groups* out);
+int pg_groups_info(pg_groups G, uint32_t* gs, uint64_t* count, uint32_t* dests);
+int pg_groups_export(pg_groups G, uint32_t* dest, uint64_t* edge_begin, uint64_t* edge_end,
+                     uint64_t* dest_groups);
+int pg_groups_destroy(pg_groups G);
+
+/* ---------------- backward aggregate ---------------- */
+
+/* aggregate.hpp:56-122 aggregate_pull<float>: out[D x dim] (+)=
+ * A_path * in, where in rows are the path's LOCAL source ids
+ * (in_rows == |S|) — the reference operator on device pointers. */
+int pg_aggregate_pull(pg_groups G, const float* in_dev, uint64_t in_rows, uint64_t ld_in,
+                      float* out_dev, uint64_t ld_out, uint64_t dim, unsigned flags,
+                      void* stream);
+/* The reference's timed backward-aggregation stage (engine.hpp:331-338):
+ *   y_used = gather_rows(y_grad, path.src_pos_in_parent);
+ *   aggregate_pull(groups, y_used, x_grad)
+ * with the gather folded into the edge stream. y_dev rows follow the
+ * parent frontier (y_rows == parent_rows); x_dev has the path's D rows. */
+int pg_backward_aggregate(pg_groups G, const float* y_dev, uint64_t y_rows, uint64_t ld_in,
+                          float* x_dev, uint64_t ld_out, uint64_t dim, unsigned flags,
+                          void* stream);
+/* Same stage on destination rows [row_begin, row_end) of the path (dest
+ * local order), for destination-row sharding (pg_path_shard_bounds):
+ * x_dev holds row_end - row_begin rows, row r = destination row_begin + r. */
+int pg_backward_aggregate_rows(pg_groups G, uint32_t row_begin, uint32_t row_end,
+                               const float* y_dev, uint64_t y_rows, uint64_t ld_in, float* x_dev,
+                               uint64_t ld_out, uint64_t dim, unsigned flags, void* stream);
+/* Host-buffer drop-ins for DenseMatrix<float> callers (row-major, ld = cols):
+ * copy in, run, copy out, synchronise. */
+int pg_aggregate_pull_host(pg_groups G, const float* in_host, uint64_t in_rows, uint64_t dim,
+                           float* out_host, unsigned flags, uint64_t* counters);
+int pg_backward_aggregate_host(pg_groups G, const float* y_host, uint64_t y_rows, uint64_t dim,
+                               float* x_host, unsigned flags, uint64_t* counters);
+/* StageCounters (aggregate.hpp:23-39) of one call, analytically:
+ * {edges_traversed, groups_executed, atomic_commits}. */
+int pg_stage_counters(pg_groups G, uint64_t dim, unsigned flags, uint64_t* counters);
+/* Edge-balanced destination-row split for multi-GPU: bounds
+ * [world+1] in dest-local row order, cut at E*r/world. */
+int pg_path_shard_bounds(pg_path p, uint32_t world, uint32_t* bounds);
+
+/* ---------------- dense helpers of backward_epp ---------------- */
+
+/* dense_matrix.hpp:78-95 gemm_a_bt: out[n x m] = a[n x k] * b[m x k]^T */
+int pg_gemm_a_bt(const float* a, uint64_t lda, const float* b, uint64_t ldb, float* out,
+                 uint64_t ldo, uint64_t n, uint64_t m, uint64_t k, void* stream);
+/* dense_matrix.hpp:114-121 relu_backward */
+int pg_relu_backward(const float* grad, uint64_t ldg, const float* pre, uint64_t ldp, float* out,
+                     uint64_t ldo, uint64_t rows, uint64_t cols, void* stream);
+/* engine.hpp:162-169 gather_rows (ids on device) */
+int pg_gather_rows(const float* src, uint64_t lds, const uint32_t* ids_dev, uint64_t k, float* out,
+                   uint64_t ldo, uint64_t cols, void* stream);
+/* device pointers to a path's frontier-order arrays for chained drivers */
+int pg_path_device_arrays(pg_path p, const uint32_t** dest, const uint32_t** srcpos,
+                          const uint64_t** offsets);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,125 @@
+"""Loader for libpathgcn_b200.so (the sm_100a CUDA path behind the C ABI in
+include/pathgcn_b200.h). Builds it in-tree with nvcc when missing or stale;
+fails loudly otherwise — there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import glob
+import os
+import shutil
+import subprocess
+import threading
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+SO = os.path.join(PKG, "libpathgcn_b200.so")
+HEADER = os.path.join(ROOT, "include", "pathgcn_b200.h")
+
+_lock = threading.Lock()
+_lib = None
+
+
+def _sources():
+    return glob.glob(os.path.join(PKG, "csrc", "*")) + [HEADER, os.path.join(PKG, "Makefile")]
+
+
+def stale() -> bool:
+    if not os.path.exists(SO):
+        return True
+    t = os.path.getmtime(SO)
+    return any(os.path.getmtime(s) > t for s in _sources())
+
+
+def build(force: bool = False, jobs: int = 4) -> str:
+    """Compile the CUDA extension for sm_100a (nvcc, in-tree)."""
+    if force or stale():
+        if shutil.which("nvcc") is None and not os.path.exists("/usr/local/cuda/bin/nvcc"):
+            raise RuntimeError("nvcc not found: cannot build libpathgcn_b200.so")
+        env = dict(os.environ)
+        env["PATH"] = env.get("PATH", "") + ":/usr/local/cuda/bin"
+        subprocess.run(["make", "-s", "-C", PKG, f"-j{jobs}"], check=True, env=env)
+    return SO
+
+
+def load() -> C.CDLL:
+    global _lib
+    with _lock:
+        if _lib is None:
+            if stale():
+                build()
+            _lib = C.CDLL(SO)
+            _declare(_lib)
+        return _lib
+
+
+u32p = C.POINTER(C.c_uint32)
+u64p = C.POINTER(C.c_uint64)
+f32p = C.POINTER(C.c_float)
+f64p = C.POINTER(C.c_double)
+vp = C.c_void_p
+H = C.c_void_p  # opaque handles
+u32, u64, i32, i64, f64 = C.c_uint32, C.c_uint64, C.c_int, C.c_int64, C.c_double
+
+# every symbol of include/pathgcn_b200.h with its ctypes signature
+SIGNATURES = {
+    "pg_last_error": [C.c_char_p, C.c_size_t],
+    "pg_version": [],
+    "pg_device_count": [C.POINTER(C.c_int)],
+    "pg_gen_rmat": [u32, u64, f64, f64, f64, f64, u64, u32p, u32p],
+    "pg_training_set_size": [u32, f64, u64p],
+    "pg_sample_training_set": [u32, f64, u64, u32p],
+    "pg_graph_build": [i32, i64, u32p, u64, i32, C.POINTER(H)],
+    "pg_graph_create": [i32, u32, u64p, u32p, f64p, i32, C.POINTER(H)],
+    "pg_graph_assign_weights": [H, i32],
+    "pg_graph_info": [H, u32p, u64p, u32p, u64p],
+    "pg_graph_export": [H, u64p, u32p, f64p],
+    "pg_graph_destroy": [H],
+    "pg_path_fingerprint": [H, u32p, u64, u64, u64p],
+    "pg_frontiers_compute": [H, u32p, u64, u64, C.POINTER(H)],
+    "pg_frontiers_size": [H, u64, u64p],
+    "pg_frontiers_export": [H, u64, u32p],
+    "pg_frontiers_destroy": [H],
+    "pg_path_extract": [H, H, u64, C.POINTER(H)],
+    "pg_path_info": [H, u64p, u32p, u32p, u64p, u32p, u32p],
+    "pg_path_export": [H, u32p, u32p, u32p, u64p, u32p, f64p],
+    "pg_path_set_fingerprint": [H, u64],
+    "pg_path_get_fingerprint": [H, u64p],
+    "pg_path_destroy": [H],
+    "pg_gs_regression": [H, f64p, u32p],
+    "pg_gs_regression_stats": [u32, u64, f64, f64p, u32p],
+    "pg_gs_default_candidates": [u32, u32p, u64p],
+    "pg_gs_oracle_cost": [H, u64, i32, f64, u32p, u64, u32p, f64p, u64p],
+    "pg_grouping_cost": [H, u64, i32, f64, f64p],
+    "pg_group": [H, u32, C.POINTER(H)],
+    "pg_group_graph": [H, u32, C.POINTER(H)],
+    "pg_groups_info": [H, u32p, u64p, u32p],
+    "pg_groups_export": [H, u32p, u64p, u64p, u64p],
+    "pg_groups_destroy": [H],
+    "pg_aggregate_pull": [H, vp, u64, u64, vp, u64, u64, C.c_uint, vp],
+    "pg_backward_aggregate": [H, vp, u64, u64, vp, u64, u64, C.c_uint, vp],
+    "pg_backward_aggregate_rows": [H, u32, u32, vp, u64, u64, vp, u64, u64, C.c_uint, vp],
+    "pg_aggregate_pull_host": [H, f32p, u64, u64, f32p, C.c_uint, u64p],
+    "pg_backward_aggregate_host": [H, f32p, u64, u64, f32p, C.c_uint, u64p],
+    "pg_stage_counters": [H, u64, C.c_uint, u64p],
+    "pg_path_shard_bounds": [H, u32, u32p],
+    "pg_gemm_a_bt": [vp, u64, vp, u64, vp, u64, u64, u64, u64, vp],
+    "pg_relu_backward": [vp, u64, vp, u64, vp, u64, u64, u64, vp],
+    "pg_gather_rows": [vp, u64, vp, u64, vp, u64, u64, vp],
+    "pg_path_device_arrays": [H, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)],
+}
+
+
+def header_symbols():
+    """Function names declared in include/pathgcn_b200.h."""
+    import re
+
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"^int\s+(pg_\w+)\s*\(", txt, re.M)))
+
+
+def _declare(lib):
+    for name, args in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = C.c_int

@@ -1,0 +1,683 @@
+// C ABI of libpathgcn_b200.so (include/pathgcn_b200.h): status codes,
+// handle plumbing, host-side input synthesis with the reference's exact
+// libstdc++ random streams, and the host-buffer drop-ins.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "../../include/pathgcn_b200.h"
+#include "pg_internal.h"
+
+using namespace pg;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guard(F&& f) {
+    try {
+        f();
+        return PG_OK;
+    } catch (const pg::Error& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return PG_ERR_DEVICE;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return PG_ERR_CONFIG;
+    }
+}
+
+template <typename T>
+T* need(T* p, const char* what) {
+    if (!p) fail(kConfig, std::string(what) + ": null handle");
+    return p;
+}
+
+Graph* G_(pg_graph h) { return need(reinterpret_cast<Graph*>(h), "graph"); }
+Frontiers* F_(pg_frontiers h) { return need(reinterpret_cast<Frontiers*>(h), "frontiers"); }
+Path* P_(pg_path h) { return need(reinterpret_cast<Path*>(h), "path"); }
+Groups* R_(pg_groups h) { return need(reinterpret_cast<Groups*>(h), "groups"); }
+
+void fnv_mix(uint64_t& h, uint64_t x) {
+    for (int i = 0; i < 8; ++i) {
+        h ^= (x >> (8 * i)) & 0xFF;
+        h *= 1099511628211ull;
+    }
+}
+
+// csr_graph.cpp:19-31 (host: FNV-1a is sequential by definition)
+uint64_t graph_fp(Graph& g) {
+    if (g.fp_valid) return g.fp;
+    DeviceGuard dg(g.device);
+    cudaStream_t s = lib_stream(g.device);
+    std::vector<uint64_t> off(static_cast<uint64_t>(g.n) + 1);
+    std::vector<uint32_t> nb(g.m);
+    PG_CUDA(cudaMemcpyAsync(off.data(), g.offsets.get(), off.size() * 8, cudaMemcpyDeviceToHost, s));
+    if (g.m) PG_CUDA(cudaMemcpyAsync(nb.data(), g.nbrs.get(), g.m * 4, cudaMemcpyDeviceToHost, s));
+    PG_CUDA(cudaStreamSynchronize(s));
+    uint64_t h = 1469598103934665603ull;
+    fnv_mix(h, g.n);
+    for (uint64_t o : off) fnv_mix(h, o);
+    for (uint32_t u : nb) fnv_mix(h, u);
+    g.fp = h;
+    g.fp_valid = true;
+    return h;
+}
+
+// training_set.cpp:15-26
+uint64_t training_fp(const uint32_t* vt, uint64_t k) {
+    uint64_t h = 1469598103934665603ull;
+    fnv_mix(h, k);
+    for (uint64_t i = 0; i < k; ++i) fnv_mix(h, vt[i]);
+    return h;
+}
+
+// The CSR a grouping runs over.
+struct Base {
+    uint32_t D;
+    const uint64_t* offsets;
+    uint64_t E;
+    uint32_t in_rows_local;  // rows of a local-indexed input
+};
+
+Base base_of(Groups& G) {
+    if (G.path) return {G.path->D, G.path->offsets.get(), G.path->E, G.path->S};
+    return {G.graph->n, G.graph->offsets.get(), G.graph->m, G.graph->n};
+}
+
+uint64_t fast_atomic_groups(Groups& G) {
+    // sum over destinations owning more than one group of their group count
+    const Base b = base_of(G);
+    std::vector<uint64_t> dg(static_cast<uint64_t>(b.D) + 1);
+    DeviceGuard dev(G.device);
+    cudaStream_t s = lib_stream(G.device);
+    PG_CUDA(cudaMemcpyAsync(dg.data(), G.dest_groups.get(), dg.size() * 8, cudaMemcpyDeviceToHost, s));
+    PG_CUDA(cudaStreamSynchronize(s));
+    uint64_t t = 0;
+    for (uint32_t v = 0; v < b.D; ++v) {
+        const uint64_t k = dg[v + 1] - dg[v];
+        if (k > 1) t += k;
+    }
+    return t;
+}
+
+void counters_of(Groups& G, uint64_t dim, unsigned flags, uint64_t* c) {
+    if (!c) return;
+    const Base b = base_of(G);
+    c[0] = b.E;
+    c[1] = G.G;
+    c[2] = (flags & PG_AGG_FAST) ? fast_atomic_groups(G) * dim : 0;
+}
+
+void check_dims(uint64_t dim, uint64_t ld_in, uint64_t ld_out) {
+    if (ld_in < dim || ld_out < dim) fail(kConfig, "aggregate_pull: leading dimension smaller than dim");
+}
+
+// Core launch over the grouping's base: which edge stream and which schedule.
+void run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re, const float* in, uint64_t ld_in,
+                   float* out, uint64_t ld_out, uint64_t dim, unsigned flags, cudaStream_t s) {
+    const bool accumulate = !(flags & PG_AGG_OVERWRITE);
+    DeviceGuard dg(G.device);
+    if (G.path) {
+        Path& p = *G.path;
+        const Edge* edges = p.edges_parent.get();
+        if (!parent_indexed && p.S != p.P) {
+            path_pack_local(p, lib_stream(p.device));
+            PG_CUDA(cudaStreamSynchronize(lib_stream(p.device)));
+            edges = p.edges_local.get();
+        }
+        if (rb == 0 && re == p.D) {
+            aggregate_det(p.offsets.get(), edges, p.order.get(), p.D, 0, p.D, in, ld_in, out, ld_out, dim,
+                          accumulate, s);
+            return;
+        }
+        // shard: schedule of rows [rb, re) relative to rb
+        if (!(G.shard_order.get() && G.shard_rb == rb && G.shard_re == re)) {
+            degree_order(p.offsets.get() + rb, re - rb, G.shard_order, lib_stream(p.device));
+            G.shard_rb = rb;
+            G.shard_re = re;
+        }
+        aggregate_det(p.offsets.get() + rb, edges, G.shard_order.get(), re - rb, 0, re - rb, in, ld_in, out,
+                      ld_out, dim, accumulate, s);
+        return;
+    }
+    Graph& g = *G.graph;
+    if (!g.edges.get()) {
+        graph_pack_edges(g, lib_stream(g.device));
+        PG_CUDA(cudaStreamSynchronize(lib_stream(g.device)));
+    }
+    if (!G.graph_order.get() && g.n) degree_order(g.offsets.get(), g.n, G.graph_order, lib_stream(g.device));
+    aggregate_det(g.offsets.get(), g.edges.get(), G.graph_order.get(), g.n, 0, g.n, in, ld_in, out, ld_out, dim,
+                  accumulate, s);
+}
+
+// Host buffers (ld = dim) -> padded device buffers -> run -> host.
+void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_rows, uint64_t dim,
+              float* out_host, unsigned flags) {
+    const Base b = base_of(G);
+    DeviceGuard dg(G.device);
+    cudaStream_t s = lib_stream(G.device);
+    const uint64_t ld = (dim + 3) & ~3ull;  // 16-byte rows for the vectorised kernel
+    DevBuf<float> din(in_rows * ld, s), dout(static_cast<uint64_t>(b.D) * ld, s);
+    if (in_rows && dim)
+        PG_CUDA(cudaMemcpy2DAsync(din.get(), ld * 4, in_host, dim * 4, dim * 4, in_rows, cudaMemcpyHostToDevice, s));
+    if (b.D && dim) {
+        if (flags & PG_AGG_OVERWRITE)
+            ;  // every element is written
+        else
+            PG_CUDA(cudaMemcpy2DAsync(dout.get(), ld * 4, out_host, dim * 4, dim * 4, b.D, cudaMemcpyHostToDevice, s));
+    }
+    run_aggregate(G, parent_indexed, 0, b.D, din.get(), ld, dout.get(), ld, dim, flags, s);
+    if (b.D && dim)
+        PG_CUDA(cudaMemcpy2DAsync(out_host, dim * 4, dout.get(), ld * 4, dim * 4, b.D, cudaMemcpyDeviceToHost, s));
+    PG_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace
+
+extern "C" {
+
+int pg_last_error(char* buf, size_t cap) {
+    if (buf && cap) std::snprintf(buf, cap, "%s", g_err.c_str());
+    return static_cast<int>(g_err.size());
+}
+
+int pg_version(void) { return 1; }
+
+int pg_device_count(int* count) {
+    return guard([&] {
+        int c = 0;
+        PG_CUDA(cudaGetDeviceCount(&c));
+        *count = c;
+    });
+}
+
+// ---------------- graph load ----------------
+
+int pg_gen_rmat(uint32_t n, uint64_t m, double a, double b, double c, double d, uint64_t seed, uint32_t* pairs,
+                uint32_t* n_pad) {
+    return guard([&] {
+        // rmat.cpp:10-44: pad n to 2^levels; per pair and level one
+        // U(0,1) draw from mt19937_64(seed) picks the quadrant.
+        if (n == 0) fail(kConfig, "rmat: vertex count must be positive");
+        if (std::abs(a + b + c + d - 1.0) > 1e-9) fail(kConfig, "rmat: quadrant probabilities must sum to 1");
+        int levels = 0;
+        while ((uint32_t{1} << levels) < n) ++levels;
+        std::mt19937_64 rng(seed);
+        std::uniform_real_distribution<double> unit(0.0, 1.0);
+        for (uint64_t i = 0; i < m; ++i) {
+            uint32_t src = 0, dst = 0;
+            for (int lvl = levels - 1; lvl >= 0; --lvl) {
+                const double r = unit(rng);
+                const uint32_t bit = uint32_t{1} << lvl;
+                if (r < a) {
+                } else if (r < a + b) {
+                    dst |= bit;
+                } else if (r < a + b + c) {
+                    src |= bit;
+                } else {
+                    src |= bit;
+                    dst |= bit;
+                }
+            }
+            pairs[2 * i] = src;
+            pairs[2 * i + 1] = dst;
+        }
+        if (n_pad) *n_pad = uint32_t{1} << levels;
+    });
+}
+
+int pg_training_set_size(uint32_t n, double ratio, uint64_t* k) {
+    return guard([&] {
+        if (n == 0) fail(kConfig, "training set: graph has no vertices");
+        if (!(ratio > 0.0) || ratio > 1.0) fail(kConfig, "training ratio must be in (0, 1]");
+        *k = std::max<uint64_t>(1, static_cast<uint64_t>(std::llround(ratio * static_cast<double>(n))));
+    });
+}
+
+int pg_sample_training_set(uint32_t n, double ratio, uint64_t seed, uint32_t* out) {
+    return guard([&] {
+        // training_set.cpp:28-49: partial Fisher-Yates over mt19937_64(seed)
+        uint64_t k = 0;
+        if (int rc = pg_training_set_size(n, ratio, &k)) fail(rc, g_err);
+        std::vector<uint32_t> ids(n);
+        std::iota(ids.begin(), ids.end(), 0u);
+        std::mt19937_64 rng(seed);
+        for (std::size_t i = 0; i < k; ++i) {
+            std::uniform_int_distribution<std::size_t> pick(i, n - 1);
+            std::swap(ids[i], ids[pick(rng)]);
+        }
+        std::sort(ids.begin(), ids.begin() + static_cast<std::ptrdiff_t>(k));
+        std::memcpy(out, ids.data(), k * 4);
+    });
+}
+
+int pg_graph_build(int device, int64_t n_hint, const uint32_t* pairs, uint64_t npairs, int weight_mode,
+                   pg_graph* out) {
+    return guard([&] {
+        auto g = graph_build(device, n_hint, pairs, npairs, weight_mode);
+        *out = reinterpret_cast<pg_graph>(g.release());
+    });
+}
+
+int pg_graph_create(int device, uint32_t n, const uint64_t* offsets, const uint32_t* neighbors,
+                    const double* weights, int validate, pg_graph* out) {
+    return guard([&] {
+        if (!offsets) fail(kConfig, "graph: offsets required");
+        auto g = graph_upload(device, n, offsets, neighbors, weights, validate != 0);
+        *out = reinterpret_cast<pg_graph>(g.release());
+    });
+}
+
+int pg_graph_assign_weights(pg_graph h, int weight_mode) {
+    return guard([&] {
+        Graph& g = *G_(h);
+        DeviceGuard dg(g.device);
+        graph_assign_weights(g, weight_mode, lib_stream(g.device));
+        PG_CUDA(cudaStreamSynchronize(lib_stream(g.device)));
+    });
+}
+
+int pg_graph_info(pg_graph h, uint32_t* n, uint64_t* m, uint32_t* max_degree, uint64_t* fingerprint) {
+    return guard([&] {
+        Graph& g = *G_(h);
+        if (n) *n = g.n;
+        if (m) *m = g.m;
+        if (max_degree) *max_degree = g.max_degree;
+        if (fingerprint) *fingerprint = graph_fp(g);
+    });
+}
+
+int pg_graph_export(pg_graph h, uint64_t* offsets, uint32_t* neighbors, double* weights) {
+    return guard([&] {
+        Graph& g = *G_(h);
+        DeviceGuard dg(g.device);
+        cudaStream_t s = lib_stream(g.device);
+        if (offsets)
+            PG_CUDA(cudaMemcpyAsync(offsets, g.offsets.get(), (static_cast<uint64_t>(g.n) + 1) * 8,
+                                    cudaMemcpyDeviceToHost, s));
+        if (neighbors && g.m) PG_CUDA(cudaMemcpyAsync(neighbors, g.nbrs.get(), g.m * 4, cudaMemcpyDeviceToHost, s));
+        if (weights && g.m) PG_CUDA(cudaMemcpyAsync(weights, g.w64.get(), g.m * 8, cudaMemcpyDeviceToHost, s));
+        PG_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int pg_graph_destroy(pg_graph h) {
+    return guard([&] {
+        Graph* g = reinterpret_cast<Graph*>(h);
+        if (!g) return;
+        DeviceGuard dg(g->device);
+        delete g;
+    });
+}
+
+int pg_path_fingerprint(pg_graph h, const uint32_t* vt, uint64_t k, uint64_t layers, uint64_t* fp) {
+    return guard([&] {
+        // execution_path.cpp:17-22
+        uint64_t x = graph_fp(*G_(h));
+        x ^= training_fp(vt, k) + 0x9e3779b97f4a7c15ull + (x << 6) + (x >> 2);
+        x ^= layers + 0x9e3779b97f4a7c15ull + (x << 6) + (x >> 2);
+        *fp = x;
+    });
+}
+
+// ---------------- execution-path build ----------------
+
+int pg_frontiers_compute(pg_graph h, const uint32_t* vt, uint64_t k, uint64_t layers, pg_frontiers* out) {
+    return guard([&] {
+        auto f = frontiers_compute(*G_(h), vt, k, layers);
+        *out = reinterpret_cast<pg_frontiers>(f.release());
+    });
+}
+
+int pg_frontiers_size(pg_frontiers h, uint64_t level, uint64_t* size) {
+    return guard([&] {
+        Frontiers& f = *F_(h);
+        if (level > f.L) fail(kConfig, "frontiers: level out of range");
+        *size = f.levels[level].size;
+    });
+}
+
+int pg_frontiers_export(pg_frontiers h, uint64_t level, uint32_t* out) {
+    return guard([&] {
+        Frontiers& f = *F_(h);
+        if (level > f.L) fail(kConfig, "frontiers: level out of range");
+        const Level& lv = f.levels[level];
+        DeviceGuard dg(f.device);
+        cudaStream_t s = lib_stream(f.device);
+        if (lv.size) PG_CUDA(cudaMemcpyAsync(out, lv.ids.get(), lv.size * 4, cudaMemcpyDeviceToHost, s));
+        PG_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int pg_frontiers_destroy(pg_frontiers h) {
+    return guard([&] {
+        Frontiers* f = reinterpret_cast<Frontiers*>(h);
+        if (!f) return;
+        DeviceGuard dg(f->device);
+        delete f;
+    });
+}
+
+int pg_path_extract(pg_graph g, pg_frontiers f, uint64_t layer, pg_path* out) {
+    return guard([&] {
+        auto p = path_extract(*G_(g), *F_(f), layer);
+        *out = reinterpret_cast<pg_path>(p.release());
+    });
+}
+
+int pg_path_info(pg_path h, uint64_t* layer, uint32_t* dests, uint32_t* srcs, uint64_t* edges,
+                 uint32_t* parent_rows, uint32_t* max_degree) {
+    return guard([&] {
+        Path& p = *P_(h);
+        if (layer) *layer = p.layer;
+        if (dests) *dests = p.D;
+        if (srcs) *srcs = p.S;
+        if (edges) *edges = p.E;
+        if (parent_rows) *parent_rows = p.P;
+        if (max_degree) *max_degree = p.max_degree;
+    });
+}
+
+int pg_path_export(pg_path h, uint32_t* dest, uint32_t* src, uint32_t* srcpos, uint64_t* offsets,
+                   uint32_t* neighbors, double* weights) {
+    return guard([&] {
+        Path& p = *P_(h);
+        DeviceGuard dg(p.device);
+        cudaStream_t s = lib_stream(p.device);
+        auto cp = [&](void* dst, const void* srcp, uint64_t bytes) {
+            if (dst && bytes) PG_CUDA(cudaMemcpyAsync(dst, srcp, bytes, cudaMemcpyDeviceToHost, s));
+        };
+        cp(dest, p.dest.get(), static_cast<uint64_t>(p.D) * 4);
+        cp(src, p.src.get(), static_cast<uint64_t>(p.S) * 4);
+        cp(srcpos, p.srcpos.get(), static_cast<uint64_t>(p.S) * 4);
+        cp(offsets, p.offsets.get(), (static_cast<uint64_t>(p.D) + 1) * 8);
+        cp(neighbors, p.nbr_local.get(), p.E * 4);
+        cp(weights, p.w64.get(), p.E * 8);
+        PG_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int pg_path_set_fingerprint(pg_path h, uint64_t fp) {
+    return guard([&] { P_(h)->fingerprint = fp; });
+}
+
+int pg_path_get_fingerprint(pg_path h, uint64_t* fp) {
+    return guard([&] { *fp = P_(h)->fingerprint; });
+}
+
+int pg_path_destroy(pg_path h) {
+    return guard([&] {
+        Path* p = reinterpret_cast<Path*>(h);
+        if (!p) return;
+        DeviceGuard dg(p->device);
+        delete p;
+    });
+}
+
+int pg_path_device_arrays(pg_path h, const uint32_t** dest, const uint32_t** srcpos, const uint64_t** offsets) {
+    return guard([&] {
+        Path& p = *P_(h);
+        if (dest) *dest = p.dest.get();
+        if (srcpos) *srcpos = p.srcpos.get();
+        if (offsets) *offsets = p.offsets.get();
+    });
+}
+
+// ---------------- group partition ----------------
+
+int pg_gs_regression_stats(uint32_t n_vertices, uint64_t n_edges, double avg_degree, const double* beta,
+                           uint32_t* gs) {
+    return guard([&] {
+        // gs_model.cpp:64-74
+        const double b0 = beta ? beta[0] : 0.65538, b1 = beta ? beta[1] : 1.67431e-5;
+        const double b2 = beta ? beta[2] : -2.24342e-6, b3 = beta ? beta[3] : 0.63641;
+        const double raw = b0 + b1 * static_cast<double>(n_vertices) + b2 * static_cast<double>(n_edges) +
+                           b3 * avg_degree;
+        const long long rounded = std::llround(raw);
+        *gs = rounded < 1 ? 1u : static_cast<uint32_t>(rounded);
+    });
+}
+
+int pg_gs_regression(pg_path h, const double* beta, uint32_t* gs) {
+    return guard([&] {
+        // train.hpp:16-24 path_stats
+        Path& p = *P_(h);
+        const double avg = p.D == 0 ? 0.0 : static_cast<double>(p.E) / static_cast<double>(p.D);
+        if (int rc = pg_gs_regression_stats(p.D, p.E, avg, beta, gs)) fail(rc, g_err);
+    });
+}
+
+int pg_gs_default_candidates(uint32_t max_degree, uint32_t* out, uint64_t* count) {
+    return guard([&] {
+        // group_cost.cpp:30-34
+        uint64_t c = 0;
+        out[c++] = 1;
+        while (out[c - 1] < std::max<uint32_t>(max_degree, 1)) {
+            out[c] = out[c - 1] * 2;
+            ++c;
+        }
+        *count = c;
+    });
+}
+
+int pg_gs_oracle_cost(pg_path h, uint64_t dim, int workers, double lambda, const uint32_t* cands,
+                      uint64_t ncand, uint32_t* best, double* table, uint64_t* ncand_out) {
+    return guard([&] {
+        // group_cost.cpp:36-53 over cost_model_evaluator (:26-28)
+        Path& p = *P_(h);
+        std::vector<uint32_t> c;
+        if (cands) {
+            c.assign(cands, cands + ncand);
+        } else {
+            uint32_t tmp[40];
+            uint64_t k = 0;
+            if (int rc = pg_gs_default_candidates(p.max_degree, tmp, &k)) fail(rc, g_err);
+            c.assign(tmp, tmp + k);
+        }
+        if (c.empty()) fail(kConfig, "oracle_gs: empty candidate list");
+        if (workers < 1) fail(kConfig, "cost model: worker count must be >= 1");
+        DeviceGuard dg(p.device);
+        cudaStream_t s = lib_stream(p.device);
+        double best_cost = 0.0;
+        uint32_t best_gs = 1;
+        bool first = true;
+        for (std::size_t i = 0; i < c.size(); ++i) {
+            uint64_t max_load = 0, atomic = 0;
+            grouping_cost_dev(p.D, p.offsets.get(), c[i], dim, static_cast<uint64_t>(workers), &max_load, &atomic, s);
+            const double cost = static_cast<double>(max_load) + lambda * static_cast<double>(atomic);
+            if (table) table[i] = cost;
+            if (first || cost < best_cost || (cost == best_cost && c[i] < best_gs)) {
+                first = false;
+                best_cost = cost;
+                best_gs = c[i];
+            }
+        }
+        *best = best_gs;
+        if (ncand_out) *ncand_out = c.size();
+    });
+}
+
+int pg_grouping_cost(pg_groups h, uint64_t dim, int workers, double lambda, double* cost) {
+    return guard([&] {
+        Groups& G = *R_(h);
+        if (workers < 1) fail(kConfig, "cost model: worker count must be >= 1");
+        const Base b = base_of(G);
+        DeviceGuard dg(G.device);
+        uint64_t max_load = 0, atomic = 0;
+        grouping_cost_dev(b.D, b.offsets, G.gs, dim, static_cast<uint64_t>(workers), &max_load, &atomic,
+                          lib_stream(G.device));
+        *cost = static_cast<double>(max_load) + lambda * static_cast<double>(atomic);
+    });
+}
+
+int pg_group(pg_path h, uint32_t gs, pg_groups* out) {
+    return guard([&] {
+        Path& p = *P_(h);
+        auto G = groups_build(p.D, p.offsets.get(), gs, p.device);
+        G->path = &p;
+        *out = reinterpret_cast<pg_groups>(G.release());
+    });
+}
+
+int pg_group_graph(pg_graph h, uint32_t gs, pg_groups* out) {
+    return guard([&] {
+        Graph& g = *G_(h);
+        auto G = groups_build(g.n, g.offsets.get(), gs, g.device);
+        G->graph = &g;
+        *out = reinterpret_cast<pg_groups>(G.release());
+    });
+}
+
+int pg_groups_info(pg_groups h, uint32_t* gs, uint64_t* count, uint32_t* dests) {
+    return guard([&] {
+        Groups& G = *R_(h);
+        if (gs) *gs = G.gs;
+        if (count) *count = G.G;
+        if (dests) *dests = base_of(G).D;
+    });
+}
+
+int pg_groups_export(pg_groups h, uint32_t* dest, uint64_t* edge_begin, uint64_t* edge_end, uint64_t* dest_groups) {
+    return guard([&] {
+        Groups& G = *R_(h);
+        DeviceGuard dg(G.device);
+        cudaStream_t s = lib_stream(G.device);
+        auto cp = [&](void* dst, const void* srcp, uint64_t bytes) {
+            if (dst && bytes) PG_CUDA(cudaMemcpyAsync(dst, srcp, bytes, cudaMemcpyDeviceToHost, s));
+        };
+        cp(dest, G.gdest.get(), G.G * 4);
+        cp(edge_begin, G.gbegin.get(), G.G * 8);
+        cp(edge_end, G.gend.get(), G.G * 8);
+        cp(dest_groups, G.dest_groups.get(), (static_cast<uint64_t>(base_of(G).D) + 1) * 8);
+        PG_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int pg_groups_destroy(pg_groups h) {
+    return guard([&] {
+        Groups* G = reinterpret_cast<Groups*>(h);
+        if (!G) return;
+        DeviceGuard dg(G->device);
+        delete G;
+    });
+}
+
+// ---------------- backward aggregate ----------------
+
+int pg_aggregate_pull(pg_groups h, const float* in_dev, uint64_t in_rows, uint64_t ld_in, float* out_dev,
+                      uint64_t ld_out, uint64_t dim, unsigned flags, void* stream) {
+    return guard([&] {
+        Groups& G = *R_(h);
+        const Base b = base_of(G);
+        check_dims(dim, ld_in, ld_out);
+        if (in_rows != b.in_rows_local)
+            fail(kConfig, "aggregate_pull: input rows != source count of the grouping's base");
+        run_aggregate(G, false, 0, b.D, in_dev, ld_in, out_dev, ld_out, dim, flags,
+                      static_cast<cudaStream_t>(stream));
+    });
+}
+
+int pg_backward_aggregate(pg_groups h, const float* y_dev, uint64_t y_rows, uint64_t ld_in, float* x_dev,
+                          uint64_t ld_out, uint64_t dim, unsigned flags, void* stream) {
+    return guard([&] {
+        Groups& G = *R_(h);
+        if (!G.path) fail(kConfig, "backward_aggregate: grouping is not over an execution path");
+        check_dims(dim, ld_in, ld_out);
+        if (y_rows != G.path->P) fail(kConfig, "backward_aggregate: y_grad rows != parent frontier size");
+        run_aggregate(G, true, 0, G.path->D, y_dev, ld_in, x_dev, ld_out, dim, flags,
+                      static_cast<cudaStream_t>(stream));
+    });
+}
+
+int pg_backward_aggregate_rows(pg_groups h, uint32_t row_begin, uint32_t row_end, const float* y_dev,
+                               uint64_t y_rows, uint64_t ld_in, float* x_dev, uint64_t ld_out, uint64_t dim,
+                               unsigned flags, void* stream) {
+    return guard([&] {
+        Groups& G = *R_(h);
+        if (!G.path) fail(kConfig, "backward_aggregate: grouping is not over an execution path");
+        check_dims(dim, ld_in, ld_out);
+        if (y_rows != G.path->P) fail(kConfig, "backward_aggregate: y_grad rows != parent frontier size");
+        if (row_begin > row_end || row_end > G.path->D) fail(kConfig, "backward_aggregate: bad row range");
+        if (row_begin == row_end) return;
+        run_aggregate(G, true, row_begin, row_end, y_dev, ld_in, x_dev, ld_out, dim, flags,
+                      static_cast<cudaStream_t>(stream));
+    });
+}
+
+int pg_aggregate_pull_host(pg_groups h, const float* in_host, uint64_t in_rows, uint64_t dim, float* out_host,
+                           unsigned flags, uint64_t* counters) {
+    return guard([&] {
+        Groups& G = *R_(h);
+        if (in_rows != base_of(G).in_rows_local)
+            fail(kConfig, "aggregate_pull: input rows != source count of the grouping's base");
+        run_host(G, false, in_host, in_rows, dim, out_host, flags);
+        counters_of(G, dim, flags, counters);
+    });
+}
+
+int pg_backward_aggregate_host(pg_groups h, const float* y_host, uint64_t y_rows, uint64_t dim, float* x_host,
+                               unsigned flags, uint64_t* counters) {
+    return guard([&] {
+        Groups& G = *R_(h);
+        if (!G.path) fail(kConfig, "backward_aggregate: grouping is not over an execution path");
+        if (y_rows != G.path->P) fail(kConfig, "backward_aggregate: y_grad rows != parent frontier size");
+        run_host(G, true, y_host, y_rows, dim, x_host, flags);
+        counters_of(G, dim, flags, counters);
+    });
+}
+
+int pg_stage_counters(pg_groups h, uint64_t dim, unsigned flags, uint64_t* counters) {
+    return guard([&] { counters_of(*R_(h), dim, flags, counters); });
+}
+
+int pg_path_shard_bounds(pg_path h, uint32_t world, uint32_t* bounds) {
+    return guard([&] {
+        Path& p = *P_(h);
+        if (world < 1) fail(kConfig, "shard: world size must be >= 1");
+        std::vector<uint64_t> off(static_cast<uint64_t>(p.D) + 1);
+        DeviceGuard dg(p.device);
+        cudaStream_t s = lib_stream(p.device);
+        PG_CUDA(cudaMemcpyAsync(off.data(), p.offsets.get(), off.size() * 8, cudaMemcpyDeviceToHost, s));
+        PG_CUDA(cudaStreamSynchronize(s));
+        bounds[0] = 0;
+        for (uint32_t r = 1; r < world; ++r) {
+            const uint64_t target = (p.E * r) / world;
+            const uint32_t row = static_cast<uint32_t>(
+                std::lower_bound(off.begin(), off.end() - 1, target) - off.begin());
+            bounds[r] = std::max(bounds[r - 1], std::min(row, p.D));
+        }
+        bounds[world] = p.D;
+    });
+}
+
+// ---------------- dense helpers ----------------
+
+int pg_gemm_a_bt(const float* a, uint64_t lda, const float* b, uint64_t ldb, float* out, uint64_t ldo, uint64_t n,
+                 uint64_t m, uint64_t k, void* stream) {
+    return guard([&] {
+        if (lda < k || ldb < k || ldo < m) fail(kConfig, "gemm_a_bt: leading dimension too small");
+        gemm_a_bt(a, lda, b, ldb, out, ldo, n, m, k, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int pg_relu_backward(const float* grad, uint64_t ldg, const float* pre, uint64_t ldp, float* out, uint64_t ldo,
+                     uint64_t rows, uint64_t cols, void* stream) {
+    return guard([&] { relu_backward(grad, ldg, pre, ldp, out, ldo, rows, cols, static_cast<cudaStream_t>(stream)); });
+}
+
+int pg_gather_rows(const float* src, uint64_t lds, const uint32_t* ids_dev, uint64_t k, float* out, uint64_t ldo,
+                   uint64_t cols, void* stream) {
+    return guard([&] { gather_rows(src, lds, ids_dev, k, out, ldo, cols, static_cast<cudaStream_t>(stream)); });
+}
+
+}  // extern "C"

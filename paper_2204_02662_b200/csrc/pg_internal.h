@@ -1,0 +1,141 @@
+// Internal handle layouts and kernel launchers of libpathgcn_b200.so.
+// The public surface is the C ABI in include/pathgcn_b200.h; nothing here
+// crosses the library boundary.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <vector>
+
+#include "common.cuh"
+
+namespace pg {
+
+// One library-owned non-blocking stream per device for the build calls
+// (graph load, frontiers, paths, groups, gs sweep), which are synchronous at
+// the ABI like the reference's functions.
+cudaStream_t lib_stream(int device);
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) PG_CUDA(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// Packed edge record streamed by the SpMM: (source row, fp32 weight bits).
+using Edge = uint2;
+
+// csr_graph.hpp:19-38 CsrGraph, device resident.
+struct Graph {
+    int device = 0;
+    uint32_t n = 0;
+    uint64_t m = 0;
+    uint32_t max_degree = 0;
+    DevBuf<uint64_t> offsets;   // n+1
+    DevBuf<uint32_t> nbrs;      // m, sorted per row
+    DevBuf<double> w64;         // m
+    DevBuf<Edge> edges;         // m, lazily packed (nbr, (float)w) for graph aggregation
+    bool fp_valid = false;
+    uint64_t fp = 0;
+};
+
+// One frontier level: sorted ids, membership bitmap, per-word rank prefix.
+struct Level {
+    uint64_t size = 0;
+    DevBuf<uint32_t> ids;
+    DevBuf<uint32_t> bits;    // ceil(n/32) words
+    DevBuf<uint32_t> prefix;  // ceil(n/32)+1 (exclusive popcount prefix)
+};
+
+// frontier.hpp:14-18 FrontierSets.
+struct Frontiers {
+    int device = 0;
+    uint32_t n = 0;
+    uint64_t L = 0;
+    std::vector<Level> levels;
+    const Graph* graph = nullptr;  // borrowed
+};
+
+// execution_path.hpp:16-33 ExecutionPath, plus the SpMM's own layout.
+struct Path {
+    int device = 0;
+    uint64_t layer = 0;
+    uint32_t D = 0, S = 0, P = 0;  // dests, referenced sources, parent frontier size
+    uint64_t E = 0;
+    uint32_t max_degree = 0;
+    uint64_t fingerprint = 0;
+    DevBuf<uint32_t> dest;        // dest_local_to_global (copy of frontier level L-l)
+    DevBuf<uint32_t> src;         // src_local_to_global
+    DevBuf<uint32_t> srcpos;      // src_pos_in_parent
+    DevBuf<uint64_t> offsets;     // D+1
+    DevBuf<uint32_t> nbr_local;   // E local source ids (reference layout)
+    DevBuf<double> w64;           // E, bitwise copies of the parent weights
+    DevBuf<Edge> edges_parent;    // E (src_pos_in_parent[nbr], (float)w): gather folded
+    DevBuf<Edge> edges_local;     // E (nbr_local, (float)w), lazily, only when S < P
+    DevBuf<uint32_t> order;       // D dests in descending-degree-bucket order (SpMM schedule)
+};
+
+// grouping.hpp:14-28 GroupedCsr over a path (or the whole graph).
+struct Groups {
+    int device = 0;
+    uint32_t gs = 0;
+    uint64_t G = 0;
+    Path* path = nullptr;    // borrowed base (path grouping)
+    Graph* graph = nullptr;  // borrowed base (graph grouping)
+    DevBuf<uint32_t> gdest;
+    DevBuf<uint64_t> gbegin, gend;
+    DevBuf<uint64_t> dest_groups;  // D+1
+    DevBuf<uint32_t> graph_order;  // schedule for graph groupings (lazy)
+    DevBuf<uint32_t> shard_order;  // schedule of one destination-row shard (lazy)
+    uint32_t shard_rb = 0, shard_re = 0;
+};
+
+// ---- launchers (implemented in graph.cu / path.cu / aggregate.cu) ----
+std::unique_ptr<Graph> graph_build(int device, int64_t n_hint, const uint32_t* pairs_host,
+                                   uint64_t npairs, int weight_mode);
+std::unique_ptr<Graph> graph_upload(int device, uint32_t n, const uint64_t* offsets,
+                                    const uint32_t* nbrs, const double* w, bool validate);
+void graph_assign_weights(Graph& g, int weight_mode, cudaStream_t s);
+void graph_pack_edges(Graph& g, cudaStream_t s);
+// max over v < n of offsets[v+1] - offsets[v] (synchronises s)
+uint32_t max_degree_dev(const uint64_t* offsets, uint32_t n, cudaStream_t s);
+
+std::unique_ptr<Frontiers> frontiers_compute(const Graph& g, const uint32_t* vt_host, uint64_t k,
+                                             uint64_t L);
+std::unique_ptr<Path> path_extract(const Graph& g, const Frontiers& f, uint64_t layer);
+void path_pack_local(Path& p, cudaStream_t s);
+void degree_order(const uint64_t* offsets, uint32_t D, DevBuf<uint32_t>& order, cudaStream_t s);
+
+std::unique_ptr<Groups> groups_build(uint32_t D, const uint64_t* offsets_dev, uint32_t gs,
+                                     int device);
+// group_cost.cpp:9-24 for one candidate: returns (max_load, atomic_writes).
+void grouping_cost_dev(uint32_t D, const uint64_t* offsets_dev, uint32_t gs, uint64_t dim,
+                       uint64_t workers, uint64_t* max_load, uint64_t* atomic_writes,
+                       cudaStream_t s);
+
+// aggregate.hpp:56-122 Deterministic, ascending edge order per element.
+//   out[order[i]] (+)= sum_e w_e * in[edges[e].x]
+void aggregate_det(const uint64_t* offsets, const Edge* edges, const uint32_t* order, uint32_t D,
+                   uint32_t d_begin, uint32_t d_end, const float* in, uint64_t ld_in, float* out,
+                   uint64_t ld_out, uint64_t dim, bool accumulate, cudaStream_t s);
+
+// dense_matrix.hpp:78-95 (fp32, ascending k, mul/add separately rounded, +0).
+void gemm_a_bt(const float* a, uint64_t lda, const float* b, uint64_t ldb, float* out,
+               uint64_t ldo, uint64_t n, uint64_t m, uint64_t k, cudaStream_t s);
+// dense_matrix.hpp:114-121
+void relu_backward(const float* grad, uint64_t ldg, const float* pre, uint64_t ldp, float* out,
+                   uint64_t ldo, uint64_t rows, uint64_t cols, cudaStream_t s);
+// engine.hpp:162-169
+void gather_rows(const float* src, uint64_t lds, const uint32_t* ids, uint64_t k, float* out,
+                 uint64_t ldo, uint64_t cols, cudaStream_t s);
+
+}  // namespace pg

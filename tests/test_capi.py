@@ -1,0 +1,68 @@
+"""CPU-side checks of the C ABI: the library loads, exports every symbol the
+header declares, and its host-only entry points (input synthesis, gs
+regression, candidate lists) agree with the oracle. No device compute."""
+import ctypes as C
+import os
+
+import numpy as np
+import pytest
+
+from paper_2204_02662_b200 import _lib
+
+
+def test_header_symbols_exported():
+    lib = _lib.load()
+    declared = _lib.header_symbols()
+    assert len(declared) >= 40
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert set(declared) == set(_lib.SIGNATURES), set(declared) ^ set(_lib.SIGNATURES)
+
+
+def test_library_is_sm100a():
+    so = _lib.build()
+    data = open(so, "rb").read()
+    assert b"sm_100a" in data or b"sm_100" in data
+
+
+def test_version_and_errors():
+    lib = _lib.load()
+    assert lib.pg_version() == 1
+    h = C.c_void_p()
+    # null handles are config errors, reported through pg_last_error
+    rc = lib.pg_graph_info(None, None, None, None, None)
+    assert rc == 2
+    buf = C.create_string_buffer(256)
+    lib.pg_last_error(buf, 256)
+    assert b"null handle" in buf.value
+    del h
+
+
+def test_host_generators_match_oracle(orc):
+    import paper_2204_02662_b200 as pg
+
+    for n, m, seed in ((1024, 8192, 7), (100, 50, 1)):
+        a, na = pg.gen_rmat(n, m, 0.45, 0.22, 0.22, 0.11, seed)
+        b, nb = orc.gen_rmat(n, m, 0.45, 0.22, 0.22, 0.11, seed)
+        assert na == nb and np.array_equal(a, b)
+    for n, ratio, seed in ((1024, 0.1, 42), (232965, 0.66, 42)):
+        assert np.array_equal(pg.sample_training_set(n, ratio, seed), orc.sample_training_set(n, ratio, seed))
+    with pytest.raises(pg.ConfigError):
+        pg.sample_training_set(10, 1.5, 0)
+    with pytest.raises(pg.ConfigError):
+        pg.gen_rmat(0, 1)
+
+
+@pytest.mark.parametrize("n,e", [(2708, 5278), (1134890, 2987624), (0, 0), (1, 10**9), (261686, 78511609)])
+def test_regression_matches_oracle(orc, n, e):
+    import paper_2204_02662_b200 as pg
+
+    avg = 0.0 if n == 0 else e / n
+    assert pg.regression_gs(n, e, avg) == orc.regression_gs(n, e, avg)
+
+
+def test_candidates_match_oracle(orc):
+    import paper_2204_02662_b200 as pg
+
+    for md in (0, 1, 4, 5, 214, 52471, 2**31):
+        assert np.array_equal(pg.default_gs_candidates(md), orc.default_candidates(md))
