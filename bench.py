@@ -1,0 +1,520 @@
+#!/usr/bin/env python3
+"""Backward-aggregation benchmark (BASELINE.json metric) for the B200 path.
+
+One step = one epoch's backward aggregation, i.e. the reference's timed
+stage engine.hpp:331-338 (gather_rows over src_pos_in_parent +
+aggregate_pull, Deterministic) summed over the L execution paths, on the
+Reddit-shaped synthetic graph (BASELINE.json configs[3]; the largest named
+single-GPU workload the metric is quoted on). With --gpus N (torchrun) the
+destination rows of every path are edge-balanced across ranks and each path
+starts with one NCCL all_gather of the y_grad row shards.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config reddit]
+  python bench.py --impl reference ...   # the reference CPU implementation
+
+Prints one JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "backward-aggregation ms/epoch & GB/s vs HBM peak at 1/2/4/8 B200 vs CPU ref"
+
+# name: V, RMAT pair budget (tools/calibrate_rmat.py -> exact directed m),
+#       training vertices, f, dims (dim0.., classes)
+CONFIGS = {
+    "cora": dict(V=2708, pairs=7196, m=10556, train=140, f=1433, dims=[16, 7]),
+    "pubmed": dict(V=19717, pairs=67703, m=88648, train=60, f=500, dims=[16, 3]),
+    "arxiv": dict(V=169343, pairs=814390, m=1166244, train_ratio=0.54, f=128, dims=[256, 40]),
+    "reddit": dict(V=232965, pairs=62701101, m=114615892, train_ratio=0.66, f=602, dims=[16, 41]),
+    "products": dict(V=2449029, pairs=48600820, m=61859140, train_ratio=0.08, f=100, dims=[256, 47]),
+}
+RMAT = (0.45, 0.22, 0.22, 0.11)
+RMAT_SEED, TRAIN_SEED, GRAD_SEED = 7, 42, 17
+FALLBACK_HBM = 6650.0  # B200_PROFILING.md fallback (GB/s)
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ------------------------------------------------------------------ inputs --
+
+def make_pairs(cfg, gen):
+    """Exact-V RMAT: gen_rmat over n_pad = 2^ceil(log2 V), reject pairs with an
+    endpoint >= V. `gen` is the reference's gen_rmat semantics."""
+    pairs, _ = gen(cfg["V"], cfg["pairs"], *RMAT, RMAT_SEED)
+    keep = (pairs[:, 0] < cfg["V"]) & (pairs[:, 1] < cfg["V"])
+    return np.ascontiguousarray(pairs[keep])
+
+
+def train_ratio(cfg):
+    return cfg.get("train_ratio") or cfg["train"] / cfg["V"]
+
+
+def agg_dims(cfg):
+    """Aggregation width per path (SG_{L-1} first): in_dim of layer L-1-i
+    (train.hpp:114: l == 0 ? f : dims[l-1])."""
+    L = len(cfg["dims"])
+    in_dims = [cfg["f"]] + cfg["dims"][:-1]
+    return [in_dims[L - 1 - i] for i in range(L)]
+
+
+def path_bytes(D, E, dim):
+    """Algorithmic bytes of one path's stage (SURVEY §8d B_l): offsets, 4 B
+    source index + 4 B fp32 weight per edge, one gathered source row per edge,
+    one destination row written."""
+    return 8 * (D + 1) + 8 * E + 4 * dim * E + 4 * dim * D
+
+
+def compulsory_bytes(D, S, E, dim):
+    return 8 * (D + 1) + 8 * E + 4 * dim * S + 4 * dim * D
+
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return float(json.load(open(p))["hbm_gbs"]), "measured (MEASURED_PEAKS.json copy)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """dram read+write bytes per launch of the dominant kernel, from the
+    committed ncu --set full summary (profiles/)."""
+    import glob
+
+    best = None
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_full_*.json"))):
+        try:
+            d = json.load(open(f))
+            best = d
+        except Exception:
+            pass
+    if best and "dram_bytes_per_launch" in best:
+        return best["dram_bytes_per_launch"], os.path.basename(f)
+    return None, None
+
+
+# ------------------------------------------------------------------ clocks --
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        loaded = [s for s in sm if s > 500] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------- reference arm --
+
+def run_reference(args):
+    """bench.py --impl reference: the reference's own CPU implementation
+    (oracle/_ref: /root/reference/proj/core compiled from source) builds the
+    graph, frontiers, paths and groupings itself and times its stage
+    (gather_rows + aggregate_pull<float> Deterministic, engine.hpp:331-338)
+    with all host threads on a bounded sample of the workload."""
+    from oracle.oracle import Ref, ref_available
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    if not ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libpathgcn_ref.so not built"}))
+        return
+    R = Ref()
+    t0 = time.time()
+    pairs = make_pairs(cfg, R.gen_rmat)
+    g = R.build_graph(pairs, n_hint=cfg["V"], symnorm=True)
+    vt = R.sample_training_set(cfg["V"], train_ratio(cfg), TRAIN_SEED)
+    L = len(cfg["dims"])
+    items = R.backward_stage_handles(g, vt, L, sample_stride=args.sample_stride)
+    levels_rows = [len(vt)]
+    # parent rows of path i: |levels[i]|; recover from the unsampled frontiers
+    lv = R.compute_frontiers(g, vt, L)
+    dims = agg_dims(cfg)
+    rng = np.random.default_rng(GRAD_SEED)
+    ys = [rng.uniform(-1, 1, size=(len(lv[i]), dims[i])).astype(np.float32) for i in range(L)]
+    setup_s = time.time() - t0
+    del levels_rows
+    threads = R.max_threads()
+    bytes_step = sum(path_bytes(it["D"], it["E"], dims[i]) for i, it in enumerate(items))
+    for _ in range(args.warmup):
+        for i, it in enumerate(items):
+            R.run_backward_stage(it, ys[i])
+    times = []
+    for _ in range(args.steps):
+        s = 0.0
+        for i, it in enumerate(items):
+            sec, _ = R.run_backward_stage(it, ys[i])
+            s += sec
+        times.append(s)
+    R.free_stage_handles(items)
+    step_s = statistics.mean(times)
+    gbs = bytes_step / step_s / 1e9
+    sample = (f"every {args.sample_stride}th destination of each path "
+              f"(D={[it['D'] for it in items]}, E={[it['E'] for it in items]}) of the {args.config}-shaped workload")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(gbs, 3), "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_s * 1e3, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": workload_config(cfg, args, [it["gs"] for it in items]),
+        "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "setup_s": round(setup_s, 1),
+        "ms_per_epoch_extrapolated": round(step_s * 1e3 * args.sample_stride, 1),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(cfg, args, gs):
+    return {"workload": f"{args.config}-shaped", "V": cfg["V"], "E_directed": cfg["m"], "L": len(cfg["dims"]),
+            "f": cfg["f"], "dims": cfg["dims"], "agg_widths": agg_dims(cfg), "train_ratio": round(train_ratio(cfg), 4),
+            "weights": "sym-norm", "gs": gs, "gs_strategy": "regression",
+            "l2": "inputs larger than L2 (each step streams the layer-0 y_grad/x_grad, > 1 GB at reddit)",
+            "parallelism": f"dest-row shards x{args.gpus} + NCCL all_gather" if args.gpus > 1 else "1 GPU"}
+
+
+# ------------------------------------------------------------- our arm ---
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="reddit", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--sample-stride", type=int, default=16, help="CPU baseline: keep every k-th destination")
+    ap.add_argument("--cpu-steps", type=int, default=3)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="few steps, no extras (for ncu)")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2204_02662_b200 as pg
+    from paper_2204_02662_b200 import dist as pgd
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    cfg = CONFIGS[args.config]
+    L = len(cfg["dims"])
+    dims = agg_dims(cfg)
+
+    t0 = time.time()
+    pairs = make_pairs(cfg, pg.gen_rmat)
+    vt = pg.sample_training_set(cfg["V"], train_ratio(cfg), TRAIN_SEED)
+    t_gen = time.time() - t0
+    torch.cuda.synchronize()
+    t1 = time.time()
+    g = pg.build_undirected_csr(pairs, n_hint=cfg["V"], weights="symnorm", device=local)
+    t_graph = time.time() - t1
+    t2 = time.time()
+    prep = pg.prepare_paths(g, vt, L, dims, gs_strategy="regression")
+    t_prep = time.time() - t2
+    paths, groups = prep.paths, prep.groups
+    assert g.m == cfg["m"], (g.m, cfg["m"])
+    log(f"[bench] gen {t_gen:.1f}s graph {t_graph:.2f}s prep {t_prep:.2f}s n={g.n} m={g.m} "
+        f"paths D/S/E={[(p.D, p.S, p.E) for p in paths]} gs={prep.gs}")
+
+    # ---- sharding plan (identity at N=1)
+    dest_bounds = [p.shard_bounds(world) for p in paths]
+    parent_rows = [p.P for p in paths]
+    shards = pgd.plan([None] * L, parent_rows, world, dest_bounds)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(GRAD_SEED)
+    y_shard, y_full, x_out, rows = [], [], [], []
+    for i, p in enumerate(paths):
+        ld = pg.padded_ld(dims[i])
+        sh = shards[i]
+        if world > 1:
+            groups[i].remap_sources(sh.source_map, sh.gathered_rows)
+            ys = torch.zeros((sh.max_rows, ld), dtype=torch.float32, device=dev)
+            pb, pe = sh.my_parent_rows(rank)
+            ys[: pe - pb, : dims[i]].uniform_(-1, 1, generator=gen)
+            y_shard.append(ys)
+            y_full.append(torch.empty((sh.gathered_rows, ld), dtype=torch.float32, device=dev))
+            db, de = sh.my_dest_rows(rank)
+            rows.append((db, de))
+        else:
+            yf = torch.zeros((p.P, ld), dtype=torch.float32, device=dev)
+            yf[:, : dims[i]].uniform_(-1, 1, generator=gen)
+            y_shard.append(yf)
+            y_full.append(yf)
+            rows.append((0, p.D))
+        x_out.append(pg.empty_rows(rows[i][1] - rows[i][0], dims[i], device=dev))
+
+    stream = torch.cuda.current_stream()
+
+    def step(ev=None):
+        for i in range(L):
+            if ev is not None:
+                ev[i][0].record(stream)
+            if world > 1:
+                pgd.allgather_rows(y_shard[i], y_full[i])
+            if ev is not None:
+                ev[i][1].record(stream)
+            pg.backward_aggregation(groups[i], y_full[i][:, : dims[i]], x_out[i], overwrite=True,
+                                    rows=rows[i] if world > 1 else None)
+            if ev is not None:
+                ev[i][2].record(stream)
+
+    for _ in range(max(args.warmup, 1)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(L)] for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.15)
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for k in range(args.steps):
+        step(evs[k])
+    end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    total_ms = start.elapsed_time(end)
+    spmm_ms = [[evs[k][i][1].elapsed_time(evs[k][i][2]) for k in range(args.steps)] for i in range(L)]
+    ag_ms = [[evs[k][i][0].elapsed_time(evs[k][i][1]) for k in range(args.steps)] for i in range(L)]
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item()) / args.steps
+    ep_bytes = sum(path_bytes(p.D, p.E, dims[i]) for i, p in enumerate(paths))
+    value = ep_bytes / (ms_step / 1e3) / 1e9
+
+    # ---- roofline of the dominant kernel (largest per-launch time): the
+    # layer-0 SpMM; bytes of this rank's rows
+    dom = max(range(L), key=lambda i: statistics.mean(spmm_ms[i]))
+    p = paths[dom]
+    offs = None
+    db, de = rows[dom]
+    if (db, de) == (0, p.D):
+        dom_bytes = path_bytes(p.D, p.E, dims[dom])
+    else:
+        offs = p.export()["offsets"]
+        dom_bytes = path_bytes(de - db, int(offs[de] - offs[db]), dims[dom])
+    dom_ms = statistics.mean(spmm_ms[dom])
+    peak, peak_src = hbm_peak()
+    achieved = dom_bytes / (dom_ms / 1e3) / 1e9
+    traffic, traffic_src = ncu_traffic()
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "kernel": f"k_agg_vec4 (path SG_{p.layer}, width {dims[dom]})",
+                "algorithmic_bytes_per_launch": dom_bytes, "avg_launch_ms": round(dom_ms, 4),
+                "peak_source": peak_src, "traffic_source": traffic_src,
+                "frac_vs_8TBps_spec": round(achieved / 8000.0, 4)}
+
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic: exact-V RMAT(.45/.22/.22/.11, seed 7), sym-norm weights, "
+                "V_t = sample_training_set(V, ratio, 42), y_grad ~ U(-1,1) fp32",
+        "config": workload_config(cfg, args, prep.gs),
+        "roofline": roofline,
+        "gpu_launches": L * args.steps,
+        "clocks": clk,
+        "per_path_ms": [round(statistics.mean(x), 4) for x in spmm_ms],
+        "allgather_ms": [round(statistics.mean(x), 4) for x in ag_ms] if world > 1 else None,
+        "epoch_algorithmic_bytes": ep_bytes,
+        "epoch_compulsory_bytes": sum(compulsory_bytes(p.D, p.S, p.E, dims[i]) for i, p in enumerate(paths)),
+        "prep_s": {"rmat_gen_host": round(t_gen, 2), "graph_build": round(t_graph, 3),
+                   "paths_groups_gs": round(t_prep, 3)},
+        "paths": [{"layer": p.layer, "D": p.D, "S": p.S, "E": p.E, "gs": prep.gs[i]} for i, p in enumerate(paths)],
+    }
+
+    if not args.profile and not args.no_e2e:
+        line["e2e"] = measure_e2e(pg, pgd, torch, dist, paths, groups, shards, dims, rows, world, rank, dev,
+                                  max(3, min(args.steps, 10)), ep_bytes)
+    if not args.profile and not args.no_cpu and world == 1 and rank == 0:
+        line["cpu_baseline"] = cpu_baseline(paths, dims, args)
+
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def measure_e2e(pg, pgd, torch, dist, paths, groups, shards, dims, rows, world, rank, dev, steps, ep_bytes):
+    """Same metric through the public API with HOST buffers: every step
+    copies this rank's y_grad rows host->device (pinned), aggregates, and
+    reads this rank's x_grad rows back. N=1: the host DenseMatrix drop-in
+    (pg_backward_aggregate_host: H2D, SpMM, D2H, synchronise)."""
+    L = len(paths)
+    rng = np.random.default_rng(GRAD_SEED + 1)
+    h2d = d2h = 0
+    if world == 1:
+        ys, xs = [], []
+        for i, p in enumerate(paths):
+            yh = torch.empty((p.P, dims[i]), dtype=torch.float32, pin_memory=True).numpy()
+            yh[:] = rng.uniform(-1, 1, size=yh.shape).astype(np.float32)
+            xh = torch.empty((p.D, dims[i]), dtype=torch.float32, pin_memory=True).numpy()
+            ys.append(yh)
+            xs.append(xh)
+            h2d += yh.nbytes
+            d2h += xh.nbytes
+
+        def one():
+            for i in range(L):
+                pg.backward_aggregation(groups[i], ys[i], xs[i], overwrite=True)
+        one()
+        t = time.perf_counter()
+        for _ in range(steps):
+            one()
+        sec = (time.perf_counter() - t) / steps
+    else:
+        ys, yd, yf, xd, xh = [], [], [], [], []
+        for i, p in enumerate(paths):
+            sh = shards[i]
+            pb, pe = sh.my_parent_rows(rank)
+            ld = pg.padded_ld(dims[i])
+            yh = torch.empty((pe - pb, dims[i]), dtype=torch.float32, pin_memory=True)
+            yh.uniform_(-1, 1)
+            ys.append(yh)
+            yd.append(torch.zeros((sh.max_rows, ld), dtype=torch.float32, device=dev))
+            yf.append(torch.empty((sh.gathered_rows, ld), dtype=torch.float32, device=dev))
+            xd.append(pg.empty_rows(rows[i][1] - rows[i][0], dims[i], device=dev))
+            xh.append(torch.empty((rows[i][1] - rows[i][0], dims[i]), dtype=torch.float32, pin_memory=True))
+            h2d += yh.numel() * 4
+            d2h += xh[-1].numel() * 4
+
+        def one():
+            for i in range(L):
+                yd[i][: ys[i].shape[0], : dims[i]].copy_(ys[i], non_blocking=True)
+                pgd.allgather_rows(yd[i], yf[i])
+                pg.backward_aggregation(groups[i], yf[i][:, : dims[i]], xd[i], overwrite=True, rows=rows[i])
+                xh[i].copy_(xd[i], non_blocking=True)
+            torch.cuda.synchronize()
+        one()
+        dist.barrier()
+        t = time.perf_counter()
+        for _ in range(steps):
+            one()
+        dist.barrier()
+        sec = (time.perf_counter() - t) / steps
+        tt = torch.tensor([sec], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        sec = float(tt.item())
+    return {"value": round(ep_bytes / sec / 1e9, 2), "unit": "GB/s", "ms_per_step": round(sec * 1e3, 3),
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": steps,
+            "api": "pg_backward_aggregate_host (pinned host buffers)" if world == 1 else
+                   "H2D shard + NCCL all_gather + pg_backward_aggregate_rows + D2H shard"}
+
+
+def cpu_baseline(paths, dims, args):
+    """The reference's own stage (oracle/_ref, engine.hpp:331-338) on this
+    host's cores, on a bounded stride sample of the same paths (bytes
+    identical to the device paths, which the parity tests prove equal to
+    extract_execution_path's)."""
+    try:
+        from oracle.oracle import Ref, ref_available
+    except Exception as e:  # pragma: no cover
+        return {"unavailable": str(e)}
+    if not ref_available():
+        return {"unavailable": "oracle/_ref not built"}
+    R = Ref()
+    arrays = []
+    for p in paths:
+        x = p.export()
+        x["layer"] = p.layer
+        arrays.append(x)
+    items = R.stage_items_from_arrays(arrays, sample_stride=args.sample_stride)
+    del arrays
+    rng = np.random.default_rng(GRAD_SEED)
+    ys = [rng.uniform(-1, 1, size=(p.P, dims[i])).astype(np.float32) for i, p in enumerate(paths)]
+    for i, it in enumerate(items):
+        R.run_backward_stage(it, ys[i])
+    times = []
+    for _ in range(args.cpu_steps):
+        times.append(sum(R.run_backward_stage(it, ys[i])[0] for i, it in enumerate(items)))
+    sec = statistics.median(times)
+    b = sum(path_bytes(it["D"], it["E"], dims[i]) for i, it in enumerate(items))
+    out = {"value": round(b / sec / 1e9, 3), "unit": "GB/s", "cores": R.max_threads(), "kind": "reference",
+           "sample": f"every {args.sample_stride}th destination of each path (D={[it['D'] for it in items]}, "
+                     f"E={[it['E'] for it in items]}); median of {args.cpu_steps} after 1 warm-up",
+           "ms_per_sample_epoch": round(sec * 1e3, 2),
+           "ms_per_epoch_extrapolated": round(sec * 1e3 * args.sample_stride, 1)}
+    R.free_stage_handles(items)
+    return out
+
+
+if __name__ == "__main__":
+    main()

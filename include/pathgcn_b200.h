@@ -173,6 +173,12 @@ int pg_stage_counters(pg_groups G, uint64_t dim, unsigned flags, uint64_t* count
  * [world+1] in dest-local row order, cut at E*r/world. */
 int pg_path_shard_bounds(pg_path p, uint32_t world, uint32_t* bounds);
 
+/* Multi-GPU: after a padded allgather of y_grad row shards, parent row p
+ * lives at row map[p] of a new_rows-row buffer. Installs the remapped edge
+ * stream on this grouping (pg_backward_aggregate* then expect
+ * y_rows == new_rows); map NULL removes it. map: host u32[parent_rows]. */
+int pg_groups_remap_sources(pg_groups G, const uint32_t* map, uint64_t map_len, uint64_t new_rows);
+
 /* ---------------- dense helpers of backward_epp ---------------- */
 
 /* dense_matrix.hpp:78-95 gemm_a_bt: out[n x m] = a[n x k] * b[m x k]^T */

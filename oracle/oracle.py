@@ -357,6 +357,8 @@ class Ref:
         L.ref_path_info.argtypes = [vp, u32p, u32p, u64p]
         L.ref_path_export.argtypes = [vp, u32p, u32p, u32p, u64p, u32p, f64p]
         L.ref_path_sample.argtypes = [vp, C.c_uint32, C.POINTER(vp)]
+        L.ref_path_from_arrays.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, u32p, u32p, u32p, u64p, u32p, f64p,
+                                           C.POINTER(vp)]
         L.ref_group.argtypes = [vp, C.c_int, C.c_uint32, C.POINTER(vp)]
         L.ref_group_count.restype = C.c_uint64
         L.ref_group_count.argtypes = [vp]
@@ -656,6 +658,33 @@ class Ref:
             items.append(dict(hp=hp, hgr=hgr, layer=layer, gs=gs, D=D.value, S=S.value, E=E.value))
         self.L.ref_free_front(hf)
         self.L.ref_free_graph(hg)
+        return items
+
+    def stage_items_from_arrays(self, paths, sample_stride=1, gs_list=None):
+        """Reference handles for paths given as dicts of ExecutionPath arrays
+        (dest, src, srcpos, offsets, neighbors, weights, layer), optionally
+        stride-sampled (ref_path_sample), grouped with regression gs."""
+        items = []
+        for i, p in enumerate(paths):
+            arr = {k: np.ascontiguousarray(p[k]) for k in ("dest", "src", "srcpos", "offsets", "neighbors", "weights")}
+            hp = vp()
+            self._check(self.L.ref_path_from_arrays(
+                p["layer"], len(arr["dest"]), len(arr["src"]), _p(arr["dest"], u32p), _p(arr["src"], u32p),
+                _p(arr["srcpos"], u32p), _p(arr["offsets"], u64p), _p(arr["neighbors"], u32p),
+                _p(arr["weights"], f64p), C.byref(hp)))
+            if sample_stride > 1:
+                hs = vp()
+                self._check(self.L.ref_path_sample(hp, sample_stride, C.byref(hs)))
+                self.L.ref_free_path(hp)
+                hp = hs
+            gs = self.L.ref_path_regression_gs(hp) if gs_list is None else gs_list[i]
+            hgr = vp()
+            self._check(self.L.ref_group(hp, 1, gs, C.byref(hgr)))
+            D = C.c_uint32()
+            S = C.c_uint32()
+            E = C.c_uint64()
+            self.L.ref_path_info(hp, C.byref(D), C.byref(S), C.byref(E))
+            items.append(dict(hp=hp, hgr=hgr, layer=p["layer"], gs=gs, D=D.value, S=S.value, E=E.value))
         return items
 
     def run_backward_stage(self, item, y_grad, fast=False, workers=0, want_out=False):

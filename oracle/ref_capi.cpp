@@ -208,6 +208,26 @@ void ref_path_export(void* hp, uint32_t* dest, uint32_t* src, uint32_t* srcpos,
     std::memcpy(w, p.weights.data(), p.weights.size() * 8);
 }
 
+// An ExecutionPath from arrays (e.g. exported by the device path, which the
+// parity tests prove bit-identical to extract_execution_path's output).
+int ref_path_from_arrays(uint64_t layer, uint32_t D, uint32_t S, const uint32_t* dest,
+                         const uint32_t* src, const uint32_t* srcpos, const uint64_t* offsets,
+                         const uint32_t* nbrs, const double* w, void** out) {
+    return guard([&] {
+        auto* h = new RefPath;
+        ExecutionPath& p = h->p;
+        p.layer = layer;
+        p.dest_local_to_global.assign(dest, dest + D);
+        p.src_local_to_global.assign(src, src + S);
+        p.src_pos_in_parent.assign(srcpos, srcpos + S);
+        p.offsets.assign(offsets, offsets + D + 1);
+        const uint64_t E = offsets[D];
+        p.neighbors.assign(nbrs, nbrs + E);
+        p.weights.assign(w, w + E);
+        *out = h;
+    });
+}
+
 // Bounded-sample sub-path for the CPU baseline: keeps every `stride`-th
 // destination (all of its edges) and re-compacts the referenced sources the
 // same way extract_execution_path does, so the sample is itself a valid

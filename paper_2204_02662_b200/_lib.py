@@ -103,6 +103,7 @@ SIGNATURES = {
     "pg_backward_aggregate_host": [H, f32p, u64, u64, f32p, C.c_uint, u64p],
     "pg_stage_counters": [H, u64, C.c_uint, u64p],
     "pg_path_shard_bounds": [H, u32, u32p],
+    "pg_groups_remap_sources": [H, u32p, u64, u64],
     "pg_gemm_a_bt": [vp, u64, vp, u64, vp, u64, u64, u64, u64, vp],
     "pg_relu_backward": [vp, u64, vp, u64, vp, u64, u64, u64, vp],
     "pg_gather_rows": [vp, u64, vp, u64, vp, u64, u64, vp],

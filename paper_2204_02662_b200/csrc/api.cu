@@ -118,6 +118,10 @@ void counters_of(Groups& G, uint64_t dim, unsigned flags, uint64_t* c) {
     c[2] = (flags & PG_AGG_FAST) ? fast_atomic_groups(G) * dim : 0;
 }
 
+// rows of the parent-indexed input: the parent frontier, or the padded
+// allgather layout once pg_groups_remap_sources installed a map
+uint64_t y_rows_of(const Groups& G) { return G.edges_remap.get() ? G.remap_rows : G.path->P; }
+
 void check_dims(uint64_t dim, uint64_t ld_in, uint64_t ld_out) {
     if (ld_in < dim || ld_out < dim) fail(kConfig, "aggregate_pull: leading dimension smaller than dim");
 }
@@ -130,6 +134,7 @@ void run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re, con
     if (G.path) {
         Path& p = *G.path;
         const Edge* edges = p.edges_parent.get();
+        if (parent_indexed && G.edges_remap.get()) edges = G.edges_remap.get();
         if (!parent_indexed && p.S != p.P) {
             path_pack_local(p, lib_stream(p.device));
             PG_CUDA(cudaStreamSynchronize(lib_stream(p.device)));
@@ -593,7 +598,7 @@ int pg_backward_aggregate(pg_groups h, const float* y_dev, uint64_t y_rows, uint
         Groups& G = *R_(h);
         if (!G.path) fail(kConfig, "backward_aggregate: grouping is not over an execution path");
         check_dims(dim, ld_in, ld_out);
-        if (y_rows != G.path->P) fail(kConfig, "backward_aggregate: y_grad rows != parent frontier size");
+        if (y_rows != y_rows_of(G)) fail(kConfig, "backward_aggregate: y_grad rows != parent frontier size");
         run_aggregate(G, true, 0, G.path->D, y_dev, ld_in, x_dev, ld_out, dim, flags,
                       static_cast<cudaStream_t>(stream));
     });
@@ -606,7 +611,7 @@ int pg_backward_aggregate_rows(pg_groups h, uint32_t row_begin, uint32_t row_end
         Groups& G = *R_(h);
         if (!G.path) fail(kConfig, "backward_aggregate: grouping is not over an execution path");
         check_dims(dim, ld_in, ld_out);
-        if (y_rows != G.path->P) fail(kConfig, "backward_aggregate: y_grad rows != parent frontier size");
+        if (y_rows != y_rows_of(G)) fail(kConfig, "backward_aggregate: y_grad rows != parent frontier size");
         if (row_begin > row_end || row_end > G.path->D) fail(kConfig, "backward_aggregate: bad row range");
         if (row_begin == row_end) return;
         run_aggregate(G, true, row_begin, row_end, y_dev, ld_in, x_dev, ld_out, dim, flags,
@@ -630,9 +635,34 @@ int pg_backward_aggregate_host(pg_groups h, const float* y_host, uint64_t y_rows
     return guard([&] {
         Groups& G = *R_(h);
         if (!G.path) fail(kConfig, "backward_aggregate: grouping is not over an execution path");
-        if (y_rows != G.path->P) fail(kConfig, "backward_aggregate: y_grad rows != parent frontier size");
+        if (y_rows != y_rows_of(G)) fail(kConfig, "backward_aggregate: y_grad rows != parent frontier size");
         run_host(G, true, y_host, y_rows, dim, x_host, flags);
         counters_of(G, dim, flags, counters);
+    });
+}
+
+int pg_groups_remap_sources(pg_groups h, const uint32_t* map, uint64_t map_len, uint64_t new_rows) {
+    return guard([&] {
+        Groups& G = *R_(h);
+        if (!G.path) fail(kConfig, "remap: grouping is not over an execution path");
+        Path& p = *G.path;
+        DeviceGuard dg(G.device);
+        cudaStream_t s = lib_stream(G.device);
+        if (!map) {
+            G.edges_remap.reset();
+            G.remap_rows = 0;
+            return;
+        }
+        if (map_len != p.P) fail(kConfig, "remap: map length != parent frontier size");
+        for (uint64_t i = 0; i < map_len; ++i)
+            if (map[i] >= new_rows) fail(kConfig, "remap: map entry out of range");
+        DevBuf<uint32_t> dmap(map_len, s);
+        if (map_len) PG_CUDA(cudaMemcpyAsync(dmap.get(), map, map_len * 4, cudaMemcpyHostToDevice, s));
+        DevBuf<Edge> out(p.E, s);
+        remap_edges(p.edges_parent.get(), p.E, dmap.get(), out.get(), s);
+        PG_CUDA(cudaStreamSynchronize(s));
+        G.edges_remap = std::move(out);
+        G.remap_rows = new_rows;
     });
 }
 

@@ -176,6 +176,15 @@ __global__ void k_src_pos(const uint32_t* __restrict__ src, uint32_t S,
     if (s < S) srcpos[s] = rank_of(parent_bits, parent_prefix, src[s]);
 }
 
+__global__ void k_remap(const Edge* __restrict__ in, uint64_t E, const uint32_t* __restrict__ map,
+                        Edge* __restrict__ out) {
+    const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (i < E) {
+        const Edge e = in[i];
+        out[i] = make_uint2(map[e.x], e.y);
+    }
+}
+
 __global__ void k_pack_local(const uint32_t* __restrict__ nl, const Edge* __restrict__ ep, uint64_t E,
                              Edge* __restrict__ out) {
     const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
@@ -413,6 +422,12 @@ std::unique_ptr<Path> path_extract(const Graph& g, const Frontiers& f, uint64_t 
     p->max_degree = max_degree_dev(p->offsets.get(), D, s);
     PG_CUDA(cudaStreamSynchronize(s));
     return p;
+}
+
+void remap_edges(const Edge* in, uint64_t E, const uint32_t* map, Edge* out, cudaStream_t s) {
+    if (E == 0) return;
+    k_remap<<<grid_for(E, kThreads), kThreads, 0, s>>>(in, E, map, out);
+    PG_LAUNCH("k_remap");
 }
 
 void path_pack_local(Path& p, cudaStream_t s) {

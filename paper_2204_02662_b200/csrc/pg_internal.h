@@ -97,7 +97,13 @@ struct Groups {
     DevBuf<uint32_t> graph_order;  // schedule for graph groupings (lazy)
     DevBuf<uint32_t> shard_order;  // schedule of one destination-row shard (lazy)
     uint32_t shard_rb = 0, shard_re = 0;
+    // multi-GPU: parent rows remapped into a padded allgather layout
+    DevBuf<Edge> edges_remap;
+    uint64_t remap_rows = 0;
 };
+
+// edges_out[e] = (map[edges_in[e].x], edges_in[e].y)
+void remap_edges(const Edge* in, uint64_t E, const uint32_t* map, Edge* out, cudaStream_t s);
 
 // ---- launchers (implemented in graph.cu / path.cu / aggregate.cu) ----
 std::unique_ptr<Graph> graph_build(int device, int64_t n_hint, const uint32_t* pairs_host,

@@ -1,0 +1,95 @@
+"""Multi-GPU destination-row sharding of the execution paths.
+
+Each rank holds the full graph and all paths (replicated, built on device),
+owns an edge-balanced slice of every path's destination rows
+(pg_path_shard_bounds) and computes only those rows of X'. The rows of
+y_grad entering path i follow the parent frontier levels[i]; they are
+produced in the previous path's destination partition (path i-1), or an
+equal split of V_t for the top path. Before each path's SpMM one NCCL
+all_gather of the padded y_grad row shards gives every rank the full
+matrix; the SpMM reads it in place through a remapped edge stream
+(parent row p -> rank(p) * max_rows + (p - start(rank(p)))), so no unpad
+copy is needed. Only host-side planning lives here; the exchange is
+torch.distributed (NCCL on GPU, gloo in the CPU tests).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+def equal_bounds(rows: int, world: int) -> np.ndarray:
+    return np.array([(rows * r) // world for r in range(world + 1)], np.int64)
+
+
+def edge_balanced_bounds(offsets: np.ndarray, world: int) -> np.ndarray:
+    """Host restatement of pg_path_shard_bounds: cut dest rows at E*r/world."""
+    E = int(offsets[-1])
+    D = len(offsets) - 1
+    b = [0]
+    for r in range(1, world):
+        target = (E * r) // world
+        row = int(np.searchsorted(offsets[:-1], target, side="left"))
+        b.append(max(b[-1], min(row, D)))
+    b.append(D)
+    return np.array(b, np.int64)
+
+
+@dataclass
+class LayerShard:
+    """Row ownership of one path on one rank."""
+    parent_bounds: np.ndarray  # world+1 cuts of the parent frontier (y_grad rows)
+    dest_bounds: np.ndarray  # world+1 cuts of the destination rows (x_grad rows)
+    max_rows: int  # padded y_grad shard rows (allgather unit)
+    source_map: np.ndarray  # parent row -> row of the padded allgather buffer
+
+    def my_parent_rows(self, rank):
+        return int(self.parent_bounds[rank]), int(self.parent_bounds[rank + 1])
+
+    def my_dest_rows(self, rank):
+        return int(self.dest_bounds[rank]), int(self.dest_bounds[rank + 1])
+
+    @property
+    def gathered_rows(self):
+        return self.max_rows * (len(self.parent_bounds) - 1)
+
+
+def padded_source_map(parent_bounds: np.ndarray) -> tuple[np.ndarray, int]:
+    world = len(parent_bounds) - 1
+    sizes = np.diff(parent_bounds)
+    max_rows = int(max(sizes.max(initial=0), 1))
+    P = int(parent_bounds[-1])
+    owner = np.searchsorted(parent_bounds[1:], np.arange(P), side="right")
+    local = np.arange(P) - parent_bounds[owner]
+    m = (owner * max_rows + local).astype(np.uint32)
+    assert owner.max(initial=0) < world
+    return m, max_rows
+
+
+def plan(path_offsets: list, parent_rows: list, world: int, dest_bounds: list | None = None) -> list:
+    """LayerShard per path (SG_{L-1} first). path_offsets[i]: u64[D_i+1];
+    parent_rows[i] = |levels[i]|; dest_bounds[i] optional precomputed cuts
+    (from the device, pg_path_shard_bounds); path_offsets may then be None."""
+    out = []
+    prev_dest = None
+    for i, offs in enumerate(path_offsets):
+        db = np.asarray(dest_bounds[i], np.int64) if dest_bounds is not None else edge_balanced_bounds(offs, world)
+        if i == 0 or prev_dest is None:
+            pb = equal_bounds(parent_rows[i], world)
+        else:
+            pb = prev_dest
+        if int(pb[-1]) != parent_rows[i]:
+            raise ValueError("path chain: parent frontier of path i must be the destinations of path i-1")
+        smap, mr = padded_source_map(pb)
+        out.append(LayerShard(pb, db, mr, smap))
+        prev_dest = db
+    return out
+
+
+def allgather_rows(shard, out, group=None):
+    """All-gather equal-sized padded row shards: out[world*max_rows, ...]."""
+    import torch.distributed as dist
+
+    dist.all_gather_into_tensor(out, shard, group=group)
+    return out

@@ -362,6 +362,19 @@ class GroupedCsr:
         _check(_lib_().pg_groups_export(self._h, _p(gd, u32p), _p(gb, u64p), _p(ge, u64p), _p(dg, u64p)))
         return dict(dest=gd[:G], begin=gb[:G], end=ge[:G], dest_groups=dg)
 
+    remap_rows = None
+
+    def remap_sources(self, mapping, new_rows):
+        """Multi-GPU: parent row p of y_grad lives at row mapping[p] of a
+        new_rows-row (padded allgather) buffer. None removes the map."""
+        if mapping is None:
+            _check(_lib_().pg_groups_remap_sources(self._h, None, 0, 0))
+            self.remap_rows = None
+            return
+        m = _u32(mapping)
+        _check(_lib_().pg_groups_remap_sources(self._h, _p(m, u32p), len(m), int(new_rows)))
+        self.remap_rows = int(new_rows)
+
     def counters(self, dim, mode=DETERMINISTIC):
         c = np.zeros(3, np.uint64)
         _check(_lib_().pg_stage_counters(self._h, dim, _flags(mode), _p(c, u64p)))
@@ -474,7 +487,7 @@ def backward_aggregation(grouped: GroupedCsr, y_grad, x_grad, mode=DETERMINISTIC
         _check(_lib_().pg_backward_aggregate_host(grouped._h, _p(y, f32p), y.shape[0], y.shape[1],
                                                   _p(x_grad, f32p), flags, _p(c, u64p)))
         return x_grad
-    _dev(y_grad, "y_grad", rows=path.P)
+    _dev(y_grad, "y_grad", rows=path.P if grouped.remap_rows is None else grouped.remap_rows)
     if rows is None:
         _dev(x_grad, "x_grad", rows=path.D, cols=y_grad.shape[1])
         _check(_lib_().pg_backward_aggregate(grouped._h, C.c_void_p(y_grad.data_ptr()), y_grad.shape[0],
@@ -522,8 +535,10 @@ def gather_rows(src, ids, out, stream=None):
 
 
 def padded_ld(cols):
-    """Device row pitch used for gradient matrices: 32 floats (128 B)."""
-    return (cols + 31) // 32 * 32
+    """Device row pitch for gradient matrices: 16-B rows for narrow widths,
+    whole 128-B lines (32 floats) beyond 32 columns, so every row gather is
+    sector aligned (e.g. 602 -> 608: 19 full lines instead of 76-77 sectors)."""
+    return (cols + 3) // 4 * 4 if cols <= 32 else (cols + 31) // 32 * 32
 
 
 def empty_rows(rows, cols, device="cuda"):
