@@ -57,6 +57,10 @@ typedef struct pg_groups_s* pg_groups;       /* GroupedCsr    grouping.hpp:14-28
 int pg_last_error(char* buf, size_t cap);
 int pg_version(void);
 int pg_device_count(int* count);
+/* Scheduling knob (never changes results): destinations with at least this
+ * many path edges run on the TMA-ring heavy kernel (default 1024 or
+ * $PG_HEAVY_MIN_DEG; 0 disables). */
+int pg_set_heavy_min_degree(uint64_t min_degree);
 
 /* ---------------- graph load ---------------- */
 

@@ -13,6 +13,9 @@
 // from U edges in flight per lane (U independent LDG.128 before the ordered
 // adds). The gather of gradient rows (engine.hpp:334) is folded into the
 // packed edge record (src_pos_in_parent composed at path build).
+#include <algorithm>
+#include <vector>
+
 #include "pg_internal.h"
 
 namespace pg {
@@ -125,6 +128,188 @@ __global__ void __launch_bounds__(256) k_agg_scalar(const uint64_t* __restrict__
     if (active) out[d * ld_out + col] = __fadd_rn(acc, 0.f);
 }
 
+// ---- heavy destinations: TMA bulk-copy ring ---------------------------------
+// One CTA = one producer warp + one consumer warp per (heavy destination,
+// 32-float4 column chunk). The producer streams the destination's gradient
+// row chunks into a kHeavyStages-deep shared-memory ring with
+// cp.async.bulk (one 16..512-byte copy per edge, UBLKCP in SASS) completing
+// on mbarriers; the consumer warp applies them in ascending edge order
+// (lane = float4 column), so the summation order — and hence every bit —
+// is the reference's while a 50K-edge hub still has ~64 KB in flight.
+constexpr int kHeavyStages = 4;
+constexpr int kHeavyStageBytes = 16384;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "LAB_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra.uni DONE;\n\t"
+        "bra.uni LAB_WAIT;\n"
+        "DONE:\n\t}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+template <int CHQ>
+__host__ __device__ constexpr int heavy_T() {
+    return kHeavyStageBytes / (CHQ * 16);
+}
+template <int CHQ>
+constexpr size_t heavy_smem() {
+    return kHeavyStages * (kHeavyStageBytes + heavy_T<CHQ>() * 4) + 2 * kHeavyStages * 8;
+}
+
+template <int CHQ>
+__global__ void __launch_bounds__(64) k_agg_heavy(const uint64_t* __restrict__ offsets,
+                                                 const Edge* __restrict__ edges,
+                                                 const uint32_t* __restrict__ order, uint32_t d_begin,
+                                                 uint32_t chunks, uint32_t nq_total,
+                                                 const float* __restrict__ in, uint64_t ld_in,
+                                                 float* __restrict__ out, uint64_t ld_out, uint32_t dim,
+                                                 int accumulate) {
+    constexpr int T = heavy_T<CHQ>();
+    constexpr int NS = kHeavyStages;
+    extern __shared__ __align__(128) unsigned char smem[];
+    float4* buf = reinterpret_cast<float4*>(smem);
+    float* wbuf = reinterpret_cast<float*>(smem + NS * kHeavyStageBytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + NS * (kHeavyStageBytes + T * 4));
+    uint64_t* empty = full + NS;
+
+    const uint32_t item = blockIdx.x;
+    const uint32_t d = order[d_begin + item / chunks];
+    const uint32_t c = item % chunks;
+    const uint32_t q0 = c * CHQ;
+    const uint32_t nqc = min(static_cast<uint32_t>(CHQ), nq_total - q0);
+    const uint32_t row_bytes = nqc * 16;
+    const uint64_t eb = offsets[d], ee = offsets[d + 1];
+    const uint64_t ntiles = (ee - eb + T - 1) / T;
+    const unsigned lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(&full[s], 32);
+            mbar_init(&empty[s], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // producer warp
+        for (uint64_t t = 0; t < ntiles; ++t) {
+            const int s = static_cast<int>(t % NS);
+            const uint32_t ph = static_cast<uint32_t>((t / NS) & 1);
+            mbar_wait(&empty[s], ph ^ 1u);
+            const uint64_t e0 = eb + t * T;
+            const uint32_t n = static_cast<uint32_t>(min(static_cast<uint64_t>(T), ee - e0));
+            if (lane == 0) mbar_expect_tx(&full[s], n * row_bytes);
+            __syncwarp();
+            for (uint32_t j = lane; j < n; j += 32) {
+                const Edge ed = __ldg(edges + e0 + j);
+                wbuf[s * T + j] = __uint_as_float(ed.y);
+                bulk_g2s(buf + (static_cast<size_t>(s) * T + j) * CHQ, in + ed.x * ld_in + q0 * 4, row_bytes,
+                         &full[s]);
+            }
+            mbar_arrive(&full[s]);
+        }
+        return;
+    }
+    // consumer warp: lane = float4 column of the chunk
+    const bool active = lane < nqc;
+    const uint32_t col = (q0 + lane) * 4;
+    float* orow = out + d * ld_out + col;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (accumulate && active && col < dim) {
+        if (col + 3 < dim) acc = *reinterpret_cast<const float4*>(orow);
+        else {
+            acc.x = orow[0];
+            if (col + 1 < dim) acc.y = orow[1];
+            if (col + 2 < dim) acc.z = orow[2];
+        }
+    }
+    for (uint64_t t = 0; t < ntiles; ++t) {
+        const int s = static_cast<int>(t % NS);
+        const uint32_t ph = static_cast<uint32_t>((t / NS) & 1);
+        mbar_wait(&full[s], ph);
+        const uint32_t n = static_cast<uint32_t>(min(static_cast<uint64_t>(T), ee - (eb + t * T)));
+        if (active) {
+            const float4* sb = buf + static_cast<size_t>(s) * T * CHQ + lane;
+            const float* sw = wbuf + s * T;
+            for (uint32_t j = 0; j < n; ++j) acc4(acc, sw[j], sb[j * CHQ]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    if (!active || col >= dim) return;
+    acc.x = __fadd_rn(acc.x, 0.f);
+    acc.y = __fadd_rn(acc.y, 0.f);
+    acc.z = __fadd_rn(acc.z, 0.f);
+    acc.w = __fadd_rn(acc.w, 0.f);
+    if (col + 3 < dim) {
+        __stcs(reinterpret_cast<float4*>(orow), acc);
+    } else {
+        orow[0] = acc.x;
+        if (col + 1 < dim) orow[1] = acc.y;
+        if (col + 2 < dim) orow[2] = acc.z;
+    }
+}
+
+template <int CHQ>
+void launch_heavy(const uint64_t* offsets, const Edge* edges, const uint32_t* order, uint32_t d_begin, uint32_t nh,
+                  uint32_t nq, const float* in, uint64_t ld_in, float* out, uint64_t ld_out, uint32_t dim,
+                  bool accumulate, cudaStream_t s) {
+    static thread_local std::vector<char> attr_set;  // per device
+    constexpr size_t smem = heavy_smem<CHQ>();
+    int dev = 0;
+    PG_CUDA(cudaGetDevice(&dev));
+    if (static_cast<int>(attr_set.size()) <= dev) attr_set.resize(dev + 1, 0);
+    if (!attr_set[dev]) {
+        PG_CUDA(cudaFuncSetAttribute(k_agg_heavy<CHQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+        attr_set[dev] = 1;
+    }
+    const uint32_t chunks = (nq + CHQ - 1) / CHQ;
+    k_agg_heavy<CHQ><<<nh * chunks, 64, smem, s>>>(offsets, edges, order, d_begin, chunks, nq, in, ld_in, out,
+                                                   ld_out, dim, accumulate);
+    PG_LAUNCH("k_agg_heavy");
+}
+
+struct SideStream {
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+
+SideStream& side_stream() {
+    static thread_local std::vector<SideStream> per_dev;
+    int dev = 0;
+    PG_CUDA(cudaGetDevice(&dev));
+    if (static_cast<int>(per_dev.size()) <= dev) per_dev.resize(dev + 1);
+    SideStream& ss = per_dev[dev];
+    if (!ss.s) {
+        PG_CUDA(cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking));
+        PG_CUDA(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming));
+        PG_CUDA(cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming));
+    }
+    return ss;
+}
+
 template <int LPD, int U>
 void launch_vec4(const uint64_t* offsets, const Edge* edges, const uint32_t* order, uint32_t d_begin,
                  uint32_t nd, uint32_t chunks, const float* in, uint64_t ld_in, float* out, uint64_t ld_out,
@@ -192,15 +377,39 @@ __global__ void k_gather_rows(const float* __restrict__ src, uint64_t lds, const
 }  // namespace
 
 void aggregate_det(const uint64_t* offsets, const Edge* edges, const uint32_t* order, uint32_t D,
-                   uint32_t d_begin, uint32_t d_end, const float* in, uint64_t ld_in, float* out,
-                   uint64_t ld_out, uint64_t dim, bool accumulate, cudaStream_t s) {
+                   uint32_t d_begin, uint32_t d_end, uint32_t n_heavy, const float* in, uint64_t ld_in,
+                   float* out, uint64_t ld_out, uint64_t dim, bool accumulate, cudaStream_t s) {
     (void)D;
     if (d_end <= d_begin || dim == 0) return;
-    const uint32_t nd = d_end - d_begin;
+    uint32_t nd = d_end - d_begin;
     const uint32_t dim32 = static_cast<uint32_t>(dim);
     const bool vec = (ld_in % 4 == 0) && (ld_out % 4 == 0) &&
                      (reinterpret_cast<uintptr_t>(in) % 16 == 0) &&
                      (reinterpret_cast<uintptr_t>(out) % 16 == 0) && ld_in >= ((dim + 3) & ~3ull);
+    const uint32_t nh = vec ? std::min(n_heavy, nd) : 0;
+    if (nh) {
+        // heavy prefix of the degree order on a forked stream, concurrent
+        // with the main kernel over the rest; joined back into s
+        const uint32_t nq = (dim32 + 3) / 4;
+        SideStream& ss = side_stream();
+        PG_CUDA(cudaEventRecord(ss.fork, s));
+        PG_CUDA(cudaStreamWaitEvent(ss.s, ss.fork, 0));
+        if (nq > 16)
+            launch_heavy<32>(offsets, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim32, accumulate, ss.s);
+        else if (nq > 8)
+            launch_heavy<16>(offsets, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim32, accumulate, ss.s);
+        else if (nq > 4)
+            launch_heavy<8>(offsets, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim32, accumulate, ss.s);
+        else
+            launch_heavy<4>(offsets, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim32, accumulate, ss.s);
+        PG_CUDA(cudaEventRecord(ss.join, ss.s));
+        d_begin += nh;
+        nd -= nh;
+        if (nd) aggregate_det(offsets, edges, order, D, d_begin, d_begin + nd, 0, in, ld_in, out, ld_out, dim,
+                              accumulate, s);
+        PG_CUDA(cudaStreamWaitEvent(s, ss.join, 0));
+        return;
+    }
     if (!vec) {
         const uint32_t chunks = (dim32 + 31) / 32;
         const uint64_t items = static_cast<uint64_t>(nd) * chunks;

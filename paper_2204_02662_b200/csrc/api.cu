@@ -140,19 +140,20 @@ void run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re, con
             PG_CUDA(cudaStreamSynchronize(lib_stream(p.device)));
             edges = p.edges_local.get();
         }
+        const uint64_t hmin = heavy_min_degree();
         if (rb == 0 && re == p.D) {
-            aggregate_det(p.offsets.get(), edges, p.order.get(), p.D, 0, p.D, in, ld_in, out, ld_out, dim,
-                          accumulate, s);
+            aggregate_det(p.offsets.get(), edges, p.order.get(), p.D, 0, p.D, p.hist.heavy(hmin), in, ld_in, out,
+                          ld_out, dim, accumulate, s);
             return;
         }
         // shard: schedule of rows [rb, re) relative to rb
         if (!(G.shard_order.get() && G.shard_rb == rb && G.shard_re == re)) {
-            degree_order(p.offsets.get() + rb, re - rb, G.shard_order, lib_stream(p.device));
+            degree_order(p.offsets.get() + rb, re - rb, G.shard_order, lib_stream(p.device), &G.shard_hist);
             G.shard_rb = rb;
             G.shard_re = re;
         }
-        aggregate_det(p.offsets.get() + rb, edges, G.shard_order.get(), re - rb, 0, re - rb, in, ld_in, out,
-                      ld_out, dim, accumulate, s);
+        aggregate_det(p.offsets.get() + rb, edges, G.shard_order.get(), re - rb, 0, re - rb,
+                      G.shard_hist.heavy(hmin), in, ld_in, out, ld_out, dim, accumulate, s);
         return;
     }
     Graph& g = *G.graph;
@@ -160,9 +161,10 @@ void run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re, con
         graph_pack_edges(g, lib_stream(g.device));
         PG_CUDA(cudaStreamSynchronize(lib_stream(g.device)));
     }
-    if (!G.graph_order.get() && g.n) degree_order(g.offsets.get(), g.n, G.graph_order, lib_stream(g.device));
-    aggregate_det(g.offsets.get(), g.edges.get(), G.graph_order.get(), g.n, 0, g.n, in, ld_in, out, ld_out, dim,
-                  accumulate, s);
+    if (!G.graph_order.get() && g.n)
+        degree_order(g.offsets.get(), g.n, G.graph_order, lib_stream(g.device), &G.graph_hist);
+    aggregate_det(g.offsets.get(), g.edges.get(), G.graph_order.get(), g.n, 0, g.n,
+                  G.graph_hist.heavy(heavy_min_degree()), in, ld_in, out, ld_out, dim, accumulate, s);
 }
 
 // Host buffers (ld = dim) -> padded device buffers -> run -> host.
@@ -197,6 +199,10 @@ int pg_last_error(char* buf, size_t cap) {
 }
 
 int pg_version(void) { return 1; }
+
+int pg_set_heavy_min_degree(uint64_t min_degree) {
+    return guard([&] { set_heavy_min_degree(min_degree); });
+}
 
 int pg_device_count(int* count) {
     return guard([&] {

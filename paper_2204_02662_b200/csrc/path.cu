@@ -14,6 +14,8 @@
 //   * group_neighbors (grouping.cpp:7-27) and the cost-model group-size sweep
 //     (group_cost.cpp:9-53) as closed-form integer reductions.
 #include <algorithm>
+#include <atomic>
+#include <cstdlib>
 #include <vector>
 
 #include "pg_internal.h"
@@ -282,8 +284,19 @@ __global__ void k_cost_deficits(const uint64_t* __restrict__ offsets, const uint
 
 }  // namespace
 
-void degree_order(const uint64_t* offsets, uint32_t D, DevBuf<uint32_t>& order, cudaStream_t s) {
+namespace {
+std::atomic<uint64_t> g_heavy_min{[] {
+    const char* e = std::getenv("PG_HEAVY_MIN_DEG");
+    return e ? static_cast<uint64_t>(std::strtoull(e, nullptr, 10)) : uint64_t{1024};
+}()};
+}  // namespace
+
+uint64_t heavy_min_degree() { return g_heavy_min.load(std::memory_order_relaxed); }
+void set_heavy_min_degree(uint64_t v) { g_heavy_min.store(v, std::memory_order_relaxed); }
+
+void degree_order(const uint64_t* offsets, uint32_t D, DevBuf<uint32_t>& order, cudaStream_t s, DegHist* out_hist) {
     order = DevBuf<uint32_t>(D, s);
+    if (out_hist) *out_hist = DegHist{};
     if (D == 0) return;
     DevBuf<unsigned long long> hist(65, s);
     PG_CUDA(cudaMemsetAsync(hist.get(), 0, 65 * 8, s));
@@ -292,6 +305,8 @@ void degree_order(const uint64_t* offsets, uint32_t D, DevBuf<uint32_t>& order, 
     unsigned long long h[65];
     PG_CUDA(cudaMemcpyAsync(h, hist.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
     PG_CUDA(cudaStreamSynchronize(s));
+    if (out_hist)
+        for (int b = 0; b < 65; ++b) out_hist->h[b] = h[b];
     unsigned long long cur[65];
     unsigned long long run = 0;
     for (int b = 64; b >= 0; --b) {  // descending degree bucket
@@ -418,7 +433,7 @@ std::unique_ptr<Path> path_extract(const Graph& g, const Frontiers& f, uint64_t 
             p->edges_parent.get());
         PG_LAUNCH("k_fill_path");
     }
-    degree_order(p->offsets.get(), D, p->order, s);
+    degree_order(p->offsets.get(), D, p->order, s, &p->hist);
     p->max_degree = max_degree_dev(p->offsets.get(), D, s);
     PG_CUDA(cudaStreamSynchronize(s));
     return p;

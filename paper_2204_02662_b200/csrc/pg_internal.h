@@ -34,6 +34,21 @@ struct DeviceGuard {
 // Packed edge record streamed by the SpMM: (source row, fp32 weight bits).
 using Edge = uint2;
 
+// Degree-bucket histogram of a schedule (bucket b = floor(log2 deg) + 1).
+struct DegHist {
+    unsigned long long h[65] = {};
+    // destinations of degree >= min_deg (rounded up to a power of two): the
+    // prefix of the descending-bucket order
+    uint32_t heavy(uint64_t min_deg) const {
+        if (min_deg == 0) return 0;
+        int b0 = 1;
+        while ((1ull << (b0 - 1)) < min_deg) ++b0;
+        unsigned long long c = 0;
+        for (int b = b0; b < 65; ++b) c += h[b];
+        return static_cast<uint32_t>(c);
+    }
+};
+
 // csr_graph.hpp:19-38 CsrGraph, device resident.
 struct Graph {
     int device = 0;
@@ -82,6 +97,7 @@ struct Path {
     DevBuf<Edge> edges_parent;    // E (src_pos_in_parent[nbr], (float)w): gather folded
     DevBuf<Edge> edges_local;     // E (nbr_local, (float)w), lazily, only when S < P
     DevBuf<uint32_t> order;       // D dests in descending-degree-bucket order (SpMM schedule)
+    DegHist hist;                 // degree buckets of `order`
 };
 
 // grouping.hpp:14-28 GroupedCsr over a path (or the whole graph).
@@ -95,7 +111,9 @@ struct Groups {
     DevBuf<uint64_t> gbegin, gend;
     DevBuf<uint64_t> dest_groups;  // D+1
     DevBuf<uint32_t> graph_order;  // schedule for graph groupings (lazy)
+    DegHist graph_hist;
     DevBuf<uint32_t> shard_order;  // schedule of one destination-row shard (lazy)
+    DegHist shard_hist;
     uint32_t shard_rb = 0, shard_re = 0;
     // multi-GPU: parent rows remapped into a padded allgather layout
     DevBuf<Edge> edges_remap;
@@ -119,7 +137,8 @@ std::unique_ptr<Frontiers> frontiers_compute(const Graph& g, const uint32_t* vt_
                                              uint64_t L);
 std::unique_ptr<Path> path_extract(const Graph& g, const Frontiers& f, uint64_t layer);
 void path_pack_local(Path& p, cudaStream_t s);
-void degree_order(const uint64_t* offsets, uint32_t D, DevBuf<uint32_t>& order, cudaStream_t s);
+void degree_order(const uint64_t* offsets, uint32_t D, DevBuf<uint32_t>& order, cudaStream_t s,
+                  DegHist* hist = nullptr);
 
 std::unique_ptr<Groups> groups_build(uint32_t D, const uint64_t* offsets_dev, uint32_t gs,
                                      int device);
@@ -130,9 +149,13 @@ void grouping_cost_dev(uint32_t D, const uint64_t* offsets_dev, uint32_t gs, uin
 
 // aggregate.hpp:56-122 Deterministic, ascending edge order per element.
 //   out[order[i]] (+)= sum_e w_e * in[edges[e].x]
+// The first n_heavy entries of order[d_begin..] (the high-degree prefix of
+// the degree-bucket order) run on the TMA-ring kernel concurrently.
 void aggregate_det(const uint64_t* offsets, const Edge* edges, const uint32_t* order, uint32_t D,
-                   uint32_t d_begin, uint32_t d_end, const float* in, uint64_t ld_in, float* out,
-                   uint64_t ld_out, uint64_t dim, bool accumulate, cudaStream_t s);
+                   uint32_t d_begin, uint32_t d_end, uint32_t n_heavy, const float* in, uint64_t ld_in,
+                   float* out, uint64_t ld_out, uint64_t dim, bool accumulate, cudaStream_t s);
+uint64_t heavy_min_degree();  // PG_HEAVY_MIN_DEG (default 1024; 0 disables)
+void set_heavy_min_degree(uint64_t v);
 
 // dense_matrix.hpp:78-95 (fp32, ascending k, mul/add separately rounded, +0).
 void gemm_a_bt(const float* a, uint64_t lda, const float* b, uint64_t ldb, float* out,

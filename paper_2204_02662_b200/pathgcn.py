@@ -534,6 +534,12 @@ def gather_rows(src, ids, out, stream=None):
     return out
 
 
+def set_heavy_min_degree(min_degree):
+    """Scheduling knob: destinations with >= min_degree edges run on the TMA
+    ring kernel (0 disables). Never changes results."""
+    _check(_lib_().pg_set_heavy_min_degree(int(min_degree)))
+
+
 def padded_ld(cols):
     """Device row pitch for gradient matrices: 16-B rows for narrow widths,
     whole 128-B lines (32 floats) beyond 32 columns, so every row gather is

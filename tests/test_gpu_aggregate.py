@@ -98,6 +98,38 @@ def test_backward_aggregation_bit_exact(pg, orc, dim):
         tol_check(got, orc, op, y_used)
 
 
+@pytest.mark.parametrize("heavy_min", [1, 0, 64])
+@pytest.mark.parametrize("dim", [1, 16, 41, 130, 602])
+def test_heavy_ring_kernel_bit_exact(pg, orc, dim, heavy_min):
+    """Force every (heavy_min=1), none (0) or some (64) destinations onto the
+    TMA bulk-copy ring kernel; results must not change by a bit, including
+    accumulate semantics."""
+    torch = torch_mod()
+    pairs, n_pad = rmat_pairs(orc, 4096, 4096 * 8, 13)
+    vt = orc.sample_training_set(4096, 0.3, 4)
+    og, dg, F, ops, dps = build_all(pg, orc, pairs, n_pad, vt, 2)
+    rng = np.random.default_rng(dim + heavy_min)
+    try:
+        pg.set_heavy_min_degree(heavy_min)
+        for dp, op in zip(dps, ops):
+            y = rng.uniform(-1, 1, size=(dp.P, dim)).astype(np.float32)
+            base = rng.uniform(-1, 1, size=(dp.D, dim)).astype(np.float32)
+            want = orc.aggregate_pull_f32(op.offsets, op.neighbors, op.weights, y[op.srcpos], out=base)
+            x = to_dev(base, pg.padded_ld(dim))
+            pg.backward_aggregation(pg.group_neighbors(dp, 7), to_dev(y, pg.padded_ld(dim)), x)
+            torch.cuda.synchronize()
+            got = x.cpu().numpy()
+            assert np.array_equal(bits(got), bits(want)), (dim, heavy_min)
+            b = dp.shard_bounds(3)
+            x2 = to_dev(base[b[1]:b[2]], pg.padded_ld(dim))
+            pg.backward_aggregation(pg.group_neighbors(dp, 7), to_dev(y, pg.padded_ld(dim)), x2,
+                                    rows=(b[1], b[2]))
+            torch.cuda.synchronize()
+            assert np.array_equal(bits(x2.cpu().numpy()), bits(want[b[1]:b[2]]))
+    finally:
+        pg.set_heavy_min_degree(1024)
+
+
 def test_aggregate_pull_local_and_accumulate(pg, orc):
     torch = torch_mod()
     pairs, n_pad = rmat_pairs(orc, 2048, 2048 * 6, 3)
