@@ -249,6 +249,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="few steps, no extras (for ncu)")
+    ap.add_argument("--heavy-sweep", action="store_true", help="diagnostics: heavy-kernel threshold sweep")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -329,6 +330,8 @@ def main():
             if ev is not None:
                 ev[i][2].record(stream)
 
+    if args.heavy_sweep:
+        sweep(pg, torch, step, paths, dims, stream)
     for _ in range(max(args.warmup, 1)):
         step()
     torch.cuda.synchronize()
@@ -411,6 +414,35 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def sweep(pg, torch, step, paths, dims, stream):
+    """Diagnostics (stderr): per-path kernel ms vs the heavy-kernel degree
+    threshold, and raw pinned H2D/D2H copy bandwidth."""
+    L = len(paths)
+    for hmin in (1024, 0, 1, 64, 256, 4096, 16384, 1024):
+        pg.set_heavy_min_degree(hmin)
+        for _ in range(3):
+            step()
+        evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(L)] for _ in range(10)]
+        for k in range(10):
+            step(evs[k])
+        torch.cuda.synchronize()
+        ms = [statistics.mean(evs[k][i][1].elapsed_time(evs[k][i][2]) for k in range(10)) for i in range(L)]
+        log(f"[sweep] heavy_min_deg={hmin:6d} per-path ms={[round(x, 3) for x in ms]} total={sum(ms):.3f}")
+    nbytes = paths[-1].P * dims[-1] * 4
+    h = torch.empty(nbytes // 4, dtype=torch.float32, pin_memory=True)
+    d = torch.empty(nbytes // 4, dtype=torch.float32, device="cuda")
+    for name, fn in (("h2d", lambda: d.copy_(h, non_blocking=True)), ("d2h", lambda: h.copy_(d, non_blocking=True))):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(5):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        log(f"[sweep] pinned {name} {nbytes / 1e6:.0f} MB: {nbytes * 5 / (a.elapsed_time(b) / 1e3) / 1e9:.1f} GB/s")
 
 
 def measure_e2e(pg, pgd, torch, dist, paths, groups, shards, dims, rows, world, rank, dev, steps, ep_bytes):

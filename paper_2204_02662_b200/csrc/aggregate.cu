@@ -291,6 +291,146 @@ void launch_heavy(const uint64_t* offsets, const Edge* edges, const uint32_t* or
     PG_LAUNCH("k_agg_heavy");
 }
 
+// ---- heavy destinations: cooperative LDG-staged double buffer -----------------
+// One 256-thread CTA per (heavy destination, column chunk). All 8 warps
+// gather the next tile of T edges' row chunks (128-bit LDG into registers,
+// then shared memory) while warp 0's column lanes fold the current tile in
+// ascending edge order. 32 KB per tile, ~64 KB in flight per CTA.
+constexpr int kCoopTileBytes = 32768;
+
+template <int CHQ>
+__host__ __device__ constexpr int coop_T() {
+    return kCoopTileBytes / (CHQ * 16);
+}
+
+template <int CHQ>
+__global__ void __launch_bounds__(256) k_agg_heavy_coop(const uint64_t* __restrict__ offsets,
+                                                       const Edge* __restrict__ edges,
+                                                       const uint32_t* __restrict__ order, uint32_t d_begin,
+                                                       uint32_t chunks, uint32_t nq_total,
+                                                       const float* __restrict__ in, uint64_t ld_in,
+                                                       float* __restrict__ out, uint64_t ld_out, uint32_t dim,
+                                                       int accumulate) {
+    constexpr int T = coop_T<CHQ>();
+    constexpr int PER = T * CHQ / 256;  // float4 gathers per thread per tile
+    extern __shared__ __align__(128) unsigned char smem[];
+    float4* tile = reinterpret_cast<float4*>(smem);                          // [2][T*CHQ]
+    float* wt = reinterpret_cast<float*>(smem + 2 * kCoopTileBytes);         // [2][T]
+
+    const uint32_t item = blockIdx.x;
+    const uint32_t d = order[d_begin + item / chunks];
+    const uint32_t c = item % chunks;
+    const uint32_t q0 = c * CHQ;
+    const uint32_t nqc = min(static_cast<uint32_t>(CHQ), nq_total - q0);
+    const uint64_t eb = offsets[d], ee = offsets[d + 1];
+    const uint64_t ntiles = (ee - eb + T - 1) / T;
+    const unsigned tid = threadIdx.x, lane = tid & 31;
+
+    float4 r[PER];
+    float rw[PER];
+    auto gather = [&](uint64_t t) {
+        const uint64_t e0 = eb + t * T;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const unsigned idx = tid + 256u * k;
+            const unsigned j = idx / CHQ, q = idx % CHQ;
+            const bool ok = e0 + j < ee && q < nqc;
+            Edge ed = make_uint2(0u, 0u);
+            if (ok) ed = __ldg(edges + e0 + j);
+            r[k] = ok ? ldg4(in + ed.x * ld_in + (q0 + q) * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+            rw[k] = __uint_as_float(ed.y);
+        }
+    };
+    auto stash = [&](int b) {
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const unsigned idx = tid + 256u * k;
+            tile[b * T * CHQ + idx] = r[k];
+            if (idx % CHQ == 0) wt[b * T + idx / CHQ] = rw[k];
+        }
+    };
+
+    const bool owner = tid < 32 && lane < nqc;
+    const uint32_t col = (q0 + lane) * 4;
+    float* orow = out + d * ld_out + col;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (owner && accumulate && col < dim) {
+        if (col + 3 < dim) acc = *reinterpret_cast<const float4*>(orow);
+        else {
+            acc.x = orow[0];
+            if (col + 1 < dim) acc.y = orow[1];
+            if (col + 2 < dim) acc.z = orow[2];
+        }
+    }
+    if (ntiles) {
+        gather(0);
+        stash(0);
+    }
+    __syncthreads();
+    for (uint64_t t = 0; t < ntiles; ++t) {
+        const int b = static_cast<int>(t & 1);
+        if (t + 1 < ntiles) gather(t + 1);  // loads in flight during the fold
+        if (owner) {
+            const uint32_t n = static_cast<uint32_t>(min(static_cast<uint64_t>(T), ee - (eb + t * T)));
+            const float4* sb = tile + b * T * CHQ + lane;
+            const float* sw = wt + b * T;
+            for (uint32_t j = 0; j < n; ++j) acc4(acc, sw[j], sb[j * CHQ]);
+        }
+        if (t + 1 < ntiles) stash(b ^ 1);
+        __syncthreads();
+    }
+    if (!owner || col >= dim) return;
+    acc.x = __fadd_rn(acc.x, 0.f);
+    acc.y = __fadd_rn(acc.y, 0.f);
+    acc.z = __fadd_rn(acc.z, 0.f);
+    acc.w = __fadd_rn(acc.w, 0.f);
+    if (col + 3 < dim) {
+        __stcs(reinterpret_cast<float4*>(orow), acc);
+    } else {
+        orow[0] = acc.x;
+        if (col + 1 < dim) orow[1] = acc.y;
+        if (col + 2 < dim) orow[2] = acc.z;
+    }
+}
+
+template <int CHQ>
+void launch_heavy_coop(const uint64_t* offsets, const Edge* edges, const uint32_t* order, uint32_t d_begin,
+                       uint32_t nh, uint32_t nq, const float* in, uint64_t ld_in, float* out, uint64_t ld_out,
+                       uint32_t dim, bool accumulate, cudaStream_t s) {
+    static thread_local std::vector<char> attr_set;
+    constexpr size_t smem = 2 * kCoopTileBytes + 2 * coop_T<CHQ>() * 4;
+    int dev = 0;
+    PG_CUDA(cudaGetDevice(&dev));
+    if (static_cast<int>(attr_set.size()) <= dev) attr_set.resize(dev + 1, 0);
+    if (!attr_set[dev]) {
+        PG_CUDA(cudaFuncSetAttribute(k_agg_heavy_coop<CHQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+        attr_set[dev] = 1;
+    }
+    const uint32_t chunks = (nq + CHQ - 1) / CHQ;
+    k_agg_heavy_coop<CHQ><<<nh * chunks, 256, smem, s>>>(offsets, edges, order, d_begin, chunks, nq, in, ld_in, out,
+                                                         ld_out, dim, accumulate);
+    PG_LAUNCH("k_agg_heavy_coop");
+}
+
+bool heavy_use_tma() {
+    static const bool v = [] {
+        const char* e = std::getenv("PG_HEAVY_KERNEL");
+        return e && std::string(e) == "tma";
+    }();
+    return v;
+}
+
+template <int CHQ>
+void launch_heavy_any(const uint64_t* offsets, const Edge* edges, const uint32_t* order, uint32_t d_begin,
+                      uint32_t nh, uint32_t nq, const float* in, uint64_t ld_in, float* out, uint64_t ld_out,
+                      uint32_t dim, bool accumulate, cudaStream_t s) {
+    if (heavy_use_tma())
+        launch_heavy<CHQ>(offsets, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim, accumulate, s);
+    else
+        launch_heavy_coop<CHQ>(offsets, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim, accumulate, s);
+}
+
 struct SideStream {
     cudaStream_t s = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
@@ -395,13 +535,17 @@ void aggregate_det(const uint64_t* offsets, const Edge* edges, const uint32_t* o
         PG_CUDA(cudaEventRecord(ss.fork, s));
         PG_CUDA(cudaStreamWaitEvent(ss.s, ss.fork, 0));
         if (nq > 16)
-            launch_heavy<32>(offsets, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim32, accumulate, ss.s);
+            launch_heavy_any<32>(offsets, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim32, accumulate,
+                                 ss.s);
         else if (nq > 8)
-            launch_heavy<16>(offsets, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim32, accumulate, ss.s);
+            launch_heavy_any<16>(offsets, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim32, accumulate,
+                                 ss.s);
         else if (nq > 4)
-            launch_heavy<8>(offsets, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim32, accumulate, ss.s);
+            launch_heavy_any<8>(offsets, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim32, accumulate,
+                                ss.s);
         else
-            launch_heavy<4>(offsets, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim32, accumulate, ss.s);
+            launch_heavy_any<4>(offsets, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim32, accumulate,
+                                ss.s);
         PG_CUDA(cudaEventRecord(ss.join, ss.s));
         d_begin += nh;
         nd -= nh;
