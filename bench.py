@@ -420,7 +420,7 @@ def sweep(pg, torch, step, paths, dims, stream):
     """Diagnostics (stderr): per-path kernel ms vs the heavy-kernel degree
     threshold, and raw pinned H2D/D2H copy bandwidth."""
     L = len(paths)
-    for hmin in (1024, 0, 1, 64, 256, 4096, 16384, 1024):
+    for hmin in (None, 0, 2048, 4096, 8192, 16384, 32768, None):
         pg.set_heavy_min_degree(hmin)
         for _ in range(3):
             step()
@@ -429,7 +429,7 @@ def sweep(pg, torch, step, paths, dims, stream):
             step(evs[k])
         torch.cuda.synchronize()
         ms = [statistics.mean(evs[k][i][1].elapsed_time(evs[k][i][2]) for k in range(10)) for i in range(L)]
-        log(f"[sweep] heavy_min_deg={hmin:6d} per-path ms={[round(x, 3) for x in ms]} total={sum(ms):.3f}")
+        log(f"[sweep] heavy_min_deg={str(hmin):>7s} per-path ms={[round(x, 3) for x in ms]} total={sum(ms):.3f}")
     nbytes = paths[-1].P * dims[-1] * 4
     h = torch.empty(nbytes // 4, dtype=torch.float32, pin_memory=True)
     d = torch.empty(nbytes // 4, dtype=torch.float32, device="cuda")

@@ -58,8 +58,10 @@ int pg_last_error(char* buf, size_t cap);
 int pg_version(void);
 int pg_device_count(int* count);
 /* Scheduling knob (never changes results): destinations with at least this
- * many path edges run on the TMA-ring heavy kernel (default 1024 or
- * $PG_HEAVY_MIN_DEG; 0 disables). */
+ * many path edges run on the heavy-destination kernel (cooperative staged,
+ * or the TMA bulk ring with PG_HEAVY_KERNEL=tma). 0 disables; UINT64_MAX
+ * (default, or $PG_HEAVY_MIN_DEG) = width dependent: 4096 for rows of <= 32
+ * floats, off for wider rows. */
 int pg_set_heavy_min_degree(uint64_t min_degree);
 
 /* ---------------- graph load ---------------- */

@@ -506,6 +506,14 @@ __global__ void k_relu_backward(const float* __restrict__ g, uint64_t ldg, const
     out[r * ldo + c] = pre[r * ldp + c] > 0.f ? g[r * ldg + c] : 0.f;
 }
 
+__global__ void k_copy_rows(const float* __restrict__ src, uint64_t lds, float* __restrict__ dst, uint64_t ldd,
+                            uint64_t rows, uint64_t cols) {
+    const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (i >= rows * cols) return;
+    const uint64_t r = i / cols, c = i % cols;
+    dst[r * ldd + c] = src[r * lds + c];
+}
+
 __global__ void k_gather_rows(const float* __restrict__ src, uint64_t lds, const uint32_t* __restrict__ ids,
                               uint64_t k, float* __restrict__ out, uint64_t ldo, uint64_t cols) {
     const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
@@ -588,6 +596,13 @@ void relu_backward(const float* grad, uint64_t ldg, const float* pre, uint64_t l
     if (rows * cols == 0) return;
     k_relu_backward<<<grid_for(rows * cols, 256), 256, 0, s>>>(grad, ldg, pre, ldp, out, ldo, rows, cols);
     PG_LAUNCH("k_relu_backward");
+}
+
+void copy_rows(const float* src, uint64_t lds, float* dst, uint64_t ldd, uint64_t rows, uint64_t cols,
+               cudaStream_t s) {
+    if (rows * cols == 0) return;
+    k_copy_rows<<<grid_for(rows * cols, 256), 256, 0, s>>>(src, lds, dst, ldd, rows, cols);
+    PG_LAUNCH("k_copy_rows");
 }
 
 void gather_rows(const float* src, uint64_t lds, const uint32_t* ids, uint64_t k, float* out, uint64_t ldo,

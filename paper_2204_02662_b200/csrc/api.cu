@@ -140,20 +140,25 @@ void run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re, con
             PG_CUDA(cudaStreamSynchronize(lib_stream(p.device)));
             edges = p.edges_local.get();
         }
-        const uint64_t hmin = heavy_min_degree();
+        const uint64_t hmin = heavy_min_degree(dim);
         if (rb == 0 && re == p.D) {
             aggregate_det(p.offsets.get(), edges, p.order.get(), p.D, 0, p.D, p.hist.heavy(hmin), in, ld_in, out,
                           ld_out, dim, accumulate, s);
             return;
         }
-        // shard: schedule of rows [rb, re) relative to rb
-        if (!(G.shard_order.get() && G.shard_rb == rb && G.shard_re == re)) {
-            degree_order(p.offsets.get() + rb, re - rb, G.shard_order, lib_stream(p.device), &G.shard_hist);
-            G.shard_rb = rb;
-            G.shard_re = re;
+        // row range: schedule of rows [rb, re) relative to rb (cached)
+        Groups::RowSched* rs = nullptr;
+        for (auto& x : G.row_scheds)
+            if (x.rb == rb && x.re == re) rs = &x;
+        if (!rs) {
+            G.row_scheds.emplace_back();
+            rs = &G.row_scheds.back();
+            rs->rb = rb;
+            rs->re = re;
+            degree_order(p.offsets.get() + rb, re - rb, rs->order, lib_stream(p.device), &rs->hist);
         }
-        aggregate_det(p.offsets.get() + rb, edges, G.shard_order.get(), re - rb, 0, re - rb,
-                      G.shard_hist.heavy(hmin), in, ld_in, out, ld_out, dim, accumulate, s);
+        aggregate_det(p.offsets.get() + rb, edges, rs->order.get(), re - rb, 0, re - rb, rs->hist.heavy(hmin), in,
+                      ld_in, out, ld_out, dim, accumulate, s);
         return;
     }
     Graph& g = *G.graph;
@@ -164,29 +169,88 @@ void run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re, con
     if (!G.graph_order.get() && g.n)
         degree_order(g.offsets.get(), g.n, G.graph_order, lib_stream(g.device), &G.graph_hist);
     aggregate_det(g.offsets.get(), g.edges.get(), G.graph_order.get(), g.n, 0, g.n,
-                  G.graph_hist.heavy(heavy_min_degree()), in, ld_in, out, ld_out, dim, accumulate, s);
+                  G.graph_hist.heavy(heavy_min_degree(dim)), in, ld_in, out, ld_out, dim, accumulate, s);
 }
 
-// Host buffers (ld = dim) -> padded device buffers -> run -> host.
+struct CopyStream {
+    cudaStream_t s = nullptr;
+    std::vector<cudaEvent_t> ev;
+};
+
+CopyStream& copy_stream(int device, size_t nev) {
+    static std::vector<CopyStream> per_dev;
+    if (static_cast<int>(per_dev.size()) <= device) per_dev.resize(device + 1);
+    CopyStream& c = per_dev[device];
+    if (!c.s) PG_CUDA(cudaStreamCreateWithFlags(&c.s, cudaStreamNonBlocking));
+    while (c.ev.size() < nev) {
+        cudaEvent_t e;
+        PG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c.ev.push_back(e);
+    }
+    return c;
+}
+
+// Host buffers (row-major, ld = dim): flat H2D at full link rate, on-device
+// repack to 16-byte rows when dim % 4 != 0, SpMM in edge-balanced row chunks
+// whose D2H overlaps the next chunk's compute, synchronise.
 void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_rows, uint64_t dim,
               float* out_host, unsigned flags) {
     const Base b = base_of(G);
+    if (parent_indexed && G.edges_remap.get())
+        fail(kConfig, "backward_aggregate_host: a multi-GPU source remap is installed on this grouping");
     DeviceGuard dg(G.device);
     cudaStream_t s = lib_stream(G.device);
-    const uint64_t ld = (dim + 3) & ~3ull;  // 16-byte rows for the vectorised kernel
-    DevBuf<float> din(in_rows * ld, s), dout(static_cast<uint64_t>(b.D) * ld, s);
-    if (in_rows && dim)
-        PG_CUDA(cudaMemcpy2DAsync(din.get(), ld * 4, in_host, dim * 4, dim * 4, in_rows, cudaMemcpyHostToDevice, s));
-    if (b.D && dim) {
-        if (flags & PG_AGG_OVERWRITE)
-            ;  // every element is written
-        else
-            PG_CUDA(cudaMemcpy2DAsync(dout.get(), ld * 4, out_host, dim * 4, dim * 4, b.D, cudaMemcpyHostToDevice, s));
+    const bool packed = dim % 4 == 0;  // host rows are already 16-byte rows
+    const uint64_t ld = (dim + 3) & ~3ull;
+    const uint64_t D = b.D;
+    DevBuf<float> fin(packed ? 0 : in_rows * dim, s), din(in_rows * ld, s);
+    DevBuf<float> fout(packed ? 0 : D * dim, s), dout(D * ld, s);
+    if (in_rows && dim) {
+        float* dst = packed ? din.get() : fin.get();
+        PG_CUDA(cudaMemcpyAsync(dst, in_host, in_rows * dim * 4, cudaMemcpyHostToDevice, s));
+        if (!packed) copy_rows(fin.get(), dim, din.get(), ld, in_rows, dim, s);
     }
-    run_aggregate(G, parent_indexed, 0, b.D, din.get(), ld, dout.get(), ld, dim, flags, s);
-    if (b.D && dim)
-        PG_CUDA(cudaMemcpy2DAsync(out_host, dim * 4, dout.get(), ld * 4, dim * 4, b.D, cudaMemcpyDeviceToHost, s));
+    if (D && dim && !(flags & PG_AGG_OVERWRITE)) {
+        float* dst = packed ? dout.get() : fout.get();
+        PG_CUDA(cudaMemcpyAsync(dst, out_host, D * dim * 4, cudaMemcpyHostToDevice, s));
+        if (!packed) copy_rows(fout.get(), dim, dout.get(), ld, D, dim, s);
+    }
+    // row chunks (path groupings with enough rows): overlap D2H with compute
+    std::vector<uint32_t> cuts{0, static_cast<uint32_t>(D)};
+    if (G.path && D >= 16384 && dim * 4 * D >= (32ull << 20)) {
+        if (G.host_chunks.empty()) {
+            constexpr uint32_t R = 4;
+            std::vector<uint64_t> off(D + 1);
+            PG_CUDA(cudaMemcpyAsync(off.data(), G.path->offsets.get(), off.size() * 8, cudaMemcpyDeviceToHost, s));
+            PG_CUDA(cudaStreamSynchronize(s));
+            G.host_chunks.push_back(0);
+            for (uint32_t r = 1; r < R; ++r) {
+                const uint64_t target = off[D] * r / R;
+                const uint32_t row = static_cast<uint32_t>(std::lower_bound(off.begin(), off.end() - 1, target) - off.begin());
+                G.host_chunks.push_back(std::max(G.host_chunks.back(), row));
+            }
+            G.host_chunks.push_back(static_cast<uint32_t>(D));
+        }
+        cuts = G.host_chunks;
+    }
+    CopyStream& cs = copy_stream(G.device, cuts.size());
+    for (size_t r = 0; r + 1 < cuts.size(); ++r) {
+        const uint32_t rb = cuts[r], re = cuts[r + 1];
+        if (rb == re) continue;
+        run_aggregate(G, parent_indexed, rb, re, din.get(), ld, dout.get() + rb * ld, ld, dim, flags, s);
+        PG_CUDA(cudaEventRecord(cs.ev[r], s));
+        PG_CUDA(cudaStreamWaitEvent(cs.s, cs.ev[r], 0));
+        if (!dim) continue;
+        const float* src = dout.get() + rb * ld;
+        if (!packed) {
+            copy_rows(dout.get() + rb * ld, ld, fout.get() + rb * dim, dim, re - rb, dim, cs.s);
+            src = fout.get() + rb * dim;
+        }
+        PG_CUDA(cudaMemcpyAsync(out_host + rb * dim, src, (re - rb) * dim * 4, cudaMemcpyDeviceToHost, cs.s));
+    }
+    PG_CUDA(cudaStreamSynchronize(cs.s));
     PG_CUDA(cudaStreamSynchronize(s));
+    // buffers are freed stream-ordered on s after the copies completed
 }
 
 }  // namespace

@@ -112,9 +112,15 @@ struct Groups {
     DevBuf<uint64_t> dest_groups;  // D+1
     DevBuf<uint32_t> graph_order;  // schedule for graph groupings (lazy)
     DegHist graph_hist;
-    DevBuf<uint32_t> shard_order;  // schedule of one destination-row shard (lazy)
-    DegHist shard_hist;
-    uint32_t shard_rb = 0, shard_re = 0;
+    // schedules of destination-row ranges (multi-GPU shards, host-call
+    // copy/compute chunks), built lazily and cached
+    struct RowSched {
+        uint32_t rb = 0, re = 0;
+        DevBuf<uint32_t> order;
+        DegHist hist;
+    };
+    std::vector<RowSched> row_scheds;
+    std::vector<uint32_t> host_chunks;  // edge-balanced cuts for pg_*_host overlap
     // multi-GPU: parent rows remapped into a padded allgather layout
     DevBuf<Edge> edges_remap;
     uint64_t remap_rows = 0;
@@ -154,7 +160,9 @@ void grouping_cost_dev(uint32_t D, const uint64_t* offsets_dev, uint32_t gs, uin
 void aggregate_det(const uint64_t* offsets, const Edge* edges, const uint32_t* order, uint32_t D,
                    uint32_t d_begin, uint32_t d_end, uint32_t n_heavy, const float* in, uint64_t ld_in,
                    float* out, uint64_t ld_out, uint64_t dim, bool accumulate, cudaStream_t s);
-uint64_t heavy_min_degree();  // PG_HEAVY_MIN_DEG (default 1024; 0 disables)
+// PG_HEAVY_MIN_DEG / pg_set_heavy_min_degree (0 disables; UINT64_MAX restores
+// the width-dependent default)
+uint64_t heavy_min_degree(uint64_t dim);
 void set_heavy_min_degree(uint64_t v);
 
 // dense_matrix.hpp:78-95 (fp32, ascending k, mul/add separately rounded, +0).
@@ -163,6 +171,9 @@ void gemm_a_bt(const float* a, uint64_t lda, const float* b, uint64_t ldb, float
 // dense_matrix.hpp:114-121
 void relu_backward(const float* grad, uint64_t ldg, const float* pre, uint64_t ldp, float* out,
                    uint64_t ldo, uint64_t rows, uint64_t cols, cudaStream_t s);
+// row-pitch change (host-layout <-> 16-byte device rows)
+void copy_rows(const float* src, uint64_t lds, float* dst, uint64_t ldd, uint64_t rows, uint64_t cols,
+               cudaStream_t s);
 // engine.hpp:162-169
 void gather_rows(const float* src, uint64_t lds, const uint32_t* ids, uint64_t k, float* out,
                  uint64_t ldo, uint64_t cols, cudaStream_t s);

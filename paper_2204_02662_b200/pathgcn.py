@@ -534,10 +534,11 @@ def gather_rows(src, ids, out, stream=None):
     return out
 
 
-def set_heavy_min_degree(min_degree):
-    """Scheduling knob: destinations with >= min_degree edges run on the TMA
-    ring kernel (0 disables). Never changes results."""
-    _check(_lib_().pg_set_heavy_min_degree(int(min_degree)))
+def set_heavy_min_degree(min_degree=None):
+    """Scheduling knob: destinations with >= min_degree edges run on the
+    heavy-destination kernel (0 disables, None restores the width-dependent
+    default). Never changes results."""
+    _check(_lib_().pg_set_heavy_min_degree(2**64 - 1 if min_degree is None else int(min_degree)))
 
 
 def padded_ld(cols):

@@ -127,7 +127,7 @@ def test_heavy_ring_kernel_bit_exact(pg, orc, dim, heavy_min):
             torch.cuda.synchronize()
             assert np.array_equal(bits(x2.cpu().numpy()), bits(want[b[1]:b[2]]))
     finally:
-        pg.set_heavy_min_degree(1024)
+        pg.set_heavy_min_degree(None)
 
 
 def test_aggregate_pull_local_and_accumulate(pg, orc):
@@ -280,8 +280,27 @@ def test_large_checksum(pg, orc):
     dim = 602
     y = np.random.default_rng(7).uniform(-1, 1, size=(dp.P, dim)).astype(np.float32)
     want = orc.aggregate_pull_f32(op.offsets, op.neighbors, op.weights, y[op.srcpos])
+    G = pg.group_neighbors(dp, pg.path_regression_gs(dp))
     x = pg.empty_rows(dp.D, dim)
-    pg.backward_aggregation(pg.group_neighbors(dp, pg.path_regression_gs(dp)), to_dev(y, pg.padded_ld(dim)), x,
-                            overwrite=True)
+    pg.backward_aggregation(G, to_dev(y, pg.padded_ld(dim)), x, overwrite=True)
     torch.cuda.synchronize()
     assert np.array_equal(bits(x.cpu().numpy()), bits(want))
+    # host drop-in: flat copies, on-device repack (602 % 4 != 0), chunked
+    # D2H overlap; pinned and pageable buffers, overwrite and accumulate
+    assert dp.D >= 16384 and dp.D * dim * 4 >= 32 << 20
+    for pinned in (True, False):
+        yh = torch.from_numpy(y).pin_memory().numpy() if pinned else y.copy()
+        xh = np.full((dp.D, dim), np.nan, np.float32)
+        pg.backward_aggregation(G, yh, xh, overwrite=True)
+        assert np.array_equal(bits(xh), bits(want))
+    base = np.random.default_rng(8).uniform(-1, 1, size=(dp.D, dim)).astype(np.float32)
+    want2 = orc.aggregate_pull_f32(op.offsets, op.neighbors, op.weights, y[op.srcpos], out=base)
+    xh = base.copy()
+    pg.backward_aggregation(G, y, xh)
+    assert np.array_equal(bits(xh), bits(want2))
+    # a width that is a multiple of 4 takes the no-repack branch
+    y4 = y[:, :600].copy()
+    want4 = orc.aggregate_pull_f32(op.offsets, op.neighbors, op.weights, y4[op.srcpos])
+    xh4 = np.zeros((dp.D, 600), np.float32)
+    pg.backward_aggregation(G, y4, xh4, overwrite=True)
+    assert np.array_equal(bits(xh4), bits(want4))
