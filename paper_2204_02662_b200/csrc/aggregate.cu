@@ -506,12 +506,12 @@ __global__ void k_relu_backward(const float* __restrict__ g, uint64_t ldg, const
     out[r * ldo + c] = pre[r * ldp + c] > 0.f ? g[r * ldg + c] : 0.f;
 }
 
+// blockIdx.y strides rows, x covers columns: no 64-bit div/mod per element
 __global__ void k_copy_rows(const float* __restrict__ src, uint64_t lds, float* __restrict__ dst, uint64_t ldd,
-                            uint64_t rows, uint64_t cols) {
-    const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-    if (i >= rows * cols) return;
-    const uint64_t r = i / cols, c = i % cols;
-    dst[r * ldd + c] = src[r * lds + c];
+                            uint64_t rows, uint32_t cols) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= cols) return;
+    for (uint64_t r = blockIdx.y; r < rows; r += gridDim.y) dst[r * ldd + c] = src[r * lds + c];
 }
 
 __global__ void k_gather_rows(const float* __restrict__ src, uint64_t lds, const uint32_t* __restrict__ ids,
@@ -601,7 +601,9 @@ void relu_backward(const float* grad, uint64_t ldg, const float* pre, uint64_t l
 void copy_rows(const float* src, uint64_t lds, float* dst, uint64_t ldd, uint64_t rows, uint64_t cols,
                cudaStream_t s) {
     if (rows * cols == 0) return;
-    k_copy_rows<<<grid_for(rows * cols, 256), 256, 0, s>>>(src, lds, dst, ldd, rows, cols);
+    const unsigned tx = cols >= 256 ? 256 : 128;
+    dim3 grid(static_cast<unsigned>((cols + tx - 1) / tx), static_cast<unsigned>(std::min<uint64_t>(rows, 16384)));
+    k_copy_rows<<<grid, tx, 0, s>>>(src, lds, dst, ldd, rows, static_cast<uint32_t>(cols));
     PG_LAUNCH("k_copy_rows");
 }
 

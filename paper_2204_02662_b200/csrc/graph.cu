@@ -195,6 +195,13 @@ cudaStream_t lib_stream(int device) {
     if (!g_streams[device]) {
         DeviceGuard dg(device);
         PG_CUDA(cudaStreamCreateWithFlags(&g_streams[device], cudaStreamNonBlocking));
+        // keep freed stream-ordered allocations in the pool instead of
+        // returning them to the driver at every synchronisation (the
+        // host-buffer calls stage ~GBs per call)
+        cudaMemPool_t pool;
+        PG_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t keep = UINT64_MAX;
+        PG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     }
     return g_streams[device];
 }
