@@ -1,0 +1,410 @@
+// pathgcn_b200.hpp — header-only C++20 host side over the C ABI
+// (pathgcn_b200.h), re-exposing the reference's operator API for the
+// backward-aggregation path (namespace pathgcn, proj/core/include/pathgcn):
+//
+//   reference                                   here (namespace pathgcn::b200)
+//   build_undirected_csr + assign_edge_weights  build_undirected_csr(EdgeList, WeightMode)
+//     (csr_graph.hpp:48-51)                     DeviceGraph::from_csr(CsrView-like arrays)
+//   compute_frontiers (frontier.hpp:20)         compute_frontiers(g, vt, L) -> DeviceFrontiers
+//   extract_execution_path (execution_path.hpp:37-38), prepare_all_paths (:41)
+//   path_fingerprint (:35)                      path_fingerprint(g, vt, L)
+//   group_neighbors (grouping.hpp:30)           group_neighbors(path, gs) -> DeviceGroups
+//   regression_gs (gs_model.hpp:24)             regression_gs(stats) / regression_gs(path)
+//   oracle_gs + cost_model_evaluator            oracle_gs_cost(path, dim, {workers, lambda})
+//     (group_cost.hpp:19-43)
+//   aggregate_pull<float> (aggregate.hpp:56-59) aggregate_pull(groups, in, out, mode, counters)
+//   engine.hpp:331-338 stage                    backward_aggregation(groups, y_grad, x_grad)
+//
+// Errors are thrown as exceptions mirroring error.hpp:10-47 (ConfigError,
+// ShapeError, StalenessError, IoError, NumericError) plus DeviceError for
+// CUDA failures; calls are synchronous for host buffers, like the
+// reference. All compute runs on the GPU (libpathgcn_b200.so, sm_100a).
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <optional>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "pathgcn_b200.h"
+
+namespace pathgcn::b200 {
+
+using VertexId = std::uint32_t;
+using EdgeIndex = std::uint64_t;
+
+struct Error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct ConfigError : Error {
+    using Error::Error;
+};
+struct ShapeError : ConfigError {
+    using ConfigError::ConfigError;
+};
+struct StalenessError : ConfigError {
+    using ConfigError::ConfigError;
+};
+struct IoError : Error {
+    using Error::Error;
+};
+struct NumericError : Error {
+    using Error::Error;
+};
+struct DeviceError : Error {
+    using Error::Error;
+};
+
+inline void check(int rc) {
+    if (rc == PG_OK) return;
+    std::string msg(512, '\0');
+    pg_last_error(msg.data(), msg.size());
+    msg.resize(msg.find('\0'));
+    switch (rc) {
+        case PG_ERR_CONFIG:
+            if (msg.find("rows") != std::string::npos || msg.find("dimension") != std::string::npos)
+                throw ShapeError(msg);
+            throw ConfigError(msg);
+        case PG_ERR_IO: throw IoError(msg);
+        case PG_ERR_NUMERIC: throw NumericError(msg);
+        case PG_ERR_DEVICE: throw DeviceError(msg);
+        default: throw Error(msg);
+    }
+}
+
+enum class WeightMode { Unit, SymNorm };          // csr_graph.hpp:13
+enum class CommitMode { Deterministic, Fast };    // aggregate.hpp:21
+
+struct EdgeList {                                 // edge_list.hpp:14-18
+    std::vector<std::pair<VertexId, VertexId>> pairs;
+    std::optional<VertexId> n_hint;
+};
+
+struct StageCounters {                            // aggregate.hpp:23-39 (work part)
+    std::uint64_t edges_traversed = 0;
+    std::uint64_t groups_executed = 0;
+    std::uint64_t atomic_commits = 0;
+};
+
+struct GraphStats {                               // csr_graph.hpp:40-44
+    VertexId n_vertices = 0;
+    EdgeIndex n_undirected_edges = 0;
+    double avg_degree = 0.0;
+};
+
+template <typename T>
+struct DenseMatrix {                              // dense_matrix.hpp:14-30 (row-major, ld = cols)
+    std::size_t rows = 0, cols = 0;
+    std::vector<T> data;
+    DenseMatrix() = default;
+    DenseMatrix(std::size_t r, std::size_t c) : rows(r), cols(c), data(r * c, T(0)) {}
+};
+using MatrixF = DenseMatrix<float>;
+
+// Host copy of an ExecutionPath (execution_path.hpp:16-33 field names).
+struct ExecutionPathHost {
+    std::size_t layer = 0;
+    std::vector<VertexId> dest_local_to_global, src_local_to_global, src_pos_in_parent;
+    std::vector<EdgeIndex> offsets;
+    std::vector<VertexId> neighbors;
+    std::vector<double> weights;
+    std::uint64_t fingerprint = 0;
+};
+
+template <typename H, int (*Destroy)(H)>
+struct Handle {
+    H h = nullptr;
+    Handle() = default;
+    explicit Handle(H x) : h(x) {}
+    Handle(const Handle&) = delete;
+    Handle& operator=(const Handle&) = delete;
+    Handle(Handle&& o) noexcept : h(std::exchange(o.h, nullptr)) {}
+    Handle& operator=(Handle&& o) noexcept {
+        if (this != &o) {
+            reset();
+            h = std::exchange(o.h, nullptr);
+        }
+        return *this;
+    }
+    ~Handle() { reset(); }
+    void reset() {
+        if (h) Destroy(h);
+        h = nullptr;
+    }
+};
+
+class DeviceGraph {                               // CsrGraph (csr_graph.hpp:19-38)
+public:
+    static DeviceGraph from_csr(VertexId n, std::span<const EdgeIndex> offsets, std::span<const VertexId> neighbors,
+                                std::span<const double> weights, int device = 0, bool validate = true) {
+        pg_graph g = nullptr;
+        check(pg_graph_create(device, n, offsets.data(), neighbors.data(), weights.data(), validate, &g));
+        return DeviceGraph(g);
+    }
+    VertexId n() const { return info().n; }
+    EdgeIndex m() const { return info().m; }
+    VertexId max_degree() const { return info().maxdeg; }
+    std::uint64_t fingerprint() const {
+        std::uint64_t fp = 0;
+        check(pg_graph_info(h_.h, nullptr, nullptr, nullptr, &fp));
+        return fp;
+    }
+    void assign_edge_weights(WeightMode mode) {
+        check(pg_graph_assign_weights(h_.h, mode == WeightMode::SymNorm ? PG_WEIGHTS_SYMNORM : PG_WEIGHTS_UNIT));
+    }
+    void to_host(std::vector<EdgeIndex>& offsets, std::vector<VertexId>& neighbors, std::vector<double>& weights) const {
+        const auto i = info();
+        offsets.resize(i.n + 1);
+        neighbors.resize(i.m);
+        weights.resize(i.m);
+        check(pg_graph_export(h_.h, offsets.data(), neighbors.data(), weights.data()));
+    }
+    pg_graph raw() const { return h_.h; }
+    explicit DeviceGraph(pg_graph g) : h_(g) {}
+
+private:
+    struct Info {
+        VertexId n;
+        EdgeIndex m;
+        VertexId maxdeg;
+    };
+    Info info() const {
+        Info i{};
+        check(pg_graph_info(h_.h, &i.n, &i.m, &i.maxdeg, nullptr));
+        return i;
+    }
+    Handle<pg_graph, pg_graph_destroy> h_;
+};
+
+// csr_graph.cpp:33-77 on the device
+inline DeviceGraph build_undirected_csr(const EdgeList& el, WeightMode mode = WeightMode::Unit, int device = 0) {
+    std::vector<VertexId> flat(el.pairs.size() * 2);
+    for (std::size_t i = 0; i < el.pairs.size(); ++i) {
+        flat[2 * i] = el.pairs[i].first;
+        flat[2 * i + 1] = el.pairs[i].second;
+    }
+    pg_graph g = nullptr;
+    check(pg_graph_build(device, el.n_hint ? static_cast<std::int64_t>(*el.n_hint) : -1, flat.data(),
+                         el.pairs.size(), mode == WeightMode::SymNorm ? PG_WEIGHTS_SYMNORM : PG_WEIGHTS_UNIT, &g));
+    return DeviceGraph(g);
+}
+
+class DeviceFrontiers {                           // FrontierSets (frontier.hpp:14-18)
+public:
+    explicit DeviceFrontiers(pg_frontiers f, std::size_t L) : h_(f), L_(L) {}
+    std::size_t depth() const { return L_; }
+    std::vector<VertexId> level(std::size_t k) const {
+        std::uint64_t sz = 0;
+        check(pg_frontiers_size(h_.h, k, &sz));
+        std::vector<VertexId> out(sz);
+        check(pg_frontiers_export(h_.h, k, out.data()));
+        return out;
+    }
+    std::vector<std::vector<VertexId>> levels() const {
+        std::vector<std::vector<VertexId>> out;
+        for (std::size_t k = 0; k <= L_; ++k) out.push_back(level(k));
+        return out;
+    }
+    pg_frontiers raw() const { return h_.h; }
+
+private:
+    Handle<pg_frontiers, pg_frontiers_destroy> h_;
+    std::size_t L_;
+};
+
+inline DeviceFrontiers compute_frontiers(const DeviceGraph& g, std::span<const VertexId> vt, std::size_t layers) {
+    pg_frontiers f = nullptr;
+    check(pg_frontiers_compute(g.raw(), vt.data(), vt.size(), layers, &f));
+    return DeviceFrontiers(f, layers);
+}
+
+class DevicePath {                                // ExecutionPath (execution_path.hpp:16-33)
+public:
+    explicit DevicePath(pg_path p) : h_(p) {
+        check(pg_path_info(p, &layer_, &D_, &S_, &E_, &P_, &maxdeg_));
+    }
+    std::size_t layer() const { return layer_; }
+    VertexId dest_count() const { return D_; }
+    VertexId src_count() const { return S_; }
+    EdgeIndex edge_count() const { return E_; }
+    VertexId parent_rows() const { return P_; }
+    VertexId max_degree() const { return maxdeg_; }
+    std::uint64_t fingerprint() const {
+        std::uint64_t fp = 0;
+        check(pg_path_get_fingerprint(h_.h, &fp));
+        return fp;
+    }
+    void set_fingerprint(std::uint64_t fp) { check(pg_path_set_fingerprint(h_.h, fp)); }
+    ExecutionPathHost to_host() const {
+        ExecutionPathHost p;
+        p.layer = layer_;
+        p.dest_local_to_global.resize(D_);
+        p.src_local_to_global.resize(S_);
+        p.src_pos_in_parent.resize(S_);
+        p.offsets.resize(D_ + 1);
+        p.neighbors.resize(E_);
+        p.weights.resize(E_);
+        check(pg_path_export(h_.h, p.dest_local_to_global.data(), p.src_local_to_global.data(),
+                             p.src_pos_in_parent.data(), p.offsets.data(), p.neighbors.data(), p.weights.data()));
+        p.fingerprint = fingerprint();
+        return p;
+    }
+    pg_path raw() const { return h_.h; }
+
+private:
+    Handle<pg_path, pg_path_destroy> h_;
+    std::uint64_t layer_ = 0;
+    VertexId D_ = 0, S_ = 0, P_ = 0, maxdeg_ = 0;
+    EdgeIndex E_ = 0;
+};
+
+inline DevicePath extract_execution_path(const DeviceGraph& g, const DeviceFrontiers& f, std::size_t layer) {
+    pg_path p = nullptr;
+    check(pg_path_extract(g.raw(), f.raw(), layer, &p));
+    return DevicePath(p);
+}
+
+// execution_path.cpp:90-96: SG_{L-1} first
+inline std::vector<DevicePath> prepare_all_paths(const DeviceGraph& g, const DeviceFrontiers& f) {
+    std::vector<DevicePath> out;
+    for (std::size_t l = f.depth(); l-- > 0;) out.push_back(extract_execution_path(g, f, l));
+    return out;
+}
+
+inline std::uint64_t path_fingerprint(const DeviceGraph& g, std::span<const VertexId> vt, std::size_t layers) {
+    std::uint64_t fp = 0;
+    check(pg_path_fingerprint(g.raw(), vt.data(), vt.size(), layers, &fp));
+    return fp;
+}
+
+struct GsModel {                                  // gs_model.hpp:12-17 / default_gs_model
+    double beta0 = 0.65538, beta1 = 1.67431e-5, beta2 = -2.24342e-6, beta3 = 0.63641;
+};
+
+inline VertexId regression_gs(const GraphStats& s, const GsModel& m = {}) {
+    const double b[4] = {m.beta0, m.beta1, m.beta2, m.beta3};
+    VertexId gs = 0;
+    check(pg_gs_regression_stats(s.n_vertices, s.n_undirected_edges, s.avg_degree, b, &gs));
+    return gs;
+}
+
+// regression_gs(path_stats(path)) (train.hpp:16-24)
+inline VertexId regression_gs(const DevicePath& p, const GsModel& m = {}) {
+    const double b[4] = {m.beta0, m.beta1, m.beta2, m.beta3};
+    VertexId gs = 0;
+    check(pg_gs_regression(p.raw(), b, &gs));
+    return gs;
+}
+
+inline std::vector<VertexId> default_gs_candidates(VertexId max_degree) {
+    std::vector<VertexId> out(40);
+    std::uint64_t k = 0;
+    check(pg_gs_default_candidates(max_degree, out.data(), &k));
+    out.resize(k);
+    return out;
+}
+
+struct GroupCostModel {                           // group_cost.hpp:14-17
+    int worker_count = 1;
+    double atomic_penalty = 0.25;
+};
+struct GsSweepEntry {
+    VertexId gs;
+    double cost;
+};
+struct GsSweepResult {                            // group_cost.hpp:26-29
+    VertexId best_gs = 1;
+    std::vector<GsSweepEntry> table;
+};
+
+// oracle_gs(csr, candidates, cost_model_evaluator(dim, model)) on device
+inline GsSweepResult oracle_gs_cost(const DevicePath& p, std::size_t dim, const GroupCostModel& model,
+                                    std::vector<VertexId> candidates = {}) {
+    if (candidates.empty()) candidates = default_gs_candidates(p.max_degree());
+    std::vector<double> table(candidates.size());
+    GsSweepResult r;
+    std::uint64_t n = 0;
+    check(pg_gs_oracle_cost(p.raw(), dim, model.worker_count, model.atomic_penalty, candidates.data(),
+                            candidates.size(), &r.best_gs, table.data(), &n));
+    for (std::size_t i = 0; i < n; ++i) r.table.push_back({candidates[i], table[i]});
+    return r;
+}
+
+class DeviceGroups {                              // GroupedCsr (grouping.hpp:14-28)
+public:
+    explicit DeviceGroups(pg_groups g) : h_(g) { check(pg_groups_info(g, &gs_, &count_, &dests_)); }
+    VertexId gs() const { return gs_; }
+    std::size_t group_count() const { return count_; }
+    VertexId dest_count() const { return dests_; }
+    void to_host(std::vector<VertexId>& dest, std::vector<EdgeIndex>& begin, std::vector<EdgeIndex>& end,
+                 std::vector<std::uint64_t>& dest_groups) const {
+        dest.resize(count_);
+        begin.resize(count_);
+        end.resize(count_);
+        dest_groups.resize(dests_ + 1);
+        check(pg_groups_export(h_.h, dest.data(), begin.data(), end.data(), dest_groups.data()));
+    }
+    double grouping_cost(std::size_t dim, const GroupCostModel& m) const {
+        double c = 0;
+        check(pg_grouping_cost(h_.h, dim, m.worker_count, m.atomic_penalty, &c));
+        return c;
+    }
+    pg_groups raw() const { return h_.h; }
+
+private:
+    Handle<pg_groups, pg_groups_destroy> h_;
+    VertexId gs_ = 0, dests_ = 0;
+    std::uint64_t count_ = 0;
+};
+
+inline DeviceGroups group_neighbors(const DevicePath& p, VertexId gs) {
+    pg_groups g = nullptr;
+    check(pg_group(p.raw(), gs, &g));
+    return DeviceGroups(g);
+}
+inline DeviceGroups group_neighbors(const DeviceGraph& graph, VertexId gs) {
+    pg_groups g = nullptr;
+    check(pg_group_graph(graph.raw(), gs, &g));
+    return DeviceGroups(g);
+}
+
+// aggregate.hpp:56-122 aggregate_pull<float>: output accumulates, like the
+// reference (pass a zeroed output). `workers` is accepted for signature
+// compatibility; the device schedule is worker independent.
+inline void aggregate_pull(const DeviceGroups& grouped, const MatrixF& input, MatrixF& output,
+                           CommitMode mode = CommitMode::Deterministic, int workers = 0,
+                           StageCounters* counters = nullptr) {
+    (void)workers;
+    if (output.rows != grouped.dest_count()) throw ShapeError("aggregate_pull: output rows != dest count");
+    if (output.cols != input.cols) throw ShapeError("aggregate_pull: input/output dims differ");
+    std::uint64_t c[3] = {0, 0, 0};
+    check(pg_aggregate_pull_host(grouped.raw(), input.data.data(), input.rows, input.cols, output.data.data(),
+                                 mode == CommitMode::Fast ? PG_AGG_FAST : 0u, c));
+    if (counters) {
+        counters->edges_traversed += c[0];
+        counters->groups_executed += c[1];
+        counters->atomic_commits += c[2];
+    }
+}
+
+// engine.hpp:331-338: x_grad = aggregate_pull(groups, gather_rows(y_grad,
+// src_pos_in_parent)); y_grad rows follow the parent frontier.
+inline void backward_aggregation(const DeviceGroups& grouped, const MatrixF& y_grad, MatrixF& x_grad,
+                                 CommitMode mode = CommitMode::Deterministic, StageCounters* counters = nullptr) {
+    if (x_grad.rows != grouped.dest_count() || x_grad.cols != y_grad.cols)
+        throw ShapeError("backward_aggregation: x_grad shape mismatch");
+    std::uint64_t c[3] = {0, 0, 0};
+    check(pg_backward_aggregate_host(grouped.raw(), y_grad.data.data(), y_grad.rows, y_grad.cols,
+                                     x_grad.data.data(), mode == CommitMode::Fast ? PG_AGG_FAST : 0u, c));
+    if (counters) {
+        counters->edges_traversed += c[0];
+        counters->groups_executed += c[1];
+        counters->atomic_commits += c[2];
+    }
+}
+
+}  // namespace pathgcn::b200

@@ -1,0 +1,153 @@
+// C++ drop-in test: the reference's own known-answer cases
+// (proj/tests/unit/test_*.cpp, acceptance.cpp) written against the C++
+// host API in include/pathgcn_b200.hpp, plus bit-exact comparisons with the
+// C oracle (oracle/pathgcn_oracle.h) on the RMAT fixture. One PASS/FAIL
+// line per check like acceptance.cpp; exit code = number of failures.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <set>
+#include <vector>
+
+#include "../../include/pathgcn_b200.hpp"
+#include "../../oracle/pathgcn_oracle.h"
+
+using namespace pathgcn::b200;
+
+static int g_fail = 0;
+static void report(const char* name, bool ok) {
+    std::printf("[%s] %s\n", ok ? "PASS" : "FAIL", name);
+    if (!ok) ++g_fail;
+}
+
+static EdgeList gex_edges() {
+    EdgeList el;
+    el.pairs = {{0, 1}, {1, 2}, {1, 3}, {1, 4}, {2, 3}, {3, 4}};
+    return el;
+}
+
+static std::set<std::pair<VertexId, VertexId>> path_edges(const ExecutionPathHost& p) {
+    std::set<std::pair<VertexId, VertexId>> out;
+    for (std::size_t d = 0; d < p.dest_local_to_global.size(); ++d)
+        for (auto e = p.offsets[d]; e < p.offsets[d + 1]; ++e)
+            out.insert({p.src_local_to_global[p.neighbors[e]], p.dest_local_to_global[d]});
+    return out;
+}
+
+int main() {
+    // test_frontier.cpp:10-18
+    DeviceGraph g = build_undirected_csr(gex_edges());
+    const std::vector<VertexId> vt = {2, 4};
+    DeviceFrontiers f = compute_frontiers(g, vt, 2);
+    report("frontiers worked example",
+           f.level(0) == std::vector<VertexId>{2, 4} && f.level(1) == std::vector<VertexId>{1, 3} &&
+               f.level(2) == std::vector<VertexId>{0, 1, 2, 3, 4});
+    // test_execution_path.cpp:23-47
+    auto paths = prepare_all_paths(g, f);
+    const auto sg1 = paths[0].to_host(), sg0 = paths[1].to_host();
+    report("SG_1 carries the four listed edges",
+           sg1.layer == 1 && sg1.offsets == std::vector<EdgeIndex>{0, 2, 4} &&
+               path_edges(sg1) == std::set<std::pair<VertexId, VertexId>>{{2, 1}, {4, 1}, {2, 3}, {4, 3}});
+    report("SG_0 carries the seven listed edges",
+           sg0.dest_local_to_global.size() == 5 && paths[1].edge_count() == 7 &&
+               path_edges(sg0) ==
+                   std::set<std::pair<VertexId, VertexId>>{{1, 0}, {3, 1}, {1, 2}, {3, 2}, {1, 3}, {1, 4}, {3, 4}});
+    // test_grouping.cpp:8-18 (graph grouping, gs = 3)
+    {
+        DeviceGroups gr = group_neighbors(g, 3);
+        std::vector<VertexId> d;
+        std::vector<EdgeIndex> b, e;
+        std::vector<std::uint64_t> dg;
+        gr.to_host(d, b, e, dg);
+        report("gs=3 splits the degree-4 vertex 3+1",
+               gr.group_count() == 6 && dg[2] - dg[1] == 2 && e[dg[1]] - b[dg[1]] == 3 &&
+                   e[dg[1] + 1] - b[dg[1] + 1] == 1);
+        bool threw = false;
+        try {
+            group_neighbors(g, 0);
+        } catch (const ConfigError&) {
+            threw = true;
+        }
+        report("gs=0 is a config error", threw);
+    }
+    // test_engine.cpp:72-80
+    {
+        DeviceGroups gr = group_neighbors(g, 3);
+        MatrixF x(5, 1), y(5, 1);
+        x.data = {1, 2, 3, 4, 5};
+        StageCounters c;
+        aggregate_pull(gr, x, y, CommitMode::Deterministic, 0, &c);
+        report("aggregate_pull hand sums [2,13,6,10,6]",
+               y.data == std::vector<float>{2, 13, 6, 10, 6} && c.edges_traversed == 12 && c.groups_executed == 6);
+    }
+    // test_engine.cpp:169-180
+    {
+        DeviceGroups gr = group_neighbors(paths[0], 2);
+        MatrixF yu(2, 1), xg(2, 1);
+        yu.data = {1.0f, 2.0f};
+        aggregate_pull(gr, yu, xg);
+        report("SG_1 hand case [3,3]", xg.data == std::vector<float>{3.0f, 3.0f});
+    }
+    // test_gs_model.cpp:47-58
+    report("regression Cora/Youtube", regression_gs(GraphStats{2708, 5278, 5278.0 / 2708}) == 2 &&
+                                          regression_gs(GraphStats{1134890, 2987624, 2987624.0 / 1134890}) == 15);
+    // test_group_cost.cpp:60-68 (star(64), W=8, lambda=0.1)
+    {
+        EdgeList st;
+        for (VertexId i = 1; i <= 64; ++i) st.pairs.push_back({0, i});
+        DeviceGraph sg = build_undirected_csr(st);
+        report("hub grouping cost gs=8 = 267.2",
+               std::abs(group_neighbors(sg, 8).grouping_cost(16, {8, 0.1}) - 267.2) < 1e-9);
+    }
+    // staleness stamp (engine.hpp:278-283 uses path_fingerprint)
+    report("path fingerprint depends on L", path_fingerprint(g, vt, 2) != path_fingerprint(g, vt, 3));
+    // shape errors (aggregate.hpp:61-62)
+    {
+        bool threw = false;
+        try {
+            DeviceGroups gr = group_neighbors(paths[1], 2);
+            MatrixF in(2, 4), out(5, 3);
+            aggregate_pull(gr, in, out);
+        } catch (const ShapeError&) {
+            threw = true;
+        }
+        report("shape mismatch throws ShapeError", threw);
+    }
+
+    // RMAT fixture (test_rmat.cpp:72-81) vs the C oracle, bit for bit
+    {
+        const std::uint64_t m = 8192;
+        std::vector<std::uint32_t> pairs(2 * m);
+        const std::uint32_t n_pad = orc_gen_rmat(1024, m, 0.45, 0.22, 0.22, 0.11, 7, pairs.data());
+        EdgeList el;
+        el.n_hint = n_pad;
+        for (std::uint64_t i = 0; i < m; ++i) el.pairs.push_back({pairs[2 * i], pairs[2 * i + 1]});
+        DeviceGraph rg = build_undirected_csr(el, WeightMode::SymNorm);
+        report("rmat fixture n/m/maxdeg", rg.n() == 1024 && rg.m() == 15376 && rg.max_degree() == 214);
+        std::vector<VertexId> rvt(orc_training_set_size(1024, 0.1));
+        orc_sample_training_set(1024, 0.1, 42, rvt.data());
+        DeviceFrontiers rf = compute_frontiers(rg, rvt, 2);
+        auto rpaths = prepare_all_paths(rg, rf);
+        std::vector<EdgeIndex> off;
+        std::vector<VertexId> nb;
+        std::vector<double> w;
+        rg.to_host(off, nb, w);
+        bool ok = true;
+        for (auto& dp : rpaths) {
+            const auto p = dp.to_host();
+            const std::size_t D = p.dest_local_to_global.size(), S = p.src_local_to_global.size();
+            MatrixF y(S, 37), out(D, 37);
+            for (std::size_t i = 0; i < y.data.size(); ++i) y.data[i] = std::sin(0.37 * double(i));
+            DeviceGroups gr = group_neighbors(dp, regression_gs(dp));
+            aggregate_pull(gr, y, out);
+            std::vector<float> want(D * 37, 0.0f);
+            orc_aggregate_pull_f32(D, p.offsets.data(), p.neighbors.data(), p.weights.data(), y.data.data(), 37,
+                                   want.data());
+            ok = ok && std::memcmp(want.data(), out.data.data(), want.size() * 4) == 0;
+        }
+        report("rmat fixture SpMM bit-exact vs oracle", ok);
+        report("rmat probe gs 2 / 9", regression_gs(rpaths[0]) == 2 && regression_gs(rpaths[1]) == 9);
+    }
+    std::printf("%d failure(s)\n", g_fail);
+    return g_fail;
+}

@@ -181,9 +181,12 @@ def test_row_shards_concatenate(pg, orc):
         want = orc.aggregate_pull_f32(op.offsets, op.neighbors, op.weights, y[op.srcpos])
         G = pg.group_neighbors(dp, 4)
         yd = to_dev(y, 64)
+        from paper_2204_02662_b200 import dist as pgd
+
         for world in (1, 2, 3, 8):
             b = dp.shard_bounds(world)
             assert b[0] == 0 and b[-1] == dp.D and (np.diff(b.astype(np.int64)) >= 0).all()
+            assert np.array_equal(b.astype(np.int64), pgd.edge_balanced_bounds(op.offsets, world))
             parts = []
             for r in range(world):
                 xs = to_dev(np.zeros((int(b[r + 1] - b[r]), dim), np.float32), 64)
@@ -192,6 +195,46 @@ def test_row_shards_concatenate(pg, orc):
             torch.cuda.synchronize()
             got = torch.cat(parts).cpu().numpy()
             assert np.array_equal(bits(got), bits(want)), world
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_remapped_allgather_layout(pg, orc, world):
+    """The multi-GPU data path on one device: y_grad row shards laid out as a
+    padded all_gather buffer, the remapped edge stream, per-rank row ranges
+    (the heavy kernel forced on for some ranks' hubs)."""
+    torch = torch_mod()
+    from paper_2204_02662_b200 import dist as pgd
+
+    pairs, n_pad = rmat_pairs(orc, 4096, 4096 * 8, 19)
+    vt = orc.sample_training_set(4096, 0.25, 6)
+    og, dg, F, ops, dps = build_all(pg, orc, pairs, n_pad, vt, 2)
+    plan = pgd.plan([None, None], [dps[0].P, dps[1].P], world, [p.shard_bounds(world) for p in dps])
+    dims = [16, 41]
+    try:
+        pg.set_heavy_min_degree(256)
+        for i, (dp, op) in enumerate(zip(dps, ops)):
+            sh = plan[i]
+            y = np.random.default_rng(i).uniform(-1, 1, size=(dp.P, dims[i])).astype(np.float32)
+            want = orc.aggregate_pull_f32(op.offsets, op.neighbors, op.weights, y[op.srcpos])
+            padded = np.zeros((sh.gathered_rows, dims[i]), np.float32)
+            padded[sh.source_map] = y
+            G = pg.group_neighbors(dp, 3)
+            G.remap_sources(sh.source_map, sh.gathered_rows)
+            yd = to_dev(padded, pg.padded_ld(dims[i]))
+            parts = []
+            for r in range(world):
+                db, de = sh.my_dest_rows(r)
+                xs = pg.empty_rows(de - db, dims[i])
+                pg.backward_aggregation(G, yd, xs, overwrite=True, rows=(db, de))
+                parts.append(xs)
+            torch.cuda.synchronize()
+            got = torch.cat(parts).cpu().numpy()
+            assert np.array_equal(bits(got), bits(want))
+            with pytest.raises(pg.ConfigError):  # host path refuses a remapped grouping
+                pg.backward_aggregation(G, y, np.zeros((dp.D, dims[i]), np.float32))
+            G.remap_sources(None, 0)
+    finally:
+        pg.set_heavy_min_degree(None)
 
 
 def test_unit_weights_hub_heavy(pg, orc):
