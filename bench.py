@@ -430,6 +430,35 @@ def sweep(pg, torch, step, paths, dims, stream):
         torch.cuda.synchronize()
         ms = [statistics.mean(evs[k][i][1].elapsed_time(evs[k][i][2]) for k in range(10)) for i in range(L)]
         log(f"[sweep] heavy_min_deg={str(hmin):>7s} per-path ms={[round(x, 3) for x in ms]} total={sum(ms):.3f}")
+    # simulated destination-row shards: each rank's SpMM rows timed alone
+    from paper_2204_02662_b200 import pathgcn as pgm
+
+    groups = [pgm.group_neighbors(p, 1) for p in paths]
+    for hmin in (None, 0):
+        pg.set_heavy_min_degree(hmin)
+        for world in (2, 4, 8):
+            per = []
+            for i, p in enumerate(paths):
+                b = p.shard_bounds(world)
+                y = pg.empty_rows(p.P, dims[i])
+                y.uniform_(-1, 1)
+                ts = []
+                for r in range(world):
+                    x = pg.empty_rows(int(b[r + 1] - b[r]), dims[i])
+                    for _ in range(2):
+                        pg.backward_aggregation(groups[i], y, x, overwrite=True, rows=(b[r], b[r + 1]))
+                    a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record()
+                    for _ in range(3):
+                        pg.backward_aggregation(groups[i], y, x, overwrite=True, rows=(b[r], b[r + 1]))
+                    z.record()
+                    torch.cuda.synchronize()
+                    ts.append(a.elapsed_time(z) / 3)
+                per.append(ts)
+            log(f"[shards] heavy={hmin} world={world} per-path max/mean ms="
+                f"{[(round(max(t), 3), round(sum(t) / len(t), 3)) for t in per]} rank-max sum="
+                f"{sum(max(t) for t in per):.3f}")
+    pg.set_heavy_min_degree(None)
     nbytes = paths[-1].P * dims[-1] * 4
     h = torch.empty(nbytes // 4, dtype=torch.float32, pin_memory=True)
     d = torch.empty(nbytes // 4, dtype=torch.float32, device="cuda")

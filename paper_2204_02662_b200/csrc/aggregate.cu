@@ -92,6 +92,91 @@ __global__ void __launch_bounds__(256) k_agg_vec4(const uint64_t* __restrict__ o
     }
 }
 
+// Wide rows (> 16 float4 columns): a full warp per (destination, 32-float4
+// chunk). Edge records are loaded 32 at a time, one per lane (coalesced), and
+// the next batch is prefetched while the current one is consumed; records
+// are broadcast with shuffles, so each group of U row gathers waits on one
+// memory round trip instead of two.
+template <int U>
+__global__ void __launch_bounds__(256) k_agg_wide(const uint64_t* __restrict__ offsets,
+                                                 const Edge* __restrict__ edges,
+                                                 const uint32_t* __restrict__ order, uint32_t d_begin,
+                                                 uint64_t n_items, uint32_t chunks,
+                                                 const float* __restrict__ in, uint64_t ld_in,
+                                                 float* __restrict__ out, uint64_t ld_out, uint32_t dim,
+                                                 int accumulate) {
+    static_assert(32 % U == 0, "U divides the 32-edge batch");
+    const uint64_t item = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+    if (item >= n_items) return;
+    const unsigned lane = lane_id();
+    const uint32_t d = order[d_begin + item / chunks];
+    const uint32_t col = (static_cast<uint32_t>(item % chunks) * 32 + lane) * 4;
+    const bool active = col < dim;
+    const uint64_t eb = offsets[d], ee = offsets[d + 1];
+    float* orow = out + d * ld_out + col;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (accumulate && active) {
+        if (col + 3 < dim) acc = *reinterpret_cast<const float4*>(orow);
+        else {
+            acc.x = orow[0];
+            if (col + 1 < dim) acc.y = orow[1];
+            if (col + 2 < dim) acc.z = orow[2];
+        }
+    }
+    const float* icol = in + col;
+    Edge nxt = eb + lane < ee ? __ldg(edges + eb + lane) : make_uint2(0u, 0u);
+    for (uint64_t e0 = eb; e0 < ee; e0 += 32) {
+        const Edge cur = nxt;
+        if (e0 + 32 + lane < ee) nxt = __ldg(edges + e0 + 32 + lane);  // prefetch next batch
+        const uint32_t n = static_cast<uint32_t>(min(static_cast<uint64_t>(32), ee - e0));
+        if (n == 32) {
+#pragma unroll
+            for (int s = 0; s < 32; s += U) {
+                uint32_t src[U];
+                float w[U];
+                float4 x[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    src[u] = __shfl_sync(0xffffffffu, cur.x, s + u);
+                    w[u] = __uint_as_float(__shfl_sync(0xffffffffu, cur.y, s + u));
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    x[u] = active ? ldg4(icol + src[u] * ld_in) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int u = 0; u < U; ++u) acc4(acc, w[u], x[u]);
+            }
+        } else {
+            for (uint32_t j = 0; j < n; ++j) {
+                const uint32_t src = __shfl_sync(0xffffffffu, cur.x, j);
+                const float w = __uint_as_float(__shfl_sync(0xffffffffu, cur.y, j));
+                const float4 x = active ? ldg4(icol + src * ld_in) : make_float4(0.f, 0.f, 0.f, 0.f);
+                acc4(acc, w, x);
+            }
+        }
+    }
+    if (!active) return;
+    acc.x = __fadd_rn(acc.x, 0.f);
+    acc.y = __fadd_rn(acc.y, 0.f);
+    acc.z = __fadd_rn(acc.z, 0.f);
+    acc.w = __fadd_rn(acc.w, 0.f);
+    if (col + 3 < dim) {
+        __stcs(reinterpret_cast<float4*>(orow), acc);
+    } else {
+        orow[0] = acc.x;
+        if (col + 1 < dim) orow[1] = acc.y;
+        if (col + 2 < dim) orow[2] = acc.z;
+    }
+}
+
+int wide_unroll() {
+    static const int v = [] {
+        const char* e = std::getenv("PG_WIDE_U");
+        return e ? std::atoi(e) : 16;
+    }();
+    return v;
+}
+
 // Scalar fallback for unaligned rows (ld or base not 16-byte aligned).
 template <int U>
 __global__ void __launch_bounds__(256) k_agg_scalar(const uint64_t* __restrict__ offsets,
@@ -572,8 +657,21 @@ void aggregate_det(const uint64_t* offsets, const Edge* edges, const uint32_t* o
     }
     const uint32_t nq = (dim32 + 3) / 4;
     if (nq > 16) {
-        launch_vec4<32, 8>(offsets, edges, order, d_begin, nd, (nq + 31) / 32, in, ld_in, out, ld_out, dim32,
-                           accumulate, s);
+        const int U = wide_unroll();
+        const uint32_t chunks = (nq + 31) / 32;
+        const uint64_t items = static_cast<uint64_t>(nd) * chunks;
+        if (U == 0) {  // the round-1 kernel, for A/B
+            launch_vec4<32, 8>(offsets, edges, order, d_begin, nd, chunks, in, ld_in, out, ld_out, dim32,
+                               accumulate, s);
+        } else if (U == 8) {
+            k_agg_wide<8><<<grid_for(items * 32, 256), 256, 0, s>>>(offsets, edges, order, d_begin, items, chunks,
+                                                                   in, ld_in, out, ld_out, dim32, accumulate);
+            PG_LAUNCH("k_agg_wide");
+        } else {
+            k_agg_wide<16><<<grid_for(items * 32, 256), 256, 0, s>>>(offsets, edges, order, d_begin, items, chunks,
+                                                                    in, ld_in, out, ld_out, dim32, accumulate);
+            PG_LAUNCH("k_agg_wide");
+        }
     } else if (nq > 8) {
         launch_vec4<16, 8>(offsets, edges, order, d_begin, nd, 1, in, ld_in, out, ld_out, dim32, accumulate, s);
     } else if (nq > 4) {
