@@ -434,9 +434,9 @@ def sweep(pg, torch, step, paths, dims, stream):
     from paper_2204_02662_b200 import pathgcn as pgm
 
     groups = [pgm.group_neighbors(p, 1) for p in paths]
-    for hmin in (None, 0):
+    for hmin in (None, 0, 2048, 4096, 8192, 16384):
         pg.set_heavy_min_degree(hmin)
-        for world in (2, 4, 8):
+        for world in (1, 2, 4, 8):
             per = []
             for i, p in enumerate(paths):
                 b = p.shard_bounds(world)

@@ -169,10 +169,13 @@ __global__ void __launch_bounds__(256) k_agg_wide(const uint64_t* __restrict__ o
     }
 }
 
+// Main-kernel choice for wide rows (PG_WIDE_U): 0 = k_agg_vec4<32,8>
+// (default; 54 registers, 4 blocks/SM — best throughput), 8/16 =
+// k_agg_wide<U>. Heavy wide destinations always use k_agg_wide<32>.
 int wide_unroll() {
     static const int v = [] {
         const char* e = std::getenv("PG_WIDE_U");
-        return e ? std::atoi(e) : 16;
+        return e ? std::atoi(e) : 0;
     }();
     return v;
 }
@@ -627,10 +630,15 @@ void aggregate_det(const uint64_t* offsets, const Edge* edges, const uint32_t* o
         SideStream& ss = side_stream();
         PG_CUDA(cudaEventRecord(ss.fork, s));
         PG_CUDA(cudaStreamWaitEvent(ss.s, ss.fork, 0));
-        if (nq > 16)
-            launch_heavy_any<32>(offsets, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim32, accumulate,
-                                 ss.s);
-        else if (nq > 8)
+        if (nq > 16) {
+            // wide rows: latency-optimised warp kernel, 32 row gathers in
+            // flight per lane, 5 column-chunk warps per 602-wide destination
+            const uint32_t chunks = (nq + 31) / 32;
+            const uint64_t items = static_cast<uint64_t>(nh) * chunks;
+            k_agg_wide<32><<<grid_for(items * 32, 256), 256, 0, ss.s>>>(offsets, edges, order, d_begin, items, chunks,
+                                                                       in, ld_in, out, ld_out, dim32, accumulate);
+            PG_LAUNCH("k_agg_wide<32>");
+        } else if (nq > 8)
             launch_heavy_any<16>(offsets, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim32, accumulate,
                                  ss.s);
         else if (nq > 4)
