@@ -26,11 +26,72 @@ __device__ __forceinline__ float4 ldg4(const float* p) {
     return __ldg(reinterpret_cast<const float4*>(p));
 }
 
-__device__ __forceinline__ void acc4(float4& a, float w, const float4& x) {
-    a.x = __fadd_rn(a.x, __fmul_rn(w, x.x));
-    a.y = __fadd_rn(a.y, __fmul_rn(w, x.y));
-    a.z = __fadd_rn(a.z, __fmul_rn(w, x.z));
-    a.w = __fadd_rn(a.w, __fmul_rn(w, x.w));
+// float4 accumulator held as two packed fp32 pairs for Blackwell's FFMA2 /
+// FADD2, with the reference's separately rounded multiply and add:
+//   p = fma.rn.f32x2(w, x, nz) with nz = -0.0 passed at RUN time, which is
+//       exactly round(w*x) (w*x + -0 == w*x for every w*x, signed zeros
+//       included);
+//   acc = add.rn.f32x2(acc, p).
+// A compile-time -0 (or plain mul.rn.f32x2 + add.rn.f32x2) lets ptxas fold
+// the pair into one FFMA2 that rounds once — not the reference's result.
+// Half the FP instructions of scalar FMUL+FADD; bit-identical.
+struct Acc {
+    unsigned long long lo, hi;
+};
+struct Zs {
+    unsigned long long nz, pz;  // (-0,-0) and (+0,+0), from a kernel argument
+};
+const float2 kZeros = make_float2(-0.0f, 0.0f);  // host side: the kernel argument
+
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ float2 unpk2(unsigned long long v) {
+    float2 r;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+    return r;
+}
+__device__ __forceinline__ Zs zs_of(float2 z) { return {pk2(z.x, z.x), pk2(z.y, z.y)}; }
+
+__device__ __forceinline__ void acc_step(Acc& a, float w, const float4& x, const Zs& z) {
+    const unsigned long long ww = pk2(w, w);
+    unsigned long long p0, p1;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p0) : "l"(ww), "l"(pk2(x.x, x.y)), "l"(z.nz));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p1) : "l"(ww), "l"(pk2(x.z, x.w)), "l"(z.nz));
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(a.lo) : "l"(a.lo), "l"(p0));
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(a.hi) : "l"(a.hi), "l"(p1));
+}
+
+// zero, or the current output (accumulate semantics, aggregate.hpp:50-55)
+__device__ __forceinline__ Acc acc_load(const float* orow, uint32_t col, uint32_t dim, bool doit) {
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (doit && col < dim) {
+        if (col + 3 < dim) v = *reinterpret_cast<const float4*>(orow);
+        else {
+            v.x = orow[0];
+            if (col + 1 < dim) v.y = orow[1];
+            if (col + 2 < dim) v.z = orow[2];
+        }
+    }
+    return {pk2(v.x, v.y), pk2(v.z, v.w)};
+}
+
+// acc + 0 (-0 -> +0, aggregate.hpp:82), then a streaming store of the
+// columns inside dim
+__device__ __forceinline__ void acc_store(float* orow, uint32_t col, uint32_t dim, Acc a, const Zs& z) {
+    if (col >= dim) return;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(a.lo) : "l"(a.lo), "l"(z.pz));
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(a.hi) : "l"(a.hi), "l"(z.pz));
+    const float2 l = unpk2(a.lo), h = unpk2(a.hi);
+    if (col + 3 < dim) {
+        __stcs(reinterpret_cast<float4*>(orow), make_float4(l.x, l.y, h.x, h.y));
+    } else {
+        orow[0] = l.x;
+        if (col + 1 < dim) orow[1] = l.y;
+        if (col + 2 < dim) orow[2] = h.x;
+    }
 }
 
 // LPD lanes per (destination, chunk); each lane one float4 column.
@@ -41,10 +102,11 @@ __global__ void __launch_bounds__(256) k_agg_vec4(const uint64_t* __restrict__ o
                                                  uint64_t n_items, uint32_t chunks,
                                                  const float* __restrict__ in, uint64_t ld_in,
                                                  float* __restrict__ out, uint64_t ld_out, uint32_t dim,
-                                                 int accumulate) {
+                                                 int accumulate, float2 zeros) {
     const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     const uint64_t item = t / LPD;
     if (item >= n_items) return;
+    const Zs z = zs_of(zeros);
     const uint32_t d = order[d_begin + item / chunks];
     const uint32_t q = static_cast<uint32_t>(item % chunks) * LPD + static_cast<uint32_t>(t % LPD);
     const uint32_t col = q * 4;
@@ -52,15 +114,7 @@ __global__ void __launch_bounds__(256) k_agg_vec4(const uint64_t* __restrict__ o
     uint64_t e = offsets[d];
     const uint64_t end = offsets[d + 1];
     float* orow = out + d * ld_out + col;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (accumulate && active) {
-        if (col + 3 < dim) acc = *reinterpret_cast<const float4*>(orow);
-        else {
-            acc.x = orow[0];
-            if (col + 1 < dim) acc.y = orow[1];
-            if (col + 2 < dim) acc.z = orow[2];
-        }
-    }
+    Acc acc = acc_load(orow, col, dim, accumulate);
     const float* icol = in + col;
     for (; e + U <= end; e += U) {
         Edge ed[U];
@@ -71,25 +125,14 @@ __global__ void __launch_bounds__(256) k_agg_vec4(const uint64_t* __restrict__ o
         for (int u = 0; u < U; ++u)
             x[u] = active ? ldg4(icol + ed[u].x * ld_in) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int u = 0; u < U; ++u) acc4(acc, __uint_as_float(ed[u].y), x[u]);
+        for (int u = 0; u < U; ++u) acc_step(acc, __uint_as_float(ed[u].y), x[u], z);
     }
     for (; e < end; ++e) {
         const Edge ed = __ldg(edges + e);
         const float4 x = active ? ldg4(icol + ed.x * ld_in) : make_float4(0.f, 0.f, 0.f, 0.f);
-        acc4(acc, __uint_as_float(ed.y), x);
+        acc_step(acc, __uint_as_float(ed.y), x, z);
     }
-    if (!active) return;
-    acc.x = __fadd_rn(acc.x, 0.f);
-    acc.y = __fadd_rn(acc.y, 0.f);
-    acc.z = __fadd_rn(acc.z, 0.f);
-    acc.w = __fadd_rn(acc.w, 0.f);
-    if (col + 3 < dim) {
-        __stcs(reinterpret_cast<float4*>(orow), acc);
-    } else {
-        orow[0] = acc.x;
-        if (col + 1 < dim) orow[1] = acc.y;
-        if (col + 2 < dim) orow[2] = acc.z;
-    }
+    acc_store(orow, col, dim, acc, z);
 }
 
 // Wide rows (> 16 float4 columns): a full warp per (destination, 32-float4
@@ -104,25 +147,18 @@ __global__ void __launch_bounds__(256) k_agg_wide(const uint64_t* __restrict__ o
                                                  uint64_t n_items, uint32_t chunks,
                                                  const float* __restrict__ in, uint64_t ld_in,
                                                  float* __restrict__ out, uint64_t ld_out, uint32_t dim,
-                                                 int accumulate) {
+                                                 int accumulate, float2 zeros) {
     static_assert(32 % U == 0, "U divides the 32-edge batch");
     const uint64_t item = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
     if (item >= n_items) return;
+    const Zs z = zs_of(zeros);
     const unsigned lane = lane_id();
     const uint32_t d = order[d_begin + item / chunks];
     const uint32_t col = (static_cast<uint32_t>(item % chunks) * 32 + lane) * 4;
     const bool active = col < dim;
     const uint64_t eb = offsets[d], ee = offsets[d + 1];
     float* orow = out + d * ld_out + col;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (accumulate && active) {
-        if (col + 3 < dim) acc = *reinterpret_cast<const float4*>(orow);
-        else {
-            acc.x = orow[0];
-            if (col + 1 < dim) acc.y = orow[1];
-            if (col + 2 < dim) acc.z = orow[2];
-        }
-    }
+    Acc acc = acc_load(orow, col, dim, accumulate);
     const float* icol = in + col;
     Edge nxt = eb + lane < ee ? __ldg(edges + eb + lane) : make_uint2(0u, 0u);
     for (uint64_t e0 = eb; e0 < ee; e0 += 32) {
@@ -144,29 +180,18 @@ __global__ void __launch_bounds__(256) k_agg_wide(const uint64_t* __restrict__ o
                 for (int u = 0; u < U; ++u)
                     x[u] = active ? ldg4(icol + src[u] * ld_in) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-                for (int u = 0; u < U; ++u) acc4(acc, w[u], x[u]);
+                for (int u = 0; u < U; ++u) acc_step(acc, w[u], x[u], z);
             }
         } else {
             for (uint32_t j = 0; j < n; ++j) {
                 const uint32_t src = __shfl_sync(0xffffffffu, cur.x, j);
                 const float w = __uint_as_float(__shfl_sync(0xffffffffu, cur.y, j));
                 const float4 x = active ? ldg4(icol + src * ld_in) : make_float4(0.f, 0.f, 0.f, 0.f);
-                acc4(acc, w, x);
+                acc_step(acc, w, x, z);
             }
         }
     }
-    if (!active) return;
-    acc.x = __fadd_rn(acc.x, 0.f);
-    acc.y = __fadd_rn(acc.y, 0.f);
-    acc.z = __fadd_rn(acc.z, 0.f);
-    acc.w = __fadd_rn(acc.w, 0.f);
-    if (col + 3 < dim) {
-        __stcs(reinterpret_cast<float4*>(orow), acc);
-    } else {
-        orow[0] = acc.x;
-        if (col + 1 < dim) orow[1] = acc.y;
-        if (col + 2 < dim) orow[2] = acc.z;
-    }
+    acc_store(orow, col, dim, acc, z);
 }
 
 // Main-kernel choice for wide rows (PG_WIDE_U): 0 = k_agg_vec4<32,8>
@@ -274,7 +299,7 @@ __global__ void __launch_bounds__(64) k_agg_heavy(const uint64_t* __restrict__ o
                                                  uint32_t chunks, uint32_t nq_total,
                                                  const float* __restrict__ in, uint64_t ld_in,
                                                  float* __restrict__ out, uint64_t ld_out, uint32_t dim,
-                                                 int accumulate) {
+                                                 int accumulate, float2 zeros) {
     constexpr int T = heavy_T<CHQ>();
     constexpr int NS = kHeavyStages;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -320,18 +345,11 @@ __global__ void __launch_bounds__(64) k_agg_heavy(const uint64_t* __restrict__ o
         return;
     }
     // consumer warp: lane = float4 column of the chunk
+    const Zs z = zs_of(zeros);
     const bool active = lane < nqc;
     const uint32_t col = (q0 + lane) * 4;
     float* orow = out + d * ld_out + col;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (accumulate && active && col < dim) {
-        if (col + 3 < dim) acc = *reinterpret_cast<const float4*>(orow);
-        else {
-            acc.x = orow[0];
-            if (col + 1 < dim) acc.y = orow[1];
-            if (col + 2 < dim) acc.z = orow[2];
-        }
-    }
+    Acc acc = acc_load(orow, col, dim, accumulate && active);
     for (uint64_t t = 0; t < ntiles; ++t) {
         const int s = static_cast<int>(t % NS);
         const uint32_t ph = static_cast<uint32_t>((t / NS) & 1);
@@ -340,23 +358,12 @@ __global__ void __launch_bounds__(64) k_agg_heavy(const uint64_t* __restrict__ o
         if (active) {
             const float4* sb = buf + static_cast<size_t>(s) * T * CHQ + lane;
             const float* sw = wbuf + s * T;
-            for (uint32_t j = 0; j < n; ++j) acc4(acc, sw[j], sb[j * CHQ]);
+            for (uint32_t j = 0; j < n; ++j) acc_step(acc, sw[j], sb[j * CHQ], z);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
     }
-    if (!active || col >= dim) return;
-    acc.x = __fadd_rn(acc.x, 0.f);
-    acc.y = __fadd_rn(acc.y, 0.f);
-    acc.z = __fadd_rn(acc.z, 0.f);
-    acc.w = __fadd_rn(acc.w, 0.f);
-    if (col + 3 < dim) {
-        __stcs(reinterpret_cast<float4*>(orow), acc);
-    } else {
-        orow[0] = acc.x;
-        if (col + 1 < dim) orow[1] = acc.y;
-        if (col + 2 < dim) orow[2] = acc.z;
-    }
+    if (active) acc_store(orow, col, dim, acc, z);
 }
 
 template <int CHQ>
@@ -375,7 +382,7 @@ void launch_heavy(const uint64_t* offsets, const Edge* edges, const uint32_t* or
     }
     const uint32_t chunks = (nq + CHQ - 1) / CHQ;
     k_agg_heavy<CHQ><<<nh * chunks, 64, smem, s>>>(offsets, edges, order, d_begin, chunks, nq, in, ld_in, out,
-                                                   ld_out, dim, accumulate);
+                                                   ld_out, dim, accumulate, kZeros);
     PG_LAUNCH("k_agg_heavy");
 }
 
@@ -398,7 +405,7 @@ __global__ void __launch_bounds__(256) k_agg_heavy_coop(const uint64_t* __restri
                                                        uint32_t chunks, uint32_t nq_total,
                                                        const float* __restrict__ in, uint64_t ld_in,
                                                        float* __restrict__ out, uint64_t ld_out, uint32_t dim,
-                                                       int accumulate) {
+                                                       int accumulate, float2 zeros) {
     constexpr int T = coop_T<CHQ>();
     constexpr int PER = T * CHQ / 256;  // float4 gathers per thread per tile
     extern __shared__ __align__(128) unsigned char smem[];
@@ -438,18 +445,11 @@ __global__ void __launch_bounds__(256) k_agg_heavy_coop(const uint64_t* __restri
         }
     };
 
+    const Zs z = zs_of(zeros);
     const bool owner = tid < 32 && lane < nqc;
     const uint32_t col = (q0 + lane) * 4;
     float* orow = out + d * ld_out + col;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (owner && accumulate && col < dim) {
-        if (col + 3 < dim) acc = *reinterpret_cast<const float4*>(orow);
-        else {
-            acc.x = orow[0];
-            if (col + 1 < dim) acc.y = orow[1];
-            if (col + 2 < dim) acc.z = orow[2];
-        }
-    }
+    Acc acc = acc_load(orow, col, dim, owner && accumulate);
     if (ntiles) {
         gather(0);
         stash(0);
@@ -462,23 +462,12 @@ __global__ void __launch_bounds__(256) k_agg_heavy_coop(const uint64_t* __restri
             const uint32_t n = static_cast<uint32_t>(min(static_cast<uint64_t>(T), ee - (eb + t * T)));
             const float4* sb = tile + b * T * CHQ + lane;
             const float* sw = wt + b * T;
-            for (uint32_t j = 0; j < n; ++j) acc4(acc, sw[j], sb[j * CHQ]);
+            for (uint32_t j = 0; j < n; ++j) acc_step(acc, sw[j], sb[j * CHQ], z);
         }
         if (t + 1 < ntiles) stash(b ^ 1);
         __syncthreads();
     }
-    if (!owner || col >= dim) return;
-    acc.x = __fadd_rn(acc.x, 0.f);
-    acc.y = __fadd_rn(acc.y, 0.f);
-    acc.z = __fadd_rn(acc.z, 0.f);
-    acc.w = __fadd_rn(acc.w, 0.f);
-    if (col + 3 < dim) {
-        __stcs(reinterpret_cast<float4*>(orow), acc);
-    } else {
-        orow[0] = acc.x;
-        if (col + 1 < dim) orow[1] = acc.y;
-        if (col + 2 < dim) orow[2] = acc.z;
-    }
+    if (owner) acc_store(orow, col, dim, acc, z);
 }
 
 template <int CHQ>
@@ -497,7 +486,7 @@ void launch_heavy_coop(const uint64_t* offsets, const Edge* edges, const uint32_
     }
     const uint32_t chunks = (nq + CHQ - 1) / CHQ;
     k_agg_heavy_coop<CHQ><<<nh * chunks, 256, smem, s>>>(offsets, edges, order, d_begin, chunks, nq, in, ld_in, out,
-                                                         ld_out, dim, accumulate);
+                                                         ld_out, dim, accumulate, kZeros);
     PG_LAUNCH("k_agg_heavy_coop");
 }
 
@@ -544,7 +533,7 @@ void launch_vec4(const uint64_t* offsets, const Edge* edges, const uint32_t* ord
                  uint32_t dim, bool accumulate, cudaStream_t s) {
     const uint64_t items = static_cast<uint64_t>(nd) * chunks;
     k_agg_vec4<LPD, U><<<grid_for(items * LPD, 256), 256, 0, s>>>(offsets, edges, order, d_begin, items, chunks,
-                                                                 in, ld_in, out, ld_out, dim, accumulate);
+                                                                 in, ld_in, out, ld_out, dim, accumulate, kZeros);
     PG_LAUNCH("k_agg_vec4");
 }
 
@@ -636,7 +625,8 @@ void aggregate_det(const uint64_t* offsets, const Edge* edges, const uint32_t* o
             const uint32_t chunks = (nq + 31) / 32;
             const uint64_t items = static_cast<uint64_t>(nh) * chunks;
             k_agg_wide<32><<<grid_for(items * 32, 256), 256, 0, ss.s>>>(offsets, edges, order, d_begin, items, chunks,
-                                                                       in, ld_in, out, ld_out, dim32, accumulate);
+                                                                       in, ld_in, out, ld_out, dim32, accumulate,
+                                                                       kZeros);
             PG_LAUNCH("k_agg_wide<32>");
         } else if (nq > 8)
             launch_heavy_any<16>(offsets, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim32, accumulate,
@@ -673,11 +663,12 @@ void aggregate_det(const uint64_t* offsets, const Edge* edges, const uint32_t* o
                                accumulate, s);
         } else if (U == 8) {
             k_agg_wide<8><<<grid_for(items * 32, 256), 256, 0, s>>>(offsets, edges, order, d_begin, items, chunks,
-                                                                   in, ld_in, out, ld_out, dim32, accumulate);
+                                                                   in, ld_in, out, ld_out, dim32, accumulate, kZeros);
             PG_LAUNCH("k_agg_wide");
         } else {
             k_agg_wide<16><<<grid_for(items * 32, 256), 256, 0, s>>>(offsets, edges, order, d_begin, items, chunks,
-                                                                    in, ld_in, out, ld_out, dim32, accumulate);
+                                                                    in, ld_in, out, ld_out, dim32, accumulate,
+                                                                    kZeros);
             PG_LAUNCH("k_agg_wide");
         }
     } else if (nq > 8) {

@@ -140,10 +140,9 @@ void run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re, con
             PG_CUDA(cudaStreamSynchronize(lib_stream(p.device)));
             edges = p.edges_local.get();
         }
-        const uint64_t hmin = heavy_min_degree(dim);
         if (rb == 0 && re == p.D) {
-            aggregate_det(p.offsets.get(), edges, p.order.get(), p.D, 0, p.D, p.hist.heavy(hmin), in, ld_in, out,
-                          ld_out, dim, accumulate, s);
+            aggregate_det(p.offsets.get(), edges, p.order.get(), p.D, 0, p.D,
+                          p.hist.heavy(heavy_min_degree(dim, p.E)), in, ld_in, out, ld_out, dim, accumulate, s);
             return;
         }
         // row range: schedule of rows [rb, re) relative to rb (cached)
@@ -157,8 +156,9 @@ void run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re, con
             rs->re = re;
             degree_order(p.offsets.get() + rb, re - rb, rs->order, lib_stream(p.device), &rs->hist);
         }
-        aggregate_det(p.offsets.get() + rb, edges, rs->order.get(), re - rb, 0, re - rb, rs->hist.heavy(hmin), in,
-                      ld_in, out, ld_out, dim, accumulate, s);
+        aggregate_det(p.offsets.get() + rb, edges, rs->order.get(), re - rb, 0, re - rb,
+                      rs->hist.heavy(heavy_min_degree(dim, rs->hist.edges)), in, ld_in, out, ld_out, dim, accumulate,
+                      s);
         return;
     }
     Graph& g = *G.graph;
@@ -169,7 +169,7 @@ void run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re, con
     if (!G.graph_order.get() && g.n)
         degree_order(g.offsets.get(), g.n, G.graph_order, lib_stream(g.device), &G.graph_hist);
     aggregate_det(g.offsets.get(), g.edges.get(), G.graph_order.get(), g.n, 0, g.n,
-                  G.graph_hist.heavy(heavy_min_degree(dim)), in, ld_in, out, ld_out, dim, accumulate, s);
+                  G.graph_hist.heavy(heavy_min_degree(dim, g.m)), in, ld_in, out, ld_out, dim, accumulate, s);
 }
 
 struct CopyStream {

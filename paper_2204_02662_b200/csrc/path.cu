@@ -295,10 +295,15 @@ std::atomic<uint64_t> g_heavy_min{[] {
 }()};
 }  // namespace
 
-uint64_t heavy_min_degree(uint64_t dim) {
+uint64_t heavy_min_degree(uint64_t dim, uint64_t range_edges) {
     const uint64_t v = g_heavy_min.load(std::memory_order_relaxed);
     if (v != UINT64_MAX) return v;
-    return (dim + 3) / 4 <= 8 ? 4096 : 0;
+    // Measured on B200 (profiles/README.md, Reddit shape, 1/2/4/8 shards):
+    // a destination is a tail once its serial chain outlasts the range's
+    // bandwidth-bound time, which shrinks with the range's edge count.
+    if ((dim + 3) / 4 <= 8) return range_edges > 20000000ull ? 4096 : 2048;
+    const uint64_t t = range_edges / 7000;
+    return t > 12288 ? 0 : std::max<uint64_t>(t, 2048);
 }
 void set_heavy_min_degree(uint64_t v) { g_heavy_min.store(v, std::memory_order_relaxed); }
 
@@ -312,9 +317,14 @@ void degree_order(const uint64_t* offsets, uint32_t D, DevBuf<uint32_t>& order, 
     PG_LAUNCH("k_bucket_hist");
     unsigned long long h[65];
     PG_CUDA(cudaMemcpyAsync(h, hist.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
+    uint64_t ends[2] = {0, 0};
+    PG_CUDA(cudaMemcpyAsync(&ends[0], offsets, 8, cudaMemcpyDeviceToHost, s));
+    PG_CUDA(cudaMemcpyAsync(&ends[1], offsets + D, 8, cudaMemcpyDeviceToHost, s));
     PG_CUDA(cudaStreamSynchronize(s));
-    if (out_hist)
+    if (out_hist) {
         for (int b = 0; b < 65; ++b) out_hist->h[b] = h[b];
+        out_hist->edges = ends[1] - ends[0];
+    }
     unsigned long long cur[65];
     unsigned long long run = 0;
     for (int b = 64; b >= 0; --b) {  // descending degree bucket

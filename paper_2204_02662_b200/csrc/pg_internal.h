@@ -37,6 +37,7 @@ using Edge = uint2;
 // Degree-bucket histogram of a schedule (bucket b = floor(log2 deg) + 1).
 struct DegHist {
     unsigned long long h[65] = {};
+    uint64_t edges = 0;  // edges of the scheduled range
     // destinations of degree >= min_deg (rounded up to a power of two): the
     // prefix of the descending-bucket order
     uint32_t heavy(uint64_t min_deg) const {
@@ -162,7 +163,7 @@ void aggregate_det(const uint64_t* offsets, const Edge* edges, const uint32_t* o
                    float* out, uint64_t ld_out, uint64_t dim, bool accumulate, cudaStream_t s);
 // PG_HEAVY_MIN_DEG / pg_set_heavy_min_degree (0 disables; UINT64_MAX restores
 // the width-dependent default)
-uint64_t heavy_min_degree(uint64_t dim);
+uint64_t heavy_min_degree(uint64_t dim, uint64_t range_edges);
 void set_heavy_min_degree(uint64_t v);
 
 // dense_matrix.hpp:78-95 (fp32, ascending k, mul/add separately rounded, +0).
