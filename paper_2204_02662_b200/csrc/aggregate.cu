@@ -26,6 +26,18 @@ __device__ __forceinline__ float4 ldg4(const float* p) {
     return __ldg(reinterpret_cast<const float4*>(p));
 }
 
+// Volatile 128-bit read-only load: volatile asm keeps program order with the
+// (volatile) accumulate steps, so a batch of U gathers is issued before the
+// first use — the scheduler cannot trade memory-level parallelism for
+// registers.
+__device__ __forceinline__ float4 ldg4_batch(const float* p) {
+    float4 r;
+    asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                 : "l"(p));
+    return r;
+}
+
 // float4 accumulator held as two packed fp32 pairs for Blackwell's FFMA2 /
 // FADD2, with the reference's separately rounded multiply and add:
 //   p = fma.rn.f32x2(w, x, nz) with nz = -0.0 passed at RUN time, which is
@@ -62,6 +74,20 @@ __device__ __forceinline__ void acc_step(Acc& a, float w, const float4& x, const
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p1) : "l"(ww), "l"(pk2(x.z, x.w)), "l"(z.nz));
     asm("add.rn.f32x2 %0, %1, %2;" : "=l"(a.lo) : "l"(a.lo), "l"(p0));
     asm("add.rn.f32x2 %0, %1, %2;" : "=l"(a.hi) : "l"(a.hi), "l"(p1));
+}
+
+// Scalar FMUL + FADD form of acc_step (same bits). Used where latency, not
+// issue rate, bounds the kernel: with the longer scalar chain ptxas keeps a
+// whole batch of gathers in flight ahead of the math (measured: the packed
+// form let it interleave loads and lose memory-level parallelism).
+__device__ __forceinline__ void acc_step_scalar(Acc& a, float w, const float4& x) {
+    float2 l = unpk2(a.lo), h = unpk2(a.hi);
+    l.x = __fadd_rn(l.x, __fmul_rn(w, x.x));
+    l.y = __fadd_rn(l.y, __fmul_rn(w, x.y));
+    h.x = __fadd_rn(h.x, __fmul_rn(w, x.z));
+    h.y = __fadd_rn(h.y, __fmul_rn(w, x.w));
+    a.lo = pk2(l.x, l.y);
+    a.hi = pk2(h.x, h.y);
 }
 
 // zero, or the current output (accumulate semantics, aggregate.hpp:50-55)
@@ -176,11 +202,15 @@ __global__ void __launch_bounds__(256) k_agg_wide(const uint64_t* __restrict__ o
                     src[u] = __shfl_sync(0xffffffffu, cur.x, s + u);
                     w[u] = __uint_as_float(__shfl_sync(0xffffffffu, cur.y, s + u));
                 }
+                if (active) {
 #pragma unroll
-                for (int u = 0; u < U; ++u)
-                    x[u] = active ? ldg4(icol + src[u] * ld_in) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    for (int u = 0; u < U; ++u) x[u] = ldg4(icol + src[u] * ld_in);
 #pragma unroll
-                for (int u = 0; u < U; ++u) acc_step(acc, w[u], x[u], z);
+                    for (int u = 0; u < U; ++u) {
+                        if (U >= 32) acc_step_scalar(acc, w[u], x[u]);
+                        else acc_step(acc, w[u], x[u], z);
+                    }
+                }
             }
         } else {
             for (uint32_t j = 0; j < n; ++j) {
@@ -192,6 +222,84 @@ __global__ void __launch_bounds__(256) k_agg_wide(const uint64_t* __restrict__ o
         }
     }
     acc_store(orow, col, dim, acc, z);
+}
+
+// Heavy wide destinations: warp per (destination, 32-float4 chunk) like
+// k_agg_wide, but each lane stages its column of NB 32-edge batches in
+// shared memory with cp.async (LDGSTS, 16 B), so NB*32 row gathers (up to
+// 32 KB per warp) are in flight by construction; wait_group retires one batch
+// at a time and the lane folds it in edge order.
+constexpr int kAsyncWarps = 2;
+constexpr int kAsyncBatches = 2;  // 2 x 32 rows x 512 B = 32 KB in flight per warp
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                 "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int NB>
+__global__ void __launch_bounds__(kAsyncWarps * 32) k_agg_wide_async(
+    const uint64_t* __restrict__ offsets, const Edge* __restrict__ edges, const uint32_t* __restrict__ order,
+    uint32_t d_begin, uint64_t n_items, uint32_t chunks, const float* __restrict__ in, uint64_t ld_in,
+    float* __restrict__ out, uint64_t ld_out, uint32_t dim, int accumulate, float2 zeros) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const unsigned lane = lane_id(), wib = threadIdx.x >> 5;
+    float4* ring = reinterpret_cast<float4*>(smem) + static_cast<size_t>(wib) * NB * 32 * 32;  // [NB][32 e][32 l]
+    const uint64_t item = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+    if (item >= n_items) return;
+    const Zs z = zs_of(zeros);
+    const uint32_t d = order[d_begin + item / chunks];
+    const uint32_t col = (static_cast<uint32_t>(item % chunks) * 32 + lane) * 4;
+    const bool active = col < dim;
+    const uint64_t eb = offsets[d], ee = offsets[d + 1];
+    const uint64_t nbatch = (ee - eb + 31) / 32;
+    float* orow = out + d * ld_out + col;
+    Acc acc = acc_load(orow, col, dim, accumulate && active);
+    const float* icol = in + col;
+    auto rec_of = [&](uint64_t b) {
+        const uint64_t e = eb + b * 32 + lane;
+        return e < ee ? __ldg(edges + e) : make_uint2(0u, 0u);
+    };
+    auto issue = [&](uint64_t b, const Edge& r) {
+        float4* slot = ring + (b % NB) * 1024;
+        const uint32_t n = static_cast<uint32_t>(min(static_cast<uint64_t>(32), ee - (eb + b * 32)));
+        for (uint32_t j = 0; j < n; ++j) {
+            const uint32_t src = __shfl_sync(0xffffffffu, r.x, j);
+            if (active) cp_async16(slot + j * 32 + lane, icol + src * ld_in);
+        }
+    };
+    Edge rec[NB];  // rec[k]: edge records of batch t + k (static indices only)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) rec[b] = rec_of(b);
+#pragma unroll
+    for (int b = 0; b < NB - 1; ++b) {
+        if (b < static_cast<int>(nbatch)) issue(b, rec[b]);
+        cp_async_commit();
+    }
+    for (uint64_t t = 0; t < nbatch; ++t) {
+        if (t + NB - 1 < nbatch) issue(t + NB - 1, rec[NB - 1]);
+        cp_async_commit();
+        cp_async_wait<NB - 1>();  // batch t has landed (this lane's copies) ...
+        __syncwarp();             // ... and every lane's
+        const float4* slot = ring + (t % NB) * 1024;
+        const uint32_t n = static_cast<uint32_t>(min(static_cast<uint64_t>(32), ee - (eb + t * 32)));
+        for (uint32_t j = 0; j < n; ++j) {
+            const float w = __uint_as_float(__shfl_sync(0xffffffffu, rec[0].y, j));
+            if (active) acc_step(acc, w, slot[j * 32 + lane], z);
+        }
+        __syncwarp();  // slot free for batch t + NB
+#pragma unroll
+        for (int k = 0; k + 1 < NB; ++k) rec[k] = rec[k + 1];
+        rec[NB - 1] = rec_of(t + NB);
+    }
+    if (active) acc_store(orow, col, dim, acc, z);
 }
 
 // Main-kernel choice for wide rows (PG_WIDE_U): 0 = k_agg_vec4<32,8>
@@ -624,10 +732,19 @@ void aggregate_det(const uint64_t* offsets, const Edge* edges, const uint32_t* o
             // flight per lane, 5 column-chunk warps per 602-wide destination
             const uint32_t chunks = (nq + 31) / 32;
             const uint64_t items = static_cast<uint64_t>(nh) * chunks;
-            k_agg_wide<32><<<grid_for(items * 32, 256), 256, 0, ss.s>>>(offsets, edges, order, d_begin, items, chunks,
-                                                                       in, ld_in, out, ld_out, dim32, accumulate,
-                                                                       kZeros);
-            PG_LAUNCH("k_agg_wide<32>");
+            constexpr size_t smem = static_cast<size_t>(kAsyncWarps) * kAsyncBatches * 32 * 32 * 16;
+            static thread_local std::vector<char> attr_set;
+            int dev = 0;
+            PG_CUDA(cudaGetDevice(&dev));
+            if (static_cast<int>(attr_set.size()) <= dev) attr_set.resize(dev + 1, 0);
+            if (!attr_set[dev]) {
+                PG_CUDA(cudaFuncSetAttribute(k_agg_wide_async<kAsyncBatches>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+                attr_set[dev] = 1;
+            }
+            k_agg_wide_async<kAsyncBatches><<<grid_for(items * 32, kAsyncWarps * 32), kAsyncWarps * 32, smem, ss.s>>>(
+                offsets, edges, order, d_begin, items, chunks, in, ld_in, out, ld_out, dim32, accumulate, kZeros);
+            PG_LAUNCH("k_agg_wide_async");
         } else if (nq > 8)
             launch_heavy_any<16>(offsets, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim32, accumulate,
                                  ss.s);
