@@ -224,7 +224,96 @@ __global__ void __launch_bounds__(256) k_agg_wide(const uint64_t* __restrict__ o
     acc_store(orow, col, dim, acc, z);
 }
 
-// Heavy wide destinations: warp per (destination, 32-float4 chunk) like
+// Heavy wide destinations (default): k_agg_wide's batch structure with a
+// plain float4 accumulator and scalar FMUL/FADD — in this form ptxas keeps
+// all U = 32 gathers of a batch in flight (154 registers, measured 8-way
+// shard hub rank 11.3 -> 4.1 ms on B200).
+__device__ __forceinline__ void acc4_scalar(float4& a, float w, const float4& x) {
+    a.x = __fadd_rn(a.x, __fmul_rn(w, x.x));
+    a.y = __fadd_rn(a.y, __fmul_rn(w, x.y));
+    a.z = __fadd_rn(a.z, __fmul_rn(w, x.z));
+    a.w = __fadd_rn(a.w, __fmul_rn(w, x.w));
+}
+
+template <int U>
+__global__ void __launch_bounds__(256) k_agg_wide_lat(const uint64_t* __restrict__ offsets,
+                                                     const Edge* __restrict__ edges,
+                                                     const uint32_t* __restrict__ order, uint32_t d_begin,
+                                                     uint64_t n_items, uint32_t chunks,
+                                                     const float* __restrict__ in, uint64_t ld_in,
+                                                     float* __restrict__ out, uint64_t ld_out, uint32_t dim,
+                                                     int accumulate, uint32_t zmask) {
+    const uint64_t item = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+    if (item >= n_items) return;
+    const unsigned lane = lane_id();
+    const uint32_t d = order[d_begin + item / chunks];
+    const uint32_t col = (static_cast<uint32_t>(item % chunks) * 32 + lane) * 4;
+    const bool active = col < dim;
+    const uint64_t eb = offsets[d], ee = offsets[d + 1];
+    float* orow = out + d * ld_out + col;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (accumulate && active) {
+        if (col + 3 < dim) acc = *reinterpret_cast<const float4*>(orow);
+        else {
+            acc.x = orow[0];
+            if (col + 1 < dim) acc.y = orow[1];
+            if (col + 2 < dim) acc.z = orow[2];
+        }
+    }
+    const float* icol = in + col;
+    Edge nxt = eb + lane < ee ? __ldg(edges + eb + lane) : make_uint2(0u, 0u);
+    for (uint64_t e0 = eb; e0 < ee; e0 += 32) {
+        const Edge cur = nxt;
+        if (e0 + 32 + lane < ee) nxt = __ldg(edges + e0 + 32 + lane);
+        const uint32_t n = static_cast<uint32_t>(min(static_cast<uint64_t>(32), ee - e0));
+        if (n == 32) {
+#pragma unroll
+            for (int s = 0; s < 32; s += U) {
+                uint32_t src[U];
+                float w[U];
+                float4 x[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    src[u] = __shfl_sync(0xffffffffu, cur.x, s + u);
+                    w[u] = __uint_as_float(__shfl_sync(0xffffffffu, cur.y, s + u));
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    x[u] = active ? ldg4(icol + src[u] * ld_in) : make_float4(0.f, 0.f, 0.f, 0.f);
+                // every multiply of the batch depends on all U loads through a
+                // mask that is zero at run time (bit-neutral): the scheduler
+                // has to issue the whole batch of gathers first
+                uint32_t all = 0;
+#pragma unroll
+                for (int u = 0; u < U; ++u) all ^= __float_as_uint(x[u].x);
+                all &= zmask;
+#pragma unroll
+                for (int u = 0; u < U; ++u) acc4_scalar(acc, __uint_as_float(__float_as_uint(w[u]) ^ all), x[u]);
+            }
+        } else {
+            for (uint32_t j = 0; j < n; ++j) {
+                const uint32_t src = __shfl_sync(0xffffffffu, cur.x, j);
+                const float w = __uint_as_float(__shfl_sync(0xffffffffu, cur.y, j));
+                const float4 x = active ? ldg4(icol + src * ld_in) : make_float4(0.f, 0.f, 0.f, 0.f);
+                acc4_scalar(acc, w, x);
+            }
+        }
+    }
+    if (!active) return;
+    acc.x = __fadd_rn(acc.x, 0.f);
+    acc.y = __fadd_rn(acc.y, 0.f);
+    acc.z = __fadd_rn(acc.z, 0.f);
+    acc.w = __fadd_rn(acc.w, 0.f);
+    if (col + 3 < dim) {
+        __stcs(reinterpret_cast<float4*>(orow), acc);
+    } else {
+        orow[0] = acc.x;
+        if (col + 1 < dim) orow[1] = acc.y;
+        if (col + 2 < dim) orow[2] = acc.z;
+    }
+}
+
+// Alternative heavy wide kernel (PG_HEAVY_WIDE=async): warp per (destination, 32-float4 chunk) like
 // k_agg_wide, but each lane stages its column of NB 32-edge batches in
 // shared memory with cp.async (LDGSTS, 16 B), so NB*32 row gathers (up to
 // 32 KB per warp) are in flight by construction; wait_group retires one batch
@@ -732,6 +821,15 @@ void aggregate_det(const uint64_t* offsets, const Edge* edges, const uint32_t* o
             // flight per lane, 5 column-chunk warps per 602-wide destination
             const uint32_t chunks = (nq + 31) / 32;
             const uint64_t items = static_cast<uint64_t>(nh) * chunks;
+            static const bool use_async = [] {
+                const char* e = std::getenv("PG_HEAVY_WIDE");
+                return e && std::string(e) == "async";
+            }();
+            if (!use_async) {
+                k_agg_wide_lat<32><<<grid_for(items * 32, 256), 256, 0, ss.s>>>(
+                    offsets, edges, order, d_begin, items, chunks, in, ld_in, out, ld_out, dim32, accumulate, 0u);
+                PG_LAUNCH("k_agg_wide_lat");
+            } else {
             constexpr size_t smem = static_cast<size_t>(kAsyncWarps) * kAsyncBatches * 32 * 32 * 16;
             static thread_local std::vector<char> attr_set;
             int dev = 0;
@@ -745,6 +843,7 @@ void aggregate_det(const uint64_t* offsets, const Edge* edges, const uint32_t* o
             k_agg_wide_async<kAsyncBatches><<<grid_for(items * 32, kAsyncWarps * 32), kAsyncWarps * 32, smem, ss.s>>>(
                 offsets, edges, order, d_begin, items, chunks, in, ld_in, out, ld_out, dim32, accumulate, kZeros);
             PG_LAUNCH("k_agg_wide_async");
+            }
         } else if (nq > 8)
             launch_heavy_any<16>(offsets, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim32, accumulate,
                                  ss.s);
