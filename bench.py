@@ -264,9 +264,17 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # PG_BENCH_BACKEND=gloo + PG_BENCH_ONE_DEVICE=1: every rank on cuda:0 —
+    # exercises the N>1 code path (shards, remap, all_gather) on one GPU
+    backend = os.environ.get("PG_BENCH_BACKEND", "nccl")
+    if os.environ.get("PG_BENCH_ONE_DEVICE") == "1":
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     cfg = CONFIGS[args.config]
     L = len(cfg["dims"])

@@ -88,8 +88,15 @@ def plan(path_offsets: list, parent_rows: list, world: int, dest_bounds: list | 
 
 
 def allgather_rows(shard, out, group=None):
-    """All-gather equal-sized padded row shards: out[world*max_rows, ...]."""
+    """All-gather equal-sized padded row shards: out[world*max_rows, ...].
+    NCCL gathers device buffers in place over NVLink; a gloo group (CPU tests,
+    single-GPU rehearsal of the N>1 path) stages CUDA tensors through host."""
     import torch.distributed as dist
 
+    if shard.is_cuda and dist.get_backend(group) != "nccl":
+        host = out.cpu()
+        dist.all_gather_into_tensor(host, shard.cpu(), group=group)
+        out.copy_(host)
+        return out
     dist.all_gather_into_tensor(out, shard, group=group)
     return out
