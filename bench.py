@@ -188,14 +188,12 @@ def run_reference(args):
     vt = R.sample_training_set(cfg["V"], train_ratio(cfg), TRAIN_SEED)
     L = len(cfg["dims"])
     items = R.backward_stage_handles(g, vt, L, sample_stride=args.sample_stride)
-    levels_rows = [len(vt)]
-    # parent rows of path i: |levels[i]|; recover from the unsampled frontiers
+    # y_grad of path i has |levels[i]| rows (the parent frontier)
     lv = R.compute_frontiers(g, vt, L)
     dims = agg_dims(cfg)
     rng = np.random.default_rng(GRAD_SEED)
     ys = [rng.uniform(-1, 1, size=(len(lv[i]), dims[i])).astype(np.float32) for i in range(L)]
     setup_s = time.time() - t0
-    del levels_rows
     threads = R.max_threads()
     bytes_step = sum(path_bytes(it["D"], it["E"], dims[i]) for i, it in enumerate(items))
     for _ in range(args.warmup):
@@ -232,7 +230,8 @@ def workload_config(cfg, args, gs):
             "f": cfg["f"], "dims": cfg["dims"], "agg_widths": agg_dims(cfg), "train_ratio": round(train_ratio(cfg), 4),
             "weights": "sym-norm", "gs": gs, "gs_strategy": "regression",
             "l2": "inputs larger than L2 (each step streams the layer-0 y_grad/x_grad, > 1 GB at reddit)",
-            "parallelism": f"dest-row shards x{args.gpus} + NCCL all_gather" if args.gpus > 1 else "1 GPU"}
+            "parallelism": (f"dest-row shards x{args.gpus} (edge-balanced) + per-path NCCL all-gather-v of y_grad rows "
+                             f"({os.environ.get('PG_ALLGATHER', 'p2p')})") if args.gpus > 1 else "1 GPU"}
 
 
 # ------------------------------------------------------------- our arm ---
@@ -302,19 +301,27 @@ def main():
     shards = pgd.plan([None] * L, parent_rows, world, dest_bounds)
     gen = torch.Generator(device=dev)
     gen.manual_seed(GRAD_SEED)
+    # PG_ALLGATHER=p2p (default): unpadded all-gather-v straight into
+    # frontier order; =padded: equal-size all_gather + remapped edge stream
+    padded = os.environ.get("PG_ALLGATHER", "p2p") == "padded"
     y_shard, y_full, x_out, rows = [], [], [], []
     for i, p in enumerate(paths):
         ld = pg.padded_ld(dims[i])
         sh = shards[i]
-        if world > 1:
+        pb, pe = sh.my_parent_rows(rank)
+        if world > 1 and padded:
             groups[i].remap_sources(sh.source_map, sh.gathered_rows)
             ys = torch.zeros((sh.max_rows, ld), dtype=torch.float32, device=dev)
-            pb, pe = sh.my_parent_rows(rank)
             ys[: pe - pb, : dims[i]].uniform_(-1, 1, generator=gen)
             y_shard.append(ys)
             y_full.append(torch.empty((sh.gathered_rows, ld), dtype=torch.float32, device=dev))
-            db, de = sh.my_dest_rows(rank)
-            rows.append((db, de))
+            rows.append(sh.my_dest_rows(rank))
+        elif world > 1:
+            yf = torch.zeros((p.P, ld), dtype=torch.float32, device=dev)
+            yf[pb:pe, : dims[i]].uniform_(-1, 1, generator=gen)
+            y_shard.append(None)
+            y_full.append(yf)
+            rows.append(sh.my_dest_rows(rank))
         else:
             yf = torch.zeros((p.P, ld), dtype=torch.float32, device=dev)
             yf[:, : dims[i]].uniform_(-1, 1, generator=gen)
@@ -329,8 +336,10 @@ def main():
         for i in range(L):
             if ev is not None:
                 ev[i][0].record(stream)
-            if world > 1:
+            if world > 1 and padded:
                 pgd.allgather_rows(y_shard[i], y_full[i])
+            elif world > 1:
+                pgd.allgatherv_rows(y_full[i], shards[i].parent_bounds, rank)
             if ev is not None:
                 ev[i][1].record(stream)
             pg.backward_aggregation(groups[i], y_full[i][:, : dims[i]], x_out[i], overwrite=True,
@@ -385,7 +394,7 @@ def main():
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9
     traffic, traffic_src = ncu_traffic()
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "frac": round(achieved / peak, 4), "traffic": traffic if world == 1 else None,
                 "kernel": f"k_agg_vec4 (path SG_{p.layer}, width {dims[dom]})",
                 "algorithmic_bytes_per_launch": dom_bytes, "avg_launch_ms": round(dom_ms, 4),
                 "peak_source": peak_src, "traffic_source": traffic_src,
@@ -483,6 +492,7 @@ def sweep(pg, torch, step, paths, dims, stream):
 
 
 def measure_e2e(pg, pgd, torch, dist, paths, groups, shards, dims, rows, world, rank, dev, steps, ep_bytes):
+    padded = os.environ.get("PG_ALLGATHER", "p2p") == "padded"
     """Same metric through the public API with HOST buffers: every step
     copies this rank's y_grad rows host->device (pinned), aggregates, and
     reads this rank's x_grad rows back. N=1: the host DenseMatrix drop-in
@@ -518,8 +528,12 @@ def measure_e2e(pg, pgd, torch, dist, paths, groups, shards, dims, rows, world, 
             yh = torch.empty((pe - pb, dims[i]), dtype=torch.float32, pin_memory=True)
             yh.uniform_(-1, 1)
             ys.append(yh)
-            yd.append(torch.zeros((sh.max_rows, ld), dtype=torch.float32, device=dev))
-            yf.append(torch.empty((sh.gathered_rows, ld), dtype=torch.float32, device=dev))
+            if padded:
+                yd.append(torch.zeros((sh.max_rows, ld), dtype=torch.float32, device=dev))
+                yf.append(torch.empty((sh.gathered_rows, ld), dtype=torch.float32, device=dev))
+            else:
+                yd.append(None)
+                yf.append(torch.zeros((p.P, ld), dtype=torch.float32, device=dev))
             xd.append(pg.empty_rows(rows[i][1] - rows[i][0], dims[i], device=dev))
             xh.append(torch.empty((rows[i][1] - rows[i][0], dims[i]), dtype=torch.float32, pin_memory=True))
             h2d += yh.numel() * 4
@@ -527,8 +541,13 @@ def measure_e2e(pg, pgd, torch, dist, paths, groups, shards, dims, rows, world, 
 
         def one():
             for i in range(L):
-                yd[i][: ys[i].shape[0], : dims[i]].copy_(ys[i], non_blocking=True)
-                pgd.allgather_rows(yd[i], yf[i])
+                if padded:
+                    yd[i][: ys[i].shape[0], : dims[i]].copy_(ys[i], non_blocking=True)
+                    pgd.allgather_rows(yd[i], yf[i])
+                else:
+                    pb, pe = shards[i].my_parent_rows(rank)
+                    yf[i][pb:pe, : dims[i]].copy_(ys[i], non_blocking=True)
+                    pgd.allgatherv_rows(yf[i], shards[i].parent_bounds, rank)
                 pg.backward_aggregation(groups[i], yf[i][:, : dims[i]], xd[i], overwrite=True, rows=rows[i])
                 xh[i].copy_(xd[i], non_blocking=True)
             torch.cuda.synchronize()
@@ -545,7 +564,7 @@ def measure_e2e(pg, pgd, torch, dist, paths, groups, shards, dims, rows, world, 
     return {"value": round(ep_bytes / sec / 1e9, 2), "unit": "GB/s", "ms_per_step": round(sec * 1e3, 3),
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": steps,
             "api": "pg_backward_aggregate_host (pinned host buffers)" if world == 1 else
-                   "H2D shard + NCCL all_gather + pg_backward_aggregate_rows + D2H shard"}
+                   "H2D shard + NCCL all-gather-v + pg_backward_aggregate_rows + D2H shard"}
 
 
 def cpu_baseline(paths, dims, args):

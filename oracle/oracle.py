@@ -643,12 +643,13 @@ class Ref:
         for i, layer in enumerate(range(L - 1, -1, -1)):
             hp = vp()
             self._check(self.L.ref_path(hg, hf, layer, C.byref(hp)))
+            # gs of the full path (train.hpp:63-64), kept for its sample
+            gs = self.L.ref_path_regression_gs(hp) if gs_list is None else gs_list[i]
             if sample_stride > 1:
                 hs = vp()
                 self._check(self.L.ref_path_sample(hp, sample_stride, C.byref(hs)))
                 self.L.ref_free_path(hp)
                 hp = hs
-            gs = self.L.ref_path_regression_gs(hp) if gs_list is None else gs_list[i]
             hgr = vp()
             self._check(self.L.ref_group(hp, 1, gs, C.byref(hgr)))
             D = C.c_uint32()
@@ -672,12 +673,12 @@ class Ref:
                 p["layer"], len(arr["dest"]), len(arr["src"]), _p(arr["dest"], u32p), _p(arr["src"], u32p),
                 _p(arr["srcpos"], u32p), _p(arr["offsets"], u64p), _p(arr["neighbors"], u32p),
                 _p(arr["weights"], f64p), C.byref(hp)))
+            gs = self.L.ref_path_regression_gs(hp) if gs_list is None else gs_list[i]
             if sample_stride > 1:
                 hs = vp()
                 self._check(self.L.ref_path_sample(hp, sample_stride, C.byref(hs)))
                 self.L.ref_free_path(hp)
                 hp = hs
-            gs = self.L.ref_path_regression_gs(hp) if gs_list is None else gs_list[i]
             hgr = vp()
             self._check(self.L.ref_group(hp, 1, gs, C.byref(hgr)))
             D = C.c_uint32()

@@ -87,6 +87,39 @@ def plan(path_offsets: list, parent_rows: list, world: int, dest_bounds: list | 
     return out
 
 
+def allgatherv_rows(full, bounds, rank, group=None):
+    """Unpadded all-gather-v in place: rank r owns rows [bounds[r],
+    bounds[r+1]) of `full` (frontier order); afterwards every rank holds all
+    rows. One grouped NCCL call (batch_isend_irecv): each rank sends its rows
+    to every peer and receives theirs straight into place, so uneven
+    edge-balanced shards cost no padding and the SpMM needs no remap."""
+    import torch.distributed as dist
+
+    world = len(bounds) - 1
+    if world == 1:
+        return full
+    if full.is_cuda and dist.get_backend(group) != "nccl":
+        host = full.cpu()
+        allgatherv_rows(host, bounds, rank, group)
+        full.copy_(host)
+        return full
+    b = [int(x) for x in bounds]
+    mine = full[b[rank]:b[rank + 1]]
+    ops = []
+    for r in range(world):
+        if r == rank:
+            continue
+        if mine.shape[0]:
+            ops.append(dist.P2POp(dist.isend, mine, r, group))
+        theirs = full[b[r]:b[r + 1]]
+        if theirs.shape[0]:
+            ops.append(dist.P2POp(dist.irecv, theirs, r, group))
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+    return full
+
+
 def allgather_rows(shard, out, group=None):
     """All-gather equal-sized padded row shards: out[world*max_rows, ...].
     NCCL gathers device buffers in place over NVLink; a gloo group (CPU tests,
