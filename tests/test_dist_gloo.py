@@ -52,6 +52,11 @@ def _worker(rank, world, port, result_q):
             pgd.allgather_rows(shard, gathered)
             # remapped edge stream reads the padded buffer in place
             assert np.array_equal(gathered.numpy()[sh.source_map], y_full)
+            # unpadded all-gather-v straight into frontier order
+            fv = torch.zeros((P, dims[i]), dtype=torch.float32)
+            fv[pb:pe] = torch.from_numpy(y_full[pb:pe])
+            pgd.allgatherv_rows(fv, sh.parent_bounds, rank)
+            assert np.array_equal(fv.numpy(), y_full)
             db, de = sh.my_dest_rows(rank)
             offs = p.offsets[db:de + 1]
             src_rows = sh.source_map[p.srcpos[p.neighbors]]  # gather folded + remapped

@@ -61,6 +61,15 @@ def _worker(rank, world, port, q):
             torch.cuda.synchronize()
             want = orc.aggregate_pull_f32(op.offsets, op.neighbors, op.weights, y[op.srcpos])[db:de]
             ok = ok and np.array_equal(x.cpu().numpy().view(np.uint32), want.view(np.uint32))
+            # the default exchange: unpadded all-gather-v, no remap
+            G.remap_sources(None, 0)
+            fv = torch.zeros((p.P, ld), dtype=torch.float32, device="cuda")
+            fv[pb:pe, : dims[i]] = torch.from_numpy(y[pb:pe]).cuda()
+            pgd.allgatherv_rows(fv, sh.parent_bounds, rank)
+            x2 = pg.empty_rows(de - db, dims[i])
+            pg.backward_aggregation(G, fv[:, : dims[i]], x2, overwrite=True, rows=(db, de))
+            torch.cuda.synchronize()
+            ok = ok and np.array_equal(x2.cpu().numpy().view(np.uint32), want.view(np.uint32))
     except Exception as e:  # pragma: no cover - reported through the queue
         q.put((rank, repr(e)))
         raise
