@@ -153,10 +153,18 @@ __global__ void __launch_bounds__(256) k_agg_vec4(const uint64_t* __restrict__ o
 #pragma unroll
         for (int u = 0; u < U; ++u) acc_step(acc, __uint_as_float(ed[u].y), x[u], z);
     }
-    for (; e < end; ++e) {
-        const Edge ed = __ldg(edges + e);
-        const float4 x = active ? ldg4(icol + ed.x * ld_in) : make_float4(0.f, 0.f, 0.f, 0.f);
-        acc_step(acc, __uint_as_float(ed.y), x, z);
+    if (e < end) {  // remainder (< U edges) as one predicated batch: all gathers in flight
+        const uint32_t n = static_cast<uint32_t>(end - e);
+        Edge ed[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) ed[u] = u < static_cast<int>(n) ? __ldg(edges + e + u) : make_uint2(0u, 0u);
+        float4 x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            x[u] = (active && u < static_cast<int>(n)) ? ldg4(icol + ed[u].x * ld_in) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (u < static_cast<int>(n)) acc_step(acc, __uint_as_float(ed[u].y), x[u], z);
     }
     acc_store(orow, col, dim, acc, z);
 }
