@@ -303,7 +303,8 @@ def main():
     gen.manual_seed(GRAD_SEED)
     # PG_ALLGATHER=p2p (default): unpadded all-gather-v straight into
     # frontier order; =padded: equal-size all_gather + remapped edge stream
-    padded = os.environ.get("PG_ALLGATHER", "p2p") == "padded"
+    xmode = os.environ.get("PG_ALLGATHER", "p2p")  # p2p | padded | bcast
+    padded = xmode == "padded"
     y_shard, y_full, x_out, rows = [], [], [], []
     for i, p in enumerate(paths):
         ld = pg.padded_ld(dims[i])
@@ -322,6 +323,8 @@ def main():
             y_shard.append(None)
             y_full.append(yf)
             rows.append(sh.my_dest_rows(rank))
+            if xmode == "bcast":
+                groups[i].set_segments(sh.parent_bounds)
         else:
             yf = torch.zeros((p.P, ld), dtype=torch.float32, device=dev)
             yf[:, : dims[i]].uniform_(-1, 1, generator=gen)
@@ -336,14 +339,27 @@ def main():
         for i in range(L):
             if ev is not None:
                 ev[i][0].record(stream)
-            if world > 1 and padded:
-                pgd.allgather_rows(y_shard[i], y_full[i])
-            elif world > 1:
-                pgd.allgatherv_rows(y_full[i], shards[i].parent_bounds, rank)
-            if ev is not None:
-                ev[i][1].record(stream)
-            pg.backward_aggregation(groups[i], y_full[i][:, : dims[i]], x_out[i], overwrite=True,
-                                    rows=rows[i] if world > 1 else None)
+            if world > 1 and xmode == "bcast":
+                # rank s's rows arrive by broadcast s (all issued async, in
+                # order); segment s's pass starts as soon as they are in —
+                # the exchange overlaps the SpMM of earlier segments
+                works = pgd.bcast_rows_async(y_full[i], shards[i].parent_bounds)
+                if ev is not None:
+                    ev[i][1].record(stream)
+                for sgi in range(world):
+                    if works[sgi] is not None:
+                        works[sgi].wait()
+                    pg.backward_aggregation(groups[i], y_full[i][:, : dims[i]], x_out[i], overwrite=(sgi == 0),
+                                            rows=rows[i], segment=sgi)
+            else:
+                if world > 1 and xmode == "padded":
+                    pgd.allgather_rows(y_shard[i], y_full[i])
+                elif world > 1:
+                    pgd.allgatherv_rows(y_full[i], shards[i].parent_bounds, rank)
+                if ev is not None:
+                    ev[i][1].record(stream)
+                pg.backward_aggregation(groups[i], y_full[i][:, : dims[i]], x_out[i], overwrite=True,
+                                        rows=rows[i] if world > 1 else None)
             if ev is not None:
                 ev[i][2].record(stream)
 
@@ -476,6 +492,28 @@ def sweep(pg, torch, step, paths, dims, stream):
                 f"{[(round(max(t), 3), round(sum(t) / len(t), 3)) for t in per]} rank-max sum="
                 f"{sum(max(t) for t in per):.3f}")
     pg.set_heavy_min_degree(None)
+    # cost of running a path as K source-segment passes (bcast exchange, H2D
+    # overlap) on one GPU, full destination range
+    for i, p in enumerate(paths):
+        y = pg.empty_rows(p.P, dims[i])
+        y.uniform_(-1, 1)
+        x = pg.empty_rows(p.D, dims[i])
+        res = []
+        for K in (1, 2, 4, 8):
+            G = pgm.group_neighbors(p, 1)
+            G.set_segments([(p.P * k) // K for k in range(K + 1)])
+            for _ in range(2):
+                for k in range(K):
+                    pg.backward_aggregation(G, y, x, overwrite=(k == 0), segment=k)
+            a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(3):
+                for k in range(K):
+                    pg.backward_aggregation(G, y, x, overwrite=(k == 0), segment=k)
+            z.record()
+            torch.cuda.synchronize()
+            res.append((K, round(a.elapsed_time(z) / 3, 3)))
+        log(f"[segments] path {i} (K, ms) = {res}")
     nbytes = paths[-1].P * dims[-1] * 4
     h = torch.empty(nbytes // 4, dtype=torch.float32, pin_memory=True)
     d = torch.empty(nbytes // 4, dtype=torch.float32, device="cuda")
@@ -492,12 +530,12 @@ def sweep(pg, torch, step, paths, dims, stream):
 
 
 def measure_e2e(pg, pgd, torch, dist, paths, groups, shards, dims, rows, world, rank, dev, steps, ep_bytes):
-    padded = os.environ.get("PG_ALLGATHER", "p2p") == "padded"
     """Same metric through the public API with HOST buffers: every step
     copies this rank's y_grad rows host->device (pinned), aggregates, and
     reads this rank's x_grad rows back. N=1: the host DenseMatrix drop-in
     (pg_backward_aggregate_host: H2D, SpMM, D2H, synchronise)."""
     L = len(paths)
+    padded = os.environ.get("PG_ALLGATHER", "p2p") == "padded"  # bcast falls back to all-gather-v here
     rng = np.random.default_rng(GRAD_SEED + 1)
     h2d = d2h = 0
     if world == 1:

@@ -185,6 +185,19 @@ int pg_path_shard_bounds(pg_path p, uint32_t world, uint32_t* bounds);
  * y_rows == new_rows); map NULL removes it. map: host u32[parent_rows]. */
 int pg_groups_remap_sources(pg_groups G, const uint32_t* map, uint64_t map_len, uint64_t new_rows);
 
+/* Source-row segments: cuts[0..nseg] (cuts[0] = 0, cuts[nseg] = input rows)
+ * split every destination's edge list by source row. Edges are sorted by
+ * source within a destination, so running segments 0..nseg-1 in order —
+ * the first with PG_AGG_OVERWRITE (or onto the caller's initial output),
+ * the rest accumulating — reproduces the serial fp32 order bit for bit.
+ * This lets compute on rows that have arrived overlap the transfer of the
+ * rest (H2D, or per-rank broadcasts in the multi-GPU exchange).
+ * cuts NULL / nseg 0 clears. */
+int pg_groups_set_segments(pg_groups G, const uint64_t* cuts, uint32_t nseg);
+int pg_backward_aggregate_segment(pg_groups G, uint32_t seg, uint32_t row_begin, uint32_t row_end,
+                                  const float* y_dev, uint64_t y_rows, uint64_t ld_in, float* x_dev,
+                                  uint64_t ld_out, uint64_t dim, unsigned flags, void* stream);
+
 /* ---------------- dense helpers of backward_epp ---------------- */
 
 /* dense_matrix.hpp:78-95 gemm_a_bt: out[n x m] = a[n x k] * b[m x k]^T */

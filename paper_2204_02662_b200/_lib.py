@@ -105,6 +105,8 @@ SIGNATURES = {
     "pg_stage_counters": [H, u64, C.c_uint, u64p],
     "pg_path_shard_bounds": [H, u32, u32p],
     "pg_groups_remap_sources": [H, u32p, u64, u64],
+    "pg_groups_set_segments": [H, u64p, u32],
+    "pg_backward_aggregate_segment": [H, u32, u32, u32, vp, u64, u64, vp, u64, u64, C.c_uint, vp],
     "pg_gemm_a_bt": [vp, u64, vp, u64, vp, u64, u64, u64, u64, vp],
     "pg_relu_backward": [vp, u64, vp, u64, vp, u64, u64, u64, vp],
     "pg_gather_rows": [vp, u64, vp, u64, vp, u64, u64, vp],

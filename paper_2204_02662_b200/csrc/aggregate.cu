@@ -122,7 +122,7 @@ __device__ __forceinline__ void acc_store(float* orow, uint32_t col, uint32_t di
 
 // LPD lanes per (destination, chunk); each lane one float4 column.
 template <int LPD, int U>
-__global__ void __launch_bounds__(256) k_agg_vec4(const uint64_t* __restrict__ offsets,
+__global__ void __launch_bounds__(256) k_agg_vec4(const uint64_t* __restrict__ ebeg, const uint64_t* __restrict__ eend,
                                                  const Edge* __restrict__ edges,
                                                  const uint32_t* __restrict__ order, uint32_t d_begin,
                                                  uint64_t n_items, uint32_t chunks,
@@ -137,8 +137,8 @@ __global__ void __launch_bounds__(256) k_agg_vec4(const uint64_t* __restrict__ o
     const uint32_t q = static_cast<uint32_t>(item % chunks) * LPD + static_cast<uint32_t>(t % LPD);
     const uint32_t col = q * 4;
     const bool active = col < dim;
-    uint64_t e = offsets[d];
-    const uint64_t end = offsets[d + 1];
+    uint64_t e = ebeg[d];
+    const uint64_t end = eend[d];
     float* orow = out + d * ld_out + col;
     Acc acc = acc_load(orow, col, dim, accumulate);
     const float* icol = in + col;
@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(256) k_agg_vec4(const uint64_t* __restrict__ o
 // are broadcast with shuffles, so each group of U row gathers waits on one
 // memory round trip instead of two.
 template <int U>
-__global__ void __launch_bounds__(256) k_agg_wide(const uint64_t* __restrict__ offsets,
+__global__ void __launch_bounds__(256) k_agg_wide(const uint64_t* __restrict__ ebeg, const uint64_t* __restrict__ eend,
                                                  const Edge* __restrict__ edges,
                                                  const uint32_t* __restrict__ order, uint32_t d_begin,
                                                  uint64_t n_items, uint32_t chunks,
@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(256) k_agg_wide(const uint64_t* __restrict__ o
     const uint32_t d = order[d_begin + item / chunks];
     const uint32_t col = (static_cast<uint32_t>(item % chunks) * 32 + lane) * 4;
     const bool active = col < dim;
-    const uint64_t eb = offsets[d], ee = offsets[d + 1];
+    const uint64_t eb = ebeg[d], ee = eend[d];
     float* orow = out + d * ld_out + col;
     Acc acc = acc_load(orow, col, dim, accumulate);
     const float* icol = in + col;
@@ -244,7 +244,7 @@ __device__ __forceinline__ void acc4_scalar(float4& a, float w, const float4& x)
 }
 
 template <int U>
-__global__ void __launch_bounds__(256) k_agg_wide_lat(const uint64_t* __restrict__ offsets,
+__global__ void __launch_bounds__(256) k_agg_wide_lat(const uint64_t* __restrict__ ebeg, const uint64_t* __restrict__ eend,
                                                      const Edge* __restrict__ edges,
                                                      const uint32_t* __restrict__ order, uint32_t d_begin,
                                                      uint64_t n_items, uint32_t chunks,
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(256) k_agg_wide_lat(const uint64_t* __restrict
     const uint32_t d = order[d_begin + item / chunks];
     const uint32_t col = (static_cast<uint32_t>(item % chunks) * 32 + lane) * 4;
     const bool active = col < dim;
-    const uint64_t eb = offsets[d], ee = offsets[d + 1];
+    const uint64_t eb = ebeg[d], ee = eend[d];
     float* orow = out + d * ld_out + col;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     if (accumulate && active) {
@@ -343,7 +343,7 @@ __device__ __forceinline__ void cp_async_wait() {
 
 template <int NB>
 __global__ void __launch_bounds__(kAsyncWarps * 32) k_agg_wide_async(
-    const uint64_t* __restrict__ offsets, const Edge* __restrict__ edges, const uint32_t* __restrict__ order,
+    const uint64_t* __restrict__ ebeg, const uint64_t* __restrict__ eend, const Edge* __restrict__ edges, const uint32_t* __restrict__ order,
     uint32_t d_begin, uint64_t n_items, uint32_t chunks, const float* __restrict__ in, uint64_t ld_in,
     float* __restrict__ out, uint64_t ld_out, uint32_t dim, int accumulate, float2 zeros) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(kAsyncWarps * 32) k_agg_wide_async(
     const uint32_t d = order[d_begin + item / chunks];
     const uint32_t col = (static_cast<uint32_t>(item % chunks) * 32 + lane) * 4;
     const bool active = col < dim;
-    const uint64_t eb = offsets[d], ee = offsets[d + 1];
+    const uint64_t eb = ebeg[d], ee = eend[d];
     const uint64_t nbatch = (ee - eb + 31) / 32;
     float* orow = out + d * ld_out + col;
     Acc acc = acc_load(orow, col, dim, accumulate && active);
@@ -412,7 +412,7 @@ int wide_unroll() {
 
 // Scalar fallback for unaligned rows (ld or base not 16-byte aligned).
 template <int U>
-__global__ void __launch_bounds__(256) k_agg_scalar(const uint64_t* __restrict__ offsets,
+__global__ void __launch_bounds__(256) k_agg_scalar(const uint64_t* __restrict__ ebeg, const uint64_t* __restrict__ eend,
                                                    const Edge* __restrict__ edges,
                                                    const uint32_t* __restrict__ order, uint32_t d_begin,
                                                    uint64_t n_items, uint32_t chunks,
@@ -425,8 +425,8 @@ __global__ void __launch_bounds__(256) k_agg_scalar(const uint64_t* __restrict__
     const uint32_t d = order[d_begin + item / chunks];
     const uint32_t col = static_cast<uint32_t>(item % chunks) * 32 + lane_id();
     const bool active = col < dim;
-    uint64_t e = offsets[d];
-    const uint64_t end = offsets[d + 1];
+    uint64_t e = ebeg[d];
+    const uint64_t end = eend[d];
     float acc = (accumulate && active) ? out[d * ld_out + col] : 0.f;
     for (; e + U <= end; e += U) {
         Edge ed[U];
@@ -498,7 +498,7 @@ constexpr size_t heavy_smem() {
 }
 
 template <int CHQ>
-__global__ void __launch_bounds__(64) k_agg_heavy(const uint64_t* __restrict__ offsets,
+__global__ void __launch_bounds__(64) k_agg_heavy(const uint64_t* __restrict__ ebeg, const uint64_t* __restrict__ eend,
                                                  const Edge* __restrict__ edges,
                                                  const uint32_t* __restrict__ order, uint32_t d_begin,
                                                  uint32_t chunks, uint32_t nq_total,
@@ -519,7 +519,7 @@ __global__ void __launch_bounds__(64) k_agg_heavy(const uint64_t* __restrict__ o
     const uint32_t q0 = c * CHQ;
     const uint32_t nqc = min(static_cast<uint32_t>(CHQ), nq_total - q0);
     const uint32_t row_bytes = nqc * 16;
-    const uint64_t eb = offsets[d], ee = offsets[d + 1];
+    const uint64_t eb = ebeg[d], ee = eend[d];
     const uint64_t ntiles = (ee - eb + T - 1) / T;
     const unsigned lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -572,7 +572,7 @@ __global__ void __launch_bounds__(64) k_agg_heavy(const uint64_t* __restrict__ o
 }
 
 template <int CHQ>
-void launch_heavy(const uint64_t* offsets, const Edge* edges, const uint32_t* order, uint32_t d_begin, uint32_t nh,
+void launch_heavy(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges, const uint32_t* order, uint32_t d_begin, uint32_t nh,
                   uint32_t nq, const float* in, uint64_t ld_in, float* out, uint64_t ld_out, uint32_t dim,
                   bool accumulate, cudaStream_t s) {
     static thread_local std::vector<char> attr_set;  // per device
@@ -586,7 +586,7 @@ void launch_heavy(const uint64_t* offsets, const Edge* edges, const uint32_t* or
         attr_set[dev] = 1;
     }
     const uint32_t chunks = (nq + CHQ - 1) / CHQ;
-    k_agg_heavy<CHQ><<<nh * chunks, 64, smem, s>>>(offsets, edges, order, d_begin, chunks, nq, in, ld_in, out,
+    k_agg_heavy<CHQ><<<nh * chunks, 64, smem, s>>>(ebeg, eend, edges, order, d_begin, chunks, nq, in, ld_in, out,
                                                    ld_out, dim, accumulate, kZeros);
     PG_LAUNCH("k_agg_heavy");
 }
@@ -604,7 +604,7 @@ __host__ __device__ constexpr int coop_T() {
 }
 
 template <int CHQ>
-__global__ void __launch_bounds__(256) k_agg_heavy_coop(const uint64_t* __restrict__ offsets,
+__global__ void __launch_bounds__(256) k_agg_heavy_coop(const uint64_t* __restrict__ ebeg, const uint64_t* __restrict__ eend,
                                                        const Edge* __restrict__ edges,
                                                        const uint32_t* __restrict__ order, uint32_t d_begin,
                                                        uint32_t chunks, uint32_t nq_total,
@@ -622,7 +622,7 @@ __global__ void __launch_bounds__(256) k_agg_heavy_coop(const uint64_t* __restri
     const uint32_t c = item % chunks;
     const uint32_t q0 = c * CHQ;
     const uint32_t nqc = min(static_cast<uint32_t>(CHQ), nq_total - q0);
-    const uint64_t eb = offsets[d], ee = offsets[d + 1];
+    const uint64_t eb = ebeg[d], ee = eend[d];
     const uint64_t ntiles = (ee - eb + T - 1) / T;
     const unsigned tid = threadIdx.x, lane = tid & 31;
 
@@ -676,7 +676,7 @@ __global__ void __launch_bounds__(256) k_agg_heavy_coop(const uint64_t* __restri
 }
 
 template <int CHQ>
-void launch_heavy_coop(const uint64_t* offsets, const Edge* edges, const uint32_t* order, uint32_t d_begin,
+void launch_heavy_coop(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges, const uint32_t* order, uint32_t d_begin,
                        uint32_t nh, uint32_t nq, const float* in, uint64_t ld_in, float* out, uint64_t ld_out,
                        uint32_t dim, bool accumulate, cudaStream_t s) {
     static thread_local std::vector<char> attr_set;
@@ -690,7 +690,7 @@ void launch_heavy_coop(const uint64_t* offsets, const Edge* edges, const uint32_
         attr_set[dev] = 1;
     }
     const uint32_t chunks = (nq + CHQ - 1) / CHQ;
-    k_agg_heavy_coop<CHQ><<<nh * chunks, 256, smem, s>>>(offsets, edges, order, d_begin, chunks, nq, in, ld_in, out,
+    k_agg_heavy_coop<CHQ><<<nh * chunks, 256, smem, s>>>(ebeg, eend, edges, order, d_begin, chunks, nq, in, ld_in, out,
                                                          ld_out, dim, accumulate, kZeros);
     PG_LAUNCH("k_agg_heavy_coop");
 }
@@ -704,13 +704,13 @@ bool heavy_use_tma() {
 }
 
 template <int CHQ>
-void launch_heavy_any(const uint64_t* offsets, const Edge* edges, const uint32_t* order, uint32_t d_begin,
+void launch_heavy_any(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges, const uint32_t* order, uint32_t d_begin,
                       uint32_t nh, uint32_t nq, const float* in, uint64_t ld_in, float* out, uint64_t ld_out,
                       uint32_t dim, bool accumulate, cudaStream_t s) {
     if (heavy_use_tma())
-        launch_heavy<CHQ>(offsets, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim, accumulate, s);
+        launch_heavy<CHQ>(ebeg, eend, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim, accumulate, s);
     else
-        launch_heavy_coop<CHQ>(offsets, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim, accumulate, s);
+        launch_heavy_coop<CHQ>(ebeg, eend, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim, accumulate, s);
 }
 
 struct SideStream {
@@ -733,11 +733,11 @@ SideStream& side_stream() {
 }
 
 template <int LPD, int U>
-void launch_vec4(const uint64_t* offsets, const Edge* edges, const uint32_t* order, uint32_t d_begin,
+void launch_vec4(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges, const uint32_t* order, uint32_t d_begin,
                  uint32_t nd, uint32_t chunks, const float* in, uint64_t ld_in, float* out, uint64_t ld_out,
                  uint32_t dim, bool accumulate, cudaStream_t s) {
     const uint64_t items = static_cast<uint64_t>(nd) * chunks;
-    k_agg_vec4<LPD, U><<<grid_for(items * LPD, 256), 256, 0, s>>>(offsets, edges, order, d_begin, items, chunks,
+    k_agg_vec4<LPD, U><<<grid_for(items * LPD, 256), 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks,
                                                                  in, ld_in, out, ld_out, dim, accumulate, kZeros);
     PG_LAUNCH("k_agg_vec4");
 }
@@ -806,7 +806,7 @@ __global__ void k_gather_rows(const float* __restrict__ src, uint64_t lds, const
 
 }  // namespace
 
-void aggregate_det(const uint64_t* offsets, const Edge* edges, const uint32_t* order, uint32_t D,
+void aggregate_det(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges, const uint32_t* order, uint32_t D,
                    uint32_t d_begin, uint32_t d_end, uint32_t n_heavy, const float* in, uint64_t ld_in,
                    float* out, uint64_t ld_out, uint64_t dim, bool accumulate, cudaStream_t s) {
     (void)D;
@@ -835,7 +835,7 @@ void aggregate_det(const uint64_t* offsets, const Edge* edges, const uint32_t* o
             }();
             if (!use_async) {
                 k_agg_wide_lat<32><<<grid_for(items * 32, 256), 256, 0, ss.s>>>(
-                    offsets, edges, order, d_begin, items, chunks, in, ld_in, out, ld_out, dim32, accumulate, 0u);
+                    ebeg, eend, edges, order, d_begin, items, chunks, in, ld_in, out, ld_out, dim32, accumulate, 0u);
                 PG_LAUNCH("k_agg_wide_lat");
             } else {
             constexpr size_t smem = static_cast<size_t>(kAsyncWarps) * kAsyncBatches * 32 * 32 * 16;
@@ -849,22 +849,22 @@ void aggregate_det(const uint64_t* offsets, const Edge* edges, const uint32_t* o
                 attr_set[dev] = 1;
             }
             k_agg_wide_async<kAsyncBatches><<<grid_for(items * 32, kAsyncWarps * 32), kAsyncWarps * 32, smem, ss.s>>>(
-                offsets, edges, order, d_begin, items, chunks, in, ld_in, out, ld_out, dim32, accumulate, kZeros);
+                ebeg, eend, edges, order, d_begin, items, chunks, in, ld_in, out, ld_out, dim32, accumulate, kZeros);
             PG_LAUNCH("k_agg_wide_async");
             }
         } else if (nq > 8)
-            launch_heavy_any<16>(offsets, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim32, accumulate,
+            launch_heavy_any<16>(ebeg, eend, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim32, accumulate,
                                  ss.s);
         else if (nq > 4)
-            launch_heavy_any<8>(offsets, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim32, accumulate,
+            launch_heavy_any<8>(ebeg, eend, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim32, accumulate,
                                 ss.s);
         else
-            launch_heavy_any<4>(offsets, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim32, accumulate,
+            launch_heavy_any<4>(ebeg, eend, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim32, accumulate,
                                 ss.s);
         PG_CUDA(cudaEventRecord(ss.join, ss.s));
         d_begin += nh;
         nd -= nh;
-        if (nd) aggregate_det(offsets, edges, order, D, d_begin, d_begin + nd, 0, in, ld_in, out, ld_out, dim,
+        if (nd) aggregate_det(ebeg, eend, edges, order, D, d_begin, d_begin + nd, 0, in, ld_in, out, ld_out, dim,
                               accumulate, s);
         PG_CUDA(cudaStreamWaitEvent(s, ss.join, 0));
         return;
@@ -872,7 +872,7 @@ void aggregate_det(const uint64_t* offsets, const Edge* edges, const uint32_t* o
     if (!vec) {
         const uint32_t chunks = (dim32 + 31) / 32;
         const uint64_t items = static_cast<uint64_t>(nd) * chunks;
-        k_agg_scalar<8><<<grid_for(items * 32, 256), 256, 0, s>>>(offsets, edges, order, d_begin, items, chunks,
+        k_agg_scalar<8><<<grid_for(items * 32, 256), 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks,
                                                                  in, ld_in, out, ld_out, dim32, accumulate);
         PG_LAUNCH("k_agg_scalar");
         return;
@@ -883,24 +883,24 @@ void aggregate_det(const uint64_t* offsets, const Edge* edges, const uint32_t* o
         const uint32_t chunks = (nq + 31) / 32;
         const uint64_t items = static_cast<uint64_t>(nd) * chunks;
         if (U == 0) {  // the round-1 kernel, for A/B
-            launch_vec4<32, 8>(offsets, edges, order, d_begin, nd, chunks, in, ld_in, out, ld_out, dim32,
+            launch_vec4<32, 8>(ebeg, eend, edges, order, d_begin, nd, chunks, in, ld_in, out, ld_out, dim32,
                                accumulate, s);
         } else if (U == 8) {
-            k_agg_wide<8><<<grid_for(items * 32, 256), 256, 0, s>>>(offsets, edges, order, d_begin, items, chunks,
+            k_agg_wide<8><<<grid_for(items * 32, 256), 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks,
                                                                    in, ld_in, out, ld_out, dim32, accumulate, kZeros);
             PG_LAUNCH("k_agg_wide");
         } else {
-            k_agg_wide<16><<<grid_for(items * 32, 256), 256, 0, s>>>(offsets, edges, order, d_begin, items, chunks,
+            k_agg_wide<16><<<grid_for(items * 32, 256), 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks,
                                                                     in, ld_in, out, ld_out, dim32, accumulate,
                                                                     kZeros);
             PG_LAUNCH("k_agg_wide");
         }
     } else if (nq > 8) {
-        launch_vec4<16, 8>(offsets, edges, order, d_begin, nd, 1, in, ld_in, out, ld_out, dim32, accumulate, s);
+        launch_vec4<16, 8>(ebeg, eend, edges, order, d_begin, nd, 1, in, ld_in, out, ld_out, dim32, accumulate, s);
     } else if (nq > 4) {
-        launch_vec4<8, 8>(offsets, edges, order, d_begin, nd, 1, in, ld_in, out, ld_out, dim32, accumulate, s);
+        launch_vec4<8, 8>(ebeg, eend, edges, order, d_begin, nd, 1, in, ld_in, out, ld_out, dim32, accumulate, s);
     } else {
-        launch_vec4<4, 8>(offsets, edges, order, d_begin, nd, 1, in, ld_in, out, ld_out, dim32, accumulate, s);
+        launch_vec4<4, 8>(ebeg, eend, edges, order, d_begin, nd, 1, in, ld_in, out, ld_out, dim32, accumulate, s);
     }
 }
 

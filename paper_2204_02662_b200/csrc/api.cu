@@ -128,7 +128,7 @@ void check_dims(uint64_t dim, uint64_t ld_in, uint64_t ld_out) {
 
 // Core launch over the grouping's base: which edge stream and which schedule.
 void run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re, const float* in, uint64_t ld_in,
-                   float* out, uint64_t ld_out, uint64_t dim, unsigned flags, cudaStream_t s) {
+                   float* out, uint64_t ld_out, uint64_t dim, unsigned flags, cudaStream_t s, int seg = -1) {
     const bool accumulate = !(flags & PG_AGG_OVERWRITE);
     DeviceGuard dg(G.device);
     if (G.path) {
@@ -140,9 +140,19 @@ void run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re, con
             PG_CUDA(cudaStreamSynchronize(lib_stream(p.device)));
             edges = p.edges_local.get();
         }
+        // edge ranges: whole lists, or source segment `seg`
+        const uint64_t* eb = p.offsets.get();
+        const uint64_t* ee = p.offsets.get() + 1;
+        uint64_t range_div = 1;
+        if (seg >= 0) {
+            eb = G.seg_bnd.get() + static_cast<uint64_t>(seg) * p.D;
+            ee = eb + p.D;
+            range_div = G.seg_cuts.size() - 1;
+        }
         if (rb == 0 && re == p.D) {
-            aggregate_det(p.offsets.get(), edges, p.order.get(), p.D, 0, p.D,
-                          p.hist.heavy(heavy_min_degree(dim, p.E)), in, ld_in, out, ld_out, dim, accumulate, s);
+            aggregate_det(eb, ee, edges, p.order.get(), p.D, 0, p.D,
+                          p.hist.heavy(heavy_min_degree(dim, p.E / range_div)), in, ld_in, out, ld_out, dim,
+                          accumulate, s);
             return;
         }
         // row range: schedule of rows [rb, re) relative to rb (cached)
@@ -156,9 +166,9 @@ void run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re, con
             rs->re = re;
             degree_order(p.offsets.get() + rb, re - rb, rs->order, lib_stream(p.device), &rs->hist);
         }
-        aggregate_det(p.offsets.get() + rb, edges, rs->order.get(), re - rb, 0, re - rb,
-                      rs->hist.heavy(heavy_min_degree(dim, rs->hist.edges)), in, ld_in, out, ld_out, dim, accumulate,
-                      s);
+        aggregate_det(eb + rb, ee + rb, edges, rs->order.get(), re - rb, 0, re - rb,
+                      rs->hist.heavy(heavy_min_degree(dim, rs->hist.edges / range_div)), in, ld_in, out, ld_out, dim,
+                      accumulate, s);
         return;
     }
     Graph& g = *G.graph;
@@ -168,7 +178,7 @@ void run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re, con
     }
     if (!G.graph_order.get() && g.n)
         degree_order(g.offsets.get(), g.n, G.graph_order, lib_stream(g.device), &G.graph_hist);
-    aggregate_det(g.offsets.get(), g.edges.get(), G.graph_order.get(), g.n, 0, g.n,
+    aggregate_det(g.offsets.get(), g.offsets.get() + 1, g.edges.get(), G.graph_order.get(), g.n, 0, g.n,
                   G.graph_hist.heavy(heavy_min_degree(dim, g.m)), in, ld_in, out, ld_out, dim, accumulate, s);
 }
 
@@ -733,6 +743,45 @@ int pg_groups_remap_sources(pg_groups h, const uint32_t* map, uint64_t map_len, 
         PG_CUDA(cudaStreamSynchronize(s));
         G.edges_remap = std::move(out);
         G.remap_rows = new_rows;
+    });
+}
+
+int pg_groups_set_segments(pg_groups h, const uint64_t* cuts, uint32_t nseg) {
+    return guard([&] {
+        Groups& G = *R_(h);
+        if (!G.path) fail(kConfig, "segments: grouping is not over an execution path");
+        Path& p = *G.path;
+        if (!cuts || nseg == 0) {
+            G.seg_cuts.clear();
+            G.seg_bnd.reset();
+            return;
+        }
+        const uint64_t rows = y_rows_of(G);
+        if (cuts[0] != 0 || cuts[nseg] != (G.edges_remap.get() ? G.remap_rows : p.P))
+            fail(kConfig, "segments: cuts must start at 0 and end at the input row count");
+        for (uint32_t k = 0; k < nseg; ++k)
+            if (cuts[k + 1] < cuts[k]) fail(kConfig, "segments: cuts must be non-decreasing");
+        (void)rows;
+        DeviceGuard dg(G.device);
+        const Edge* edges = G.edges_remap.get() ? G.edges_remap.get() : p.edges_parent.get();
+        segment_bounds(p.offsets.get(), edges, p.D, cuts, nseg, G.seg_bnd, lib_stream(G.device));
+        G.seg_cuts.assign(cuts, cuts + nseg + 1);
+    });
+}
+
+int pg_backward_aggregate_segment(pg_groups h, uint32_t seg, uint32_t row_begin, uint32_t row_end,
+                                  const float* y_dev, uint64_t y_rows, uint64_t ld_in, float* x_dev, uint64_t ld_out,
+                                  uint64_t dim, unsigned flags, void* stream) {
+    return guard([&] {
+        Groups& G = *R_(h);
+        if (!G.path) fail(kConfig, "backward_aggregate: grouping is not over an execution path");
+        if (G.seg_cuts.empty() || seg + 1 >= G.seg_cuts.size()) fail(kConfig, "segments: segment index out of range");
+        check_dims(dim, ld_in, ld_out);
+        if (y_rows != y_rows_of(G)) fail(kConfig, "backward_aggregate: y_grad rows != parent frontier size");
+        if (row_begin > row_end || row_end > G.path->D) fail(kConfig, "backward_aggregate: bad row range");
+        if (row_begin == row_end) return;
+        run_aggregate(G, true, row_begin, row_end, y_dev, ld_in, x_dev, ld_out, dim, flags,
+                      static_cast<cudaStream_t>(stream), static_cast<int>(seg));
     });
 }
 

@@ -457,6 +457,40 @@ std::unique_ptr<Path> path_extract(const Graph& g, const Frontiers& f, uint64_t 
     return p;
 }
 
+namespace {
+__global__ void k_segment_bounds(const uint64_t* __restrict__ offsets, const Edge* __restrict__ edges, uint32_t D,
+                                 const uint64_t* __restrict__ cuts, uint32_t K, uint64_t* __restrict__ bnd) {
+    const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (i >= static_cast<uint64_t>(D) * (K + 1)) return;
+    const uint32_t k = static_cast<uint32_t>(i / D), d = static_cast<uint32_t>(i % D);
+    const uint64_t b = offsets[d], e = offsets[d + 1];
+    if (k == K) {
+        bnd[i] = e;
+        return;
+    }
+    const uint64_t c = cuts[k];
+    uint64_t lo = b, hi = e;  // first edge with source row >= c
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (edges[mid].x < c) lo = mid + 1;
+        else hi = mid;
+    }
+    bnd[i] = lo;
+}
+}  // namespace
+
+void segment_bounds(const uint64_t* offsets, const Edge* edges, uint32_t D, const uint64_t* cuts_host, uint32_t K,
+                    DevBuf<uint64_t>& bnd, cudaStream_t s) {
+    bnd = DevBuf<uint64_t>(static_cast<uint64_t>(D) * (K + 1), s);
+    if (!D) return;
+    DevBuf<uint64_t> cuts(K + 1, s);
+    PG_CUDA(cudaMemcpyAsync(cuts.get(), cuts_host, (K + 1) * 8, cudaMemcpyHostToDevice, s));
+    k_segment_bounds<<<grid_for(static_cast<uint64_t>(D) * (K + 1), kThreads), kThreads, 0, s>>>(
+        offsets, edges, D, cuts.get(), K, bnd.get());
+    PG_LAUNCH("k_segment_bounds");
+    PG_CUDA(cudaStreamSynchronize(s));
+}
+
 void remap_edges(const Edge* in, uint64_t E, const uint32_t* map, Edge* out, cudaStream_t s) {
     if (E == 0) return;
     k_remap<<<grid_for(E, kThreads), kThreads, 0, s>>>(in, E, map, out);

@@ -125,7 +125,19 @@ struct Groups {
     // multi-GPU: parent rows remapped into a padded allgather layout
     DevBuf<Edge> edges_remap;
     uint64_t remap_rows = 0;
+    // source-row segments [cuts[k], cuts[k+1]) of the parent frontier:
+    // seg_bnd[k*D + d] = first edge of d with source row >= cuts[k]
+    // (k = 0..K), so segment k of d is [seg_bnd[k*D+d], seg_bnd[(k+1)*D+d]).
+    // Edges are sorted by source row within a destination, so running the
+    // segments in order as accumulate passes is exactly the serial order.
+    std::vector<uint64_t> seg_cuts;
+    DevBuf<uint64_t> seg_bnd;
 };
+
+// seg_bnd for cuts[0..K] over the path's edge stream (binary search per
+// (destination, cut)); cuts[0] = 0, cuts[K] = parent rows.
+void segment_bounds(const uint64_t* offsets, const Edge* edges, uint32_t D, const uint64_t* cuts_host, uint32_t K,
+                    DevBuf<uint64_t>& bnd, cudaStream_t s);
 
 // edges_out[e] = (map[edges_in[e].x], edges_in[e].y)
 void remap_edges(const Edge* in, uint64_t E, const uint32_t* map, Edge* out, cudaStream_t s);
@@ -155,10 +167,12 @@ void grouping_cost_dev(uint32_t D, const uint64_t* offsets_dev, uint32_t gs, uin
                        cudaStream_t s);
 
 // aggregate.hpp:56-122 Deterministic, ascending edge order per element.
-//   out[order[i]] (+)= sum_e w_e * in[edges[e].x]
+//   out[d] (+)= sum_{e in [ebeg[d], eend[d])} w_e * in[edges[e].x],  d = order[i]
+// (ebeg = offsets, eend = offsets + 1 for whole lists; source-range segments
+// pass per-destination sub-ranges)
 // The first n_heavy entries of order[d_begin..] (the high-degree prefix of
 // the degree-bucket order) run on the TMA-ring kernel concurrently.
-void aggregate_det(const uint64_t* offsets, const Edge* edges, const uint32_t* order, uint32_t D,
+void aggregate_det(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges, const uint32_t* order, uint32_t D,
                    uint32_t d_begin, uint32_t d_end, uint32_t n_heavy, const float* in, uint64_t ld_in,
                    float* out, uint64_t ld_out, uint64_t dim, bool accumulate, cudaStream_t s);
 // PG_HEAVY_MIN_DEG / pg_set_heavy_min_degree (0 disables; UINT64_MAX restores

@@ -120,6 +120,32 @@ def allgatherv_rows(full, bounds, rank, group=None):
     return full
 
 
+def bcast_rows_async(full, bounds, group=None):
+    """Per-rank broadcasts of the row shards of `full` (frontier order),
+    issued asynchronously in rank order; returns one work per rank (None when
+    complete already or empty). Waiting on work s makes the current stream
+    wait for rank s's rows only, so source segment s can be aggregated while
+    later broadcasts are still in flight."""
+    import torch.distributed as dist
+
+    b = [int(x) for x in bounds]
+    world = len(b) - 1
+    if world == 1:
+        return [None]
+    if full.is_cuda and dist.get_backend(group) != "nccl":
+        host = full.cpu()
+        for s in range(world):
+            if b[s + 1] > b[s]:
+                dist.broadcast(host[b[s]:b[s + 1]], src=s, group=group)
+        full.copy_(host)
+        return [None] * world
+    works = []
+    for s in range(world):
+        works.append(dist.broadcast(full[b[s]:b[s + 1]], src=s, group=group, async_op=True)
+                     if b[s + 1] > b[s] else None)
+    return works
+
+
 def allgather_rows(shard, out, group=None):
     """All-gather equal-sized padded row shards: out[world*max_rows, ...].
     NCCL gathers device buffers in place over NVLink; a gloo group (CPU tests,

@@ -375,6 +375,17 @@ class GroupedCsr:
         _check(_lib_().pg_groups_remap_sources(self._h, _p(m, u32p), len(m), int(new_rows)))
         self.remap_rows = int(new_rows)
 
+    def set_segments(self, cuts):
+        """Source-row segments (cuts[0] = 0 ... cuts[-1] = input rows); run
+        them in order with backward_aggregation(..., segment=k)."""
+        if cuts is None:
+            _check(_lib_().pg_groups_set_segments(self._h, None, 0))
+            self.nseg = 0
+            return
+        c = np.ascontiguousarray(cuts, np.uint64)
+        _check(_lib_().pg_groups_set_segments(self._h, _p(c, u64p), len(c) - 1))
+        self.nseg = len(c) - 1
+
     def counters(self, dim, mode=DETERMINISTIC):
         c = np.zeros(3, np.uint64)
         _check(_lib_().pg_stage_counters(self._h, dim, _flags(mode), _p(c, u64p)))
@@ -470,7 +481,7 @@ def aggregate_pull(grouped: GroupedCsr, inp, out, mode=DETERMINISTIC, counters=N
 
 
 def backward_aggregation(grouped: GroupedCsr, y_grad, x_grad, mode=DETERMINISTIC, overwrite=False, stream=None,
-                         rows=None):
+                         rows=None, segment=None):
     """The reference's timed stage engine.hpp:331-338 (gather_rows over
     src_pos_in_parent + aggregate_pull), gather folded into the edge stream.
     y_grad rows follow the parent frontier. ``rows=(b, e)`` computes only
@@ -488,6 +499,13 @@ def backward_aggregation(grouped: GroupedCsr, y_grad, x_grad, mode=DETERMINISTIC
                                                   _p(x_grad, f32p), flags, _p(c, u64p)))
         return x_grad
     _dev(y_grad, "y_grad", rows=path.P if grouped.remap_rows is None else grouped.remap_rows)
+    if segment is not None:
+        b, e = (0, path.D) if rows is None else (int(rows[0]), int(rows[1]))
+        _dev(x_grad, "x_grad", rows=e - b, cols=y_grad.shape[1])
+        _check(_lib_().pg_backward_aggregate_segment(grouped._h, int(segment), b, e, C.c_void_p(y_grad.data_ptr()),
+                                                     y_grad.shape[0], y_grad.stride(0), C.c_void_p(x_grad.data_ptr()),
+                                                     x_grad.stride(0), y_grad.shape[1], flags, _stream(stream)))
+        return x_grad
     if rows is None:
         _dev(x_grad, "x_grad", rows=path.D, cols=y_grad.shape[1])
         _check(_lib_().pg_backward_aggregate(grouped._h, C.c_void_p(y_grad.data_ptr()), y_grad.shape[0],

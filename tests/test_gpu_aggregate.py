@@ -237,6 +237,46 @@ def test_remapped_allgather_layout(pg, orc, world):
         pg.set_heavy_min_degree(None)
 
 
+@pytest.mark.parametrize("nseg", [1, 2, 3, 8])
+def test_source_segments_bit_exact(pg, orc, nseg):
+    """Segments of source rows run as successive accumulate passes must give
+    the serial order's bits (edges are sorted by source within each
+    destination), including empty segments, row ranges and heavy routing."""
+    torch = torch_mod()
+    pairs, n_pad = rmat_pairs(orc, 4096, 4096 * 8, 29)
+    vt = orc.sample_training_set(4096, 0.3, 8)
+    og, dg, F, ops, dps = build_all(pg, orc, pairs, n_pad, vt, 2)
+    rng = np.random.default_rng(nseg)
+    for dim, hmin in ((16, None), (602, None), (41, 128)):
+        pg.set_heavy_min_degree(hmin)
+        for dp, op in zip(dps, ops):
+            y = rng.uniform(-1, 1, size=(dp.P, dim)).astype(np.float32)
+            base = rng.uniform(-1, 1, size=(dp.D, dim)).astype(np.float32)
+            want0 = orc.aggregate_pull_f32(op.offsets, op.neighbors, op.weights, y[op.srcpos])
+            want1 = orc.aggregate_pull_f32(op.offsets, op.neighbors, op.weights, y[op.srcpos], out=base)
+            cuts = np.unique(np.concatenate([[0, dp.P], rng.integers(0, dp.P + 1, size=nseg - 1)]))
+            if nseg == 3:
+                cuts = np.array([0, 0, dp.P // 3, dp.P])  # an empty first segment
+            G = pg.group_neighbors(dp, 4)
+            G.set_segments(cuts)
+            yd = to_dev(y, pg.padded_ld(dim))
+            x = pg.empty_rows(dp.D, dim)
+            for k in range(len(cuts) - 1):
+                pg.backward_aggregation(G, yd, x, overwrite=(k == 0), segment=k)
+            xa = to_dev(base, pg.padded_ld(dim))
+            for k in range(len(cuts) - 1):
+                pg.backward_aggregation(G, yd, xa, segment=k)
+            b = dp.shard_bounds(2)
+            xr = pg.empty_rows(int(b[2] - b[1]), dim)
+            for k in range(len(cuts) - 1):
+                pg.backward_aggregation(G, yd, xr, overwrite=(k == 0), segment=k, rows=(b[1], b[2]))
+            torch.cuda.synchronize()
+            assert np.array_equal(bits(x.cpu().numpy()), bits(want0)), (dim, nseg)
+            assert np.array_equal(bits(xa.cpu().numpy()), bits(want1)), (dim, nseg)
+            assert np.array_equal(bits(xr.cpu().numpy()), bits(want0[b[1]:b[2]])), (dim, nseg)
+    pg.set_heavy_min_degree(None)
+
+
 def test_unit_weights_hub_heavy(pg, orc):
     """Unit weights on a hub-heavy graph: bit-exact with the fp32 reference
     even where the reference itself leaves the 1e-5 tolerance of the exact
