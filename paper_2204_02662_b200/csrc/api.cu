@@ -127,8 +127,16 @@ void check_dims(uint64_t dim, uint64_t ld_in, uint64_t ld_out) {
 }
 
 // Core launch over the grouping's base: which edge stream and which schedule.
+// Source-segment selector for run_aggregate: bounds array [(nseg+1) x D] and
+// the segment to run (seg < 0: whole edge lists).
+struct SegSel {
+    const uint64_t* bnd = nullptr;
+    int seg = -1;
+    uint32_t nseg = 1;
+};
+
 void run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re, const float* in, uint64_t ld_in,
-                   float* out, uint64_t ld_out, uint64_t dim, unsigned flags, cudaStream_t s, int seg = -1) {
+                   float* out, uint64_t ld_out, uint64_t dim, unsigned flags, cudaStream_t s, SegSel sel = {}) {
     const bool accumulate = !(flags & PG_AGG_OVERWRITE);
     DeviceGuard dg(G.device);
     if (G.path) {
@@ -144,10 +152,10 @@ void run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re, con
         const uint64_t* eb = p.offsets.get();
         const uint64_t* ee = p.offsets.get() + 1;
         uint64_t range_div = 1;
-        if (seg >= 0) {
-            eb = G.seg_bnd.get() + static_cast<uint64_t>(seg) * p.D;
+        if (sel.seg >= 0) {
+            eb = sel.bnd + static_cast<uint64_t>(sel.seg) * p.D;
             ee = eb + p.D;
-            range_div = G.seg_cuts.size() - 1;
+            range_div = sel.nseg;
         }
         if (rb == 0 && re == p.D) {
             aggregate_det(eb, ee, edges, p.order.get(), p.D, 0, p.D,
@@ -215,19 +223,43 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
     const uint64_t D = b.D;
     DevBuf<float> fin(packed ? 0 : in_rows * dim, s), din(in_rows * ld, s);
     DevBuf<float> fout(packed ? 0 : D * dim, s), dout(D * ld, s);
-    if (in_rows && dim) {
-        float* dst = packed ? din.get() : fin.get();
-        PG_CUDA(cudaMemcpyAsync(dst, in_host, in_rows * dim * 4, cudaMemcpyHostToDevice, s));
-        if (!packed) copy_rows(fin.get(), dim, din.get(), ld, in_rows, dim, s);
+    const bool big = G.path && D >= 16384 && dim * 4 * D >= (32ull << 20);
+    // Input in two source-row halves: the second half's H2D overlaps the
+    // first half's SpMM pass (source segments keep the serial fp32 order).
+    const bool split = big && parent_indexed && in_rows >= 2;
+    std::vector<uint64_t> rcut{0, in_rows};
+    if (split) {
+        rcut = {0, in_rows / 2, in_rows};
+        if (G.host_seg_rows != in_rows) {
+            segment_bounds(G.path->offsets.get(), G.path->edges_parent.get(), D, rcut.data(), 2, G.host_seg_bnd, s);
+            G.host_seg_rows = in_rows;
+        }
     }
+    CopyStream& cs = copy_stream(G.device, 16);
     if (D && dim && !(flags & PG_AGG_OVERWRITE)) {
-        float* dst = packed ? dout.get() : fout.get();
-        PG_CUDA(cudaMemcpyAsync(dst, out_host, D * dim * 4, cudaMemcpyHostToDevice, s));
+        PG_CUDA(cudaMemcpyAsync(packed ? dout.get() : fout.get(), out_host, D * dim * 4, cudaMemcpyHostToDevice, cs.s));
+        PG_CUDA(cudaEventRecord(cs.ev[0], cs.s));
+        PG_CUDA(cudaStreamWaitEvent(s, cs.ev[0], 0));
         if (!packed) copy_rows(fout.get(), dim, dout.get(), ld, D, dim, s);
     }
+    for (size_t h = 0; h + 1 < rcut.size(); ++h) {
+        const uint64_t r0 = rcut[h], r1 = rcut[h + 1];
+        if (r1 > r0 && dim) {
+            float* dst = packed ? din.get() + r0 * ld : fin.get() + r0 * dim;
+            PG_CUDA(cudaMemcpyAsync(dst, in_host + r0 * dim, (r1 - r0) * dim * 4, cudaMemcpyHostToDevice, cs.s));
+            PG_CUDA(cudaEventRecord(cs.ev[1 + h], cs.s));
+            PG_CUDA(cudaStreamWaitEvent(s, cs.ev[1 + h], 0));
+            if (!packed) copy_rows(fin.get() + r0 * dim, dim, din.get() + r0 * ld, ld, r1 - r0, dim, s);
+        }
+        if (split && h == 0)  // first half over every destination while the second half uploads
+            run_aggregate(G, parent_indexed, 0, static_cast<uint32_t>(D), din.get(), ld, dout.get(), ld, dim, flags, s,
+                          SegSel{G.host_seg_bnd.get(), 0, 2});
+    }
+    const unsigned rest_flags = split ? (flags & ~PG_AGG_OVERWRITE) : flags;
+    const SegSel rest = split ? SegSel{G.host_seg_bnd.get(), 1, 2} : SegSel{};
     // row chunks (path groupings with enough rows): overlap D2H with compute
     std::vector<uint32_t> cuts{0, static_cast<uint32_t>(D)};
-    if (G.path && D >= 16384 && dim * 4 * D >= (32ull << 20)) {
+    if (big) {
         if (G.host_chunks.empty()) {
             constexpr uint32_t R = 4;
             std::vector<uint64_t> off(D + 1);
@@ -243,13 +275,12 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
         }
         cuts = G.host_chunks;
     }
-    CopyStream& cs = copy_stream(G.device, cuts.size());
     for (size_t r = 0; r + 1 < cuts.size(); ++r) {
         const uint32_t rb = cuts[r], re = cuts[r + 1];
         if (rb == re) continue;
-        run_aggregate(G, parent_indexed, rb, re, din.get(), ld, dout.get() + rb * ld, ld, dim, flags, s);
-        PG_CUDA(cudaEventRecord(cs.ev[r], s));
-        PG_CUDA(cudaStreamWaitEvent(cs.s, cs.ev[r], 0));
+        run_aggregate(G, parent_indexed, rb, re, din.get(), ld, dout.get() + rb * ld, ld, dim, rest_flags, s, rest);
+        PG_CUDA(cudaEventRecord(cs.ev[4 + r], s));
+        PG_CUDA(cudaStreamWaitEvent(cs.s, cs.ev[4 + r], 0));
         if (!dim) continue;
         const float* src = dout.get() + rb * ld;
         if (!packed) {
@@ -781,7 +812,8 @@ int pg_backward_aggregate_segment(pg_groups h, uint32_t seg, uint32_t row_begin,
         if (row_begin > row_end || row_end > G.path->D) fail(kConfig, "backward_aggregate: bad row range");
         if (row_begin == row_end) return;
         run_aggregate(G, true, row_begin, row_end, y_dev, ld_in, x_dev, ld_out, dim, flags,
-                      static_cast<cudaStream_t>(stream), static_cast<int>(seg));
+                      static_cast<cudaStream_t>(stream),
+                      SegSel{G.seg_bnd.get(), static_cast<int>(seg), static_cast<uint32_t>(G.seg_cuts.size() - 1)});
     });
 }
 

@@ -132,6 +132,9 @@ struct Groups {
     // segments in order as accumulate passes is exactly the serial order.
     std::vector<uint64_t> seg_cuts;
     DevBuf<uint64_t> seg_bnd;
+    // the host-buffer drop-in's own two-half segmentation (H2D overlap)
+    DevBuf<uint64_t> host_seg_bnd;
+    uint64_t host_seg_rows = 0;
 };
 
 // seg_bnd for cuts[0..K] over the path's edge stream (binary search per
