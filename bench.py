@@ -249,6 +249,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="few steps, no extras (for ncu)")
     ap.add_argument("--heavy-sweep", action="store_true", help="diagnostics: heavy-kernel threshold sweep")
+    ap.add_argument("--tune-sweep", action="store_true", help="diagnostics: SpMM scheduling-knob sweep")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -365,6 +366,8 @@ def main():
 
     if args.heavy_sweep:
         sweep(pg, torch, step, paths, dims, stream)
+    if args.tune_sweep:
+        tune_sweep(pg, torch, step, L)
     for _ in range(max(args.warmup, 1)):
         step()
     torch.cuda.synchronize()
@@ -447,6 +450,28 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def time_steps(torch, step, L, reps=10):
+    for _ in range(3):
+        step()
+    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(L)] for _ in range(reps)]
+    for k in range(reps):
+        step(evs[k])
+    torch.cuda.synchronize()
+    return [statistics.mean(evs[k][i][1].elapsed_time(evs[k][i][2]) for k in range(reps)) for i in range(L)]
+
+
+def tune_sweep(pg, torch, step, L):
+    """Diagnostics (stderr): per-path kernel ms for each SpMM scheduling
+    knob combination (results are bit-identical across all of them)."""
+    for vu, cm in [(4, 0), (4, 1), (8, 0), (8, 1), (16, 1), (8, 1), (8, 0), (4, 1), (4, 0)]:
+            pg.set_tuning("vec_u", vu)
+            pg.set_tuning("chunk_major", cm)
+            ms = time_steps(torch, step, L, reps=30)
+            log(f"[tune] vec_u={vu} chunk_major={cm} per-path ms={[round(x, 3) for x in ms]} total={sum(ms):.3f}")
+    pg.set_tuning("vec_u")
+    pg.set_tuning("chunk_major")
 
 
 def sweep(pg, torch, step, paths, dims, stream):

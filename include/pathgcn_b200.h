@@ -63,6 +63,13 @@ int pg_device_count(int* count);
  * (default, or $PG_HEAVY_MIN_DEG) = width dependent: 4096 for rows of <= 32
  * floats, off for wider rows. */
 int pg_set_heavy_min_degree(uint64_t min_degree);
+/* Other SpMM scheduling knobs (never change results), by name: "vec_u"
+ * (edges per gather batch: 4, 8, 16), "chunk_major" (0/1: column-chunk-major
+ * item order for rows wider than 128 floats), "wide_u" (0 = k_agg_vec4 for
+ * wide rows, 8/16 = the shuffle-broadcast k_agg_wide<U>). A negative value
+ * restores the default ($PG_<KEY> at load, else built-in). Unknown key ->
+ * PG_ERR_CONFIG. */
+int pg_set_tuning(const char* key, int64_t value);
 
 /* ---------------- graph load ---------------- */
 

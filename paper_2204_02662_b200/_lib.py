@@ -67,6 +67,7 @@ SIGNATURES = {
     "pg_version": [],
     "pg_device_count": [C.POINTER(C.c_int)],
     "pg_set_heavy_min_degree": [u64],
+    "pg_set_tuning": [C.c_char_p, i64],
     "pg_gen_rmat": [u32, u64, f64, f64, f64, f64, u64, u32p, u32p],
     "pg_training_set_size": [u32, f64, u64p],
     "pg_sample_training_set": [u32, f64, u64, u32p],

@@ -14,11 +14,52 @@
 // adds). The gather of gradient rows (engine.hpp:334) is folded into the
 // packed edge record (src_pos_in_parent composed at path build).
 #include <algorithm>
+#include <atomic>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "pg_internal.h"
 
 namespace pg {
+
+// Scheduling knobs (pg_set_tuning / $PG_<KEY>); none changes a result bit.
+namespace {
+struct TuneKey {
+    const char* name;
+    const char* env;
+    int64_t def;
+};
+constexpr TuneKey kTuneKeys[] = {
+    {"wide_u", "PG_WIDE_U", 0},            // wide rows: 0 = k_agg_vec4<32,U>, 8/16 = k_agg_wide<U>
+    {"vec_u", "PG_VEC_U", 8},              // edges per gather batch in k_agg_vec4 (4, 8, 16)
+    {"chunk_major", "PG_CHUNK_MAJOR", 1},  // k_agg_vec4 item order for multi-chunk rows
+};
+std::atomic<int64_t> g_tune[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];
+std::once_flag g_tune_once;
+void tune_init() {
+    for (size_t i = 0; i < sizeof(kTuneKeys) / sizeof(kTuneKeys[0]); ++i) {
+        const char* e = std::getenv(kTuneKeys[i].env);
+        g_tune[i].store(e ? std::atoll(e) : kTuneKeys[i].def);
+    }
+}
+}  // namespace
+
+int64_t tuning(int key) {
+    std::call_once(g_tune_once, tune_init);
+    return g_tune[key].load(std::memory_order_relaxed);
+}
+
+bool set_tuning(const char* name, int64_t value) {
+    std::call_once(g_tune_once, tune_init);
+    for (size_t i = 0; i < sizeof(kTuneKeys) / sizeof(kTuneKeys[0]); ++i)
+        if (std::strcmp(kTuneKeys[i].name, name) == 0) {
+            g_tune[i].store(value < 0 ? kTuneKeys[i].def : value);
+            return true;
+        }
+    return false;
+}
 
 namespace {
 
@@ -120,51 +161,94 @@ __device__ __forceinline__ void acc_store(float* orow, uint32_t col, uint32_t di
     }
 }
 
-// LPD lanes per (destination, chunk); each lane one float4 column.
+// 128-bit read-only row gather at base + src * ld_bytes: one IMAD.WIDE.U32
+// per edge (the 32x32->64 multiply-add cannot overflow for ld_bytes < 2^32).
+__device__ __forceinline__ float4 ld_row(const char* base, uint32_t src, uint32_t ld_bytes) {
+    float4 r;
+    const char* p = base + static_cast<uint64_t>(src) * ld_bytes;
+    asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ Edge ld_rec(const Edge* p) {
+    Edge r;
+    asm volatile("ld.global.nc.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+    return r;
+}
+
+// A runtime-zero value that depends on all U gathered rows. Folded into the
+// -0 addend of every multiply (bit-neutral: zmask is 0 at run time), it makes
+// every FP op of the batch wait for the whole batch, so ptxas has to issue
+// all U row gathers back to back (without it, it interleaves load/use pairs
+// and a warp keeps one or two gathers in flight).
+template <int U>
+__device__ __forceinline__ Zs batch_dep(const float4 (&x)[U], const Zs& z, uint32_t zmask) {
+    uint32_t all = 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) all ^= __float_as_uint(x[u].x);
+    all &= zmask;
+    Zs r = z;
+    r.nz ^= (static_cast<unsigned long long>(all) << 32) | all;
+    return r;
+}
+
+// LPD lanes per (destination, chunk); each lane one float4 column. Per batch
+// of U edges: U edge-record loads, U row gathers (all in flight), then the
+// U ordered accumulate steps. Lanes past dim gather column 0 (in bounds,
+// discarded) so no load is predicated.
 template <int LPD, int U>
 __global__ void __launch_bounds__(256) k_agg_vec4(const uint64_t* __restrict__ ebeg, const uint64_t* __restrict__ eend,
                                                  const Edge* __restrict__ edges,
                                                  const uint32_t* __restrict__ order, uint32_t d_begin,
                                                  uint64_t n_items, uint32_t chunks,
-                                                 const float* __restrict__ in, uint64_t ld_in,
+                                                 const float* __restrict__ in, uint32_t ld_in_bytes,
                                                  float* __restrict__ out, uint64_t ld_out, uint32_t dim,
-                                                 int accumulate, float2 zeros) {
+                                                 int accumulate, float2 zeros, uint32_t zmask,
+                                                 int chunk_major) {
     const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     const uint64_t item = t / LPD;
     if (item >= n_items) return;
     const Zs z = zs_of(zeros);
-    const uint32_t d = order[d_begin + item / chunks];
-    const uint32_t q = static_cast<uint32_t>(item % chunks) * LPD + static_cast<uint32_t>(t % LPD);
+    // destination-major (the chunks of one destination on neighbouring warps)
+    // or chunk-major (one column chunk of every destination, then the next:
+    // the per-pass source working set is S x chunk bytes)
+    const uint64_t nd = n_items / chunks;
+    const uint32_t di = static_cast<uint32_t>(chunk_major ? item % nd : item / chunks);
+    const uint32_t ci = static_cast<uint32_t>(chunk_major ? item / nd : item % chunks);
+    const uint32_t d = __ldg(order + d_begin + di);
+    const uint32_t q = ci * LPD + static_cast<uint32_t>(t % LPD);
     const uint32_t col = q * 4;
     const bool active = col < dim;
-    uint64_t e = ebeg[d];
-    const uint64_t end = eend[d];
+    uint64_t e = __ldg(ebeg + d);
+    const uint64_t end = __ldg(eend + d);
+    const char* base = reinterpret_cast<const char*>(in) + (active ? col : 0u) * 4u;
+    asm("mov.b64 %0, %0;" : "+l"(base));  // per-lane 64-bit base: IMAD.WIDE adds it
     float* orow = out + d * ld_out + col;
     Acc acc = acc_load(orow, col, dim, accumulate);
-    const float* icol = in + col;
     for (; e + U <= end; e += U) {
         Edge ed[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) ed[u] = __ldg(edges + e + u);
+        for (int u = 0; u < U; ++u) ed[u] = ld_rec(edges + e + u);
         float4 x[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-            x[u] = active ? ldg4(icol + ed[u].x * ld_in) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int u = 0; u < U; ++u) x[u] = ld_row(base, ed[u].x, ld_in_bytes);
+        const Zs zz = batch_dep<U>(x, z, zmask);
 #pragma unroll
-        for (int u = 0; u < U; ++u) acc_step(acc, __uint_as_float(ed[u].y), x[u], z);
+        for (int u = 0; u < U; ++u) acc_step(acc, __uint_as_float(ed[u].y), x[u], zz);
     }
-    if (e < end) {  // remainder (< U edges) as one predicated batch: all gathers in flight
+    if (e < end) {  // remainder (< U edges) as one batch: all gathers in flight
         const uint32_t n = static_cast<uint32_t>(end - e);
         Edge ed[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) ed[u] = u < static_cast<int>(n) ? __ldg(edges + e + u) : make_uint2(0u, 0u);
+        for (int u = 0; u < U; ++u) ed[u] = ld_rec(edges + e + (u < static_cast<int>(n) ? u : n - 1));
         float4 x[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-            x[u] = (active && u < static_cast<int>(n)) ? ldg4(icol + ed[u].x * ld_in) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int u = 0; u < U; ++u) x[u] = ld_row(base, ed[u].x, ld_in_bytes);
+        const Zs zz = batch_dep<U>(x, z, zmask);
 #pragma unroll
         for (int u = 0; u < U; ++u)
-            if (u < static_cast<int>(n)) acc_step(acc, __uint_as_float(ed[u].y), x[u], z);
+            if (u < static_cast<int>(n)) acc_step(acc, __uint_as_float(ed[u].y), x[u], zz);
     }
     acc_store(orow, col, dim, acc, z);
 }
@@ -399,16 +483,10 @@ __global__ void __launch_bounds__(kAsyncWarps * 32) k_agg_wide_async(
     if (active) acc_store(orow, col, dim, acc, z);
 }
 
-// Main-kernel choice for wide rows (PG_WIDE_U): 0 = k_agg_vec4<32,8>
+// Main-kernel choice for wide rows (tuning "wide_u", PG_WIDE_U): 0 = k_agg_vec4<32,8>
 // (default; 54 registers, 4 blocks/SM — best throughput), 8/16 =
 // k_agg_wide<U>. Heavy wide destinations always use k_agg_wide<32>.
-int wide_unroll() {
-    static const int v = [] {
-        const char* e = std::getenv("PG_WIDE_U");
-        return e ? std::atoi(e) : 0;
-    }();
-    return v;
-}
+int wide_unroll() { return static_cast<int>(tuning(kTuneWideU)); }
 
 // Scalar fallback for unaligned rows (ld or base not 16-byte aligned).
 template <int U>
@@ -738,7 +816,9 @@ void launch_vec4(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges, 
                  uint32_t dim, bool accumulate, cudaStream_t s) {
     const uint64_t items = static_cast<uint64_t>(nd) * chunks;
     k_agg_vec4<LPD, U><<<grid_for(items * LPD, 256), 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks,
-                                                                 in, ld_in, out, ld_out, dim, accumulate, kZeros);
+                                                                 in, static_cast<uint32_t>(ld_in * 4), out, ld_out,
+                                                                 dim, accumulate, kZeros, 0u,
+                                                                 chunks > 1 && tuning(kTuneChunkMajor) ? 1 : 0);
     PG_LAUNCH("k_agg_vec4");
 }
 
@@ -815,7 +895,8 @@ void aggregate_det(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges
     const uint32_t dim32 = static_cast<uint32_t>(dim);
     const bool vec = (ld_in % 4 == 0) && (ld_out % 4 == 0) &&
                      (reinterpret_cast<uintptr_t>(in) % 16 == 0) &&
-                     (reinterpret_cast<uintptr_t>(out) % 16 == 0) && ld_in >= ((dim + 3) & ~3ull);
+                     (reinterpret_cast<uintptr_t>(out) % 16 == 0) && ld_in >= ((dim + 3) & ~3ull) &&
+                     ld_in < (1ull << 30);
     const uint32_t nh = vec ? std::min(n_heavy, nd) : 0;
     if (nh) {
         // heavy prefix of the degree order on a forked stream, concurrent
@@ -882,9 +963,17 @@ void aggregate_det(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges
         const int U = wide_unroll();
         const uint32_t chunks = (nq + 31) / 32;
         const uint64_t items = static_cast<uint64_t>(nd) * chunks;
-        if (U == 0) {  // the round-1 kernel, for A/B
-            launch_vec4<32, 8>(ebeg, eend, edges, order, d_begin, nd, chunks, in, ld_in, out, ld_out, dim32,
-                               accumulate, s);
+        if (U == 0) {  // the main kernel
+            const int64_t vu = tuning(kTuneVecU);
+            if (vu == 4)
+                launch_vec4<32, 4>(ebeg, eend, edges, order, d_begin, nd, chunks, in, ld_in, out, ld_out, dim32,
+                                   accumulate, s);
+            else if (vu == 16)
+                launch_vec4<32, 16>(ebeg, eend, edges, order, d_begin, nd, chunks, in, ld_in, out, ld_out, dim32,
+                                    accumulate, s);
+            else
+                launch_vec4<32, 8>(ebeg, eend, edges, order, d_begin, nd, chunks, in, ld_in, out, ld_out, dim32,
+                                   accumulate, s);
         } else if (U == 8) {
             k_agg_wide<8><<<grid_for(items * 32, 256), 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks,
                                                                    in, ld_in, out, ld_out, dim32, accumulate, kZeros);

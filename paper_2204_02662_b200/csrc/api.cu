@@ -309,6 +309,12 @@ int pg_set_heavy_min_degree(uint64_t min_degree) {
     return guard([&] { set_heavy_min_degree(min_degree); });
 }
 
+int pg_set_tuning(const char* key, int64_t value) {
+    return guard([&] {
+        if (!key || !set_tuning(key, value)) fail(kConfig, std::string("pg_set_tuning: unknown key ") + (key ? key : "(null)"));
+    });
+}
+
 int pg_device_count(int* count) {
     return guard([&] {
         int c = 0;

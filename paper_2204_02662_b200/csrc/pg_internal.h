@@ -182,6 +182,10 @@ void aggregate_det(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges
 // the width-dependent default)
 uint64_t heavy_min_degree(uint64_t dim, uint64_t range_edges);
 void set_heavy_min_degree(uint64_t v);
+// scheduling knobs of the SpMM kernels (pg_set_tuning): never change results
+enum TuneKeyId { kTuneWideU = 0, kTuneVecU = 1, kTuneChunkMajor = 2 };
+int64_t tuning(int key);
+bool set_tuning(const char* name, int64_t value);
 
 // dense_matrix.hpp:78-95 (fp32, ascending k, mul/add separately rounded, +0).
 void gemm_a_bt(const float* a, uint64_t lda, const float* b, uint64_t ldb, float* out,

@@ -559,6 +559,12 @@ def set_heavy_min_degree(min_degree=None):
     _check(_lib_().pg_set_heavy_min_degree(2**64 - 1 if min_degree is None else int(min_degree)))
 
 
+def set_tuning(key, value=None):
+    """Scheduling knob of the SpMM kernels by name ("vec_u", "chunk_major",
+    "wide_u"; None restores the default). Never changes results."""
+    _check(_lib_().pg_set_tuning(key.encode(), -1 if value is None else int(value)))
+
+
 def padded_ld(cols):
     """Device row pitch for gradient matrices: 16-B rows for narrow widths,
     whole 128-B lines (32 floats) beyond 32 columns, so every row gather is
