@@ -66,7 +66,10 @@ int pg_set_heavy_min_degree(uint64_t min_degree);
 /* Other SpMM scheduling knobs (never change results), by name: "vec_u"
  * (edges per gather batch: 4, 8, 16), "chunk_major" (0/1: column-chunk-major
  * item order for rows wider than 128 floats), "wide_u" (0 = k_agg_vec4 for
- * wide rows, 8/16 = the shuffle-broadcast k_agg_wide<U>). A negative value
+ * wide rows, 8/16 = the shuffle-broadcast k_agg_wide<U>); for the host-buffer
+ * calls "host_segs" (source-row segments uploaded and reduced in turn, 1..8),
+ * "host_chunks" (destination-row chunks of the last pass whose D2H overlaps
+ * the next chunk, 1..16) and "host_trace" (1: phase times on stderr). A negative value
  * restores the default ($PG_<KEY> at load, else built-in). Unknown key ->
  * PG_ERR_CONFIG. */
 int pg_set_tuning(const char* key, int64_t value);

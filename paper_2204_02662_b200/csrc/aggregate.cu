@@ -35,6 +35,9 @@ constexpr TuneKey kTuneKeys[] = {
     {"wide_u", "PG_WIDE_U", 0},            // wide rows: 0 = k_agg_vec4<32,U>, 8/16 = k_agg_wide<U>
     {"vec_u", "PG_VEC_U", 8},              // edges per gather batch in k_agg_vec4 (4, 8, 16)
     {"chunk_major", "PG_CHUNK_MAJOR", 1},  // k_agg_vec4 item order for multi-chunk rows
+    {"host_segs", "PG_HOST_SEGS", 3},      // host drop-in: source-row segments (H2D overlap)
+    {"host_chunks", "PG_HOST_CHUNKS", 4},  // host drop-in: row chunks of the last pass (D2H overlap)
+    {"host_trace", "PG_HOST_TRACE", 0},    // host drop-in: print phase times to stderr
 };
 std::atomic<int64_t> g_tune[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];
 std::once_flag g_tune_once;

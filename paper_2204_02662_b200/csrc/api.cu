@@ -190,27 +190,41 @@ void run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re, con
                   G.graph_hist.heavy(heavy_min_degree(dim, g.m)), in, ld_in, out, ld_out, dim, accumulate, s);
 }
 
-struct CopyStream {
-    cudaStream_t s = nullptr;
-    std::vector<cudaEvent_t> ev;
+struct CopyStreams {
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    std::vector<cudaEvent_t> ev;  // sync events
+    std::vector<cudaEvent_t> tev;  // timing events (host_trace)
 };
 
-CopyStream& copy_stream(int device, size_t nev) {
-    static std::vector<CopyStream> per_dev;
+CopyStreams& copy_streams(int device, size_t nev) {
+    static std::vector<CopyStreams> per_dev;
     if (static_cast<int>(per_dev.size()) <= device) per_dev.resize(device + 1);
-    CopyStream& c = per_dev[device];
-    if (!c.s) PG_CUDA(cudaStreamCreateWithFlags(&c.s, cudaStreamNonBlocking));
+    CopyStreams& c = per_dev[device];
+    if (!c.h2d) {
+        PG_CUDA(cudaStreamCreateWithFlags(&c.h2d, cudaStreamNonBlocking));
+        PG_CUDA(cudaStreamCreateWithFlags(&c.d2h, cudaStreamNonBlocking));
+    }
     while (c.ev.size() < nev) {
         cudaEvent_t e;
         PG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         c.ev.push_back(e);
+        PG_CUDA(cudaEventCreate(&e));
+        c.tev.push_back(e);
     }
     return c;
 }
 
-// Host buffers (row-major, ld = dim): flat H2D at full link rate, on-device
-// repack to 16-byte rows when dim % 4 != 0, SpMM in edge-balanced row chunks
-// whose D2H overlaps the next chunk's compute, synchronise.
+// Host buffers (row-major, ld = dim) through a copy/compute pipeline:
+//  * the input goes up in K source-row segments on the H2D stream (flat
+//    copies at full link rate, then an on-device repack to 16-byte rows when
+//    dim % 4 != 0); SpMM pass k (every destination, the edges whose source
+//    row lies in segment k) starts as soon as segment k is resident. Edges
+//    are sorted by source row within a destination, so running the
+//    segments in order as accumulate passes is exactly the serial fp32 order;
+//  * the last pass runs in R edge-balanced destination-row chunks, and each
+//    chunk's rows go down on the D2H stream while the next chunk computes.
+// K = tuning "host_segs" and R = "host_chunks" for path groupings above a
+// size floor (1 and 1 otherwise); "host_trace" = 1 prints phase times.
 void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_rows, uint64_t dim,
               float* out_host, unsigned flags) {
     const Base b = base_of(G);
@@ -224,74 +238,108 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
     DevBuf<float> fin(packed ? 0 : in_rows * dim, s), din(in_rows * ld, s);
     DevBuf<float> fout(packed ? 0 : D * dim, s), dout(D * ld, s);
     const bool big = G.path && D >= 16384 && dim * 4 * D >= (32ull << 20);
-    // Input in two source-row halves: the second half's H2D overlaps the
-    // first half's SpMM pass (source segments keep the serial fp32 order).
-    const bool split = big && parent_indexed && in_rows >= 2;
-    std::vector<uint64_t> rcut{0, in_rows};
-    if (split) {
-        rcut = {0, in_rows / 2, in_rows};
-        if (G.host_seg_rows != in_rows) {
-            segment_bounds(G.path->offsets.get(), G.path->edges_parent.get(), D, rcut.data(), 2, G.host_seg_bnd, s);
-            G.host_seg_rows = in_rows;
-        }
+    const uint32_t K = (big && parent_indexed && in_rows >= 4)
+                           ? static_cast<uint32_t>(std::clamp<int64_t>(tuning(kTuneHostSegs), 1, 8)) : 1;
+    const uint32_t R = big ? static_cast<uint32_t>(std::clamp<int64_t>(tuning(kTuneHostChunks), 1, 16)) : 1;
+    const bool trace = tuning(kTuneHostTrace) != 0;
+    std::vector<uint64_t> rcut(K + 1);
+    for (uint32_t k = 0; k <= K; ++k) rcut[k] = in_rows * k / K;
+    if (K > 1 && (G.host_seg_rows != in_rows || G.host_seg_k != K)) {
+        segment_bounds(G.path->offsets.get(), G.path->edges_parent.get(), static_cast<uint32_t>(D), rcut.data(), K,
+                       G.host_seg_bnd, s);
+        G.host_seg_rows = in_rows;
+        G.host_seg_k = K;
     }
-    CopyStream& cs = copy_stream(G.device, 16);
-    if (D && dim && !(flags & PG_AGG_OVERWRITE)) {
-        PG_CUDA(cudaMemcpyAsync(packed ? dout.get() : fout.get(), out_host, D * dim * 4, cudaMemcpyHostToDevice, cs.s));
-        PG_CUDA(cudaEventRecord(cs.ev[0], cs.s));
-        PG_CUDA(cudaStreamWaitEvent(s, cs.ev[0], 0));
-        if (!packed) copy_rows(fout.get(), dim, dout.get(), ld, D, dim, s);
-    }
-    for (size_t h = 0; h + 1 < rcut.size(); ++h) {
-        const uint64_t r0 = rcut[h], r1 = rcut[h + 1];
-        if (r1 > r0 && dim) {
-            float* dst = packed ? din.get() + r0 * ld : fin.get() + r0 * dim;
-            PG_CUDA(cudaMemcpyAsync(dst, in_host + r0 * dim, (r1 - r0) * dim * 4, cudaMemcpyHostToDevice, cs.s));
-            PG_CUDA(cudaEventRecord(cs.ev[1 + h], cs.s));
-            PG_CUDA(cudaStreamWaitEvent(s, cs.ev[1 + h], 0));
-            if (!packed) copy_rows(fin.get() + r0 * dim, dim, din.get() + r0 * ld, ld, r1 - r0, dim, s);
-        }
-        if (split && h == 0)  // first half over every destination while the second half uploads
-            run_aggregate(G, parent_indexed, 0, static_cast<uint32_t>(D), din.get(), ld, dout.get(), ld, dim, flags, s,
-                          SegSel{G.host_seg_bnd.get(), 0, 2});
-    }
-    const unsigned rest_flags = split ? (flags & ~PG_AGG_OVERWRITE) : flags;
-    const SegSel rest = split ? SegSel{G.host_seg_bnd.get(), 1, 2} : SegSel{};
-    // row chunks (path groupings with enough rows): overlap D2H with compute
     std::vector<uint32_t> cuts{0, static_cast<uint32_t>(D)};
-    if (big) {
-        if (G.host_chunks.empty()) {
-            constexpr uint32_t R = 4;
+    if (R > 1) {
+        if (G.host_chunks.size() != R + 1) {
             std::vector<uint64_t> off(D + 1);
             PG_CUDA(cudaMemcpyAsync(off.data(), G.path->offsets.get(), off.size() * 8, cudaMemcpyDeviceToHost, s));
             PG_CUDA(cudaStreamSynchronize(s));
-            G.host_chunks.push_back(0);
+            G.host_chunks.assign(1, 0);
             for (uint32_t r = 1; r < R; ++r) {
                 const uint64_t target = off[D] * r / R;
-                const uint32_t row = static_cast<uint32_t>(std::lower_bound(off.begin(), off.end() - 1, target) - off.begin());
+                const uint32_t row =
+                    static_cast<uint32_t>(std::lower_bound(off.begin(), off.end() - 1, target) - off.begin());
                 G.host_chunks.push_back(std::max(G.host_chunks.back(), row));
             }
             G.host_chunks.push_back(static_cast<uint32_t>(D));
         }
         cuts = G.host_chunks;
     }
+    CopyStreams& cs = copy_streams(G.device, 2 + K + 2 * R + 2);
+    size_t nt = 0;  // trace events used
+    auto mark = [&](cudaStream_t st) {
+        if (trace) PG_CUDA(cudaEventRecord(cs.tev[nt++], st));
+    };
+    std::vector<std::string> tname;
+    auto tmark = [&](cudaStream_t st, std::string name) {
+        if (!trace) return;
+        tname.push_back(std::move(name));
+        mark(st);
+    };
+    tmark(s, "start");
+    // the (h2d, d2h) streams join s's prior work
+    PG_CUDA(cudaEventRecord(cs.ev[0], s));
+    PG_CUDA(cudaStreamWaitEvent(cs.h2d, cs.ev[0], 0));
+    PG_CUDA(cudaStreamWaitEvent(cs.d2h, cs.ev[0], 0));
+    if (D && dim && !(flags & PG_AGG_OVERWRITE)) {  // accumulate: current output goes up first
+        PG_CUDA(cudaMemcpyAsync(packed ? dout.get() : fout.get(), out_host, D * dim * 4, cudaMemcpyHostToDevice,
+                                cs.h2d));
+        if (!packed) copy_rows(fout.get(), dim, dout.get(), ld, D, dim, cs.h2d);
+    }
+    for (uint32_t k = 0; k < K; ++k) {
+        const uint64_t r0 = rcut[k], r1 = rcut[k + 1];
+        if (r1 > r0 && dim) {
+            float* dst = packed ? din.get() + r0 * ld : fin.get() + r0 * dim;
+            PG_CUDA(cudaMemcpyAsync(dst, in_host + r0 * dim, (r1 - r0) * dim * 4, cudaMemcpyHostToDevice, cs.h2d));
+            if (!packed) copy_rows(fin.get() + r0 * dim, dim, din.get() + r0 * ld, ld, r1 - r0, dim, cs.h2d);
+        }
+        PG_CUDA(cudaEventRecord(cs.ev[1 + k], cs.h2d));
+        tmark(cs.h2d, "h2d" + std::to_string(k));
+    }
+    // passes 0 .. K-2 over every destination
+    for (uint32_t k = 0; k + 1 < K; ++k) {
+        PG_CUDA(cudaStreamWaitEvent(s, cs.ev[1 + k], 0));
+        run_aggregate(G, parent_indexed, 0, static_cast<uint32_t>(D), din.get(), ld, dout.get(), ld, dim,
+                      k == 0 ? flags : (flags & ~PG_AGG_OVERWRITE), s, SegSel{G.host_seg_bnd.get(), static_cast<int>(k), K});
+        tmark(s, "pass" + std::to_string(k));
+    }
+    PG_CUDA(cudaStreamWaitEvent(s, cs.ev[K], 0));
+    const unsigned last_flags = K > 1 ? (flags & ~PG_AGG_OVERWRITE) : flags;
+    const SegSel last = K > 1 ? SegSel{G.host_seg_bnd.get(), static_cast<int>(K - 1), K} : SegSel{};
     for (size_t r = 0; r + 1 < cuts.size(); ++r) {
         const uint32_t rb = cuts[r], re = cuts[r + 1];
         if (rb == re) continue;
-        run_aggregate(G, parent_indexed, rb, re, din.get(), ld, dout.get() + rb * ld, ld, dim, rest_flags, s, rest);
-        PG_CUDA(cudaEventRecord(cs.ev[4 + r], s));
-        PG_CUDA(cudaStreamWaitEvent(cs.s, cs.ev[4 + r], 0));
+        run_aggregate(G, parent_indexed, rb, re, din.get(), ld, dout.get() + rb * ld, ld, dim, last_flags, s, last);
+        PG_CUDA(cudaEventRecord(cs.ev[1 + K + r], s));
+        tmark(s, "chunk" + std::to_string(r));
+        PG_CUDA(cudaStreamWaitEvent(cs.d2h, cs.ev[1 + K + r], 0));
         if (!dim) continue;
         const float* src = dout.get() + rb * ld;
         if (!packed) {
-            copy_rows(dout.get() + rb * ld, ld, fout.get() + rb * dim, dim, re - rb, dim, cs.s);
+            copy_rows(dout.get() + rb * ld, ld, fout.get() + rb * dim, dim, re - rb, dim, cs.d2h);
             src = fout.get() + rb * dim;
         }
-        PG_CUDA(cudaMemcpyAsync(out_host + rb * dim, src, (re - rb) * dim * 4, cudaMemcpyDeviceToHost, cs.s));
+        PG_CUDA(cudaMemcpyAsync(out_host + rb * dim, src, (re - rb) * dim * 4, cudaMemcpyDeviceToHost, cs.d2h));
+        tmark(cs.d2h, "d2h" + std::to_string(r));
     }
-    PG_CUDA(cudaStreamSynchronize(cs.s));
+    // buffers are freed stream-ordered on s: s waits for both copy streams
+    PG_CUDA(cudaEventRecord(cs.ev[1 + K + R], cs.d2h));
+    PG_CUDA(cudaStreamWaitEvent(s, cs.ev[1 + K + R], 0));
     PG_CUDA(cudaStreamSynchronize(s));
-    // buffers are freed stream-ordered on s after the copies completed
+    if (trace) {
+        std::string line = "[host_trace] D=" + std::to_string(D) + " dim=" + std::to_string(dim) +
+                           " K=" + std::to_string(K) + " R=" + std::to_string(R) + ":";
+        for (size_t i = 1; i < nt; ++i) {
+            float ms = 0.f;
+            PG_CUDA(cudaEventElapsedTime(&ms, cs.tev[0], cs.tev[i]));
+            char buf[64];
+            std::snprintf(buf, sizeof(buf), " %s=%.2f", tname[i].c_str(), ms);
+            line += buf;
+        }
+        std::fprintf(stderr, "%s\n", line.c_str());
+    }
 }
 
 }  // namespace

@@ -132,9 +132,10 @@ struct Groups {
     // segments in order as accumulate passes is exactly the serial order.
     std::vector<uint64_t> seg_cuts;
     DevBuf<uint64_t> seg_bnd;
-    // the host-buffer drop-in's own two-half segmentation (H2D overlap)
+    // the host-buffer drop-in's own K-segment source split (H2D overlap)
     DevBuf<uint64_t> host_seg_bnd;
     uint64_t host_seg_rows = 0;
+    uint32_t host_seg_k = 0;
 };
 
 // seg_bnd for cuts[0..K] over the path's edge stream (binary search per
@@ -183,7 +184,14 @@ void aggregate_det(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges
 uint64_t heavy_min_degree(uint64_t dim, uint64_t range_edges);
 void set_heavy_min_degree(uint64_t v);
 // scheduling knobs of the SpMM kernels (pg_set_tuning): never change results
-enum TuneKeyId { kTuneWideU = 0, kTuneVecU = 1, kTuneChunkMajor = 2 };
+enum TuneKeyId {
+    kTuneWideU = 0,
+    kTuneVecU = 1,
+    kTuneChunkMajor = 2,
+    kTuneHostSegs = 3,
+    kTuneHostChunks = 4,
+    kTuneHostTrace = 5
+};
 int64_t tuning(int key);
 bool set_tuning(const char* name, int64_t value);
 

@@ -1,5 +1,8 @@
-"""Diagnostics: time the host-buffer drop-in (pg_backward_aggregate_host)
-per path on the Reddit-shaped workload, against the device-only kernel."""
+"""Diagnostics: the host-buffer drop-in (pg_backward_aggregate_host) on the
+Reddit-shaped workload — per-path host-call time for each pipeline shape
+(source segments K x last-pass row chunks R), a phase trace of the default,
+raw pinned copy rates (one direction and both at once), and the device-only
+kernel time for reference. Results are checked bit-equal to the device call."""
 import os
 import sys
 import time
@@ -12,7 +15,36 @@ import bench  # noqa: E402
 import paper_2204_02662_b200 as pg  # noqa: E402
 
 
+def copy_rates(nbytes=566 << 20):
+    h = torch.empty(nbytes // 4, dtype=torch.float32, pin_memory=True)
+    h2 = torch.empty(nbytes // 4, dtype=torch.float32, pin_memory=True)
+    d = torch.empty(nbytes // 4, dtype=torch.float32, device="cuda")
+    d2 = torch.empty(nbytes // 4, dtype=torch.float32, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for name, fn in [("h2d", lambda: d.copy_(h, non_blocking=True)),
+                     ("d2h", lambda: h2.copy_(d2, non_blocking=True))]:
+        fn()
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        for _ in range(5):
+            fn()
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t) / 5
+        print(f"[copy] {name}: {nbytes / dt / 1e9:.1f} GB/s ({dt * 1e3:.2f} ms)", flush=True)
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    for _ in range(5):
+        with torch.cuda.stream(s1):
+            d.copy_(h, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h2.copy_(d2, non_blocking=True)
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t) / 5
+    print(f"[copy] both directions at once: {2 * nbytes / dt / 1e9:.1f} GB/s total ({dt * 1e3:.2f} ms)", flush=True)
+
+
 def main(config="reddit"):
+    copy_rates()
     cfg = bench.CONFIGS[config]
     pairs = bench.make_pairs(cfg, pg.gen_rmat)
     vt = pg.sample_training_set(cfg["V"], bench.train_ratio(cfg), bench.TRAIN_SEED)
@@ -24,11 +56,6 @@ def main(config="reddit"):
         yh = torch.empty((p.P, dim), dtype=torch.float32, pin_memory=True).numpy()
         yh[:] = np.random.default_rng(0).uniform(-1, 1, size=yh.shape)
         xh = torch.empty((p.D, dim), dtype=torch.float32, pin_memory=True).numpy()
-        for rep in range(4):
-            t = time.perf_counter()
-            pg.backward_aggregation(G, yh, xh, overwrite=True)
-            dt = time.perf_counter() - t
-            print(f"path {i} dim {dim}: host call {dt * 1e3:.2f} ms (rep {rep})", flush=True)
         yd = pg.empty_rows(p.P, dim)
         yd.copy_(torch.from_numpy(yh))
         xd = pg.empty_rows(p.D, dim)
@@ -37,8 +64,25 @@ def main(config="reddit"):
             t = time.perf_counter()
             pg.backward_aggregation(G, yd, xd, overwrite=True)
             torch.cuda.synchronize()
-            print(f"path {i}: device call {(time.perf_counter() - t) * 1e3:.2f} ms", flush=True)
-        assert np.array_equal(xd.cpu().numpy().view(np.uint32), xh.view(np.uint32))
+            dev_ms = (time.perf_counter() - t) * 1e3
+        print(f"path {i} dim {dim}: device call {dev_ms:.2f} ms", flush=True)
+        want = xd.cpu().numpy().view(np.uint32)
+        shapes = [(2, 4)] if i == 0 else [(1, 1), (1, 4), (2, 1), (2, 4), (2, 8), (3, 4), (4, 4), (4, 8), (2, 4)]
+        for K, R in shapes:
+            pg.set_tuning("host_segs", K)
+            pg.set_tuning("host_chunks", R)
+            ts = []
+            for rep in range(4):
+                t = time.perf_counter()
+                pg.backward_aggregation(G, yh, xh, overwrite=True)
+                ts.append((time.perf_counter() - t) * 1e3)
+            assert np.array_equal(xh.view(np.uint32), want), (K, R)
+            print(f"path {i} dim {dim}: host call K={K} R={R}: {min(ts[1:]):.2f} ms (min of 3)", flush=True)
+        pg.set_tuning("host_trace", 1)
+        pg.backward_aggregation(G, yh, xh, overwrite=True)
+        pg.set_tuning("host_trace", 0)
+        pg.set_tuning("host_segs")
+        pg.set_tuning("host_chunks")
 
 
 if __name__ == "__main__":
