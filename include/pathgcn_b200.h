@@ -223,6 +223,66 @@ int pg_gather_rows(const float* src, uint64_t lds, const uint32_t* ids_dev, uint
 int pg_path_device_arrays(pg_path p, const uint32_t** dest, const uint32_t** srcpos,
                           const uint64_t** offsets);
 
+/* ---------------- the GCN chain around the aggregation (engine.hpp) ----------------
+ * Device-resident and bit-exact with the reference's f32 build. Matrices are
+ * device fp32, rows x cols with row pitch ld floats (the reference's
+ * DenseMatrix<float> is ld = cols; ld a multiple of 4 with a 16-byte-aligned
+ * base lets the SpMM use 128-bit gathers). All calls are asynchronous on
+ * `stream` except where a counter is returned. */
+typedef struct pg_mat {
+    float* data;
+    uint64_t rows, cols, ld;
+} pg_mat;
+
+/* dense_matrix.hpp:40-55 gemm (b_transposed = 0) and :78-95 gemm_a_bt
+ * (b_transposed = 1): ascending k, separately rounded, + 0 */
+int pg_gemm(pg_mat a, pg_mat b, int b_transposed, pg_mat out, void* stream);
+/* dense_matrix.hpp:57-76 gemm_at_b: out = a^T b, or with a_rows (device
+ * u32[b.rows]) out = gather_rows(a, a_rows)^T b (engine.hpp:323-324 fused) */
+int pg_gemm_at_b(pg_mat a, const uint32_t* a_rows, pg_mat b, pg_mat out, void* stream);
+/* dense_matrix.hpp:98-104 relu and :116-135 row_softmax (expf bit-exact
+ * with glibc 2.39 on FMA x86-64) */
+int pg_relu(pg_mat x, pg_mat out, void* stream);
+int pg_row_softmax(pg_mat x, pg_mat out, void* stream);
+/* engine.hpp:146-156 top_grad_from_probs: out = 0; out[v] = (probs[v] -
+ * ref[v]) / |V_t| for v in vt (device u32[k]) */
+int pg_top_grad_from_probs(pg_mat probs, pg_mat ref, const uint32_t* vt_dev, uint64_t k, pg_mat out,
+                           void* stream);
+/* aggregate.hpp:127-210 aggregate_pull_filtered (Deterministic) over a
+ * full-graph grouping: destinations outside frontier level dest_level keep
+ * their rows, sources outside src_level are skipped. counters (nullable,
+ * synchronising): {edges_traversed, groups_executed, edges_skipped,
+ * groups_skipped}. */
+int pg_aggregate_pull_filtered(pg_groups G, pg_frontiers F, uint64_t dest_level, uint64_t src_level,
+                               const float* in_dev, uint64_t in_rows, uint64_t ld_in, float* out_dev,
+                               uint64_t ld_out, uint64_t dim, unsigned flags, uint64_t* counters,
+                               void* stream);
+/* engine.hpp:114-140 forward over a full-graph grouping: per layer
+ * y[l] = pull(x_l), pre[l] = y[l] W[l], x[l] = relu(pre[l]) (softmax at the
+ * last layer); x_0 = x0 and x[l] holds X^(l+1). Arrays of `layers`. */
+int pg_forward(pg_groups graph_groups, pg_mat x0, const pg_mat* w, uint64_t layers, pg_mat* y, pg_mat* pre,
+               pg_mat* x, void* stream);
+/* engine.hpp:267-349 backward_epp: path_groups[i] groups the execution
+ * path of layer L-1-i; y/pre/w are the forward artefacts (n rows);
+ * top_grad n x dims[L-1]; w_grads[l] receives W^(l)'. gather_mode 0 = Local
+ * (compact frontier-order matrices, relu_backward fused into the SpMM
+ * epilogue unless x_grads is given), 1 = Global. x_grads (nullable, Local
+ * only): |levels[i+1]| x in_dim rows per path i. edges_per_layer (nullable):
+ * backward_edges_per_layer. Stale fingerprints / depth -> PG_ERR_CONFIG. */
+int pg_backward_epp(const pg_groups* path_groups, pg_frontiers F, uint64_t layers, const pg_mat* y,
+                    const pg_mat* pre, pg_mat top_grad, const pg_mat* w, uint64_t expected_fingerprint,
+                    int gather_mode, pg_mat* w_grads, pg_mat* x_grads, uint64_t* edges_per_layer, void* stream);
+/* engine.hpp:177-214 backward_all_active (Alg. 1) over a full-graph
+ * grouping; x_grads (nullable) n x in_dim, layer L-1 first. */
+int pg_backward_all_active(pg_groups graph_groups, uint64_t layers, const pg_mat* y, const pg_mat* pre,
+                           pg_mat top_grad, const pg_mat* w, pg_mat* w_grads, pg_mat* x_grads,
+                           uint64_t* edges_per_layer, void* stream);
+/* engine.hpp:218-257 backward_ifelse: the full-graph traversal with the
+ * frontier activity filters; edges_per_layer (nullable, synchronising). */
+int pg_backward_ifelse(pg_groups graph_groups, pg_frontiers F, uint64_t layers, const pg_mat* y,
+                       const pg_mat* pre, pg_mat top_grad, const pg_mat* w, pg_mat* w_grads, pg_mat* x_grads,
+                       uint64_t* edges_per_layer, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

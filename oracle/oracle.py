@@ -140,6 +140,14 @@ class Oracle:
         L.orc_gemm_a_bt_f32.argtypes = [f32p, C.c_uint64, C.c_uint64, f32p, C.c_uint64, f32p]
         L.orc_gemm_a_bt_f64.argtypes = [f64p, C.c_uint64, C.c_uint64, f64p, C.c_uint64, f64p]
         L.orc_relu_backward_f32.argtypes = [f32p, f32p, C.c_uint64, f32p]
+        L.orc_gemm_f32.argtypes = [f32p, C.c_uint64, C.c_uint64, f32p, C.c_uint64, f32p]
+        L.orc_gemm_at_b_f32.argtypes = [f32p, C.c_uint64, C.c_uint64, f32p, C.c_uint64, f32p]
+        L.orc_relu_f32.argtypes = [f32p, C.c_uint64, f32p]
+        L.orc_row_softmax_f32.argtypes = [f32p, C.c_uint64, C.c_uint64, f32p]
+        L.orc_top_grad_f32.argtypes = [f32p, f32p, C.c_uint64, C.c_uint64, u32p, C.c_uint64, f32p]
+        L.orc_aggregate_pull_filtered_f32.argtypes = [C.c_uint32, u64p, u32p, f64p, f32p, C.c_uint64,
+                                                      C.POINTER(C.c_uint8), C.POINTER(C.c_uint8), C.c_uint32,
+                                                      f32p, u64p]
 
     # -- inputs --
     def gen_rmat(self, n, m, a=0.45, b=0.22, c=0.22, d=0.11, seed=7):
@@ -318,6 +326,132 @@ class Oracle:
         return out
 
 
+    # -- the GCN chain (engine.hpp), compositions of the C kernels --
+    def gemm_f32(self, a, b):
+        a = np.ascontiguousarray(a, np.float32)
+        b = np.ascontiguousarray(b, np.float32)
+        out = np.empty((a.shape[0], b.shape[1]), np.float32)
+        self.L.orc_gemm_f32(_p(a, f32p), a.shape[0], a.shape[1], _p(b, f32p), b.shape[1], _p(out, f32p))
+        return out
+
+    def gemm_at_b_f32(self, a, b):
+        a = np.ascontiguousarray(a, np.float32)
+        b = np.ascontiguousarray(b, np.float32)
+        out = np.empty((a.shape[1], b.shape[1]), np.float32)
+        self.L.orc_gemm_at_b_f32(_p(a, f32p), a.shape[0], a.shape[1], _p(b, f32p), b.shape[1], _p(out, f32p))
+        return out
+
+    def relu_f32(self, x):
+        x = np.ascontiguousarray(x, np.float32)
+        out = np.empty_like(x)
+        self.L.orc_relu_f32(_p(x, f32p), x.size, _p(out, f32p))
+        return out
+
+    def row_softmax_f32(self, x):
+        x = np.ascontiguousarray(x, np.float32)
+        out = np.empty_like(x)
+        self.L.orc_row_softmax_f32(_p(x, f32p), x.shape[0], x.shape[1], _p(out, f32p))
+        return out
+
+    def top_grad_f32(self, probs, ref, vt):
+        probs = np.ascontiguousarray(probs, np.float32)
+        ref = np.ascontiguousarray(ref, np.float32)
+        vt = np.ascontiguousarray(vt, np.uint32)
+        out = np.empty_like(probs)
+        self.L.orc_top_grad_f32(_p(probs, f32p), _p(ref, f32p), probs.shape[0], probs.shape[1], _p(vt, u32p),
+                                len(vt), _p(out, f32p))
+        return out
+
+    def aggregate_pull_filtered_f32(self, offsets, nbrs, w, inp, dest_active, src_active, gs):
+        offsets = np.ascontiguousarray(offsets, np.uint64)
+        nbrs = np.ascontiguousarray(nbrs, np.uint32)
+        w = np.ascontiguousarray(w, np.float64)
+        inp = np.ascontiguousarray(inp, np.float32)
+        da = np.ascontiguousarray(dest_active, np.uint8)
+        sa = np.ascontiguousarray(src_active, np.uint8)
+        D = len(offsets) - 1
+        out = np.zeros((D, inp.shape[1]), np.float32)
+        c = np.zeros(4, np.uint64)
+        u8p = C.POINTER(C.c_uint8)
+        self.L.orc_aggregate_pull_filtered_f32(D, _p(offsets, u64p), _p(nbrs, u32p), _p(w, f64p), _p(inp, f32p),
+                                               inp.shape[1], _p(da, u8p), _p(sa, u8p), gs, _p(out, f32p),
+                                               _p(c, u64p))
+        return out, dict(edges_traversed=int(c[0]), groups_executed=int(c[1]), edges_skipped=int(c[2]),
+                         groups_skipped=int(c[3]))
+
+    def forward(self, g: Csr, x0, weights):
+        """engine.hpp:114-140 (Deterministic pull over the full graph)."""
+        x, y, pre = [np.ascontiguousarray(x0, np.float32)], [], []
+        L = len(weights)
+        for l, w in enumerate(weights):
+            yl = self.aggregate_pull_f32(g.offsets, g.neighbors, g.weights, x[-1])
+            p = self.gemm_f32(yl, w)
+            x.append(self.relu_f32(p) if l + 1 < L else self.row_softmax_f32(p))
+            y.append(yl)
+            pre.append(p)
+        return dict(x=x, y=y, pre=pre)
+
+    def backward_full(self, g: Csr, arts, top_grad, weights, levels=None, gs=1):
+        """engine.hpp:177-214 backward_all_active, or with ``levels`` (the
+        frontier arrays) :218-257 backward_ifelse. Returns (w_grads, x_grads
+        layer L-1 first, backward_edges_per_layer)."""
+        L = len(weights)
+        n = len(g.offsets) - 1
+        wg, xg, edges = [None] * L, [], []
+        gm = np.ascontiguousarray(top_grad, np.float32)
+        for l in range(L - 1, -1, -1):
+            wg[l] = self.gemm_at_b_f32(arts["y"][l], gm)
+            yg = self.gemm_a_bt_f32(gm, weights[l])
+            if levels is None:
+                x = self.aggregate_pull_f32(g.offsets, g.neighbors, g.weights, yg)
+                edges.append(int(g.offsets[-1]))
+            else:
+                da = np.zeros(n, np.uint8)
+                da[levels[L - l]] = 1
+                sa = np.zeros(n, np.uint8)
+                sa[levels[L - l - 1]] = 1
+                x, c = self.aggregate_pull_filtered_f32(g.offsets, g.neighbors, g.weights, yg, da, sa, gs)
+                edges.append(c["edges_traversed"])
+            xg.append(x)
+            if l > 0:
+                gm = self.relu_backward_f32(x, arts["pre"][l - 1])
+        return wg, xg, edges
+
+    def backward_epp(self, paths, levels, arts, top_grad, weights, gather="local"):
+        """engine.hpp:267-349 (paths[i] = SG of layer L-1-i, oracle Path
+        objects). Returns (w_grads, x_grads per path (Local), edges)."""
+        L = len(weights)
+        wg, xg, edges = [None] * L, [], []
+        if gather == "global":
+            n = top_grad.shape[0]
+            gm = np.ascontiguousarray(top_grad, np.float32)
+            for i in range(L):
+                l = L - 1 - i
+                p = paths[i]
+                wg[l] = self.gemm_at_b_f32(arts["y"][l], gm)
+                yg = self.gemm_a_bt_f32(gm, weights[l])
+                x = np.zeros((n, yg.shape[1]), np.float32)
+                # aggregate_pull_path_global (engine.hpp:352-376), Deterministic
+                xr = self.aggregate_pull_f32(p.offsets, p.src[p.neighbors], p.weights, yg)
+                x[p.dest] = xr
+                edges.append(int(p.offsets[-1]))
+                if l > 0:
+                    gm = self.relu_backward_f32(x, arts["pre"][l - 1])
+            return wg, xg, edges
+        gm = np.ascontiguousarray(top_grad[levels[0]], np.float32)
+        for i in range(L):
+            l = L - 1 - i
+            p = paths[i]
+            wg[l] = self.gemm_at_b_f32(arts["y"][l][levels[L - l - 1]], gm)
+            yg = self.gemm_a_bt_f32(gm, weights[l])
+            x = self.aggregate_pull_f32(p.offsets, p.neighbors, p.weights, yg[p.srcpos])
+            xg.append(x)
+            edges.append(int(p.offsets[-1]))
+            if l > 0:
+                gm = self.relu_backward_f32(x, arts["pre"][l - 1][levels[L - l]])
+        return wg, xg, edges
+
+
 class RefError(RuntimeError):
     def __init__(self, code, msg):
         super().__init__(msg)
@@ -382,6 +516,9 @@ class Ref:
         L.ref_epp_chain_f32.argtypes = [vp, u32p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
                                         C.c_uint64, C.c_uint32, C.c_uint32, f32p, C.POINTER(f32p),
                                         C.POINTER(f32p), C.POINTER(f32p), C.POINTER(f32p)]
+        L.ref_chain_f32.argtypes = [vp, u32p, C.c_uint64, C.c_uint64, C.c_uint64, u64p, f32p, C.POINTER(f32p),
+                                    f32p, C.c_uint32, C.c_uint32, C.c_int, C.POINTER(f32p), C.POINTER(f32p),
+                                    C.POINTER(f32p), f32p, C.POINTER(f32p), C.POINTER(f32p), u64p]
 
     def _check(self, rc):
         if rc:
@@ -696,6 +833,37 @@ class Ref:
                                                         y_grad.shape[1], None if out is None else _p(out, f32p),
                                                         int(fast), workers, C.byref(secs)))
         return secs.value, out
+
+    def chain_f32(self, g: Csr, vt, x0, weights, rmat, mode, graph_gs=4, path_gs=2):
+        """The reference's forward + top_grad_from_probs + backward variant
+        on given inputs (ref_capi.cpp ref_chain_f32). mode: 0 all-active,
+        1 ifelse, 2 epp local, 3 epp global."""
+        vt = np.ascontiguousarray(vt, np.uint32)
+        x0 = np.ascontiguousarray(x0, np.float32)
+        L = len(weights)
+        n = g.n
+        f = x0.shape[1]
+        dims = np.array([w.shape[1] for w in weights], np.uint64)
+        in_dims = [f] + dims[:-1].tolist()
+        ws = [np.ascontiguousarray(w, np.float32) for w in weights]
+        rmat = np.ascontiguousarray(rmat, np.float32)
+        y = [np.empty((n, in_dims[l]), np.float32) for l in range(L)]
+        pre = [np.empty((n, int(dims[l])), np.float32) for l in range(L)]
+        x = [np.empty((n, int(dims[l])), np.float32) for l in range(L)]
+        top = np.empty((n, int(dims[-1])), np.float32)
+        wg = [np.empty_like(w) for w in ws]
+        xg = [np.empty((n, in_dims[L - 1 - i]), np.float32) for i in range(L)] if mode == 0 else None
+        edges = np.zeros(L, np.uint64)
+        arr = lambda lst: (f32p * len(lst))(*[_p(a, f32p) for a in lst])
+        hg = self.graph_handle(g)
+        try:
+            self._check(self.L.ref_chain_f32(hg, _p(vt, u32p), len(vt), L, f, _p(dims, u64p), _p(x0, f32p), arr(ws),
+                                             _p(rmat, f32p), graph_gs, path_gs, mode, arr(y), arr(pre), arr(x),
+                                             _p(top, f32p), arr(wg), None if xg is None else arr(xg),
+                                             _p(edges, u64p)))
+        finally:
+            self.L.ref_free_graph(hg)
+        return dict(y=y, pre=pre, x=[x0] + x, top=top, w_grads=wg, x_grads=xg, edges=edges.tolist())
 
     def free_stage_handles(self, items):
         for it in items:

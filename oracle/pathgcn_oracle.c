@@ -534,3 +534,104 @@ void orc_gemm_a_bt_f64(const double* a, uint64_t n, uint64_t k, const double* b,
 void orc_relu_backward_f32(const float* grad, const float* pre, uint64_t count, float* out) {
     for (uint64_t i = 0; i < count; ++i) out[i] = pre[i] > 0.0f ? grad[i] : 0.0f;
 }
+
+/* ---- the GCN chain (engine.hpp / dense_matrix.hpp), f32 ---- */
+
+/* dense_matrix.hpp:40-55 gemm: per i, k ascending, orow[j] += a[i][k]*b[k][j]; + 0 */
+void orc_gemm_f32(const float* a, uint64_t n, uint64_t k, const float* b, uint64_t m, float* out) {
+    memset(out, 0, n * m * 4);
+    for (uint64_t i = 0; i < n; ++i) {
+        float* o = out + i * m;
+        for (uint64_t t = 0; t < k; ++t) {
+            const float aik = a[i * k + t];
+            const float* br = b + t * m;
+            for (uint64_t j = 0; j < m; ++j) o[j] += aik * br[j];
+        }
+        for (uint64_t j = 0; j < m; ++j) o[j] += 0.0f;
+    }
+}
+
+/* dense_matrix.hpp:57-76 gemm_at_b: out[i][j] = sum_k a[k][i]*b[k][j], k ascending; + 0 */
+void orc_gemm_at_b_f32(const float* a, uint64_t n, uint64_t r, const float* b, uint64_t c, float* out) {
+    memset(out, 0, r * c * 4);
+    for (uint64_t i = 0; i < r; ++i) {
+        float* o = out + i * c;
+        for (uint64_t t = 0; t < n; ++t) {
+            const float aki = a[t * r + i];
+            const float* br = b + t * c;
+            for (uint64_t j = 0; j < c; ++j) o[j] += aki * br[j];
+        }
+        for (uint64_t j = 0; j < c; ++j) o[j] += 0.0f;
+    }
+}
+
+/* dense_matrix.hpp:98-104 */
+void orc_relu_f32(const float* x, uint64_t count, float* out) {
+    for (uint64_t i = 0; i < count; ++i) out[i] = x[i] > 0.0f ? x[i] : 0.0f;
+}
+
+/* dense_matrix.hpp:116-135 row_softmax: std::max((a < b) ? b : a), expf, serial sum, divide */
+void orc_row_softmax_f32(const float* x, uint64_t rows, uint64_t cols, float* out) {
+    for (uint64_t i = 0; i < rows; ++i) {
+        const float* in = x + i * cols;
+        float* o = out + i * cols;
+        float mx = in[0];
+        for (uint64_t j = 1; j < cols; ++j) mx = (mx < in[j]) ? in[j] : mx;
+        float sum = 0.0f;
+        for (uint64_t j = 0; j < cols; ++j) {
+            o[j] = expf(in[j] - mx);
+            sum += o[j];
+        }
+        for (uint64_t j = 0; j < cols; ++j) o[j] /= sum;
+    }
+}
+
+/* engine.hpp:146-156 top_grad_from_probs */
+void orc_top_grad_f32(const float* probs, const float* ref, uint64_t n, uint64_t c, const uint32_t* vt,
+                      uint64_t k, float* out) {
+    memset(out, 0, n * c * 4);
+    const float inv = 1.0f / (float)k;
+    for (uint64_t t = 0; t < k; ++t) {
+        const uint64_t v = vt[t];
+        for (uint64_t j = 0; j < c; ++j) out[v * c + j] = (probs[v * c + j] - ref[v * c + j]) * inv;
+    }
+}
+
+/* aggregate.hpp:127-170 aggregate_pull_filtered, Deterministic branch, and
+ * its counters {edges, groups, edges_skipped, groups_skipped} (groups of a
+ * destination = ceil(deg / gs), grouping.cpp:7-27) */
+void orc_aggregate_pull_filtered_f32(uint32_t D, const uint64_t* offsets, const uint32_t* nbrs,
+                                     const double* w, const float* in, uint64_t dim,
+                                     const uint8_t* dest_active, const uint8_t* src_active, uint32_t gs,
+                                     float* out, uint64_t* counters) {
+    uint64_t edges = 0, groups = 0, eskip = 0, gskip = 0;
+    for (uint32_t v = 0; v < D; ++v) {
+        const uint64_t deg = offsets[v + 1] - offsets[v];
+        const uint64_t g = (deg + gs - 1) / gs;
+        if (!dest_active[v]) {
+            gskip += g;
+            eskip += deg;
+            continue;
+        }
+        groups += g;
+        float* o = out + (uint64_t)v * dim;
+        for (uint64_t e = offsets[v]; e < offsets[v + 1]; ++e) {
+            const uint32_t u = nbrs[e];
+            if (!src_active[u]) {
+                ++eskip;
+                continue;
+            }
+            ++edges;
+            const float we = (float)w[e];
+            const float* x = in + (uint64_t)u * dim;
+            for (uint64_t j = 0; j < dim; ++j) o[j] += we * x[j];
+        }
+        for (uint64_t j = 0; j < dim; ++j) o[j] += 0.0f;
+    }
+    if (counters) {
+        counters[0] = edges;
+        counters[1] = groups;
+        counters[2] = eskip;
+        counters[3] = gskip;
+    }
+}

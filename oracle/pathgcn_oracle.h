@@ -83,6 +83,18 @@ void orc_gemm_a_bt_f64(const double* a, uint64_t n, uint64_t k, const double* b,
                        double* out);
 void orc_relu_backward_f32(const float* grad, const float* pre, uint64_t count, float* out);
 
+/* ---- the GCN chain around the aggregation (engine.hpp), f32 ---- */
+void orc_gemm_f32(const float* a, uint64_t n, uint64_t k, const float* b, uint64_t m, float* out);
+void orc_gemm_at_b_f32(const float* a, uint64_t n, uint64_t r, const float* b, uint64_t c, float* out);
+void orc_relu_f32(const float* x, uint64_t count, float* out);
+void orc_row_softmax_f32(const float* x, uint64_t rows, uint64_t cols, float* out);
+void orc_top_grad_f32(const float* probs, const float* ref, uint64_t n, uint64_t c, const uint32_t* vt,
+                      uint64_t k, float* out);
+void orc_aggregate_pull_filtered_f32(uint32_t D, const uint64_t* offsets, const uint32_t* nbrs,
+                                     const double* w, const float* in, uint64_t dim,
+                                     const uint8_t* dest_active, const uint8_t* src_active, uint32_t gs,
+                                     float* out, uint64_t* counters);
+
 #ifdef __cplusplus
 }
 #endif

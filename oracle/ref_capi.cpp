@@ -469,4 +469,71 @@ int ref_epp_chain_f32(void* hg, const uint32_t* vt, uint64_t k, uint64_t L, uint
     });
 }
 
+// The reference's own chain on caller-given inputs: forward (engine.hpp:
+// 114-140) over group_neighbors(g, graph_gs), top_grad_from_probs
+// (:146-156), then one backward variant, mode 0 = backward_all_active
+// (:177-214), 1 = backward_ifelse (:218-257), 2 = backward_epp Local,
+// 3 = backward_epp Global (:267-349; paths grouped with path_gs, stamped
+// with path_fingerprint). Outputs: y[l] n x in_dim_l, pre[l] n x dims[l],
+// x[l] = X^(l+1) n x dims[l], top n x dims[L-1], w_grads[l], x_grads
+// (mode 0 only, nullable: n x in_dim per layer, layer L-1 first),
+// edges[L] = backward_edges_per_layer.
+int ref_chain_f32(void* hg, const uint32_t* vt, uint64_t k, uint64_t L, uint64_t f, const uint64_t* dims,
+                  const float* x0, const float* const* w, const float* rmat, uint32_t graph_gs, uint32_t path_gs,
+                  int mode, float** y_out, float** pre_out, float** x_out, float* top_out, float** wg_out,
+                  float** xg_out, uint64_t* edges) {
+    return guard([&] {
+        const CsrGraph& g = static_cast<RefGraph*>(hg)->g;
+        const TrainingSet ts = make_vt(vt, k);
+        const std::size_t c = dims[L - 1];
+        ModelParams<float> params;
+        std::size_t in_dim = f;
+        for (uint64_t l = 0; l < L; ++l) {
+            DenseMatrix<float> wl(in_dim, dims[l]);
+            std::memcpy(wl.data.data(), w[l], wl.data.size() * 4);
+            params.weights.push_back(std::move(wl));
+            in_dim = dims[l];
+        }
+        DenseMatrix<float> x(g.n, f);
+        std::memcpy(x.data.data(), x0, x.data.size() * 4);
+        DenseMatrix<float> r(g.n, c);
+        std::memcpy(r.data.data(), rmat, r.data.size() * 4);
+        WorkCounters counters;
+        const GroupedCsr grouped = group_neighbors(g.view(), graph_gs);
+        EpochArtifacts<float> arts = forward(grouped, x, params, CommitMode::Deterministic, 0, counters);
+        const DenseMatrix<float> top = top_grad_from_probs(arts.x[L], r, ts);
+        for (uint64_t l = 0; l < L; ++l) {
+            std::memcpy(y_out[l], arts.y[l].data.data(), arts.y[l].data.size() * 4);
+            std::memcpy(pre_out[l], arts.pre_act[l].data.data(), arts.pre_act[l].data.size() * 4);
+            std::memcpy(x_out[l], arts.x[l + 1].data.data(), arts.x[l + 1].data.size() * 4);
+        }
+        std::memcpy(top_out, top.data.data(), top.data.size() * 4);
+        std::vector<DenseMatrix<float>> wg;
+        if (mode == 0) {
+            std::vector<DenseMatrix<float>> xg;
+            wg = backward_all_active(grouped, arts, top, params, CommitMode::Deterministic, 0, counters, &xg);
+            if (xg_out)
+                for (uint64_t i = 0; i < L; ++i) std::memcpy(xg_out[i], xg[i].data.data(), xg[i].data.size() * 4);
+        } else {
+            const FrontierSets fr = compute_frontiers(g, ts, L);
+            if (mode == 1) {
+                wg = backward_ifelse(grouped, fr, arts, top, params, CommitMode::Deterministic, 0, counters);
+            } else {
+                auto paths = prepare_all_paths(g, fr);
+                const uint64_t stamp = path_fingerprint(g, ts, L);
+                std::vector<GroupedCsr> pg;
+                for (auto& p : paths) {
+                    p.fingerprint = stamp;
+                    pg.push_back(group_neighbors(p.view(), path_gs));
+                }
+                wg = backward_epp(paths, pg, fr, arts, top, params,
+                                  mode == 2 ? GatherMode::Local : GatherMode::Global, CommitMode::Deterministic, 0,
+                                  counters, stamp);
+            }
+        }
+        for (uint64_t l = 0; l < L; ++l) std::memcpy(wg_out[l], wg[l].data.data(), wg[l].data.size() * 4);
+        for (uint64_t i = 0; i < L; ++i) edges[i] = counters.backward_edges_per_layer[i];
+    });
+}
+
 }  // extern "C"

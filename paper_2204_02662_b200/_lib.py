@@ -61,6 +61,13 @@ vp = C.c_void_p
 H = C.c_void_p  # opaque handles
 u32, u64, i32, i64, f64 = C.c_uint32, C.c_uint64, C.c_int, C.c_int64, C.c_double
 
+class PgMat(C.Structure):
+    """pg_mat: a device fp32 matrix (rows x cols, row pitch ld floats)."""
+    _fields_ = [("data", C.c_void_p), ("rows", C.c_uint64), ("cols", C.c_uint64), ("ld", C.c_uint64)]
+
+
+matp = C.POINTER(PgMat)
+
 # every symbol of include/pathgcn_b200.h with its ctypes signature
 SIGNATURES = {
     "pg_last_error": [C.c_char_p, C.c_size_t],
@@ -112,6 +119,16 @@ SIGNATURES = {
     "pg_relu_backward": [vp, u64, vp, u64, vp, u64, u64, u64, vp],
     "pg_gather_rows": [vp, u64, vp, u64, vp, u64, u64, vp],
     "pg_path_device_arrays": [H, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)],
+    "pg_gemm": [PgMat, PgMat, i32, PgMat, vp],
+    "pg_gemm_at_b": [PgMat, vp, PgMat, PgMat, vp],
+    "pg_relu": [PgMat, PgMat, vp],
+    "pg_row_softmax": [PgMat, PgMat, vp],
+    "pg_top_grad_from_probs": [PgMat, PgMat, vp, u64, PgMat, vp],
+    "pg_aggregate_pull_filtered": [H, H, u64, u64, vp, u64, u64, vp, u64, u64, C.c_uint, u64p, vp],
+    "pg_forward": [H, PgMat, matp, u64, matp, matp, matp, vp],
+    "pg_backward_epp": [C.POINTER(H), H, u64, matp, matp, PgMat, matp, u64, i32, matp, matp, u64p, vp],
+    "pg_backward_all_active": [H, u64, matp, matp, PgMat, matp, matp, matp, u64p, vp],
+    "pg_backward_ifelse": [H, H, u64, matp, matp, PgMat, matp, matp, matp, u64p, vp],
 }
 
 

@@ -70,18 +70,6 @@ __device__ __forceinline__ float4 ldg4(const float* p) {
     return __ldg(reinterpret_cast<const float4*>(p));
 }
 
-// Volatile 128-bit read-only load: volatile asm keeps program order with the
-// (volatile) accumulate steps, so a batch of U gathers is issued before the
-// first use — the scheduler cannot trade memory-level parallelism for
-// registers.
-__device__ __forceinline__ float4 ldg4_batch(const float* p) {
-    float4 r;
-    asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];"
-                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
-                 : "l"(p));
-    return r;
-}
-
 // float4 accumulator held as two packed fp32 pairs for Blackwell's FFMA2 /
 // FADD2, with the reference's separately rounded multiply and add:
 //   p = fma.rn.f32x2(w, x, nz) with nz = -0.0 passed at RUN time, which is
@@ -196,19 +184,59 @@ __device__ __forceinline__ Zs batch_dep(const float4 (&x)[U], const Zs& z, uint3
     return r;
 }
 
+// ---- AggExt helpers (engine chains) ----
+__device__ __forceinline__ uint32_t ext_out_row(const AggExt& x, uint32_t d) {
+    return x.out_rows ? __ldg(x.out_rows + d) : d;
+}
+// relu_backward on a finished row slice (dense_matrix.hpp:107-113):
+// pre > 0 ? v : +0, element by element for the columns inside dim
+__device__ __forceinline__ float4 ext_relu(const AggExt& x, uint32_t d, uint32_t row, uint32_t col, uint32_t dim,
+                                           float4 v) {
+    if (!x.relu_pre) return v;
+    const uint32_t prow = x.pre_rows ? __ldg(x.pre_rows + d) : row;
+    const float* pr = x.relu_pre + static_cast<uint64_t>(prow) * x.ld_pre + col;
+    v.x = pr[0] > 0.f ? v.x : 0.f;
+    if (col + 1 < dim) v.y = pr[1] > 0.f ? v.y : 0.f;
+    if (col + 2 < dim) v.z = pr[2] > 0.f ? v.z : 0.f;
+    if (col + 3 < dim) v.w = pr[3] > 0.f ? v.w : 0.f;
+    return v;
+}
+__device__ __forceinline__ bool ext_dst_on(const AggExt& x, uint32_t d) {
+    return !x.dst_bits || ((__ldg(x.dst_bits + (d >> 5)) >> (d & 31)) & 1u);
+}
+__device__ __forceinline__ bool ext_src_on(const AggExt& x, uint32_t u) {
+    return (__ldg(x.src_bits + (u >> 5)) >> (u & 31)) & 1u;
+}
+// acc + 0, relu epilogue, store of the columns inside dim
+__device__ __forceinline__ void acc_store_ext(float* orow, uint32_t col, uint32_t dim, Acc a, const Zs& z,
+                                              const AggExt& x, uint32_t d, uint32_t row) {
+    if (col >= dim) return;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(a.lo) : "l"(a.lo), "l"(z.pz));
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(a.hi) : "l"(a.hi), "l"(z.pz));
+    const float2 l = unpk2(a.lo), h = unpk2(a.hi);
+    float4 v = ext_relu(x, d, row, col, dim, make_float4(l.x, l.y, h.x, h.y));
+    if (col + 3 < dim) {
+        __stcs(reinterpret_cast<float4*>(orow), v);
+    } else {
+        orow[0] = v.x;
+        if (col + 1 < dim) orow[1] = v.y;
+        if (col + 2 < dim) orow[2] = v.z;
+    }
+}
+
 // LPD lanes per (destination, chunk); each lane one float4 column. Per batch
 // of U edges: U edge-record loads, U row gathers (all in flight), then the
 // U ordered accumulate steps. Lanes past dim gather column 0 (in bounds,
 // discarded) so no load is predicated.
-template <int LPD, int U>
-__global__ void __launch_bounds__(256) k_agg_vec4(const uint64_t* __restrict__ ebeg, const uint64_t* __restrict__ eend,
+template <int LPD, int U, bool FILT>
+__global__ void __launch_bounds__(256, (U <= 8 ? 4 : 2)) k_agg_vec4(const uint64_t* __restrict__ ebeg, const uint64_t* __restrict__ eend,
                                                  const Edge* __restrict__ edges,
                                                  const uint32_t* __restrict__ order, uint32_t d_begin,
                                                  uint64_t n_items, uint32_t chunks,
                                                  const float* __restrict__ in, uint32_t ld_in_bytes,
                                                  float* __restrict__ out, uint64_t ld_out, uint32_t dim,
                                                  int accumulate, float2 zeros, uint32_t zmask,
-                                                 int chunk_major) {
+                                                 int chunk_major, AggExt ext) {
     const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     const uint64_t item = t / LPD;
     if (item >= n_items) return;
@@ -220,6 +248,7 @@ __global__ void __launch_bounds__(256) k_agg_vec4(const uint64_t* __restrict__ e
     const uint32_t di = static_cast<uint32_t>(chunk_major ? item % nd : item / chunks);
     const uint32_t ci = static_cast<uint32_t>(chunk_major ? item / nd : item % chunks);
     const uint32_t d = __ldg(order + d_begin + di);
+    if (FILT && !ext_dst_on(ext, d)) return;
     const uint32_t q = ci * LPD + static_cast<uint32_t>(t % LPD);
     const uint32_t col = q * 4;
     const bool active = col < dim;
@@ -227,7 +256,8 @@ __global__ void __launch_bounds__(256) k_agg_vec4(const uint64_t* __restrict__ e
     const uint64_t end = __ldg(eend + d);
     const char* base = reinterpret_cast<const char*>(in) + (active ? col : 0u) * 4u;
     asm("mov.b64 %0, %0;" : "+l"(base));  // per-lane 64-bit base: IMAD.WIDE adds it
-    float* orow = out + d * ld_out + col;
+    const uint32_t row = ext_out_row(ext, d);
+    float* orow = out + row * ld_out + col;
     Acc acc = acc_load(orow, col, dim, accumulate);
     for (; e + U <= end; e += U) {
         Edge ed[U];
@@ -235,7 +265,10 @@ __global__ void __launch_bounds__(256) k_agg_vec4(const uint64_t* __restrict__ e
         for (int u = 0; u < U; ++u) ed[u] = ld_rec(edges + e + u);
         float4 x[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) x[u] = ld_row(base, ed[u].x, ld_in_bytes);
+        for (int u = 0; u < U; ++u) {
+            if (FILT && !ext_src_on(ext, ed[u].x)) x[u] = make_float4(0.f, 0.f, 0.f, 0.f);  // skipped: +-0 term
+            else x[u] = ld_row(base, ed[u].x, ld_in_bytes);
+        }
         const Zs zz = batch_dep<U>(x, z, zmask);
 #pragma unroll
         for (int u = 0; u < U; ++u) acc_step(acc, __uint_as_float(ed[u].y), x[u], zz);
@@ -247,13 +280,16 @@ __global__ void __launch_bounds__(256) k_agg_vec4(const uint64_t* __restrict__ e
         for (int u = 0; u < U; ++u) ed[u] = ld_rec(edges + e + (u < static_cast<int>(n) ? u : n - 1));
         float4 x[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) x[u] = ld_row(base, ed[u].x, ld_in_bytes);
+        for (int u = 0; u < U; ++u) {
+            if (FILT && !ext_src_on(ext, ed[u].x)) x[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+            else x[u] = ld_row(base, ed[u].x, ld_in_bytes);
+        }
         const Zs zz = batch_dep<U>(x, z, zmask);
 #pragma unroll
         for (int u = 0; u < U; ++u)
             if (u < static_cast<int>(n)) acc_step(acc, __uint_as_float(ed[u].y), x[u], zz);
     }
-    acc_store(orow, col, dim, acc, z);
+    acc_store_ext(orow, col, dim, acc, z, ext, d, row);
 }
 
 // Wide rows (> 16 float4 columns): a full warp per (destination, 32-float4
@@ -337,7 +373,7 @@ __global__ void __launch_bounds__(256) k_agg_wide_lat(const uint64_t* __restrict
                                                      uint64_t n_items, uint32_t chunks,
                                                      const float* __restrict__ in, uint64_t ld_in,
                                                      float* __restrict__ out, uint64_t ld_out, uint32_t dim,
-                                                     int accumulate, uint32_t zmask) {
+                                                     int accumulate, uint32_t zmask, AggExt ext) {
     const uint64_t item = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
     if (item >= n_items) return;
     const unsigned lane = lane_id();
@@ -345,7 +381,8 @@ __global__ void __launch_bounds__(256) k_agg_wide_lat(const uint64_t* __restrict
     const uint32_t col = (static_cast<uint32_t>(item % chunks) * 32 + lane) * 4;
     const bool active = col < dim;
     const uint64_t eb = ebeg[d], ee = eend[d];
-    float* orow = out + d * ld_out + col;
+    const uint32_t row = ext_out_row(ext, d);
+    float* orow = out + row * ld_out + col;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     if (accumulate && active) {
         if (col + 3 < dim) acc = *reinterpret_cast<const float4*>(orow);
@@ -399,6 +436,7 @@ __global__ void __launch_bounds__(256) k_agg_wide_lat(const uint64_t* __restrict
     acc.y = __fadd_rn(acc.y, 0.f);
     acc.z = __fadd_rn(acc.z, 0.f);
     acc.w = __fadd_rn(acc.w, 0.f);
+    acc = ext_relu(ext, d, row, col, dim, acc);
     if (col + 3 < dim) {
         __stcs(reinterpret_cast<float4*>(orow), acc);
     } else {
@@ -499,32 +537,42 @@ __global__ void __launch_bounds__(256) k_agg_scalar(const uint64_t* __restrict__
                                                    uint64_t n_items, uint32_t chunks,
                                                    const float* __restrict__ in, uint64_t ld_in,
                                                    float* __restrict__ out, uint64_t ld_out, uint32_t dim,
-                                                   int accumulate) {
+                                                   int accumulate, AggExt ext) {
     const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     const uint64_t item = t / 32;
     if (item >= n_items) return;
     const uint32_t d = order[d_begin + item / chunks];
+    if (!ext_dst_on(ext, d)) return;
     const uint32_t col = static_cast<uint32_t>(item % chunks) * 32 + lane_id();
     const bool active = col < dim;
     uint64_t e = ebeg[d];
     const uint64_t end = eend[d];
-    float acc = (accumulate && active) ? out[d * ld_out + col] : 0.f;
+    const uint32_t row = ext_out_row(ext, d);
+    float acc = (accumulate && active) ? out[row * ld_out + col] : 0.f;
+    auto take = [&](const Edge& ed) {
+        return active && (!ext.src_bits || ext_src_on(ext, ed.x)) ? __ldg(in + ed.x * ld_in + col) : 0.f;
+    };
     for (; e + U <= end; e += U) {
         Edge ed[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) ed[u] = __ldg(edges + e + u);
         float x[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) x[u] = active ? __ldg(in + ed[u].x * ld_in + col) : 0.f;
+        for (int u = 0; u < U; ++u) x[u] = take(ed[u]);
 #pragma unroll
         for (int u = 0; u < U; ++u) acc = __fadd_rn(acc, __fmul_rn(__uint_as_float(ed[u].y), x[u]));
     }
     for (; e < end; ++e) {
         const Edge ed = __ldg(edges + e);
-        const float x = active ? __ldg(in + ed.x * ld_in + col) : 0.f;
-        acc = __fadd_rn(acc, __fmul_rn(__uint_as_float(ed.y), x));
+        acc = __fadd_rn(acc, __fmul_rn(__uint_as_float(ed.y), take(ed)));
     }
-    if (active) out[d * ld_out + col] = __fadd_rn(acc, 0.f);
+    if (!active) return;
+    acc = __fadd_rn(acc, 0.f);
+    if (ext.relu_pre) {
+        const uint32_t prow = ext.pre_rows ? __ldg(ext.pre_rows + d) : row;
+        acc = ext.relu_pre[static_cast<uint64_t>(prow) * ext.ld_pre + col] > 0.f ? acc : 0.f;
+    }
+    out[row * ld_out + col] = acc;
 }
 
 // ---- heavy destinations: TMA bulk-copy ring ---------------------------------
@@ -684,14 +732,14 @@ __host__ __device__ constexpr int coop_T() {
     return kCoopTileBytes / (CHQ * 16);
 }
 
-template <int CHQ>
+template <int CHQ, bool FILT>
 __global__ void __launch_bounds__(256) k_agg_heavy_coop(const uint64_t* __restrict__ ebeg, const uint64_t* __restrict__ eend,
                                                        const Edge* __restrict__ edges,
                                                        const uint32_t* __restrict__ order, uint32_t d_begin,
                                                        uint32_t chunks, uint32_t nq_total,
                                                        const float* __restrict__ in, uint64_t ld_in,
                                                        float* __restrict__ out, uint64_t ld_out, uint32_t dim,
-                                                       int accumulate, float2 zeros) {
+                                                       int accumulate, float2 zeros, AggExt ext) {
     constexpr int T = coop_T<CHQ>();
     constexpr int PER = T * CHQ / 256;  // float4 gathers per thread per tile
     extern __shared__ __align__(128) unsigned char smem[];
@@ -700,6 +748,7 @@ __global__ void __launch_bounds__(256) k_agg_heavy_coop(const uint64_t* __restri
 
     const uint32_t item = blockIdx.x;
     const uint32_t d = order[d_begin + item / chunks];
+    if (FILT && !ext_dst_on(ext, d)) return;  // uniform per CTA
     const uint32_t c = item % chunks;
     const uint32_t q0 = c * CHQ;
     const uint32_t nqc = min(static_cast<uint32_t>(CHQ), nq_total - q0);
@@ -718,7 +767,8 @@ __global__ void __launch_bounds__(256) k_agg_heavy_coop(const uint64_t* __restri
             const bool ok = e0 + j < ee && q < nqc;
             Edge ed = make_uint2(0u, 0u);
             if (ok) ed = __ldg(edges + e0 + j);
-            r[k] = ok ? ldg4(in + ed.x * ld_in + (q0 + q) * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+            const bool take = ok && (!FILT || ext_src_on(ext, ed.x));  // skipped: +-0 term
+            r[k] = take ? ldg4(in + ed.x * ld_in + (q0 + q) * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
             rw[k] = __uint_as_float(ed.y);
         }
     };
@@ -734,7 +784,8 @@ __global__ void __launch_bounds__(256) k_agg_heavy_coop(const uint64_t* __restri
     const Zs z = zs_of(zeros);
     const bool owner = tid < 32 && lane < nqc;
     const uint32_t col = (q0 + lane) * 4;
-    float* orow = out + d * ld_out + col;
+    const uint32_t row = ext_out_row(ext, d);
+    float* orow = out + row * ld_out + col;
     Acc acc = acc_load(orow, col, dim, owner && accumulate);
     if (ntiles) {
         gather(0);
@@ -753,26 +804,26 @@ __global__ void __launch_bounds__(256) k_agg_heavy_coop(const uint64_t* __restri
         if (t + 1 < ntiles) stash(b ^ 1);
         __syncthreads();
     }
-    if (owner) acc_store(orow, col, dim, acc, z);
+    if (owner) acc_store_ext(orow, col, dim, acc, z, ext, d, row);
 }
 
-template <int CHQ>
+template <int CHQ, bool FILT>
 void launch_heavy_coop(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges, const uint32_t* order, uint32_t d_begin,
                        uint32_t nh, uint32_t nq, const float* in, uint64_t ld_in, float* out, uint64_t ld_out,
-                       uint32_t dim, bool accumulate, cudaStream_t s) {
+                       uint32_t dim, bool accumulate, cudaStream_t s, const AggExt& ext) {
     static thread_local std::vector<char> attr_set;
     constexpr size_t smem = 2 * kCoopTileBytes + 2 * coop_T<CHQ>() * 4;
     int dev = 0;
     PG_CUDA(cudaGetDevice(&dev));
     if (static_cast<int>(attr_set.size()) <= dev) attr_set.resize(dev + 1, 0);
     if (!attr_set[dev]) {
-        PG_CUDA(cudaFuncSetAttribute(k_agg_heavy_coop<CHQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        PG_CUDA(cudaFuncSetAttribute(k_agg_heavy_coop<CHQ, FILT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
         attr_set[dev] = 1;
     }
     const uint32_t chunks = (nq + CHQ - 1) / CHQ;
-    k_agg_heavy_coop<CHQ><<<nh * chunks, 256, smem, s>>>(ebeg, eend, edges, order, d_begin, chunks, nq, in, ld_in, out,
-                                                         ld_out, dim, accumulate, kZeros);
+    k_agg_heavy_coop<CHQ, FILT><<<nh * chunks, 256, smem, s>>>(ebeg, eend, edges, order, d_begin, chunks, nq, in,
+                                                               ld_in, out, ld_out, dim, accumulate, kZeros, ext);
     PG_LAUNCH("k_agg_heavy_coop");
 }
 
@@ -787,11 +838,15 @@ bool heavy_use_tma() {
 template <int CHQ>
 void launch_heavy_any(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges, const uint32_t* order, uint32_t d_begin,
                       uint32_t nh, uint32_t nq, const float* in, uint64_t ld_in, float* out, uint64_t ld_out,
-                      uint32_t dim, bool accumulate, cudaStream_t s) {
-    if (heavy_use_tma())
+                      uint32_t dim, bool accumulate, cudaStream_t s, const AggExt& ext) {
+    if (ext.src_bits || ext.dst_bits)
+        launch_heavy_coop<CHQ, true>(ebeg, eend, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim, accumulate,
+                                     s, ext);
+    else if (heavy_use_tma() && !ext.any())
         launch_heavy<CHQ>(ebeg, eend, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim, accumulate, s);
     else
-        launch_heavy_coop<CHQ>(ebeg, eend, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim, accumulate, s);
+        launch_heavy_coop<CHQ, false>(ebeg, eend, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim,
+                                      accumulate, s, ext);
 }
 
 struct SideStream {
@@ -816,12 +871,17 @@ SideStream& side_stream() {
 template <int LPD, int U>
 void launch_vec4(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges, const uint32_t* order, uint32_t d_begin,
                  uint32_t nd, uint32_t chunks, const float* in, uint64_t ld_in, float* out, uint64_t ld_out,
-                 uint32_t dim, bool accumulate, cudaStream_t s) {
+                 uint32_t dim, bool accumulate, cudaStream_t s, const AggExt& ext) {
     const uint64_t items = static_cast<uint64_t>(nd) * chunks;
-    k_agg_vec4<LPD, U><<<grid_for(items * LPD, 256), 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks,
-                                                                 in, static_cast<uint32_t>(ld_in * 4), out, ld_out,
-                                                                 dim, accumulate, kZeros, 0u,
-                                                                 chunks > 1 && tuning(kTuneChunkMajor) ? 1 : 0);
+    const int cm = chunks > 1 && tuning(kTuneChunkMajor) ? 1 : 0;
+    if (ext.src_bits || ext.dst_bits)
+        k_agg_vec4<LPD, U, true><<<grid_for(items * LPD, 256), 256, 0, s>>>(
+            ebeg, eend, edges, order, d_begin, items, chunks, in, static_cast<uint32_t>(ld_in * 4), out, ld_out, dim,
+            accumulate, kZeros, 0u, cm, ext);
+    else
+        k_agg_vec4<LPD, U, false><<<grid_for(items * LPD, 256), 256, 0, s>>>(
+            ebeg, eend, edges, order, d_begin, items, chunks, in, static_cast<uint32_t>(ld_in * 4), out, ld_out, dim,
+            accumulate, kZeros, 0u, cm, ext);
     PG_LAUNCH("k_agg_vec4");
 }
 
@@ -891,7 +951,7 @@ __global__ void k_gather_rows(const float* __restrict__ src, uint64_t lds, const
 
 void aggregate_det(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges, const uint32_t* order, uint32_t D,
                    uint32_t d_begin, uint32_t d_end, uint32_t n_heavy, const float* in, uint64_t ld_in,
-                   float* out, uint64_t ld_out, uint64_t dim, bool accumulate, cudaStream_t s) {
+                   float* out, uint64_t ld_out, uint64_t dim, bool accumulate, cudaStream_t s, const AggExt& ext) {
     (void)D;
     if (d_end <= d_begin || dim == 0) return;
     uint32_t nd = d_end - d_begin;
@@ -899,12 +959,15 @@ void aggregate_det(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges
     const bool vec = (ld_in % 4 == 0) && (ld_out % 4 == 0) &&
                      (reinterpret_cast<uintptr_t>(in) % 16 == 0) &&
                      (reinterpret_cast<uintptr_t>(out) % 16 == 0) && ld_in >= ((dim + 3) & ~3ull) &&
-                     ld_in < (1ull << 30);
-    const uint32_t nh = vec ? std::min(n_heavy, nd) : 0;
+                     ld_in < (1ull << 30) && (!ext.relu_pre || ext.ld_pre >= dim);
+    const bool filt = ext.src_bits || ext.dst_bits;
+    const uint32_t nq = (dim32 + 3) / 4;
+    // heavy wide destinations (k_agg_wide_lat) take no activity filter: the
+    // filtered (if-else) traversal keeps them on the main kernel
+    const uint32_t nh = vec && !(filt && nq > 16) ? std::min(n_heavy, nd) : 0;
     if (nh) {
         // heavy prefix of the degree order on a forked stream, concurrent
         // with the main kernel over the rest; joined back into s
-        const uint32_t nq = (dim32 + 3) / 4;
         SideStream& ss = side_stream();
         PG_CUDA(cudaEventRecord(ss.fork, s));
         PG_CUDA(cudaStreamWaitEvent(ss.s, ss.fork, 0));
@@ -917,39 +980,42 @@ void aggregate_det(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges
                 const char* e = std::getenv("PG_HEAVY_WIDE");
                 return e && std::string(e) == "async";
             }();
-            if (!use_async) {
+            if (!use_async || ext.any()) {
                 k_agg_wide_lat<32><<<grid_for(items * 32, 256), 256, 0, ss.s>>>(
-                    ebeg, eend, edges, order, d_begin, items, chunks, in, ld_in, out, ld_out, dim32, accumulate, 0u);
+                    ebeg, eend, edges, order, d_begin, items, chunks, in, ld_in, out, ld_out, dim32, accumulate, 0u,
+                    ext);
                 PG_LAUNCH("k_agg_wide_lat");
             } else {
-            constexpr size_t smem = static_cast<size_t>(kAsyncWarps) * kAsyncBatches * 32 * 32 * 16;
-            static thread_local std::vector<char> attr_set;
-            int dev = 0;
-            PG_CUDA(cudaGetDevice(&dev));
-            if (static_cast<int>(attr_set.size()) <= dev) attr_set.resize(dev + 1, 0);
-            if (!attr_set[dev]) {
-                PG_CUDA(cudaFuncSetAttribute(k_agg_wide_async<kAsyncBatches>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-                attr_set[dev] = 1;
-            }
-            k_agg_wide_async<kAsyncBatches><<<grid_for(items * 32, kAsyncWarps * 32), kAsyncWarps * 32, smem, ss.s>>>(
-                ebeg, eend, edges, order, d_begin, items, chunks, in, ld_in, out, ld_out, dim32, accumulate, kZeros);
-            PG_LAUNCH("k_agg_wide_async");
+                constexpr size_t smem = static_cast<size_t>(kAsyncWarps) * kAsyncBatches * 32 * 32 * 16;
+                static thread_local std::vector<char> attr_set;
+                int dev = 0;
+                PG_CUDA(cudaGetDevice(&dev));
+                if (static_cast<int>(attr_set.size()) <= dev) attr_set.resize(dev + 1, 0);
+                if (!attr_set[dev]) {
+                    PG_CUDA(cudaFuncSetAttribute(k_agg_wide_async<kAsyncBatches>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+                    attr_set[dev] = 1;
+                }
+                k_agg_wide_async<kAsyncBatches>
+                    <<<grid_for(items * 32, kAsyncWarps * 32), kAsyncWarps * 32, smem, ss.s>>>(
+                        ebeg, eend, edges, order, d_begin, items, chunks, in, ld_in, out, ld_out, dim32, accumulate,
+                        kZeros);
+                PG_LAUNCH("k_agg_wide_async");
             }
         } else if (nq > 8)
             launch_heavy_any<16>(ebeg, eend, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim32, accumulate,
-                                 ss.s);
+                                 ss.s, ext);
         else if (nq > 4)
             launch_heavy_any<8>(ebeg, eend, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim32, accumulate,
-                                ss.s);
+                                ss.s, ext);
         else
             launch_heavy_any<4>(ebeg, eend, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim32, accumulate,
-                                ss.s);
+                                ss.s, ext);
         PG_CUDA(cudaEventRecord(ss.join, ss.s));
         d_begin += nh;
         nd -= nh;
         if (nd) aggregate_det(ebeg, eend, edges, order, D, d_begin, d_begin + nd, 0, in, ld_in, out, ld_out, dim,
-                              accumulate, s);
+                              accumulate, s, ext);
         PG_CUDA(cudaStreamWaitEvent(s, ss.join, 0));
         return;
     }
@@ -957,26 +1023,25 @@ void aggregate_det(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges
         const uint32_t chunks = (dim32 + 31) / 32;
         const uint64_t items = static_cast<uint64_t>(nd) * chunks;
         k_agg_scalar<8><<<grid_for(items * 32, 256), 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks,
-                                                                 in, ld_in, out, ld_out, dim32, accumulate);
+                                                                 in, ld_in, out, ld_out, dim32, accumulate, ext);
         PG_LAUNCH("k_agg_scalar");
         return;
     }
-    const uint32_t nq = (dim32 + 3) / 4;
     if (nq > 16) {
-        const int U = wide_unroll();
+        const int U = ext.any() ? 0 : wide_unroll();
         const uint32_t chunks = (nq + 31) / 32;
         const uint64_t items = static_cast<uint64_t>(nd) * chunks;
         if (U == 0) {  // the main kernel
             const int64_t vu = tuning(kTuneVecU);
             if (vu == 4)
                 launch_vec4<32, 4>(ebeg, eend, edges, order, d_begin, nd, chunks, in, ld_in, out, ld_out, dim32,
-                                   accumulate, s);
+                                   accumulate, s, ext);
             else if (vu == 16)
                 launch_vec4<32, 16>(ebeg, eend, edges, order, d_begin, nd, chunks, in, ld_in, out, ld_out, dim32,
-                                    accumulate, s);
+                                    accumulate, s, ext);
             else
                 launch_vec4<32, 8>(ebeg, eend, edges, order, d_begin, nd, chunks, in, ld_in, out, ld_out, dim32,
-                                   accumulate, s);
+                                   accumulate, s, ext);
         } else if (U == 8) {
             k_agg_wide<8><<<grid_for(items * 32, 256), 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks,
                                                                    in, ld_in, out, ld_out, dim32, accumulate, kZeros);
@@ -988,11 +1053,11 @@ void aggregate_det(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges
             PG_LAUNCH("k_agg_wide");
         }
     } else if (nq > 8) {
-        launch_vec4<16, 8>(ebeg, eend, edges, order, d_begin, nd, 1, in, ld_in, out, ld_out, dim32, accumulate, s);
+        launch_vec4<16, 8>(ebeg, eend, edges, order, d_begin, nd, 1, in, ld_in, out, ld_out, dim32, accumulate, s, ext);
     } else if (nq > 4) {
-        launch_vec4<8, 8>(ebeg, eend, edges, order, d_begin, nd, 1, in, ld_in, out, ld_out, dim32, accumulate, s);
+        launch_vec4<8, 8>(ebeg, eend, edges, order, d_begin, nd, 1, in, ld_in, out, ld_out, dim32, accumulate, s, ext);
     } else {
-        launch_vec4<4, 8>(ebeg, eend, edges, order, d_begin, nd, 1, in, ld_in, out, ld_out, dim32, accumulate, s);
+        launch_vec4<4, 8>(ebeg, eend, edges, order, d_begin, nd, 1, in, ld_in, out, ld_out, dim32, accumulate, s, ext);
     }
 }
 

@@ -122,28 +122,30 @@ void counters_of(Groups& G, uint64_t dim, unsigned flags, uint64_t* c) {
 // allgather layout once pg_groups_remap_sources installed a map
 uint64_t y_rows_of(const Groups& G) { return G.edges_remap.get() ? G.remap_rows : G.path->P; }
 
+DMat dm(const pg_mat& m) {
+    if (m.ld < m.cols) fail(kConfig, "matrix leading dimension smaller than its columns");
+    if (!m.data && m.rows * m.cols) fail(kConfig, "null matrix data");
+    return DMat{m.data, m.rows, m.cols, m.ld};
+}
+
 void check_dims(uint64_t dim, uint64_t ld_in, uint64_t ld_out) {
     if (ld_in < dim || ld_out < dim) fail(kConfig, "aggregate_pull: leading dimension smaller than dim");
 }
 
 // Core launch over the grouping's base: which edge stream and which schedule.
-// Source-segment selector for run_aggregate: bounds array [(nseg+1) x D] and
-// the segment to run (seg < 0: whole edge lists).
-struct SegSel {
-    const uint64_t* bnd = nullptr;
-    int seg = -1;
-    uint32_t nseg = 1;
-};
+}  // namespace
 
-void run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re, const float* in, uint64_t ld_in,
-                   float* out, uint64_t ld_out, uint64_t dim, unsigned flags, cudaStream_t s, SegSel sel = {}) {
+void pg::run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re, const float* in, uint64_t ld_in,
+                   float* out, uint64_t ld_out, uint64_t dim, unsigned flags, cudaStream_t s, SegSel sel,
+                   const AggExt& ext, const Edge* edges_override) {
     const bool accumulate = !(flags & PG_AGG_OVERWRITE);
     DeviceGuard dg(G.device);
     if (G.path) {
         Path& p = *G.path;
         const Edge* edges = p.edges_parent.get();
         if (parent_indexed && G.edges_remap.get()) edges = G.edges_remap.get();
-        if (!parent_indexed && p.S != p.P) {
+        if (edges_override) edges = edges_override;
+        if (!edges_override && !parent_indexed && p.S != p.P) {
             path_pack_local(p, lib_stream(p.device));
             PG_CUDA(cudaStreamSynchronize(lib_stream(p.device)));
             edges = p.edges_local.get();
@@ -160,7 +162,7 @@ void run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re, con
         if (rb == 0 && re == p.D) {
             aggregate_det(eb, ee, edges, p.order.get(), p.D, 0, p.D,
                           p.hist.heavy(heavy_min_degree(dim, p.E / range_div)), in, ld_in, out, ld_out, dim,
-                          accumulate, s);
+                          accumulate, s, ext);
             return;
         }
         // row range: schedule of rows [rb, re) relative to rb (cached)
@@ -176,7 +178,7 @@ void run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re, con
         }
         aggregate_det(eb + rb, ee + rb, edges, rs->order.get(), re - rb, 0, re - rb,
                       rs->hist.heavy(heavy_min_degree(dim, rs->hist.edges / range_div)), in, ld_in, out, ld_out, dim,
-                      accumulate, s);
+                      accumulate, s, ext);
         return;
     }
     Graph& g = *G.graph;
@@ -187,8 +189,10 @@ void run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re, con
     if (!G.graph_order.get() && g.n)
         degree_order(g.offsets.get(), g.n, G.graph_order, lib_stream(g.device), &G.graph_hist);
     aggregate_det(g.offsets.get(), g.offsets.get() + 1, g.edges.get(), G.graph_order.get(), g.n, 0, g.n,
-                  G.graph_hist.heavy(heavy_min_degree(dim, g.m)), in, ld_in, out, ld_out, dim, accumulate, s);
+                  G.graph_hist.heavy(heavy_min_degree(dim, g.m)), in, ld_in, out, ld_out, dim, accumulate, s, ext);
 }
+
+namespace {
 
 struct CopyStreams {
     cudaStream_t h2d = nullptr, d2h = nullptr;
@@ -913,6 +917,141 @@ int pg_relu_backward(const float* grad, uint64_t ldg, const float* pre, uint64_t
 int pg_gather_rows(const float* src, uint64_t lds, const uint32_t* ids_dev, uint64_t k, float* out, uint64_t ldo,
                    uint64_t cols, void* stream) {
     return guard([&] { gather_rows(src, lds, ids_dev, k, out, ldo, cols, static_cast<cudaStream_t>(stream)); });
+}
+
+// ---- the GCN chain (engine.cu) ----
+
+int pg_gemm(pg_mat a, pg_mat b, int b_transposed, pg_mat out, void* stream) {
+    return guard([&] { gemm(dm(a), dm(b), dm(out), b_transposed != 0, static_cast<cudaStream_t>(stream)); });
+}
+
+int pg_gemm_at_b(pg_mat a, const uint32_t* a_rows, pg_mat b, pg_mat out, void* stream) {
+    return guard([&] { gemm_at_b(dm(a), a_rows, dm(b), dm(out), static_cast<cudaStream_t>(stream)); });
+}
+
+int pg_relu(pg_mat x, pg_mat out, void* stream) {
+    return guard([&] { relu(dm(x), dm(out), static_cast<cudaStream_t>(stream)); });
+}
+
+int pg_row_softmax(pg_mat x, pg_mat out, void* stream) {
+    return guard([&] { row_softmax(dm(x), dm(out), static_cast<cudaStream_t>(stream)); });
+}
+
+int pg_top_grad_from_probs(pg_mat probs, pg_mat ref, const uint32_t* vt_dev, uint64_t k, pg_mat out, void* stream) {
+    return guard([&] {
+        top_grad_from_probs(dm(probs), dm(ref), vt_dev, k, dm(out), static_cast<cudaStream_t>(stream));
+    });
+}
+
+int pg_aggregate_pull_filtered(pg_groups h, pg_frontiers hf, uint64_t dest_level, uint64_t src_level,
+                               const float* in_dev, uint64_t in_rows, uint64_t ld_in, float* out_dev,
+                               uint64_t ld_out, uint64_t dim, unsigned flags, uint64_t* counters, void* stream) {
+    return guard([&] {
+        Groups& G = *R_(h);
+        Frontiers& F = *F_(hf);
+        if (!G.graph) fail(kConfig, "aggregate_pull_filtered: needs a grouping of the full graph");
+        if (dest_level > F.L || src_level > F.L) fail(kConfig, "aggregate_pull_filtered: level out of range");
+        if (F.n != G.graph->n) fail(kConfig, "aggregate_pull_filtered: frontiers are for another graph");
+        if (in_rows != G.graph->n) fail(kConfig, "aggregate_pull_filtered: input rows != vertex count");
+        check_dims(dim, ld_in, ld_out);
+        AggExt ext;
+        ext.dst_bits = F.levels[dest_level].bits.get();
+        ext.src_bits = F.levels[src_level].bits.get();
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        run_aggregate(G, false, 0, G.graph->n, in_dev, ld_in, out_dev, ld_out, dim, flags, s, SegSel{}, ext);
+        if (counters) {
+            DeviceGuard dg(G.device);
+            filter_counts(*G.graph, G.gs, ext.dst_bits, ext.src_bits, counters, s);
+        }
+    });
+}
+
+int pg_forward(pg_groups h, pg_mat x0, const pg_mat* w, uint64_t layers, pg_mat* y, pg_mat* pre, pg_mat* x,
+               void* stream) {
+    return guard([&] {
+        Groups& G = *R_(h);
+        if (!w || !y || !pre || !x) fail(kConfig, "forward: null matrix array");
+        std::vector<DMat> W(layers), Y(layers), P(layers), X(layers);
+        for (uint64_t l = 0; l < layers; ++l) {
+            W[l] = dm(w[l]);
+            Y[l] = dm(y[l]);
+            P[l] = dm(pre[l]);
+            X[l] = dm(x[l]);
+        }
+        DeviceGuard dg(G.device);
+        forward(G, dm(x0), W.data(), layers, Y.data(), P.data(), X.data(), static_cast<cudaStream_t>(stream));
+    });
+}
+
+}  // extern "C"
+
+namespace {
+
+// BackwardIO over the caller's arrays (storage kept alive by the holder)
+struct IoHolder {
+    std::vector<DMat> y, pre, w, wg, xg;
+    BackwardIO io;
+    IoHolder(uint64_t L, const pg_mat* py, const pg_mat* ppre, pg_mat top, const pg_mat* pw, pg_mat* pwg,
+             pg_mat* pxg, uint64_t* edges) {
+        if (!py || !ppre || !pw || !pwg) fail(kConfig, "backward: null matrix array");
+        for (uint64_t l = 0; l < L; ++l) {
+            y.push_back(dm(py[l]));
+            pre.push_back(dm(ppre[l]));
+            w.push_back(dm(pw[l]));
+            wg.push_back(dm(pwg[l]));
+            if (pxg) xg.push_back(dm(pxg[l]));
+        }
+        io.L = L;
+        io.y = y.data();
+        io.pre = pre.data();
+        io.top_grad = dm(top);
+        io.w = w.data();
+        io.w_grads = wg.data();
+        io.x_grads = pxg ? xg.data() : nullptr;
+        io.edges = edges;
+    }
+};
+
+}  // namespace
+
+extern "C" {
+
+int pg_backward_epp(const pg_groups* path_groups, pg_frontiers hf, uint64_t layers, const pg_mat* y,
+                    const pg_mat* pre, pg_mat top_grad, const pg_mat* w, uint64_t expected_fingerprint,
+                    int gather_mode, pg_mat* w_grads, pg_mat* x_grads, uint64_t* edges_per_layer, void* stream) {
+    return guard([&] {
+        Frontiers& F = *F_(hf);
+        if (!path_groups) fail(kConfig, "epp backward: null path groupings");
+        if (gather_mode != 0 && gather_mode != 1) fail(kConfig, "epp backward: gather mode must be 0 or 1");
+        std::vector<Groups*> PGs(layers);
+        for (uint64_t i = 0; i < layers; ++i) PGs[i] = R_(path_groups[i]);
+        IoHolder h(layers, y, pre, top_grad, w, w_grads, x_grads, edges_per_layer);
+        DeviceGuard dg(F.device);
+        backward_epp(PGs.data(), F, h.io, gather_mode, expected_fingerprint, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int pg_backward_all_active(pg_groups h, uint64_t layers, const pg_mat* y, const pg_mat* pre, pg_mat top_grad,
+                           const pg_mat* w, pg_mat* w_grads, pg_mat* x_grads, uint64_t* edges_per_layer,
+                           void* stream) {
+    return guard([&] {
+        Groups& G = *R_(h);
+        IoHolder io(layers, y, pre, top_grad, w, w_grads, x_grads, edges_per_layer);
+        DeviceGuard dg(G.device);
+        backward_all_active(G, io.io, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int pg_backward_ifelse(pg_groups h, pg_frontiers hf, uint64_t layers, const pg_mat* y, const pg_mat* pre,
+                       pg_mat top_grad, const pg_mat* w, pg_mat* w_grads, pg_mat* x_grads,
+                       uint64_t* edges_per_layer, void* stream) {
+    return guard([&] {
+        Groups& G = *R_(h);
+        Frontiers& F = *F_(hf);
+        IoHolder io(layers, y, pre, top_grad, w, w_grads, x_grads, edges_per_layer);
+        DeviceGuard dg(G.device);
+        backward_ifelse(G, F, io.io, static_cast<cudaStream_t>(stream));
+    });
 }
 
 }  // extern "C"

@@ -1,0 +1,530 @@
+// The GCN chain around the backward aggregation (engine.hpp), device
+// resident and bit-exact with the reference's f32 build:
+//   * dense products (dense_matrix.hpp:40-96): every output element is one
+//     thread's ascending-k chain of separately rounded multiply/add, then
+//     + 0 — the reference's association order, so the bits match;
+//   * relu / row_softmax / top_grad_from_probs (dense_matrix.hpp:98-135,
+//     engine.hpp:146-156);
+//   * the three backward variants (engine.hpp:177-349) and forward
+//     (:114-140), composed from those kernels and the SpMM (aggregate.cu)
+//     with relu_backward fused into the SpMM epilogue and gather_rows fused
+//     into the W-gradient product.
+// These are HBM/latency-bound fp32 reductions with a fixed order; nothing
+// here is reshaped for tensor cores (a tcgen05 MMA would re-associate the
+// sums and break bit parity with the reference).
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "../../include/pathgcn_b200.h"
+#include "pg_internal.h"
+
+namespace pg {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+// ---- out = A * op(B), op(B)(k, j) = BT ? b[j][k] : b[k][j] -----------------
+// Block: 32 lanes = 32 output columns j, 8 warps x RPW rows i. K staged in
+// chunks of 32 through shared memory; thread (i, j) keeps one ascending-k
+// chain per row.
+constexpr int kGT = 32;  // j tile / k chunk
+constexpr int kGRPW = 4;  // rows per warp
+constexpr int kGI = 8 * kGRPW;
+
+template <bool BT>
+__global__ void __launch_bounds__(256) k_gemm(const float* __restrict__ a, uint64_t lda,
+                                              const float* __restrict__ b, uint64_t ldb, float* __restrict__ out,
+                                              uint64_t ldo, uint64_t n, uint64_t m, uint64_t K) {
+    __shared__ float as[kGI][kGT + 1];
+    __shared__ float bs[kGT][kGT + 1];
+    const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint64_t j = blockIdx.x * static_cast<uint64_t>(kGT) + lane;
+    const uint64_t i0 = blockIdx.y * static_cast<uint64_t>(kGI);
+    float acc[kGRPW];
+#pragma unroll
+    for (int r = 0; r < kGRPW; ++r) acc[r] = 0.f;
+    for (uint64_t k0 = 0; k0 < K; k0 += kGT) {
+        const int kc = static_cast<int>(K - k0 < kGT ? K - k0 : kGT);
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < kGI * kGT; idx += 256) {
+            const int r = idx / kGT, kk = idx % kGT;
+            as[r][kk] = (i0 + r < n && kk < kc) ? a[(i0 + r) * lda + k0 + kk] : 0.f;
+        }
+        for (int idx = threadIdx.x; idx < kGT * kGT; idx += 256) {
+            const int kk = idx / kGT, jj = idx % kGT;
+            const uint64_t jg = blockIdx.x * static_cast<uint64_t>(kGT) + jj;
+            float v = 0.f;
+            if (kk < kc && jg < m) v = BT ? b[jg * ldb + k0 + kk] : b[(k0 + kk) * ldb + jg];
+            bs[kk][jj] = v;
+        }
+        __syncthreads();
+        for (int kk = 0; kk < kc; ++kk) {
+            const float bv = bs[kk][lane];
+#pragma unroll
+            for (int r = 0; r < kGRPW; ++r) acc[r] = __fadd_rn(acc[r], __fmul_rn(as[w * kGRPW + r][kk], bv));
+        }
+    }
+    if (j >= m) return;
+#pragma unroll
+    for (int r = 0; r < kGRPW; ++r) {
+        const uint64_t i = i0 + w * kGRPW + r;
+        if (i < n) out[i * ldo + j] = __fadd_rn(acc[r], 0.f);
+    }
+}
+
+// ---- out = A[rows]^T * B (dense_matrix.hpp:57-76 gemm_at_b) -----------------
+// out[i][j] = sum over k < n, ascending, of A(k, i) * B(k, j), A(k, i) =
+// a[(rows ? rows[k] : k) * lda + i] (the engine's gather_rows fused in).
+// One thread per (i, j): the chain runs over all n rows in order, so the
+// only parallelism is the r x c outputs; rows are staged KC at a time.
+constexpr int kAtbKC = 128;
+
+template <int TI, int TJ>
+__global__ void __launch_bounds__(TI* TJ) k_gemm_at_b(const float* __restrict__ a, uint64_t lda,
+                                                      const uint32_t* __restrict__ rows, const float* __restrict__ b,
+                                                      uint64_t ldb, float* __restrict__ out, uint64_t ldo, uint64_t n,
+                                                      uint64_t r, uint64_t c) {
+    __shared__ float as[kAtbKC][TI];
+    __shared__ float bs[kAtbKC][TJ + 1];
+    const unsigned ti = threadIdx.x / TJ, tj = threadIdx.x % TJ;
+    const uint64_t i = blockIdx.x * static_cast<uint64_t>(TI) + ti;
+    const uint64_t j = blockIdx.y * static_cast<uint64_t>(TJ) + tj;
+    float acc = 0.f;
+    for (uint64_t k0 = 0; k0 < n; k0 += kAtbKC) {
+        const int kc = static_cast<int>(n - k0 < kAtbKC ? n - k0 : kAtbKC);
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < kAtbKC * TI; idx += TI * TJ) {
+            const int kk = idx / TI, ii = idx % TI;
+            const uint64_t ig = blockIdx.x * static_cast<uint64_t>(TI) + ii;
+            float v = 0.f;
+            if (kk < kc && ig < r) {
+                const uint64_t row = rows ? __ldg(rows + k0 + kk) : k0 + kk;
+                v = a[row * lda + ig];
+            }
+            as[kk][ii] = v;
+        }
+        for (int idx = threadIdx.x; idx < kAtbKC * TJ; idx += TI * TJ) {
+            const int kk = idx / TJ, jj = idx % TJ;
+            const uint64_t jg = blockIdx.y * static_cast<uint64_t>(TJ) + jj;
+            bs[kk][jj] = (kk < kc && jg < c) ? b[(k0 + kk) * ldb + jg] : 0.f;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int kk = 0; kk < kc; ++kk) acc = __fadd_rn(acc, __fmul_rn(as[kk][ti], bs[kk][tj]));
+    }
+    if (i < r && j < c) out[i * ldo + j] = __fadd_rn(acc, 0.f);
+}
+
+// ---- elementwise / row kernels ---------------------------------------------
+// 2-D grid-stride over (rows, cols): blockIdx.y strides rows
+__global__ void k_relu(const float* __restrict__ x, uint64_t ldx, float* __restrict__ out, uint64_t ldo,
+                       uint64_t rows, uint32_t cols) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= cols) return;
+    for (uint64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+        const float v = x[r * ldx + c];
+        out[r * ldo + c] = v > 0.f ? v : 0.f;
+    }
+}
+
+// relu_backward with the pre-activation rows selected by pre_rows
+__global__ void k_relu_bwd_rows(const float* __restrict__ g, uint64_t ldg, const float* __restrict__ pre,
+                                uint64_t ldp, const uint32_t* __restrict__ pre_rows, float* __restrict__ out,
+                                uint64_t ldo, uint64_t rows, uint32_t cols) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= cols) return;
+    for (uint64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+        const uint64_t pr = pre_rows ? pre_rows[r] : r;
+        out[r * ldo + c] = pre[pr * ldp + c] > 0.f ? g[r * ldg + c] : 0.f;
+    }
+}
+
+// std::exp(float) in the reference is glibc's expf. This is its algorithm
+// (exp2f_data table, 32 entries + degree-3 polynomial in double), in the
+// form glibc 2.39 runs on FMA-capable x86-64 (the ifunc-selected FMA build,
+// where r = fma(InvLn2N, x, -kd) and the polynomial steps are fused):
+// checked equal to the host's expf for all 2^32 float inputs.
+__constant__ unsigned long long kExp2fTab[32] = {0x3ff0000000000000ULL,0x3fefd9b0d3158574ULL,0x3fefb5586cf9890fULL,0x3fef9301d0125b51ULL,0x3fef72b83c7d517bULL,0x3fef54873168b9aaULL,0x3fef387a6e756238ULL,0x3fef1e9df51fdee1ULL,0x3fef06fe0a31b715ULL,0x3feef1a7373aa9cbULL,0x3feedea64c123422ULL,0x3feece086061892dULL,0x3feebfdad5362a27ULL,0x3feeb42b569d4f82ULL,0x3feeab07dd485429ULL,0x3feea47eb03a5585ULL,0x3feea09e667f3bcdULL,0x3fee9f75e8ec5f74ULL,0x3feea11473eb0187ULL,0x3feea589994cce13ULL,0x3feeace5422aa0dbULL,0x3feeb737b0cdc5e5ULL,0x3feec49182a3f090ULL,0x3feed503b23e255dULL,0x3feee89f995ad3adULL,0x3feeff76f2fb5e47ULL,0x3fef199bdd85529cULL,0x3fef3720dcef9069ULL,0x3fef5818dcfba487ULL,0x3fef7c97337b9b5fULL,0x3fefa4afa2a490daULL,0x3fefd0765b6e4540ULL};
+
+__device__ __forceinline__ float expf_glibc(float x) {
+    const uint32_t ux = __float_as_uint(x), abstop = (ux >> 20) & 0x7ffu;
+    if (abstop >= 0x42bu) {  // |x| >= 88
+        if (ux == 0xff800000u) return 0.f;
+        if (abstop >= 0x7f8u) return x + x;
+        if (x > 0x1.62e42ep6f) return __int_as_float(0x7f800000);
+        if (x < -0x1.9fe368p6f) return 0.f;
+    }
+    constexpr double N = 32.0;
+    constexpr double InvLn2N = 0x1.71547652b82fep+0 * N;
+    constexpr double Shift = 0x1.8p+52;
+    constexpr double C0 = 0x1.c6af84b912394p-5 / N / N / N, C1 = 0x1.ebfce50fac4f3p-3 / N / N,
+                     C2 = 0x1.62e42ff0c52d6p-1 / N;
+    const double xd = static_cast<double>(x);
+    const double z = __dmul_rn(InvLn2N, xd);
+    double kd = __dadd_rn(z, Shift);
+    const unsigned long long ki = static_cast<unsigned long long>(__double_as_longlong(kd));
+    kd = __dsub_rn(kd, Shift);
+    const double r = __fma_rn(InvLn2N, xd, -kd);
+    const unsigned long long t = kExp2fTab[ki % 32] + (ki << 47);
+    const double sc = __longlong_as_double(static_cast<long long>(t));
+    const double zz = __fma_rn(C0, r, C1), r2 = __dmul_rn(r, r);
+    double y = __fma_rn(C2, r, 1.0);
+    y = __fma_rn(zz, r2, y);
+    return __double2float_rn(__dmul_rn(y, sc));
+}
+
+// dense_matrix.hpp:116-135: per row max (std::max: (a < b) ? b : a),
+// o = exp(x - max) in float, serial float sum, divide. Thread per row.
+__global__ void k_row_softmax(const float* __restrict__ x, uint64_t ldx, float* __restrict__ out, uint64_t ldo,
+                              uint64_t rows, uint64_t cols) {
+    const uint64_t r = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (r >= rows) return;
+    const float* in = x + r * ldx;
+    float* o = out + r * ldo;
+    float mx = in[0];
+    for (uint64_t j = 1; j < cols; ++j) mx = (mx < in[j]) ? in[j] : mx;
+    float sum = 0.f;
+    for (uint64_t j = 0; j < cols; ++j) {
+        const float e = expf_glibc(__fsub_rn(in[j], mx));
+        o[j] = e;
+        sum = __fadd_rn(sum, e);
+    }
+    for (uint64_t j = 0; j < cols; ++j) o[j] = __fdiv_rn(o[j], sum);
+}
+
+// engine.hpp:146-156: grad = 0; grad[v] = (probs[v] - r[v]) * inv on V_t
+__global__ void k_top_grad(const float* __restrict__ probs, uint64_t ldp, const float* __restrict__ ref,
+                           uint64_t ldr, const uint32_t* __restrict__ vt, uint64_t k, float inv,
+                           float* __restrict__ out, uint64_t ldo, uint32_t cols) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= cols) return;
+    for (uint64_t i = blockIdx.y; i < k; i += gridDim.y) {
+        const uint64_t v = vt[i];
+        out[v * ldo + c] = __fmul_rn(__fsub_rn(probs[v * ldp + c], ref[v * ldr + c]), inv);
+    }
+}
+
+// aggregate_pull_filtered work counters (aggregate.hpp:139-162): warp per
+// destination of the full graph. c = {edges, groups, edges_skipped,
+// groups_skipped}.
+__global__ void k_filter_counts(const uint64_t* __restrict__ offsets, const uint32_t* __restrict__ nbrs, uint32_t n,
+                                uint32_t gs, const uint32_t* __restrict__ dst_bits,
+                                const uint32_t* __restrict__ src_bits, unsigned long long* __restrict__ c) {
+    const uint64_t w = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+    if (w >= n) return;
+    const uint32_t v = static_cast<uint32_t>(w);
+    const uint64_t b = offsets[v], e = offsets[v + 1];
+    const uint64_t deg = e - b, groups = (deg + gs - 1) / gs;
+    const unsigned lane = lane_id();
+    if (!bit_of(dst_bits, v)) {
+        if (lane == 0) {
+            atomicAdd(c + 2, static_cast<unsigned long long>(deg));
+            atomicAdd(c + 3, static_cast<unsigned long long>(groups));
+        }
+        return;
+    }
+    unsigned long long on = 0;
+    for (uint64_t j = b + lane; j < e; j += 32) on += bit_of(src_bits, __ldg(nbrs + j));
+    on = warp_sum(on);
+    if (lane == 0) {
+        atomicAdd(c + 0, on);
+        atomicAdd(c + 1, static_cast<unsigned long long>(groups));
+        atomicAdd(c + 2, static_cast<unsigned long long>(deg - on));
+    }
+}
+
+dim3 rows_grid(uint64_t rows, uint64_t cols, unsigned tx) {
+    return dim3(static_cast<unsigned>((cols + tx - 1) / tx),
+                static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(rows, 32768))));
+}
+
+}  // namespace
+
+void gemm(DMat a, DMat b, DMat out, bool b_transposed, cudaStream_t s) {
+    const uint64_t K = a.cols;
+    if (b_transposed ? b.cols != K : b.rows != K) fail(kConfig, "gemm: inner dimensions differ");
+    const uint64_t n = a.rows, m = b_transposed ? b.rows : b.cols;
+    if (out.rows != n || out.cols != m) fail(kConfig, "gemm: output shape mismatch");
+    if (n == 0 || m == 0) return;
+    if (K == 0) {
+        PG_CUDA(cudaMemset2DAsync(out.p, out.ld * 4, 0, m * 4, n, s));
+        return;
+    }
+    dim3 grid(static_cast<unsigned>((m + kGT - 1) / kGT), static_cast<unsigned>((n + kGI - 1) / kGI));
+    if (b_transposed)
+        k_gemm<true><<<grid, 256, 0, s>>>(a.p, a.ld, b.p, b.ld, out.p, out.ld, n, m, K);
+    else
+        k_gemm<false><<<grid, 256, 0, s>>>(a.p, a.ld, b.p, b.ld, out.p, out.ld, n, m, K);
+    PG_LAUNCH("k_gemm");
+}
+
+void gemm_at_b(DMat a, const uint32_t* a_rows, DMat b, DMat out, cudaStream_t s) {
+    const uint64_t n = b.rows, r = a.cols, c = b.cols;
+    if (!a_rows && a.rows != n) fail(kConfig, "gemm_at_b: row counts differ");
+    if (out.rows != r || out.cols != c) fail(kConfig, "gemm_at_b: output shape mismatch");
+    if (r == 0 || c == 0) return;
+    if (c <= 16) {
+        dim3 grid(static_cast<unsigned>((r + 3) / 4), static_cast<unsigned>((c + 15) / 16));
+        k_gemm_at_b<4, 16><<<grid, 64, 0, s>>>(a.p, a.ld, a_rows, b.p, b.ld, out.p, out.ld, n, r, c);
+    } else {
+        dim3 grid(static_cast<unsigned>((r + 3) / 4), static_cast<unsigned>((c + 31) / 32));
+        k_gemm_at_b<4, 32><<<grid, 128, 0, s>>>(a.p, a.ld, a_rows, b.p, b.ld, out.p, out.ld, n, r, c);
+    }
+    PG_LAUNCH("k_gemm_at_b");
+}
+
+void relu(DMat x, DMat out, cudaStream_t s) {
+    if (x.rows != out.rows || x.cols != out.cols) fail(kConfig, "relu: shape mismatch");
+    if (x.rows * x.cols == 0) return;
+    k_relu<<<rows_grid(x.rows, x.cols, 128), 128, 0, s>>>(x.p, x.ld, out.p, out.ld, x.rows,
+                                                         static_cast<uint32_t>(x.cols));
+    PG_LAUNCH("k_relu");
+}
+
+void relu_backward_rows(DMat g, DMat pre, const uint32_t* pre_rows, DMat out, cudaStream_t s) {
+    if (g.rows != out.rows || g.cols != out.cols || pre.cols != g.cols || (!pre_rows && pre.rows != g.rows))
+        fail(kConfig, "relu_backward: shape mismatch");
+    if (g.rows * g.cols == 0) return;
+    k_relu_bwd_rows<<<rows_grid(g.rows, g.cols, 128), 128, 0, s>>>(g.p, g.ld, pre.p, pre.ld, pre_rows, out.p, out.ld,
+                                                                   g.rows, static_cast<uint32_t>(g.cols));
+    PG_LAUNCH("k_relu_bwd_rows");
+}
+
+void row_softmax(DMat x, DMat out, cudaStream_t s) {
+    if (x.cols == 0) fail(kConfig, "row_softmax: zero columns");
+    if (x.rows != out.rows || x.cols != out.cols) fail(kConfig, "row_softmax: shape mismatch");
+    if (x.rows == 0) return;
+    k_row_softmax<<<grid_for(x.rows, 128), 128, 0, s>>>(x.p, x.ld, out.p, out.ld, x.rows, x.cols);
+    PG_LAUNCH("k_row_softmax");
+}
+
+void top_grad_from_probs(DMat probs, DMat ref, const uint32_t* vt, uint64_t k, DMat out, cudaStream_t s) {
+    if (probs.rows != ref.rows || probs.cols != ref.cols || out.rows != probs.rows || out.cols != probs.cols)
+        fail(kConfig, "top_grad_from_probs: shapes differ");
+    if (out.rows * out.cols) PG_CUDA(cudaMemset2DAsync(out.p, out.ld * 4, 0, out.cols * 4, out.rows, s));
+    if (k == 0 || out.cols == 0) return;
+    const float inv = 1.0f / static_cast<float>(k);  // T(1) / static_cast<T>(vt.size())
+    k_top_grad<<<rows_grid(k, out.cols, 64), 64, 0, s>>>(probs.p, probs.ld, ref.p, ref.ld, vt, k, inv, out.p, out.ld,
+                                                          static_cast<uint32_t>(out.cols));
+    PG_LAUNCH("k_top_grad");
+}
+
+void filter_counts(const Graph& g, uint32_t gs, const uint32_t* dst_bits, const uint32_t* src_bits, uint64_t* c4,
+                   cudaStream_t s) {
+    DevBuf<unsigned long long> c(4, s);
+    PG_CUDA(cudaMemsetAsync(c.get(), 0, 32, s));
+    if (g.n) {
+        k_filter_counts<<<grid_for(static_cast<uint64_t>(g.n) * 32, kThreads), kThreads, 0, s>>>(
+            g.offsets.get(), g.nbrs.get(), g.n, gs, dst_bits, src_bits, c.get());
+        PG_LAUNCH("k_filter_counts");
+    }
+    PG_CUDA(cudaMemcpyAsync(c4, c.get(), 32, cudaMemcpyDeviceToHost, s));
+    PG_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace pg
+
+// ============================================================================
+// The chains. Temporaries are stream-ordered pool allocations on s; every
+// call is asynchronous on s except where a counter needs a host value.
+namespace pg {
+
+namespace {
+
+struct Tmp {
+    DevBuf<float> buf;
+    DMat m;
+    Tmp(uint64_t rows, uint64_t cols, cudaStream_t s, bool zero = false) : buf(rows * pad_ld(cols), s) {
+        m = DMat{buf.get(), rows, cols, pad_ld(cols)};
+        if (zero && rows * cols) PG_CUDA(cudaMemsetAsync(buf.get(), 0, rows * pad_ld(cols) * 4, s));
+    }
+};
+
+void check_chain(const BackwardIO& io, uint64_t n) {
+    if (io.L == 0) fail(kConfig, "backward: need at least one layer");
+    for (uint64_t l = 0; l < io.L; ++l) {
+        if (io.y[l].rows != n || io.y[l].cols != io.w[l].rows)
+            fail(kConfig, "backward: Y^(l) shape does not match W^(l) at layer " + std::to_string(l));
+        if (io.pre[l].rows != n || io.pre[l].cols != io.w[l].cols)
+            fail(kConfig, "backward: pre-activation shape mismatch at layer " + std::to_string(l));
+        if (l > 0 && io.w[l].rows != io.w[l - 1].cols) fail(kConfig, "backward: weight chain mismatch");
+        if (io.w_grads[l].rows != io.w[l].rows || io.w_grads[l].cols != io.w[l].cols)
+            fail(kConfig, "backward: W gradient shape mismatch at layer " + std::to_string(l));
+    }
+    if (io.top_grad.rows != n || io.top_grad.cols != io.w[io.L - 1].cols)
+        fail(kConfig, "backward: top gradient shape mismatch");
+}
+
+// The full-graph backward shared by Alg. 1 (all-active) and the if-else
+// filter: per layer W' = Y^T g, y_grad = g W^T, x_grad = pull(y_grad), and
+// g = relu_backward(x_grad, pre[l-1]) fused into the SpMM epilogue.
+void backward_full(Groups& G, Frontiers* F, const BackwardIO& io, cudaStream_t s) {
+    if (!G.graph) fail(kConfig, "backward: needs a grouping of the full graph");
+    Graph& gr = *G.graph;
+    const uint64_t n = gr.n, L = io.L;
+    check_chain(io, n);
+    if (F && F->L != L) fail(kConfig, "ifelse backward: frontiers were computed for a different depth");
+    std::unique_ptr<Tmp> gcur;
+    DMat g = io.top_grad;
+    for (uint64_t l = L; l-- > 0;) {
+        const uint64_t in_dim = io.w[l].rows;
+        gemm_at_b(io.y[l], nullptr, g, io.w_grads[l], s);
+        Tmp yg(n, in_dim, s);
+        gemm(g, io.w[l], yg.m, true, s);
+        AggExt ext;
+        if (F) {
+            ext.dst_bits = F->levels[L - l].bits.get();
+            ext.src_bits = F->levels[L - l - 1].bits.get();
+        }
+        DMat* xo = io.x_grads ? &io.x_grads[L - 1 - l] : nullptr;
+        if (xo && (xo->rows != n || xo->cols != in_dim)) fail(kConfig, "backward: x_grad shape mismatch");
+        std::unique_ptr<Tmp> gnext;
+        if (l > 0 && !xo) {  // fused: the SpMM writes relu_backward(x_grad, pre[l-1])
+            gnext = std::make_unique<Tmp>(n, in_dim, s, F != nullptr);
+            ext.relu_pre = io.pre[l - 1].p;
+            ext.ld_pre = io.pre[l - 1].ld;
+            run_aggregate(G, false, 0, gr.n, yg.m.p, yg.m.ld, gnext->m.p, gnext->m.ld, in_dim, PG_AGG_OVERWRITE, s,
+                          SegSel{}, ext);
+        } else {
+            std::unique_ptr<Tmp> xt;
+            DMat x = xo ? *xo : DMat{};
+            if (!xo) {
+                xt = std::make_unique<Tmp>(n, in_dim, s, F != nullptr);
+                x = xt->m;
+            } else if (F) {
+                PG_CUDA(cudaMemset2DAsync(x.p, x.ld * 4, 0, x.cols * 4, x.rows, s));
+            }
+            run_aggregate(G, false, 0, gr.n, yg.m.p, yg.m.ld, x.p, x.ld, in_dim, PG_AGG_OVERWRITE, s, SegSel{}, ext);
+            if (l > 0) {
+                gnext = std::make_unique<Tmp>(n, in_dim, s);
+                relu_backward_rows(x, io.pre[l - 1], nullptr, gnext->m, s);
+            }
+        }
+        if (io.edges) {
+            if (F) {
+                uint64_t c[4];
+                filter_counts(gr, G.gs, ext.dst_bits, ext.src_bits, c, s);
+                io.edges[L - 1 - l] = c[0];
+            } else {
+                io.edges[L - 1 - l] = gr.m;
+            }
+        }
+        if (l > 0) {
+            gcur = std::move(gnext);
+            g = gcur->m;
+        }
+    }
+}
+
+}  // namespace
+
+void forward(Groups& G, DMat x0, const DMat* w, uint64_t L, DMat* y, DMat* pre, DMat* x, cudaStream_t s) {
+    if (!G.graph) fail(kConfig, "forward: needs a grouping of the full graph");
+    const uint64_t n = G.graph->n;
+    DMat cur = x0;
+    if (x0.rows != n) fail(kConfig, "forward: feature rows != vertex count");
+    for (uint64_t l = 0; l < L; ++l) {
+        if (cur.cols != w[l].rows)
+            fail(kConfig, "forward: feature/weight shape mismatch at layer " + std::to_string(l));
+        if (y[l].rows != n || y[l].cols != cur.cols || pre[l].rows != n || pre[l].cols != w[l].cols ||
+            x[l].rows != n || x[l].cols != w[l].cols)
+            fail(kConfig, "forward: output shape mismatch at layer " + std::to_string(l));
+        run_aggregate(G, false, 0, G.graph->n, cur.p, cur.ld, y[l].p, y[l].ld, cur.cols, PG_AGG_OVERWRITE, s);
+        gemm(y[l], w[l], pre[l], false, s);
+        if (l + 1 < L) relu(pre[l], x[l], s);
+        else row_softmax(pre[l], x[l], s);
+        cur = x[l];
+    }
+}
+
+void backward_all_active(Groups& G, const BackwardIO& io, cudaStream_t s) { backward_full(G, nullptr, io, s); }
+
+void backward_ifelse(Groups& G, Frontiers& F, const BackwardIO& io, cudaStream_t s) { backward_full(G, &F, io, s); }
+
+void backward_epp(Groups* const* PG, Frontiers& F, const BackwardIO& io, int gather_mode, uint64_t expected_fp,
+                  cudaStream_t s) {
+    const uint64_t L = io.L;
+    if (F.L != L) fail(kConfig, "epp backward: paths were prepared for a different layer count");
+    for (uint64_t i = 0; i < L; ++i) {
+        if (!PG[i] || !PG[i]->path) fail(kConfig, "epp backward: every grouping must be over an execution path");
+        if (PG[i]->path->layer != L - 1 - i) fail(kConfig, "epp backward: paths were prepared for a different layer count");
+        if (PG[i]->path->fingerprint != expected_fp)
+            fail(kConfig, "epp backward: execution paths are stale for this graph/training set");
+    }
+    const uint64_t n = F.n;
+    check_chain(io, n);
+    if (gather_mode == 1) {  // Global: full-width matrices, the path walked with global ids
+        if (io.x_grads) fail(kConfig, "epp backward: x_grads are only captured in Local gather mode");
+        std::unique_ptr<Tmp> gcur;
+        DMat g = io.top_grad;
+        for (uint64_t i = 0; i < L; ++i) {
+            const uint64_t l = L - 1 - i, in_dim = io.w[l].rows;
+            Path& p = *PG[i]->path;
+            if (!p.edges_global.get() && p.E) {
+                p.edges_global = DevBuf<Edge>(p.E, s);
+                remap_edges(p.edges_parent.get(), p.E, F.levels[i].ids.get(), p.edges_global.get(), s);
+            }
+            gemm_at_b(io.y[l], nullptr, g, io.w_grads[l], s);
+            Tmp yg(n, in_dim, s);
+            gemm(g, io.w[l], yg.m, true, s);
+            auto gn = std::make_unique<Tmp>(n, in_dim, s, true);  // rows off the path stay +0
+            AggExt ext;
+            ext.out_rows = p.dest.get();
+            if (l > 0) {
+                ext.relu_pre = io.pre[l - 1].p;
+                ext.ld_pre = io.pre[l - 1].ld;
+            }
+            run_aggregate(*PG[i], true, 0, p.D, yg.m.p, yg.m.ld, gn->m.p, gn->m.ld, in_dim, PG_AGG_OVERWRITE, s,
+                          SegSel{}, ext, p.edges_global.get());
+            if (io.edges) io.edges[i] = p.E;
+            gcur = std::move(gn);
+            g = gcur->m;
+        }
+        return;
+    }
+    // Local: compact matrices whose rows follow the frontier arrays
+    const uint64_t c = io.top_grad.cols;
+    auto g0 = std::make_unique<Tmp>(F.levels[0].size, c, s);
+    gather_rows(io.top_grad.p, io.top_grad.ld, F.levels[0].ids.get(), F.levels[0].size, g0->m.p, g0->m.ld, c, s);
+    std::unique_ptr<Tmp> gcur = std::move(g0);
+    for (uint64_t i = 0; i < L; ++i) {
+        const uint64_t l = L - 1 - i, in_dim = io.w[l].rows;
+        Path& p = *PG[i]->path;
+        if (p.P != F.levels[i].size || p.D != F.levels[i + 1].size)
+            fail(kConfig, "epp backward: path does not follow the frontiers");
+        const DMat g = gcur->m;
+        gemm_at_b(io.y[l], F.levels[i].ids.get(), g, io.w_grads[l], s);  // gather_rows(Y, in_rows) fused
+        Tmp yg(p.P, in_dim, s);
+        gemm(g, io.w[l], yg.m, true, s);
+        DMat* xo = io.x_grads ? &io.x_grads[i] : nullptr;
+        if (xo && (xo->rows != p.D || xo->cols != in_dim)) fail(kConfig, "backward: x_grad shape mismatch");
+        std::unique_ptr<Tmp> gn;
+        if (l > 0 && !xo) {  // relu_backward(x_grad, gather_rows(pre, levels[L-l])) in the SpMM epilogue
+            gn = std::make_unique<Tmp>(p.D, in_dim, s);
+            AggExt ext;
+            ext.relu_pre = io.pre[l - 1].p;
+            ext.ld_pre = io.pre[l - 1].ld;
+            ext.pre_rows = p.dest.get();
+            run_aggregate(*PG[i], true, 0, p.D, yg.m.p, yg.m.ld, gn->m.p, gn->m.ld, in_dim, PG_AGG_OVERWRITE, s,
+                          SegSel{}, ext);
+        } else {
+            std::unique_ptr<Tmp> xt;
+            DMat x = xo ? *xo : DMat{};
+            if (!xo) {
+                xt = std::make_unique<Tmp>(p.D, in_dim, s);
+                x = xt->m;
+            }
+            run_aggregate(*PG[i], true, 0, p.D, yg.m.p, yg.m.ld, x.p, x.ld, in_dim, PG_AGG_OVERWRITE, s);
+            if (l > 0) {
+                gn = std::make_unique<Tmp>(p.D, in_dim, s);
+                relu_backward_rows(x, io.pre[l - 1], p.dest.get(), gn->m, s);
+            }
+        }
+        if (io.edges) io.edges[i] = p.E;
+        if (gn) gcur = std::move(gn);
+    }
+}
+
+}  // namespace pg

@@ -97,6 +97,7 @@ struct Path {
     DevBuf<double> w64;           // E, bitwise copies of the parent weights
     DevBuf<Edge> edges_parent;    // E (src_pos_in_parent[nbr], (float)w): gather folded
     DevBuf<Edge> edges_local;     // E (nbr_local, (float)w), lazily, only when S < P
+    DevBuf<Edge> edges_global;    // E (src_local_to_global[nbr], (float)w), lazily (GatherMode::Global)
     DevBuf<uint32_t> order;       // D dests in descending-degree-bucket order (SpMM schedule)
     DegHist hist;                 // degree buckets of `order`
 };
@@ -170,6 +171,20 @@ void grouping_cost_dev(uint32_t D, const uint64_t* offsets_dev, uint32_t gs, uin
                        uint64_t workers, uint64_t* max_load, uint64_t* atomic_writes,
                        cudaStream_t s);
 
+// Optional extensions of the SpMM used by the engine chains (engine.hpp):
+// output-row remap (GatherMode::Global), a fused relu_backward epilogue
+// (dense_matrix.hpp:107-113 applied to the finished row), and the if-else
+// activity filters of aggregate_pull_filtered (aggregate.hpp:127-170).
+struct AggExt {
+    const uint32_t* out_rows = nullptr;  // output row of destination d (default d)
+    const float* relu_pre = nullptr;     // epilogue: out = pre[prow] > 0 ? acc : +0
+    uint64_t ld_pre = 0;
+    const uint32_t* pre_rows = nullptr;  // prow of destination d (default: the output row)
+    const uint32_t* src_bits = nullptr;  // skip edges whose source (edges[e].x) bit is 0
+    const uint32_t* dst_bits = nullptr;  // skip destinations whose bit (of d) is 0: row untouched
+    bool any() const { return out_rows || relu_pre || src_bits || dst_bits; }
+};
+
 // aggregate.hpp:56-122 Deterministic, ascending edge order per element.
 //   out[d] (+)= sum_{e in [ebeg[d], eend[d])} w_e * in[edges[e].x],  d = order[i]
 // (ebeg = offsets, eend = offsets + 1 for whole lists; source-range segments
@@ -178,7 +193,23 @@ void grouping_cost_dev(uint32_t D, const uint64_t* offsets_dev, uint32_t gs, uin
 // the degree-bucket order) run on the TMA-ring kernel concurrently.
 void aggregate_det(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges, const uint32_t* order, uint32_t D,
                    uint32_t d_begin, uint32_t d_end, uint32_t n_heavy, const float* in, uint64_t ld_in,
-                   float* out, uint64_t ld_out, uint64_t dim, bool accumulate, cudaStream_t s);
+                   float* out, uint64_t ld_out, uint64_t dim, bool accumulate, cudaStream_t s,
+                   const AggExt& ext = AggExt{});
+// Source-segment selector for run_aggregate: bounds array [(nseg+1) x D] and
+// the segment to run (seg < 0: whole edge lists).
+struct SegSel {
+    const uint64_t* bnd = nullptr;
+    int seg = -1;
+    uint32_t nseg = 1;
+};
+// The SpMM over a grouping's base (path: parent-indexed or local sources;
+// graph: vertex ids), destination rows [rb, re) with their cached degree
+// schedule; flags = PG_AGG_* of the C ABI. edges_override replaces the
+// path's edge stream (same destinations and order, other source ids).
+void run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re, const float* in, uint64_t ld_in,
+                   float* out, uint64_t ld_out, uint64_t dim, unsigned flags, cudaStream_t s, SegSel sel = {},
+                   const AggExt& ext = AggExt{}, const Edge* edges_override = nullptr);
+
 // PG_HEAVY_MIN_DEG / pg_set_heavy_min_degree (0 disables; UINT64_MAX restores
 // the width-dependent default)
 uint64_t heavy_min_degree(uint64_t dim, uint64_t range_edges);
@@ -207,5 +238,50 @@ void copy_rows(const float* src, uint64_t lds, float* dst, uint64_t ldd, uint64_
 // engine.hpp:162-169
 void gather_rows(const float* src, uint64_t lds, const uint32_t* ids, uint64_t k, float* out,
                  uint64_t ldo, uint64_t cols, cudaStream_t s);
+
+// ---- the GCN chain (engine.cu) -----------------------------------------------
+// A dense fp32 device matrix: rows x cols, row pitch ld floats.
+struct DMat {
+    float* p = nullptr;
+    uint64_t rows = 0, cols = 0, ld = 0;
+};
+// row pitch of the library's own temporaries: 16-byte rows up to 32 floats,
+// whole 128-byte lines beyond
+inline uint64_t pad_ld(uint64_t c) { return c <= 32 ? (c + 3) & ~3ull : (c + 31) & ~31ull; }
+
+// dense_matrix.hpp:40-96: out = a * b (b_transposed: a * b^T, gemm_a_bt)
+void gemm(DMat a, DMat b, DMat out, bool b_transposed, cudaStream_t s);
+// dense_matrix.hpp:57-76: out = a[a_rows]^T * b (a_rows nullable: all rows)
+void gemm_at_b(DMat a, const uint32_t* a_rows, DMat b, DMat out, cudaStream_t s);
+void relu(DMat x, DMat out, cudaStream_t s);
+// out[r] = pre[pre_rows[r]] > 0 ? g[r] : 0 (pre_rows nullable)
+void relu_backward_rows(DMat g, DMat pre, const uint32_t* pre_rows, DMat out, cudaStream_t s);
+void row_softmax(DMat x, DMat out, cudaStream_t s);
+void top_grad_from_probs(DMat probs, DMat ref, const uint32_t* vt, uint64_t k, DMat out, cudaStream_t s);
+// aggregate_pull_filtered counters {edges, groups, edges_skipped,
+// groups_skipped} over the full graph (synchronises s)
+void filter_counts(const Graph& g, uint32_t gs, const uint32_t* dst_bits, const uint32_t* src_bits, uint64_t* c4,
+                   cudaStream_t s);
+
+// engine.hpp:114-140 forward over a full-graph grouping: x[l] = X^(l+1)
+void forward(Groups& graph_groups, DMat x0, const DMat* w, uint64_t L, DMat* y, DMat* pre, DMat* x, cudaStream_t s);
+
+struct BackwardIO {
+    uint64_t L = 0;
+    const DMat* y = nullptr;    // Y^(l), n x in_dim_l
+    const DMat* pre = nullptr;  // pre-activations, n x dims[l]
+    DMat top_grad;              // n x dims[L-1]
+    const DMat* w = nullptr;    // W^(l), in_dim_l x dims[l]
+    DMat* w_grads = nullptr;    // out: in_dim_l x dims[l]
+    DMat* x_grads = nullptr;    // optional out, index L-1-l (layer L-1 first)
+    uint64_t* edges = nullptr;  // optional out: backward_edges_per_layer
+};
+// engine.hpp:267-349 (gather_mode 0 = Local, 1 = Global)
+void backward_epp(Groups* const* path_groups, Frontiers& F, const BackwardIO& io, int gather_mode,
+                  uint64_t expected_fp, cudaStream_t s);
+// engine.hpp:177-214
+void backward_all_active(Groups& graph_groups, const BackwardIO& io, cudaStream_t s);
+// engine.hpp:218-257
+void backward_ifelse(Groups& graph_groups, Frontiers& F, const BackwardIO& io, cudaStream_t s);
 
 }  // namespace pg

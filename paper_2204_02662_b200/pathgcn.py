@@ -618,3 +618,171 @@ def prepare_paths(g: CsrGraph, vt, layers, agg_dims, gs_strategy="regression", w
         gss.append(gs)
         groups.append(group_neighbors(p, gs))
     return PreparedPaths(F, paths, groups, gss, stamp)
+
+
+# ------------------------------------------------- the chain (engine.hpp) ---
+# Device-resident forward / backward variants, bit-exact with the
+# reference's f32 build. Matrices are float32 CUDA tensors (row-major,
+# unit column stride; any row pitch — empty_rows() gives the 16-byte rows
+# the SpMM's 128-bit gathers want).
+
+def _mat(t, name, rows=None, cols=None):
+    _dev(t, name, rows, cols)
+    return _lib.PgMat(t.data_ptr(), t.shape[0], t.shape[1], t.stride(0))
+
+
+def _mats(ts, name):
+    arr = (_lib.PgMat * max(len(ts), 1))()
+    for i, t in enumerate(ts):
+        arr[i] = _mat(t, f"{name}[{i}]")
+    return arr
+
+
+def gemm(a, b, out, stream=None):
+    """dense_matrix.hpp:40-55: out = a * b."""
+    _check(_lib_().pg_gemm(_mat(a, "a"), _mat(b, "b"), 0, _mat(out, "out"), _stream(stream)))
+    return out
+
+
+def gemm_at_b(a, b, out, a_rows=None, stream=None):
+    """dense_matrix.hpp:57-76: out = a^T * b; with a_rows (int32/uint32 CUDA
+    tensor of b.rows ids) out = gather_rows(a, a_rows)^T * b."""
+    rows = None if a_rows is None else C.c_void_p(a_rows.data_ptr())
+    _check(_lib_().pg_gemm_at_b(_mat(a, "a"), rows, _mat(b, "b"), _mat(out, "out"), _stream(stream)))
+    return out
+
+
+def relu(x, out, stream=None):
+    """dense_matrix.hpp:98-104"""
+    _check(_lib_().pg_relu(_mat(x, "x"), _mat(out, "out"), _stream(stream)))
+    return out
+
+
+def row_softmax(x, out, stream=None):
+    """dense_matrix.hpp:116-135 (expf bit-exact with glibc)."""
+    _check(_lib_().pg_row_softmax(_mat(x, "x"), _mat(out, "out"), _stream(stream)))
+    return out
+
+
+def top_grad_from_probs(probs, ref, vt_dev, out, stream=None):
+    """engine.hpp:146-156 (vt_dev: int32/uint32 CUDA tensor of V_t)."""
+    _check(_lib_().pg_top_grad_from_probs(_mat(probs, "probs"), _mat(ref, "ref"), C.c_void_p(vt_dev.data_ptr()),
+                                          vt_dev.shape[0], _mat(out, "out"), _stream(stream)))
+    return out
+
+
+def aggregate_pull_filtered(grouped: GroupedCsr, frontiers: FrontierSets, dest_level, src_level, inp, out,
+                            overwrite=False, counters=None, stream=None):
+    """aggregate.hpp:127-210 (Deterministic): destinations outside frontier
+    level dest_level keep their rows, sources outside src_level are
+    skipped. ``counters`` (dict) receives the reference's StageCounters."""
+    _dev(inp, "input")
+    _dev(out, "output", cols=inp.shape[1])
+    c = np.zeros(4, np.uint64) if counters is not None else None
+    _check(_lib_().pg_aggregate_pull_filtered(grouped._h, frontiers._h, dest_level, src_level,
+                                              C.c_void_p(inp.data_ptr()), inp.shape[0], inp.stride(0),
+                                              C.c_void_p(out.data_ptr()), out.stride(0), inp.shape[1],
+                                              _flags(DETERMINISTIC, overwrite),
+                                              None if c is None else _p(c, u64p), _stream(stream)))
+    if counters is not None:
+        for k, v in zip(("edges_traversed", "groups_executed", "edges_skipped", "groups_skipped"), c.tolist()):
+            counters[k] = counters.get(k, 0) + int(v)
+    return out
+
+
+@dataclass
+class EpochArtifacts:
+    """engine.hpp:27-31: x[0..L], y[0..L-1], pre_act[0..L-1] (device)."""
+    x: list
+    y: list
+    pre_act: list
+
+
+def forward(graph_grouped: GroupedCsr, x0, weights, stream=None) -> EpochArtifacts:
+    """engine.hpp:114-140 over a full-graph grouping."""
+    import torch
+
+    n = x0.shape[0]
+    y, pre, xs = [], [], []
+    cur = x0.shape[1]
+    for w in weights:
+        y.append(empty_rows(n, cur, device=x0.device))
+        pre.append(empty_rows(n, w.shape[1], device=x0.device))
+        xs.append(empty_rows(n, w.shape[1], device=x0.device))
+        cur = w.shape[1]
+    _check(_lib_().pg_forward(graph_grouped._h, _mat(x0, "x0"), _mats(weights, "w"), len(weights), _mats(y, "y"),
+                              _mats(pre, "pre"), _mats(xs, "x"), _stream(stream)))
+    del torch
+    return EpochArtifacts([x0] + xs, y, pre)
+
+
+def _wgrads(weights):
+    return [empty_rows(w.shape[0], w.shape[1], device=w.device) for w in weights]
+
+
+def backward_epp(prepared: PreparedPaths, arts: EpochArtifacts, top_grad, weights, gather="local",
+                 expected_fingerprint=None, x_grads_out=None, counters=None, stream=None):
+    """engine.hpp:267-349. Returns W' per layer. ``x_grads_out`` (list)
+    receives X^(l)' per path (Local mode); ``counters`` (dict) gets
+    backward_edges_per_layer."""
+    L = len(weights)
+    if len(prepared.groups) != L or prepared.frontiers.L != L:  # engine.hpp:278-279
+        raise StalenessError("epp backward: paths were prepared for a different layer count")
+    fp = prepared.fingerprint if expected_fingerprint is None else expected_fingerprint
+    hs = (C.c_void_p * max(L, 1))(*[g._h.value for g in prepared.groups])
+    wg = _wgrads(weights)
+    xg = None
+    if x_grads_out is not None:
+        xg = [empty_rows(prepared.paths[i].D, weights[L - 1 - i].shape[0], device=top_grad.device) for i in range(L)]
+    e = np.zeros(max(L, 1), np.uint64)
+    _check(_lib_().pg_backward_epp(hs, prepared.frontiers._h, L, _mats(arts.y, "y"), _mats(arts.pre_act, "pre"),
+                                   _mat(top_grad, "top_grad"), _mats(weights, "w"), fp,
+                                   {"local": 0, "global": 1}[gather], _mats(wg, "w_grads"),
+                                   None if xg is None else _mats(xg, "x_grads"), _p(e, u64p), _stream(stream)))
+    if x_grads_out is not None:
+        x_grads_out.extend(xg)
+    if counters is not None:
+        counters["backward_edges_per_layer"] = e[:L].tolist()
+    return wg
+
+
+def backward_all_active(graph_grouped: GroupedCsr, arts: EpochArtifacts, top_grad, weights, x_grads_out=None,
+                        counters=None, stream=None):
+    """engine.hpp:177-214 (Alg. 1 over the full graph)."""
+    L = len(weights)
+    n = top_grad.shape[0]
+    wg = _wgrads(weights)
+    xg = None
+    if x_grads_out is not None:
+        xg = [empty_rows(n, weights[L - 1 - i].shape[0], device=top_grad.device) for i in range(L)]
+    e = np.zeros(max(L, 1), np.uint64)
+    _check(_lib_().pg_backward_all_active(graph_grouped._h, L, _mats(arts.y, "y"), _mats(arts.pre_act, "pre"),
+                                          _mat(top_grad, "top_grad"), _mats(weights, "w"), _mats(wg, "w_grads"),
+                                          None if xg is None else _mats(xg, "x_grads"), _p(e, u64p),
+                                          _stream(stream)))
+    if x_grads_out is not None:
+        x_grads_out.extend(xg)
+    if counters is not None:
+        counters["backward_edges_per_layer"] = e[:L].tolist()
+    return wg
+
+
+def backward_ifelse(graph_grouped: GroupedCsr, frontiers: FrontierSets, arts: EpochArtifacts, top_grad, weights,
+                    x_grads_out=None, counters=None, stream=None):
+    """engine.hpp:218-257 (full graph with the frontier activity tests)."""
+    L = len(weights)
+    n = top_grad.shape[0]
+    wg = _wgrads(weights)
+    xg = None
+    if x_grads_out is not None:
+        xg = [empty_rows(n, weights[L - 1 - i].shape[0], device=top_grad.device) for i in range(L)]
+    e = np.zeros(max(L, 1), np.uint64)
+    _check(_lib_().pg_backward_ifelse(graph_grouped._h, frontiers._h, L, _mats(arts.y, "y"),
+                                      _mats(arts.pre_act, "pre"), _mat(top_grad, "top_grad"), _mats(weights, "w"),
+                                      _mats(wg, "w_grads"), None if xg is None else _mats(xg, "x_grads"),
+                                      None if counters is None else _p(e, u64p), _stream(stream)))
+    if x_grads_out is not None:
+        x_grads_out.extend(xg)
+    if counters is not None:
+        counters["backward_edges_per_layer"] = e[:L].tolist()
+    return wg
