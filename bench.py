@@ -250,6 +250,7 @@ def main():
     ap.add_argument("--profile", action="store_true", help="few steps, no extras (for ncu)")
     ap.add_argument("--heavy-sweep", action="store_true", help="diagnostics: heavy-kernel threshold sweep")
     ap.add_argument("--tune-sweep", action="store_true", help="diagnostics: SpMM scheduling-knob sweep")
+    ap.add_argument("--no-chain", action="store_true", help="skip the forward/backward-variant chain timing")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -441,6 +442,8 @@ def main():
     if not args.profile and not args.no_e2e:
         line["e2e"] = measure_e2e(pg, pgd, torch, dist, paths, groups, shards, dims, rows, world, rank, dev,
                                   max(3, min(args.steps, 10)), ep_bytes)
+    if not args.profile and not args.no_chain and world == 1:
+        line["chain"] = measure_chain(pg, torch, g, prep, cfg, vt, dev)
     if not args.profile and not args.no_cpu and world == 1 and rank == 0:
         line["cpu_baseline"] = cpu_baseline(paths, dims, args)
 
@@ -450,6 +453,68 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def measure_chain(pg, torch, g, prep, cfg, vt, dev, reps=5):
+    """The whole device-resident GCN chain on the same graph (SURVEY §8f
+    rank 1-3): forward (engine.hpp:114-140) and the three backward variants
+    of the paper's Fig. 6 comparison — all-active (Alg. 1), if-else, and the
+    execution-path backward_epp (Local, relu fused into the SpMM) — each
+    timed whole with CUDA events (median of reps after a warm-up). Random
+    weights / features; the chain is bit-exact with the reference
+    (tests/test_gpu_chain.py)."""
+    n, f, dims = g.n, cfg["f"], cfg["dims"]
+    L = len(dims)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(GRAD_SEED + 7)
+    x0 = pg.empty_rows(n, f, device=dev)
+    x0.uniform_(0, 1, generator=gen)
+    ins = [f] + dims[:-1]
+    ws = []
+    for l in range(L):
+        w = pg.empty_rows(ins[l], dims[l], device=dev)
+        w.uniform_(-0.1, 0.1, generator=gen)
+        ws.append(w)
+    r = pg.empty_rows(n, dims[-1], device=dev)
+    r.zero_()
+    vtd = torch.from_numpy(vt.astype(np.int32)).to(dev)
+    r[vtd.long(), torch.randint(0, dims[-1], (len(vt),), device=dev, generator=gen)] = 1.0
+    Gg = pg.group_neighbors(g, 1)
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return round(statistics.median(ts), 3)
+
+    arts = pg.forward(Gg, x0, ws)
+    top = pg.empty_rows(n, dims[-1], device=dev)
+    pg.top_grad_from_probs(arts.x[-1], r, vtd, top)
+    out = {"forward_ms": timed(lambda: pg.forward(Gg, x0, ws)),
+           "backward_epp_ms": timed(lambda: pg.backward_epp(prep, arts, top, ws)),
+           "backward_epp_global_ms": timed(lambda: pg.backward_epp(prep, arts, top, ws, gather="global")),
+           "backward_all_active_ms": timed(lambda: pg.backward_all_active(Gg, arts, top, ws)),
+           "backward_ifelse_ms": timed(lambda: pg.backward_ifelse(Gg, prep.frontiers, arts, top, ws))}
+    c_epp, c_all, c_if = {}, {}, {}
+    pg.backward_epp(prep, arts, top, ws, counters=c_epp)
+    pg.backward_all_active(Gg, arts, top, ws, counters=c_all)
+    pg.backward_ifelse(Gg, prep.frontiers, arts, top, ws, counters=c_if)
+    out["backward_edges_per_layer"] = {"epp": c_epp["backward_edges_per_layer"],
+                                       "all_active": c_all["backward_edges_per_layer"],
+                                       "ifelse": c_if["backward_edges_per_layer"]}
+    out["epp_speedup_vs_all_active"] = round(out["backward_all_active_ms"] / out["backward_epp_ms"], 3)
+    out["epp_speedup_vs_ifelse"] = round(out["backward_ifelse_ms"] / out["backward_epp_ms"], 3)
+    out["note"] = "whole chains incl. W' and y_grad products; random-init weights, U(0,1) features"
+    del arts, top, x0
+    torch.cuda.synchronize()
+    return out
 
 
 def time_steps(torch, step, L, reps=10):

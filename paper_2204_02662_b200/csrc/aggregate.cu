@@ -885,43 +885,6 @@ void launch_vec4(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges, 
     PG_LAUNCH("k_agg_vec4");
 }
 
-// dense_matrix.hpp:78-95: out[i][j] = sum_k a[i][k] * b[j][k] in ascending
-// k with separately rounded mul/add, then + 0. Block: 128 columns j x 32 rows
-// i; b^T chunk and the a-row tile staged in shared memory, k in chunks of 32.
-constexpr int kGemmJ = 128, kGemmI = 32, kGemmK = 32;
-
-__global__ void __launch_bounds__(kGemmJ) k_gemm_a_bt(const float* __restrict__ a, uint64_t lda,
-                                                     const float* __restrict__ b, uint64_t ldb,
-                                                     float* __restrict__ out, uint64_t ldo, uint64_t n,
-                                                     uint64_t m, uint64_t K) {
-    __shared__ float bt[kGemmK][kGemmJ];
-    __shared__ float at[kGemmI][kGemmK + 1];
-    const uint64_t j = blockIdx.x * static_cast<uint64_t>(kGemmJ) + threadIdx.x;
-    const uint64_t i0 = blockIdx.y * static_cast<uint64_t>(kGemmI);
-    float acc[kGemmI];
-#pragma unroll
-    for (int r = 0; r < kGemmI; ++r) acc[r] = 0.f;
-    for (uint64_t k0 = 0; k0 < K; k0 += kGemmK) {
-        const int kc = static_cast<int>(K - k0 < kGemmK ? K - k0 : kGemmK);
-        __syncthreads();
-        for (int kk = 0; kk < kc; ++kk) bt[kk][threadIdx.x] = j < m ? b[j * ldb + k0 + kk] : 0.f;
-        for (int idx = threadIdx.x; idx < kGemmI * kGemmK; idx += kGemmJ) {
-            const int r = idx / kGemmK, kk = idx % kGemmK;
-            at[r][kk] = (i0 + r < n && kk < kc) ? a[(i0 + r) * lda + k0 + kk] : 0.f;
-        }
-        __syncthreads();
-        for (int kk = 0; kk < kc; ++kk) {
-            const float bv = bt[kk][threadIdx.x];
-#pragma unroll
-            for (int r = 0; r < kGemmI; ++r) acc[r] = __fadd_rn(acc[r], __fmul_rn(at[r][kk], bv));
-        }
-    }
-    if (j >= m) return;
-#pragma unroll
-    for (int r = 0; r < kGemmI; ++r)
-        if (i0 + r < n) out[(i0 + r) * ldo + j] = __fadd_rn(acc[r], 0.f);
-}
-
 __global__ void k_relu_backward(const float* __restrict__ g, uint64_t ldg, const float* __restrict__ pre,
                                 uint64_t ldp, float* __restrict__ out, uint64_t ldo, uint64_t rows,
                                 uint64_t cols) {
@@ -1059,14 +1022,6 @@ void aggregate_det(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges
     } else {
         launch_vec4<4, 8>(ebeg, eend, edges, order, d_begin, nd, 1, in, ld_in, out, ld_out, dim32, accumulate, s, ext);
     }
-}
-
-void gemm_a_bt(const float* a, uint64_t lda, const float* b, uint64_t ldb, float* out, uint64_t ldo,
-               uint64_t n, uint64_t m, uint64_t k, cudaStream_t s) {
-    if (n == 0 || m == 0) return;
-    dim3 grid(static_cast<unsigned>((m + kGemmJ - 1) / kGemmJ), static_cast<unsigned>((n + kGemmI - 1) / kGemmI));
-    k_gemm_a_bt<<<grid, kGemmJ, 0, s>>>(a, lda, b, ldb, out, ldo, n, m, k);
-    PG_LAUNCH("k_gemm_a_bt");
 }
 
 void relu_backward(const float* grad, uint64_t ldg, const float* pre, uint64_t ldp, float* out, uint64_t ldo,

@@ -905,7 +905,8 @@ int pg_gemm_a_bt(const float* a, uint64_t lda, const float* b, uint64_t ldb, flo
                  uint64_t m, uint64_t k, void* stream) {
     return guard([&] {
         if (lda < k || ldb < k || ldo < m) fail(kConfig, "gemm_a_bt: leading dimension too small");
-        gemm_a_bt(a, lda, b, ldb, out, ldo, n, m, k, static_cast<cudaStream_t>(stream));
+        gemm(DMat{const_cast<float*>(a), n, k, lda}, DMat{const_cast<float*>(b), m, k, ldb}, DMat{out, n, m, ldo},
+             true, static_cast<cudaStream_t>(stream));
     });
 }
 

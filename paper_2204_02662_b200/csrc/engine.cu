@@ -40,8 +40,8 @@ __global__ void __launch_bounds__(256) k_gemm(const float* __restrict__ a, uint6
     __shared__ float as[kGI][kGT + 1];
     __shared__ float bs[kGT][kGT + 1];
     const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const uint64_t j = blockIdx.x * static_cast<uint64_t>(kGT) + lane;
-    const uint64_t i0 = blockIdx.y * static_cast<uint64_t>(kGI);
+    const uint64_t j = blockIdx.y * static_cast<uint64_t>(kGT) + lane;
+    const uint64_t i0 = blockIdx.x * static_cast<uint64_t>(kGI);  // rows on x: no 65535 cap
     float acc[kGRPW];
 #pragma unroll
     for (int r = 0; r < kGRPW; ++r) acc[r] = 0.f;
@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(256) k_gemm(const float* __restrict__ a, uint6
         }
         for (int idx = threadIdx.x; idx < kGT * kGT; idx += 256) {
             const int kk = idx / kGT, jj = idx % kGT;
-            const uint64_t jg = blockIdx.x * static_cast<uint64_t>(kGT) + jj;
+            const uint64_t jg = blockIdx.y * static_cast<uint64_t>(kGT) + jj;
             float v = 0.f;
             if (kk < kc && jg < m) v = BT ? b[jg * ldb + k0 + kk] : b[(k0 + kk) * ldb + jg];
             bs[kk][jj] = v;
@@ -77,44 +77,103 @@ __global__ void __launch_bounds__(256) k_gemm(const float* __restrict__ a, uint6
 // ---- out = A[rows]^T * B (dense_matrix.hpp:57-76 gemm_at_b) -----------------
 // out[i][j] = sum over k < n, ascending, of A(k, i) * B(k, j), A(k, i) =
 // a[(rows ? rows[k] : k) * lda + i] (the engine's gather_rows fused in).
-// One thread per (i, j): the chain runs over all n rows in order, so the
-// only parallelism is the r x c outputs; rows are staged KC at a time.
-constexpr int kAtbKC = 128;
+// The order forces one serial chain per output over all n rows, so the
+// only parallelism is the r x c outputs and the floor is n dependent FADDs.
+// A 128-thread block owns TI columns of A x TC columns of B, one chain per
+// thread; rows stream through a kAtbStages-deep cp.async pipeline of
+// KC-row tiles, so a chain step is two shared loads (immediate
+// offsets: TI/TC are compile-time) + FMUL + FADD.
+constexpr int kAtbStages = 4;
 
-template <int TI, int TJ>
-__global__ void __launch_bounds__(TI* TJ) k_gemm_at_b(const float* __restrict__ a, uint64_t lda,
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* dst, const void* src, bool ok) {
+    if (BYTES == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                         static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                     "l"(src), "r"(ok ? 16 : 0)
+                     : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(
+                         static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                     "l"(src), "r"(ok ? 4 : 0)
+                     : "memory");
+}
+
+// V = floats per cp.async (4: 16-byte copies, needs 16-byte aligned rows and
+// column tiles; 1: any layout)
+template <int TI, int TC, int V>
+__host__ __device__ constexpr int atb_kc() {  // rows per tile: the stage ring stays under 48 KB of static smem
+    return TC <= 32 ? 64 : (TC <= 64 ? 32 : 16);
+}
+
+template <int TI, int TC, int V>
+__global__ void __launch_bounds__(TI* TC) k_gemm_at_b(const float* __restrict__ a, uint64_t lda,
                                                       const uint32_t* __restrict__ rows, const float* __restrict__ b,
                                                       uint64_t ldb, float* __restrict__ out, uint64_t ldo, uint64_t n,
                                                       uint64_t r, uint64_t c) {
-    __shared__ float as[kAtbKC][TI];
-    __shared__ float bs[kAtbKC][TJ + 1];
-    const unsigned ti = threadIdx.x / TJ, tj = threadIdx.x % TJ;
-    const uint64_t i = blockIdx.x * static_cast<uint64_t>(TI) + ti;
-    const uint64_t j = blockIdx.y * static_cast<uint64_t>(TJ) + tj;
-    float acc = 0.f;
-    for (uint64_t k0 = 0; k0 < n; k0 += kAtbKC) {
-        const int kc = static_cast<int>(n - k0 < kAtbKC ? n - k0 : kAtbKC);
-        __syncthreads();
-        for (int idx = threadIdx.x; idx < kAtbKC * TI; idx += TI * TJ) {
-            const int kk = idx / TI, ii = idx % TI;
-            const uint64_t ig = blockIdx.x * static_cast<uint64_t>(TI) + ii;
-            float v = 0.f;
-            if (kk < kc && ig < r) {
-                const uint64_t row = rows ? __ldg(rows + k0 + kk) : k0 + kk;
-                v = a[row * lda + ig];
-            }
-            as[kk][ii] = v;
+    constexpr int kAtbKC = atb_kc<TI, TC, V>();
+    constexpr int NT = TI * TC;
+    constexpr int TILE = kAtbKC * (TI + TC);
+    __shared__ __align__(16) float sm[kAtbStages * TILE];
+    const unsigned tid = threadIdx.x;
+    const uint64_t i0 = blockIdx.x * static_cast<uint64_t>(TI), j0 = blockIdx.y * static_cast<uint64_t>(TC);
+    const unsigned ti = tid / TC, tj = tid % TC;
+    const uint64_t ntiles = (n + kAtbKC - 1) / kAtbKC;
+    auto load = [&](uint64_t t) {
+        float* st = sm + (t % kAtbStages) * TILE;
+        const uint64_t k0 = t * kAtbKC;
+        constexpr int AV = TI % V == 0 ? V : 1;  // A tile rows of TI floats
+        for (int e = tid; e < kAtbKC * TI / AV; e += NT) {
+            const int kk = e / (TI / AV), ii = (e % (TI / AV)) * AV;
+            const bool ok = k0 + kk < n && i0 + ii < r;
+            const uint64_t row = ok ? (rows ? __ldg(rows + k0 + kk) : k0 + kk) : 0;
+            cp_async<AV * 4>(st + kk * TI + ii, ok ? a + row * lda + i0 + ii : a, ok);
         }
-        for (int idx = threadIdx.x; idx < kAtbKC * TJ; idx += TI * TJ) {
-            const int kk = idx / TJ, jj = idx % TJ;
-            const uint64_t jg = blockIdx.y * static_cast<uint64_t>(TJ) + jj;
-            bs[kk][jj] = (kk < kc && jg < c) ? b[(k0 + kk) * ldb + jg] : 0.f;
+        float* sb = st + kAtbKC * TI;
+        for (int e = tid; e < kAtbKC * TC / V; e += NT) {
+            const int kk = e / (TC / V), jj = (e % (TC / V)) * V;
+            const bool ok = k0 + kk < n && j0 + jj < c;
+            cp_async<V * 4>(sb + kk * TC + jj, ok ? b + (k0 + kk) * ldb + j0 + jj : b, ok);
         }
-        __syncthreads();
-#pragma unroll 8
-        for (int kk = 0; kk < kc; ++kk) acc = __fadd_rn(acc, __fmul_rn(as[kk][ti], bs[kk][tj]));
+    };
+#pragma unroll
+    for (int t = 0; t < kAtbStages - 1; ++t) {
+        if (static_cast<uint64_t>(t) < ntiles) load(t);
+        asm volatile("cp.async.commit_group;" ::: "memory");
     }
+    float acc = 0.f;
+    for (uint64_t t = 0; t < ntiles; ++t) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(kAtbStages - 2) : "memory");
+        __syncthreads();  // tile t resident for every thread; tile t-1's slot is free
+        if (t + kAtbStages - 1 < ntiles) load(t + kAtbStages - 1);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        const float* sa = sm + (t % kAtbStages) * TILE + ti;
+        const float* sb = sm + (t % kAtbStages) * TILE + kAtbKC * TI + tj;
+        const uint64_t rem = n - t * kAtbKC;
+        if (rem >= static_cast<uint64_t>(kAtbKC)) {
+#pragma unroll
+            for (int kk = 0; kk < kAtbKC; ++kk) acc = __fadd_rn(acc, __fmul_rn(sa[kk * TI], sb[kk * TC]));
+        } else {
+            for (int kk = 0; kk < static_cast<int>(rem); ++kk)
+                acc = __fadd_rn(acc, __fmul_rn(sa[kk * TI], sb[kk * TC]));
+        }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    const uint64_t i = i0 + ti, j = j0 + tj;
     if (i < r && j < c) out[i * ldo + j] = __fadd_rn(acc, 0.f);
+}
+
+template <int TI, int TC>
+void launch_at_b(DMat a, const uint32_t* rows, DMat b, DMat out, uint64_t n, uint64_t r, uint64_t c,
+                 cudaStream_t s) {
+    dim3 grid(static_cast<unsigned>((r + TI - 1) / TI), static_cast<unsigned>((c + TC - 1) / TC));
+    const bool v4 = a.ld % 4 == 0 && b.ld % 4 == 0 && reinterpret_cast<uintptr_t>(a.p) % 16 == 0 &&
+                    reinterpret_cast<uintptr_t>(b.p) % 16 == 0;
+    if (v4)
+        k_gemm_at_b<TI, TC, 4><<<grid, TI * TC, 0, s>>>(a.p, a.ld, rows, b.p, b.ld, out.p, out.ld, n, r, c);
+    else
+        k_gemm_at_b<TI, TC, 1><<<grid, TI * TC, 0, s>>>(a.p, a.ld, rows, b.p, b.ld, out.p, out.ld, n, r, c);
+    PG_LAUNCH("k_gemm_at_b");
 }
 
 // ---- elementwise / row kernels ---------------------------------------------
@@ -252,7 +311,7 @@ void gemm(DMat a, DMat b, DMat out, bool b_transposed, cudaStream_t s) {
         PG_CUDA(cudaMemset2DAsync(out.p, out.ld * 4, 0, m * 4, n, s));
         return;
     }
-    dim3 grid(static_cast<unsigned>((m + kGT - 1) / kGT), static_cast<unsigned>((n + kGI - 1) / kGI));
+    dim3 grid(static_cast<unsigned>((n + kGI - 1) / kGI), static_cast<unsigned>((m + kGT - 1) / kGT));
     if (b_transposed)
         k_gemm<true><<<grid, 256, 0, s>>>(a.p, a.ld, b.p, b.ld, out.p, out.ld, n, m, K);
     else
@@ -265,14 +324,11 @@ void gemm_at_b(DMat a, const uint32_t* a_rows, DMat b, DMat out, cudaStream_t s)
     if (!a_rows && a.rows != n) fail(kConfig, "gemm_at_b: row counts differ");
     if (out.rows != r || out.cols != c) fail(kConfig, "gemm_at_b: output shape mismatch");
     if (r == 0 || c == 0) return;
-    if (c <= 16) {
-        dim3 grid(static_cast<unsigned>((r + 3) / 4), static_cast<unsigned>((c + 15) / 16));
-        k_gemm_at_b<4, 16><<<grid, 64, 0, s>>>(a.p, a.ld, a_rows, b.p, b.ld, out.p, out.ld, n, r, c);
-    } else {
-        dim3 grid(static_cast<unsigned>((r + 3) / 4), static_cast<unsigned>((c + 31) / 32));
-        k_gemm_at_b<4, 32><<<grid, 128, 0, s>>>(a.p, a.ld, a_rows, b.p, b.ld, out.p, out.ld, n, r, c);
-    }
-    PG_LAUNCH("k_gemm_at_b");
+    // 128 chains per block: the column tile of B fitted to c
+    if (c <= 16) launch_at_b<8, 16>(a, a_rows, b, out, n, r, c, s);
+    else if (c <= 32) launch_at_b<4, 32>(a, a_rows, b, out, n, r, c, s);
+    else if (c <= 64) launch_at_b<2, 64>(a, a_rows, b, out, n, r, c, s);
+    else launch_at_b<1, 128>(a, a_rows, b, out, n, r, c, s);
 }
 
 void relu(DMat x, DMat out, cudaStream_t s) {

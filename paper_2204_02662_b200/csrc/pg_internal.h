@@ -226,9 +226,6 @@ enum TuneKeyId {
 int64_t tuning(int key);
 bool set_tuning(const char* name, int64_t value);
 
-// dense_matrix.hpp:78-95 (fp32, ascending k, mul/add separately rounded, +0).
-void gemm_a_bt(const float* a, uint64_t lda, const float* b, uint64_t ldb, float* out,
-               uint64_t ldo, uint64_t n, uint64_t m, uint64_t k, cudaStream_t s);
 // dense_matrix.hpp:114-121
 void relu_backward(const float* grad, uint64_t ldg, const float* pre, uint64_t ldp, float* out,
                    uint64_t ldo, uint64_t rows, uint64_t cols, cudaStream_t s);
