@@ -53,6 +53,7 @@ typedef struct pg_graph_s* pg_graph;         /* CsrGraph      csr_graph.hpp:19-3
 typedef struct pg_frontiers_s* pg_frontiers; /* FrontierSets  frontier.hpp:14-18    */
 typedef struct pg_path_s* pg_path;           /* ExecutionPath execution_path.hpp:16-33 */
 typedef struct pg_groups_s* pg_groups;       /* GroupedCsr    grouping.hpp:14-28    */
+typedef struct pg_edge_list_s* pg_edge_list; /* EdgeList      edge_list.hpp:14-18   */
 
 int pg_last_error(char* buf, size_t cap);
 int pg_version(void);
@@ -83,6 +84,27 @@ int pg_gen_rmat(uint32_t n, uint64_t m, double a, double b, double c, double d, 
 /* training_set.cpp:28-49 sample_training_set (host). *k = max(1, llround(ratio*n)). */
 int pg_training_set_size(uint32_t n, double ratio, uint64_t* k);
 int pg_sample_training_set(uint32_t n, double ratio, uint64_t seed, uint32_t* out);
+
+/* edge_list.cpp:34-62 load_edge_list_file: "src dst" lines, '#' comments and
+ * blank lines skipped, tokens trimmed, ids strict non-negative u32; self
+ * loops dropped and counted. Malformed line -> PG_ERR_CONFIG (ParseError,
+ * the message ends "(line N)"); unreadable file -> PG_ERR_IO. */
+int pg_edge_list_load(const char* path, pg_edge_list* out);
+int pg_edge_list_info(pg_edge_list el, uint64_t* npairs, uint64_t* self_loops_dropped);
+int pg_edge_list_export(pg_edge_list el, uint32_t* pairs);  /* 2*npairs ids */
+int pg_edge_list_destroy(pg_edge_list el);
+/* edge_list.cpp:70-73 write_edge_list ("u v" per line) */
+int pg_edge_list_write(const char* path, const uint32_t* pairs, uint64_t npairs);
+/* load_edge_list_file + build_undirected_csr + assign_edge_weights
+ * (no n_hint: n = 1 + max id), the graph built on `device` */
+int pg_graph_load_file(int device, const char* path, int weight_mode, pg_graph* out);
+/* training_set.cpp:51-73 load_training_set: one id per line (std::stoll),
+ * '#' comments and blank lines skipped; ids >= n or negative ->
+ * PG_ERR_CONFIG; sorted, de-duplicated; empty -> PG_ERR_CONFIG. out NULL:
+ * only *k. Otherwise cap must be >= *k. */
+int pg_training_set_load(const char* path, uint32_t n, uint32_t* out, uint64_t cap, uint64_t* k);
+/* training_set.cpp:81-83 write_training_set (one id per line) */
+int pg_training_set_write(const char* path, const uint32_t* vt, uint64_t k);
 
 /* csr_graph.cpp:33-63 build_undirected_csr + :65-77 assign_edge_weights, on
  * device. n_hint < 0: none. pairs: 2*npairs host ids. */

@@ -78,6 +78,14 @@ SIGNATURES = {
     "pg_gen_rmat": [u32, u64, f64, f64, f64, f64, u64, u32p, u32p],
     "pg_training_set_size": [u32, f64, u64p],
     "pg_sample_training_set": [u32, f64, u64, u32p],
+    "pg_edge_list_load": [C.c_char_p, C.POINTER(H)],
+    "pg_edge_list_info": [H, u64p, u64p],
+    "pg_edge_list_export": [H, u32p],
+    "pg_edge_list_destroy": [H],
+    "pg_edge_list_write": [C.c_char_p, u32p, u64],
+    "pg_graph_load_file": [i32, C.c_char_p, i32, C.POINTER(H)],
+    "pg_training_set_load": [C.c_char_p, u32, u32p, u64, u64p],
+    "pg_training_set_write": [C.c_char_p, u32p, u64],
     "pg_graph_build": [i32, i64, u32p, u64, i32, C.POINTER(H)],
     "pg_graph_create": [i32, u32, u64p, u32p, f64p, i32, C.POINTER(H)],
     "pg_graph_assign_weights": [H, i32],

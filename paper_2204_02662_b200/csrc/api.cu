@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <numeric>
 #include <random>
 #include <string>
@@ -441,6 +442,60 @@ int pg_graph_build(int device, int64_t n_hint, const uint32_t* pairs, uint64_t n
         auto g = graph_build(device, n_hint, pairs, npairs, weight_mode);
         *out = reinterpret_cast<pg_graph>(g.release());
     });
+}
+
+int pg_edge_list_load(const char* path, pg_edge_list* out) {
+    return guard([&] {
+        if (!out) fail(kConfig, "edge_list_load: null output handle");
+        auto el = std::make_unique<EdgeListData>(load_edge_list(path));
+        *out = reinterpret_cast<pg_edge_list>(el.release());
+    });
+}
+
+int pg_edge_list_info(pg_edge_list h, uint64_t* npairs, uint64_t* self_loops_dropped) {
+    return guard([&] {
+        auto* el = need(reinterpret_cast<EdgeListData*>(h), "edge list");
+        if (npairs) *npairs = el->pairs.size() / 2;
+        if (self_loops_dropped) *self_loops_dropped = el->self_loops;
+    });
+}
+
+int pg_edge_list_export(pg_edge_list h, uint32_t* pairs) {
+    return guard([&] {
+        auto* el = need(reinterpret_cast<EdgeListData*>(h), "edge list");
+        if (!el->pairs.empty()) std::memcpy(pairs, el->pairs.data(), el->pairs.size() * 4);
+    });
+}
+
+int pg_edge_list_destroy(pg_edge_list h) {
+    delete reinterpret_cast<EdgeListData*>(h);
+    return PG_OK;
+}
+
+int pg_edge_list_write(const char* path, const uint32_t* pairs, uint64_t npairs) {
+    return guard([&] { write_edge_list(path, pairs, npairs); });
+}
+
+int pg_graph_load_file(int device, const char* path, int weight_mode, pg_graph* out) {
+    return guard([&] {
+        const EdgeListData el = load_edge_list(path);
+        auto g = graph_build(device, -1, el.pairs.data(), el.pairs.size() / 2, weight_mode);
+        *out = reinterpret_cast<pg_graph>(g.release());
+    });
+}
+
+int pg_training_set_load(const char* path, uint32_t n, uint32_t* out, uint64_t cap, uint64_t* k) {
+    return guard([&] {
+        const std::vector<uint32_t> vt = load_training_set(path, n);
+        if (k) *k = vt.size();
+        if (!out) return;
+        if (cap < vt.size()) fail(kConfig, "training_set_load: output capacity too small");
+        std::memcpy(out, vt.data(), vt.size() * 4);
+    });
+}
+
+int pg_training_set_write(const char* path, const uint32_t* vt, uint64_t k) {
+    return guard([&] { write_training_set(path, vt, k); });
 }
 
 int pg_graph_create(int device, uint32_t n, const uint64_t* offsets, const uint32_t* neighbors,

@@ -147,6 +147,16 @@ void segment_bounds(const uint64_t* offsets, const Edge* edges, uint32_t D, cons
 // edges_out[e] = (map[edges_in[e].x], edges_in[e].y)
 void remap_edges(const Edge* in, uint64_t E, const uint32_t* map, Edge* out, cudaStream_t s);
 
+// ---- file formats (io.cu) ----
+struct EdgeListData {  // edge_list.hpp:14-18
+    std::vector<uint32_t> pairs;  // 2 ids per pair
+    uint64_t self_loops = 0;
+};
+EdgeListData load_edge_list(const char* path);
+void write_edge_list(const char* path, const uint32_t* pairs, uint64_t npairs);
+std::vector<uint32_t> load_training_set(const char* path, uint32_t n);
+void write_training_set(const char* path, const uint32_t* vt, uint64_t k);
+
 // ---- launchers (implemented in graph.cu / path.cu / aggregate.cu) ----
 std::unique_ptr<Graph> graph_build(int device, int64_t n_hint, const uint32_t* pairs_host,
                                    uint64_t npairs, int weight_mode);

@@ -40,6 +40,14 @@ class ShapeError(ConfigError):
     pass
 
 
+class ParseError(ConfigError):
+    """error.hpp:18-22: carries the 1-based line number."""
+
+    def __init__(self, msg, line_number=None):
+        super().__init__(msg)
+        self.line_number = line_number
+
+
 class StalenessError(ConfigError):
     pass
 
@@ -71,6 +79,14 @@ def _check(rc):
         cls = _CODES.get(rc, Error)
         if cls is ConfigError and ("rows" in msg or "dimension" in msg):
             cls = ShapeError
+        if cls is ConfigError and "stale" in msg:
+            cls = StalenessError
+        if cls is ConfigError and msg.endswith(")") and "(line " in msg:
+            import re
+
+            m = re.search(r"\(line (\d+)\)$", msg)
+            if m:
+                raise ParseError(msg, int(m.group(1)))
         raise cls(msg)
 
 
@@ -155,6 +171,56 @@ def build_undirected_csr(pairs, n_hint=None, weights="unit", device=0) -> CsrGra
     _check(_lib_().pg_graph_build(device, -1 if n_hint is None else int(n_hint), _p(pairs, u32p), len(pairs),
                                   _weight_mode(weights), C.byref(h)))
     return CsrGraph(h.value, device)
+
+
+@dataclass
+class EdgeList:
+    """edge_list.hpp:14-18"""
+    pairs: np.ndarray  # [m, 2] u32
+    n_hint: int | None = None
+    self_loops_dropped: int = 0
+
+
+def load_edge_list_file(path) -> EdgeList:
+    """edge_list.cpp:34-68 (ParseError with line_number, IoError)."""
+    h = C.c_void_p()
+    _check(_lib_().pg_edge_list_load(str(path).encode(), C.byref(h)))
+    try:
+        n, sl = C.c_uint64(), C.c_uint64()
+        _check(_lib_().pg_edge_list_info(h, C.byref(n), C.byref(sl)))
+        pairs = np.empty((n.value, 2), np.uint32)
+        _check(_lib_().pg_edge_list_export(h, _p(pairs, u32p)))
+    finally:
+        _lib_().pg_edge_list_destroy(h)
+    return EdgeList(pairs, None, sl.value)
+
+
+def write_edge_list(path, pairs):
+    """edge_list.cpp:70-73"""
+    pairs = _u32(pairs).reshape(-1, 2)
+    _check(_lib_().pg_edge_list_write(str(path).encode(), _p(pairs, u32p), len(pairs)))
+
+
+def load_graph_file(path, weights="unit", device=0) -> CsrGraph:
+    """load_edge_list_file + build_undirected_csr + assign_edge_weights."""
+    h = C.c_void_p()
+    _check(_lib_().pg_graph_load_file(device, str(path).encode(), _weight_mode(weights), C.byref(h)))
+    return CsrGraph(h.value, device)
+
+
+def load_training_set_file(path, n):
+    """training_set.cpp:51-79: sorted unique u32 ids."""
+    k = C.c_uint64()
+    _check(_lib_().pg_training_set_load(str(path).encode(), n, None, 0, C.byref(k)))
+    out = np.empty(max(k.value, 1), np.uint32)
+    _check(_lib_().pg_training_set_load(str(path).encode(), n, _p(out, u32p), len(out), C.byref(k)))
+    return out[: k.value]
+
+
+def write_training_set(path, vt):
+    """training_set.cpp:81-83"""
+    vt = _u32(vt)
+    _check(_lib_().pg_training_set_write(str(path).encode(), _p(vt, u32p), len(vt)))
 
 
 def graph_from_csr(n, offsets, neighbors, weights, device=0, validate=True) -> CsrGraph:
