@@ -251,6 +251,9 @@ def main():
     ap.add_argument("--heavy-sweep", action="store_true", help="diagnostics: heavy-kernel threshold sweep")
     ap.add_argument("--tune-sweep", action="store_true", help="diagnostics: SpMM scheduling-knob sweep")
     ap.add_argument("--no-chain", action="store_true", help="skip the forward/backward-variant chain timing")
+    ap.add_argument("--gs-sweep", action="store_true",
+                    help="structure-aware gs sweep (default on for arxiv): measured grouped-kernel curve vs the "
+                         "regression and cost-model choices")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -442,6 +445,8 @@ def main():
     if not args.profile and not args.no_e2e:
         line["e2e"] = measure_e2e(pg, pgd, torch, dist, paths, groups, shards, dims, rows, world, rank, dev,
                                   max(3, min(args.steps, 10)), ep_bytes)
+    if not args.profile and world == 1 and (args.gs_sweep or args.config == "arxiv"):
+        line["gs_sweep"] = gs_sweep(pg, prep, dims)
     if not args.profile and not args.no_chain and world == 1:
         line["chain"] = measure_chain(pg, torch, g, prep, cfg, vt, dev)
     if not args.profile and not args.no_cpu and world == 1 and rank == 0:
@@ -453,6 +458,45 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def gs_sweep(pg, prep, dims, repeats=5):
+    """SURVEY §8d (arxiv config): per path, the GPU time of the group-
+    partitioned Fast aggregation for every default gs candidate (the
+    measured oracle, train.hpp:35-54), against the gs the regression model
+    (gs_model.cpp:64-74) and the cost model (group_cost.cpp:9-53, W=8,
+    lambda=0.25) pick, and the gs-invariant Deterministic kernel."""
+    import torch
+
+    out = []
+    for i, p in enumerate(prep.paths):
+        best, table = pg.oracle_gs_measured(p, dims[i], repeats=repeats)
+        reg = pg.path_regression_gs(p)
+        cost_best, _ = pg.oracle_gs(p, dims[i], 8, 0.25)
+        tab = dict(table)
+        y = pg.empty_rows(p.P, dims[i])
+        y.uniform_(0, 1)
+        x = pg.empty_rows(p.D, dims[i])
+        G = pg.group_neighbors(p, reg)
+        ts = []
+        for _ in range(repeats + 1):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            pg.backward_aggregation(G, y, x, overwrite=True)
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        det_ms = statistics.median(ts[1:])
+        nearest = lambda gs: min(tab, key=lambda c: (abs(c - gs), c))
+        out.append({"path": i, "layer": p.layer, "dim": dims[i], "max_degree": p.max_degree,
+                    "measured_ms": {str(gs): round(t * 1e3, 4) for gs, t in table},
+                    "measured_best_gs": best, "regression_gs": reg, "cost_model_gs": cost_best,
+                    "grouped_ms_at_regression_gs": round(tab[nearest(reg)] * 1e3, 4),
+                    "grouped_ms_at_cost_model_gs": round(tab[cost_best] * 1e3, 4) if cost_best in tab else None,
+                    "deterministic_ms": round(det_ms, 4)})
+        log(f"[gs_sweep] path {i} dim {dims[i]}: best {best} regression {reg} cost {cost_best} "
+            f"det {det_ms:.3f} ms table {[(gs, round(t * 1e3, 3)) for gs, t in table]}")
+    return out
 
 
 def measure_chain(pg, torch, g, prep, cfg, vt, dev, reps=5):

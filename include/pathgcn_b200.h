@@ -48,6 +48,12 @@ extern "C" {
  * reports the reference's Fast counters. */
 #define PG_AGG_FAST 1u
 #define PG_AGG_OVERWRITE 2u
+/* PG_AGG_GROUPED (implies Fast): the group-partitioned kernel of
+ * aggregate.hpp:84-115 — one (sub-)warp per neighbour group, plain commit
+ * for single-group destinations, fp32 atomics for the rest, so gs sets the
+ * GPU's unit of work. Within fp32 tolerance of Deterministic, not bit-exact.
+ * Whole groupings only (no row ranges / segments / host buffers). */
+#define PG_AGG_GROUPED 4u
 
 typedef struct pg_graph_s* pg_graph;         /* CsrGraph      csr_graph.hpp:19-38   */
 typedef struct pg_frontiers_s* pg_frontiers; /* FrontierSets  frontier.hpp:14-18    */
@@ -166,6 +172,14 @@ int pg_gs_oracle_cost(pg_path p, uint64_t dim, int workers, double lambda, const
                       uint64_t ncand, uint32_t* best, double* table, uint64_t* ncand_out);
 /* group_cost.cpp:9-24 grouping_cost for a built grouping */
 int pg_grouping_cost(pg_groups G, uint64_t dim, int workers, double lambda, double* cost);
+/* train.hpp:35-54 measured_evaluator + group_cost.cpp:36-53 oracle_gs on
+ * the device ("oracle:measured"): per candidate gs, the path is grouped and
+ * the PG_AGG_GROUPED aggregation of a U(0,1) input (mt19937_64(derive_seed(
+ * seed, 17)), parent-frontier rows x dim) is timed with CUDA events, median
+ * of `repeats`; argmin, ties -> smaller gs. table[i] = seconds. cands NULL:
+ * default_gs_candidates(max degree). Timing based: not bit-reproducible. */
+int pg_gs_oracle_measured(pg_path p, uint64_t dim, int repeats, uint64_t seed, const uint32_t* cands,
+                          uint64_t ncand, uint32_t* best, double* table, uint64_t* ncand_out);
 
 /* grouping.cpp:7-27 group_neighbors over a path (or the whole graph). The
  * grouping borrows its base, which must outlive it (grouping.hpp:10-13). */

@@ -108,6 +108,7 @@ SIGNATURES = {
     "pg_gs_default_candidates": [u32, u32p, u64p],
     "pg_gs_oracle_cost": [H, u64, i32, f64, u32p, u64, u32p, f64p, u64p],
     "pg_grouping_cost": [H, u64, i32, f64, f64p],
+    "pg_gs_oracle_measured": [H, u64, i32, u64, u32p, u64, u32p, f64p, u64p],
     "pg_group": [H, u32, C.POINTER(H)],
     "pg_group_graph": [H, u32, C.POINTER(H)],
     "pg_groups_info": [H, u32p, u64p, u32p],

@@ -292,6 +292,109 @@ __global__ void __launch_bounds__(256, (U <= 8 ? 4 : 2)) k_agg_vec4(const uint64
     acc_store_ext(orow, col, dim, acc, z, ext, d, row);
 }
 
+// ---- CommitMode::Fast, group partitioned (PG_AGG_GROUPED) ----------------
+// aggregate.hpp:84-115: one (sub-)warp per (neighbour group, column chunk):
+// the group's <= gs edges accumulate in edge order into a zero scratch,
+// then commit — a plain out += scratch when the destination owns a single
+// group, atomic adds (red.global.add.v4.f32) otherwise. Load balance comes
+// from the group size, so the structure-aware gs selector (gs_model.cpp,
+// group_cost.cpp) shapes the GPU schedule here. Across groups of one
+// destination the fp32 order follows the atomics: within tolerance of the
+// reference's Fast (and Deterministic) result, not bit-exact.
+template <int LPD, int U>
+__global__ void __launch_bounds__(256, (U <= 8 ? 4 : 2)) k_agg_groups(
+    const uint64_t* __restrict__ gbeg, const uint64_t* __restrict__ gend, const uint32_t* __restrict__ gdest,
+    const uint64_t* __restrict__ dest_groups, const Edge* __restrict__ edges, uint64_t n_items, uint32_t chunks,
+    const float* __restrict__ in, uint32_t ld_in_bytes, float* __restrict__ out, uint64_t ld_out, uint32_t dim,
+    int accumulate, float2 zeros, uint32_t zmask, int chunk_major) {
+    const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    const uint64_t item = t / LPD;
+    if (item >= n_items) return;
+    const Zs z = zs_of(zeros);
+    const uint64_t ng = n_items / chunks;
+    const uint64_t gi = chunk_major ? item % ng : item / chunks;
+    const uint32_t ci = static_cast<uint32_t>(chunk_major ? item / ng : item % chunks);
+    const uint32_t d = __ldg(gdest + gi);
+    const uint32_t col = (ci * LPD + static_cast<uint32_t>(t % LPD)) * 4;
+    const bool active = col < dim;
+    uint64_t e = __ldg(gbeg + gi);
+    const uint64_t end = __ldg(gend + gi);
+    const bool multi = __ldg(dest_groups + d + 1) - __ldg(dest_groups + d) > 1;
+    const char* base = reinterpret_cast<const char*>(in) + (active ? col : 0u) * 4u;
+    asm("mov.b64 %0, %0;" : "+l"(base));
+    Acc acc{0ull, 0ull};  // scratch, zero filled (aggregate.hpp:93)
+    for (; e + U <= end; e += U) {
+        Edge ed[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) ed[u] = ld_rec(edges + e + u);
+        float4 x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) x[u] = ld_row(base, ed[u].x, ld_in_bytes);
+        const Zs zz = batch_dep<U>(x, z, zmask);
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc_step(acc, __uint_as_float(ed[u].y), x[u], zz);
+    }
+    if (e < end) {
+        const uint32_t n = static_cast<uint32_t>(end - e);
+        Edge ed[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) ed[u] = ld_rec(edges + e + (u < static_cast<int>(n) ? u : n - 1));
+        float4 x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) x[u] = ld_row(base, ed[u].x, ld_in_bytes);
+        const Zs zz = batch_dep<U>(x, z, zmask);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (u < static_cast<int>(n)) acc_step(acc, __uint_as_float(ed[u].y), x[u], zz);
+    }
+    if (!active) return;
+    float* orow = out + d * ld_out + col;
+    const float2 l = unpk2(acc.lo), h = unpk2(acc.hi);
+    const float4 v = make_float4(l.x, l.y, h.x, h.y);
+    const bool full = col + 3 < dim;
+    if (multi) {  // #pragma omp atomic (aggregate.hpp:105-109); output zeroed by the caller
+        if (full) {
+            atomicAdd(reinterpret_cast<float4*>(orow), v);
+        } else {
+            atomicAdd(orow, v.x);
+            if (col + 1 < dim) atomicAdd(orow + 1, v.y);
+            if (col + 2 < dim) atomicAdd(orow + 2, v.z);
+        }
+        return;
+    }
+    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);  // out += scratch (aggregate.hpp:102-103)
+    if (accumulate) {
+        if (full) o = *reinterpret_cast<const float4*>(orow);
+        else {
+            o.x = orow[0];
+            if (col + 1 < dim) o.y = orow[1];
+            if (col + 2 < dim) o.z = orow[2];
+        }
+    }
+    o.x = __fadd_rn(o.x, v.x);
+    o.y = __fadd_rn(o.y, v.y);
+    o.z = __fadd_rn(o.z, v.z);
+    o.w = __fadd_rn(o.w, v.w);
+    if (full) {
+        *reinterpret_cast<float4*>(orow) = o;
+    } else {
+        orow[0] = o.x;
+        if (col + 1 < dim) orow[1] = o.y;
+        if (col + 2 < dim) orow[2] = o.z;
+    }
+}
+
+template <int LPD>
+void launch_groups(const uint64_t* gbeg, const uint64_t* gend, const uint32_t* gdest, const uint64_t* dest_groups,
+                   const Edge* edges, uint64_t G, uint32_t chunks, const float* in, uint64_t ld_in, float* out,
+                   uint64_t ld_out, uint32_t dim, bool accumulate, cudaStream_t s) {
+    const uint64_t items = G * chunks;
+    k_agg_groups<LPD, 8><<<grid_for(items * LPD, 256), 256, 0, s>>>(
+        gbeg, gend, gdest, dest_groups, edges, items, chunks, in, static_cast<uint32_t>(ld_in * 4), out, ld_out, dim,
+        accumulate, kZeros, 0u, chunks > 1 && tuning(kTuneChunkMajor) ? 1 : 0);
+    PG_LAUNCH("k_agg_groups");
+}
+
 // Wide rows (> 16 float4 columns): a full warp per (destination, 32-float4
 // chunk). Edge records are loaded 32 at a time, one per lane (coalesced), and
 // the next batch is prefetched while the current one is consumed; records
@@ -1022,6 +1125,29 @@ void aggregate_det(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges
     } else {
         launch_vec4<4, 8>(ebeg, eend, edges, order, d_begin, nd, 1, in, ld_in, out, ld_out, dim32, accumulate, s, ext);
     }
+}
+
+void aggregate_groups(const uint64_t* gbeg, const uint64_t* gend, const uint32_t* gdest, const uint64_t* dest_groups,
+                      uint32_t D, uint64_t G, const Edge* edges, const float* in, uint64_t ld_in, float* out,
+                      uint64_t ld_out, uint64_t dim, bool accumulate, cudaStream_t s) {
+    if (dim == 0) return;
+    if (!accumulate && D) PG_CUDA(cudaMemset2DAsync(out, ld_out * 4, 0, dim * 4, D, s));
+    if (G == 0) return;
+    const bool vec = (ld_in % 4 == 0) && (ld_out % 4 == 0) && (reinterpret_cast<uintptr_t>(in) % 16 == 0) &&
+                     (reinterpret_cast<uintptr_t>(out) % 16 == 0) && ld_in >= ((dim + 3) & ~3ull) &&
+                     ld_in < (1ull << 30);
+    if (!vec) fail(kConfig, "grouped aggregation needs 16-byte rows (ld % 4 == 0, aligned base)");
+    const uint32_t dim32 = static_cast<uint32_t>(dim);
+    const uint32_t nq = (dim32 + 3) / 4;
+    if (nq > 16)
+        launch_groups<32>(gbeg, gend, gdest, dest_groups, edges, G, (nq + 31) / 32, in, ld_in, out, ld_out, dim32,
+                          true, s);
+    else if (nq > 8)
+        launch_groups<16>(gbeg, gend, gdest, dest_groups, edges, G, 1, in, ld_in, out, ld_out, dim32, true, s);
+    else if (nq > 4)
+        launch_groups<8>(gbeg, gend, gdest, dest_groups, edges, G, 1, in, ld_in, out, ld_out, dim32, true, s);
+    else
+        launch_groups<4>(gbeg, gend, gdest, dest_groups, edges, G, 1, in, ld_in, out, ld_out, dim32, true, s);
 }
 
 void relu_backward(const float* grad, uint64_t ldg, const float* pre, uint64_t ldp, float* out, uint64_t ldo,

@@ -48,6 +48,17 @@ Frontiers* F_(pg_frontiers h) { return need(reinterpret_cast<Frontiers*>(h), "fr
 Path* P_(pg_path h) { return need(reinterpret_cast<Path*>(h), "path"); }
 Groups* R_(pg_groups h) { return need(reinterpret_cast<Groups*>(h), "groups"); }
 
+// engine.hpp:60-68 derive_seed (splitmix-style stream derivation)
+uint64_t derive_seed(uint64_t seed, uint64_t stream) {
+    uint64_t h = seed ^ (0x9e3779b97f4a7c15ull + stream);
+    h ^= h >> 30;
+    h *= 0xbf58476d1ce4e5b9ull;
+    h ^= h >> 27;
+    h *= 0x94d049bb133111ebull;
+    h ^= h >> 31;
+    return h;
+}
+
 void fnv_mix(uint64_t& h, uint64_t x) {
     for (int i = 0; i < 8; ++i) {
         h ^= (x >> (8 * i)) & 0xFF;
@@ -141,6 +152,33 @@ void pg::run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re,
                    const AggExt& ext, const Edge* edges_override) {
     const bool accumulate = !(flags & PG_AGG_OVERWRITE);
     DeviceGuard dg(G.device);
+    if (flags & PG_AGG_GROUPED) {  // aggregate.hpp:84-115 over the groups
+        const Base b = base_of(G);
+        if (rb != 0 || re != b.D || sel.seg >= 0 || ext.any())
+            fail(kConfig, "grouped aggregation runs over a whole grouping (no row ranges, segments or chains)");
+        const Edge* edges = nullptr;
+        if (G.path) {
+            Path& p = *G.path;
+            edges = p.edges_parent.get();
+            if (parent_indexed && G.edges_remap.get()) edges = G.edges_remap.get();
+            if (edges_override) edges = edges_override;
+            if (!edges_override && !parent_indexed && p.S != p.P) {
+                path_pack_local(p, lib_stream(p.device));
+                PG_CUDA(cudaStreamSynchronize(lib_stream(p.device)));
+                edges = p.edges_local.get();
+            }
+        } else {
+            Graph& g = *G.graph;
+            if (!g.edges.get()) {
+                graph_pack_edges(g, lib_stream(g.device));
+                PG_CUDA(cudaStreamSynchronize(lib_stream(g.device)));
+            }
+            edges = g.edges.get();
+        }
+        aggregate_groups(G.gbegin.get(), G.gend.get(), G.gdest.get(), G.dest_groups.get(), b.D, G.G, edges, in, ld_in,
+                         out, ld_out, dim, accumulate, s);
+        return;
+    }
     if (G.path) {
         Path& p = *G.path;
         const Edge* edges = p.edges_parent.get();
@@ -731,6 +769,69 @@ int pg_gs_oracle_cost(pg_path h, uint64_t dim, int workers, double lambda, const
                 best_gs = c[i];
             }
         }
+        *best = best_gs;
+        if (ncand_out) *ncand_out = c.size();
+    });
+}
+
+int pg_gs_oracle_measured(pg_path h, uint64_t dim, int repeats, uint64_t seed, const uint32_t* cands,
+                          uint64_t ncand, uint32_t* best, double* table, uint64_t* ncand_out) {
+    return guard([&] {
+        Path& p = *P_(h);
+        std::vector<uint32_t> c;
+        if (cands) {
+            c.assign(cands, cands + ncand);
+        } else {
+            uint32_t tmp[40];
+            uint64_t k = 0;
+            if (int rc = pg_gs_default_candidates(p.max_degree, tmp, &k)) fail(rc, g_err);
+            c.assign(tmp, tmp + k);
+        }
+        if (c.empty()) fail(kConfig, "oracle_gs: empty candidate list");
+        if (repeats < 1) fail(kConfig, "measured oracle: repeats must be >= 1");
+        DeviceGuard dg(p.device);
+        cudaStream_t s = lib_stream(p.device);
+        // measured_evaluator's input (train.hpp:38-41): U(0,1) from
+        // mt19937_64(derive_seed(seed, 17)), row-major rows x dim
+        const uint64_t rows = p.P, ld = (dim + 3) & ~3ull;
+        std::vector<float> host(rows * dim);
+        std::mt19937_64 rng(derive_seed(seed, 17));
+        std::uniform_real_distribution<double> u(0.0, 1.0);
+        for (float& v : host) v = static_cast<float>(u(rng));
+        DevBuf<float> in(std::max<uint64_t>(rows * ld, 1), s), out(std::max<uint64_t>(uint64_t(p.D) * ld, 1), s);
+        if (rows * dim)
+            PG_CUDA(cudaMemcpy2DAsync(in.get(), ld * 4, host.data(), dim * 4, dim * 4, rows, cudaMemcpyHostToDevice, s));
+        cudaEvent_t e0, e1;
+        PG_CUDA(cudaEventCreate(&e0));
+        PG_CUDA(cudaEventCreate(&e1));
+        double best_t = 0.0;
+        uint32_t best_gs = 1;
+        bool first = true;
+        for (std::size_t i = 0; i < c.size(); ++i) {
+            auto G = groups_build(p.D, p.offsets.get(), c[i], p.device);
+            G->path = &p;
+            std::vector<double> ts;
+            for (int r = 0; r < repeats; ++r) {
+                PG_CUDA(cudaEventRecord(e0, s));
+                run_aggregate(*G, true, 0, p.D, in.get(), ld, out.get(), ld, dim, PG_AGG_OVERWRITE | PG_AGG_GROUPED, s);
+                PG_CUDA(cudaEventRecord(e1, s));
+                PG_CUDA(cudaEventSynchronize(e1));
+                float ms = 0.f;
+                PG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+                ts.push_back(ms * 1e-3);
+            }
+            std::sort(ts.begin(), ts.end());
+            const double cost = ts[ts.size() / 2];
+            if (table) table[i] = cost;
+            if (first || cost < best_t || (cost == best_t && c[i] < best_gs)) {
+                first = false;
+                best_t = cost;
+                best_gs = c[i];
+            }
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        PG_CUDA(cudaStreamSynchronize(s));
         *best = best_gs;
         if (ncand_out) *ncand_out = c.size();
     });

@@ -220,6 +220,13 @@ void run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re, con
                    float* out, uint64_t ld_out, uint64_t dim, unsigned flags, cudaStream_t s, SegSel sel = {},
                    const AggExt& ext = AggExt{}, const Edge* edges_override = nullptr);
 
+// aggregate.hpp:84-115 CommitMode::Fast over the groups (PG_AGG_GROUPED):
+// warp per (group, chunk), plain commit for single-group destinations,
+// atomics otherwise; zeroes the D output rows first unless accumulate.
+void aggregate_groups(const uint64_t* gbeg, const uint64_t* gend, const uint32_t* gdest, const uint64_t* dest_groups,
+                      uint32_t D, uint64_t G, const Edge* edges, const float* in, uint64_t ld_in, float* out,
+                      uint64_t ld_out, uint64_t dim, bool accumulate, cudaStream_t s);
+
 // PG_HEAVY_MIN_DEG / pg_set_heavy_min_degree (0 disables; UINT64_MAX restores
 // the width-dependent default)
 uint64_t heavy_min_degree(uint64_t dim, uint64_t range_edges);

@@ -24,8 +24,10 @@ from ._lib import f32p, f64p, u32p, u64p
 
 DETERMINISTIC = "deterministic"
 FAST = "fast"
+GROUPED = "grouped"  # Fast on the group-partitioned kernel (PG_AGG_GROUPED)
 AGG_FAST = 1
 AGG_OVERWRITE = 2
+AGG_GROUPED = 4
 
 
 class Error(RuntimeError):
@@ -398,6 +400,21 @@ def oracle_gs(path: ExecutionPath, dim, workers, atomic_penalty=0.25, candidates
     return best.value, list(zip(cands.tolist(), table[: n.value].tolist()))
 
 
+def oracle_gs_measured(path: ExecutionPath, dim, repeats=5, seed=42, candidates=None):
+    """train.hpp:35-54 + group_cost.cpp:36-53 on the device: each candidate's
+    grouped (Fast) aggregation timed, median of repeats; (best_gs,
+    [(gs, seconds)]). Timing based — not bit-reproducible."""
+    if candidates is None:
+        candidates = default_gs_candidates(path.max_degree)
+    cands = _u32(candidates)
+    table = np.empty(max(len(cands), 1), np.float64)
+    best = C.c_uint32()
+    n = C.c_uint64()
+    _check(_lib_().pg_gs_oracle_measured(path._h, dim, repeats, seed, _p(cands, u32p), len(cands), C.byref(best),
+                                         _p(table, f64p), C.byref(n)))
+    return best.value, list(zip(cands.tolist(), table[: n.value].tolist()))
+
+
 class GroupedCsr:
     """grouping.hpp:14-28 (borrows its base)."""
 
@@ -481,6 +498,8 @@ def _flags(mode, overwrite=False):
     f = 0
     if mode in (FAST, "Fast", AGG_FAST):
         f |= AGG_FAST
+    elif mode in (GROUPED, AGG_GROUPED):
+        f |= AGG_FAST | AGG_GROUPED
     elif mode not in (DETERMINISTIC, "Deterministic", 0, None):
         raise ConfigError(f"unknown commit mode {mode!r}")
     if overwrite:
@@ -666,6 +685,8 @@ def choose_gs(strategy, path: ExecutionPath, dim, workers=8, atomic_penalty=0.25
         return path_regression_gs(path)
     if strategy in ("oracle:cost", "oracle"):
         return oracle_gs(path, dim, workers, atomic_penalty)[0]
+    if strategy == "oracle:measured":
+        return oracle_gs_measured(path, dim)[0]
     raise ConfigError(f"unknown gs strategy {strategy!r}")
 
 
