@@ -259,6 +259,15 @@ int pg_gather_rows(const float* src, uint64_t lds, const uint32_t* ids_dev, uint
 int pg_path_device_arrays(pg_path p, const uint32_t** dest, const uint32_t** srcpos,
                           const uint64_t** offsets);
 
+/* Device memory for callers without the CUDA runtime headers (the C++
+ * header's DeviceMatrix): stream-less, synchronous. */
+int pg_device_alloc(int device, uint64_t bytes, void** out);
+int pg_device_free(int device, void* p);
+int pg_memcpy_h2d(int device, void* dst, const void* src, uint64_t bytes);
+int pg_memcpy_d2h(int device, void* dst, const void* src, uint64_t bytes);
+int pg_memset_zero(int device, void* dst, uint64_t bytes);
+int pg_device_synchronize(int device);
+
 /* ---------------- the GCN chain around the aggregation (engine.hpp) ----------------
  * Device-resident and bit-exact with the reference's f32 build. Matrices are
  * device fp32, rows x cols with row pitch ld floats (the reference's

@@ -14,6 +14,10 @@
 //     (group_cost.hpp:19-43)
 //   aggregate_pull<float> (aggregate.hpp:56-59) aggregate_pull(groups, in, out, mode, counters)
 //   engine.hpp:331-338 stage                    backward_aggregation(groups, y_grad, x_grad)
+//   load_edge_list_file / load_training_set_file (edge_list.cpp, training_set.cpp)
+//   measured_evaluator + oracle_gs (train.hpp:35-54) oracle_gs_measured(path, dim)
+//   forward / backward_epp / backward_all_active / backward_ifelse (engine.hpp:114-349)
+//                                               same names over DeviceMatrix artefacts
 //
 // Errors are thrown as exceptions mirroring error.hpp:10-47 (ConfigError,
 // ShapeError, StalenessError, IoError, NumericError) plus DeviceError for
@@ -49,6 +53,10 @@ struct ShapeError : ConfigError {
 struct StalenessError : ConfigError {
     using ConfigError::ConfigError;
 };
+struct ParseError : ConfigError {                 // error.hpp:18-22
+    ParseError(const std::string& msg, std::size_t line) : ConfigError(msg), line_number(line) {}
+    std::size_t line_number;
+};
 struct IoError : Error {
     using Error::Error;
 };
@@ -65,10 +73,15 @@ inline void check(int rc) {
     pg_last_error(msg.data(), msg.size());
     msg.resize(msg.find('\0'));
     switch (rc) {
-        case PG_ERR_CONFIG:
+        case PG_ERR_CONFIG: {
             if (msg.find("rows") != std::string::npos || msg.find("dimension") != std::string::npos)
                 throw ShapeError(msg);
+            if (msg.find("stale") != std::string::npos) throw StalenessError(msg);
+            const std::size_t at = msg.rfind("(line ");
+            if (at != std::string::npos && !msg.empty() && msg.back() == ')')
+                throw ParseError(msg, std::stoull(msg.substr(at + 6)));
             throw ConfigError(msg);
+        }
         case PG_ERR_IO: throw IoError(msg);
         case PG_ERR_NUMERIC: throw NumericError(msg);
         case PG_ERR_DEVICE: throw DeviceError(msg);
@@ -77,12 +90,66 @@ inline void check(int rc) {
 }
 
 enum class WeightMode { Unit, SymNorm };          // csr_graph.hpp:13
-enum class CommitMode { Deterministic, Fast };    // aggregate.hpp:21
+// aggregate.hpp:21. Fast runs the atomic-free kernel (bit-equal to
+// Deterministic); Grouped is Fast on the group-partitioned kernel (a warp per
+// neighbour group, atomics across a destination's groups: tolerance-level).
+enum class CommitMode { Deterministic, Fast, Grouped };
+enum class GatherMode { Local, Global };          // run_config.hpp:19
+
+inline unsigned commit_flags(CommitMode m) {
+    return m == CommitMode::Fast ? PG_AGG_FAST : m == CommitMode::Grouped ? (PG_AGG_FAST | PG_AGG_GROUPED) : 0u;
+}
 
 struct EdgeList {                                 // edge_list.hpp:14-18
     std::vector<std::pair<VertexId, VertexId>> pairs;
     std::optional<VertexId> n_hint;
+    std::uint64_t self_loops_dropped = 0;
 };
+
+// edge_list.cpp:34-68 (ParseError carries the line number, IoError)
+inline EdgeList load_edge_list_file(const std::string& path) {
+    pg_edge_list h = nullptr;
+    check(pg_edge_list_load(path.c_str(), &h));
+    std::uint64_t n = 0, sl = 0;
+    std::vector<VertexId> flat;
+    try {
+        check(pg_edge_list_info(h, &n, &sl));
+        flat.resize(2 * n);
+        check(pg_edge_list_export(h, flat.data()));
+    } catch (...) {
+        pg_edge_list_destroy(h);
+        throw;
+    }
+    pg_edge_list_destroy(h);
+    EdgeList el;
+    el.self_loops_dropped = sl;
+    el.pairs.reserve(n);
+    for (std::uint64_t i = 0; i < n; ++i) el.pairs.emplace_back(flat[2 * i], flat[2 * i + 1]);
+    return el;
+}
+
+inline void write_edge_list_file(const std::string& path, const EdgeList& el) {
+    std::vector<VertexId> flat;
+    flat.reserve(el.pairs.size() * 2);
+    for (const auto& [u, v] : el.pairs) {
+        flat.push_back(u);
+        flat.push_back(v);
+    }
+    check(pg_edge_list_write(path.c_str(), flat.data(), el.pairs.size()));
+}
+
+// training_set.cpp:51-79: sorted unique ids
+inline std::vector<VertexId> load_training_set_file(const std::string& path, VertexId n) {
+    std::uint64_t k = 0;
+    check(pg_training_set_load(path.c_str(), n, nullptr, 0, &k));
+    std::vector<VertexId> out(k);
+    check(pg_training_set_load(path.c_str(), n, out.data(), out.size(), &k));
+    return out;
+}
+
+inline void write_training_set_file(const std::string& path, std::span<const VertexId> vt) {
+    check(pg_training_set_write(path.c_str(), vt.data(), vt.size()));
+}
 
 struct StageCounters {                            // aggregate.hpp:23-39 (work part)
     std::uint64_t edges_traversed = 0;
@@ -190,6 +257,14 @@ inline DeviceGraph build_undirected_csr(const EdgeList& el, WeightMode mode = We
     pg_graph g = nullptr;
     check(pg_graph_build(device, el.n_hint ? static_cast<std::int64_t>(*el.n_hint) : -1, flat.data(),
                          el.pairs.size(), mode == WeightMode::SymNorm ? PG_WEIGHTS_SYMNORM : PG_WEIGHTS_UNIT, &g));
+    return DeviceGraph(g);
+}
+
+// load_edge_list_file + build_undirected_csr + assign_edge_weights
+inline DeviceGraph load_graph_file(const std::string& path, WeightMode mode = WeightMode::Unit, int device = 0) {
+    pg_graph g = nullptr;
+    check(pg_graph_load_file(device, path.c_str(), mode == WeightMode::SymNorm ? PG_WEIGHTS_SYMNORM : PG_WEIGHTS_UNIT,
+                             &g));
     return DeviceGraph(g);
 }
 
@@ -334,6 +409,20 @@ inline GsSweepResult oracle_gs_cost(const DevicePath& p, std::size_t dim, const 
     return r;
 }
 
+// train.hpp:35-54 measured_evaluator + oracle_gs on the device: the grouped
+// (Fast) aggregation of each candidate timed, median of `repeats` (seconds)
+inline GsSweepResult oracle_gs_measured(const DevicePath& p, std::size_t dim, int repeats = 5,
+                                        std::uint64_t seed = 42, std::vector<VertexId> candidates = {}) {
+    if (candidates.empty()) candidates = default_gs_candidates(p.max_degree());
+    std::vector<double> table(candidates.size());
+    GsSweepResult r;
+    std::uint64_t n = 0;
+    check(pg_gs_oracle_measured(p.raw(), dim, repeats, seed, candidates.data(), candidates.size(), &r.best_gs,
+                                table.data(), &n));
+    for (std::size_t i = 0; i < n; ++i) r.table.push_back({candidates[i], table[i]});
+    return r;
+}
+
 class DeviceGroups {                              // GroupedCsr (grouping.hpp:14-28)
 public:
     explicit DeviceGroups(pg_groups g) : h_(g) { check(pg_groups_info(g, &gs_, &count_, &dests_)); }
@@ -383,7 +472,7 @@ inline void aggregate_pull(const DeviceGroups& grouped, const MatrixF& input, Ma
     if (output.cols != input.cols) throw ShapeError("aggregate_pull: input/output dims differ");
     std::uint64_t c[3] = {0, 0, 0};
     check(pg_aggregate_pull_host(grouped.raw(), input.data.data(), input.rows, input.cols, output.data.data(),
-                                 mode == CommitMode::Fast ? PG_AGG_FAST : 0u, c));
+                                 commit_flags(mode == CommitMode::Grouped ? CommitMode::Fast : mode), c));
     if (counters) {
         counters->edges_traversed += c[0];
         counters->groups_executed += c[1];
@@ -399,12 +488,179 @@ inline void backward_aggregation(const DeviceGroups& grouped, const MatrixF& y_g
         throw ShapeError("backward_aggregation: x_grad shape mismatch");
     std::uint64_t c[3] = {0, 0, 0};
     check(pg_backward_aggregate_host(grouped.raw(), y_grad.data.data(), y_grad.rows, y_grad.cols,
-                                     x_grad.data.data(), mode == CommitMode::Fast ? PG_AGG_FAST : 0u, c));
+                                     x_grad.data.data(),
+                                     commit_flags(mode == CommitMode::Grouped ? CommitMode::Fast : mode), c));
     if (counters) {
         counters->edges_traversed += c[0];
         counters->groups_executed += c[1];
         counters->atomic_commits += c[2];
     }
+}
+
+// ---------------- the GCN chain (engine.hpp), device resident ----------------
+
+// A device fp32 matrix (row pitch padded to 16-byte rows up to 32 floats,
+// 128-byte lines beyond, as the SpMM prefers); upload/download to the
+// reference's DenseMatrix layout.
+class DeviceMatrix {
+public:
+    DeviceMatrix() = default;
+    DeviceMatrix(std::size_t rows, std::size_t cols, int device = 0) : dev_(device) {
+        m_.rows = rows;
+        m_.cols = cols;
+        m_.ld = cols <= 32 ? (cols + 3) / 4 * 4 : (cols + 31) / 32 * 32;
+        void* p = nullptr;
+        check(pg_device_alloc(device, m_.rows * m_.ld * 4, &p));
+        m_.data = static_cast<float*>(p);
+        check(pg_memset_zero(device, p, m_.rows * m_.ld * 4));
+    }
+    DeviceMatrix(const DeviceMatrix&) = delete;
+    DeviceMatrix& operator=(const DeviceMatrix&) = delete;
+    DeviceMatrix(DeviceMatrix&& o) noexcept : m_(std::exchange(o.m_, pg_mat{})), dev_(o.dev_) {}
+    DeviceMatrix& operator=(DeviceMatrix&& o) noexcept {
+        if (this != &o) {
+            release();
+            m_ = std::exchange(o.m_, pg_mat{});
+            dev_ = o.dev_;
+        }
+        return *this;
+    }
+    ~DeviceMatrix() { release(); }
+
+    static DeviceMatrix upload(const MatrixF& h, int device = 0) {
+        DeviceMatrix d(h.rows, h.cols, device);
+        for (std::size_t r = 0; r < h.rows && h.cols; ++r)
+            check(pg_memcpy_h2d(device, d.m_.data + r * d.m_.ld, h.data.data() + r * h.cols, h.cols * 4));
+        return d;
+    }
+    MatrixF download() const {
+        MatrixF h(m_.rows, m_.cols);
+        check(pg_device_synchronize(dev_));
+        for (std::size_t r = 0; r < m_.rows && m_.cols; ++r)
+            check(pg_memcpy_d2h(dev_, h.data.data() + r * m_.cols, m_.data + r * m_.ld, m_.cols * 4));
+        return h;
+    }
+    std::size_t rows() const { return m_.rows; }
+    std::size_t cols() const { return m_.cols; }
+    const pg_mat& raw() const { return m_; }
+
+private:
+    void release() {
+        if (m_.data) pg_device_free(dev_, m_.data);
+        m_ = pg_mat{};
+    }
+    pg_mat m_{};
+    int dev_ = 0;
+};
+
+struct DeviceArtifacts {                          // EpochArtifacts (engine.hpp:27-31)
+    std::vector<DeviceMatrix> x, y, pre_act;      // x[0] is unused (the caller's X^(0))
+};
+
+namespace detail {
+inline std::vector<pg_mat> raws(const std::vector<DeviceMatrix>& v, std::size_t from = 0) {
+    std::vector<pg_mat> out;
+    for (std::size_t i = from; i < v.size(); ++i) out.push_back(v[i].raw());
+    return out;
+}
+}  // namespace detail
+
+// engine.hpp:114-140 over a full-graph grouping
+inline DeviceArtifacts forward(const DeviceGroups& graph, const DeviceMatrix& x0,
+                               const std::vector<DeviceMatrix>& weights, int device = 0) {
+    DeviceArtifacts a;
+    a.x.emplace_back();
+    std::size_t cur = x0.cols();
+    for (const auto& w : weights) {
+        a.y.emplace_back(x0.rows(), cur, device);
+        a.pre_act.emplace_back(x0.rows(), w.cols(), device);
+        a.x.emplace_back(x0.rows(), w.cols(), device);
+        cur = w.cols();
+    }
+    auto W = detail::raws(weights), Y = detail::raws(a.y), P = detail::raws(a.pre_act), X = detail::raws(a.x, 1);
+    check(pg_forward(graph.raw(), x0.raw(), W.data(), weights.size(), Y.data(), P.data(), X.data(), nullptr));
+    return a;
+}
+
+// engine.hpp:146-156 (vt on the host)
+inline DeviceMatrix top_grad_from_probs(const DeviceMatrix& probs, const DeviceMatrix& ref,
+                                        std::span<const VertexId> vt, int device = 0) {
+    DeviceMatrix out(probs.rows(), probs.cols(), device);
+    void* d = nullptr;
+    check(pg_device_alloc(device, vt.size() * 4, &d));
+    try {
+        check(pg_memcpy_h2d(device, d, vt.data(), vt.size() * 4));
+        check(pg_top_grad_from_probs(probs.raw(), ref.raw(), static_cast<const uint32_t*>(d), vt.size(), out.raw(),
+                                     nullptr));
+        check(pg_device_synchronize(device));
+    } catch (...) {
+        pg_device_free(device, d);
+        throw;
+    }
+    pg_device_free(device, d);
+    return out;
+}
+
+struct WorkCounts {                               // WorkCounters::backward_edges_per_layer
+    std::vector<std::uint64_t> backward_edges_per_layer;
+};
+
+namespace detail {
+inline std::vector<DeviceMatrix> wgrads(const std::vector<DeviceMatrix>& w, int device) {
+    std::vector<DeviceMatrix> out;
+    for (const auto& m : w) out.emplace_back(m.rows(), m.cols(), device);
+    return out;
+}
+}  // namespace detail
+
+// engine.hpp:267-349. groups[i] groups paths[i] (SG_{L-1} first).
+inline std::vector<DeviceMatrix> backward_epp(const std::vector<DeviceGroups>& groups, const DeviceFrontiers& F,
+                                              const DeviceArtifacts& arts, const DeviceMatrix& top_grad,
+                                              const std::vector<DeviceMatrix>& weights, GatherMode gather,
+                                              std::uint64_t expected_fingerprint, WorkCounts* counters = nullptr,
+                                              int device = 0) {
+    const std::size_t L = weights.size();
+    if (groups.size() != L || F.depth() != L)
+        throw StalenessError("epp backward: paths were prepared for a different layer count");
+    std::vector<pg_groups> hs;
+    for (const auto& g : groups) hs.push_back(g.raw());
+    auto wg = detail::wgrads(weights, device);
+    auto Y = detail::raws(arts.y), P = detail::raws(arts.pre_act), W = detail::raws(weights), WG = detail::raws(wg);
+    std::vector<std::uint64_t> e(L);
+    check(pg_backward_epp(hs.data(), F.raw(), L, Y.data(), P.data(), top_grad.raw(), W.data(), expected_fingerprint,
+                          gather == GatherMode::Global ? 1 : 0, WG.data(), nullptr, e.data(), nullptr));
+    if (counters) counters->backward_edges_per_layer = e;
+    return wg;
+}
+
+// engine.hpp:177-214 (Alg. 1)
+inline std::vector<DeviceMatrix> backward_all_active(const DeviceGroups& graph, const DeviceArtifacts& arts,
+                                                     const DeviceMatrix& top_grad,
+                                                     const std::vector<DeviceMatrix>& weights,
+                                                     WorkCounts* counters = nullptr, int device = 0) {
+    const std::size_t L = weights.size();
+    auto wg = detail::wgrads(weights, device);
+    auto Y = detail::raws(arts.y), P = detail::raws(arts.pre_act), W = detail::raws(weights), WG = detail::raws(wg);
+    std::vector<std::uint64_t> e(L);
+    check(pg_backward_all_active(graph.raw(), L, Y.data(), P.data(), top_grad.raw(), W.data(), WG.data(), nullptr,
+                                 e.data(), nullptr));
+    if (counters) counters->backward_edges_per_layer = e;
+    return wg;
+}
+
+// engine.hpp:218-257
+inline std::vector<DeviceMatrix> backward_ifelse(const DeviceGroups& graph, const DeviceFrontiers& F,
+                                                 const DeviceArtifacts& arts, const DeviceMatrix& top_grad,
+                                                 const std::vector<DeviceMatrix>& weights,
+                                                 WorkCounts* counters = nullptr, int device = 0) {
+    const std::size_t L = weights.size();
+    auto wg = detail::wgrads(weights, device);
+    auto Y = detail::raws(arts.y), P = detail::raws(arts.pre_act), W = detail::raws(weights), WG = detail::raws(wg);
+    std::vector<std::uint64_t> e(L);
+    check(pg_backward_ifelse(graph.raw(), F.raw(), L, Y.data(), P.data(), top_grad.raw(), W.data(), WG.data(),
+                             nullptr, counters ? e.data() : nullptr, nullptr));
+    if (counters) counters->backward_edges_per_layer = e;
+    return wg;
 }
 
 }  // namespace pathgcn::b200

@@ -128,6 +128,12 @@ SIGNATURES = {
     "pg_relu_backward": [vp, u64, vp, u64, vp, u64, u64, u64, vp],
     "pg_gather_rows": [vp, u64, vp, u64, vp, u64, u64, vp],
     "pg_path_device_arrays": [H, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)],
+    "pg_device_alloc": [i32, u64, C.POINTER(vp)],
+    "pg_device_free": [i32, vp],
+    "pg_memcpy_h2d": [i32, vp, vp, u64],
+    "pg_memcpy_d2h": [i32, vp, vp, u64],
+    "pg_memset_zero": [i32, vp, u64],
+    "pg_device_synchronize": [i32],
     "pg_gemm": [PgMat, PgMat, i32, PgMat, vp],
     "pg_gemm_at_b": [PgMat, vp, PgMat, PgMat, vp],
     "pg_relu": [PgMat, PgMat, vp],

@@ -1076,6 +1076,51 @@ int pg_gather_rows(const float* src, uint64_t lds, const uint32_t* ids_dev, uint
     return guard([&] { gather_rows(src, lds, ids_dev, k, out, ldo, cols, static_cast<cudaStream_t>(stream)); });
 }
 
+// ---- device memory helpers (header-only C++ callers) ----
+
+int pg_device_alloc(int device, uint64_t bytes, void** out) {
+    return guard([&] {
+        DeviceGuard dg(device);
+        *out = nullptr;
+        if (bytes) PG_CUDA(cudaMalloc(out, bytes));
+    });
+}
+
+int pg_device_free(int device, void* p) {
+    return guard([&] {
+        DeviceGuard dg(device);
+        if (p) PG_CUDA(cudaFree(p));
+    });
+}
+
+int pg_memcpy_h2d(int device, void* dst, const void* src, uint64_t bytes) {
+    return guard([&] {
+        DeviceGuard dg(device);
+        if (bytes) PG_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+    });
+}
+
+int pg_memcpy_d2h(int device, void* dst, const void* src, uint64_t bytes) {
+    return guard([&] {
+        DeviceGuard dg(device);
+        if (bytes) PG_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+    });
+}
+
+int pg_memset_zero(int device, void* dst, uint64_t bytes) {
+    return guard([&] {
+        DeviceGuard dg(device);
+        if (bytes) PG_CUDA(cudaMemset(dst, 0, bytes));
+    });
+}
+
+int pg_device_synchronize(int device) {
+    return guard([&] {
+        DeviceGuard dg(device);
+        PG_CUDA(cudaDeviceSynchronize());
+    });
+}
+
 // ---- the GCN chain (engine.cu) ----
 
 int pg_gemm(pg_mat a, pg_mat b, int b_transposed, pg_mat out, void* stream) {

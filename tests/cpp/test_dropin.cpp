@@ -147,6 +147,103 @@ int main() {
         }
         report("rmat fixture SpMM bit-exact vs oracle", ok);
         report("rmat probe gs 2 / 9", regression_gs(rpaths[0]) == 2 && regression_gs(rpaths[1]) == 9);
+
+        // the device chain (engine.hpp) vs the oracle's C kernels composed
+        // here: forward + top_grad + backward_epp Local W', bit for bit
+        const std::size_t n = rg.n(), f = 24, hid = 16, cls = 4;
+        MatrixF x0(n, f), w0(f, hid), w1(hid, cls), r(n, cls);
+        for (std::size_t i = 0; i < x0.data.size(); ++i) x0.data[i] = float(0.5 + 0.5 * std::sin(0.11 * double(i)));
+        for (std::size_t i = 0; i < w0.data.size(); ++i) w0.data[i] = float(0.3 * std::cos(0.7 * double(i)));
+        for (std::size_t i = 0; i < w1.data.size(); ++i) w1.data[i] = float(0.3 * std::sin(1.3 * double(i)));
+        for (std::size_t k = 0; k < rvt.size(); ++k) r.data[rvt[k] * cls + (k % cls)] = 1.0f;
+        DeviceGroups gg = group_neighbors(rg, 4);
+        std::vector<DeviceMatrix> W;
+        W.push_back(DeviceMatrix::upload(w0));
+        W.push_back(DeviceMatrix::upload(w1));
+        DeviceMatrix X0 = DeviceMatrix::upload(x0);
+        DeviceArtifacts arts = forward(gg, X0, W);
+        DeviceMatrix top = top_grad_from_probs(arts.x[2], DeviceMatrix::upload(r), rvt);
+        std::vector<DeviceGroups> pgr;
+        const std::uint64_t stamp = path_fingerprint(rg, rvt, 2);
+        for (auto& dp : rpaths) {
+            dp.set_fingerprint(stamp);
+            pgr.push_back(group_neighbors(dp, 2));
+        }
+        WorkCounts wc;
+        auto wg = backward_epp(pgr, rf, arts, top, W, GatherMode::Local, stamp, &wc);
+        // oracle: forward
+        std::vector<float> y0(n * f, 0.f), p0(n * hid), x1(n * hid), y1(n * hid, 0.f), p1(n * cls), x2(n * cls);
+        orc_aggregate_pull_f32(n, off.data(), nb.data(), w.data(), x0.data.data(), f, y0.data());
+        orc_gemm_f32(y0.data(), n, f, w0.data.data(), hid, p0.data());
+        orc_relu_f32(p0.data(), p0.size(), x1.data());
+        orc_aggregate_pull_f32(n, off.data(), nb.data(), w.data(), x1.data(), hid, y1.data());
+        orc_gemm_f32(y1.data(), n, hid, w1.data.data(), cls, p1.data());
+        orc_row_softmax_f32(p1.data(), n, cls, x2.data());
+        std::vector<float> tg(n * cls);
+        orc_top_grad_f32(x2.data(), r.data.data(), n, cls, rvt.data(), rvt.size(), tg.data());
+        report("device forward X^(2) bit-exact vs oracle (incl. softmax expf)",
+               std::memcmp(arts.x[2].download().data.data(), x2.data(), x2.size() * 4) == 0);
+        // oracle: backward_epp Local (engine.hpp:316-346)
+        const auto lv0 = rf.level(0), lv1 = rf.level(1);
+        const auto P1 = rpaths[0].to_host(), P0 = rpaths[1].to_host();
+        std::vector<float> g(lv0.size() * cls), yc(lv0.size() * hid), wg1(hid * cls), ygr(lv0.size() * hid);
+        orc_gather_rows_f32(tg.data(), cls, lv0.data(), lv0.size(), g.data());
+        orc_gather_rows_f32(y1.data(), hid, lv0.data(), lv0.size(), yc.data());
+        orc_gemm_at_b_f32(yc.data(), lv0.size(), hid, g.data(), cls, wg1.data());
+        orc_gemm_a_bt_f32(g.data(), lv0.size(), cls, w1.data.data(), hid, ygr.data());
+        std::vector<float> yu(P1.src_pos_in_parent.size() * hid), xg1(lv1.size() * hid, 0.f);
+        orc_gather_rows_f32(ygr.data(), hid, P1.src_pos_in_parent.data(), P1.src_pos_in_parent.size(), yu.data());
+        orc_aggregate_pull_f32(lv1.size(), P1.offsets.data(), P1.neighbors.data(), P1.weights.data(), yu.data(), hid,
+                               xg1.data());
+        std::vector<float> pc(lv1.size() * hid), g1(lv1.size() * hid), yc0(lv1.size() * f), wg0(f * hid);
+        orc_gather_rows_f32(p0.data(), hid, lv1.data(), lv1.size(), pc.data());
+        orc_relu_backward_f32(xg1.data(), pc.data(), pc.size(), g1.data());
+        orc_gather_rows_f32(y0.data(), f, lv1.data(), lv1.size(), yc0.data());
+        orc_gemm_at_b_f32(yc0.data(), lv1.size(), f, g1.data(), hid, wg0.data());
+        report("device backward_epp W' bit-exact vs oracle",
+               std::memcmp(wg[1].download().data.data(), wg1.data(), wg1.size() * 4) == 0 &&
+                   std::memcmp(wg[0].download().data.data(), wg0.data(), wg0.size() * 4) == 0);
+        report("backward_edges_per_layer = path edge counts",
+               wc.backward_edges_per_layer == std::vector<std::uint64_t>{P1.offsets.back(), P0.offsets.back()});
+        bool stale = false;
+        try {
+            backward_epp(pgr, rf, arts, top, W, GatherMode::Local, stamp ^ 1);
+        } catch (const StalenessError&) {
+            stale = true;
+        }
+        report("stale fingerprint -> StalenessError", stale);
+        // Alg. 1 and if-else reproduce the same top-layer W' only up to the
+        // inactive rows' zero terms; both must run and return finite shapes
+        auto wa = backward_all_active(gg, arts, top, W);
+        auto wi = backward_ifelse(gg, rf, arts, top, W);
+        report("all-active / if-else backward shapes", wa[0].rows() == f && wi[1].cols() == cls);
+    }
+    // file formats (test_edge_list.cpp, test_training_set.cpp)
+    {
+        const std::string path = "/tmp/pg_dropin_edges.txt";
+        FILE* fp = std::fopen(path.c_str(), "w");
+        std::fputs("# c\n3 3\n0 3\n1 2\n", fp);
+        std::fclose(fp);
+        const EdgeList el = load_edge_list_file(path);
+        report("load_edge_list_file comments / self loops",
+               el.pairs.size() == 2 && el.pairs[0] == std::pair<VertexId, VertexId>{0, 3} && el.self_loops_dropped == 1);
+        fp = std::fopen(path.c_str(), "w");
+        std::fputs("0 1\n0 x\n", fp);
+        std::fclose(fp);
+        std::size_t line = 0;
+        try {
+            load_edge_list_file(path);
+        } catch (const ParseError& e) {
+            line = e.line_number;
+        }
+        report("ParseError carries line 2", line == 2);
+        bool io = false;
+        try {
+            load_edge_list_file("/nonexistent/x.txt");
+        } catch (const IoError&) {
+            io = true;
+        }
+        report("missing file -> IoError", io);
     }
     std::printf("%d failure(s)\n", g_fail);
     return g_fail;

@@ -37,4 +37,4 @@ def test_cpp_dropin_runs():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert "[FAIL]" not in r.stdout and r.stdout.count("[PASS]") >= 14
+    assert "[FAIL]" not in r.stdout and r.stdout.count("[PASS]") >= 22

@@ -1,0 +1,60 @@
+"""Summarise an `ncu --page raw --csv` export into the profiles/ JSON that
+bench.py reads for roofline.traffic (dram read+write bytes per launch of the
+dominant kernel) and the judge reads for the kernel metrics.
+
+usage: python tools/ncu_summary.py RAW.csv OUT.json --command "..." \
+           --algorithmic-bytes B [--dominant REGEX]"""
+import argparse
+import csv
+import json
+import re
+
+METRICS = [
+    "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_sector_hit_rate.pct",
+    "l1tex__t_sector_hit_rate.pct", "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "launch__registers_per_thread", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+    "lts__throughput.avg.pct_of_peak_sustained_elapsed", "l1tex__throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed", "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
+    "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum",
+    "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio", "launch__grid_size",
+    "launch__block_size", "sm__inst_executed.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+]
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+
+
+def to_bytes(val, unit):
+    return float(val.replace(",", "")) * SCALE.get(unit, 1)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("raw")
+    ap.add_argument("out")
+    ap.add_argument("--command", required=True)
+    ap.add_argument("--workload", default="reddit-shaped (V=232965, E=114.6M), 1x B200")
+    ap.add_argument("--algorithmic-bytes", type=int, required=True)
+    ap.add_argument("--dominant", default=r"k_agg_vec4<32")
+    ap.add_argument("--round", type=int, default=1)
+    a = ap.parse_args()
+    rows = list(csv.reader(open(a.raw)))
+    hdr, units = rows[0], rows[1]
+    kernels, dom = [], None
+    for r in rows[2:]:
+        k = {"kernel": r[hdr.index("Kernel Name")].split("(")[0]}
+        for m in METRICS:
+            if m in hdr:
+                i = hdr.index(m)
+                k[m] = f"{r[i]} {units[i]}".strip()
+        kernels.append(k)
+        if dom is None and re.search(a.dominant, r[hdr.index("Kernel Name")]):
+            i, j = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
+            dom = (k["kernel"], int(to_bytes(r[i], units[i]) + to_bytes(r[j], units[j])))
+    out = {"round": a.round, "command": a.command, "workload": a.workload,
+           "dominant_kernel": dom[0] if dom else None, "dram_bytes_per_launch": dom[1] if dom else None,
+           "algorithmic_bytes_per_launch": a.algorithmic_bytes, "kernels": kernels}
+    json.dump(out, open(a.out, "w"), indent=1)
+    print(json.dumps({k: v for k, v in out.items() if k != "kernels"}))
+
+
+if __name__ == "__main__":
+    main()
