@@ -686,11 +686,20 @@ def measure_e2e(pg, pgd, torch, dist, paths, groups, shards, dims, rows, world, 
         def one():
             for i in range(L):
                 pg.backward_aggregation(groups[i], ys[i], xs[i], overwrite=True)
-        one()
-        t = time.perf_counter()
-        for _ in range(steps):
+        for _ in range(3):
             one()
-        sec = (time.perf_counter() - t) / steps
+        per = []
+        for _ in range(steps):
+            t1 = time.perf_counter()
+            one()
+            per.append((time.perf_counter() - t1) * 1e3)
+        log(f"[e2e] per-step ms {[round(x, 2) for x in per]}")
+        # the host call's wall time has rare multi-x outliers on the shared
+        # VM boxes (host-side stalls, not the pipeline: the device phase
+        # trace is flat); the median is reported, the mean kept beside it
+        sec = statistics.median(per) / 1e3
+        stats = {"stat": f"median of {steps} steps", "mean_ms": round(statistics.mean(per), 3),
+                 "min_ms": round(min(per), 3), "max_ms": round(max(per), 3)}
     else:
         ys, yd, yf, xd, xh = [], [], [], [], []
         for i, p in enumerate(paths):
@@ -733,8 +742,9 @@ def measure_e2e(pg, pgd, torch, dist, paths, groups, shards, dims, rows, world, 
         tt = torch.tensor([sec], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         sec = float(tt.item())
+        stats = {"stat": f"mean of {steps} steps, max over ranks"}
     return {"value": round(ep_bytes / sec / 1e9, 2), "unit": "GB/s", "ms_per_step": round(sec * 1e3, 3),
-            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": steps,
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": steps, **stats,
             "api": "pg_backward_aggregate_host (pinned host buffers)" if world == 1 else
                    "H2D shard + NCCL all-gather-v + pg_backward_aggregate_rows + D2H shard"}
 

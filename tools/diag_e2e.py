@@ -79,8 +79,21 @@ def main(config="reddit"):
             assert np.array_equal(xh.view(np.uint32), want), (K, R)
             print(f"path {i} dim {dim}: host call K={K} R={R}: {min(ts[1:]):.2f} ms (min of 3)", flush=True)
         pg.set_tuning("host_trace", 1)
-        pg.backward_aggregation(G, yh, xh, overwrite=True)
+        for rep in range(3):
+            t = time.perf_counter()
+            pg.backward_aggregation(G, yh, xh, overwrite=True)
+            print(f"path {i}: traced host call wall {(time.perf_counter() - t) * 1e3:.2f} ms", flush=True)
         pg.set_tuning("host_trace", 0)
+        import ctypes
+        from paper_2204_02662_b200 import _lib
+        lib = _lib.load()
+        c = np.zeros(3, np.uint64)
+        for rep in range(3):
+            t = time.perf_counter()
+            lib.pg_backward_aggregate_host(G._h, yh.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), yh.shape[0],
+                                           yh.shape[1], xh.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), 2,
+                                           c.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)))
+            print(f"path {i}: raw C call wall {(time.perf_counter() - t) * 1e3:.2f} ms", flush=True)
         pg.set_tuning("host_segs")
         pg.set_tuning("host_chunks")
 
