@@ -38,6 +38,7 @@ constexpr TuneKey kTuneKeys[] = {
     {"host_segs", "PG_HOST_SEGS", 3},      // host drop-in: source-row segments (H2D overlap)
     {"host_chunks", "PG_HOST_CHUNKS", 4},  // host drop-in: row chunks of the last pass (D2H overlap)
     {"host_trace", "PG_HOST_TRACE", 0},    // host drop-in: print phase times to stderr
+    {"heavy_narrow", "PG_HEAVY_NARROW", 0},  // heavy rows <= 64 floats: 1 = k_agg_narrow_lat, 0 = coop tiles (default: measured faster)
 };
 std::atomic<int64_t> g_tune[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];
 std::once_flag g_tune_once;
@@ -547,6 +548,74 @@ __global__ void __launch_bounds__(256) k_agg_wide_lat(const uint64_t* __restrict
         if (col + 1 < dim) orow[1] = acc.y;
         if (col + 2 < dim) orow[2] = acc.z;
     }
+}
+
+// Heavy narrow destinations (rows of <= 64 floats): a warp per (hub, 32-float
+// column chunk), one SCALAR column per lane. A float4-per-lane layout leaves
+// a 16-float row on 4 lanes and its serial chain at ~6 instructions per
+// edge; here every lane carries one column's chain (FMUL + FADD per edge)
+// while all 32 lanes keep a 32-edge batch of row gathers in flight (records
+// loaded coalesced one per lane, sources broadcast by shuffle, the batch
+// forced in flight by the runtime-zero dependency). The hub's chain is the
+// only serial part: ~deg x 4 cycles.
+template <bool FILT>
+__global__ void __launch_bounds__(256) k_agg_narrow_lat(const uint64_t* __restrict__ ebeg,
+                                                       const uint64_t* __restrict__ eend,
+                                                       const Edge* __restrict__ edges,
+                                                       const uint32_t* __restrict__ order, uint32_t d_begin,
+                                                       uint64_t n_items, uint32_t chunks,
+                                                       const float* __restrict__ in, uint64_t ld_in,
+                                                       float* __restrict__ out, uint64_t ld_out, uint32_t dim,
+                                                       int accumulate, uint32_t zmask, AggExt ext) {
+    const uint64_t item = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+    if (item >= n_items) return;
+    const unsigned lane = lane_id();
+    const uint32_t d = order[d_begin + item / chunks];
+    if (FILT && !ext_dst_on(ext, d)) return;
+    const uint32_t col = static_cast<uint32_t>(item % chunks) * 32 + lane;
+    const bool active = col < dim;
+    const uint64_t eb = ebeg[d], ee = eend[d];
+    const uint32_t row = ext_out_row(ext, d);
+    float* orow = out + row * ld_out + col;
+    float acc = (accumulate && active) ? *orow : 0.f;
+    const float* icol = in + (active ? col : 0u);
+    Edge nxt = eb + lane < ee ? __ldg(edges + eb + lane) : make_uint2(0u, 0u);
+    for (uint64_t e0 = eb; e0 < ee; e0 += 32) {
+        Edge cur = nxt;
+        if (e0 + 32 + lane < ee) nxt = __ldg(edges + e0 + 32 + lane);
+        const uint32_t n = static_cast<uint32_t>(min(static_cast<uint64_t>(32), ee - e0));
+        if (FILT && lane < n && !ext_src_on(ext, cur.x)) cur.y = 0u;  // skipped: a +-0 term
+        if (n == 32) {
+            float x[32];
+#pragma unroll
+            for (int u = 0; u < 32; ++u) {
+                const uint32_t src = __shfl_sync(0xffffffffu, cur.x, u);
+                x[u] = __ldg(icol + static_cast<uint64_t>(src) * ld_in);
+            }
+            uint32_t all = 0;
+#pragma unroll
+            for (int u = 0; u < 32; ++u) all ^= __float_as_uint(x[u]);
+            all &= zmask;
+#pragma unroll
+            for (int u = 0; u < 32; ++u) {
+                const float w = __uint_as_float(__shfl_sync(0xffffffffu, cur.y, u) ^ all);
+                acc = __fadd_rn(acc, __fmul_rn(w, x[u]));
+            }
+        } else {
+            for (uint32_t j = 0; j < n; ++j) {
+                const uint32_t src = __shfl_sync(0xffffffffu, cur.x, j);
+                const float w = __uint_as_float(__shfl_sync(0xffffffffu, cur.y, j));
+                acc = __fadd_rn(acc, __fmul_rn(w, __ldg(icol + static_cast<uint64_t>(src) * ld_in)));
+            }
+        }
+    }
+    if (!active) return;
+    acc = __fadd_rn(acc, 0.f);
+    if (ext.relu_pre) {
+        const uint32_t prow = ext.pre_rows ? __ldg(ext.pre_rows + d) : row;
+        acc = ext.relu_pre[static_cast<uint64_t>(prow) * ext.ld_pre + col] > 0.f ? acc : 0.f;
+    }
+    *orow = acc;
 }
 
 // Alternative heavy wide kernel (PG_HEAVY_WIDE=async): warp per (destination, 32-float4 chunk) like
@@ -1068,6 +1137,19 @@ void aggregate_det(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges
                         kZeros);
                 PG_LAUNCH("k_agg_wide_async");
             }
+        } else if (tuning(kTuneHeavyNarrow) == 1 && !heavy_use_tma()) {
+            // narrow rows: scalar column per lane, 32-edge batches in flight
+            const uint32_t chunks = (dim32 + 31) / 32;
+            const uint64_t items = static_cast<uint64_t>(nh) * chunks;
+            if (filt)
+                k_agg_narrow_lat<true><<<grid_for(items * 32, 256), 256, 0, ss.s>>>(
+                    ebeg, eend, edges, order, d_begin, items, chunks, in, ld_in, out, ld_out, dim32, accumulate, 0u,
+                    ext);
+            else
+                k_agg_narrow_lat<false><<<grid_for(items * 32, 256), 256, 0, ss.s>>>(
+                    ebeg, eend, edges, order, d_begin, items, chunks, in, ld_in, out, ld_out, dim32, accumulate, 0u,
+                    ext);
+            PG_LAUNCH("k_agg_narrow_lat");
         } else if (nq > 8)
             launch_heavy_any<16>(ebeg, eend, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim32, accumulate,
                                  ss.s, ext);

@@ -238,7 +238,8 @@ enum TuneKeyId {
     kTuneChunkMajor = 2,
     kTuneHostSegs = 3,
     kTuneHostChunks = 4,
-    kTuneHostTrace = 5
+    kTuneHostTrace = 5,
+    kTuneHeavyNarrow = 6
 };
 int64_t tuning(int key);
 bool set_tuning(const char* name, int64_t value);

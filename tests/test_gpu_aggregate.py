@@ -98,9 +98,10 @@ def test_backward_aggregation_bit_exact(pg, orc, dim):
         tol_check(got, orc, op, y_used)
 
 
+@pytest.mark.parametrize("narrow", [0, 1])
 @pytest.mark.parametrize("heavy_min", [1, 0, 64])
 @pytest.mark.parametrize("dim", [1, 16, 41, 130, 602])
-def test_heavy_ring_kernel_bit_exact(pg, orc, dim, heavy_min):
+def test_heavy_ring_kernel_bit_exact(pg, orc, dim, heavy_min, narrow):
     """Force every (heavy_min=1), none (0) or some (64) destinations onto the
     TMA bulk-copy ring kernel; results must not change by a bit, including
     accumulate semantics."""
@@ -111,6 +112,7 @@ def test_heavy_ring_kernel_bit_exact(pg, orc, dim, heavy_min):
     rng = np.random.default_rng(dim + heavy_min)
     try:
         pg.set_heavy_min_degree(heavy_min)
+        pg.set_tuning("heavy_narrow", narrow)
         for dp, op in zip(dps, ops):
             y = rng.uniform(-1, 1, size=(dp.P, dim)).astype(np.float32)
             base = rng.uniform(-1, 1, size=(dp.D, dim)).astype(np.float32)
@@ -128,6 +130,7 @@ def test_heavy_ring_kernel_bit_exact(pg, orc, dim, heavy_min):
             assert np.array_equal(bits(x2.cpu().numpy()), bits(want[b[1]:b[2]]))
     finally:
         pg.set_heavy_min_degree(None)
+        pg.set_tuning("heavy_narrow")
 
 
 def test_aggregate_pull_local_and_accumulate(pg, orc):
