@@ -251,6 +251,8 @@ def main():
     ap.add_argument("--heavy-sweep", action="store_true", help="diagnostics: heavy-kernel threshold sweep")
     ap.add_argument("--tune-sweep", action="store_true", help="diagnostics: SpMM scheduling-knob sweep")
     ap.add_argument("--no-chain", action="store_true", help="skip the forward/backward-variant chain timing")
+    ap.add_argument("--train-sweep", action="store_true",
+                    help="training-fraction sweep (default on for products): EPP stage vs the all-active pull")
     ap.add_argument("--gs-sweep", action="store_true",
                     help="structure-aware gs sweep (default on for arxiv): measured grouped-kernel curve vs the "
                          "regression and cost-model choices")
@@ -445,6 +447,8 @@ def main():
     if not args.profile and not args.no_e2e:
         line["e2e"] = measure_e2e(pg, pgd, torch, dist, paths, groups, shards, dims, rows, world, rank, dev,
                                   max(3, min(args.steps, 10)), ep_bytes)
+    if not args.profile and world == 1 and (args.train_sweep or args.config == "products"):
+        line["train_sweep"] = train_sweep(pg, torch, g, cfg, dims, dev)
     if not args.profile and world == 1 and (args.gs_sweep or args.config == "arxiv"):
         line["gs_sweep"] = gs_sweep(pg, prep, dims)
     if not args.profile and not args.no_chain and world == 1:
@@ -458,6 +462,57 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def train_sweep(pg, torch, g, cfg, dims, dev, ratios=(0.01, 0.02, 0.05, 0.08, 0.2, 0.5, 1.0), reps=5):
+    """configs[4] (products): the backward-aggregation stage per epoch as the
+    training fraction goes 1 -> 100 %, execution paths (this build) against
+    the all-active pull over the whole graph at the same widths — the
+    paper's work-reduction claim, on the device. Also the path-build time."""
+    L = len(cfg["dims"])
+    Gg = pg.group_neighbors(g, 1)
+    ys_full = []
+    for i in range(L):
+        y = pg.empty_rows(g.n, dims[i], device=dev)
+        y.uniform_(-1, 1)
+        ys_full.append(y)
+    xs_full = [pg.empty_rows(g.n, dims[i], device=dev) for i in range(L)]
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return statistics.median(ts)
+
+    all_ms = timed(lambda: [pg.aggregate_pull(Gg, ys_full[i], xs_full[i], overwrite=True) for i in range(L)])
+    out = {"all_active_stage_ms": round(all_ms, 4), "all_active_edges": [g.m] * L, "points": []}
+    for r in ratios:
+        vt = pg.sample_training_set(g.n, r, TRAIN_SEED)
+        torch.cuda.synchronize()
+        t0 = time.time()
+        prep = pg.prepare_paths(g, vt, L, dims, gs_strategy="regression")
+        prep_s = time.time() - t0
+        ys = []
+        for i, p in enumerate(prep.paths):
+            y = pg.empty_rows(p.P, dims[i], device=dev)
+            y.uniform_(-1, 1)
+            ys.append(y)
+        xs = [pg.empty_rows(p.D, dims[i], device=dev) for i, p in enumerate(prep.paths)]
+        ms = timed(lambda: [pg.backward_aggregation(prep.groups[i], ys[i], xs[i], overwrite=True) for i in range(L)])
+        out["points"].append({"train_ratio": r, "V_t": int(len(vt)), "epp_stage_ms": round(ms, 4),
+                              "epp_edges": [p.E for p in prep.paths],
+                              "speedup_vs_all_active": round(all_ms / ms, 3), "path_prep_s": round(prep_s, 3)})
+        log(f"[train_sweep] ratio {r}: epp {ms:.3f} ms vs all-active {all_ms:.3f} ms, edges "
+            f"{[p.E for p in prep.paths]}, prep {prep_s:.2f} s")
+        del prep, ys, xs
+    return out
 
 
 def gs_sweep(pg, prep, dims, repeats=5):
