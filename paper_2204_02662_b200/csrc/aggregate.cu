@@ -38,7 +38,8 @@ constexpr TuneKey kTuneKeys[] = {
     {"host_segs", "PG_HOST_SEGS", 3},      // host drop-in: source-row segments (H2D overlap)
     {"host_chunks", "PG_HOST_CHUNKS", 4},  // host drop-in: row chunks of the last pass (D2H overlap)
     {"host_trace", "PG_HOST_TRACE", 0},    // host drop-in: print phase times to stderr
-    {"heavy_narrow", "PG_HEAVY_NARROW", 0},  // heavy rows <= 64 floats: 1 = k_agg_narrow_lat, 0 = coop tiles (default: measured faster)
+    {"heavy_narrow", "PG_HEAVY_NARROW", 0},
+    {"wide_lpd", "PG_WIDE_LPD", 32},       // wide rows: lanes per (destination, chunk) item, 32 or 16  // heavy rows <= 64 floats: 1 = k_agg_narrow_lat, 0 = coop tiles (default: measured faster)
 };
 std::atomic<int64_t> g_tune[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];
 std::once_flag g_tune_once;
@@ -1181,7 +1182,10 @@ void aggregate_det(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges
         const uint64_t items = static_cast<uint64_t>(nd) * chunks;
         if (U == 0) {  // the main kernel
             const int64_t vu = tuning(kTuneVecU);
-            if (vu == 4)
+            if (tuning(kTuneWideLpd) == 16)  // 64-float chunks: half the per-pass source working set
+                launch_vec4<16, 8>(ebeg, eend, edges, order, d_begin, nd, (nq + 15) / 16, in, ld_in, out, ld_out,
+                                   dim32, accumulate, s, ext);
+            else if (vu == 4)
                 launch_vec4<32, 4>(ebeg, eend, edges, order, d_begin, nd, chunks, in, ld_in, out, ld_out, dim32,
                                    accumulate, s, ext);
             else if (vu == 16)

@@ -239,7 +239,8 @@ enum TuneKeyId {
     kTuneHostSegs = 3,
     kTuneHostChunks = 4,
     kTuneHostTrace = 5,
-    kTuneHeavyNarrow = 6
+    kTuneHeavyNarrow = 6,
+    kTuneWideLpd = 7
 };
 int64_t tuning(int key);
 bool set_tuning(const char* name, int64_t value);
