@@ -39,7 +39,8 @@ constexpr TuneKey kTuneKeys[] = {
     {"host_chunks", "PG_HOST_CHUNKS", 4},  // host drop-in: row chunks of the last pass (D2H overlap)
     {"host_trace", "PG_HOST_TRACE", 0},    // host drop-in: print phase times to stderr
     {"heavy_narrow", "PG_HEAVY_NARROW", 0},
-    {"wide_lpd", "PG_WIDE_LPD", 32},       // wide rows: lanes per (destination, chunk) item, 32 or 16  // heavy rows <= 64 floats: 1 = k_agg_narrow_lat, 0 = coop tiles (default: measured faster)
+    {"wide_lpd", "PG_WIDE_LPD", 32},       // wide rows: lanes per (destination, chunk) item, 32 or 16
+    {"src_segs", "PG_SRC_SEGS", 0},        // whole-path SpMM source segments: 0 = auto (L2-sized), K = forced  // heavy rows <= 64 floats: 1 = k_agg_narrow_lat, 0 = coop tiles (default: measured faster)
 };
 std::atomic<int64_t> g_tune[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];
 std::once_flag g_tune_once;

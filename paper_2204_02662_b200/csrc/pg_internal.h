@@ -137,6 +137,9 @@ struct Groups {
     DevBuf<uint64_t> host_seg_bnd;
     uint64_t host_seg_rows = 0;
     uint32_t host_seg_k = 0;
+    // automatic L2-sized source segments of a whole-path SpMM (api.cu)
+    DevBuf<uint64_t> auto_seg_bnd;
+    uint32_t auto_seg_k = 0;
 };
 
 // seg_bnd for cuts[0..K] over the path's edge stream (binary search per
@@ -240,7 +243,8 @@ enum TuneKeyId {
     kTuneHostChunks = 4,
     kTuneHostTrace = 5,
     kTuneHeavyNarrow = 6,
-    kTuneWideLpd = 7
+    kTuneWideLpd = 7,
+    kTuneSrcSegs = 8
 };
 int64_t tuning(int key);
 bool set_tuning(const char* name, int64_t value);
