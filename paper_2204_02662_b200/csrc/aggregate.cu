@@ -956,29 +956,66 @@ __global__ void __launch_bounds__(256) k_agg_heavy_coop(const uint64_t* __restri
     };
 
     const Zs z = zs_of(zeros);
-    const bool owner = tid < 32 && lane < nqc;
-    const uint32_t col = (q0 + lane) * 4;
     const uint32_t row = ext_out_row(ext, d);
-    float* orow = out + row * ld_out + col;
-    Acc acc = acc_load(orow, col, dim, owner && accumulate);
-    if (ntiles) {
-        gather(0);
-        stash(0);
-    }
-    __syncthreads();
-    for (uint64_t t = 0; t < ntiles; ++t) {
-        const int b = static_cast<int>(t & 1);
-        if (t + 1 < ntiles) gather(t + 1);  // loads in flight during the fold
-        if (owner) {
-            const uint32_t n = static_cast<uint32_t>(min(static_cast<uint64_t>(T), ee - (eb + t * T)));
-            const float4* sb = tile + b * T * CHQ + lane;
-            const float* sw = wt + b * T;
-            for (uint32_t j = 0; j < n; ++j) acc_step(acc, sw[j], sb[j * CHQ], z);
+    if constexpr (CHQ <= 8) {
+        // rows of <= 32 floats: fold one SCALAR column per lane (FMUL + FADD
+        // per edge) instead of a float4 on CHQ lanes (6 instructions per
+        // edge on a quarter of the warp) — the hub's serial chain is the
+        // critical path of the narrow top-layer SpMM
+        const uint32_t scol = q0 * 4 + lane;
+        const bool sowner = tid < 32 && scol < dim && lane < 4 * nqc;
+        float* srow = out + row * ld_out + scol;
+        float sacc = (sowner && accumulate) ? *srow : 0.f;
+        if (ntiles) {
+            gather(0);
+            stash(0);
         }
-        if (t + 1 < ntiles) stash(b ^ 1);
         __syncthreads();
+        for (uint64_t t = 0; t < ntiles; ++t) {
+            const int b = static_cast<int>(t & 1);
+            if (t + 1 < ntiles) gather(t + 1);  // loads in flight during the fold
+            if (sowner) {
+                const uint32_t n = static_cast<uint32_t>(min(static_cast<uint64_t>(T), ee - (eb + t * T)));
+                const float* sb = reinterpret_cast<const float*>(tile + b * T * CHQ) + lane;
+                const float* sw = wt + b * T;
+#pragma unroll 4
+                for (uint32_t j = 0; j < n; ++j) sacc = __fadd_rn(sacc, __fmul_rn(sw[j], sb[j * CHQ * 4]));
+            }
+            if (t + 1 < ntiles) stash(b ^ 1);
+            __syncthreads();
+        }
+        if (sowner) {
+            float v = __fadd_rn(sacc, 0.f);
+            if (ext.relu_pre) {
+                const uint32_t prow = ext.pre_rows ? __ldg(ext.pre_rows + d) : row;
+                v = ext.relu_pre[static_cast<uint64_t>(prow) * ext.ld_pre + scol] > 0.f ? v : 0.f;
+            }
+            *srow = v;
+        }
+    } else {
+        const bool owner = tid < 32 && lane < nqc;
+        const uint32_t col = (q0 + lane) * 4;
+        float* orow = out + row * ld_out + col;
+        Acc acc = acc_load(orow, col, dim, owner && accumulate);
+        if (ntiles) {
+            gather(0);
+            stash(0);
+        }
+        __syncthreads();
+        for (uint64_t t = 0; t < ntiles; ++t) {
+            const int b = static_cast<int>(t & 1);
+            if (t + 1 < ntiles) gather(t + 1);  // loads in flight during the fold
+            if (owner) {
+                const uint32_t n = static_cast<uint32_t>(min(static_cast<uint64_t>(T), ee - (eb + t * T)));
+                const float4* sb = tile + b * T * CHQ + lane;
+                const float* sw = wt + b * T;
+                for (uint32_t j = 0; j < n; ++j) acc_step(acc, sw[j], sb[j * CHQ], z);
+            }
+            if (t + 1 < ntiles) stash(b ^ 1);
+            __syncthreads();
+        }
+        if (owner) acc_store_ext(orow, col, dim, acc, z, ext, d, row);
     }
-    if (owner) acc_store_ext(orow, col, dim, acc, z, ext, d, row);
 }
 
 template <int CHQ, bool FILT>
