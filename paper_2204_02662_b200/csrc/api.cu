@@ -148,10 +148,14 @@ void check_dims(uint64_t dim, uint64_t ld_in, uint64_t ld_out) {
 // rule): two when one chunk-major pass would gather from more than ~80 MB
 // (P rows x 512 B) and at most ~400 MB; more passes cost an output
 // read+write each and lost in the measured sweep (K = 3, 4, 6).
-uint32_t auto_src_segments(uint64_t P, uint64_t dim) {
+uint32_t auto_src_segments(uint64_t P, uint64_t D, uint64_t E, uint64_t dim) {
     const int64_t forced = tuning(kTuneSrcSegs);
     if (forced > 0) return static_cast<uint32_t>(std::min<int64_t>(forced, 16));
     if ((dim + 3) / 4 <= 16) return 1;  // narrow rows: one pass, the rows are small
+    // an extra pass re-reads and re-writes every output row: only worth it
+    // when gathers dominate (measured: products' top path, E/D = 4, lost
+    // 1.5 -> 2.8 ms with two passes)
+    if (E < 64 * D) return 1;
     const uint64_t w = P * 512;
     return (w > (80ull << 20) && w <= (400ull << 20)) ? 2 : 1;
 }
@@ -207,7 +211,7 @@ void pg::run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re,
         // pass gathers from a working set of P/K rows x 512 B that stays in
         // L2 (measured on the Reddit layer-0 path: K = 2 17.9 -> 16.3 ms).
         if (sel.seg < 0 && parent_indexed && !G.edges_remap.get() && !edges_override) {
-            const uint32_t K = auto_src_segments(p.P, dim);
+            const uint32_t K = auto_src_segments(p.P, p.D, p.E, dim);
             if (K > 1) {
                 if (G.auto_seg_k != K) {
                     std::vector<uint64_t> cuts(K + 1);

@@ -34,6 +34,8 @@ def main():
     ap.add_argument("--workload", default="reddit-shaped (V=232965, E=114.6M), 1x B200")
     ap.add_argument("--algorithmic-bytes", type=int, required=True)
     ap.add_argument("--dominant", default=r"k_agg_vec4<32")
+    ap.add_argument("--path-kernels", default=None,
+                    help="regex of every launch of the dominant path (summed: passes + concurrent heavy kernel)")
     ap.add_argument("--round", type=int, default=1)
     a = ap.parse_args()
     rows = list(csv.reader(open(a.raw)))
@@ -49,6 +51,17 @@ def main():
         if dom is None and re.search(a.dominant, r[hdr.index("Kernel Name")]):
             i, j = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
             dom = (k["kernel"], int(to_bytes(r[i], units[i]) + to_bytes(r[j], units[j])))
+    if a.path_kernels:
+        tot, names, dur = 0, [], 0.0
+        for r in rows[2:]:
+            name = r[hdr.index("Kernel Name")]
+            if re.search(a.path_kernels, name):
+                i, j = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
+                tot += int(to_bytes(r[i], units[i]) + to_bytes(r[j], units[j]))
+                names.append(name.split("(")[0])
+                k = hdr.index("gpu__time_duration.sum")
+                dur += float(r[k].replace(",", "")) * (1e-3 if units[k] == "us" else (1e-6 if units[k] == "ns" else 1.0))
+        dom = ("+".join(names) + " (one path execution)", tot)
     out = {"round": a.round, "command": a.command, "workload": a.workload,
            "dominant_kernel": dom[0] if dom else None, "dram_bytes_per_launch": dom[1] if dom else None,
            "algorithmic_bytes_per_launch": a.algorithmic_bytes, "kernels": kernels}
