@@ -322,7 +322,9 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
     DevBuf<float> fin(packed ? 0 : in_rows * dim, s), din(in_rows * ld, s);
     DevBuf<float> fout(packed ? 0 : D * dim, s), dout(D * ld, s);
     const bool big = G.path && D >= 16384 && dim * 4 * D >= (32ull << 20);
-    const uint32_t K = (big && parent_indexed && in_rows >= 4)
+    // source segments re-read and re-write the output once per extra pass:
+    // only when gathers dominate (E >= 64 D), like the device-side rule
+    const uint32_t K = (big && parent_indexed && in_rows >= 4 && b.E >= 64ull * D)
                            ? static_cast<uint32_t>(std::clamp<int64_t>(tuning(kTuneHostSegs), 1, 8)) : 1;
     const uint32_t R = big ? static_cast<uint32_t>(std::clamp<int64_t>(tuning(kTuneHostChunks), 1, 16)) : 1;
     const bool trace = tuning(kTuneHostTrace) != 0;
