@@ -298,6 +298,7 @@ def main():
     prep = pg.prepare_paths(g, vt, L, dims, gs_strategy="regression")
     t_prep = time.time() - t2
     paths, groups = prep.paths, prep.groups
+    path_build = measure_path_build(pg, torch, g, vt, L) if world == 1 and not args.profile else None
     assert g.m == cfg["m"], (g.m, cfg["m"])
     log(f"[bench] gen {t_gen:.1f}s graph {t_graph:.2f}s prep {t_prep:.2f}s n={g.n} m={g.m} "
         f"paths D/S/E={[(p.D, p.S, p.E) for p in paths]} gs={prep.gs}")
@@ -441,6 +442,7 @@ def main():
         "epoch_compulsory_bytes": sum(compulsory_bytes(p.D, p.S, p.E, dims[i]) for i, p in enumerate(paths)),
         "prep_s": {"rmat_gen_host": round(t_gen, 2), "graph_build": round(t_graph, 3),
                    "paths_groups_gs": round(t_prep, 3)},
+        "path_build": path_build,
         "paths": [{"layer": p.layer, "D": p.D, "S": p.S, "E": p.E, "gs": prep.gs[i]} for i, p in enumerate(paths)],
     }
 
@@ -462,6 +464,42 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def measure_path_build(pg, torch, g, vt, L, reps=3):
+    """The execution-path preparer on the device (compute_frontiers +
+    prepare_all_paths, a-4..a-6), timed apart from the host-serial FNV
+    fingerprint, with its algorithmic bytes: per frontier level
+    sum over the level of (16 + 4 deg) + n/8; per path sum over D of
+    (16 + 4 deg_G) + 8E (weights read) + 12E (index + f64 weight written) +
+    8D + 8S."""
+    offs = g.export()[0].astype(np.int64)
+    deg = np.diff(offs)
+
+    def run():
+        F = pg.compute_frontiers(g, vt, L)
+        return F, pg.prepare_all_paths(g, F)
+
+    run()
+    ts = []
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        F, paths = run()
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t)
+    sec = statistics.median(ts)
+    levels = [F.level(k) for k in range(L + 1)]
+    b = sum(int((16 + 4 * deg[lv]).sum()) + g.n // 8 for lv in levels[:-1])
+    for i, p in enumerate(paths):
+        b += int((16 + 4 * deg[levels[i + 1]]).sum()) + 20 * p.E + 8 * p.D + 8 * p.S
+    t = time.perf_counter()
+    pg.path_fingerprint(g, vt, L)
+    fp_s = time.perf_counter() - t
+    return {"frontiers_and_paths_ms": round(sec * 1e3, 3), "algorithmic_bytes": b,
+            "GBps": round(b / sec / 1e9, 1), "fingerprint_host_s": round(fp_s, 3),
+            "note": "device path build (a-4..a-6) vs the reference's serial build; fingerprint is the "
+                    "host FNV-1a over the graph (csr_graph.cpp:19-31), cached per graph"}
 
 
 def train_sweep(pg, torch, g, cfg, dims, dev, ratios=(0.01, 0.02, 0.05, 0.08, 0.2, 0.5, 1.0), reps=5):

@@ -66,3 +66,14 @@ def test_candidates_match_oracle(orc):
 
     for md in (0, 1, 4, 5, 214, 52471, 2**31):
         assert np.array_equal(pg.default_gs_candidates(md), orc.default_candidates(md))
+
+
+def test_tuning_keys(pg):
+    """pg_set_tuning: scheduling knobs by name; unknown keys are config errors."""
+    for key in ("vec_u", "chunk_major", "wide_u", "host_segs", "host_chunks", "host_trace", "heavy_narrow",
+                "wide_lpd", "src_segs"):
+        pg.set_tuning(key, None)
+    import pytest
+
+    with pytest.raises(pg.ConfigError):
+        pg.set_tuning("no_such_knob", 1)
