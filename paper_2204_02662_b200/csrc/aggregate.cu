@@ -40,7 +40,8 @@ constexpr TuneKey kTuneKeys[] = {
     {"host_trace", "PG_HOST_TRACE", 0},    // host drop-in: print phase times to stderr
     {"heavy_narrow", "PG_HEAVY_NARROW", 0},
     {"wide_lpd", "PG_WIDE_LPD", 32},       // wide rows: lanes per (destination, chunk) item, 32 or 16
-    {"src_segs", "PG_SRC_SEGS", 0},        // whole-path SpMM source segments: 0 = auto (L2-sized), K = forced  // heavy rows <= 64 floats: 1 = k_agg_narrow_lat, 0 = coop tiles (default: measured faster)
+    {"src_segs", "PG_SRC_SEGS", 0},        // whole-path SpMM source segments: 0 = auto (L2-sized), K = forced
+    {"ld_cg", "PG_LD_CG", 0},              // row gathers: 0/1 = ld.global.nc (L1), 2 = ld.global.cg (L2 only)  // heavy rows <= 64 floats: 1 = k_agg_narrow_lat, 0 = coop tiles (default: measured faster)
 };
 std::atomic<int64_t> g_tune[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];
 std::once_flag g_tune_once;
@@ -157,7 +158,18 @@ __device__ __forceinline__ void acc_store(float* orow, uint32_t col, uint32_t di
 
 // 128-bit read-only row gather at base + src * ld_bytes: one IMAD.WIDE.U32
 // per edge (the 32x32->64 multiply-add cannot overflow for ld_bytes < 2^32).
+// CG = true: ld.global.cg (L2 only, no L1 allocation) — for gathers whose
+// L1 reuse does not pay for the L1/TEX wavefront cost
+template <bool CG = false>
 __device__ __forceinline__ float4 ld_row(const char* base, uint32_t src, uint32_t ld_bytes) {
+    if constexpr (CG) {
+        float4 r;
+        const char* p = base + static_cast<uint64_t>(src) * ld_bytes;
+        asm volatile("ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                     : "l"(p));
+        return r;
+    }
     float4 r;
     const char* p = base + static_cast<uint64_t>(src) * ld_bytes;
     asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];"
@@ -231,7 +243,7 @@ __device__ __forceinline__ void acc_store_ext(float* orow, uint32_t col, uint32_
 // of U edges: U edge-record loads, U row gathers (all in flight), then the
 // U ordered accumulate steps. Lanes past dim gather column 0 (in bounds,
 // discarded) so no load is predicated.
-template <int LPD, int U, bool FILT>
+template <int LPD, int U, bool FILT, bool CG = false>
 __global__ void __launch_bounds__(256, (U <= 8 ? 4 : 2)) k_agg_vec4(const uint64_t* __restrict__ ebeg, const uint64_t* __restrict__ eend,
                                                  const Edge* __restrict__ edges,
                                                  const uint32_t* __restrict__ order, uint32_t d_begin,
@@ -270,7 +282,7 @@ __global__ void __launch_bounds__(256, (U <= 8 ? 4 : 2)) k_agg_vec4(const uint64
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             if (FILT && !ext_src_on(ext, ed[u].x)) x[u] = make_float4(0.f, 0.f, 0.f, 0.f);  // skipped: +-0 term
-            else x[u] = ld_row(base, ed[u].x, ld_in_bytes);
+            else x[u] = ld_row<CG>(base, ed[u].x, ld_in_bytes);
         }
         const Zs zz = batch_dep<U>(x, z, zmask);
 #pragma unroll
@@ -285,7 +297,7 @@ __global__ void __launch_bounds__(256, (U <= 8 ? 4 : 2)) k_agg_vec4(const uint64
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             if (FILT && !ext_src_on(ext, ed[u].x)) x[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-            else x[u] = ld_row(base, ed[u].x, ld_in_bytes);
+            else x[u] = ld_row<CG>(base, ed[u].x, ld_in_bytes);
         }
         const Zs zz = batch_dep<U>(x, z, zmask);
 #pragma unroll
@@ -1085,8 +1097,15 @@ void launch_vec4(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges, 
                  uint32_t dim, bool accumulate, cudaStream_t s, const AggExt& ext) {
     const uint64_t items = static_cast<uint64_t>(nd) * chunks;
     const int cm = chunks > 1 && tuning(kTuneChunkMajor) ? 1 : 0;
+    // L2-only gathers measured no faster for narrow rows and slower for wide
+    // ones (layer 0 16.7 -> 17.1 ms), so only on request
+    const bool cg = tuning(kTuneLdCg) == 2;
     if (ext.src_bits || ext.dst_bits)
         k_agg_vec4<LPD, U, true><<<grid_for(items * LPD, 256), 256, 0, s>>>(
+            ebeg, eend, edges, order, d_begin, items, chunks, in, static_cast<uint32_t>(ld_in * 4), out, ld_out, dim,
+            accumulate, kZeros, 0u, cm, ext);
+    else if (cg)
+        k_agg_vec4<LPD, U, false, true><<<grid_for(items * LPD, 256), 256, 0, s>>>(
             ebeg, eend, edges, order, d_begin, items, chunks, in, static_cast<uint32_t>(ld_in * 4), out, ld_out, dim,
             accumulate, kZeros, 0u, cm, ext);
     else

@@ -244,7 +244,8 @@ enum TuneKeyId {
     kTuneHostTrace = 5,
     kTuneHeavyNarrow = 6,
     kTuneWideLpd = 7,
-    kTuneSrcSegs = 8
+    kTuneSrcSegs = 8,
+    kTuneLdCg = 9
 };
 int64_t tuning(int key);
 bool set_tuning(const char* name, int64_t value);
