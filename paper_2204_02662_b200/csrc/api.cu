@@ -394,7 +394,13 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
     PG_CUDA(cudaStreamWaitEvent(s, cs.ev[K], 0));
     const unsigned last_flags = K > 1 ? (flags & ~PG_AGG_OVERWRITE) : flags;
     const SegSel last = K > 1 ? SegSel{G.host_seg_bnd.get(), static_cast<int>(K - 1), K} : SegSel{};
-    for (size_t r = 0; r + 1 < cuts.size(); ++r) {
+    // Chunks are edge-balanced, so in destination order (hubs first) the
+    // first chunks hold few rows and the last hold most of them: run them
+    // last-first (tuning "host_chunk_order" = 1, default) so the big D2H
+    // copies start early and the tail after the final chunk is a small one.
+    const bool reverse = tuning(kTuneHostChunkOrder) == 1;
+    for (size_t ri = 0; ri + 1 < cuts.size(); ++ri) {
+        const size_t r = reverse ? cuts.size() - 2 - ri : ri;
         const uint32_t rb = cuts[r], re = cuts[r + 1];
         if (rb == re) continue;
         run_aggregate(G, parent_indexed, rb, re, din.get(), ld, dout.get() + rb * ld, ld, dim, last_flags, s, last);

@@ -245,7 +245,8 @@ enum TuneKeyId {
     kTuneHeavyNarrow = 6,
     kTuneWideLpd = 7,
     kTuneSrcSegs = 8,
-    kTuneLdCg = 9
+    kTuneLdCg = 9,
+    kTuneHostChunkOrder = 10
 };
 int64_t tuning(int key);
 bool set_tuning(const char* name, int64_t value);

@@ -67,17 +67,20 @@ def main(config="reddit"):
             dev_ms = (time.perf_counter() - t) * 1e3
         print(f"path {i} dim {dim}: device call {dev_ms:.2f} ms", flush=True)
         want = xd.cpu().numpy().view(np.uint32)
-        shapes = [(2, 4)] if i == 0 else [(1, 1), (1, 4), (2, 1), (2, 4), (2, 8), (3, 4), (4, 4), (4, 8), (2, 4)]
-        for K, R in shapes:
+        shapes = [(2, 4, 1)] if i == 0 else [(1, 1, 1), (2, 4, 0), (2, 4, 1), (3, 4, 0), (3, 4, 1), (3, 8, 1),
+                                              (2, 8, 1), (4, 8, 1), (3, 16, 1), (3, 4, 1)]
+        for K, R, order in shapes:
             pg.set_tuning("host_segs", K)
             pg.set_tuning("host_chunks", R)
+            pg.set_tuning("host_chunk_order", order)
             ts = []
             for rep in range(4):
                 t = time.perf_counter()
                 pg.backward_aggregation(G, yh, xh, overwrite=True)
                 ts.append((time.perf_counter() - t) * 1e3)
             assert np.array_equal(xh.view(np.uint32), want), (K, R)
-            print(f"path {i} dim {dim}: host call K={K} R={R}: {min(ts[1:]):.2f} ms (min of 3)", flush=True)
+            print(f"path {i} dim {dim}: host call K={K} R={R} reversed={order}: {min(ts[1:]):.2f} ms (min of 3)",
+                  flush=True)
         pg.set_tuning("host_trace", 1)
         for rep in range(3):
             t = time.perf_counter()
@@ -96,6 +99,7 @@ def main(config="reddit"):
             print(f"path {i}: raw C call wall {(time.perf_counter() - t) * 1e3:.2f} ms", flush=True)
         pg.set_tuning("host_segs")
         pg.set_tuning("host_chunks")
+        pg.set_tuning("host_chunk_order")
 
 
 if __name__ == "__main__":
