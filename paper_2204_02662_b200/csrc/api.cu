@@ -268,6 +268,27 @@ void pg::run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re,
     }
     if (!G.graph_order.get() && g.n)
         degree_order(g.offsets.get(), g.n, G.graph_order, lib_stream(g.device), &G.graph_hist);
+    // the same L2-sized source segments as a path (forward / all-active /
+    // if-else pulls over the whole graph): rows of g.edges are sorted by
+    // neighbour id, so segment passes in order are the serial order
+    const uint32_t K = auto_src_segments(g.n, g.n, g.m, dim);
+    if (K > 1) {
+        if (G.auto_seg_k != K) {
+            std::vector<uint64_t> cuts(K + 1);
+            for (uint32_t k = 0; k <= K; ++k) cuts[k] = static_cast<uint64_t>(g.n) * k / K;
+            segment_bounds(g.offsets.get(), g.edges.get(), g.n, cuts.data(), K, G.auto_seg_bnd, lib_stream(g.device));
+            G.auto_seg_k = K;
+        }
+        for (uint32_t k = 0; k < K; ++k) {
+            AggExt ek = ext;
+            if (k + 1 < K) ek.relu_pre = nullptr;  // the epilogue applies to finished rows only
+            const uint64_t* eb = G.auto_seg_bnd.get() + static_cast<uint64_t>(k) * g.n;
+            aggregate_det(eb, eb + g.n, g.edges.get(), G.graph_order.get(), g.n, 0, g.n,
+                          G.graph_hist.heavy(heavy_min_degree(dim, g.m / K)), in, ld_in, out, ld_out, dim,
+                          accumulate || k > 0, s, ek);
+        }
+        return;
+    }
     aggregate_det(g.offsets.get(), g.offsets.get() + 1, g.edges.get(), G.graph_order.get(), g.n, 0, g.n,
                   G.graph_hist.heavy(heavy_min_degree(dim, g.m)), in, ld_in, out, ld_out, dim, accumulate, s, ext);
 }

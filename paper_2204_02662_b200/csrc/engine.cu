@@ -99,60 +99,84 @@ __device__ __forceinline__ void cp_async(void* dst, const void* src, bool ok) {
                      : "memory");
 }
 
-// V = floats per cp.async (4: 16-byte copies, needs 16-byte aligned rows and
-// column tiles; 1: any layout)
-template <int TI, int TC, int V>
+template <int TI, int TC>
 __host__ __device__ constexpr int atb_kc() {  // rows per tile: the stage ring stays under 48 KB of static smem
     return TC <= 32 ? 64 : (TC <= 64 ? 32 : 16);
 }
 
+// V = floats per cp.async (4: 16-byte copies, needs 16-byte aligned rows and
+// column tiles; 1: any layout). The gathered A row ids of each thread's
+// copies (engine.hpp:323 gather_rows fused) are read one tile ahead of the
+// copies, so no copy issue waits on a rows[] load (that wait was ~30% of the
+// kernel when the id load sat in front of every tile's copies).
 template <int TI, int TC, int V>
 __global__ void __launch_bounds__(TI* TC) k_gemm_at_b(const float* __restrict__ a, uint64_t lda,
                                                       const uint32_t* __restrict__ rows, const float* __restrict__ b,
                                                       uint64_t ldb, float* __restrict__ out, uint64_t ldo, uint64_t n,
                                                       uint64_t r, uint64_t c) {
-    constexpr int kAtbKC = atb_kc<TI, TC, V>();
+    constexpr int KC = atb_kc<TI, TC>();
     constexpr int NT = TI * TC;
-    constexpr int TILE = kAtbKC * (TI + TC);
+    constexpr int TILE = KC * (TI + TC);
+    constexpr int AV = TI % V == 0 ? V : 1;  // A tile rows of TI floats
+    constexpr int AE = KC * TI / AV;           // A copies per tile
+    constexpr int EPT = (AE + NT - 1) / NT;    // ... per thread
     __shared__ __align__(16) float sm[kAtbStages * TILE];
     const unsigned tid = threadIdx.x;
     const uint64_t i0 = blockIdx.x * static_cast<uint64_t>(TI), j0 = blockIdx.y * static_cast<uint64_t>(TC);
     const unsigned ti = tid / TC, tj = tid % TC;
-    const uint64_t ntiles = (n + kAtbKC - 1) / kAtbKC;
-    auto load = [&](uint64_t t) {
-        float* st = sm + (t % kAtbStages) * TILE;
-        const uint64_t k0 = t * kAtbKC;
-        constexpr int AV = TI % V == 0 ? V : 1;  // A tile rows of TI floats
-        for (int e = tid; e < kAtbKC * TI / AV; e += NT) {
-            const int kk = e / (TI / AV), ii = (e % (TI / AV)) * AV;
-            const bool ok = k0 + kk < n && i0 + ii < r;
-            const uint64_t row = ok ? (rows ? __ldg(rows + k0 + kk) : k0 + kk) : 0;
-            cp_async<AV * 4>(st + kk * TI + ii, ok ? a + row * lda + i0 + ii : a, ok);
+    const uint64_t ntiles = (n + KC - 1) / KC;
+    struct Rows {
+        uint64_t r[EPT];
+    };
+    auto row_of = [&](uint64_t t) {  // A rows of this thread's elements of tile t
+        Rows out;
+#pragma unroll
+        for (int q = 0; q < EPT; ++q) {
+            const int e = tid + q * NT;
+            const uint64_t k = t * KC + e / (TI / AV);
+            out.r[q] = (e < AE && k < n) ? (rows ? __ldg(rows + k) : k) : 0;
         }
-        float* sb = st + kAtbKC * TI;
-        for (int e = tid; e < kAtbKC * TC / V; e += NT) {
+        return out;
+    };
+    auto load = [&](uint64_t t, const Rows& ar) {
+        float* st = sm + (t % kAtbStages) * TILE;
+        const uint64_t k0 = t * KC;
+#pragma unroll
+        for (int q = 0; q < EPT; ++q) {
+            const int e = tid + q * NT;
+            if (e < AE) {
+                const int kk = e / (TI / AV), ii = (e % (TI / AV)) * AV;
+                const bool ok = k0 + kk < n && i0 + ii < r;
+                cp_async<AV * 4>(st + kk * TI + ii, ok ? a + ar.r[q] * lda + i0 + ii : a, ok);
+            }
+        }
+        float* sb = st + KC * TI;
+#pragma unroll
+        for (int e = tid; e < KC * TC / V; e += NT) {
             const int kk = e / (TC / V), jj = (e % (TC / V)) * V;
             const bool ok = k0 + kk < n && j0 + jj < c;
             cp_async<V * 4>(sb + kk * TC + jj, ok ? b + (k0 + kk) * ldb + j0 + jj : b, ok);
         }
     };
-#pragma unroll
+#pragma unroll 1
     for (int t = 0; t < kAtbStages - 1; ++t) {
-        if (static_cast<uint64_t>(t) < ntiles) load(t);
+        if (static_cast<uint64_t>(t) < ntiles) load(t, row_of(t));
         asm volatile("cp.async.commit_group;" ::: "memory");
     }
+    Rows next_row = row_of(kAtbStages - 1);
     float acc = 0.f;
     for (uint64_t t = 0; t < ntiles; ++t) {
         asm volatile("cp.async.wait_group %0;" ::"n"(kAtbStages - 2) : "memory");
         __syncthreads();  // tile t resident for every thread; tile t-1's slot is free
-        if (t + kAtbStages - 1 < ntiles) load(t + kAtbStages - 1);
+        if (t + kAtbStages - 1 < ntiles) load(t + kAtbStages - 1, next_row);
         asm volatile("cp.async.commit_group;" ::: "memory");
+        next_row = row_of(t + kAtbStages);  // consumed next iteration: its latency hides behind this tile
         const float* sa = sm + (t % kAtbStages) * TILE + ti;
-        const float* sb = sm + (t % kAtbStages) * TILE + kAtbKC * TI + tj;
-        const uint64_t rem = n - t * kAtbKC;
-        if (rem >= static_cast<uint64_t>(kAtbKC)) {
+        const float* sb = sm + (t % kAtbStages) * TILE + KC * TI + tj;
+        const uint64_t rem = n - t * KC;
+        if (rem >= static_cast<uint64_t>(KC)) {
 #pragma unroll
-            for (int kk = 0; kk < kAtbKC; ++kk) acc = __fadd_rn(acc, __fmul_rn(sa[kk * TI], sb[kk * TC]));
+            for (int kk = 0; kk < KC; ++kk) acc = __fadd_rn(acc, __fmul_rn(sa[kk * TI], sb[kk * TC]));
         } else {
             for (int kk = 0; kk < static_cast<int>(rem); ++kk)
                 acc = __fadd_rn(acc, __fmul_rn(sa[kk * TI], sb[kk * TC]));

@@ -67,8 +67,8 @@ def main(config="reddit"):
             dev_ms = (time.perf_counter() - t) * 1e3
         print(f"path {i} dim {dim}: device call {dev_ms:.2f} ms", flush=True)
         want = xd.cpu().numpy().view(np.uint32)
-        shapes = [(2, 4, 1)] if i == 0 else [(1, 1, 1), (2, 4, 0), (2, 4, 1), (3, 4, 0), (3, 4, 1), (3, 8, 1),
-                                              (2, 8, 1), (4, 8, 1), (3, 16, 1), (3, 4, 1)]
+        shapes = [(2, 4, 1)] if i == 0 else [(1, 1, 1), (1, 8, 1), (1, 16, 1), (1, 32, 1), (2, 16, 1), (2, 32, 1),
+                                              (3, 16, 1), (3, 32, 1), (4, 16, 1), (3, 16, 0)]
         for K, R, order in shapes:
             pg.set_tuning("host_segs", K)
             pg.set_tuning("host_chunks", R)
