@@ -50,6 +50,7 @@ CASES = [
     (1024, 8192, 7, 0.1, 2, 24, 16, 4, True),
     (512, 3000, 3, 0.05, 3, 12, 8, 3, False),
     (2048, 9000, 11, 0.5, 2, 40, 33, 7, True),
+    (700, 2500, 5, 0.2, 1, 9, 0, 5, True),  # a single layer: no relu, W'^(0) only
 ]
 
 

@@ -180,3 +180,25 @@ def test_aggregate_pull_filtered(pg, orc, cuda):
             want, wc = orc.aggregate_pull_filtered_f32(g_o.offsets, g_o.neighbors, g_o.weights, y, da, sa, 4)
             assert same(host(out), want), (dim, dl, sl)
             assert c == wc
+
+
+def test_filtered_unaligned_rows_scalar_path(pg, orc, cuda):
+    """aggregate_pull_filtered on rows whose pitch is not a multiple of 4
+    floats (the scalar kernel) — same bits as the oracle."""
+    import torch
+
+    case = CASES[0]
+    g_o, vt, x0, ws, r, g, Gg, prep, d = gpu_setup(pg, orc, case)
+    levels = orc.compute_frontiers(g_o, vt, 2)
+    dim = 7
+    y = np.random.default_rng(3).uniform(-1, 1, (g.n, dim)).astype(np.float32)
+    yd = torch.from_numpy(y).cuda()  # ld = 7: unaligned rows
+    out = torch.zeros((g.n, dim), dtype=torch.float32, device="cuda")
+    c = {}
+    pg.aggregate_pull_filtered(Gg, prep.frontiers, 2, 1, yd, out, counters=c)
+    da = np.zeros(g.n, np.uint8)
+    da[levels[2]] = 1
+    sa = np.zeros(g.n, np.uint8)
+    sa[levels[1]] = 1
+    want, wc = orc.aggregate_pull_filtered_f32(g_o.offsets, g_o.neighbors, g_o.weights, y, da, sa, 4)
+    assert same(host(out), want) and c == wc
