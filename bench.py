@@ -455,6 +455,8 @@ def main():
         line["gs_sweep"] = gs_sweep(pg, prep, dims)
     if not args.profile and not args.no_chain and world == 1:
         line["chain"] = measure_chain(pg, torch, g, prep, cfg, vt, dev)
+    elif not args.profile and not args.no_chain:
+        line["chain"] = measure_chain_sharded(pg, pgd, torch, dist, g, prep, cfg, vt, dev, shards, rank, world)
     if not args.profile and not args.no_cpu and world == 1 and rank == 0:
         line["cpu_baseline"] = cpu_baseline(paths, dims, args)
 
@@ -652,6 +654,42 @@ def measure_chain(pg, torch, g, prep, cfg, vt, dev, reps=5):
     del arts, top, x0
     torch.cuda.synchronize()
     return out
+
+
+def measure_chain_sharded(pg, pgd, torch, dist, g, prep, cfg, vt, dev, shards, rank, world, reps=5):
+    """N > 1: the row-sharded backward_epp chain (dist.backward_epp: narrow g
+    all-gathered, W' and y_grad recomputed per rank, own destination rows
+    aggregated), timed with CUDA events, max over ranks; forward replicated."""
+    n, f, dims = g.n, cfg["f"], cfg["dims"]
+    L = len(dims)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(GRAD_SEED + 7)
+    x0 = pg.empty_rows(n, f, device=dev)
+    x0.uniform_(0, 1, generator=gen)
+    ins = [f] + dims[:-1]
+    ws = []
+    for l in range(L):
+        w = pg.empty_rows(ins[l], dims[l], device=dev)
+        w.uniform_(-0.1, 0.1, generator=gen)
+        ws.append(w)
+    arts = pg.forward(pg.group_neighbors(g, 1), x0, ws)
+    top = pg.empty_rows(n, dims[-1], device=dev)
+    top.uniform_(-1e-3, 1e-3, generator=gen)
+    pgd.backward_epp(prep, arts, top, ws, shards, rank)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        pgd.backward_epp(prep, arts, top, ws, shards, rank)
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    t = torch.tensor([statistics.median(ts)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return {"backward_epp_sharded_ms": round(float(t.item()), 3), "n_ranks": world,
+            "note": "row-sharded chain, narrow g all-gather-v per layer, max over ranks"}
 
 
 def time_steps(torch, step, L, reps=10):

@@ -159,3 +159,59 @@ def allgather_rows(shard, out, group=None):
         return out
     dist.all_gather_into_tensor(out, shard, group=group)
     return out
+
+
+def backward_epp(prepared, arts, top_grad, weights, plan_, rank, group=None):
+    """engine.hpp:316-346 (Local gather) row-sharded over the ranks of
+    ``group``, bit-identical to the single-GPU ``backward_epp``.
+
+    Every rank holds the forward artefacts, W and top_grad (replicated, as in
+    data-parallel GCN training). Per path i (layer l = L-1-i):
+      * W'[l] = gather_rows(Y[l], levels[i])^T g is computed on every rank
+        from the full g — one serial ascending chain per entry, like the
+        reference (a sum of per-rank partials + all-reduce would re-associate
+        the chain and change the bits);
+      * y_grad = g W[l]^T is also recomputed on every rank: it is the SpMM's
+        source matrix and every rank gathers arbitrary rows of it, and the
+        narrow g (dims[l] wide) is what travels — at Reddit layer 0 that is
+        233K x 16 floats (15 MB) instead of the 602-wide y_grad (566 MB);
+      * each rank aggregates its edge-balanced destination rows and applies
+        relu_backward with the gathered pre-activation rows (engine.hpp:
+        340-345), then one all-gather-v of the g row shards (NCCL P2P)
+        assembles the next layer's g in frontier order.
+    ``plan_`` is ``plan(...)`` over the paths (dest bounds per path).
+    Returns W' per layer (full, identical on every rank)."""
+    import torch
+
+    from . import pathgcn as pg
+
+    L = len(weights)
+    if len(prepared.groups) != L:
+        raise pg.StalenessError("epp backward: paths were prepared for a different layer count")
+    F = prepared.frontiers
+    dev = top_grad.device
+    lv = [torch.from_numpy(F.level(k).astype(np.int32)).to(dev) for k in range(L + 1)]
+    c = top_grad.shape[1]
+    g = pg.empty_rows(lv[0].shape[0], c, device=dev)
+    pg.gather_rows(top_grad, lv[0], g)
+    w_grads = [None] * L
+    for i in range(L):
+        l = L - 1 - i
+        p, G = prepared.paths[i], prepared.groups[i]
+        in_dim = weights[l].shape[0]
+        wg = pg.empty_rows(in_dim, weights[l].shape[1], device=dev)
+        pg.gemm_at_b(arts.y[l], g, wg, a_rows=lv[i])
+        w_grads[l] = wg
+        yg = pg.empty_rows(p.P, in_dim, device=dev)
+        pg.gemm_a_bt(g, weights[l], yg)
+        db, de = plan_[i].my_dest_rows(rank)
+        x = pg.empty_rows(de - db, in_dim, device=dev)
+        pg.backward_aggregation(G, yg, x, overwrite=True, rows=(db, de))
+        if l == 0:
+            break
+        pre = pg.empty_rows(de - db, in_dim, device=dev)
+        pg.gather_rows(arts.pre_act[l - 1], lv[i + 1][db:de], pre)
+        g = pg.empty_rows(p.D, in_dim, device=dev)
+        pg.relu_backward(x, pre, g[db:de])
+        allgatherv_rows(g, plan_[i].dest_bounds, rank, group)
+    return w_grads

@@ -90,3 +90,68 @@ def test_two_ranks_on_device_match_oracle():
     res = dict(q.get(timeout=10) for _ in range(2))
     assert res == {0: True, 1: True}, res
     assert all(p.exitcode == 0 for p in procs)
+
+
+def _chain_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    import torch
+    import torch.distributed as dist
+
+    import paper_2204_02662_b200 as pg
+    from conftest import rmat_pairs
+    from oracle.oracle import Oracle
+    from paper_2204_02662_b200 import dist as pgd
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ok = True
+    try:
+        orc = Oracle()
+        pairs, n_pad = rmat_pairs(orc, 4096, 4096 * 12, 31)
+        vt = orc.sample_training_set(4096, 0.2, 5)
+        g = pg.build_undirected_csr(pairs, n_hint=n_pad, weights="symnorm")
+        f, dims = 37, [19, 6]
+        prep = pg.prepare_paths(g, vt, 2, [dims[0], f])
+        rng = np.random.default_rng(9)  # identical inputs on every rank
+
+        def dev(a):
+            t = pg.empty_rows(a.shape[0], a.shape[1])
+            t.copy_(torch.from_numpy(a))
+            return t
+
+        x0 = dev(rng.uniform(0, 1, (g.n, f)).astype(np.float32))
+        ws = [dev(rng.uniform(-0.5, 0.5, (f, dims[0])).astype(np.float32)),
+              dev(rng.uniform(-0.5, 0.5, (dims[0], dims[1])).astype(np.float32))]
+        r = np.zeros((g.n, dims[1]), np.float32)
+        r[vt, rng.integers(0, dims[1], len(vt))] = 1
+        arts = pg.forward(pg.group_neighbors(g, 3), x0, ws)
+        top = pg.empty_rows(g.n, dims[1])
+        pg.top_grad_from_probs(arts.x[-1], dev(r), torch.from_numpy(vt.astype(np.int32)).cuda(), top)
+        want = pg.backward_epp(prep, arts, top, ws)
+        plan = pgd.plan([None, None], [p.P for p in prep.paths], world, [p.shard_bounds(world) for p in prep.paths])
+        got = pgd.backward_epp(prep, arts, top, ws, plan, rank)
+        torch.cuda.synchronize()
+        for a, b in zip(got, want):
+            ok = ok and torch.equal(a.view(torch.int32), b.view(torch.int32))
+    except Exception as e:  # pragma: no cover
+        q.put((rank, repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+    q.put((rank, ok))
+
+
+def test_sharded_backward_epp_chain_matches_single_gpu():
+    """dist.backward_epp (row-sharded chain, narrow g all-gathered, W' and
+    y_grad recomputed per rank) == the single-GPU chain, bit for bit."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_chain_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=600)
+    res = dict(q.get(timeout=10) for _ in range(2))
+    assert res == {0: True, 1: True}, res
+    assert all(p.exitcode == 0 for p in procs)
