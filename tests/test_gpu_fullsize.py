@@ -1,5 +1,6 @@
 """Full-size parity (BASELINE configs[3], the Reddit-shaped bench workload:
-V = 232,965, m = 114,615,892): at this size the CPU oracle cannot redo the
+V = 232,965, m = 114,615,892, and configs[4], products-shaped: V = 2,449,029,
+m = 61,859,140 at 8 % train — the sparse-frontier regime): at this size the CPU oracle cannot redo the
 whole epoch inside a test, so the checks are the size-independent ones —
 structural invariants of the device-built paths, bit-exact SpMM rows on a
 stride sample of destinations (the oracle restricted to those rows), and
@@ -16,11 +17,11 @@ def bits(a):
     return np.ascontiguousarray(a, np.float32).view(np.uint32)
 
 
-@pytest.fixture(scope="module")
-def reddit(pg):
+@pytest.fixture(scope="module", params=["reddit", "products"])
+def reddit(pg, request):
     import bench
 
-    cfg = bench.CONFIGS["reddit"]
+    cfg = bench.CONFIGS[request.param]
     pairs = bench.make_pairs(cfg, pg.gen_rmat)
     vt = pg.sample_training_set(cfg["V"], bench.train_ratio(cfg), bench.TRAIN_SEED)
     g = pg.build_undirected_csr(pairs, n_hint=cfg["V"], weights="symnorm")
