@@ -42,7 +42,8 @@ constexpr TuneKey kTuneKeys[] = {
     {"wide_lpd", "PG_WIDE_LPD", 32},       // wide rows: lanes per (destination, chunk) item, 32 or 16
     {"src_segs", "PG_SRC_SEGS", 0},        // whole-path SpMM source segments: 0 = auto (L2-sized), K = forced
     {"ld_cg", "PG_LD_CG", 0},              // row gathers: 0/1 = ld.global.nc (L1), 2 = ld.global.cg (L2 only)
-    {"host_chunk_order", "PG_HOST_CHUNK_ORDER", 1},  // host drop-in last pass: 1 = last row chunk first  // heavy rows <= 64 floats: 1 = k_agg_narrow_lat, 0 = coop tiles (default: measured faster)
+    {"host_chunk_order", "PG_HOST_CHUNK_ORDER", 1},  // host drop-in last pass: 1 = last row chunk first
+    {"grouped_seg", "PG_GROUPED_SEG", 0},  // grouped Fast: 1 = CTA-segmented reduction, 0 = an atomic per extra group  // heavy rows <= 64 floats: 1 = k_agg_narrow_lat, 0 = coop tiles (default: measured faster)
 };
 std::atomic<int64_t> g_tune[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];
 std::once_flag g_tune_once;
@@ -400,11 +401,134 @@ __global__ void __launch_bounds__(256, (U <= 8 ? 4 : 2)) k_agg_groups(
     }
 }
 
+// Fast with a CTA-segmented reduction (tuning "grouped_seg", off by default:
+// measured 1.6x faster at gs = 1 but 5-40 % slower over gs 8-512, where the
+// barrier and the serial run sums cost more than the atomics they save):
+// the items of a CTA are consecutive groups of one column chunk, so the
+// groups of a destination that land in the same CTA are combined in shared
+// memory, in group order, by the run's first item, which commits once — a
+// plain store when the run holds all of the destination's groups, one
+// atomic add per column otherwise. Global atomics drop from one per extra
+// group to one per CTA boundary a destination straddles.
+template <int LPD, int U>
+__global__ void __launch_bounds__(256, 4) k_agg_groups_seg(
+    const uint64_t* __restrict__ gbeg, const uint64_t* __restrict__ gend, const uint32_t* __restrict__ gdest,
+    const uint64_t* __restrict__ dest_groups, const Edge* __restrict__ edges, uint64_t n_items, uint32_t chunks,
+    const float* __restrict__ in, uint32_t ld_in_bytes, float* __restrict__ out, uint64_t ld_out, uint32_t dim,
+    int accumulate, float2 zeros, uint32_t zmask) {
+    constexpr int IPC = 256 / LPD;  // items per CTA
+    __shared__ float4 part[256];
+    __shared__ uint32_t s_dest[IPC], s_chunk[IPC];
+    __shared__ uint64_t s_group[IPC];
+    const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    const uint64_t item = t / LPD;
+    const unsigned it = threadIdx.x / LPD, sub = threadIdx.x % LPD;
+    const bool valid = item < n_items;
+    const Zs z = zs_of(zeros);
+    const uint64_t ng = n_items / chunks;
+    const uint64_t gi = valid ? item % ng : 0;  // chunk-major: consecutive items are consecutive groups
+    const uint32_t ci = valid ? static_cast<uint32_t>(item / ng) : 0;
+    const uint32_t d = valid ? __ldg(gdest + gi) : 0xffffffffu;
+    const uint32_t col = (ci * LPD + sub) * 4;
+    const bool active = valid && col < dim;
+    Acc acc{0ull, 0ull};
+    if (valid) {
+        uint64_t e = __ldg(gbeg + gi);
+        const uint64_t end = __ldg(gend + gi);
+        const char* base = reinterpret_cast<const char*>(in) + (active ? col : 0u) * 4u;
+        asm("mov.b64 %0, %0;" : "+l"(base));
+        for (; e + U <= end; e += U) {
+            Edge ed[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) ed[u] = ld_rec(edges + e + u);
+            float4 x[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) x[u] = ld_row(base, ed[u].x, ld_in_bytes);
+            const Zs zz = batch_dep<U>(x, z, zmask);
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc_step(acc, __uint_as_float(ed[u].y), x[u], zz);
+        }
+        if (e < end) {
+            const uint32_t n = static_cast<uint32_t>(end - e);
+            Edge ed[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) ed[u] = ld_rec(edges + e + (u < static_cast<int>(n) ? u : n - 1));
+            float4 x[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) x[u] = ld_row(base, ed[u].x, ld_in_bytes);
+            const Zs zz = batch_dep<U>(x, z, zmask);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (u < static_cast<int>(n)) acc_step(acc, __uint_as_float(ed[u].y), x[u], zz);
+        }
+    }
+    const float2 l = unpk2(acc.lo), h = unpk2(acc.hi);
+    part[threadIdx.x] = make_float4(l.x, l.y, h.x, h.y);
+    if (sub == 0) {
+        s_dest[it] = d;
+        s_chunk[it] = ci;
+        s_group[it] = gi;
+    }
+    __syncthreads();
+    if (!active) return;
+    if (it > 0 && s_dest[it - 1] == d && s_chunk[it - 1] == ci) return;  // not the head of its run
+    int last = it;
+    while (last + 1 < IPC && s_dest[last + 1] == d && s_chunk[last + 1] == ci) ++last;
+    float4 v = part[it * LPD + sub];
+    for (int k = it + 1; k <= last; ++k) {  // the run's partials in group order
+        const float4 p = part[k * LPD + sub];
+        v.x = __fadd_rn(v.x, p.x);
+        v.y = __fadd_rn(v.y, p.y);
+        v.z = __fadd_rn(v.z, p.z);
+        v.w = __fadd_rn(v.w, p.w);
+    }
+    float* orow = out + d * ld_out + col;
+    const bool full = col + 3 < dim;
+    const bool whole = s_group[it] == __ldg(dest_groups + d) && s_group[last] + 1 == __ldg(dest_groups + d + 1);
+    if (!whole) {  // the destination's other groups commit from other CTAs: output zeroed by the caller
+        if (full) {
+            atomicAdd(reinterpret_cast<float4*>(orow), v);
+        } else {
+            atomicAdd(orow, v.x);
+            if (col + 1 < dim) atomicAdd(orow + 1, v.y);
+            if (col + 2 < dim) atomicAdd(orow + 2, v.z);
+        }
+        return;
+    }
+    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (accumulate) {
+        if (full) o = *reinterpret_cast<const float4*>(orow);
+        else {
+            o.x = orow[0];
+            if (col + 1 < dim) o.y = orow[1];
+            if (col + 2 < dim) o.z = orow[2];
+        }
+    }
+    o.x = __fadd_rn(o.x, v.x);
+    o.y = __fadd_rn(o.y, v.y);
+    o.z = __fadd_rn(o.z, v.z);
+    o.w = __fadd_rn(o.w, v.w);
+    if (full) {
+        *reinterpret_cast<float4*>(orow) = o;
+    } else {
+        orow[0] = o.x;
+        if (col + 1 < dim) orow[1] = o.y;
+        if (col + 2 < dim) orow[2] = o.z;
+    }
+}
+
 template <int LPD>
 void launch_groups(const uint64_t* gbeg, const uint64_t* gend, const uint32_t* gdest, const uint64_t* dest_groups,
                    const Edge* edges, uint64_t G, uint32_t chunks, const float* in, uint64_t ld_in, float* out,
                    uint64_t ld_out, uint32_t dim, bool accumulate, cudaStream_t s) {
     const uint64_t items = G * chunks;
+    if (tuning(kTuneGroupedSeg)) {
+        k_agg_groups_seg<LPD, 8><<<grid_for(items * LPD, 256), 256, 0, s>>>(
+            gbeg, gend, gdest, dest_groups, edges, items, chunks, in, static_cast<uint32_t>(ld_in * 4), out, ld_out,
+            dim, accumulate, kZeros, 0u);
+        PG_LAUNCH("k_agg_groups_seg");
+        return;
+    }
     k_agg_groups<LPD, 8><<<grid_for(items * LPD, 256), 256, 0, s>>>(
         gbeg, gend, gdest, dest_groups, edges, items, chunks, in, static_cast<uint32_t>(ld_in * 4), out, ld_out, dim,
         accumulate, kZeros, 0u, chunks > 1 && tuning(kTuneChunkMajor) ? 1 : 0);

@@ -246,7 +246,8 @@ enum TuneKeyId {
     kTuneWideLpd = 7,
     kTuneSrcSegs = 8,
     kTuneLdCg = 9,
-    kTuneHostChunkOrder = 10
+    kTuneHostChunkOrder = 10,
+    kTuneGroupedSeg = 11
 };
 int64_t tuning(int key);
 bool set_tuning(const char* name, int64_t value);

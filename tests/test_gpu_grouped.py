@@ -23,10 +23,12 @@ def setup(pg, orc, n=2048, m=30000, seed=3, ratio=0.2):
     return g, paths, og, ops
 
 
+@pytest.mark.parametrize("seg", [0, 1])
 @pytest.mark.parametrize("dim", [16, 41, 602])
-def test_grouped_within_tolerance(pg, orc, cuda, dim):
+def test_grouped_within_tolerance(pg, orc, cuda, dim, seg):
     import torch
 
+    pg.set_tuning("grouped_seg", seg)
     g, paths, og, ops = setup(pg, orc)
     for p, op in zip(paths, ops):
         y = np.random.default_rng(dim).uniform(-1, 1, size=(p.P, dim)).astype(np.float32)
@@ -56,6 +58,7 @@ def test_grouped_within_tolerance(pg, orc, cuda, dim):
         torch.cuda.synchronize()
         err = np.abs(x.cpu().numpy().astype(np.float64) - (want64 + 1.0))
         assert (err <= 2e-6 + 1e-5 * (absum + 1.0)).all()
+    pg.set_tuning("grouped_seg")
 
 
 def test_grouped_graph_forward_pull(pg, orc, cuda):
