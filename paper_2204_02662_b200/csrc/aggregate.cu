@@ -31,6 +31,7 @@ struct TuneKey {
     const char* env;
     int64_t def;
 };
+// order = enum TuneKeyId (pg_internal.h)
 constexpr TuneKey kTuneKeys[] = {
     {"wide_u", "PG_WIDE_U", 0},            // wide rows: 0 = k_agg_vec4<32,U>, 8/16 = k_agg_wide<U>
     {"vec_u", "PG_VEC_U", 8},              // edges per gather batch in k_agg_vec4 (4, 8, 16)
@@ -38,12 +39,12 @@ constexpr TuneKey kTuneKeys[] = {
     {"host_segs", "PG_HOST_SEGS", 3},      // host drop-in: source-row segments (H2D overlap)
     {"host_chunks", "PG_HOST_CHUNKS", 16}, // host drop-in: row chunks of the last pass (D2H overlap)
     {"host_trace", "PG_HOST_TRACE", 0},    // host drop-in: print phase times to stderr
-    {"heavy_narrow", "PG_HEAVY_NARROW", 0},
+    {"heavy_narrow", "PG_HEAVY_NARROW", 0},  // heavy rows <= 64 floats: 1 = k_agg_narrow_lat, 0 = coop tiles
     {"wide_lpd", "PG_WIDE_LPD", 32},       // wide rows: lanes per (destination, chunk) item, 32 or 16
     {"src_segs", "PG_SRC_SEGS", 0},        // whole-path SpMM source segments: 0 = auto (L2-sized), K = forced
     {"ld_cg", "PG_LD_CG", 0},              // row gathers: 0/1 = ld.global.nc (L1), 2 = ld.global.cg (L2 only)
     {"host_chunk_order", "PG_HOST_CHUNK_ORDER", 1},  // host drop-in last pass: 1 = last row chunk first
-    {"grouped_seg", "PG_GROUPED_SEG", 0},  // grouped Fast: 1 = CTA-segmented reduction, 0 = an atomic per extra group  // heavy rows <= 64 floats: 1 = k_agg_narrow_lat, 0 = coop tiles (default: measured faster)
+    {"grouped_seg", "PG_GROUPED_SEG", 0},  // grouped Fast: 1 = CTA-segmented reduction, 0 = an atomic per extra group
 };
 std::atomic<int64_t> g_tune[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];
 std::once_flag g_tune_once;
