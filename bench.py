@@ -303,8 +303,37 @@ def main():
     log(f"[bench] gen {t_gen:.1f}s graph {t_graph:.2f}s prep {t_prep:.2f}s n={g.n} m={g.m} "
         f"paths D/S/E={[(p.D, p.S, p.E) for p in paths]} gs={prep.gs}")
 
-    # ---- sharding plan (identity at N=1)
+    # ---- sharding plan (identity at N=1): edge-balanced destination cuts,
+    # then calibrated once on measured shard times (hub chains make the
+    # shard holding the biggest hubs the slowest; dist.calibrate_bounds)
     dest_bounds = [p.shard_bounds(world) for p in paths]
+    shard_balance = None
+    if world > 1 and os.environ.get("PG_CALIBRATE_SHARDS", "1") == "1":
+        shard_balance = []
+        for i, p in enumerate(paths):
+            yt = pg.empty_rows(p.P, dims[i], device=dev)
+            yt.uniform_(-1, 1)
+
+            def time_shard(b0, b1, i=i, yt=yt):
+                x = pg.empty_rows(b1 - b0, dims[i], device=dev)
+                for _ in range(2):
+                    pg.backward_aggregation(groups[i], yt, x, overwrite=True, rows=(b0, b1))
+                ev = []
+                for _ in range(3):
+                    a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record()
+                    pg.backward_aggregation(groups[i], yt, x, overwrite=True, rows=(b0, b1))
+                    z.record()
+                    torch.cuda.synchronize()
+                    ev.append(a.elapsed_time(z))
+                return statistics.median(ev)
+
+            nb, t0, t1 = pgd.calibrate_bounds(time_shard, p.export()["offsets"], dest_bounds[i], iters=2, rank=rank)
+            dest_bounds[i] = nb
+            shard_balance.append({"path": i, "max_mean_ms_edge_balanced": [round(max(t0), 3),
+                                                                           round(statistics.mean(t0), 3)],
+                                  "max_mean_ms_calibrated": [round(max(t1), 3), round(statistics.mean(t1), 3)]})
+            del yt
     parent_rows = [p.P for p in paths]
     shards = pgd.plan([None] * L, parent_rows, world, dest_bounds)
     gen = torch.Generator(device=dev)
@@ -438,6 +467,7 @@ def main():
         "clocks": clk,
         "per_path_ms": [round(statistics.mean(x), 4) for x in spmm_ms],
         "allgather_ms": [round(statistics.mean(x), 4) for x in ag_ms] if world > 1 else None,
+        "shard_balance": shard_balance,
         "epoch_algorithmic_bytes": ep_bytes,
         "epoch_compulsory_bytes": sum(compulsory_bytes(p.D, p.S, p.E, dims[i]) for i, p in enumerate(paths)),
         "prep_s": {"rmat_gen_host": round(t_gen, 2), "graph_build": round(t_graph, 3),

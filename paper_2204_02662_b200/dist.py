@@ -215,3 +215,62 @@ def backward_epp(prepared, arts, top_grad, weights, plan_, rank, group=None):
         pg.relu_backward(x, pre, g[db:de])
         allgatherv_rows(g, plan_[i].dest_bounds, rank, group)
     return w_grads
+
+
+def balance_bounds(offsets, bounds, times):
+    """One re-balancing step of the destination-row cuts from measured
+    per-shard times: inside current shard r every edge is assumed to cost
+    times[r] / edges[r]; the new cuts split that piecewise-linear cost into
+    equal parts (at destination-row granularity, cuts kept monotone). Edge-
+    balanced cuts treat a hub's edges like any others, but a hub is a serial
+    chain: the shard holding the biggest hubs runs longest."""
+    offsets = np.asarray(offsets, np.int64)
+    b = [int(x) for x in bounds]
+    world = len(b) - 1
+    D = len(offsets) - 1
+    cost = np.zeros(D + 1, np.float64)  # cumulative cost at each destination row
+    for r in range(world):
+        e0, e1 = offsets[b[r]], offsets[b[r + 1]]
+        rate = float(times[r]) / max(int(e1 - e0), 1)
+        seg = offsets[b[r]:b[r + 1] + 1] - e0
+        cost[b[r]:b[r + 1] + 1] = cost[b[r]] + seg * rate
+    total = cost[-1]
+    out = [0]
+    for r in range(1, world):
+        row = int(np.searchsorted(cost, total * r / world, side="left"))
+        out.append(max(out[-1], min(row, D)))
+    out.append(D)
+    return np.array(out, np.int64)
+
+
+def calibrate_bounds(time_shard, offsets, bounds, iters=2, group=None, rank=None):
+    """Adjust the cuts until the measured shard times even out: ``time_shard
+    (b, e)`` runs destination rows [b, e) and returns milliseconds. With
+    ``rank`` set (N GPUs) each rank times its own shard and the times are
+    all-gathered, so every rank derives the same cuts; without it (one GPU)
+    all shards are timed in turn. Returns (bounds, times before, times after)."""
+    import torch
+
+    def measure(bb):
+        world = len(bb) - 1
+        if rank is None:
+            return [time_shard(int(bb[r]), int(bb[r + 1])) for r in range(world)]
+        import torch.distributed as dist
+
+        on = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+        t = torch.zeros(world, dtype=torch.float64, device=on)
+        t[rank] = time_shard(int(bb[rank]), int(bb[rank + 1]))
+        dist.all_reduce(t, group=group)  # every other entry is 0
+        return t.cpu().tolist()
+
+    b = np.asarray(bounds, np.int64)
+    first = measure(b)
+    times = first
+    for _ in range(iters):
+        nb = balance_bounds(offsets, b, times)
+        nt = measure(nb)
+        if max(nt) < max(times):
+            b, times = nb, nt
+        else:
+            break
+    return b, first, times

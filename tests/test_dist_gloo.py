@@ -103,3 +103,25 @@ def test_bounds_and_source_map(world):
     assert len(set(m.tolist())) == 1000 and m.max() < mr * world
     for r in range(world):
         assert np.array_equal(m[b[r]:b[r + 1]], r * mr + np.arange(b[r + 1] - b[r]))
+
+
+def test_balance_bounds_moves_cuts_toward_the_slow_shard():
+    """dist.balance_bounds: a shard measured slower than its edge share
+    loses destination rows; cuts stay monotone and cover every row."""
+    from paper_2204_02662_b200 import dist as pgd
+
+    deg = np.array([500, 400, 300] + [10] * 300, np.int64)
+    offs = np.concatenate([[0], np.cumsum(deg)])
+    b = pgd.edge_balanced_bounds(offs, 4)
+    t = [4.0, 1.0, 1.0, 1.0]  # shard 0 (the hubs) twice as slow per edge
+    nb = pgd.balance_bounds(offs, b, t)
+    assert nb[0] == 0 and nb[-1] == len(deg) and (np.diff(nb) >= 0).all()
+    assert nb[1] <= b[1]
+    # equal times leave edge-balanced cuts (up to row granularity) in place
+    eq = pgd.balance_bounds(offs, b, [1.0] * 4)
+    assert np.abs(eq - b).max() <= 1
+    # calibrate_bounds on one process: a synthetic cost model
+    rate = np.where(np.arange(len(deg)) < 3, 3.0, 1.0)
+    cost = lambda b0, b1: float((deg[b0:b1] * rate[b0:b1]).sum())
+    cb, t0, t1 = pgd.calibrate_bounds(cost, offs, b, iters=3)
+    assert max(t1) <= max(t0)
