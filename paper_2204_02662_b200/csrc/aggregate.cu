@@ -45,6 +45,7 @@ constexpr TuneKey kTuneKeys[] = {
     {"ld_cg", "PG_LD_CG", 0},              // row gathers: 0/1 = ld.global.nc (L1), 2 = ld.global.cg (L2 only)
     {"host_chunk_order", "PG_HOST_CHUNK_ORDER", 1},  // host drop-in last pass: 1 = last row chunk first
     {"grouped_seg", "PG_GROUPED_SEG", 0},  // grouped Fast: 1 = CTA-segmented reduction, 0 = an atomic per extra group
+    {"heavy_wide_pipe", "PG_HEAVY_WIDE_PIPE", 1},  // heavy wide rows: 1 = software-pipelined k_agg_wide_pipe
 };
 std::atomic<int64_t> g_tune[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];
 std::once_flag g_tune_once;
@@ -758,6 +759,97 @@ __global__ void __launch_bounds__(256) k_agg_narrow_lat(const uint64_t* __restri
     *orow = acc;
 }
 
+// Heavy wide destinations, software-pipelined (tuning "heavy_wide_pipe"):
+// a hub is one serial chain per column, so its time is (edges / batch) x
+// (gather latency + fold). Here the gathers of batch t+1 are issued before
+// batch t is folded (two register batches of U rows, ~160 registers: hubs
+// are few, occupancy is irrelevant), so the fold hides under the next
+// batch's latency. Records are loaded coalesced one per lane 32 at a time
+// and broadcast by shuffle; the runtime-zero dependency keeps each batch's
+// gathers issued together.
+template <int U>
+__global__ void __launch_bounds__(64) k_agg_wide_pipe(const uint64_t* __restrict__ ebeg,
+                                                     const uint64_t* __restrict__ eend,
+                                                     const Edge* __restrict__ edges,
+                                                     const uint32_t* __restrict__ order, uint32_t d_begin,
+                                                     uint64_t n_items, uint32_t chunks,
+                                                     const float* __restrict__ in, uint32_t ld_in_bytes,
+                                                     float* __restrict__ out, uint64_t ld_out, uint32_t dim,
+                                                     int accumulate, uint32_t zmask, AggExt ext) {
+    static_assert(32 % U == 0, "U divides the 32-record window");
+    const uint64_t item = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+    if (item >= n_items) return;
+    const unsigned lane = lane_id();
+    const uint32_t d = order[d_begin + item / chunks];
+    const uint32_t col = (static_cast<uint32_t>(item % chunks) * 32 + lane) * 4;
+    const bool active = col < dim;
+    const uint64_t eb = ebeg[d], ee = eend[d];
+    const uint32_t row = ext_out_row(ext, d);
+    float* orow = out + row * ld_out + col;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (accumulate && active) {
+        if (col + 3 < dim) acc = *reinterpret_cast<const float4*>(orow);
+        else {
+            acc.x = orow[0];
+            if (col + 1 < dim) acc.y = orow[1];
+            if (col + 2 < dim) acc.z = orow[2];
+        }
+    }
+    const char* base = reinterpret_cast<const char*>(in) + (active ? col : 0u) * 4u;
+    asm("mov.b64 %0, %0;" : "+l"(base));
+    const uint64_t nb = (ee - eb + U - 1) / U;
+    // record window: 32 records, one per lane; batch b uses records
+    // [eb + b*U, eb + b*U + U) = lanes ((b*U) % 32) ... of window (b*U)/32
+    Edge win = eb + lane < ee ? __ldg(edges + eb + lane) : make_uint2(0u, 0u);
+    Edge nwin = eb + 32 + lane < ee ? __ldg(edges + eb + 32 + lane) : make_uint2(0u, 0u);
+    float4 xa[U], xb[U];
+    float wa[U], wb[U];
+    auto gather = [&](uint64_t b, float4 (&x)[U], float (&w)[U]) {
+        const int s0 = static_cast<int>((b * U) & 31);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t src = __shfl_sync(0xffffffffu, win.x, s0 + u);
+            w[u] = __uint_as_float(__shfl_sync(0xffffffffu, win.y, s0 + u));  // 0 past the end
+            x[u] = ld_row(base, src, ld_in_bytes);
+        }
+        if (s0 + U == 32) {  // window consumed: slide
+            win = nwin;
+            const uint64_t e = eb + (b + 1) * U + 32 + lane;
+            nwin = e < ee ? __ldg(edges + e) : make_uint2(0u, 0u);
+        }
+    };
+    auto fold = [&](const float4 (&x)[U], const float (&w)[U]) {
+        uint32_t all = 0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) all ^= __float_as_uint(x[u].x);
+        all &= zmask;
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc4_scalar(acc, __uint_as_float(__float_as_uint(w[u]) ^ all), x[u]);
+    };
+    if (nb) gather(0, xa, wa);
+    for (uint64_t b = 0; b < nb; b += 2) {
+        if (b + 1 < nb) gather(b + 1, xb, wb);  // in flight while batch b folds
+        fold(xa, wa);
+        if (b + 1 < nb) {
+            if (b + 2 < nb) gather(b + 2, xa, wa);
+            fold(xb, wb);
+        }
+    }
+    if (!active) return;
+    acc.x = __fadd_rn(acc.x, 0.f);
+    acc.y = __fadd_rn(acc.y, 0.f);
+    acc.z = __fadd_rn(acc.z, 0.f);
+    acc.w = __fadd_rn(acc.w, 0.f);
+    acc = ext_relu(ext, d, row, col, dim, acc);
+    if (col + 3 < dim) {
+        __stcs(reinterpret_cast<float4*>(orow), acc);
+    } else {
+        orow[0] = acc.x;
+        if (col + 1 < dim) orow[1] = acc.y;
+        if (col + 2 < dim) orow[2] = acc.z;
+    }
+}
+
 // Alternative heavy wide kernel (PG_HEAVY_WIDE=async): warp per (destination, 32-float4 chunk) like
 // k_agg_wide, but each lane stages its column of NB 32-edge batches in
 // shared memory with cp.async (LDGSTS, 16 B), so NB*32 row gathers (up to
@@ -1299,7 +1391,12 @@ void aggregate_det(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges
                 const char* e = std::getenv("PG_HEAVY_WIDE");
                 return e && std::string(e) == "async";
             }();
-            if (!use_async || ext.any()) {
+            if (tuning(kTuneHeavyWidePipe) == 1 && !use_async) {
+                k_agg_wide_pipe<16><<<grid_for(items * 32, 64), 64, 0, ss.s>>>(
+                    ebeg, eend, edges, order, d_begin, items, chunks, in, static_cast<uint32_t>(ld_in * 4), out,
+                    ld_out, dim32, accumulate, 0u, ext);
+                PG_LAUNCH("k_agg_wide_pipe");
+            } else if (!use_async || ext.any()) {
                 k_agg_wide_lat<32><<<grid_for(items * 32, 256), 256, 0, ss.s>>>(
                     ebeg, eend, edges, order, d_begin, items, chunks, in, ld_in, out, ld_out, dim32, accumulate, 0u,
                     ext);

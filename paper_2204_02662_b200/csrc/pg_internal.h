@@ -247,7 +247,8 @@ enum TuneKeyId {
     kTuneSrcSegs = 8,
     kTuneLdCg = 9,
     kTuneHostChunkOrder = 10,
-    kTuneGroupedSeg = 11
+    kTuneGroupedSeg = 11,
+    kTuneHeavyWidePipe = 12
 };
 int64_t tuning(int key);
 bool set_tuning(const char* name, int64_t value);
