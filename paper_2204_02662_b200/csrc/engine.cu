@@ -280,11 +280,12 @@ __global__ void k_row_softmax(const float* __restrict__ x, uint64_t ldx, float* 
 // engine.hpp:146-156: grad = 0; grad[v] = (probs[v] - r[v]) * inv on V_t
 __global__ void k_top_grad(const float* __restrict__ probs, uint64_t ldp, const float* __restrict__ ref,
                            uint64_t ldr, const uint32_t* __restrict__ vt, uint64_t k, float inv,
-                           float* __restrict__ out, uint64_t ldo, uint32_t cols) {
+                           float* __restrict__ out, uint64_t ldo, uint32_t cols, uint64_t rows) {
     const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= cols) return;
     for (uint64_t i = blockIdx.y; i < k; i += gridDim.y) {
         const uint64_t v = vt[i];
+        if (v >= rows) continue;  // not a vertex of this graph: nothing to write
         out[v * ldo + c] = __fmul_rn(__fsub_rn(probs[v * ldp + c], ref[v * ldr + c]), inv);
     }
 }
@@ -387,7 +388,7 @@ void top_grad_from_probs(DMat probs, DMat ref, const uint32_t* vt, uint64_t k, D
     if (k == 0 || out.cols == 0) return;
     const float inv = 1.0f / static_cast<float>(k);  // T(1) / static_cast<T>(vt.size())
     k_top_grad<<<rows_grid(k, out.cols, 64), 64, 0, s>>>(probs.p, probs.ld, ref.p, ref.ld, vt, k, inv, out.p, out.ld,
-                                                          static_cast<uint32_t>(out.cols));
+                                                          static_cast<uint32_t>(out.cols), out.rows);
     PG_LAUNCH("k_top_grad");
 }
 
