@@ -30,7 +30,7 @@ constexpr int kThreads = 256;
 // chunks of 32 through shared memory; thread (i, j) keeps one ascending-k
 // chain per row.
 constexpr int kGT = 32;  // j tile / k chunk
-constexpr int kGRPW = 4;  // rows per warp
+constexpr int kGRPW = 16;  // rows per warp: 128-row tiles keep the grid of a write-bound gemm_a_bt (K = 16) from being launch-bound
 constexpr int kGI = 8 * kGRPW;
 
 template <bool BT>
