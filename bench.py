@@ -448,12 +448,20 @@ def main():
     peak, peak_src = hbm_peak()
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9
     traffic, traffic_src = ncu_traffic()
+    l2c = None
+    try:
+        gc = json.load(open(os.path.join(ROOT, "profiles", "gather_ceiling_r01.json")))
+        l2c = {"GBps": gc["l2_ceiling_GBps"], "frac": round(achieved / gc["l2_ceiling_GBps"], 4),
+               "source": "profiles/gather_ceiling_r01.json: " + gc["l2_ceiling_note"]}
+    except Exception:
+        pass
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic if world == 1 else None,
                 "kernel": f"k_agg_vec4 (path SG_{p.layer}, width {dims[dom]})",
                 "algorithmic_bytes_per_launch": dom_bytes, "avg_launch_ms": round(dom_ms, 4),
                 "peak_source": peak_src, "traffic_source": traffic_src,
-                "frac_vs_8TBps_spec": round(achieved / 8000.0, 4)}
+                "frac_vs_8TBps_spec": round(achieved / 8000.0, 4),
+                "l2_gather_ceiling": l2c}
 
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
