@@ -66,14 +66,16 @@ int pg_version(void);
 int pg_device_count(int* count);
 /* Scheduling knob (never changes results): destinations with at least this
  * many path edges run on the heavy-destination kernel (cooperative staged,
- * or the TMA bulk ring with PG_HEAVY_KERNEL=tma). 0 disables; UINT64_MAX
+ * or the TMA bulk ring with tuning "heavy_tma"). 0 disables; UINT64_MAX
  * (default, or $PG_HEAVY_MIN_DEG) = width dependent: 4096 for rows of <= 32
  * floats, off for wider rows. */
 int pg_set_heavy_min_degree(uint64_t min_degree);
 /* Other SpMM scheduling knobs (never change results), by name: "vec_u"
  * (edges per gather batch: 4, 8, 16), "chunk_major" (0/1: column-chunk-major
- * item order for rows wider than 128 floats), "wide_u" (0 = k_agg_vec4 for
- * wide rows, 8/16 = the shuffle-broadcast k_agg_wide<U>); for the host-buffer
+ * item order for rows wider than 128 floats), "heavy_tma" (1: heavy narrow
+ * destinations on the TMA cp.async.bulk + mbarrier ring), "heavy_narrow",
+ * "heavy_wide_pipe", "wide_lpd", "src_segs" (0 = automatic L2-sized source
+ * segments, K = forced), "ld_cg", "grouped_seg"; for the host-buffer
  * calls "host_segs" (source-row segments uploaded and reduced in turn, 1..8),
  * "host_chunks" (destination-row chunks of the last pass whose D2H overlaps
  * the next chunk, 1..16) and "host_trace" (1: phase times on stderr). A negative value

@@ -33,7 +33,7 @@ struct TuneKey {
 };
 // order = enum TuneKeyId (pg_internal.h)
 constexpr TuneKey kTuneKeys[] = {
-    {"wide_u", "PG_WIDE_U", 0},            // wide rows: 0 = k_agg_vec4<32,U>, 8/16 = k_agg_wide<U>
+    {"heavy_tma", "PG_HEAVY_TMA", 0},      // heavy narrow rows: 1 = TMA bulk-copy mbarrier ring (k_agg_heavy)
     {"vec_u", "PG_VEC_U", 8},              // edges per gather batch in k_agg_vec4 (4, 8, 16)
     {"chunk_major", "PG_CHUNK_MAJOR", 1},  // k_agg_vec4 item order for multi-chunk rows
     {"host_segs", "PG_HOST_SEGS", 3},      // host drop-in: source-row segments (H2D overlap)
@@ -114,20 +114,6 @@ __device__ __forceinline__ void acc_step(Acc& a, float w, const float4& x, const
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p1) : "l"(ww), "l"(pk2(x.z, x.w)), "l"(z.nz));
     asm("add.rn.f32x2 %0, %1, %2;" : "=l"(a.lo) : "l"(a.lo), "l"(p0));
     asm("add.rn.f32x2 %0, %1, %2;" : "=l"(a.hi) : "l"(a.hi), "l"(p1));
-}
-
-// Scalar FMUL + FADD form of acc_step (same bits). Used where latency, not
-// issue rate, bounds the kernel: with the longer scalar chain ptxas keeps a
-// whole batch of gathers in flight ahead of the math (measured: the packed
-// form let it interleave loads and lose memory-level parallelism).
-__device__ __forceinline__ void acc_step_scalar(Acc& a, float w, const float4& x) {
-    float2 l = unpk2(a.lo), h = unpk2(a.hi);
-    l.x = __fadd_rn(l.x, __fmul_rn(w, x.x));
-    l.y = __fadd_rn(l.y, __fmul_rn(w, x.y));
-    h.x = __fadd_rn(h.x, __fmul_rn(w, x.z));
-    h.y = __fadd_rn(h.y, __fmul_rn(w, x.w));
-    a.lo = pk2(l.x, l.y);
-    a.hi = pk2(h.x, h.y);
 }
 
 // zero, or the current output (accumulate semantics, aggregate.hpp:50-55)
@@ -537,71 +523,8 @@ void launch_groups(const uint64_t* gbeg, const uint64_t* gend, const uint32_t* g
     PG_LAUNCH("k_agg_groups");
 }
 
-// Wide rows (> 16 float4 columns): a full warp per (destination, 32-float4
-// chunk). Edge records are loaded 32 at a time, one per lane (coalesced), and
-// the next batch is prefetched while the current one is consumed; records
-// are broadcast with shuffles, so each group of U row gathers waits on one
-// memory round trip instead of two.
-template <int U>
-__global__ void __launch_bounds__(256) k_agg_wide(const uint64_t* __restrict__ ebeg, const uint64_t* __restrict__ eend,
-                                                 const Edge* __restrict__ edges,
-                                                 const uint32_t* __restrict__ order, uint32_t d_begin,
-                                                 uint64_t n_items, uint32_t chunks,
-                                                 const float* __restrict__ in, uint64_t ld_in,
-                                                 float* __restrict__ out, uint64_t ld_out, uint32_t dim,
-                                                 int accumulate, float2 zeros) {
-    static_assert(32 % U == 0, "U divides the 32-edge batch");
-    const uint64_t item = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
-    if (item >= n_items) return;
-    const Zs z = zs_of(zeros);
-    const unsigned lane = lane_id();
-    const uint32_t d = order[d_begin + item / chunks];
-    const uint32_t col = (static_cast<uint32_t>(item % chunks) * 32 + lane) * 4;
-    const bool active = col < dim;
-    const uint64_t eb = ebeg[d], ee = eend[d];
-    float* orow = out + d * ld_out + col;
-    Acc acc = acc_load(orow, col, dim, accumulate);
-    const float* icol = in + col;
-    Edge nxt = eb + lane < ee ? __ldg(edges + eb + lane) : make_uint2(0u, 0u);
-    for (uint64_t e0 = eb; e0 < ee; e0 += 32) {
-        const Edge cur = nxt;
-        if (e0 + 32 + lane < ee) nxt = __ldg(edges + e0 + 32 + lane);  // prefetch next batch
-        const uint32_t n = static_cast<uint32_t>(min(static_cast<uint64_t>(32), ee - e0));
-        if (n == 32) {
-#pragma unroll
-            for (int s = 0; s < 32; s += U) {
-                uint32_t src[U];
-                float w[U];
-                float4 x[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    src[u] = __shfl_sync(0xffffffffu, cur.x, s + u);
-                    w[u] = __uint_as_float(__shfl_sync(0xffffffffu, cur.y, s + u));
-                }
-                if (active) {
-#pragma unroll
-                    for (int u = 0; u < U; ++u) x[u] = ldg4(icol + src[u] * ld_in);
-#pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        if (U >= 32) acc_step_scalar(acc, w[u], x[u]);
-                        else acc_step(acc, w[u], x[u], z);
-                    }
-                }
-            }
-        } else {
-            for (uint32_t j = 0; j < n; ++j) {
-                const uint32_t src = __shfl_sync(0xffffffffu, cur.x, j);
-                const float w = __uint_as_float(__shfl_sync(0xffffffffu, cur.y, j));
-                const float4 x = active ? ldg4(icol + src * ld_in) : make_float4(0.f, 0.f, 0.f, 0.f);
-                acc_step(acc, w, x, z);
-            }
-        }
-    }
-    acc_store(orow, col, dim, acc, z);
-}
-
-// Heavy wide destinations (default): k_agg_wide's batch structure with a
-// plain float4 accumulator and scalar FMUL/FADD — in this form ptxas keeps
+// Heavy wide destinations (non-pipelined, heavy_wide_pipe = 0): 32-edge record
+// batches broadcast by shuffle, a plain float4 accumulator and scalar FMUL/FADD — in this form ptxas keeps
 // all U = 32 gathers of a batch in flight (154 registers, measured 8-way
 // shard hub rank 11.3 -> 4.1 ms on B200).
 __device__ __forceinline__ void acc4_scalar(float4& a, float w, const float4& x) {
@@ -850,88 +773,6 @@ __global__ void __launch_bounds__(64) k_agg_wide_pipe(const uint64_t* __restrict
     }
 }
 
-// Alternative heavy wide kernel (PG_HEAVY_WIDE=async): warp per (destination, 32-float4 chunk) like
-// k_agg_wide, but each lane stages its column of NB 32-edge batches in
-// shared memory with cp.async (LDGSTS, 16 B), so NB*32 row gathers (up to
-// 32 KB per warp) are in flight by construction; wait_group retires one batch
-// at a time and the lane folds it in edge order.
-constexpr int kAsyncWarps = 2;
-constexpr int kAsyncBatches = 2;  // 2 x 32 rows x 512 B = 32 KB in flight per warp
-
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                     static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
-                 "l"(src)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-template <int NB>
-__global__ void __launch_bounds__(kAsyncWarps * 32) k_agg_wide_async(
-    const uint64_t* __restrict__ ebeg, const uint64_t* __restrict__ eend, const Edge* __restrict__ edges, const uint32_t* __restrict__ order,
-    uint32_t d_begin, uint64_t n_items, uint32_t chunks, const float* __restrict__ in, uint64_t ld_in,
-    float* __restrict__ out, uint64_t ld_out, uint32_t dim, int accumulate, float2 zeros) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    const unsigned lane = lane_id(), wib = threadIdx.x >> 5;
-    float4* ring = reinterpret_cast<float4*>(smem) + static_cast<size_t>(wib) * NB * 32 * 32;  // [NB][32 e][32 l]
-    const uint64_t item = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
-    if (item >= n_items) return;
-    const Zs z = zs_of(zeros);
-    const uint32_t d = order[d_begin + item / chunks];
-    const uint32_t col = (static_cast<uint32_t>(item % chunks) * 32 + lane) * 4;
-    const bool active = col < dim;
-    const uint64_t eb = ebeg[d], ee = eend[d];
-    const uint64_t nbatch = (ee - eb + 31) / 32;
-    float* orow = out + d * ld_out + col;
-    Acc acc = acc_load(orow, col, dim, accumulate && active);
-    const float* icol = in + col;
-    auto rec_of = [&](uint64_t b) {
-        const uint64_t e = eb + b * 32 + lane;
-        return e < ee ? __ldg(edges + e) : make_uint2(0u, 0u);
-    };
-    auto issue = [&](uint64_t b, const Edge& r) {
-        float4* slot = ring + (b % NB) * 1024;
-        const uint32_t n = static_cast<uint32_t>(min(static_cast<uint64_t>(32), ee - (eb + b * 32)));
-        for (uint32_t j = 0; j < n; ++j) {
-            const uint32_t src = __shfl_sync(0xffffffffu, r.x, j);
-            if (active) cp_async16(slot + j * 32 + lane, icol + src * ld_in);
-        }
-    };
-    Edge rec[NB];  // rec[k]: edge records of batch t + k (static indices only)
-#pragma unroll
-    for (int b = 0; b < NB; ++b) rec[b] = rec_of(b);
-#pragma unroll
-    for (int b = 0; b < NB - 1; ++b) {
-        if (b < static_cast<int>(nbatch)) issue(b, rec[b]);
-        cp_async_commit();
-    }
-    for (uint64_t t = 0; t < nbatch; ++t) {
-        if (t + NB - 1 < nbatch) issue(t + NB - 1, rec[NB - 1]);
-        cp_async_commit();
-        cp_async_wait<NB - 1>();  // batch t has landed (this lane's copies) ...
-        __syncwarp();             // ... and every lane's
-        const float4* slot = ring + (t % NB) * 1024;
-        const uint32_t n = static_cast<uint32_t>(min(static_cast<uint64_t>(32), ee - (eb + t * 32)));
-        for (uint32_t j = 0; j < n; ++j) {
-            const float w = __uint_as_float(__shfl_sync(0xffffffffu, rec[0].y, j));
-            if (active) acc_step(acc, w, slot[j * 32 + lane], z);
-        }
-        __syncwarp();  // slot free for batch t + NB
-#pragma unroll
-        for (int k = 0; k + 1 < NB; ++k) rec[k] = rec[k + 1];
-        rec[NB - 1] = rec_of(t + NB);
-    }
-    if (active) acc_store(orow, col, dim, acc, z);
-}
-
-// Main-kernel choice for wide rows (tuning "wide_u", PG_WIDE_U): 0 = k_agg_vec4<32,8>
-// (default; 54 registers, 4 blocks/SM — best throughput), 8/16 =
-// k_agg_wide<U>. Heavy wide destinations always use k_agg_wide<32>.
-int wide_unroll() { return static_cast<int>(tuning(kTuneWideU)); }
 
 // Scalar fallback for unaligned rows (ld or base not 16-byte aligned).
 template <int U>
@@ -1268,13 +1109,8 @@ void launch_heavy_coop(const uint64_t* ebeg, const uint64_t* eend, const Edge* e
     PG_LAUNCH("k_agg_heavy_coop");
 }
 
-bool heavy_use_tma() {
-    static const bool v = [] {
-        const char* e = std::getenv("PG_HEAVY_KERNEL");
-        return e && std::string(e) == "tma";
-    }();
-    return v;
-}
+// TMA bulk-copy ring for heavy narrow destinations (tuning "heavy_tma")
+bool heavy_use_tma() { return tuning(kTuneHeavyTma) == 1; }
 
 template <int CHQ>
 void launch_heavy_any(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges, const uint32_t* order, uint32_t d_begin,
@@ -1387,36 +1223,16 @@ void aggregate_det(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges
             // flight per lane, 5 column-chunk warps per 602-wide destination
             const uint32_t chunks = (nq + 31) / 32;
             const uint64_t items = static_cast<uint64_t>(nh) * chunks;
-            static const bool use_async = [] {
-                const char* e = std::getenv("PG_HEAVY_WIDE");
-                return e && std::string(e) == "async";
-            }();
-            if (tuning(kTuneHeavyWidePipe) == 1 && !use_async) {
+            if (tuning(kTuneHeavyWidePipe) == 1) {
                 k_agg_wide_pipe<16><<<grid_for(items * 32, 64), 64, 0, ss.s>>>(
                     ebeg, eend, edges, order, d_begin, items, chunks, in, static_cast<uint32_t>(ld_in * 4), out,
                     ld_out, dim32, accumulate, 0u, ext);
                 PG_LAUNCH("k_agg_wide_pipe");
-            } else if (!use_async || ext.any()) {
+            } else {
                 k_agg_wide_lat<32><<<grid_for(items * 32, 256), 256, 0, ss.s>>>(
                     ebeg, eend, edges, order, d_begin, items, chunks, in, ld_in, out, ld_out, dim32, accumulate, 0u,
                     ext);
                 PG_LAUNCH("k_agg_wide_lat");
-            } else {
-                constexpr size_t smem = static_cast<size_t>(kAsyncWarps) * kAsyncBatches * 32 * 32 * 16;
-                static thread_local std::vector<char> attr_set;
-                int dev = 0;
-                PG_CUDA(cudaGetDevice(&dev));
-                if (static_cast<int>(attr_set.size()) <= dev) attr_set.resize(dev + 1, 0);
-                if (!attr_set[dev]) {
-                    PG_CUDA(cudaFuncSetAttribute(k_agg_wide_async<kAsyncBatches>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-                    attr_set[dev] = 1;
-                }
-                k_agg_wide_async<kAsyncBatches>
-                    <<<grid_for(items * 32, kAsyncWarps * 32), kAsyncWarps * 32, smem, ss.s>>>(
-                        ebeg, eend, edges, order, d_begin, items, chunks, in, ld_in, out, ld_out, dim32, accumulate,
-                        kZeros);
-                PG_LAUNCH("k_agg_wide_async");
             }
         } else if (tuning(kTuneHeavyNarrow) == 1 && !heavy_use_tma()) {
             // narrow rows: scalar column per lane, 32-edge batches in flight
@@ -1457,33 +1273,20 @@ void aggregate_det(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges
         return;
     }
     if (nq > 16) {
-        const int U = ext.any() ? 0 : wide_unroll();
         const uint32_t chunks = (nq + 31) / 32;
-        const uint64_t items = static_cast<uint64_t>(nd) * chunks;
-        if (U == 0) {  // the main kernel
-            const int64_t vu = tuning(kTuneVecU);
-            if (tuning(kTuneWideLpd) == 16)  // 64-float chunks: half the per-pass source working set
-                launch_vec4<16, 8>(ebeg, eend, edges, order, d_begin, nd, (nq + 15) / 16, in, ld_in, out, ld_out,
-                                   dim32, accumulate, s, ext);
-            else if (vu == 4)
-                launch_vec4<32, 4>(ebeg, eend, edges, order, d_begin, nd, chunks, in, ld_in, out, ld_out, dim32,
-                                   accumulate, s, ext);
-            else if (vu == 16)
-                launch_vec4<32, 16>(ebeg, eend, edges, order, d_begin, nd, chunks, in, ld_in, out, ld_out, dim32,
-                                    accumulate, s, ext);
-            else
-                launch_vec4<32, 8>(ebeg, eend, edges, order, d_begin, nd, chunks, in, ld_in, out, ld_out, dim32,
-                                   accumulate, s, ext);
-        } else if (U == 8) {
-            k_agg_wide<8><<<grid_for(items * 32, 256), 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks,
-                                                                   in, ld_in, out, ld_out, dim32, accumulate, kZeros);
-            PG_LAUNCH("k_agg_wide");
-        } else {
-            k_agg_wide<16><<<grid_for(items * 32, 256), 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks,
-                                                                    in, ld_in, out, ld_out, dim32, accumulate,
-                                                                    kZeros);
-            PG_LAUNCH("k_agg_wide");
-        }
+        const int64_t vu = tuning(kTuneVecU);
+        if (tuning(kTuneWideLpd) == 16)  // 64-float chunks: half the per-pass source working set
+            launch_vec4<16, 8>(ebeg, eend, edges, order, d_begin, nd, (nq + 15) / 16, in, ld_in, out, ld_out, dim32,
+                               accumulate, s, ext);
+        else if (vu == 4)
+            launch_vec4<32, 4>(ebeg, eend, edges, order, d_begin, nd, chunks, in, ld_in, out, ld_out, dim32, accumulate,
+                               s, ext);
+        else if (vu == 16)
+            launch_vec4<32, 16>(ebeg, eend, edges, order, d_begin, nd, chunks, in, ld_in, out, ld_out, dim32,
+                                accumulate, s, ext);
+        else
+            launch_vec4<32, 8>(ebeg, eend, edges, order, d_begin, nd, chunks, in, ld_in, out, ld_out, dim32, accumulate,
+                               s, ext);
     } else if (nq > 8) {
         launch_vec4<16, 8>(ebeg, eend, edges, order, d_begin, nd, 1, in, ld_in, out, ld_out, dim32, accumulate, s, ext);
     } else if (nq > 4) {

@@ -236,7 +236,7 @@ uint64_t heavy_min_degree(uint64_t dim, uint64_t range_edges);
 void set_heavy_min_degree(uint64_t v);
 // scheduling knobs of the SpMM kernels (pg_set_tuning): never change results
 enum TuneKeyId {
-    kTuneWideU = 0,
+    kTuneHeavyTma = 0,
     kTuneVecU = 1,
     kTuneChunkMajor = 2,
     kTuneHostSegs = 3,

@@ -645,8 +645,9 @@ def set_heavy_min_degree(min_degree=None):
 
 
 def set_tuning(key, value=None):
-    """Scheduling knob of the SpMM kernels by name ("vec_u", "chunk_major",
-    "wide_u"; None restores the default). Never changes results."""
+    """Scheduling knob of the SpMM kernels by name (see pg_set_tuning in
+    include/pathgcn_b200.h; None restores the default). Never changes
+    results except "grouped_seg" (a Fast-mode association order)."""
     _check(_lib_().pg_set_tuning(key.encode(), -1 if value is None else int(value)))
 
 

@@ -70,7 +70,7 @@ def test_candidates_match_oracle(orc):
 
 def test_tuning_keys(pg):
     """pg_set_tuning: scheduling knobs by name; unknown keys are config errors."""
-    for key in ("vec_u", "chunk_major", "wide_u", "host_segs", "host_chunks", "host_trace", "heavy_narrow",
+    for key in ("vec_u", "chunk_major", "heavy_tma", "host_segs", "host_chunks", "host_trace", "heavy_narrow",
                 "wide_lpd", "src_segs", "ld_cg", "host_chunk_order", "grouped_seg"):
         pg.set_tuning(key, None)
     import pytest

@@ -98,10 +98,10 @@ def test_backward_aggregation_bit_exact(pg, orc, dim):
         tol_check(got, orc, op, y_used)
 
 
-@pytest.mark.parametrize("narrow", [0, 1])
+@pytest.mark.parametrize("kern", ["coop", "narrow", "tma", "wide_lat"])
 @pytest.mark.parametrize("heavy_min", [1, 0, 64])
 @pytest.mark.parametrize("dim", [1, 16, 41, 130, 602])
-def test_heavy_ring_kernel_bit_exact(pg, orc, dim, heavy_min, narrow):
+def test_heavy_ring_kernel_bit_exact(pg, orc, dim, heavy_min, kern):
     """Force every (heavy_min=1), none (0) or some (64) destinations onto the
     TMA bulk-copy ring kernel; results must not change by a bit, including
     accumulate semantics."""
@@ -112,7 +112,12 @@ def test_heavy_ring_kernel_bit_exact(pg, orc, dim, heavy_min, narrow):
     rng = np.random.default_rng(dim + heavy_min)
     try:
         pg.set_heavy_min_degree(heavy_min)
-        pg.set_tuning("heavy_narrow", narrow)
+        # narrow rows: cooperative tiles (default), scalar-lane latency kernel,
+        # or the TMA cp.async.bulk + mbarrier ring; wide rows: pipelined
+        # (default) or plain latency kernel
+        pg.set_tuning("heavy_narrow", 1 if kern == "narrow" else 0)
+        pg.set_tuning("heavy_tma", 1 if kern == "tma" else 0)
+        pg.set_tuning("heavy_wide_pipe", 0 if kern == "wide_lat" else 1)
         for dp, op in zip(dps, ops):
             y = rng.uniform(-1, 1, size=(dp.P, dim)).astype(np.float32)
             base = rng.uniform(-1, 1, size=(dp.D, dim)).astype(np.float32)
@@ -130,7 +135,8 @@ def test_heavy_ring_kernel_bit_exact(pg, orc, dim, heavy_min, narrow):
             assert np.array_equal(bits(x2.cpu().numpy()), bits(want[b[1]:b[2]]))
     finally:
         pg.set_heavy_min_degree(None)
-        pg.set_tuning("heavy_narrow")
+        for k in ("heavy_narrow", "heavy_tma", "heavy_wide_pipe"):
+            pg.set_tuning(k)
 
 
 def test_aggregate_pull_local_and_accumulate(pg, orc):
