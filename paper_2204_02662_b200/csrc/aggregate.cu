@@ -1003,18 +1003,30 @@ __global__ void __launch_bounds__(256) k_agg_heavy_coop(const uint64_t* __restri
 
     float4 r[PER];
     float rw[PER];
-    auto gather = [&](uint64_t t) {
+    // records of tile t+1 are loaded while tile t-1 folds and its rows are
+    // issued while tile t folds: no record -> row round trip on the
+    // critical path (ptxas otherwise serialises each record/row pair)
+    Edge ed[PER];
+    auto recs = [&](uint64_t t) {
         const uint64_t e0 = eb + t * T;
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
             const unsigned idx = tid + 256u * k;
             const unsigned j = idx / CHQ, q = idx % CHQ;
             const bool ok = e0 + j < ee && q < nqc;
-            Edge ed = make_uint2(0u, 0u);
-            if (ok) ed = __ldg(edges + e0 + j);
-            const bool take = ok && (!FILT || ext_src_on(ext, ed.x));  // skipped: +-0 term
-            r[k] = take ? ldg4(in + ed.x * ld_in + (q0 + q) * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
-            rw[k] = __uint_as_float(ed.y);
+            ed[k] = ok ? __ldg(edges + e0 + j) : make_uint2(0xffffffffu, 0u);
+        }
+    };
+    auto rows = [&]() {
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const unsigned idx = tid + 256u * k;
+            const unsigned q = idx % CHQ;
+            const bool ok = ed[k].x != 0xffffffffu;
+            const bool take = ok && (!FILT || ext_src_on(ext, ed[k].x));  // skipped: +-0 term
+            r[k] = take ? ldg4(in + static_cast<uint64_t>(ed[k].x) * ld_in + (q0 + q) * 4)
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+            rw[k] = __uint_as_float(ed[k].y);
         }
     };
     auto stash = [&](int b) {
@@ -1038,13 +1050,18 @@ __global__ void __launch_bounds__(256) k_agg_heavy_coop(const uint64_t* __restri
         float* srow = out + row * ld_out + scol;
         float sacc = (sowner && accumulate) ? *srow : 0.f;
         if (ntiles) {
-            gather(0);
+            recs(0);
+            rows();
             stash(0);
+            if (ntiles > 1) recs(1);
         }
         __syncthreads();
         for (uint64_t t = 0; t < ntiles; ++t) {
             const int b = static_cast<int>(t & 1);
-            if (t + 1 < ntiles) gather(t + 1);  // loads in flight during the fold
+            if (t + 1 < ntiles) {  // tile t+1's rows and tile t+2's records in flight during the fold
+                rows();
+                if (t + 2 < ntiles) recs(t + 2);
+            }
             if (sowner) {
                 const uint32_t n = static_cast<uint32_t>(min(static_cast<uint64_t>(T), ee - (eb + t * T)));
                 const float* sb = reinterpret_cast<const float*>(tile + b * T * CHQ) + lane;
@@ -1069,13 +1086,18 @@ __global__ void __launch_bounds__(256) k_agg_heavy_coop(const uint64_t* __restri
         float* orow = out + row * ld_out + col;
         Acc acc = acc_load(orow, col, dim, owner && accumulate);
         if (ntiles) {
-            gather(0);
+            recs(0);
+            rows();
             stash(0);
+            if (ntiles > 1) recs(1);
         }
         __syncthreads();
         for (uint64_t t = 0; t < ntiles; ++t) {
             const int b = static_cast<int>(t & 1);
-            if (t + 1 < ntiles) gather(t + 1);  // loads in flight during the fold
+            if (t + 1 < ntiles) {  // tile t+1's rows and tile t+2's records in flight during the fold
+                rows();
+                if (t + 2 < ntiles) recs(t + 2);
+            }
             if (owner) {
                 const uint32_t n = static_cast<uint32_t>(min(static_cast<uint64_t>(T), ee - (eb + t * T)));
                 const float4* sb = tile + b * T * CHQ + lane;
