@@ -264,10 +264,34 @@ __global__ void __launch_bounds__(256, (U <= 8 ? 4 : 2)) k_agg_vec4(const uint64
     const uint32_t row = ext_out_row(ext, d);
     float* orow = out + row * ld_out + col;
     Acc acc = acc_load(orow, col, dim, accumulate);
+    // Narrow rows (LPD <= 8 lanes per destination): the U records of a batch
+    // are loaded spread over the sub-warp's lanes (one 32-byte segment per
+    // sub-warp and instruction instead of U single-record loads, each a
+    // separate L1 wavefront per sub-warp) and handed out by sub-warp shuffles.
+    constexpr int NPL = (U + LPD - 1) / LPD;
+    const unsigned sl = static_cast<unsigned>(t % LPD);
+    const unsigned submask = LPD >= 32 ? 0xffffffffu : (((1u << LPD) - 1u) << (lane_id() & ~(LPD - 1u)));
+    auto batch_recs = [&](Edge (&ed)[U], uint32_t n) {
+        if constexpr (LPD <= 8) {
+            Edge mine[NPL];
+#pragma unroll
+            for (int i = 0; i < NPL; ++i) {
+                const unsigned k = sl + i * LPD;
+                mine[i] = ld_rec(edges + e + (k < n ? k : n - 1));
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                ed[u].x = __shfl_sync(submask, mine[u / LPD].x, u % LPD, LPD);
+                ed[u].y = __shfl_sync(submask, mine[u / LPD].y, u % LPD, LPD);
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < U; ++u) ed[u] = ld_rec(edges + e + (u < static_cast<int>(n) ? u : n - 1));
+        }
+    };
     for (; e + U <= end; e += U) {
         Edge ed[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) ed[u] = ld_rec(edges + e + u);
+        batch_recs(ed, U);
         float4 x[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -281,8 +305,7 @@ __global__ void __launch_bounds__(256, (U <= 8 ? 4 : 2)) k_agg_vec4(const uint64
     if (e < end) {  // remainder (< U edges) as one batch: all gathers in flight
         const uint32_t n = static_cast<uint32_t>(end - e);
         Edge ed[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) ed[u] = ld_rec(edges + e + (u < static_cast<int>(n) ? u : n - 1));
+        batch_recs(ed, n);
         float4 x[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
