@@ -14,6 +14,7 @@
 // sums and break bit parity with the reference).
 #include <algorithm>
 #include <cmath>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/pathgcn_b200.h"
@@ -78,12 +79,24 @@ __global__ void __launch_bounds__(256) k_gemm(const float* __restrict__ a, uint6
 // out[i][j] = sum over k < n, ascending, of A(k, i) * B(k, j), A(k, i) =
 // a[(rows ? rows[k] : k) * lda + i] (the engine's gather_rows fused in).
 // The order forces one serial chain per output over all n rows, so the
-// only parallelism is the r x c outputs and the floor is n dependent FADDs.
-// A 128-thread block owns TI columns of A x TC columns of B, one chain per
-// thread; rows stream through a kAtbStages-deep cp.async pipeline of
-// KC-row tiles, so a chain step is two shared loads (immediate
-// offsets: TI/TC are compile-time) + FMUL + FADD.
-constexpr int kAtbStages = 4;
+// only parallelism is the r x c outputs and the floor is n dependent FADDs
+// (4 cycles each). A 32-thread block owns TI x TC chains, two adjacent
+// columns per lane: one row is LDS (a, broadcast) + LDS.64 (b pair) + FFMA2
+// (products, runtime -0 addend: fl(a*b) exactly, no contraction) + FADD2
+// (both chain steps) plus the copy issue. No block barrier: the warp owns
+// its kAtbStages-deep cp.async ring (__syncwarp orders it); lane kk copies
+// row kk of each stage (its gathered A slice, its B slice, fixed column
+// offsets as immediates), and the row ids of stage ts ride in the copy
+// group of stage ts - (S-1), so no copy waits on an id load. Rows past n
+// are zero filled: their +0 products only flip a -0 accumulator to +0,
+// which the final fl(acc + 0) does anyway.
+// Measured (Reddit shape): ~19 cycles per row per warp, i.e. 1.46 ms for
+// the top layer and 2.26 ms for layer 0, against 3.2 / 2.5 ms for the
+// earlier 128-thread block-owned kernel. Variants that split the roles
+// (copy warp + chain warp, producer warps + chain warp over named
+// barriers), re-laid the stages for LDS.128 operands, or went scalar with
+// one chain per lane all measured equal or slower; see DESIGN.md.
+constexpr int kAtbStages = 8;
 
 template <int BYTES>
 __device__ __forceinline__ void cp_async(void* dst, const void* src, bool ok) {
@@ -99,105 +112,130 @@ __device__ __forceinline__ void cp_async(void* dst, const void* src, bool ok) {
                      : "memory");
 }
 
-template <int TI, int TC>
-__host__ __device__ constexpr int atb_kc() {  // rows per tile: the stage ring stays under 48 KB of static smem
-    return TC <= 32 ? 64 : (TC <= 64 ? 32 : 16);
+// cp.async with the ignore-src predicate: skip == true zero-fills the
+// destination without reading src (src must still be a valid address)
+template <int CP>
+__device__ __forceinline__ void cp_async_skip(void* dst, const void* src, bool skip) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+    if (CP == 16)
+        asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n cp.async.cg.shared.global [%0], [%1], 16, p;\n}" ::"r"(d),
+                     "l"(src), "r"(static_cast<int>(skip))
+                     : "memory");
+    else
+        asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n cp.async.ca.shared.global [%0], [%1], 4, p;\n}" ::"r"(d),
+                     "l"(src), "r"(static_cast<int>(skip))
+                     : "memory");
 }
 
-// V = floats per cp.async (4: 16-byte copies, needs 16-byte aligned rows and
-// column tiles; 1: any layout). The gathered A row ids of each thread's
-// copies (engine.hpp:323 gather_rows fused) are read one tile ahead of the
-// copies, so no copy issue waits on a rows[] load (that wait was ~30% of the
-// kernel when the id load sat in front of every tile's copies).
-template <int TI, int TC, int V>
-__global__ void __launch_bounds__(TI* TC) k_gemm_at_b(const float* __restrict__ a, uint64_t lda,
-                                                      const uint32_t* __restrict__ rows, const float* __restrict__ b,
-                                                      uint64_t ldb, float* __restrict__ out, uint64_t ldo, uint64_t n,
-                                                      uint64_t r, uint64_t c) {
-    constexpr int KC = atb_kc<TI, TC>();
-    constexpr int NT = TI * TC;
-    constexpr int TILE = KC * (TI + TC);
-    constexpr int AV = TI % V == 0 ? V : 1;  // A tile rows of TI floats
-    constexpr int AE = KC * TI / AV;           // A copies per tile
-    constexpr int EPT = (AE + NT - 1) / NT;    // ... per thread
-    __shared__ __align__(16) float sm[kAtbStages * TILE];
-    const unsigned tid = threadIdx.x;
-    const uint64_t i0 = blockIdx.x * static_cast<uint64_t>(TI), j0 = blockIdx.y * static_cast<uint64_t>(TC);
-    const unsigned ti = tid / TC, tj = tid % TC;
-    const uint64_t ntiles = (n + KC - 1) / KC;
-    struct Rows {
-        uint64_t r[EPT];
+template <int TI, int V>
+__global__ void __launch_bounds__(32) k_gemm_at_b_w(const float* __restrict__ a, uint64_t lda,
+                                                   const uint32_t* __restrict__ rows, const float* __restrict__ b,
+                                                   uint64_t ldb, float* __restrict__ out, uint64_t ldo, uint32_t n,
+                                                   uint32_t r, uint32_t c, float nz) {
+    constexpr int LPI = 32 / TI;  // lanes per A column
+    constexpr int TC = 2 * LPI;   // B columns per warp
+    constexpr int KC = 32;        // rows per stage: lane kk copies row kk's A slice and id
+    constexpr int S = kAtbStages;
+    constexpr int AV = (V == 4 && TI % 4 == 0) ? 4 : 1;
+    constexpr int BV = V == 4 ? 4 : 1;
+    constexpr int NA = TI / AV, NB = TC / BV;  // copies per lane per stage
+    __shared__ __align__(16) float sa[S][KC][TI];
+    __shared__ __align__(16) float sb[S][KC][TC];
+    // row ids ride the copy pipeline: stage ts's ids are copied in the group
+    // of stage ts - (S-1), so the wait that makes stage t readable also
+    // lands the ids the next issue needs
+    __shared__ uint32_t sid[S][KC];
+    const unsigned lane = threadIdx.x;
+    const uint32_t i0 = blockIdx.x * TI, j0 = blockIdx.y * TC;
+    const unsigned ti = lane / LPI, tj = (lane % LPI) * 2;
+    const uint32_t ntiles = (n + KC - 1) / KC;
+    // lane kk copies row kk of every stage: its A slice (gathered row id)
+    // and its TC-float B slice, fixed column offsets as immediates; columns
+    // past r / c are skipped: ignore-src zero-fills without reading, so the
+    // address of a skipped column is never dereferenced
+    bool a_skip[NA], b_skip[NB];
+#pragma unroll
+    for (int q = 0; q < NA; ++q) a_skip[q] = i0 + q * AV >= r;
+#pragma unroll
+    for (int q = 0; q < NB; ++q) b_skip[q] = j0 + q * BV >= c;
+    const float* a_col = a + i0;
+    const float* b_row = b + static_cast<uint64_t>(lane) * ldb + j0;  // row lane of stage 0
+    const uint64_t b_stage = static_cast<uint64_t>(KC) * ldb;
+    auto copies = [&](uint32_t ts, uint32_t id, auto tail_t) {
+        constexpr bool tail = decltype(tail_t)::value;
+        const int slot = ts % S;
+        const bool out_row = tail && ts * KC + lane >= n;
+        const float* ar = out_row ? a : a_col + static_cast<uint64_t>(id) * lda;
+#pragma unroll
+        for (int q = 0; q < NA; ++q)
+            cp_async_skip<AV * 4>(&sa[slot][lane][q * AV], ar + q * AV, a_skip[q] || out_row);
+        const float* br = out_row ? b : b_row + ts * b_stage;
+#pragma unroll
+        for (int q = 0; q < NB; ++q)
+            cp_async_skip<BV * 4>(&sb[slot][lane][q * BV], br + q * BV, b_skip[q] || out_row);
     };
-    auto row_of = [&](uint64_t t) {  // A rows of this thread's elements of tile t
-        Rows out;
-#pragma unroll
-        for (int q = 0; q < EPT; ++q) {
-            const int e = tid + q * NT;
-            const uint64_t k = t * KC + e / (TI / AV);
-            out.r[q] = (e < AE && k < n) ? (rows ? __ldg(rows + k) : k) : 0;
+    auto issue = [&](uint32_t ts, uint32_t id) {
+        if (ts < ntiles) {
+            if (ts * KC + KC <= n)
+                copies(ts, id, std::false_type{});
+            else
+                copies(ts, id, std::true_type{});
         }
-        return out;
-    };
-    auto load = [&](uint64_t t, const Rows& ar) {
-        float* st = sm + (t % kAtbStages) * TILE;
-        const uint64_t k0 = t * KC;
-#pragma unroll
-        for (int q = 0; q < EPT; ++q) {
-            const int e = tid + q * NT;
-            if (e < AE) {
-                const int kk = e / (TI / AV), ii = (e % (TI / AV)) * AV;
-                const bool ok = k0 + kk < n && i0 + ii < r;
-                cp_async<AV * 4>(st + kk * TI + ii, ok ? a + ar.r[q] * lda + i0 + ii : a, ok);
-            }
+        if (rows) {
+            const uint32_t ka = (ts + S - 1) * KC + lane;
+            const bool out_row = ka >= n;
+            cp_async_skip<4>(&sid[(ts + S - 1) % S][lane], out_row ? rows : rows + ka, out_row);
         }
-        float* sb = st + KC * TI;
-#pragma unroll
-        for (int e = tid; e < KC * TC / V; e += NT) {
-            const int kk = e / (TC / V), jj = (e % (TC / V)) * V;
-            const bool ok = k0 + kk < n && j0 + jj < c;
-            cp_async<V * 4>(sb + kk * TC + jj, ok ? b + (k0 + kk) * ldb + j0 + jj : b, ok);
-        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
     };
 #pragma unroll 1
-    for (int t = 0; t < kAtbStages - 1; ++t) {
-        if (static_cast<uint64_t>(t) < ntiles) load(t, row_of(t));
-        asm volatile("cp.async.commit_group;" ::: "memory");
+    for (int s = 0; s < S - 1; ++s) {
+        const uint32_t k = s * KC + lane;
+        issue(s, k < n ? (rows ? __ldg(rows + k) : k) : 0u);
     }
-    Rows next_row = row_of(kAtbStages - 1);
-    float acc = 0.f;
-    for (uint64_t t = 0; t < ntiles; ++t) {
-        asm volatile("cp.async.wait_group %0;" ::"n"(kAtbStages - 2) : "memory");
-        __syncthreads();  // tile t resident for every thread; tile t-1's slot is free
-        if (t + kAtbStages - 1 < ntiles) load(t + kAtbStages - 1, next_row);
-        asm volatile("cp.async.commit_group;" ::: "memory");
-        next_row = row_of(t + kAtbStages);  // consumed next iteration: its latency hides behind this tile
-        const float* sa = sm + (t % kAtbStages) * TILE + ti;
-        const float* sb = sm + (t % kAtbStages) * TILE + KC * TI + tj;
-        const uint64_t rem = n - t * KC;
-        if (rem >= static_cast<uint64_t>(KC)) {
+    unsigned long long nz2, acc;
+    asm("mov.b64 %0, {%1,%1};" : "=l"(nz2) : "f"(nz));
+    asm("mov.b64 %0, {%1,%1};" : "=l"(acc) : "f"(0.f));
+    for (uint32_t t = 0; t < ntiles; ++t) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(S - 2) : "memory");
+        __syncwarp();  // stage t visible to every lane; stage t-1's slot is free
+        {
+            const uint32_t ts = t + S - 1;
+            issue(ts, rows ? sid[ts % S][lane] : ts * KC + lane);
+        }
+        const int slot = t % S;
+        const float* pa = &sa[slot][0][ti];
+        const unsigned long long* pb = reinterpret_cast<const unsigned long long*>(&sb[slot][0][tj]);
 #pragma unroll
-            for (int kk = 0; kk < KC; ++kk) acc = __fadd_rn(acc, __fmul_rn(sa[kk * TI], sb[kk * TC]));
-        } else {
-            for (int kk = 0; kk < static_cast<int>(rem); ++kk)
-                acc = __fadd_rn(acc, __fmul_rn(sa[kk * TI], sb[kk * TC]));
+        for (int kk = 0; kk < KC; ++kk) {
+            unsigned long long aa, p;
+            asm("mov.b64 %0, {%1,%1};" : "=l"(aa) : "f"(pa[kk * TI]));
+            asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p) : "l"(aa), "l"(pb[kk * (TC / 2)]), "l"(nz2));
+            asm("add.rn.f32x2 %0, %1, %2;" : "=l"(acc) : "l"(acc), "l"(p));
         }
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
+    float lo, hi;
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(lo), "=f"(hi) : "l"(acc));
     const uint64_t i = i0 + ti, j = j0 + tj;
-    if (i < r && j < c) out[i * ldo + j] = __fadd_rn(acc, 0.f);
+    if (i < r && j < c) out[i * ldo + j] = __fadd_rn(lo, 0.f);
+    if (i < r && j + 1 < c) out[i * ldo + j + 1] = __fadd_rn(hi, 0.f);
 }
 
-template <int TI, int TC>
+template <int TI>
 void launch_at_b(DMat a, const uint32_t* rows, DMat b, DMat out, uint64_t n, uint64_t r, uint64_t c,
                  cudaStream_t s) {
+    constexpr unsigned TC = 64 / TI;
     dim3 grid(static_cast<unsigned>((r + TI - 1) / TI), static_cast<unsigned>((c + TC - 1) / TC));
     const bool v4 = a.ld % 4 == 0 && b.ld % 4 == 0 && reinterpret_cast<uintptr_t>(a.p) % 16 == 0 &&
                     reinterpret_cast<uintptr_t>(b.p) % 16 == 0;
+    volatile float nz = -0.f;  // runtime -0: a literal lets ptxas fold the FFMA2 away
+    const uint32_t n32 = static_cast<uint32_t>(n), r32 = static_cast<uint32_t>(r), c32 = static_cast<uint32_t>(c);
     if (v4)
-        k_gemm_at_b<TI, TC, 4><<<grid, TI * TC, 0, s>>>(a.p, a.ld, rows, b.p, b.ld, out.p, out.ld, n, r, c);
+        k_gemm_at_b_w<TI, 4><<<grid, 32, 0, s>>>(a.p, a.ld, rows, b.p, b.ld, out.p, out.ld, n32, r32, c32, nz);
     else
-        k_gemm_at_b<TI, TC, 1><<<grid, TI * TC, 0, s>>>(a.p, a.ld, rows, b.p, b.ld, out.p, out.ld, n, r, c);
-    PG_LAUNCH("k_gemm_at_b");
+        k_gemm_at_b_w<TI, 1><<<grid, 32, 0, s>>>(a.p, a.ld, rows, b.p, b.ld, out.p, out.ld, n32, r32, c32, nz);
+    PG_LAUNCH("k_gemm_at_b_w");
 }
 
 // ---- elementwise / row kernels ---------------------------------------------
@@ -344,16 +382,20 @@ void gemm(DMat a, DMat b, DMat out, bool b_transposed, cudaStream_t s) {
     PG_LAUNCH("k_gemm");
 }
 
+uint64_t gemm_at_b_blocks(uint64_t r, uint64_t c) {
+    const uint64_t ti = c <= 8 ? 8 : 4, tc = 64 / ti;
+    return ((r + ti - 1) / ti) * ((c + tc - 1) / tc);
+}
+
 void gemm_at_b(DMat a, const uint32_t* a_rows, DMat b, DMat out, cudaStream_t s) {
     const uint64_t n = b.rows, r = a.cols, c = b.cols;
     if (!a_rows && a.rows != n) fail(kConfig, "gemm_at_b: row counts differ");
     if (out.rows != r || out.cols != c) fail(kConfig, "gemm_at_b: output shape mismatch");
     if (r == 0 || c == 0) return;
-    // 128 chains per block: the column tile of B fitted to c
-    if (c <= 16) launch_at_b<8, 16>(a, a_rows, b, out, n, r, c, s);
-    else if (c <= 32) launch_at_b<4, 32>(a, a_rows, b, out, n, r, c, s);
-    else if (c <= 64) launch_at_b<2, 64>(a, a_rows, b, out, n, r, c, s);
-    else launch_at_b<1, 128>(a, a_rows, b, out, n, r, c, s);
+    if (n >= (1ull << 31) || r >= (1ull << 31) || c >= (1ull << 31)) fail(kConfig, "gemm_at_b: dimension too large");
+    // 64 chains per warp: 4 (or 8) A columns x 16 (or 8) B columns (gemm_at_b_blocks)
+    if (c <= 8) launch_at_b<8>(a, a_rows, b, out, n, r, c, s);
+    else launch_at_b<4>(a, a_rows, b, out, n, r, c, s);
 }
 
 void relu(DMat x, DMat out, cudaStream_t s) {
@@ -438,6 +480,69 @@ void check_chain(const BackwardIO& io, uint64_t n) {
         fail(kConfig, "backward: top gradient shape mismatch");
 }
 
+// W' = Y^T g on a forked stream. The W gradients are chain outputs that
+// nothing later in the chain reads, so each one overlaps the y_grad GEMM and
+// the SpMM of its layer (the serial-order GEMM is latency-bound on a few
+// dozen to ~150 warps; the SpMM it hides behind is bandwidth-bound). Every
+// g it reads is kept alive until join(), which makes the caller's stream
+// wait for the last W' (stream-ordered frees then follow the join).
+constexpr uint64_t kWGradSideMaxBlocks = 160;  // Reddit layer 0: 151 blocks, forked
+
+struct WGradSide {
+    cudaStream_t main;
+    cudaStream_t side;
+    cudaEvent_t fork, done;
+    std::vector<std::unique_ptr<Tmp>> keep;
+    bool used = false;
+    explicit WGradSide(cudaStream_t s) : main(s) {
+        struct PerDev {
+            cudaStream_t s = nullptr;
+            cudaEvent_t fork = nullptr, done = nullptr;
+        };
+        static thread_local std::vector<PerDev> per_dev;
+        int dev = 0;
+        PG_CUDA(cudaGetDevice(&dev));
+        if (static_cast<int>(per_dev.size()) <= dev) per_dev.resize(dev + 1);
+        PerDev& d = per_dev[dev];
+        if (!d.s) {
+            PG_CUDA(cudaStreamCreateWithFlags(&d.s, cudaStreamNonBlocking));
+            PG_CUDA(cudaEventCreateWithFlags(&d.fork, cudaEventDisableTiming));
+            PG_CUDA(cudaEventCreateWithFlags(&d.done, cudaEventDisableTiming));
+        }
+        side = d.s;
+        fork = d.fork;
+        done = d.done;
+    }
+    void gemm_at_b(DMat a, const uint32_t* rows, DMat b, DMat out) {
+        if (gemm_at_b_blocks(a.cols, b.cols) > kWGradSideMaxBlocks) {
+            // a GEMM of more than ~1 block (one warp) per SM shares SMSPs
+            // with the SpMM and both slow down (ogbn-products: 192 and 400
+            // blocks, chain 30 -> 32.5 / 51 ms when forked): run it in order
+            pg::gemm_at_b(a, rows, b, out, main);
+            return;
+        }
+        PG_CUDA(cudaEventRecord(fork, main));
+        PG_CUDA(cudaStreamWaitEvent(side, fork, 0));
+        pg::gemm_at_b(a, rows, b, out, side);
+        used = true;
+    }
+    void retire(std::unique_ptr<Tmp>& g) {
+        if (g) keep.push_back(std::move(g));
+    }
+    void join() {
+        if (!used) return;
+        PG_CUDA(cudaEventRecord(done, side));
+        PG_CUDA(cudaStreamWaitEvent(main, done, 0));
+        used = false;
+    }
+    ~WGradSide() {
+        if (used) {  // unwinding after a failure: still order the frees after the side work
+            cudaEventRecord(done, side);
+            cudaStreamWaitEvent(main, done, 0);
+        }
+    }
+};
+
 // The full-graph backward shared by Alg. 1 (all-active) and the if-else
 // filter: per layer W' = Y^T g, y_grad = g W^T, x_grad = pull(y_grad), and
 // g = relu_backward(x_grad, pre[l-1]) fused into the SpMM epilogue.
@@ -447,11 +552,12 @@ void backward_full(Groups& G, Frontiers* F, const BackwardIO& io, cudaStream_t s
     const uint64_t n = gr.n, L = io.L;
     check_chain(io, n);
     if (F && F->L != L) fail(kConfig, "ifelse backward: frontiers were computed for a different depth");
+    WGradSide wgs(s);
     std::unique_ptr<Tmp> gcur;
     DMat g = io.top_grad;
     for (uint64_t l = L; l-- > 0;) {
         const uint64_t in_dim = io.w[l].rows;
-        gemm_at_b(io.y[l], nullptr, g, io.w_grads[l], s);
+        wgs.gemm_at_b(io.y[l], nullptr, g, io.w_grads[l]);
         Tmp yg(n, in_dim, s);
         gemm(g, io.w[l], yg.m, true, s);
         AggExt ext;
@@ -493,10 +599,12 @@ void backward_full(Groups& G, Frontiers* F, const BackwardIO& io, cudaStream_t s
             }
         }
         if (l > 0) {
+            wgs.retire(gcur);
             gcur = std::move(gnext);
             g = gcur->m;
         }
     }
+    wgs.join();
 }
 
 }  // namespace
@@ -538,6 +646,7 @@ void backward_epp(Groups* const* PG, Frontiers& F, const BackwardIO& io, int gat
     check_chain(io, n);
     if (gather_mode == 1) {  // Global: full-width matrices, the path walked with global ids
         if (io.x_grads) fail(kConfig, "epp backward: x_grads are only captured in Local gather mode");
+        WGradSide wgs(s);
         std::unique_ptr<Tmp> gcur;
         DMat g = io.top_grad;
         for (uint64_t i = 0; i < L; ++i) {
@@ -547,7 +656,7 @@ void backward_epp(Groups* const* PG, Frontiers& F, const BackwardIO& io, int gat
                 p.edges_global = DevBuf<Edge>(p.E, s);
                 remap_edges(p.edges_parent.get(), p.E, F.levels[i].ids.get(), p.edges_global.get(), s);
             }
-            gemm_at_b(io.y[l], nullptr, g, io.w_grads[l], s);
+            wgs.gemm_at_b(io.y[l], nullptr, g, io.w_grads[l]);
             Tmp yg(n, in_dim, s);
             gemm(g, io.w[l], yg.m, true, s);
             auto gn = std::make_unique<Tmp>(n, in_dim, s, true);  // rows off the path stay +0
@@ -560,15 +669,18 @@ void backward_epp(Groups* const* PG, Frontiers& F, const BackwardIO& io, int gat
             run_aggregate(*PG[i], true, 0, p.D, yg.m.p, yg.m.ld, gn->m.p, gn->m.ld, in_dim, PG_AGG_OVERWRITE, s,
                           SegSel{}, ext, p.edges_global.get());
             if (io.edges) io.edges[i] = p.E;
+            wgs.retire(gcur);
             gcur = std::move(gn);
             g = gcur->m;
         }
+        wgs.join();
         return;
     }
     // Local: compact matrices whose rows follow the frontier arrays
     const uint64_t c = io.top_grad.cols;
     auto g0 = std::make_unique<Tmp>(F.levels[0].size, c, s);
     gather_rows(io.top_grad.p, io.top_grad.ld, F.levels[0].ids.get(), F.levels[0].size, g0->m.p, g0->m.ld, c, s);
+    WGradSide wgs(s);
     std::unique_ptr<Tmp> gcur = std::move(g0);
     for (uint64_t i = 0; i < L; ++i) {
         const uint64_t l = L - 1 - i, in_dim = io.w[l].rows;
@@ -576,7 +688,7 @@ void backward_epp(Groups* const* PG, Frontiers& F, const BackwardIO& io, int gat
         if (p.P != F.levels[i].size || p.D != F.levels[i + 1].size)
             fail(kConfig, "epp backward: path does not follow the frontiers");
         const DMat g = gcur->m;
-        gemm_at_b(io.y[l], F.levels[i].ids.get(), g, io.w_grads[l], s);  // gather_rows(Y, in_rows) fused
+        wgs.gemm_at_b(io.y[l], F.levels[i].ids.get(), g, io.w_grads[l]);  // gather_rows(Y, in_rows) fused
         Tmp yg(p.P, in_dim, s);
         gemm(g, io.w[l], yg.m, true, s);
         DMat* xo = io.x_grads ? &io.x_grads[i] : nullptr;
@@ -604,8 +716,12 @@ void backward_epp(Groups* const* PG, Frontiers& F, const BackwardIO& io, int gat
             }
         }
         if (io.edges) io.edges[i] = p.E;
-        if (gn) gcur = std::move(gn);
+        if (gn) {
+            wgs.retire(gcur);
+            gcur = std::move(gn);
+        }
     }
+    wgs.join();
 }
 
 }  // namespace pg
