@@ -78,7 +78,9 @@ int pg_set_heavy_min_degree(uint64_t min_degree);
  * segments, K = forced), "ld_cg", "grouped_seg"; for the host-buffer
  * calls "host_segs" (source-row segments uploaded and reduced in turn, 1..8),
  * "host_chunks" (destination-row chunks of the last pass whose D2H overlaps
- * the next chunk, 1..16) and "host_trace" (1: phase times on stderr). A negative value
+ * the next chunk, 1..16), "host_final_segs" (trailing source segments the
+ * chunked last pass spans, 1..host_segs) and "host_trace" (1: phase times on
+ * stderr). A negative value
  * restores the default ($PG_<KEY> at load, else built-in). Unknown key ->
  * PG_ERR_CONFIG. */
 int pg_set_tuning(const char* key, int64_t value);

@@ -46,13 +46,16 @@ constexpr TuneKey kTuneKeys[] = {
     {"host_chunk_order", "PG_HOST_CHUNK_ORDER", 1},  // host drop-in last pass: 1 = last row chunk first
     {"grouped_seg", "PG_GROUPED_SEG", 0},  // grouped Fast: 1 = CTA-segmented reduction, 0 = an atomic per extra group
     {"heavy_wide_pipe", "PG_HEAVY_WIDE_PIPE", 1},  // heavy wide rows: 1 = software-pipelined k_agg_wide_pipe
+    {"host_final_segs", "PG_HOST_FINAL_SEGS", 1},  // host drop-in: trailing source segments of the chunked last pass
 };
 std::atomic<int64_t> g_tune[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];
+int64_t g_tune_def[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];  // $PG_<KEY> at load, else built-in
 std::once_flag g_tune_once;
 void tune_init() {
     for (size_t i = 0; i < sizeof(kTuneKeys) / sizeof(kTuneKeys[0]); ++i) {
         const char* e = std::getenv(kTuneKeys[i].env);
-        g_tune[i].store(e ? std::atoll(e) : kTuneKeys[i].def);
+        g_tune_def[i] = e ? std::atoll(e) : kTuneKeys[i].def;
+        g_tune[i].store(g_tune_def[i]);
     }
 }
 }  // namespace
@@ -66,7 +69,7 @@ bool set_tuning(const char* name, int64_t value) {
     std::call_once(g_tune_once, tune_init);
     for (size_t i = 0; i < sizeof(kTuneKeys) / sizeof(kTuneKeys[0]); ++i)
         if (std::strcmp(kTuneKeys[i].name, name) == 0) {
-            g_tune[i].store(value < 0 ? kTuneKeys[i].def : value);
+            g_tune[i].store(value < 0 ? g_tune_def[i] : value);
             return true;
         }
     return false;

@@ -234,10 +234,11 @@ void pg::run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re,
         const uint64_t* eb = p.offsets.get();
         const uint64_t* ee = p.offsets.get() + 1;
         uint64_t range_div = 1;
-        if (sel.seg >= 0) {
+        if (sel.seg >= 0) {  // segments [seg, seg_end): bnd holds nseg + 1 boundary rows of D entries
+            const int end = sel.seg_end < 0 ? sel.seg + 1 : sel.seg_end;
             eb = sel.bnd + static_cast<uint64_t>(sel.seg) * p.D;
-            ee = eb + p.D;
-            range_div = sel.nseg;
+            ee = sel.bnd + static_cast<uint64_t>(end) * p.D;
+            range_div = std::max<uint64_t>(1, sel.nseg / static_cast<uint64_t>(end - sel.seg));
         }
         if (rb == 0 && re == p.D) {
             aggregate_det(eb, ee, edges, p.order.get(), p.D, 0, p.D,
@@ -348,6 +349,9 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
     const uint32_t K = (big && parent_indexed && in_rows >= 4 && b.E >= 64ull * D)
                            ? static_cast<uint32_t>(std::clamp<int64_t>(tuning(kTuneHostSegs), 1, 8)) : 1;
     const uint32_t R = big ? static_cast<uint32_t>(std::clamp<int64_t>(tuning(kTuneHostChunks), 1, 16)) : 1;
+    // the last F segments form the chunked last pass (its D2H overlaps the
+    // next chunk); the K - F before it are whole-row passes under the H2D
+    const uint32_t F = static_cast<uint32_t>(std::clamp<int64_t>(tuning(kTuneHostFinalSegs), 1, K));
     const bool trace = tuning(kTuneHostTrace) != 0;
     std::vector<uint64_t> rcut(K + 1);
     for (uint32_t k = 0; k <= K; ++k) rcut[k] = in_rows * k / K;
@@ -405,16 +409,17 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
         PG_CUDA(cudaEventRecord(cs.ev[1 + k], cs.h2d));
         tmark(cs.h2d, "h2d" + std::to_string(k));
     }
-    // passes 0 .. K-2 over every destination
-    for (uint32_t k = 0; k + 1 < K; ++k) {
+    // passes 0 .. K-F-1 over every destination
+    for (uint32_t k = 0; k + F < K; ++k) {
         PG_CUDA(cudaStreamWaitEvent(s, cs.ev[1 + k], 0));
         run_aggregate(G, parent_indexed, 0, static_cast<uint32_t>(D), din.get(), ld, dout.get(), ld, dim,
                       k == 0 ? flags : (flags & ~PG_AGG_OVERWRITE), s, SegSel{G.host_seg_bnd.get(), static_cast<int>(k), K});
         tmark(s, "pass" + std::to_string(k));
     }
     PG_CUDA(cudaStreamWaitEvent(s, cs.ev[K], 0));
-    const unsigned last_flags = K > 1 ? (flags & ~PG_AGG_OVERWRITE) : flags;
-    const SegSel last = K > 1 ? SegSel{G.host_seg_bnd.get(), static_cast<int>(K - 1), K} : SegSel{};
+    const unsigned last_flags = K > F ? (flags & ~PG_AGG_OVERWRITE) : flags;
+    const SegSel last =
+        K > 1 ? SegSel{G.host_seg_bnd.get(), static_cast<int>(K - F), K, static_cast<int>(K)} : SegSel{};
     // Chunks are edge-balanced, so in destination order (hubs first) the
     // first chunks hold few rows and the last hold most of them: run them
     // last-first (tuning "host_chunk_order" = 1, default) so the big D2H
@@ -443,7 +448,7 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
     PG_CUDA(cudaStreamSynchronize(s));
     if (trace) {
         std::string line = "[host_trace] D=" + std::to_string(D) + " dim=" + std::to_string(dim) +
-                           " K=" + std::to_string(K) + " R=" + std::to_string(R) + ":";
+                           " K=" + std::to_string(K) + " F=" + std::to_string(F) + " R=" + std::to_string(R) + ":";
         for (size_t i = 1; i < nt; ++i) {
             float ms = 0.f;
             PG_CUDA(cudaEventElapsedTime(&ms, cs.tev[0], cs.tev[i]));

@@ -212,8 +212,9 @@ void aggregate_det(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges
 // the segment to run (seg < 0: whole edge lists).
 struct SegSel {
     const uint64_t* bnd = nullptr;
-    int seg = -1;
-    uint32_t nseg = 1;
+    int seg = -1;         // first segment of the span, -1 = whole lists
+    uint32_t nseg = 1;    // segments in bnd
+    int seg_end = -1;     // one past the last segment of the span (-1: seg + 1)
 };
 // The SpMM over a grouping's base (path: parent-indexed or local sources;
 // graph: vertex ids), destination rows [rb, re) with their cached degree
@@ -248,7 +249,8 @@ enum TuneKeyId {
     kTuneLdCg = 9,
     kTuneHostChunkOrder = 10,
     kTuneGroupedSeg = 11,
-    kTuneHeavyWidePipe = 12
+    kTuneHeavyWidePipe = 12,
+    kTuneHostFinalSegs = 13
 };
 int64_t tuning(int key);
 bool set_tuning(const char* name, int64_t value);

@@ -71,7 +71,8 @@ def test_candidates_match_oracle(orc):
 def test_tuning_keys(pg):
     """pg_set_tuning: scheduling knobs by name; unknown keys are config errors."""
     for key in ("vec_u", "chunk_major", "heavy_tma", "host_segs", "host_chunks", "host_trace", "heavy_narrow",
-                "wide_lpd", "src_segs", "ld_cg", "host_chunk_order", "grouped_seg"):
+                "wide_lpd", "src_segs", "ld_cg", "host_chunk_order", "grouped_seg", "heavy_wide_pipe",
+                "host_final_segs"):
         pg.set_tuning(key, None)
     import pytest
 

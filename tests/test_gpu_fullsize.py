@@ -94,3 +94,14 @@ def test_fullsize_spmm_sampled_rows_bit_exact(pg, orc, reddit):
         xh = torch.empty((p.D, dim), dtype=torch.float32).pin_memory().numpy()
         pg.backward_aggregation(prep.groups[i], yh, xh, overwrite=True)
         assert np.array_equal(bits(xh), bits(out.cpu().numpy())), f"host path {i}"
+        # other pipeline shapes: source segments K, the last F of them in the chunked last pass
+        for ks, fs in ((4, 2), (3, 3), (5, 2)):
+            pg.set_tuning("host_segs", ks)
+            pg.set_tuning("host_final_segs", fs)
+            try:
+                xh[:] = np.nan
+                pg.backward_aggregation(prep.groups[i], yh, xh, overwrite=True)
+                assert np.array_equal(bits(xh), bits(out.cpu().numpy())), f"host path {i} K={ks} F={fs}"
+            finally:
+                pg.set_tuning("host_segs", None)
+                pg.set_tuning("host_final_segs", None)

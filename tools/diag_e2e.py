@@ -67,10 +67,16 @@ def main(config="reddit"):
             dev_ms = (time.perf_counter() - t) * 1e3
         print(f"path {i} dim {dim}: device call {dev_ms:.2f} ms", flush=True)
         want = xd.cpu().numpy().view(np.uint32)
-        shapes = [(2, 4, 1)] if i == 0 else [(1, 1, 1), (1, 8, 1), (1, 16, 1), (1, 32, 1), (2, 16, 1), (2, 32, 1),
-                                              (3, 16, 1), (3, 32, 1), (4, 16, 1), (3, 16, 0)]
-        for K, R, order in shapes:
+        # (K source segments, F of them in the chunked last pass, R row chunks, reversed order)
+        shapes = [(2, 1, 4, 1)] if i == 0 else [
+            (1, 1, 16, 1), (2, 1, 16, 1), (3, 1, 16, 1), (4, 1, 16, 1), (3, 1, 16, 0),
+            (3, 2, 16, 1), (4, 2, 16, 1), (5, 2, 16, 1), (5, 3, 16, 1), (6, 3, 16, 1), (6, 2, 16, 1),
+            (8, 3, 16, 1), (8, 4, 16, 1), (4, 3, 16, 1)]
+        if os.environ.get("DIAG_SHAPES"):
+            shapes = [tuple(int(v) for v in t.split(",")) for t in os.environ["DIAG_SHAPES"].split()]
+        for K, F, R, order in shapes:
             pg.set_tuning("host_segs", K)
+            pg.set_tuning("host_final_segs", F)
             pg.set_tuning("host_chunks", R)
             pg.set_tuning("host_chunk_order", order)
             ts = []
@@ -78,9 +84,11 @@ def main(config="reddit"):
                 t = time.perf_counter()
                 pg.backward_aggregation(G, yh, xh, overwrite=True)
                 ts.append((time.perf_counter() - t) * 1e3)
-            assert np.array_equal(xh.view(np.uint32), want), (K, R)
-            print(f"path {i} dim {dim}: host call K={K} R={R} reversed={order}: {min(ts[1:]):.2f} ms (min of 3)",
-                  flush=True)
+            assert np.array_equal(xh.view(np.uint32), want), (K, F, R)
+            print(f"path {i} dim {dim}: host call K={K} F={F} R={R} reversed={order}: {min(ts[1:]):.2f} ms "
+                  f"(min of 3)", flush=True)
+        for key in ("host_segs", "host_final_segs", "host_chunks", "host_chunk_order"):
+            pg.set_tuning(key)
         pg.set_tuning("host_trace", 1)
         for rep in range(3):
             t = time.perf_counter()
@@ -98,6 +106,7 @@ def main(config="reddit"):
                                            c.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)))
             print(f"path {i}: raw C call wall {(time.perf_counter() - t) * 1e3:.2f} ms", flush=True)
         pg.set_tuning("host_segs")
+        pg.set_tuning("host_final_segs")
         pg.set_tuning("host_chunks")
         pg.set_tuning("host_chunk_order")
 
