@@ -952,6 +952,25 @@ def cpu_baseline(paths, dims, args):
            "ms_per_sample_epoch": round(sec * 1e3, 2),
            "ms_per_epoch_extrapolated": round(sec * 1e3 * args.sample_stride, 1)}
     R.free_stage_handles(items)
+    # the same stage on one host thread (all cores and 1 thread),
+    # on a sample 8x sparser so it stays a few seconds
+    stride1 = args.sample_stride * 8
+    arrays = []
+    for p in paths:
+        x = p.export()
+        x["layer"] = p.layer
+        arrays.append(x)
+    items = R.stage_items_from_arrays(arrays, sample_stride=stride1)
+    del arrays
+    for i, it in enumerate(items):
+        R.run_backward_stage(it, ys[i], workers=1)
+    t1 = statistics.median([sum(R.run_backward_stage(it, ys[i], workers=1)[0] for i, it in enumerate(items))
+                            for _ in range(max(1, min(args.cpu_steps, 3)))])
+    b1 = sum(path_bytes(it["D"], it["E"], dims[i]) for i, it in enumerate(items))
+    out["single_thread"] = {"value": round(b1 / t1 / 1e9, 3), "unit": "GB/s", "cores": 1,
+                            "sample": f"every {stride1}th destination of each path",
+                            "ms_per_epoch_extrapolated": round(t1 * 1e3 * stride1, 1)}
+    R.free_stage_handles(items)
     return out
 
 
