@@ -869,6 +869,22 @@ def measure_e2e(pg, pgd, torch, dist, paths, groups, shards, dims, rows, world, 
         sec = statistics.median(per) / 1e3
         stats = {"stat": f"median of {steps} steps", "mean_ms": round(statistics.mean(per), 3),
                  "min_ms": round(min(per), 3), "max_ms": round(max(per), 3)}
+        # the same call with PAGEABLE buffers (a reference DenseMatrix is a
+        # std::vector): staged through the library's pinned slots
+        ysp = [np.array(y) for y in ys]
+        xsp = [np.empty_like(x) for x in xs]
+
+        def one_pageable():
+            for i in range(L):
+                pg.backward_aggregation(groups[i], ysp[i], xsp[i], overwrite=True)
+        one_pageable()
+        perp = []
+        for _ in range(max(3, min(steps, 5))):
+            t1 = time.perf_counter()
+            one_pageable()
+            perp.append((time.perf_counter() - t1) * 1e3)
+        stats["pageable_ms_per_step"] = round(statistics.median(perp), 3)
+        log(f"[e2e] pageable per-step ms {[round(x, 2) for x in perp]}")
     else:
         ys, yd, yf, xd, xh = [], [], [], [], []
         for i, p in enumerate(paths):

@@ -217,7 +217,11 @@ int pg_backward_aggregate_rows(pg_groups G, uint32_t row_begin, uint32_t row_end
                                const float* y_dev, uint64_t y_rows, uint64_t ld_in, float* x_dev,
                                uint64_t ld_out, uint64_t dim, unsigned flags, void* stream);
 /* Host-buffer drop-ins for DenseMatrix<float> callers (row-major, ld = cols):
- * copy in, run, copy out, synchronise. */
+ * copy in, run, copy out, synchronise. Pinned (cudaHostAlloc /
+ * cudaHostRegister) buffers are DMA'd directly; pageable ones (a
+ * std::vector) are staged through library-owned pinned slots by a few host
+ * threads, overlapped with the copies (Reddit layer 0: 28.5 ms pinned,
+ * ~33-40 ms pageable, vs ~105 ms for driver-staged pageable copies). */
 int pg_aggregate_pull_host(pg_groups G, const float* in_host, uint64_t in_rows, uint64_t dim,
                            float* out_host, unsigned flags, uint64_t* counters);
 int pg_backward_aggregate_host(pg_groups G, const float* y_host, uint64_t y_rows, uint64_t dim,

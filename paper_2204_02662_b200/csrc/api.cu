@@ -2,13 +2,17 @@
 // handle plumbing, host-side input synthesis with the reference's exact
 // libstdc++ random streams, and the host-buffer drop-ins.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <condition_variable>
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <numeric>
 #include <random>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/pathgcn_b200.h"
@@ -320,6 +324,166 @@ CopyStreams& copy_streams(int device, size_t nev) {
     return c;
 }
 
+// Pageable host buffers (a reference DenseMatrix is a std::vector) cannot
+// be DMA'd asynchronously: the driver would stage them synchronously at
+// ~10 GB/s. Instead they go through library-owned pinned slots: a few host
+// threads memcpy pageable <-> slot while the copy engine moves the previous
+// slot, so the link still streams.
+bool host_pinned(const void* p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
+// memcpy split over a small persistent thread pool (the caller takes part)
+class ParallelCopy {
+public:
+    explicit ParallelCopy(unsigned n) : nthreads_(n) {
+        for (unsigned t = 1; t < n; ++t) workers_.emplace_back([this, t] { loop(t); });
+    }
+    ~ParallelCopy() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+            ++gen_;
+        }
+        cv_.notify_all();
+        for (auto& w : workers_) w.join();
+    }
+    void copy(void* dst, const void* src, size_t n) {
+        if (n < (1u << 20) || nthreads_ == 1) {
+            std::memcpy(dst, src, n);
+            return;
+        }
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            dst_ = static_cast<char*>(dst);
+            src_ = static_cast<const char*>(src);
+            n_ = n;
+            pending_ = nthreads_ - 1;
+            ++gen_;
+        }
+        cv_.notify_all();
+        part(0);
+        std::unique_lock<std::mutex> lk(mu_);
+        done_cv_.wait(lk, [this] { return pending_ == 0; });
+    }
+
+private:
+    void part(unsigned t) {
+        const size_t per = (n_ / nthreads_ + 63) & ~size_t(63);
+        const size_t b = std::min(n_, per * t), e = std::min(n_, per * (t + 1));
+        if (e > b) std::memcpy(dst_ + b, src_ + b, e - b);
+    }
+    void loop(unsigned t) {
+        uint64_t seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return gen_ != seen; });
+                seen = gen_;
+                if (stop_) return;
+            }
+            part(t);
+            {
+                std::lock_guard<std::mutex> lk(mu_);
+                if (--pending_ == 0) done_cv_.notify_one();
+            }
+        }
+    }
+    unsigned nthreads_;
+    std::vector<std::thread> workers_;
+    std::mutex mu_;
+    std::condition_variable cv_, done_cv_;
+    uint64_t gen_ = 0;
+    unsigned pending_ = 0;
+    bool stop_ = false;
+    char* dst_ = nullptr;
+    const char* src_ = nullptr;
+    size_t n_ = 0;
+};
+
+struct Staging {
+    static constexpr size_t kSlot = 16u << 20;
+    static constexpr int kSlots = 4;
+    void* up[kSlots] = {};
+    void* down[kSlots] = {};
+    cudaEvent_t up_ev[kSlots] = {}, down_ev[kSlots] = {};
+    std::unique_ptr<ParallelCopy> pc;
+    std::mutex mu;  // one host call at a time per device uses the slots
+};
+
+Staging& staging(int device) {
+    static std::mutex mu;
+    static std::vector<std::unique_ptr<Staging>> per_dev;
+    std::lock_guard<std::mutex> lk(mu);
+    if (static_cast<int>(per_dev.size()) <= device) per_dev.resize(device + 1);
+    if (!per_dev[device]) {
+        auto st = std::make_unique<Staging>();
+        for (int i = 0; i < Staging::kSlots; ++i) {
+            PG_CUDA(cudaHostAlloc(&st->up[i], Staging::kSlot, cudaHostAllocDefault));
+            PG_CUDA(cudaHostAlloc(&st->down[i], Staging::kSlot, cudaHostAllocDefault));
+            PG_CUDA(cudaEventCreateWithFlags(&st->up_ev[i], cudaEventDisableTiming));
+            PG_CUDA(cudaEventCreateWithFlags(&st->down_ev[i], cudaEventDisableTiming));
+        }
+        const unsigned hc = std::max(1u, std::thread::hardware_concurrency());
+        st->pc = std::make_unique<ParallelCopy>(std::clamp(hc / 2, 1u, 8u));
+        per_dev[device] = std::move(st);
+    }
+    return *per_dev[device];
+}
+
+// H2D of n bytes from pageable src through the up slots on stream st
+// (returns once the last piece is queued; the host part is done)
+void staged_h2d(Staging& sg, void* dst, const void* src, size_t n, cudaStream_t st, int& slot) {
+    for (size_t off = 0; off < n; off += Staging::kSlot) {
+        const size_t len = std::min(Staging::kSlot, n - off);
+        PG_CUDA(cudaEventSynchronize(sg.up_ev[slot]));  // the slot's previous DMA has read it
+        sg.pc->copy(sg.up[slot], static_cast<const char*>(src) + off, len);
+        PG_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + off, sg.up[slot], len, cudaMemcpyHostToDevice, st));
+        PG_CUDA(cudaEventRecord(sg.up_ev[slot], st));
+        slot = (slot + 1) % Staging::kSlots;
+    }
+}
+
+// D2H into pageable dst: pieces DMA'd to the down slots on stream st (after
+// whatever st already waits for), each copied out by the host as soon as it
+// lands while the next piece is in flight
+struct StagedD2H {
+    Staging& sg;
+    cudaStream_t st;
+    int slot = 0;
+    struct Pending {
+        int slot;
+        char* dst;
+        size_t len;
+    };
+    std::vector<Pending> q;
+    void drain_one() {
+        const Pending pd = q.front();
+        q.erase(q.begin());
+        PG_CUDA(cudaEventSynchronize(sg.down_ev[pd.slot]));
+        sg.pc->copy(pd.dst, sg.down[pd.slot], pd.len);
+    }
+    void enqueue(void* dst, const void* src, size_t n) {
+        for (size_t off = 0; off < n; off += Staging::kSlot) {
+            const size_t len = std::min(Staging::kSlot, n - off);
+            if (q.size() + 1 >= static_cast<size_t>(Staging::kSlots)) drain_one();  // keep one slot free
+            PG_CUDA(cudaMemcpyAsync(sg.down[slot], static_cast<const char*>(src) + off, len, cudaMemcpyDeviceToHost,
+                                    st));
+            PG_CUDA(cudaEventRecord(sg.down_ev[slot], st));
+            q.push_back({slot, static_cast<char*>(dst) + off, len});
+            slot = (slot + 1) % Staging::kSlots;
+        }
+    }
+    void finish() {
+        while (!q.empty()) drain_one();
+    }
+};
+
 // Host buffers (row-major, ld = dim) through a copy/compute pipeline:
 //  * the input goes up in K source-row segments on the H2D stream (flat
 //    copies at full link rate, then an on-device repack to 16-byte rows when
@@ -394,27 +558,41 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
     PG_CUDA(cudaEventRecord(cs.ev[0], s));
     PG_CUDA(cudaStreamWaitEvent(cs.h2d, cs.ev[0], 0));
     PG_CUDA(cudaStreamWaitEvent(cs.d2h, cs.ev[0], 0));
+    // pageable host buffers go through the pinned staging slots
+    const bool in_pg = dim && in_rows && !host_pinned(in_host);
+    const bool out_pg = dim && D && !host_pinned(out_host);
+    Staging* sg = (in_pg || out_pg) ? &staging(G.device) : nullptr;
+    std::unique_lock<std::mutex> sg_lock;
+    if (sg) sg_lock = std::unique_lock<std::mutex>(sg->mu);
+    int up_slot = 0;
+    auto upload = [&](void* dst, const void* src, size_t n, bool pageable) {
+        if (pageable)
+            staged_h2d(*sg, dst, src, n, cs.h2d, up_slot);
+        else
+            PG_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, cs.h2d));
+    };
     if (D && dim && !(flags & PG_AGG_OVERWRITE)) {  // accumulate: current output goes up first
-        PG_CUDA(cudaMemcpyAsync(packed ? dout.get() : fout.get(), out_host, D * dim * 4, cudaMemcpyHostToDevice,
-                                cs.h2d));
+        upload(packed ? dout.get() : fout.get(), out_host, D * dim * 4, out_pg);
         if (!packed) copy_rows(fout.get(), dim, dout.get(), ld, D, dim, cs.h2d);
     }
+    // segment k up, then pass k (every destination, segment k's edges) for
+    // the K - F segments before the chunked last pass
     for (uint32_t k = 0; k < K; ++k) {
         const uint64_t r0 = rcut[k], r1 = rcut[k + 1];
         if (r1 > r0 && dim) {
             float* dst = packed ? din.get() + r0 * ld : fin.get() + r0 * dim;
-            PG_CUDA(cudaMemcpyAsync(dst, in_host + r0 * dim, (r1 - r0) * dim * 4, cudaMemcpyHostToDevice, cs.h2d));
+            upload(dst, in_host + r0 * dim, (r1 - r0) * dim * 4, in_pg);
             if (!packed) copy_rows(fin.get() + r0 * dim, dim, din.get() + r0 * ld, ld, r1 - r0, dim, cs.h2d);
         }
         PG_CUDA(cudaEventRecord(cs.ev[1 + k], cs.h2d));
         tmark(cs.h2d, "h2d" + std::to_string(k));
-    }
-    // passes 0 .. K-F-1 over every destination
-    for (uint32_t k = 0; k + F < K; ++k) {
-        PG_CUDA(cudaStreamWaitEvent(s, cs.ev[1 + k], 0));
-        run_aggregate(G, parent_indexed, 0, static_cast<uint32_t>(D), din.get(), ld, dout.get(), ld, dim,
-                      k == 0 ? flags : (flags & ~PG_AGG_OVERWRITE), s, SegSel{G.host_seg_bnd.get(), static_cast<int>(k), K});
-        tmark(s, "pass" + std::to_string(k));
+        if (k + F < K) {
+            PG_CUDA(cudaStreamWaitEvent(s, cs.ev[1 + k], 0));
+            run_aggregate(G, parent_indexed, 0, static_cast<uint32_t>(D), din.get(), ld, dout.get(), ld, dim,
+                          k == 0 ? flags : (flags & ~PG_AGG_OVERWRITE), s,
+                          SegSel{G.host_seg_bnd.get(), static_cast<int>(k), K});
+            tmark(s, "pass" + std::to_string(k));
+        }
     }
     PG_CUDA(cudaStreamWaitEvent(s, cs.ev[K], 0));
     const unsigned last_flags = K > F ? (flags & ~PG_AGG_OVERWRITE) : flags;
@@ -424,14 +602,23 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
     // first chunks hold few rows and the last hold most of them: run them
     // last-first (tuning "host_chunk_order" = 1, default) so the big D2H
     // copies start early and the tail after the final chunk is a small one.
+    // Every chunk is queued before any D2H, so a host that blocks on a
+    // staged (pageable) download never starves the SpMM stream.
     const bool reverse = tuning(kTuneHostChunkOrder) == 1;
+    std::vector<size_t> order;
     for (size_t ri = 0; ri + 1 < cuts.size(); ++ri) {
         const size_t r = reverse ? cuts.size() - 2 - ri : ri;
-        const uint32_t rb = cuts[r], re = cuts[r + 1];
-        if (rb == re) continue;
-        run_aggregate(G, parent_indexed, rb, re, din.get(), ld, dout.get() + rb * ld, ld, dim, last_flags, s, last);
+        if (cuts[r] == cuts[r + 1]) continue;
+        order.push_back(r);
+        run_aggregate(G, parent_indexed, cuts[r], cuts[r + 1], din.get(), ld, dout.get() + cuts[r] * ld, ld, dim,
+                      last_flags, s, last);
         PG_CUDA(cudaEventRecord(cs.ev[1 + K + r], s));
         tmark(s, "chunk" + std::to_string(r));
+    }
+    std::unique_ptr<StagedD2H> down;
+    if (out_pg) down = std::make_unique<StagedD2H>(StagedD2H{*sg, cs.d2h});
+    for (const size_t r : order) {
+        const uint32_t rb = cuts[r], re = cuts[r + 1];
         PG_CUDA(cudaStreamWaitEvent(cs.d2h, cs.ev[1 + K + r], 0));
         if (!dim) continue;
         const float* src = dout.get() + rb * ld;
@@ -439,9 +626,13 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
             copy_rows(dout.get() + rb * ld, ld, fout.get() + rb * dim, dim, re - rb, dim, cs.d2h);
             src = fout.get() + rb * dim;
         }
-        PG_CUDA(cudaMemcpyAsync(out_host + rb * dim, src, (re - rb) * dim * 4, cudaMemcpyDeviceToHost, cs.d2h));
+        if (down)
+            down->enqueue(out_host + rb * dim, src, (re - rb) * dim * 4);
+        else
+            PG_CUDA(cudaMemcpyAsync(out_host + rb * dim, src, (re - rb) * dim * 4, cudaMemcpyDeviceToHost, cs.d2h));
         tmark(cs.d2h, "d2h" + std::to_string(r));
     }
+    if (down) down->finish();
     // buffers are freed stream-ordered on s: s waits for both copy streams
     PG_CUDA(cudaEventRecord(cs.ev[1 + K + R], cs.d2h));
     PG_CUDA(cudaStreamWaitEvent(s, cs.ev[1 + K + R], 0));

@@ -396,3 +396,36 @@ def test_large_checksum(pg, orc):
     xh4 = np.zeros((dp.D, 600), np.float32)
     pg.backward_aggregation(G, y4, xh4, overwrite=True)
     assert np.array_equal(bits(xh4), bits(want4))
+
+
+@pytest.mark.parametrize("dim", [301, 264])
+def test_host_drop_in_pageable_and_pinned(pg, orc, dim):
+    """The host-buffer drop-in (pg_backward_aggregate_host) on a path big
+    enough for the K-segment / R-chunk pipeline, with PAGEABLE buffers (a
+    reference DenseMatrix is a std::vector: staged through the library's
+    pinned slots, several 16 MB pieces) and pinned ones, overwrite and
+    accumulate, odd (repacked) and 16-byte widths: bit-exact with the fp32
+    oracle."""
+    torch = torch_mod()
+    pairs, n_pad = rmat_pairs(orc, 32768, 32768 * 48, 41)
+    vt = orc.sample_training_set(32768, 0.5, 9)
+    og, dg, F, ops, dps = build_all(pg, orc, pairs, n_pad, vt, 2)
+    dp, op = dps[1], ops[1]  # the layer-0 path: every frontier vertex, E/D ~ 90
+    assert dp.E >= 64 * dp.D and dp.D * dim * 4 >= (32 << 20)
+    G = pg.group_neighbors(dp, 4)
+    rng = np.random.default_rng(dim)
+    y = rng.uniform(-1, 1, size=(dp.P, dim)).astype(np.float32)
+    base = rng.uniform(-1, 1, size=(dp.D, dim)).astype(np.float32)
+    want0 = orc.aggregate_pull_f32(op.offsets, op.neighbors, op.weights, y[op.srcpos])
+    want1 = orc.aggregate_pull_f32(op.offsets, op.neighbors, op.weights, y[op.srcpos], out=base)
+    for pinned in (False, True):
+        yh = torch.from_numpy(y).pin_memory().numpy() if pinned else y.copy()
+        x0 = np.full((dp.D, dim), np.nan, np.float32)
+        x1 = base.copy()
+        if pinned:
+            x0 = torch.from_numpy(x0).pin_memory().numpy()
+            x1 = torch.from_numpy(x1).pin_memory().numpy()
+        pg.backward_aggregation(G, yh, x0, overwrite=True)
+        pg.backward_aggregation(G, yh, x1)
+        assert np.array_equal(bits(x0), bits(want0)), ("overwrite", pinned)
+        assert np.array_equal(bits(x1), bits(want1)), ("accumulate", pinned)
