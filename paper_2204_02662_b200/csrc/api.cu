@@ -304,12 +304,22 @@ struct CopyStreams {
     cudaStream_t h2d = nullptr, d2h = nullptr;
     std::vector<cudaEvent_t> ev;  // sync events
     std::vector<cudaEvent_t> tev;  // timing events (host_trace)
+    std::mutex call;              // one host-buffer call at a time per device owns them
 };
 
-CopyStreams& copy_streams(int device, size_t nev) {
-    static std::vector<CopyStreams> per_dev;
-    if (static_cast<int>(per_dev.size()) <= device) per_dev.resize(device + 1);
-    CopyStreams& c = per_dev[device];
+// the caller holds c.call (taken here) for the whole host-buffer call
+CopyStreams& copy_streams(int device, size_t nev, std::unique_lock<std::mutex>& held) {
+    static std::mutex mu;
+    static std::vector<std::unique_ptr<CopyStreams>> per_dev;
+    CopyStreams* cp;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (static_cast<int>(per_dev.size()) <= device) per_dev.resize(device + 1);
+        if (!per_dev[device]) per_dev[device] = std::make_unique<CopyStreams>();
+        cp = per_dev[device].get();
+    }
+    held = std::unique_lock<std::mutex>(cp->call);
+    CopyStreams& c = *cp;
     if (!c.h2d) {
         PG_CUDA(cudaStreamCreateWithFlags(&c.h2d, cudaStreamNonBlocking));
         PG_CUDA(cudaStreamCreateWithFlags(&c.d2h, cudaStreamNonBlocking));
@@ -542,7 +552,8 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
         }
         cuts = G.host_chunks;
     }
-    CopyStreams& cs = copy_streams(G.device, 2 + K + 2 * R + 2);
+    std::unique_lock<std::mutex> cs_lock;
+    CopyStreams& cs = copy_streams(G.device, 2 + K + 2 * R + 2, cs_lock);
     size_t nt = 0;  // trace events used
     auto mark = [&](cudaStream_t st) {
         if (trace) PG_CUDA(cudaEventRecord(cs.tev[nt++], st));

@@ -429,3 +429,38 @@ def test_host_drop_in_pageable_and_pinned(pg, orc, dim):
         pg.backward_aggregation(G, yh, x1)
         assert np.array_equal(bits(x0), bits(want0)), ("overwrite", pinned)
         assert np.array_equal(bits(x1), bits(want1)), ("accumulate", pinned)
+
+
+def test_host_drop_in_concurrent_threads(pg, orc):
+    """Distinct groupings may be used from different host threads at once
+    (the reference's contract for built objects): concurrent host-buffer
+    calls share the per-device copy streams and staging slots safely."""
+    import threading
+
+    pairs, n_pad = rmat_pairs(orc, 4096, 4096 * 8, 31)
+    vt = orc.sample_training_set(4096, 0.3, 5)
+    og, dg, F, ops, dps = build_all(pg, orc, pairs, n_pad, vt, 2)
+    rng = np.random.default_rng(3)
+    jobs = []
+    for dp, op, dim in ((dps[0], ops[0], 41), (dps[1], ops[1], 602)):
+        y = rng.uniform(-1, 1, size=(dp.P, dim)).astype(np.float32)
+        want = orc.aggregate_pull_f32(op.offsets, op.neighbors, op.weights, y[op.srcpos])
+        jobs.append((pg.group_neighbors(dp, 4), y, want, dp.D, dim))
+    errors = []
+
+    def run(G, y, want, D, dim):
+        try:
+            for _ in range(4):
+                x = np.full((D, dim), np.nan, np.float32)
+                pg.backward_aggregation(G, y, x, overwrite=True)
+                if not np.array_equal(bits(x), bits(want)):
+                    errors.append(dim)
+        except Exception as e:  # pragma: no cover
+            errors.append(repr(e))
+
+    ts = [threading.Thread(target=run, args=j) for j in jobs * 2]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
