@@ -36,7 +36,7 @@ constexpr TuneKey kTuneKeys[] = {
     {"heavy_tma", "PG_HEAVY_TMA", 0},      // heavy narrow rows: 1 = TMA bulk-copy mbarrier ring (k_agg_heavy)
     {"vec_u", "PG_VEC_U", 8},              // edges per gather batch in k_agg_vec4 (4, 8, 16)
     {"chunk_major", "PG_CHUNK_MAJOR", 1},  // k_agg_vec4 item order for multi-chunk rows
-    {"host_segs", "PG_HOST_SEGS", 3},      // host drop-in: source-row segments (H2D overlap)
+    {"host_segs", "PG_HOST_SEGS", 6},      // host drop-in: source-row segments (H2D overlap)
     {"host_chunks", "PG_HOST_CHUNKS", 16}, // host drop-in: row chunks of the last pass (D2H overlap)
     {"host_trace", "PG_HOST_TRACE", 0},    // host drop-in: print phase times to stderr
     {"heavy_narrow", "PG_HEAVY_NARROW", 0},  // heavy rows <= 64 floats: 1 = k_agg_narrow_lat, 0 = coop tiles
@@ -46,7 +46,10 @@ constexpr TuneKey kTuneKeys[] = {
     {"host_chunk_order", "PG_HOST_CHUNK_ORDER", 1},  // host drop-in last pass: 1 = last row chunk first
     {"grouped_seg", "PG_GROUPED_SEG", 0},  // grouped Fast: 1 = CTA-segmented reduction, 0 = an atomic per extra group
     {"heavy_wide_pipe", "PG_HEAVY_WIDE_PIPE", 1},  // heavy wide rows: 1 = software-pipelined k_agg_wide_pipe
-    {"host_final_segs", "PG_HOST_FINAL_SEGS", 1},  // host drop-in: trailing source segments of the chunked last pass
+    {"host_final_segs", "PG_HOST_FINAL_SEGS", 3},  // host drop-in: trailing source segments of the chunked last pass
+    {"host_pass_smem", "PG_HOST_PASS_SMEM", 0},  // host drop-in: KB of idle smem per SpMM block in passes beside the H2D
+    {"host_pitch2d", "PG_HOST_PITCH2D", 0},  // host drop-in: odd widths by 2-D DMA (1) or flat DMA + repack kernel (0)
+    {"host_copy_prio", "PG_HOST_COPY_PRIO", 1},  // host drop-in: copy/repack streams at the highest priority (read once)
 };
 std::atomic<int64_t> g_tune[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];
 int64_t g_tune_def[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];  // $PG_<KEY> at load, else built-in
@@ -59,6 +62,8 @@ void tune_init() {
     }
 }
 }  // namespace
+
+thread_local int g_pass_smem = 0;
 
 int64_t tuning(int key) {
     std::call_once(g_tune_once, tune_init);
@@ -1202,7 +1207,20 @@ void launch_vec4(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges, 
     // L2-only gathers measured no faster for narrow rows and slower for wide
     // ones (layer 0 16.7 -> 17.1 ms), so only on request
     const bool cg = tuning(kTuneLdCg) == 2;
-    if (ext.src_bits || ext.dst_bits)
+    const int thr = g_pass_smem;
+    if (thr > 0) {
+        static thread_local std::vector<int> attr;  // per device: max dynamic smem set
+        int dev = 0;
+        PG_CUDA(cudaGetDevice(&dev));
+        if (static_cast<int>(attr.size()) <= dev) attr.resize(dev + 1, 0);
+        if (attr[dev] < thr) {
+            PG_CUDA(cudaFuncSetAttribute(k_agg_vec4<LPD, U, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, thr));
+            attr[dev] = thr;
+        }
+        k_agg_vec4<LPD, U, false><<<grid_for(items * LPD, 256), 256, thr, s>>>(
+            ebeg, eend, edges, order, d_begin, items, chunks, in, static_cast<uint32_t>(ld_in * 4), out, ld_out, dim,
+            accumulate, kZeros, 0u, cm, ext);
+    } else if (ext.src_bits || ext.dst_bits)
         k_agg_vec4<LPD, U, true><<<grid_for(items * LPD, 256), 256, 0, s>>>(
             ebeg, eend, edges, order, d_begin, items, chunks, in, static_cast<uint32_t>(ld_in * 4), out, ld_out, dim,
             accumulate, kZeros, 0u, cm, ext);

@@ -321,8 +321,14 @@ CopyStreams& copy_streams(int device, size_t nev, std::unique_lock<std::mutex>& 
     held = std::unique_lock<std::mutex>(cp->call);
     CopyStreams& c = *cp;
     if (!c.h2d) {
-        PG_CUDA(cudaStreamCreateWithFlags(&c.h2d, cudaStreamNonBlocking));
-        PG_CUDA(cudaStreamCreateWithFlags(&c.d2h, cudaStreamNonBlocking));
+        // highest priority: the repack kernels of odd-width rows on these
+        // streams must get SMs as soon as SpMM blocks retire, not after the
+        // whole pass (their segment / chunk copy waits on them)
+        int lo = 0, hi = 0;
+        PG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        const int prio = tuning(kTuneHostCopyPrio) ? hi : 0;
+        PG_CUDA(cudaStreamCreateWithPriority(&c.h2d, cudaStreamNonBlocking, prio));
+        PG_CUDA(cudaStreamCreateWithPriority(&c.d2h, cudaStreamNonBlocking, prio));
     }
     while (c.ev.size() < nev) {
         cudaEvent_t e;
@@ -582,26 +588,39 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
         else
             PG_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, cs.h2d));
     };
-    if (D && dim && !(flags & PG_AGG_OVERWRITE)) {  // accumulate: current output goes up first
-        upload(packed ? dout.get() : fout.get(), out_host, D * dim * 4, out_pg);
-        if (!packed) copy_rows(fout.get(), dim, dout.get(), ld, D, dim, cs.h2d);
-    }
+    // pinned rows of width dim go straight into the 16-byte-pitched device
+    // rows with a 2-D copy: a repack kernel on the copy stream would queue
+    // behind the SpMM's blocks and hold the segment back until the pass ends
+    const bool pitch2d = !packed && tuning(kTuneHostPitch2d) != 0;
+    auto upload_rows = [&](float* dst_pitched, float* dst_flat, const float* src, uint64_t rows, bool pageable) {
+        if (!rows) return;
+        if (packed) {
+            upload(dst_pitched, src, rows * dim * 4, pageable);
+        } else if (pitch2d && !pageable) {
+            PG_CUDA(cudaMemcpy2DAsync(dst_pitched, ld * 4, src, dim * 4, dim * 4, rows, cudaMemcpyHostToDevice,
+                                      cs.h2d));
+        } else {
+            upload(dst_flat, src, rows * dim * 4, pageable);
+            copy_rows(dst_flat, dim, dst_pitched, ld, rows, dim, cs.h2d);
+        }
+    };
+    if (D && dim && !(flags & PG_AGG_OVERWRITE))  // accumulate: current output goes up first
+        upload_rows(dout.get(), fout.get(), out_host, D, out_pg);
     // segment k up, then pass k (every destination, segment k's edges) for
     // the K - F segments before the chunked last pass
     for (uint32_t k = 0; k < K; ++k) {
         const uint64_t r0 = rcut[k], r1 = rcut[k + 1];
-        if (r1 > r0 && dim) {
-            float* dst = packed ? din.get() + r0 * ld : fin.get() + r0 * dim;
-            upload(dst, in_host + r0 * dim, (r1 - r0) * dim * 4, in_pg);
-            if (!packed) copy_rows(fin.get() + r0 * dim, dim, din.get() + r0 * ld, ld, r1 - r0, dim, cs.h2d);
-        }
+        if (r1 > r0 && dim)
+            upload_rows(din.get() + r0 * ld, fin.get() + r0 * dim, in_host + r0 * dim, r1 - r0, in_pg);
         PG_CUDA(cudaEventRecord(cs.ev[1 + k], cs.h2d));
         tmark(cs.h2d, "h2d" + std::to_string(k));
         if (k + F < K) {
             PG_CUDA(cudaStreamWaitEvent(s, cs.ev[1 + k], 0));
+            g_pass_smem = static_cast<int>(std::clamp<int64_t>(tuning(kTuneHostPassSmem), 0, 227) * 1024);
             run_aggregate(G, parent_indexed, 0, static_cast<uint32_t>(D), din.get(), ld, dout.get(), ld, dim,
                           k == 0 ? flags : (flags & ~PG_AGG_OVERWRITE), s,
                           SegSel{G.host_seg_bnd.get(), static_cast<int>(k), K});
+            g_pass_smem = 0;
             tmark(s, "pass" + std::to_string(k));
         }
     }
@@ -633,6 +652,12 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
         PG_CUDA(cudaStreamWaitEvent(cs.d2h, cs.ev[1 + K + r], 0));
         if (!dim) continue;
         const float* src = dout.get() + rb * ld;
+        if (!packed && pitch2d && !down) {
+            PG_CUDA(cudaMemcpy2DAsync(out_host + rb * dim, dim * 4, src, ld * 4, dim * 4, re - rb,
+                                      cudaMemcpyDeviceToHost, cs.d2h));
+            tmark(cs.d2h, "d2h" + std::to_string(r));
+            continue;
+        }
         if (!packed) {
             copy_rows(dout.get() + rb * ld, ld, fout.get() + rb * dim, dim, re - rb, dim, cs.d2h);
             src = fout.get() + rb * dim;

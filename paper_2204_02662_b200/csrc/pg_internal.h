@@ -250,8 +250,15 @@ enum TuneKeyId {
     kTuneHostChunkOrder = 10,
     kTuneGroupedSeg = 11,
     kTuneHeavyWidePipe = 12,
-    kTuneHostFinalSegs = 13
+    kTuneHostFinalSegs = 13,
+    kTuneHostPassSmem = 14,
+    kTuneHostPitch2d = 15,
+    kTuneHostCopyPrio = 16
 };
+// idle dynamic smem (bytes) per k_agg_vec4 block for the launches of this
+// thread while set (host drop-in passes beside the H2D: fewer resident
+// blocks, less L2 pressure against the copy engines)
+extern thread_local int g_pass_smem;
 int64_t tuning(int key);
 bool set_tuning(const char* name, int64_t value);
 

@@ -95,7 +95,7 @@ def test_fullsize_spmm_sampled_rows_bit_exact(pg, orc, reddit):
         pg.backward_aggregation(prep.groups[i], yh, xh, overwrite=True)
         assert np.array_equal(bits(xh), bits(out.cpu().numpy())), f"host path {i}"
         # other pipeline shapes: source segments K, the last F of them in the chunked last pass
-        for ks, fs in ((4, 2), (3, 3), (5, 2)):
+        for ks, fs in ((3, 1), (4, 2), (3, 3), (5, 2)):
             pg.set_tuning("host_segs", ks)
             pg.set_tuning("host_final_segs", fs)
             try:
