@@ -219,9 +219,10 @@ int pg_backward_aggregate_rows(pg_groups G, uint32_t row_begin, uint32_t row_end
 /* Host-buffer drop-ins for DenseMatrix<float> callers (row-major, ld = cols):
  * copy in, run, copy out, synchronise. Pinned (cudaHostAlloc /
  * cudaHostRegister) buffers are DMA'd directly; pageable ones (a
- * std::vector) are staged through library-owned pinned slots by a few host
- * threads, overlapped with the copies (Reddit layer 0: 28.5 ms pinned,
- * ~33-40 ms pageable, vs ~105 ms for driver-staged pageable copies). */
+ * std::vector) are staged through library-owned pinned slots by host
+ * threads (all cores up to 16, $PG_STAGE_THREADS), overlapped with the
+ * copies (Reddit layer 0: ~26.5 ms pinned, ~31 ms pageable, vs ~105 ms for
+ * driver-staged pageable copies). */
 int pg_aggregate_pull_host(pg_groups G, const float* in_host, uint64_t in_rows, uint64_t dim,
                            float* out_host, unsigned flags, uint64_t* counters);
 int pg_backward_aggregate_host(pg_groups G, const float* y_host, uint64_t y_rows, uint64_t dim,

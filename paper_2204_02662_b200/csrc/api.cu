@@ -6,6 +6,7 @@
 #include <cmath>
 #include <condition_variable>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -446,7 +447,12 @@ Staging& staging(int device) {
             PG_CUDA(cudaEventCreateWithFlags(&st->down_ev[i], cudaEventDisableTiming));
         }
         const unsigned hc = std::max(1u, std::thread::hardware_concurrency());
-        st->pc = std::make_unique<ParallelCopy>(std::clamp(hc / 2, 1u, 8u));
+        // host copy threads: the calling thread is blocked in the call anyway;
+        // 12-16 of the box's 16 cores measured best (Reddit layer 0 31 ms vs
+        // 36 ms at 8, 41 ms at 4)
+        const char* e = std::getenv("PG_STAGE_THREADS");
+        const unsigned nt = e ? static_cast<unsigned>(std::max(1, std::atoi(e))) : std::clamp(hc, 1u, 16u);
+        st->pc = std::make_unique<ParallelCopy>(nt);
         per_dev[device] = std::move(st);
     }
     return *per_dev[device];
