@@ -36,7 +36,7 @@ constexpr TuneKey kTuneKeys[] = {
     {"heavy_tma", "PG_HEAVY_TMA", 0},      // heavy narrow rows: 1 = TMA bulk-copy mbarrier ring (k_agg_heavy)
     {"vec_u", "PG_VEC_U", 8},              // edges per gather batch in k_agg_vec4 (4, 8, 16)
     {"chunk_major", "PG_CHUNK_MAJOR", 1},  // k_agg_vec4 item order for multi-chunk rows
-    {"host_segs", "PG_HOST_SEGS", 6},      // host drop-in: source-row segments (H2D overlap)
+    {"host_segs", "PG_HOST_SEGS", 3},      // host drop-in: source-row segments (H2D overlap)
     {"host_chunks", "PG_HOST_CHUNKS", 16}, // host drop-in: row chunks of the last pass (D2H overlap)
     {"host_trace", "PG_HOST_TRACE", 0},    // host drop-in: print phase times to stderr
     {"heavy_narrow", "PG_HEAVY_NARROW", 0},  // heavy rows <= 64 floats: 1 = k_agg_narrow_lat, 0 = coop tiles
@@ -46,10 +46,11 @@ constexpr TuneKey kTuneKeys[] = {
     {"host_chunk_order", "PG_HOST_CHUNK_ORDER", 1},  // host drop-in last pass: 1 = last row chunk first
     {"grouped_seg", "PG_GROUPED_SEG", 0},  // grouped Fast: 1 = CTA-segmented reduction, 0 = an atomic per extra group
     {"heavy_wide_pipe", "PG_HEAVY_WIDE_PIPE", 1},  // heavy wide rows: 1 = software-pipelined k_agg_wide_pipe
-    {"host_final_segs", "PG_HOST_FINAL_SEGS", 3},  // host drop-in: trailing source segments of the chunked last pass
+    {"host_final_segs", "PG_HOST_FINAL_SEGS", 1},  // host drop-in: trailing source segments of the chunked last pass
     {"host_pass_smem", "PG_HOST_PASS_SMEM", 0},  // host drop-in: KB of idle smem per SpMM block in passes beside the H2D
     {"host_pitch2d", "PG_HOST_PITCH2D", 0},  // host drop-in: odd widths by 2-D DMA (1) or flat DMA + repack kernel (0)
     {"host_copy_prio", "PG_HOST_COPY_PRIO", 1},  // host drop-in: copy/repack streams at the highest priority (read once)
+    {"host_seg_balance", "PG_HOST_SEG_BALANCE", 1},  // host drop-in: source segments of equal rows (0) or equal edges (1)
 };
 std::atomic<int64_t> g_tune[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];
 int64_t g_tune_def[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];  // $PG_<KEY> at load, else built-in
@@ -1249,7 +1250,9 @@ __global__ void k_copy_rows(const float* __restrict__ src, uint64_t lds, float* 
                             uint64_t rows, uint32_t cols) {
     const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= cols) return;
-    for (uint64_t r = blockIdx.y; r < rows; r += gridDim.y) dst[r * ldd + c] = src[r * lds + c];
+    // evict-first loads and stores: the host pipeline repacks segments while
+    // the SpMM keeps its gather working set in L2
+    for (uint64_t r = blockIdx.y; r < rows; r += gridDim.y) __stcs(dst + r * ldd + c, __ldcs(src + r * lds + c));
 }
 
 __global__ void k_gather_rows(const float* __restrict__ src, uint64_t lds, const uint32_t* __restrict__ ids,

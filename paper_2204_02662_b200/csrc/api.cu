@@ -539,14 +539,35 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
     // next chunk); the K - F before it are whole-row passes under the H2D
     const uint32_t F = static_cast<uint32_t>(std::clamp<int64_t>(tuning(kTuneHostFinalSegs), 1, K));
     const bool trace = tuning(kTuneHostTrace) != 0;
-    std::vector<uint64_t> rcut(K + 1);
-    for (uint32_t k = 0; k <= K; ++k) rcut[k] = in_rows * k / K;
-    if (K > 1 && (G.host_seg_rows != in_rows || G.host_seg_k != K)) {
-        segment_bounds(G.path->offsets.get(), G.path->edges_parent.get(), static_cast<uint32_t>(D), rcut.data(), K,
+    // Source-row segments: equal rows, or (default) equal edges — frontier
+    // order puts the hubs first (RMAT, power-law graphs), so equal-row
+    // segments give the first pass most of the edges while only its small
+    // slice of rows has arrived
+    const int bal = K > 1 ? static_cast<int>(tuning(kTuneHostSegBalance) != 0) : 0;
+    if (K > 1 && (G.host_seg_rows != in_rows || G.host_seg_k != K || G.host_seg_bal != bal)) {
+        std::vector<uint64_t> rc(K + 1);
+        for (uint32_t k = 0; k <= K; ++k) rc[k] = in_rows * k / K;
+        if (bal) {
+            DevBuf<uint32_t> cnt(in_rows, s);
+            source_edge_counts(G.path->edges_parent.get(), b.E, in_rows, cnt.get(), s);
+            std::vector<uint32_t> hc(in_rows);
+            PG_CUDA(cudaMemcpyAsync(hc.data(), cnt.get(), in_rows * 4, cudaMemcpyDeviceToHost, s));
+            PG_CUDA(cudaStreamSynchronize(s));
+            uint64_t acc = 0, k = 1;
+            for (uint64_t r = 0; r < in_rows && k < K; ++r) {
+                acc += hc[r];
+                while (k < K && acc * K >= b.E * k) rc[k++] = r + 1;
+            }
+            for (uint32_t j = 1; j <= K; ++j) rc[j] = std::max(rc[j], rc[j - 1]);
+        }
+        segment_bounds(G.path->offsets.get(), G.path->edges_parent.get(), static_cast<uint32_t>(D), rc.data(), K,
                        G.host_seg_bnd, s);
+        G.host_seg_cuts = rc;
         G.host_seg_rows = in_rows;
         G.host_seg_k = K;
+        G.host_seg_bal = bal;
     }
+    std::vector<uint64_t> rcut = K > 1 ? G.host_seg_cuts : std::vector<uint64_t>{0, in_rows};
     std::vector<uint32_t> cuts{0, static_cast<uint32_t>(D)};
     if (R > 1) {
         if (G.host_chunks.size() != R + 1) {

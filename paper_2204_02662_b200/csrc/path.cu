@@ -491,6 +491,21 @@ void segment_bounds(const uint64_t* offsets, const Edge* edges, uint32_t D, cons
     PG_CUDA(cudaStreamSynchronize(s));
 }
 
+namespace {
+__global__ void k_src_counts(const Edge* __restrict__ edges, uint64_t E, uint32_t* __restrict__ counts) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < E;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        atomicAdd(counts + edges[i].x, 1u);
+}
+}  // namespace
+
+void source_edge_counts(const Edge* edges, uint64_t E, uint64_t P, uint32_t* counts, cudaStream_t s) {
+    if (P) PG_CUDA(cudaMemsetAsync(counts, 0, P * 4, s));
+    if (!E) return;
+    k_src_counts<<<148 * 16, kThreads, 0, s>>>(edges, E, counts);
+    PG_LAUNCH("k_src_counts");
+}
+
 void remap_edges(const Edge* in, uint64_t E, const uint32_t* map, Edge* out, cudaStream_t s) {
     if (E == 0) return;
     k_remap<<<grid_for(E, kThreads), kThreads, 0, s>>>(in, E, map, out);

@@ -137,6 +137,8 @@ struct Groups {
     DevBuf<uint64_t> host_seg_bnd;
     uint64_t host_seg_rows = 0;
     uint32_t host_seg_k = 0;
+    int host_seg_bal = -1;
+    std::vector<uint64_t> host_seg_cuts;  // source-row cuts of the host pipeline
     // automatic L2-sized source segments of a whole-path SpMM (api.cu)
     DevBuf<uint64_t> auto_seg_bnd;
     uint32_t auto_seg_k = 0;
@@ -149,6 +151,8 @@ void segment_bounds(const uint64_t* offsets, const Edge* edges, uint32_t D, cons
 
 // edges_out[e] = (map[edges_in[e].x], edges_in[e].y)
 void remap_edges(const Edge* in, uint64_t E, const uint32_t* map, Edge* out, cudaStream_t s);
+// per source row: number of path edges reading it (counts[P], zeroed here)
+void source_edge_counts(const Edge* edges, uint64_t E, uint64_t P, uint32_t* counts, cudaStream_t s);
 
 // ---- file formats (io.cu) ----
 struct EdgeListData {  // edge_list.hpp:14-18
@@ -253,7 +257,8 @@ enum TuneKeyId {
     kTuneHostFinalSegs = 13,
     kTuneHostPassSmem = 14,
     kTuneHostPitch2d = 15,
-    kTuneHostCopyPrio = 16
+    kTuneHostCopyPrio = 16,
+    kTuneHostSegBalance = 17
 };
 // idle dynamic smem (bytes) per k_agg_vec4 block for the launches of this
 // thread while set (host drop-in passes beside the H2D: fewer resident
