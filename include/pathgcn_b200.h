@@ -79,8 +79,11 @@ int pg_set_heavy_min_degree(uint64_t min_degree);
  * calls "host_segs" (source-row segments uploaded and reduced in turn, 1..8),
  * "host_chunks" (destination-row chunks of the last pass whose D2H overlaps
  * the next chunk, 1..16), "host_final_segs" (trailing source segments the
- * chunked last pass spans, 1..host_segs) and "host_trace" (1: phase times on
- * stderr). A negative value
+ * chunked last pass spans, 1..host_segs), "host_seg_balance" (1: segments of
+ * equal edge counts, 0: equal rows), "host_chunk_balance" (chunk cuts: %
+ * weight of edges vs rows), "host_copy_prio" (copy/repack streams at the
+ * highest priority), "host_pitch2d", "host_pass_smem" (measured slower,
+ * off) and "host_trace" (1: phase times on stderr). A negative value
  * restores the default ($PG_<KEY> at load, else built-in). Unknown key ->
  * PG_ERR_CONFIG. */
 int pg_set_tuning(const char* key, int64_t value);

@@ -37,7 +37,7 @@ constexpr TuneKey kTuneKeys[] = {
     {"vec_u", "PG_VEC_U", 8},              // edges per gather batch in k_agg_vec4 (4, 8, 16)
     {"chunk_major", "PG_CHUNK_MAJOR", 1},  // k_agg_vec4 item order for multi-chunk rows
     {"host_segs", "PG_HOST_SEGS", 3},      // host drop-in: source-row segments (H2D overlap)
-    {"host_chunks", "PG_HOST_CHUNKS", 16}, // host drop-in: row chunks of the last pass (D2H overlap)
+    {"host_chunks", "PG_HOST_CHUNKS", 8},  // host drop-in: row chunks of the last pass (D2H overlap)
     {"host_trace", "PG_HOST_TRACE", 0},    // host drop-in: print phase times to stderr
     {"heavy_narrow", "PG_HEAVY_NARROW", 0},  // heavy rows <= 64 floats: 1 = k_agg_narrow_lat, 0 = coop tiles
     {"wide_lpd", "PG_WIDE_LPD", 32},       // wide rows: lanes per (destination, chunk) item, 32 or 16
@@ -51,6 +51,7 @@ constexpr TuneKey kTuneKeys[] = {
     {"host_pitch2d", "PG_HOST_PITCH2D", 0},  // host drop-in: odd widths by 2-D DMA (1) or flat DMA + repack kernel (0)
     {"host_copy_prio", "PG_HOST_COPY_PRIO", 1},  // host drop-in: copy/repack streams at the highest priority (read once)
     {"host_seg_balance", "PG_HOST_SEG_BALANCE", 1},  // host drop-in: source segments of equal rows (0) or equal edges (1)
+    {"host_chunk_balance", "PG_HOST_CHUNK_BALANCE", 0},  // host drop-in: last-pass chunk cuts, % weight of edges vs rows
 };
 std::atomic<int64_t> g_tune[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];
 int64_t g_tune_def[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];  // $PG_<KEY> at load, else built-in

@@ -570,18 +570,26 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
     std::vector<uint64_t> rcut = K > 1 ? G.host_seg_cuts : std::vector<uint64_t>{0, in_rows};
     std::vector<uint32_t> cuts{0, static_cast<uint32_t>(D)};
     if (R > 1) {
-        if (G.host_chunks.size() != R + 1) {
+        // cut where alpha * (edges so far) + (1 - alpha) * (rows so far)
+        // crosses r / R: edge-balanced chunks (alpha = 1) isolate the hub
+        // rows (frontier order: hubs first) into tiny, latency-bound chunks
+        const int alpha = static_cast<int>(std::clamp<int64_t>(tuning(kTuneHostChunkBalance), 0, 100));
+        if (G.host_chunks.size() != R + 1 || G.host_chunk_alpha != alpha) {
             std::vector<uint64_t> off(D + 1);
             PG_CUDA(cudaMemcpyAsync(off.data(), G.path->offsets.get(), off.size() * 8, cudaMemcpyDeviceToHost, s));
             PG_CUDA(cudaStreamSynchronize(s));
             G.host_chunks.assign(1, 0);
+            const double E = std::max<double>(1.0, static_cast<double>(off[D]));
+            uint64_t row = 0;
             for (uint32_t r = 1; r < R; ++r) {
-                const uint64_t target = off[D] * r / R;
-                const uint32_t row =
-                    static_cast<uint32_t>(std::lower_bound(off.begin(), off.end() - 1, target) - off.begin());
-                G.host_chunks.push_back(std::max(G.host_chunks.back(), row));
+                const double target = static_cast<double>(r) / R;
+                while (row < D && (alpha * (off[row] / E) + (100 - alpha) * (static_cast<double>(row) / D)) / 100.0 <
+                                      target)
+                    ++row;
+                G.host_chunks.push_back(std::max(G.host_chunks.back(), static_cast<uint32_t>(row)));
             }
             G.host_chunks.push_back(static_cast<uint32_t>(D));
+            G.host_chunk_alpha = alpha;
         }
         cuts = G.host_chunks;
     }

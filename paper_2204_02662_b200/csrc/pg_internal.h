@@ -138,6 +138,7 @@ struct Groups {
     uint64_t host_seg_rows = 0;
     uint32_t host_seg_k = 0;
     int host_seg_bal = -1;
+    int host_chunk_alpha = -1;
     std::vector<uint64_t> host_seg_cuts;  // source-row cuts of the host pipeline
     // automatic L2-sized source segments of a whole-path SpMM (api.cu)
     DevBuf<uint64_t> auto_seg_bnd;
@@ -258,7 +259,8 @@ enum TuneKeyId {
     kTuneHostPassSmem = 14,
     kTuneHostPitch2d = 15,
     kTuneHostCopyPrio = 16,
-    kTuneHostSegBalance = 17
+    kTuneHostSegBalance = 17,
+    kTuneHostChunkBalance = 18
 };
 // idle dynamic smem (bytes) per k_agg_vec4 block for the launches of this
 // thread while set (host drop-in passes beside the H2D: fewer resident

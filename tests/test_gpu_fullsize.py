@@ -95,13 +95,15 @@ def test_fullsize_spmm_sampled_rows_bit_exact(pg, orc, reddit):
         pg.backward_aggregation(prep.groups[i], yh, xh, overwrite=True)
         assert np.array_equal(bits(xh), bits(out.cpu().numpy())), f"host path {i}"
         # other pipeline shapes: source segments K, the last F of them in the chunked last pass
-        for ks, fs in ((3, 1), (4, 2), (3, 3), (5, 2)):
-            pg.set_tuning("host_segs", ks)
-            pg.set_tuning("host_final_segs", fs)
+        # (segment balance: 1 equal edges / 0 equal rows; chunk cuts: % edges vs rows)
+        for ks, fs, sb, cb in ((3, 1, 0, 100), (4, 2, 1, 50), (3, 3, 1, 0), (5, 2, 0, 0), (6, 3, 1, 100)):
+            knobs = {"host_segs": ks, "host_final_segs": fs, "host_seg_balance": sb, "host_chunk_balance": cb}
+            for k, v in knobs.items():
+                pg.set_tuning(k, v)
             try:
                 xh[:] = np.nan
                 pg.backward_aggregation(prep.groups[i], yh, xh, overwrite=True)
-                assert np.array_equal(bits(xh), bits(out.cpu().numpy())), f"host path {i} K={ks} F={fs}"
+                assert np.array_equal(bits(xh), bits(out.cpu().numpy())), f"host path {i} {knobs}"
             finally:
-                pg.set_tuning("host_segs", None)
-                pg.set_tuning("host_final_segs", None)
+                for k in knobs:
+                    pg.set_tuning(k, None)
