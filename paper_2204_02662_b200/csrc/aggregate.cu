@@ -52,6 +52,7 @@ constexpr TuneKey kTuneKeys[] = {
     {"host_copy_prio", "PG_HOST_COPY_PRIO", 1},  // host drop-in: copy/repack streams at the highest priority (read once)
     {"host_seg_balance", "PG_HOST_SEG_BALANCE", 1},  // host drop-in: source segments of equal rows (0) or equal edges (1)
     {"host_chunk_balance", "PG_HOST_CHUNK_BALANCE", 0},  // host drop-in: last-pass chunk cuts, % weight of edges vs rows
+    {"atb_split", "PG_ATB_SPLIT", 1},  // W' GEMM: 1 = copy warp + chain warp, 0 = one warp does both
 };
 std::atomic<int64_t> g_tune[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];
 int64_t g_tune_def[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];  // $PG_<KEY> at load, else built-in

@@ -92,10 +92,11 @@ __global__ void __launch_bounds__(256) k_gemm(const float* __restrict__ a, uint6
 // which the final fl(acc + 0) does anyway.
 // Measured (Reddit shape): ~19 cycles per row per warp, i.e. 1.46 ms for
 // the top layer and 2.26 ms for layer 0, against 3.2 / 2.5 ms for the
-// earlier 128-thread block-owned kernel. Variants that split the roles
-// (copy warp + chain warp, producer warps + chain warp over named
-// barriers), re-laid the stages for LDS.128 operands, or went scalar with
-// one chain per lane all measured equal or slower; see DESIGN.md.
+// earlier 128-thread block-owned kernel. The copy-warp variant below
+// (k_gemm_at_b_split, the default) takes the copy issue off the chain
+// warp: ~11 cycles per row, 0.83 / 1.32 ms. Producer warps forming the
+// products, LDS.128 stage layouts, and scalar one-chain-per-lane kernels
+// measured equal or slower; see DESIGN.md.
 constexpr int kAtbStages = 8;
 
 template <int BYTES>
@@ -222,6 +223,133 @@ __global__ void __launch_bounds__(32) k_gemm_at_b_w(const float* __restrict__ a,
     if (i < r && j + 1 < c) out[i * ldo + j + 1] = __fadd_rn(hi, 0.f);
 }
 
+// Copy warp + chain warp variant (tuning "atb_split", default): warp 1
+// issues every cp.async of a 64-row stage (2 rows per lane, the same 16-byte
+// copies and id pipeline as above) and warp 0 only walks the chains
+// (LDS a + LDS.64 b + FFMA2 + FADD2 per row); kAtbSlots stage slots are
+// handed over with named barriers (FULL: copy warp waits for its group and
+// arrives; EMPTY: chain warp arrives after reading). 64-row stages keep
+// the barrier cost per row small.
+constexpr int kAtbSlots = 4, kAtbLag = 2, kAtbKC = 64;
+
+template <int TI>
+struct AtbSplitSmem {
+    static constexpr int TC = 64 / TI;
+    float sa[kAtbSlots][kAtbKC][TI];
+    float sb[kAtbSlots][kAtbKC][TC];
+    uint32_t sid[kAtbLag + 2][kAtbKC];
+};
+
+__device__ __forceinline__ void named_sync(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int count) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+template <int TI, int V>
+__global__ void __launch_bounds__(64) k_gemm_at_b_split(const float* __restrict__ a, uint64_t lda,
+                                                       const uint32_t* __restrict__ rows, const float* __restrict__ b,
+                                                       uint64_t ldb, float* __restrict__ out, uint64_t ldo,
+                                                       uint32_t n, uint32_t r, uint32_t c, float nz) {
+    using Sm = AtbSplitSmem<TI>;
+    constexpr int LPI = 32 / TI, TC = Sm::TC, KC = kAtbKC, SL = kAtbSlots, LAG = kAtbLag, NI = LAG + 2;
+    constexpr int AV = (V == 4 && TI % 4 == 0) ? 4 : 1;
+    constexpr int BV = V == 4 ? 4 : 1;
+    constexpr int NA = TI / AV, NB = TC / BV;
+    __shared__ __align__(16) Sm sm;
+    const unsigned lane = threadIdx.x & 31;
+    const uint32_t i0 = blockIdx.x * TI, j0 = blockIdx.y * TC;
+    const uint32_t ntiles = (n + KC - 1) / KC;
+    auto full_bar = [](uint32_t ts) { return 1 + static_cast<int>(ts % SL); };
+    auto empty_bar = [](uint32_t ts) { return 1 + SL + static_cast<int>(ts % SL); };
+    if (threadIdx.x < 32) {  // chain warp
+        const unsigned ti = lane / LPI, tj = (lane % LPI) * 2;
+        unsigned long long nz2, acc;
+        asm("mov.b64 %0, {%1,%1};" : "=l"(nz2) : "f"(nz));
+        asm("mov.b64 %0, {%1,%1};" : "=l"(acc) : "f"(0.f));
+        for (uint32_t ts = 0; ts < ntiles; ++ts) {
+            const int slot = ts % SL;
+            named_sync(full_bar(ts), 64);
+            const float* pa = &sm.sa[slot][0][ti];
+            const unsigned long long* pb = reinterpret_cast<const unsigned long long*>(&sm.sb[slot][0][tj]);
+#pragma unroll
+            for (int kk = 0; kk < KC; ++kk) {
+                unsigned long long aa, p;
+                asm("mov.b64 %0, {%1,%1};" : "=l"(aa) : "f"(pa[kk * TI]));
+                asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p) : "l"(aa), "l"(pb[kk * (TC / 2)]), "l"(nz2));
+                asm("add.rn.f32x2 %0, %1, %2;" : "=l"(acc) : "l"(acc), "l"(p));
+            }
+            named_arrive(empty_bar(ts), 64);
+        }
+        float lo, hi;
+        asm("mov.b64 {%0,%1}, %2;" : "=f"(lo), "=f"(hi) : "l"(acc));
+        const uint64_t i = i0 + ti, j = j0 + tj;
+        if (i < r && j < c) out[i * ldo + j] = __fadd_rn(lo, 0.f);
+        if (i < r && j + 1 < c) out[i * ldo + j + 1] = __fadd_rn(hi, 0.f);
+        return;
+    }
+    // copy warp: lane copies rows lane and lane + 32 of every stage
+    bool a_skip[NA], b_skip[NB];
+#pragma unroll
+    for (int q = 0; q < NA; ++q) a_skip[q] = i0 + q * AV >= r;
+#pragma unroll
+    for (int q = 0; q < NB; ++q) b_skip[q] = j0 + q * BV >= c;
+    const float* a_col = a + i0;
+    const uint64_t b_stage = static_cast<uint64_t>(KC) * ldb;
+    auto copy_row = [&](uint32_t ts, int slot, int kk, uint32_t id) {
+        const bool out_row = ts * KC + kk >= n;
+        const float* ar = out_row ? a : a_col + static_cast<uint64_t>(id) * lda;
+#pragma unroll
+        for (int q = 0; q < NA; ++q)
+            cp_async_skip<AV * 4>(&sm.sa[slot][kk][q * AV], ar + q * AV, a_skip[q] || out_row);
+        const float* br = out_row ? b : b + static_cast<uint64_t>(kk) * ldb + j0 + ts * b_stage;
+#pragma unroll
+        for (int q = 0; q < NB; ++q)
+            cp_async_skip<BV * 4>(&sm.sb[slot][kk][q * BV], br + q * BV, b_skip[q] || out_row);
+    };
+    auto fetch_id = [&](uint32_t ts, int kk) -> uint32_t {
+        const uint32_t k = ts * KC + kk;
+        return k < n ? (rows ? __ldg(rows + k) : k) : 0u;
+    };
+    for (uint32_t ts = 0; ts < ntiles + LAG; ++ts) {
+        if (ts < ntiles) {
+            if (ts >= static_cast<uint32_t>(SL)) named_sync(empty_bar(ts), 64);
+            const int slot = ts % SL;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int kk = lane + 32 * h;
+                uint32_t id;
+                if (!rows)
+                    id = ts * KC + kk;
+                else if (ts <= static_cast<uint32_t>(LAG))
+                    id = fetch_id(ts, kk);
+                else
+                    id = sm.sid[ts % NI][kk];
+                copy_row(ts, slot, kk, id);
+            }
+            if (rows) {  // ids of stage ts + LAG + 1 ride with this group
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int kk = lane + 32 * h;
+                    const uint32_t ka = (ts + LAG + 1) * KC + kk;
+                    const bool skip = ka >= n;
+                    cp_async_skip<4>(&sm.sid[(ts + LAG + 1) % NI][kk], skip ? rows : rows + ka, skip);
+                }
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        if (ts >= static_cast<uint32_t>(LAG)) {
+            asm volatile("cp.async.wait_group %0;" ::"n"(LAG) : "memory");
+            __syncwarp();
+            named_arrive(full_bar(ts - LAG), 64);
+        }
+    }
+    // match the chain warp's last EMPTY arrivals (no barrier left half-arrived)
+    for (uint32_t ts = ntiles > static_cast<uint32_t>(SL) ? ntiles : SL; ts < ntiles + SL; ++ts)
+        named_sync(empty_bar(ts), 64);
+}
+
 template <int TI>
 void launch_at_b(DMat a, const uint32_t* rows, DMat b, DMat out, uint64_t n, uint64_t r, uint64_t c,
                  cudaStream_t s) {
@@ -231,6 +359,14 @@ void launch_at_b(DMat a, const uint32_t* rows, DMat b, DMat out, uint64_t n, uin
                     reinterpret_cast<uintptr_t>(b.p) % 16 == 0;
     volatile float nz = -0.f;  // runtime -0: a literal lets ptxas fold the FFMA2 away
     const uint32_t n32 = static_cast<uint32_t>(n), r32 = static_cast<uint32_t>(r), c32 = static_cast<uint32_t>(c);
+    if (tuning(kTuneAtbSplit)) {
+        if (v4)
+            k_gemm_at_b_split<TI, 4><<<grid, 64, 0, s>>>(a.p, a.ld, rows, b.p, b.ld, out.p, out.ld, n32, r32, c32, nz);
+        else
+            k_gemm_at_b_split<TI, 1><<<grid, 64, 0, s>>>(a.p, a.ld, rows, b.p, b.ld, out.p, out.ld, n32, r32, c32, nz);
+        PG_LAUNCH("k_gemm_at_b_split");
+        return;
+    }
     if (v4)
         k_gemm_at_b_w<TI, 4><<<grid, 32, 0, s>>>(a.p, a.ld, rows, b.p, b.ld, out.p, out.ld, n32, r32, c32, nz);
     else

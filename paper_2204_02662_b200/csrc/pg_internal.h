@@ -260,7 +260,8 @@ enum TuneKeyId {
     kTuneHostPitch2d = 15,
     kTuneHostCopyPrio = 16,
     kTuneHostSegBalance = 17,
-    kTuneHostChunkBalance = 18
+    kTuneHostChunkBalance = 18,
+    kTuneAtbSplit = 19
 };
 // idle dynamic smem (bytes) per k_agg_vec4 block for the launches of this
 // thread while set (host drop-in passes beside the H2D: fewer resident

@@ -128,18 +128,30 @@ def test_dense_kernels(pg, orc, cuda):
         out = pg.empty_rows(n, m)
         pg.gemm(dev(torch, pg, a), dev(torch, pg, b), out)
         assert same(host(out), orc.gemm_f32(a, b))
-    for n, r_, c in ((1, 1, 1), (1000, 602, 16), (777, 16, 41), (5, 3, 2)):
-        a = rng.uniform(-1, 1, (n, r_)).astype(np.float32)
-        b = rng.uniform(-1, 1, (n, c)).astype(np.float32)
-        out = pg.empty_rows(r_, c)
-        pg.gemm_at_b(dev(torch, pg, a), dev(torch, pg, b), out)
-        assert same(host(out), orc.gemm_at_b_f32(a, b))
-        # fused row gather
-        big = rng.uniform(-1, 1, (n * 2, r_)).astype(np.float32)
-        rows = np.sort(rng.choice(n * 2, n, replace=False)).astype(np.int32)
-        out = pg.empty_rows(r_, c)
-        pg.gemm_at_b(dev(torch, pg, big), dev(torch, pg, b), out, a_rows=torch.from_numpy(rows).cuda())
-        assert same(host(out), orc.gemm_at_b_f32(big[rows], b))
+    # both W' kernels (copy warp + chain warp, one warp); n around the
+    # 64-row stage edges and the 4-slot ring; odd widths take the 4-byte copies
+    for split in (1, 0):
+        pg.set_tuning("atb_split", split)
+        try:
+            for n, r_, c in ((1, 1, 1), (1000, 602, 16), (777, 16, 41), (5, 3, 2), (64, 9, 7), (257, 8, 5),
+                             (4 * 64 + 1, 20, 33)):
+                a = rng.uniform(-1, 1, (n, r_)).astype(np.float32)
+                b = rng.uniform(-1, 1, (n, c)).astype(np.float32)
+                out = pg.empty_rows(r_, c)
+                pg.gemm_at_b(dev(torch, pg, a), dev(torch, pg, b), out)
+                assert same(host(out), orc.gemm_at_b_f32(a, b)), (split, n, r_, c)
+                # fused row gather
+                big = rng.uniform(-1, 1, (n * 2, r_)).astype(np.float32)
+                rows = np.sort(rng.choice(n * 2, n, replace=False)).astype(np.int32)
+                out = pg.empty_rows(r_, c)
+                pg.gemm_at_b(dev(torch, pg, big), dev(torch, pg, b), out, a_rows=torch.from_numpy(rows).cuda())
+                assert same(host(out), orc.gemm_at_b_f32(big[rows], b)), (split, n, r_, c)
+                # unpadded operands (ld = cols, rows not 16-byte aligned): the 4-byte copy path
+                out = pg.empty_rows(r_, c)
+                pg.gemm_at_b(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), out)
+                assert same(host(out), orc.gemm_at_b_f32(a, b)), ("unpadded", split, n, r_, c)
+        finally:
+            pg.set_tuning("atb_split", None)
     x = rng.uniform(-2, 2, (513, 47)).astype(np.float32)
     x[0, :3] = [0.0, -0.0, np.float32(1e-40)]
     out = pg.empty_rows(*x.shape)
