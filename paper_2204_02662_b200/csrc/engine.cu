@@ -232,9 +232,11 @@ __global__ void __launch_bounds__(32) k_gemm_at_b_w(const float* __restrict__ a,
 // the barrier cost per row small.
 constexpr int kAtbSlots = 4, kAtbLag = 2, kAtbKC = 64;
 
-template <int TI>
+// TI A columns x TC B columns per block; CH A columns per lane (CH = 2:
+// 128 chains per block for shapes with more chains than SMs)
+template <int TI, int CH>
 struct AtbSplitSmem {
-    static constexpr int TC = 64 / TI;
+    static constexpr int TC = 2 * 32 / (TI / CH);
     float sa[kAtbSlots][kAtbKC][TI];
     float sb[kAtbSlots][kAtbKC][TC];
     uint32_t sid[kAtbLag + 2][kAtbKC];
@@ -247,13 +249,13 @@ __device__ __forceinline__ void named_arrive(int id, int count) {
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
-template <int TI, int V>
+template <int TI, int V, int CH>
 __global__ void __launch_bounds__(64) k_gemm_at_b_split(const float* __restrict__ a, uint64_t lda,
                                                        const uint32_t* __restrict__ rows, const float* __restrict__ b,
                                                        uint64_t ldb, float* __restrict__ out, uint64_t ldo,
                                                        uint32_t n, uint32_t r, uint32_t c, float nz) {
-    using Sm = AtbSplitSmem<TI>;
-    constexpr int LPI = 32 / TI, TC = Sm::TC, KC = kAtbKC, SL = kAtbSlots, LAG = kAtbLag, NI = LAG + 2;
+    using Sm = AtbSplitSmem<TI, CH>;
+    constexpr int LPI = 32 / (TI / CH), TC = Sm::TC, KC = kAtbKC, SL = kAtbSlots, LAG = kAtbLag, NI = LAG + 2;
     constexpr int AV = (V == 4 && TI % 4 == 0) ? 4 : 1;
     constexpr int BV = V == 4 ? 4 : 1;
     constexpr int NA = TI / AV, NB = TC / BV;
@@ -263,11 +265,12 @@ __global__ void __launch_bounds__(64) k_gemm_at_b_split(const float* __restrict_
     const uint32_t ntiles = (n + KC - 1) / KC;
     auto full_bar = [](uint32_t ts) { return 1 + static_cast<int>(ts % SL); };
     auto empty_bar = [](uint32_t ts) { return 1 + SL + static_cast<int>(ts % SL); };
-    if (threadIdx.x < 32) {  // chain warp
-        const unsigned ti = lane / LPI, tj = (lane % LPI) * 2;
-        unsigned long long nz2, acc;
+    if (threadIdx.x < 32) {  // chain warp: A columns ti*CH .. +CH-1, B columns tj, tj+1
+        const unsigned ti = (lane / LPI) * CH, tj = (lane % LPI) * 2;
+        unsigned long long nz2, acc[CH];
         asm("mov.b64 %0, {%1,%1};" : "=l"(nz2) : "f"(nz));
-        asm("mov.b64 %0, {%1,%1};" : "=l"(acc) : "f"(0.f));
+#pragma unroll
+        for (int h = 0; h < CH; ++h) asm("mov.b64 %0, {%1,%1};" : "=l"(acc[h]) : "f"(0.f));
         for (uint32_t ts = 0; ts < ntiles; ++ts) {
             const int slot = ts % SL;
             named_sync(full_bar(ts), 64);
@@ -275,18 +278,33 @@ __global__ void __launch_bounds__(64) k_gemm_at_b_split(const float* __restrict_
             const unsigned long long* pb = reinterpret_cast<const unsigned long long*>(&sm.sb[slot][0][tj]);
 #pragma unroll
             for (int kk = 0; kk < KC; ++kk) {
-                unsigned long long aa, p;
-                asm("mov.b64 %0, {%1,%1};" : "=l"(aa) : "f"(pa[kk * TI]));
-                asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p) : "l"(aa), "l"(pb[kk * (TC / 2)]), "l"(nz2));
-                asm("add.rn.f32x2 %0, %1, %2;" : "=l"(acc) : "l"(acc), "l"(p));
+                float av[CH];
+                if (CH == 2) {
+                    const float2 a2 = *reinterpret_cast<const float2*>(pa + kk * TI);
+                    av[0] = a2.x;
+                    av[CH - 1] = a2.y;
+                } else {
+                    av[0] = pa[kk * TI];
+                }
+                const unsigned long long bb = pb[kk * (TC / 2)];
+#pragma unroll
+                for (int h = 0; h < CH; ++h) {
+                    unsigned long long aa, p;
+                    asm("mov.b64 %0, {%1,%1};" : "=l"(aa) : "f"(av[h]));
+                    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p) : "l"(aa), "l"(bb), "l"(nz2));
+                    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(acc[h]) : "l"(acc[h]), "l"(p));
+                }
             }
             named_arrive(empty_bar(ts), 64);
         }
-        float lo, hi;
-        asm("mov.b64 {%0,%1}, %2;" : "=f"(lo), "=f"(hi) : "l"(acc));
-        const uint64_t i = i0 + ti, j = j0 + tj;
-        if (i < r && j < c) out[i * ldo + j] = __fadd_rn(lo, 0.f);
-        if (i < r && j + 1 < c) out[i * ldo + j + 1] = __fadd_rn(hi, 0.f);
+#pragma unroll
+        for (int h = 0; h < CH; ++h) {
+            float lo, hi;
+            asm("mov.b64 {%0,%1}, %2;" : "=f"(lo), "=f"(hi) : "l"(acc[h]));
+            const uint64_t i = i0 + ti + h, j = j0 + tj;
+            if (i < r && j < c) out[i * ldo + j] = __fadd_rn(lo, 0.f);
+            if (i < r && j + 1 < c) out[i * ldo + j + 1] = __fadd_rn(hi, 0.f);
+        }
         return;
     }
     // copy warp: lane copies rows lane and lane + 32 of every stage
@@ -350,6 +368,13 @@ __global__ void __launch_bounds__(64) k_gemm_at_b_split(const float* __restrict_
         named_sync(empty_bar(ts), 64);
 }
 
+// one-column-per-lane blocks (64 chains each) beyond ~1.5 per SM: use 2
+bool gemm_at_b_chain_pairs(uint64_t r, uint64_t c) {
+    if (!tuning(kTuneAtbSplit) || tuning(kTuneAtbPairs) == 0) return false;
+    const uint64_t ti = c <= 8 ? 8 : 4, tc = 64 / ti;
+    return ((r + ti - 1) / ti) * ((c + tc - 1) / tc) > static_cast<uint64_t>(tuning(kTuneAtbPairs));
+}
+
 template <int TI>
 void launch_at_b(DMat a, const uint32_t* rows, DMat b, DMat out, uint64_t n, uint64_t r, uint64_t c,
                  cudaStream_t s) {
@@ -360,10 +385,22 @@ void launch_at_b(DMat a, const uint32_t* rows, DMat b, DMat out, uint64_t n, uin
     volatile float nz = -0.f;  // runtime -0: a literal lets ptxas fold the FFMA2 away
     const uint32_t n32 = static_cast<uint32_t>(n), r32 = static_cast<uint32_t>(r), c32 = static_cast<uint32_t>(c);
     if (tuning(kTuneAtbSplit)) {
-        if (v4)
-            k_gemm_at_b_split<TI, 4><<<grid, 64, 0, s>>>(a.p, a.ld, rows, b.p, b.ld, out.p, out.ld, n32, r32, c32, nz);
-        else
-            k_gemm_at_b_split<TI, 1><<<grid, 64, 0, s>>>(a.p, a.ld, rows, b.p, b.ld, out.p, out.ld, n32, r32, c32, nz);
+        // two A columns per lane once one-per-lane blocks outnumber the SMs
+        // ~1.5x: fewer chain warps sharing SMSPs (products layer 0: 400 -> 200)
+        if (gemm_at_b_chain_pairs(r, c)) {
+            constexpr int TI2 = 2 * TI;
+            dim3 g2(static_cast<unsigned>((r + TI2 - 1) / TI2), grid.y);
+            if (v4)
+                k_gemm_at_b_split<TI2, 4, 2><<<g2, 64, 0, s>>>(a.p, a.ld, rows, b.p, b.ld, out.p, out.ld, n32, r32, c32,
+                                                              nz);
+            else
+                k_gemm_at_b_split<TI2, 1, 2><<<g2, 64, 0, s>>>(a.p, a.ld, rows, b.p, b.ld, out.p, out.ld, n32, r32, c32,
+                                                              nz);
+        } else if (v4) {
+            k_gemm_at_b_split<TI, 4, 1><<<grid, 64, 0, s>>>(a.p, a.ld, rows, b.p, b.ld, out.p, out.ld, n32, r32, c32, nz);
+        } else {
+            k_gemm_at_b_split<TI, 1, 1><<<grid, 64, 0, s>>>(a.p, a.ld, rows, b.p, b.ld, out.p, out.ld, n32, r32, c32, nz);
+        }
         PG_LAUNCH("k_gemm_at_b_split");
         return;
     }
@@ -519,7 +556,7 @@ void gemm(DMat a, DMat b, DMat out, bool b_transposed, cudaStream_t s) {
 }
 
 uint64_t gemm_at_b_blocks(uint64_t r, uint64_t c) {
-    const uint64_t ti = c <= 8 ? 8 : 4, tc = 64 / ti;
+    const uint64_t ti = (c <= 8 ? 8 : 4) * (gemm_at_b_chain_pairs(r, c) ? 2 : 1), tc = c <= 8 ? 8 : 16;
     return ((r + ti - 1) / ti) * ((c + tc - 1) / tc);
 }
 

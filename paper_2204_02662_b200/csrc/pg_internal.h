@@ -261,7 +261,8 @@ enum TuneKeyId {
     kTuneHostCopyPrio = 16,
     kTuneHostSegBalance = 17,
     kTuneHostChunkBalance = 18,
-    kTuneAtbSplit = 19
+    kTuneAtbSplit = 19,
+    kTuneAtbPairs = 20
 };
 // idle dynamic smem (bytes) per k_agg_vec4 block for the launches of this
 // thread while set (host drop-in passes beside the H2D: fewer resident

@@ -130,8 +130,9 @@ def test_dense_kernels(pg, orc, cuda):
         assert same(host(out), orc.gemm_f32(a, b))
     # both W' kernels (copy warp + chain warp, one warp); n around the
     # 64-row stage edges and the 4-slot ring; odd widths take the 4-byte copies
-    for split in (1, 0):
+    for split, pairs in ((1, None), (0, None), (1, 1)):  # (1, 1): two A columns per lane everywhere
         pg.set_tuning("atb_split", split)
+        pg.set_tuning("atb_pairs", pairs)
         try:
             for n, r_, c in ((1, 1, 1), (1000, 602, 16), (777, 16, 41), (5, 3, 2), (64, 9, 7), (257, 8, 5),
                              (4 * 64 + 1, 20, 33)):
@@ -152,6 +153,7 @@ def test_dense_kernels(pg, orc, cuda):
                 assert same(host(out), orc.gemm_at_b_f32(a, b)), ("unpadded", split, n, r_, c)
         finally:
             pg.set_tuning("atb_split", None)
+            pg.set_tuning("atb_pairs", None)
     x = rng.uniform(-2, 2, (513, 47)).astype(np.float32)
     x[0, :3] = [0.0, -0.0, np.float32(1e-40)]
     out = pg.empty_rows(*x.shape)
