@@ -75,6 +75,83 @@ __global__ void __launch_bounds__(256) k_gemm(const float* __restrict__ a, uint6
     }
 }
 
+// Packed variant (the one dispatched): a lane owns two adjacent output
+// columns, so each chain step of a row is half an FFMA2 (runtime -0 addend:
+// exactly fl(a*b)) + half an FADD2; the A values come 4 k at a time (one
+// broadcast LDS.128), the B pairs once per k for all 16 rows of the warp.
+// 128 x 64 output tiles, K in chunks of 32 through shared memory; the same
+// ascending-k chain per output as k_gemm, bit for bit.
+constexpr int kG2J = 64;
+
+template <bool BT>
+__global__ void __launch_bounds__(256) k_gemm2(const float* __restrict__ a, uint64_t lda,
+                                               const float* __restrict__ b, uint64_t ldb, float* __restrict__ out,
+                                               uint64_t ldo, uint64_t n, uint64_t m, uint64_t K, float nz) {
+    __shared__ __align__(16) float as[kGI][kGT];
+    __shared__ __align__(16) float bs[kGT][kG2J];
+    const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint64_t j0 = blockIdx.y * static_cast<uint64_t>(kG2J);
+    const uint64_t i0 = blockIdx.x * static_cast<uint64_t>(kGI);
+    unsigned long long nz2, acc[kGRPW];
+    asm("mov.b64 %0, {%1,%1};" : "=l"(nz2) : "f"(nz));
+#pragma unroll
+    for (int r = 0; r < kGRPW; ++r) asm("mov.b64 %0, {%1,%1};" : "=l"(acc[r]) : "f"(0.f));
+    for (uint64_t k0 = 0; k0 < K; k0 += kGT) {
+        const int kc = static_cast<int>(K - k0 < kGT ? K - k0 : kGT);
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < kGI * kGT; idx += 256) {
+            const int r = idx / kGT, kk = idx % kGT;
+            as[r][kk] = (i0 + r < n && kk < kc) ? a[(i0 + r) * lda + k0 + kk] : 0.f;
+        }
+        for (int idx = threadIdx.x; idx < kGT * kG2J; idx += 256) {
+            int kk, jj;
+            if (BT) {  // b[j][k]: consecutive threads walk k
+                kk = idx % kGT;
+                jj = idx / kGT;
+            } else {
+                kk = idx / kG2J;
+                jj = idx % kG2J;
+            }
+            const uint64_t jg = j0 + jj;
+            float v = 0.f;
+            if (kk < kc && jg < m) v = BT ? b[jg * ldb + k0 + kk] : b[(k0 + kk) * ldb + jg];
+            bs[kk][jj] = v;
+        }
+        __syncthreads();
+        // zero-padded k (kk >= kc) and rows/columns past the matrix add +0
+        // products after the real ones: only a -0 chain can change (to +0),
+        // which the final fl(acc + 0) does anyway
+        for (int kq = 0; kq < (kc + 3) / 4; ++kq) {
+            unsigned long long bp[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) bp[u] = *reinterpret_cast<const unsigned long long*>(&bs[4 * kq + u][2 * lane]);
+#pragma unroll
+            for (int r = 0; r < kGRPW; ++r) {
+                const float4 a4 = *reinterpret_cast<const float4*>(&as[w * kGRPW + r][4 * kq]);
+                const float av[4] = {a4.x, a4.y, a4.z, a4.w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    unsigned long long aa, p;
+                    asm("mov.b64 %0, {%1,%1};" : "=l"(aa) : "f"(av[u]));
+                    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p) : "l"(aa), "l"(bp[u]), "l"(nz2));
+                    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(acc[r]) : "l"(acc[r]), "l"(p));
+                }
+            }
+        }
+    }
+    const uint64_t j = j0 + 2 * lane;
+    if (j >= m) return;
+#pragma unroll
+    for (int r = 0; r < kGRPW; ++r) {
+        const uint64_t i = i0 + w * kGRPW + r;
+        if (i >= n) continue;
+        float lo, hi;
+        asm("mov.b64 {%0,%1}, %2;" : "=f"(lo), "=f"(hi) : "l"(acc[r]));
+        out[i * ldo + j] = __fadd_rn(lo, 0.f);
+        if (j + 1 < m) out[i * ldo + j + 1] = __fadd_rn(hi, 0.f);
+    }
+}
+
 // ---- out = A[rows]^T * B (dense_matrix.hpp:57-76 gemm_at_b) -----------------
 // out[i][j] = sum over k < n, ascending, of A(k, i) * B(k, j), A(k, i) =
 // a[(rows ? rows[k] : k) * lda + i] (the engine's gather_rows fused in).
@@ -545,6 +622,16 @@ void gemm(DMat a, DMat b, DMat out, bool b_transposed, cudaStream_t s) {
     if (n == 0 || m == 0) return;
     if (K == 0) {
         PG_CUDA(cudaMemset2DAsync(out.p, out.ld * 4, 0, m * 4, n, s));
+        return;
+    }
+    if (tuning(kTuneGemmPacked)) {
+        dim3 grid(static_cast<unsigned>((n + kGI - 1) / kGI), static_cast<unsigned>((m + kG2J - 1) / kG2J));
+        volatile float nz = -0.f;  // runtime -0: a literal lets ptxas fold the FFMA2 away
+        if (b_transposed)
+            k_gemm2<true><<<grid, 256, 0, s>>>(a.p, a.ld, b.p, b.ld, out.p, out.ld, n, m, K, nz);
+        else
+            k_gemm2<false><<<grid, 256, 0, s>>>(a.p, a.ld, b.p, b.ld, out.p, out.ld, n, m, K, nz);
+        PG_LAUNCH("k_gemm2");
         return;
     }
     dim3 grid(static_cast<unsigned>((n + kGI - 1) / kGI), static_cast<unsigned>((m + kGT - 1) / kGT));

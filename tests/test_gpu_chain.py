@@ -122,12 +122,23 @@ def test_dense_kernels(pg, orc, cuda):
     import torch
 
     rng = np.random.default_rng(5)
-    for n, k, m in ((1, 1, 1), (37, 602, 16), (300, 16, 41), (65, 33, 130)):
-        a = rng.uniform(-1, 1, (n, k)).astype(np.float32)
-        b = rng.uniform(-1, 1, (k, m)).astype(np.float32)
-        out = pg.empty_rows(n, m)
-        pg.gemm(dev(torch, pg, a), dev(torch, pg, b), out)
-        assert same(host(out), orc.gemm_f32(a, b))
+    for packed in (1, 0):  # k_gemm2 (FFMA2/FADD2 column pairs) and k_gemm
+        pg.set_tuning("gemm_packed", packed)
+        try:
+            for n, k, m in ((1, 1, 1), (37, 602, 16), (300, 16, 41), (65, 33, 130), (129, 35, 63), (200, 7, 100)):
+                a = rng.uniform(-1, 1, (n, k)).astype(np.float32)
+                b = rng.uniform(-1, 1, (k, m)).astype(np.float32)
+                a[0, : min(2, k)] = [0.0, -0.0][: min(2, k)]
+                out = pg.empty_rows(n, m)
+                pg.gemm(dev(torch, pg, a), dev(torch, pg, b), out)
+                assert same(host(out), orc.gemm_f32(a, b)), (packed, n, k, m)
+                # op(B) = B^T (gemm_a_bt), unpadded operands
+                bt = np.ascontiguousarray(b.T)
+                out = pg.empty_rows(n, m)
+                pg.gemm_a_bt(torch.from_numpy(a).cuda(), torch.from_numpy(bt).cuda(), out)
+                assert same(host(out), orc.gemm_f32(a, b)), ("a_bt", packed, n, k, m)
+        finally:
+            pg.set_tuning("gemm_packed", None)
     # both W' kernels (copy warp + chain warp, one warp); n around the
     # 64-row stage edges and the 4-slot ring; odd widths take the 4-byte copies
     for split, pairs in ((1, None), (0, None), (1, 1)):  # (1, 1): two A columns per lane everywhere
