@@ -125,7 +125,8 @@ def test_dense_kernels(pg, orc, cuda):
     for packed in (1, 0):  # k_gemm2 (FFMA2/FADD2 column pairs) and k_gemm
         pg.set_tuning("gemm_packed", packed)
         try:
-            for n, k, m in ((1, 1, 1), (37, 602, 16), (300, 16, 41), (65, 33, 130), (129, 35, 63), (200, 7, 100)):
+            for n, k, m in ((1, 1, 1), (37, 602, 16), (300, 16, 41), (65, 33, 130), (129, 35, 63), (200, 7, 100),
+                            (70, 5, 33)):
                 a = rng.uniform(-1, 1, (n, k)).astype(np.float32)
                 b = rng.uniform(-1, 1, (k, m)).astype(np.float32)
                 a[0, : min(2, k)] = [0.0, -0.0][: min(2, k)]
