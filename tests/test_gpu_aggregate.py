@@ -464,3 +464,32 @@ def test_host_drop_in_concurrent_threads(pg, orc):
     for t in ts:
         t.join()
     assert not errors, errors
+
+
+def test_degenerate_shapes(pg, orc):
+    """Empty paths (an isolated training vertex: no edges), zero-width
+    rows, and the host-buffer calls on them: no launch failures, outputs
+    as the reference leaves them (overwrite -> +0 rows, accumulate ->
+    unchanged), counters zero."""
+    torch = torch_mod()
+    pairs = np.array([[0, 1]], np.uint32)
+    vt = np.array([2], np.uint32)  # vertex 2 is isolated
+    og, dg, F, ops, dps = build_all(pg, orc, pairs, 3, vt, 2)
+    for dp, op in zip(dps, ops):
+        assert dp.E == op.E == 0
+        G = pg.group_neighbors(dp, 1)
+        for dim in (0, 5, 16):
+            y = np.ones((dp.P, dim), np.float32)
+            x = np.full((dp.D, dim), 7.0, np.float32)
+            pg.backward_aggregation(G, y, x)  # accumulate: nothing to add
+            assert (x == 7.0).all()
+            pg.backward_aggregation(G, y, x, overwrite=True)
+            assert np.array_equal(bits(x), bits(np.zeros_like(x)))
+            if dp.P and dp.D and dim:
+                yd = to_dev(y, pg.padded_ld(dim))
+                xd = pg.empty_rows(dp.D, dim)
+                xd.fill_(3.0)
+                pg.backward_aggregation(G, yd, xd, overwrite=True)
+                torch.cuda.synchronize()
+                assert (xd.cpu().numpy() == 0).all()
+        assert all(int(v) == 0 for v in G.counters(16).values())
