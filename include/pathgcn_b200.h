@@ -80,7 +80,8 @@ int pg_set_heavy_min_degree(uint64_t min_degree);
  * "host_chunks" (destination-row chunks of the last pass whose D2H overlaps
  * the next chunk, 1..16), "host_final_segs" (trailing source segments the
  * chunked last pass spans, 1..host_segs), "host_seg_balance" (1: segments of
- * equal edge counts, 0: equal rows), "host_chunk_balance" (chunk cuts: %
+ * equal edge counts, 0: equal rows), "host_last_seg_pct" (% of the edges in
+ * the last, chunked segment; 0 = 1/K), "host_chunk_balance" (chunk cuts: %
  * weight of edges vs rows), "host_copy_prio" (copy/repack streams at the
  * highest priority), "host_pitch2d", "host_pass_smem" (measured slower,
  * off) and "host_trace" (1: phase times on stderr). A negative value

@@ -544,7 +544,8 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
     // segments give the first pass most of the edges while only its small
     // slice of rows has arrived
     const int bal = K > 1 ? static_cast<int>(tuning(kTuneHostSegBalance) != 0) : 0;
-    if (K > 1 && (G.host_seg_rows != in_rows || G.host_seg_k != K || G.host_seg_bal != bal)) {
+    const int bal_key = bal ? 1 + static_cast<int>(tuning(kTuneHostLastSegPct)) : 0;
+    if (K > 1 && (G.host_seg_rows != in_rows || G.host_seg_k != K || G.host_seg_bal != bal_key)) {
         std::vector<uint64_t> rc(K + 1);
         for (uint32_t k = 0; k <= K; ++k) rc[k] = in_rows * k / K;
         if (bal) {
@@ -553,10 +554,16 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
             std::vector<uint32_t> hc(in_rows);
             PG_CUDA(cudaMemcpyAsync(hc.data(), cnt.get(), in_rows * 4, cudaMemcpyDeviceToHost, s));
             PG_CUDA(cudaStreamSynchronize(s));
+            // edge fraction of the last segment (host_last_seg_pct, 0 = 1/K);
+            // the first K-1 share the rest equally
+            const int64_t pct = tuning(kTuneHostLastSegPct);
+            const double last = pct > 0 ? std::clamp<double>(pct / 100.0, 0.01, 0.99) : 1.0 / K;
+            std::vector<double> tgt(K);
+            for (uint32_t j = 1; j < K; ++j) tgt[j] = (1.0 - last) * j / (K - 1) * static_cast<double>(b.E);
             uint64_t acc = 0, k = 1;
             for (uint64_t r = 0; r < in_rows && k < K; ++r) {
                 acc += hc[r];
-                while (k < K && acc * K >= b.E * k) rc[k++] = r + 1;
+                while (k < K && static_cast<double>(acc) >= tgt[k]) rc[k++] = r + 1;
             }
             for (uint32_t j = 1; j <= K; ++j) rc[j] = std::max(rc[j], rc[j - 1]);
         }
@@ -565,7 +572,7 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
         G.host_seg_cuts = rc;
         G.host_seg_rows = in_rows;
         G.host_seg_k = K;
-        G.host_seg_bal = bal;
+        G.host_seg_bal = bal_key;
     }
     std::vector<uint64_t> rcut = K > 1 ? G.host_seg_cuts : std::vector<uint64_t>{0, in_rows};
     std::vector<uint32_t> cuts{0, static_cast<uint32_t>(D)};

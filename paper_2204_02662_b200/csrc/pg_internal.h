@@ -263,7 +263,8 @@ enum TuneKeyId {
     kTuneHostChunkBalance = 18,
     kTuneAtbSplit = 19,
     kTuneAtbPairs = 20,
-    kTuneGemmPacked = 21
+    kTuneGemmPacked = 21,
+    kTuneHostLastSegPct = 22
 };
 // idle dynamic smem (bytes) per k_agg_vec4 block for the launches of this
 // thread while set (host drop-in passes beside the H2D: fewer resident
