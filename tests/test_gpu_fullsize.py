@@ -96,8 +96,10 @@ def test_fullsize_spmm_sampled_rows_bit_exact(pg, orc, reddit):
         assert np.array_equal(bits(xh), bits(out.cpu().numpy())), f"host path {i}"
         # other pipeline shapes: source segments K, the last F of them in the chunked last pass
         # (segment balance: 1 equal edges / 0 equal rows; chunk cuts: % edges vs rows)
-        for ks, fs, sb, cb in ((3, 1, 0, 100), (4, 2, 1, 50), (3, 3, 1, 0), (5, 2, 0, 0), (6, 3, 1, 100)):
-            knobs = {"host_segs": ks, "host_final_segs": fs, "host_seg_balance": sb, "host_chunk_balance": cb}
+        for ks, fs, sb, cb, lp in ((3, 1, 0, 100, 0), (4, 2, 1, 50, 0), (3, 3, 1, 0, 40), (5, 2, 0, 0, 40),
+                                   (6, 3, 1, 100, 55), (2, 1, 1, 0, 70)):
+            knobs = {"host_segs": ks, "host_final_segs": fs, "host_seg_balance": sb, "host_chunk_balance": cb,
+                     "host_last_seg_pct": lp}
             for k, v in knobs.items():
                 pg.set_tuning(k, v)
             try:
