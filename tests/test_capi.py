@@ -79,3 +79,25 @@ def test_tuning_keys(pg):
 
     with pytest.raises(pg.ConfigError):
         pg.set_tuning("no_such_knob", 1)
+
+
+def test_compute_fails_loudly_without_gpu(pg):
+    """No CPU fallback: on a machine without a usable GPU every compute entry
+    point raises DeviceError (status 5) instead of computing on the host."""
+    import numpy as np
+    import pytest
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(pg.DeviceError):
+        pg.build_undirected_csr(np.array([[0, 1], [1, 2]], np.uint32))
+    lib = _lib.load()
+    out = C.c_void_p()
+    offs = np.array([0, 1, 2], np.uint64)
+    nbrs = np.array([1, 0], np.uint32)
+    w = np.ones(2, np.float64)
+    rc = lib.pg_graph_create(0, 2, offs.ctypes.data_as(C.POINTER(C.c_uint64)),
+                             nbrs.ctypes.data_as(C.POINTER(C.c_uint32)),
+                             w.ctypes.data_as(C.POINTER(C.c_double)), 0, C.byref(out))
+    assert rc == 5
