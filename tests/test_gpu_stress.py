@@ -1,0 +1,75 @@
+"""Randomised parity sweep of the backward-aggregation stage: random RMAT
+graphs, training fractions, widths (odd, 16-byte, wide, multi-chunk) and
+scheduling knobs (gather batch, item order, L1/L2 loads, heavy-kernel
+routing and threshold, source segments), through the device call, a row
+range, and the host-buffer drop-in. Every output row bit-exact with the
+fp32 oracle (aggregate_pull<float> Deterministic over the same path)."""
+import numpy as np
+import pytest
+
+from conftest import rmat_pairs
+
+pytestmark = pytest.mark.gpu
+
+WIDTHS = (1, 3, 16, 17, 41, 64, 100, 128, 129, 300, 602)
+KNOBS = {
+    "vec_u": (4, 8, 16),
+    "chunk_major": (0, 1),
+    "ld_cg": (0, 2),
+    "heavy_narrow": (0, 1),
+    "heavy_wide_pipe": (0, 1),
+    "wide_lpd": (16, 32),
+    "src_segs": (0, 1, 2, 3),
+    "heavy_tma": (0, 1),
+}
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+@pytest.mark.parametrize("seed", range(32))
+def test_random_stage_parity(pg, orc, seed):
+    import torch
+
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.integers(300, 6000))
+    deg = int(rng.choice([2, 6, 24, 64]))
+    pairs, n_pad = rmat_pairs(orc, n, n * deg, 50 + seed)
+    vt = orc.sample_training_set(n_pad, float(rng.choice([0.01, 0.1, 0.5, 1.0])), seed)
+    L = int(rng.integers(1, 4))
+    dg = pg.build_undirected_csr(pairs, n_hint=n_pad, weights="symnorm" if seed % 3 else "unit")
+    og = orc.build_graph(pairs, n_hint=n_pad, symnorm=bool(seed % 3))
+    F = pg.compute_frontiers(dg, vt, L)
+    ops = orc.prepare_all_paths(og, orc.compute_frontiers(og, vt, L))
+    dps = pg.prepare_all_paths(dg, F)
+    knobs = {k: int(rng.choice(v)) for k, v in KNOBS.items()}
+    hmin = [None, 0, 8, 64, 1024][int(rng.integers(0, 5))]
+    try:
+        for k, v in knobs.items():
+            pg.set_tuning(k, v)
+        pg.set_heavy_min_degree(hmin)
+        for dp, op in zip(dps, ops):
+            dim = int(rng.choice(WIDTHS))
+            G = pg.group_neighbors(dp, int(rng.integers(1, 9)))
+            y = rng.uniform(-1, 1, size=(dp.P, dim)).astype(np.float32)
+            want = orc.aggregate_pull_f32(op.offsets, op.neighbors, op.weights, y[op.srcpos])
+            yd = pg.empty_rows(dp.P, dim)
+            yd.copy_(torch.from_numpy(y))
+            xd = pg.empty_rows(dp.D, dim)
+            pg.backward_aggregation(G, yd, xd, overwrite=True)
+            torch.cuda.synchronize()
+            assert np.array_equal(bits(xd.cpu().numpy()), bits(want)), (seed, dim, knobs, hmin)
+            if dp.D > 2:  # a row range of the same path
+                b, e = sorted(int(v) for v in rng.integers(0, dp.D + 1, size=2))
+                xr = pg.empty_rows(e - b, dim)
+                pg.backward_aggregation(G, yd, xr, overwrite=True, rows=(b, e))
+                torch.cuda.synchronize()
+                assert np.array_equal(bits(xr.cpu().numpy()), bits(want[b:e])), (seed, dim, "rows", b, e)
+            xh = np.full((dp.D, dim), np.nan, np.float32)  # host-buffer drop-in
+            pg.backward_aggregation(G, y, xh, overwrite=True)
+            assert np.array_equal(bits(xh), bits(want)), (seed, dim, "host")
+    finally:
+        for k in knobs:
+            pg.set_tuning(k, None)
+        pg.set_heavy_min_degree(None)
