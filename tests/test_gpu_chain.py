@@ -228,3 +228,41 @@ def test_filtered_unaligned_rows_scalar_path(pg, orc, cuda):
     sa[levels[1]] = 1
     want, wc = orc.aggregate_pull_filtered_f32(g_o.offsets, g_o.neighbors, g_o.weights, y, da, sa, 4)
     assert same(host(out), want) and c == wc
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_chains(pg, orc, cuda, seed):
+    """Random depths / widths / training fractions, knob settings of the
+    chain GEMMs (W' copy-warp or one-warp kernel, two A columns per lane,
+    packed or scalar y_grad GEMM): forward + every backward variant's W'
+    bit-exact with the oracle's composition of the reference."""
+    import torch
+
+    rng = np.random.default_rng(77 + seed)
+    L = int(rng.integers(1, 4))
+    f, hidden, classes = (int(rng.choice(v)) for v in ((3, 17, 64, 130), (4, 16, 33), (2, 7, 41)))
+    hidden = hidden if L > 1 else 0
+    n_req = int(rng.integers(200, 3000))
+    case = (n_req, n_req * int(rng.choice([3, 8, 20])), 90 + seed, float(rng.choice([0.05, 0.3, 1.0])), L, f,
+            hidden, classes, bool(seed % 2))
+    knobs = {"atb_split": int(rng.integers(0, 2)), "atb_pairs": int(rng.choice([1, 224])),
+             "gemm_packed": int(rng.integers(0, 2))}
+    try:
+        for k, v in knobs.items():
+            pg.set_tuning(k, v)
+        g_o, vt, x0, ws, r, g, Gg, prep, d = gpu_setup(pg, orc, case)
+        arts = pg.forward(Gg, d["x0"], d["ws"])
+        top = pg.empty_rows(g.n, ws[-1].shape[1])
+        pg.top_grad_from_probs(arts.x[-1], d["r"], d["vt"], top)
+        for mode in (0, 2, 3):
+            if mode == 0:
+                wg = pg.backward_all_active(Gg, arts, top, d["ws"])
+            else:
+                wg = pg.backward_epp(prep, arts, top, d["ws"], gather="local" if mode == 2 else "global")
+            torch.cuda.synchronize()
+            _, _, want_wg, _, _ = oracle_chain(orc, g_o, vt, x0, ws, r, mode)
+            for l in range(L):
+                assert same(host(wg[l]), want_wg[l]), (seed, mode, l, knobs, case)
+    finally:
+        for k in knobs:
+            pg.set_tuning(k, None)
