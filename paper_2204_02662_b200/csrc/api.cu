@@ -391,7 +391,7 @@ public:
 
 private:
     void part(unsigned t) {
-        const size_t per = (n_ / nthreads_ + 63) & ~size_t(63);
+        const size_t per = ((n_ + nthreads_ - 1) / nthreads_ + 63) & ~size_t(63);  // ceil: parts cover all n_ bytes
         const size_t b = std::min(n_, per * t), e = std::min(n_, per * (t + 1));
         if (e > b) std::memcpy(dst_ + b, src_ + b, e - b);
     }

@@ -4,6 +4,8 @@ scheduling knobs (gather batch, item order, L1/L2 loads, heavy-kernel
 routing and threshold, source segments), through the device call, a row
 range, and the host-buffer drop-in. Every output row bit-exact with the
 fp32 oracle (aggregate_pull<float> Deterministic over the same path)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -28,7 +30,9 @@ def bits(a):
     return np.ascontiguousarray(a, np.float32).view(np.uint32)
 
 
-@pytest.mark.parametrize("seed", range(32))
+# 240 / 384 / 540 caught a pageable-staging bug (a host copy split across
+# 16 threads dropped the last n % 16 bytes when n / 16 was a multiple of 64)
+@pytest.mark.parametrize("seed", sorted(set(range(int(os.environ.get("PG_STRESS_SEEDS", "64")))) | {240, 384, 540}))
 def test_random_stage_parity(pg, orc, seed):
     import torch
 
