@@ -77,3 +77,53 @@ def test_random_stage_parity(pg, orc, seed):
         for k in knobs:
             pg.set_tuning(k, None)
         pg.set_heavy_min_degree(None)
+
+
+HOST_KNOBS = {
+    "host_segs": (1, 2, 3, 4, 6),
+    "host_final_segs": (1, 2, 3),
+    "host_seg_balance": (0, 1),
+    "host_chunk_balance": (0, 50, 100),
+    "host_last_seg_pct": (0, 30, 40, 70),
+    "host_chunks": (1, 3, 8, 16),
+    "host_chunk_order": (0, 1),
+}
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("PG_STRESS_HOST_SEEDS", "6"))))
+def test_random_host_pipeline(pg, orc, seed):
+    """The host-buffer pipeline (source segments under the H2D, chunked last
+    pass under the D2H) on paths big enough to engage it, with random
+    pipeline knobs, pinned or pageable buffers, overwrite or accumulate."""
+    import torch
+
+    rng = np.random.default_rng(5000 + seed)
+    n = int(rng.integers(20000, 40000))
+    pairs, n_pad = rmat_pairs(orc, n, n * 56, 70 + seed)
+    vt = orc.sample_training_set(n_pad, 0.5, seed)
+    dg = pg.build_undirected_csr(pairs, n_hint=n_pad, weights="symnorm")
+    og = orc.build_graph(pairs, n_hint=n_pad, symnorm=True)
+    F = pg.compute_frontiers(dg, vt, 2)
+    ops = orc.prepare_all_paths(og, orc.compute_frontiers(og, vt, 2))
+    dp, op = pg.prepare_all_paths(dg, F)[1], ops[1]
+    dim = int(rng.choice([301, 302, 320]))
+    knobs = {k: int(rng.choice(v)) for k, v in HOST_KNOBS.items()}
+    try:
+        for k, v in knobs.items():
+            pg.set_tuning(k, v)
+        G = pg.group_neighbors(dp, 4)
+        y = rng.uniform(-1, 1, size=(dp.P, dim)).astype(np.float32)
+        base = rng.uniform(-1, 1, size=(dp.D, dim)).astype(np.float32)
+        accumulate = bool(rng.integers(0, 2))
+        want = orc.aggregate_pull_f32(op.offsets, op.neighbors, op.weights, y[op.srcpos],
+                                      out=base.copy() if accumulate else None)
+        pinned = bool(rng.integers(0, 2))
+        yh = torch.from_numpy(y).pin_memory().numpy() if pinned else y
+        xh = base.copy() if accumulate else np.full((dp.D, dim), np.nan, np.float32)
+        if pinned:
+            xh = torch.from_numpy(xh).pin_memory().numpy()
+        pg.backward_aggregation(G, yh, xh, overwrite=not accumulate)
+        assert np.array_equal(bits(xh), bits(want)), (seed, dim, knobs, pinned, accumulate, dp.D, dp.E)
+    finally:
+        for k in knobs:
+            pg.set_tuning(k, None)
