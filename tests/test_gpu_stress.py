@@ -127,3 +127,42 @@ def test_random_host_pipeline(pg, orc, seed):
     finally:
         for k in knobs:
             pg.set_tuning(k, None)
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("PG_STRESS_BUILD_SEEDS", "24"))))
+def test_random_build(pg, orc, seed):
+    """Graph load, frontiers, execution paths, groupings, regression gs and
+    the cost-model gs table on random RMAT graphs and training sets: every
+    integer array and table equal to the oracle's."""
+    rng = np.random.default_rng(9000 + seed)
+    n = int(rng.integers(50, 8000))
+    pairs, n_pad = rmat_pairs(orc, n, n * int(rng.choice([1, 4, 16, 48])), 300 + seed)
+    ratio = float(rng.choice([0.001, 0.02, 0.3, 0.9, 1.0]))
+    vt = orc.sample_training_set(n_pad, ratio, seed)
+    L = int(rng.integers(1, 5))
+    symnorm = bool(seed % 2)
+    dg = pg.build_undirected_csr(pairs, n_hint=n_pad, weights="symnorm" if symnorm else "unit")
+    og = orc.build_graph(pairs, n_hint=n_pad, symnorm=symnorm)
+    offs, nb, w = dg.export()
+    assert np.array_equal(offs, og.offsets) and np.array_equal(nb, og.neighbors)
+    assert np.array_equal(w.view(np.uint64), og.weights.view(np.uint64))
+    F = pg.compute_frontiers(dg, vt, L)
+    lv = orc.compute_frontiers(og, vt, L)
+    for k in range(L + 1):
+        assert np.array_equal(F.level(k), lv[k]), (seed, k)
+    for dp, op in zip(pg.prepare_all_paths(dg, F), orc.prepare_all_paths(og, lv)):
+        x = dp.export()
+        for f in ("dest", "src", "srcpos", "offsets", "neighbors"):
+            assert np.array_equal(x[f], getattr(op, f)), (seed, f)
+        assert np.array_equal(x["weights"].view(np.uint64), op.weights.view(np.uint64))
+        assert pg.path_regression_gs(dp) == orc.path_regression_gs(op.D, op.E)
+        gs = int(rng.integers(1, 40))
+        gx = pg.group_neighbors(dp, gs).export()
+        og_ = orc.group_neighbors(op.offsets, gs)
+        for f in ("dest", "begin", "end", "dest_groups"):
+            assert np.array_equal(gx[f], getattr(og_, f)), (seed, f, gs)
+        dim = int(rng.choice([1, 16, 100, 602]))
+        W = int(rng.choice([1, 8, 16]))
+        best, table = pg.oracle_gs(dp, dim, W, 0.25)
+        obest, otable = orc.oracle_gs_cost(op.offsets, [c for c, _ in table], dim, W, 0.25)
+        assert best == obest and [c for _, c in table] == list(otable), (seed, dim, W)
