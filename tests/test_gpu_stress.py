@@ -166,3 +166,49 @@ def test_random_build(pg, orc, seed):
         best, table = pg.oracle_gs(dp, dim, W, 0.25)
         obest, otable = orc.oracle_gs_cost(op.offsets, [c for c, _ in table], dim, W, 0.25)
         assert best == obest and [c for _, c in table] == list(otable), (seed, dim, W)
+
+
+def test_concurrent_host_calls_mixed_buffers(pg, orc):
+    """Several host threads issuing host-buffer calls at once on distinct
+    groupings, pinned and pageable, of sizes that span several 16 MB staging
+    pieces: every result bit-exact (per-device copy streams and staging
+    slots are serialised, never shared mid-call)."""
+    import threading
+
+    import torch
+
+    rng = np.random.default_rng(4242)
+    pairs, n_pad = rmat_pairs(orc, 30000, 30000 * 40, 17)
+    vt = orc.sample_training_set(n_pad, 0.5, 3)
+    dg = pg.build_undirected_csr(pairs, n_hint=n_pad, weights="symnorm")
+    og = orc.build_graph(pairs, n_hint=n_pad, symnorm=True)
+    F = pg.compute_frontiers(dg, vt, 2)
+    ops = orc.prepare_all_paths(og, orc.compute_frontiers(og, vt, 2))
+    dps = pg.prepare_all_paths(dg, F)
+    jobs = []
+    for dp, op in zip(dps, ops):
+        for dim, pinned in ((33, False), (301, True), (302, False), (128, False)):
+            y = rng.uniform(-1, 1, size=(dp.P, dim)).astype(np.float32)
+            want = orc.aggregate_pull_f32(op.offsets, op.neighbors, op.weights, y[op.srcpos])
+            yh = torch.from_numpy(y).pin_memory().numpy() if pinned else y
+            jobs.append((pg.group_neighbors(dp, 4), yh, want, pinned))
+    errors = []
+
+    def run(G, y, want, pinned):
+        try:
+            for _ in range(3):
+                x = np.full(want.shape, np.nan, np.float32)
+                if pinned:
+                    x = torch.from_numpy(x).pin_memory().numpy()
+                pg.backward_aggregation(G, y, x, overwrite=True)
+                if not np.array_equal(bits(x), bits(want)):
+                    errors.append((want.shape, pinned))
+        except Exception as e:  # pragma: no cover
+            errors.append(repr(e))
+
+    ts = [threading.Thread(target=run, args=j) for j in jobs]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
