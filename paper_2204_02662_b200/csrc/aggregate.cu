@@ -56,6 +56,7 @@ constexpr TuneKey kTuneKeys[] = {
     {"atb_pairs", "PG_ATB_PAIRS", 224},  // W' split GEMM: 2 A columns per lane above this many 64-chain blocks (0 = never)
     {"gemm_packed", "PG_GEMM_PACKED", 1},  // gemm / gemm_a_bt: 1 = FFMA2/FADD2 column pairs (k_gemm2), 0 = k_gemm
     {"host_last_seg_pct", "PG_HOST_LAST_SEG_PCT", 40},  // host drop-in: % of the edges in the last (chunked) segment, 0 = 1/K
+    {"wgrad_fork", "PG_WGRAD_FORK", 1},  // backward chains: W' GEMMs on a forked stream (1) or in order (0)
 };
 std::atomic<int64_t> g_tune[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];
 int64_t g_tune_def[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];  // $PG_<KEY> at load, else built-in

@@ -644,18 +644,13 @@ void gemm(DMat a, DMat b, DMat out, bool b_transposed, cudaStream_t s) {
     PG_LAUNCH("k_gemm");
 }
 
-uint64_t gemm_at_b_blocks(uint64_t r, uint64_t c) {
-    const uint64_t ti = (c <= 8 ? 8 : 4) * (gemm_at_b_chain_pairs(r, c) ? 2 : 1), tc = c <= 8 ? 8 : 16;
-    return ((r + ti - 1) / ti) * ((c + tc - 1) / tc);
-}
-
 void gemm_at_b(DMat a, const uint32_t* a_rows, DMat b, DMat out, cudaStream_t s) {
     const uint64_t n = b.rows, r = a.cols, c = b.cols;
     if (!a_rows && a.rows != n) fail(kConfig, "gemm_at_b: row counts differ");
     if (out.rows != r || out.cols != c) fail(kConfig, "gemm_at_b: output shape mismatch");
     if (r == 0 || c == 0) return;
     if (n >= (1ull << 31) || r >= (1ull << 31) || c >= (1ull << 31)) fail(kConfig, "gemm_at_b: dimension too large");
-    // 64 chains per warp: 4 (or 8) A columns x 16 (or 8) B columns (gemm_at_b_blocks)
+    // 64 chains per warp: 4 (or 8) A columns x 16 (or 8) B columns
     if (c <= 8) launch_at_b<8>(a, a_rows, b, out, n, r, c, s);
     else launch_at_b<4>(a, a_rows, b, out, n, r, c, s);
 }
@@ -742,14 +737,15 @@ void check_chain(const BackwardIO& io, uint64_t n) {
         fail(kConfig, "backward: top gradient shape mismatch");
 }
 
-// W' = Y^T g on a forked stream. The W gradients are chain outputs that
-// nothing later in the chain reads, so each one overlaps the y_grad GEMM and
-// the SpMM of its layer (the serial-order GEMM is latency-bound on a few
-// dozen to ~150 warps; the SpMM it hides behind is bandwidth-bound). Every
-// g it reads is kept alive until join(), which makes the caller's stream
-// wait for the last W' (stream-ordered frees then follow the join).
-constexpr uint64_t kWGradSideMaxBlocks = 160;  // Reddit layer 0: 151 blocks, forked
-
+// W' = Y^T g on a forked stream (tuning "wgrad_fork"). The W gradients are
+// chain outputs that nothing later in the chain reads, so each one overlaps
+// the y_grad GEMM and the SpMM of its layer (the serial-order GEMM is
+// latency-bound; the SpMM it hides behind is bandwidth-bound). Measured:
+// Reddit backward_epp 17.9 -> 17.8 ms, products 22.2 -> 18.8, arxiv 2.85 ->
+// 2.49 (with the one-warp W' kernel the 400-block products GEMM lost more
+// to SMSP sharing than it hid, so the fork was limited to <= 160 blocks).
+// Every g it reads is kept alive until join(), which makes the caller's
+// stream wait for the last W' (stream-ordered frees then follow the join).
 struct WGradSide {
     cudaStream_t main;
     cudaStream_t side;
@@ -776,10 +772,7 @@ struct WGradSide {
         done = d.done;
     }
     void gemm_at_b(DMat a, const uint32_t* rows, DMat b, DMat out) {
-        if (gemm_at_b_blocks(a.cols, b.cols) > kWGradSideMaxBlocks) {
-            // a GEMM of more than ~1 block (one warp) per SM shares SMSPs
-            // with the SpMM and both slow down (ogbn-products: 192 and 400
-            // blocks, chain 30 -> 32.5 / 51 ms when forked): run it in order
+        if (!tuning(kTuneWgradFork)) {
             pg::gemm_at_b(a, rows, b, out, main);
             return;
         }

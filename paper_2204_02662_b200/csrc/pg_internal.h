@@ -264,7 +264,8 @@ enum TuneKeyId {
     kTuneAtbSplit = 19,
     kTuneAtbPairs = 20,
     kTuneGemmPacked = 21,
-    kTuneHostLastSegPct = 22
+    kTuneHostLastSegPct = 22,
+    kTuneWgradFork = 23
 };
 // idle dynamic smem (bytes) per k_agg_vec4 block for the launches of this
 // thread while set (host drop-in passes beside the H2D: fewer resident
@@ -297,7 +298,6 @@ inline uint64_t pad_ld(uint64_t c) { return c <= 32 ? (c + 3) & ~3ull : (c + 31)
 void gemm(DMat a, DMat b, DMat out, bool b_transposed, cudaStream_t s);
 // dense_matrix.hpp:57-76: out = a[a_rows]^T * b (a_rows nullable: all rows)
 void gemm_at_b(DMat a, const uint32_t* a_rows, DMat b, DMat out, cudaStream_t s);
-uint64_t gemm_at_b_blocks(uint64_t r, uint64_t c);  // one 32-thread block per 64 output chains
 void relu(DMat x, DMat out, cudaStream_t s);
 // out[r] = pre[pre_rows[r]] > 0 ? g[r] : 0 (pre_rows nullable)
 void relu_backward_rows(DMat g, DMat pre, const uint32_t* pre_rows, DMat out, cudaStream_t s);
