@@ -83,7 +83,7 @@ int pg_set_heavy_min_degree(uint64_t min_degree);
  * equal edge counts, 0: equal rows), "host_last_seg_pct" (% of the edges in
  * the last, chunked segment; 0 = 1/K), "host_chunk_balance" (chunk cuts: %
  * weight of edges vs rows), "host_copy_prio" (copy/repack streams at the
- * highest priority), "host_pitch2d", "host_pass_smem" (measured slower,
+ * highest priority), "host_pitch2d" (measured slower,
  * off) and "host_trace" (1: phase times on stderr). A negative value
  * restores the default ($PG_<KEY> at load, else built-in). Unknown key ->
  * PG_ERR_CONFIG. */

@@ -47,7 +47,6 @@ constexpr TuneKey kTuneKeys[] = {
     {"grouped_seg", "PG_GROUPED_SEG", 0},  // grouped Fast: 1 = CTA-segmented reduction, 0 = an atomic per extra group
     {"heavy_wide_pipe", "PG_HEAVY_WIDE_PIPE", 1},  // heavy wide rows: 1 = software-pipelined k_agg_wide_pipe
     {"host_final_segs", "PG_HOST_FINAL_SEGS", 1},  // host drop-in: trailing source segments of the chunked last pass
-    {"host_pass_smem", "PG_HOST_PASS_SMEM", 0},  // host drop-in: KB of idle smem per SpMM block in passes beside the H2D
     {"host_pitch2d", "PG_HOST_PITCH2D", 0},  // host drop-in: odd widths by 2-D DMA (1) or flat DMA + repack kernel (0)
     {"host_copy_prio", "PG_HOST_COPY_PRIO", 1},  // host drop-in: copy/repack streams at the highest priority (read once)
     {"host_seg_balance", "PG_HOST_SEG_BALANCE", 1},  // host drop-in: source segments of equal rows (0) or equal edges (1)
@@ -58,6 +57,8 @@ constexpr TuneKey kTuneKeys[] = {
     {"host_last_seg_pct", "PG_HOST_LAST_SEG_PCT", 40},  // host drop-in: % of the edges in the last (chunked) segment, 0 = 1/K
     {"wgrad_fork", "PG_WGRAD_FORK", 1},  // backward chains: W' GEMMs on a forked stream (1) or in order (0)
 };
+static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneWgradFork + 1,
+              "kTuneKeys and enum TuneKeyId (pg_internal.h) must list the same keys in the same order");
 std::atomic<int64_t> g_tune[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];
 int64_t g_tune_def[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];  // $PG_<KEY> at load, else built-in
 std::once_flag g_tune_once;
@@ -69,8 +70,6 @@ void tune_init() {
     }
 }
 }  // namespace
-
-thread_local int g_pass_smem = 0;
 
 int64_t tuning(int key) {
     std::call_once(g_tune_once, tune_init);
@@ -1214,20 +1213,7 @@ void launch_vec4(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges, 
     // L2-only gathers measured no faster for narrow rows and slower for wide
     // ones (layer 0 16.7 -> 17.1 ms), so only on request
     const bool cg = tuning(kTuneLdCg) == 2;
-    const int thr = g_pass_smem;
-    if (thr > 0) {
-        static thread_local std::vector<int> attr;  // per device: max dynamic smem set
-        int dev = 0;
-        PG_CUDA(cudaGetDevice(&dev));
-        if (static_cast<int>(attr.size()) <= dev) attr.resize(dev + 1, 0);
-        if (attr[dev] < thr) {
-            PG_CUDA(cudaFuncSetAttribute(k_agg_vec4<LPD, U, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, thr));
-            attr[dev] = thr;
-        }
-        k_agg_vec4<LPD, U, false><<<grid_for(items * LPD, 256), 256, thr, s>>>(
-            ebeg, eend, edges, order, d_begin, items, chunks, in, static_cast<uint32_t>(ld_in * 4), out, ld_out, dim,
-            accumulate, kZeros, 0u, cm, ext);
-    } else if (ext.src_bits || ext.dst_bits)
+    if (ext.src_bits || ext.dst_bits)
         k_agg_vec4<LPD, U, true><<<grid_for(items * LPD, 256), 256, 0, s>>>(
             ebeg, eend, edges, order, d_begin, items, chunks, in, static_cast<uint32_t>(ld_in * 4), out, ld_out, dim,
             accumulate, kZeros, 0u, cm, ext);

@@ -658,11 +658,9 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
         tmark(cs.h2d, "h2d" + std::to_string(k));
         if (k + F < K) {
             PG_CUDA(cudaStreamWaitEvent(s, cs.ev[1 + k], 0));
-            g_pass_smem = static_cast<int>(std::clamp<int64_t>(tuning(kTuneHostPassSmem), 0, 227) * 1024);
             run_aggregate(G, parent_indexed, 0, static_cast<uint32_t>(D), din.get(), ld, dout.get(), ld, dim,
                           k == 0 ? flags : (flags & ~PG_AGG_OVERWRITE), s,
                           SegSel{G.host_seg_bnd.get(), static_cast<int>(k), K});
-            g_pass_smem = 0;
             tmark(s, "pass" + std::to_string(k));
         }
     }

@@ -256,21 +256,17 @@ enum TuneKeyId {
     kTuneGroupedSeg = 11,
     kTuneHeavyWidePipe = 12,
     kTuneHostFinalSegs = 13,
-    kTuneHostPassSmem = 14,
-    kTuneHostPitch2d = 15,
-    kTuneHostCopyPrio = 16,
-    kTuneHostSegBalance = 17,
-    kTuneHostChunkBalance = 18,
-    kTuneAtbSplit = 19,
-    kTuneAtbPairs = 20,
-    kTuneGemmPacked = 21,
-    kTuneHostLastSegPct = 22,
-    kTuneWgradFork = 23
+    kTuneHostPitch2d = 14,
+    kTuneHostCopyPrio = 15,
+    kTuneHostSegBalance = 16,
+    kTuneHostChunkBalance = 17,
+    kTuneAtbSplit = 18,
+    kTuneAtbPairs = 19,
+    kTuneGemmPacked = 20,
+    kTuneHostLastSegPct = 21,
+    kTuneWgradFork = 22
 };
-// idle dynamic smem (bytes) per k_agg_vec4 block for the launches of this
-// thread while set (host drop-in passes beside the H2D: fewer resident
-// blocks, less L2 pressure against the copy engines)
-extern thread_local int g_pass_smem;
+
 int64_t tuning(int key);
 bool set_tuning(const char* name, int64_t value);
 

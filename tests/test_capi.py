@@ -72,7 +72,7 @@ def test_tuning_keys(pg):
     """pg_set_tuning: scheduling knobs by name; unknown keys are config errors."""
     for key in ("vec_u", "chunk_major", "heavy_tma", "host_segs", "host_chunks", "host_trace", "heavy_narrow",
                 "wide_lpd", "src_segs", "ld_cg", "host_chunk_order", "grouped_seg", "heavy_wide_pipe",
-                "host_final_segs", "host_pass_smem", "host_pitch2d", "host_copy_prio", "host_seg_balance",
+                "host_final_segs", "host_pitch2d", "host_copy_prio", "host_seg_balance",
                 "host_chunk_balance", "atb_split", "atb_pairs", "gemm_packed", "host_last_seg_pct", "wgrad_fork"):
         pg.set_tuning(key, None)
     import pytest
