@@ -292,6 +292,12 @@ typedef struct pg_mat {
     uint64_t rows, cols, ld;
 } pg_mat;
 
+/* Whole-matrix copies between a host DenseMatrix<float> (row-major, ld =
+ * cols) and a pitched device pg_mat: one flat copy plus an on-device repack
+ * when the pitches differ (not one copy per row). Synchronous. */
+int pg_mat_upload(int device, pg_mat dst, const float* host);
+int pg_mat_download(int device, float* host, pg_mat src);
+
 /* dense_matrix.hpp:40-55 gemm (b_transposed = 0) and :78-95 gemm_a_bt
  * (b_transposed = 1): ascending k, separately rounded, + 0 */
 int pg_gemm(pg_mat a, pg_mat b, int b_transposed, pg_mat out, void* stream);

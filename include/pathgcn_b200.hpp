@@ -529,15 +529,12 @@ public:
 
     static DeviceMatrix upload(const MatrixF& h, int device = 0) {
         DeviceMatrix d(h.rows, h.cols, device);
-        for (std::size_t r = 0; r < h.rows && h.cols; ++r)
-            check(pg_memcpy_h2d(device, d.m_.data + r * d.m_.ld, h.data.data() + r * h.cols, h.cols * 4));
+        check(pg_mat_upload(device, d.m_, h.data.data()));
         return d;
     }
     MatrixF download() const {
         MatrixF h(m_.rows, m_.cols);
-        check(pg_device_synchronize(dev_));
-        for (std::size_t r = 0; r < m_.rows && m_.cols; ++r)
-            check(pg_memcpy_d2h(dev_, h.data.data() + r * m_.cols, m_.data + r * m_.ld, m_.cols * 4));
+        check(pg_mat_download(dev_, h.data.data(), m_));
         return h;
     }
     std::size_t rows() const { return m_.rows; }

@@ -134,6 +134,8 @@ SIGNATURES = {
     "pg_memcpy_d2h": [i32, vp, vp, u64],
     "pg_memset_zero": [i32, vp, u64],
     "pg_device_synchronize": [i32],
+    "pg_mat_upload": [i32, PgMat, f32p],
+    "pg_mat_download": [i32, f32p, PgMat],
     "pg_gemm": [PgMat, PgMat, i32, PgMat, vp],
     "pg_gemm_at_b": [PgMat, vp, PgMat, PgMat, vp],
     "pg_relu": [PgMat, PgMat, vp],

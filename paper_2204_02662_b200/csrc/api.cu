@@ -1456,6 +1456,45 @@ int pg_memset_zero(int device, void* dst, uint64_t bytes) {
     });
 }
 
+int pg_mat_upload(int device, pg_mat dst, const float* host) {
+    return guard([&] {
+        if (dst.rows && dst.cols && (!dst.data || !host)) fail(kConfig, "pg_mat_upload: null buffer");
+        if (dst.ld < dst.cols) fail(kConfig, "pg_mat_upload: ld < cols");
+        if (!dst.rows || !dst.cols) return;
+        DeviceGuard dg(device);
+        cudaStream_t s = lib_stream(device);
+        const uint64_t bytes = dst.rows * dst.cols * 4;
+        if (dst.ld == dst.cols) {
+            PG_CUDA(cudaMemcpyAsync(dst.data, host, bytes, cudaMemcpyHostToDevice, s));
+        } else {
+            DevBuf<float> flat(dst.rows * dst.cols, s);
+            PG_CUDA(cudaMemcpyAsync(flat.get(), host, bytes, cudaMemcpyHostToDevice, s));
+            copy_rows(flat.get(), dst.cols, dst.data, dst.ld, dst.rows, dst.cols, s);
+        }
+        PG_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int pg_mat_download(int device, float* host, pg_mat src) {
+    return guard([&] {
+        if (src.rows && src.cols && (!src.data || !host)) fail(kConfig, "pg_mat_download: null buffer");
+        if (src.ld < src.cols) fail(kConfig, "pg_mat_download: ld < cols");
+        if (!src.rows || !src.cols) return;
+        DeviceGuard dg(device);
+        PG_CUDA(cudaDeviceSynchronize());  // the matrix may have been written on any stream
+        cudaStream_t s = lib_stream(device);
+        const uint64_t bytes = src.rows * src.cols * 4;
+        if (src.ld == src.cols) {
+            PG_CUDA(cudaMemcpyAsync(host, src.data, bytes, cudaMemcpyDeviceToHost, s));
+        } else {
+            DevBuf<float> flat(src.rows * src.cols, s);
+            copy_rows(src.data, src.ld, flat.get(), src.cols, src.rows, src.cols, s);
+            PG_CUDA(cudaMemcpyAsync(host, flat.get(), bytes, cudaMemcpyDeviceToHost, s));
+        }
+        PG_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
 int pg_device_synchronize(int device) {
     return guard([&] {
         DeviceGuard dg(device);
