@@ -280,6 +280,9 @@ int pg_memcpy_h2d(int device, void* dst, const void* src, uint64_t bytes);
 int pg_memcpy_d2h(int device, void* dst, const void* src, uint64_t bytes);
 int pg_memset_zero(int device, void* dst, uint64_t bytes);
 int pg_device_synchronize(int device);
+/* Kernels launched by this library so far in this process (every launch,
+ * all devices and threads). */
+uint64_t pg_launch_count(void);
 
 /* ---------------- the GCN chain around the aggregation (engine.hpp) ----------------
  * Device-resident and bit-exact with the reference's f32 build. Matrices are

@@ -134,6 +134,7 @@ SIGNATURES = {
     "pg_memcpy_d2h": [i32, vp, vp, u64],
     "pg_memset_zero": [i32, vp, u64],
     "pg_device_synchronize": [i32],
+    "pg_launch_count": [],
     "pg_mat_upload": [i32, PgMat, f32p],
     "pg_mat_download": [i32, f32p, PgMat],
     "pg_gemm": [PgMat, PgMat, i32, PgMat, vp],
@@ -154,11 +155,14 @@ def header_symbols():
     import re
 
     txt = open(HEADER).read()
-    return sorted(set(re.findall(r"^int\s+(pg_\w+)\s*\(", txt, re.M)))
+    return sorted(set(re.findall(r"^(?:int|uint64_t)\s+(pg_\w+)\s*\(", txt, re.M)))
+
+
+RESTYPES = {"pg_launch_count": C.c_uint64}
 
 
 def _declare(lib):
     for name, args in SIGNATURES.items():
         fn = getattr(lib, name)
         fn.argtypes = args
-        fn.restype = C.c_int
+        fn.restype = RESTYPES.get(name, C.c_int)

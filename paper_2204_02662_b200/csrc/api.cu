@@ -1495,6 +1495,8 @@ int pg_mat_download(int device, float* host, pg_mat src) {
     });
 }
 
+uint64_t pg_launch_count(void) { return pg::launch_counter(); }
+
 int pg_device_synchronize(int device) {
     return guard([&] {
         DeviceGuard dg(device);

@@ -27,7 +27,14 @@ inline void cuda_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess) fail(kDevice, std::string(what) + ": " + cudaGetErrorString(e));
 }
 #define PG_CUDA(x) ::pg::cuda_check((x), #x)
-#define PG_LAUNCH(what) ::pg::cuda_check(cudaGetLastError(), what)
+// every kernel launch of the library goes through PG_LAUNCH: it checks the
+// launch and counts it (pg_launch_count, the bench's gpu_launches)
+uint64_t& launch_counter();
+inline void launched(const char* what) {
+    cuda_check(cudaGetLastError(), what);
+    __atomic_fetch_add(&launch_counter(), 1, __ATOMIC_RELAXED);
+}
+#define PG_LAUNCH(what) ::pg::launched(what)
 
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 8;

@@ -189,6 +189,11 @@ uint32_t max_degree_dev(const uint64_t* offsets, uint32_t n, cudaStream_t s) {
     return h;
 }
 
+uint64_t& launch_counter() {
+    static uint64_t n = 0;
+    return n;
+}
+
 cudaStream_t lib_stream(int device) {
     std::lock_guard<std::mutex> lk(g_stream_mu);
     if (static_cast<int>(g_streams.size()) <= device) g_streams.resize(device + 1, nullptr);

@@ -493,3 +493,21 @@ def test_degenerate_shapes(pg, orc):
                 torch.cuda.synchronize()
                 assert (xd.cpu().numpy() == 0).all()
         assert all(int(v) == 0 for v in G.counters(16).values())
+
+
+def test_launch_counter_counts_library_kernels(pg, orc):
+    """pg_launch_count (the bench's gpu_launches): every SpMM call launches
+    at least one of this library's kernels, counted."""
+    from paper_2204_02662_b200 import _lib
+
+    lib = _lib.load()
+    pairs, n_pad = rmat_pairs(orc, 1024, 8192, 7)
+    vt = orc.sample_training_set(1024, 0.1, 42)
+    og, dg, F, ops, dps = build_all(pg, orc, pairs, n_pad, vt, 2)
+    G = pg.group_neighbors(dps[1], 4)
+    y = pg.empty_rows(dps[1].P, 16)
+    x = pg.empty_rows(dps[1].D, 16)
+    before = lib.pg_launch_count()
+    for _ in range(3):
+        pg.backward_aggregation(G, y, x, overwrite=True)
+    assert lib.pg_launch_count() - before >= 3
