@@ -579,6 +579,8 @@ def backward_aggregation(grouped: GroupedCsr, y_grad, x_grad, mode=DETERMINISTIC
         y = np.ascontiguousarray(y_grad, np.float32)
         if x_grad.shape != (path.D, y.shape[1]) or x_grad.dtype != np.float32:
             raise ShapeError("backward_aggregation: x_grad shape mismatch")
+        if not (x_grad.flags.c_contiguous and x_grad.flags.writeable):
+            raise ShapeError("backward_aggregation: host x_grad must be a writeable C-contiguous float32 array")
         c = np.zeros(3, np.uint64)
         _check(_lib_().pg_backward_aggregate_host(grouped._h, _p(y, f32p), y.shape[0], y.shape[1],
                                                   _p(x_grad, f32p), flags, _p(c, u64p)))

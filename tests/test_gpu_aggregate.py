@@ -511,3 +511,25 @@ def test_launch_counter_counts_library_kernels(pg, orc):
     for _ in range(3):
         pg.backward_aggregation(G, y, x, overwrite=True)
     assert lib.pg_launch_count() - before >= 3
+
+
+def test_host_call_argument_errors(pg, orc):
+    """Host-buffer calls reject what the reference's ShapeError would:
+    wrong row counts, wrong widths, non-float32 or strided outputs — and
+    leave the output untouched."""
+    pairs, n_pad = rmat_pairs(orc, 512, 3000, 3)
+    vt = orc.sample_training_set(512, 0.2, 1)
+    og, dg, F, ops, dps = build_all(pg, orc, pairs, n_pad, vt, 2)
+    dp = dps[1]
+    G = pg.group_neighbors(dp, 4)
+    y = np.ones((dp.P, 8), np.float32)
+    x = np.full((dp.D, 8), 5.0, np.float32)
+    with pytest.raises(pg.ConfigError):  # ShapeError is a ConfigError (status 2)
+        pg.backward_aggregation(G, np.ones((dp.P + 1, 8), np.float32), x)
+    with pytest.raises(pg.ConfigError):
+        pg.backward_aggregation(G, y, np.zeros((dp.D, 9), np.float32))
+    with pytest.raises(pg.ConfigError):
+        pg.backward_aggregation(G, y, np.zeros((dp.D, 8), np.float64))
+    with pytest.raises(pg.ConfigError):
+        pg.backward_aggregation(G, y, np.zeros((dp.D, 16), np.float32)[:, ::2])
+    assert (x == 5.0).all()
