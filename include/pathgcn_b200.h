@@ -62,6 +62,18 @@ typedef struct pg_groups_s* pg_groups;       /* GroupedCsr    grouping.hpp:14-28
 typedef struct pg_edge_list_s* pg_edge_list; /* EdgeList      edge_list.hpp:14-18   */
 
 int pg_last_error(char* buf, size_t cap);
+/* The reference exception type of the calling thread's last failure
+ * (error.hpp:10-47), so wrappers rethrow the exact subtype: PG_KIND_* below;
+ * *line (nullable) = ParseError::line_number for PG_KIND_PARSE, else 0. */
+#define PG_KIND_NONE 0
+#define PG_KIND_CONFIG 1      /* ConfigError    -> status 2 */
+#define PG_KIND_SHAPE 2       /* ShapeError     -> status 2 */
+#define PG_KIND_STALENESS 3   /* StalenessError -> status 2 */
+#define PG_KIND_PARSE 4       /* ParseError     -> status 2 */
+#define PG_KIND_IO 5          /* IoError        -> status 3 */
+#define PG_KIND_NUMERIC 6     /* NumericError   -> status 4 */
+#define PG_KIND_DEVICE 7      /* (new) CUDA failure -> status 5 */
+int pg_last_error_kind(uint64_t* line);
 int pg_version(void);
 int pg_device_count(int* count);
 /* Scheduling knob (never changes results): destinations with at least this

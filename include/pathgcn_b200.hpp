@@ -72,16 +72,19 @@ inline void check(int rc) {
     std::string msg(512, '\0');
     pg_last_error(msg.data(), msg.size());
     msg.resize(msg.find('\0'));
+    std::uint64_t line = 0;
+    switch (pg_last_error_kind(&line)) {  // the exact error.hpp type, not a guess from the text
+        case PG_KIND_SHAPE: throw ShapeError(msg);
+        case PG_KIND_STALENESS: throw StalenessError(msg);
+        case PG_KIND_PARSE: throw ParseError(msg, line);
+        case PG_KIND_CONFIG: throw ConfigError(msg);
+        case PG_KIND_IO: throw IoError(msg);
+        case PG_KIND_NUMERIC: throw NumericError(msg);
+        case PG_KIND_DEVICE: throw DeviceError(msg);
+        default: break;
+    }
     switch (rc) {
-        case PG_ERR_CONFIG: {
-            if (msg.find("rows") != std::string::npos || msg.find("dimension") != std::string::npos)
-                throw ShapeError(msg);
-            if (msg.find("stale") != std::string::npos) throw StalenessError(msg);
-            const std::size_t at = msg.rfind("(line ");
-            if (at != std::string::npos && !msg.empty() && msg.back() == ')')
-                throw ParseError(msg, std::stoull(msg.substr(at + 6)));
-            throw ConfigError(msg);
-        }
+        case PG_ERR_CONFIG: throw ConfigError(msg);
         case PG_ERR_IO: throw IoError(msg);
         case PG_ERR_NUMERIC: throw NumericError(msg);
         case PG_ERR_DEVICE: throw DeviceError(msg);

@@ -71,6 +71,7 @@ matp = C.POINTER(PgMat)
 # every symbol of include/pathgcn_b200.h with its ctypes signature
 SIGNATURES = {
     "pg_last_error": [C.c_char_p, C.c_size_t],
+    "pg_last_error_kind": [u64p],
     "pg_version": [],
     "pg_device_count": [C.POINTER(C.c_int)],
     "pg_set_heavy_min_degree": [u64],

@@ -24,6 +24,8 @@ using namespace pg;
 namespace {
 
 thread_local std::string g_err;
+thread_local int g_kind = PG_KIND_NONE;
+thread_local uint64_t g_line = 0;
 
 template <typename F>
 int guard(F&& f) {
@@ -32,12 +34,18 @@ int guard(F&& f) {
         return PG_OK;
     } catch (const pg::Error& e) {
         g_err = e.what();
+        g_kind = e.kind;
+        g_line = e.line;
         return e.code;
     } catch (const std::bad_alloc&) {
         g_err = "host allocation failed";
+        g_kind = PG_KIND_DEVICE;
+        g_line = 0;
         return PG_ERR_DEVICE;
     } catch (const std::exception& e) {
         g_err = e.what();
+        g_kind = PG_KIND_CONFIG;
+        g_line = 0;
         return PG_ERR_CONFIG;
     }
 }
@@ -140,13 +148,13 @@ void counters_of(Groups& G, uint64_t dim, unsigned flags, uint64_t* c) {
 uint64_t y_rows_of(const Groups& G) { return G.edges_remap.get() ? G.remap_rows : G.path->P; }
 
 DMat dm(const pg_mat& m) {
-    if (m.ld < m.cols) fail(kConfig, "matrix leading dimension smaller than its columns");
+    if (m.ld < m.cols) fail_shape("matrix leading dimension smaller than its columns");
     if (!m.data && m.rows * m.cols) fail(kConfig, "null matrix data");
     return DMat{m.data, m.rows, m.cols, m.ld};
 }
 
 void check_dims(uint64_t dim, uint64_t ld_in, uint64_t ld_out) {
-    if (ld_in < dim || ld_out < dim) fail(kConfig, "aggregate_pull: leading dimension smaller than dim");
+    if (ld_in < dim || ld_out < dim) fail_shape("aggregate_pull: leading dimension smaller than dim");
 }
 
 // Source segments for a whole-path SpMM (tuning "src_segs": 0 = this
@@ -173,6 +181,7 @@ void pg::run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re,
                    const AggExt& ext, const Edge* edges_override) {
     const bool accumulate = !(flags & PG_AGG_OVERWRITE);
     DeviceGuard dg(G.device);
+    std::lock_guard<std::recursive_mutex> lk(G.mu);  // lazily built caches below
     if (flags & PG_AGG_GROUPED) {  // aggregate.hpp:84-115 over the groups
         const Base b = base_of(G);
         if (rb != 0 || re != b.D || sel.seg >= 0 || ext.any())
@@ -520,6 +529,7 @@ struct StagedD2H {
 void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_rows, uint64_t dim,
               float* out_host, unsigned flags) {
     const Base b = base_of(G);
+    std::lock_guard<std::recursive_mutex> lk(G.mu);  // caches stay put for the whole pipeline
     if (parent_indexed && G.edges_remap.get())
         fail(kConfig, "backward_aggregate_host: a multi-GPU source remap is installed on this grouping");
     DeviceGuard dg(G.device);
@@ -601,10 +611,12 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
         cuts = G.host_chunks;
     }
     std::unique_lock<std::mutex> cs_lock;
-    CopyStreams& cs = copy_streams(G.device, 2 + K + 2 * R + 2, cs_lock);
+    // sync events: 1 + K + R + 1 used; trace events: up to 1 + K + (K - F)
+    // + 2 R (start, uploads, whole passes, chunks, downloads)
+    CopyStreams& cs = copy_streams(G.device, 4 + 2 * K + 2 * R, cs_lock);
     size_t nt = 0;  // trace events used
     auto mark = [&](cudaStream_t st) {
-        if (trace) PG_CUDA(cudaEventRecord(cs.tev[nt++], st));
+        if (trace && nt < cs.tev.size()) PG_CUDA(cudaEventRecord(cs.tev[nt++], st));
     };
     std::vector<std::string> tname;
     auto tmark = [&](cudaStream_t st, std::string name) {
@@ -736,7 +748,12 @@ int pg_last_error(char* buf, size_t cap) {
     return static_cast<int>(g_err.size());
 }
 
-int pg_version(void) { return 1; }
+int pg_last_error_kind(uint64_t* line) {
+    if (line) *line = g_line;
+    return g_kind;
+}
+
+int pg_version(void) { return 2; }
 
 int pg_set_heavy_min_degree(uint64_t min_degree) {
     return guard([&] { set_heavy_min_degree(min_degree); });
@@ -925,6 +942,7 @@ int pg_graph_destroy(pg_graph h) {
         Graph* g = reinterpret_cast<Graph*>(h);
         if (!g) return;
         DeviceGuard dg(g->device);
+        drain_device();  // kernels on caller streams may still read its buffers
         delete g;
     });
 }
@@ -973,6 +991,7 @@ int pg_frontiers_destroy(pg_frontiers h) {
         Frontiers* f = reinterpret_cast<Frontiers*>(h);
         if (!f) return;
         DeviceGuard dg(f->device);
+        drain_device();  // kernels on caller streams may still read its buffers
         delete f;
     });
 }
@@ -1029,6 +1048,7 @@ int pg_path_destroy(pg_path h) {
         Path* p = reinterpret_cast<Path*>(h);
         if (!p) return;
         DeviceGuard dg(p->device);
+        drain_device();  // kernels on caller streams may still read its buffers
         delete p;
     });
 }
@@ -1240,6 +1260,7 @@ int pg_groups_destroy(pg_groups h) {
         Groups* G = reinterpret_cast<Groups*>(h);
         if (!G) return;
         DeviceGuard dg(G->device);
+        drain_device();  // kernels on caller streams may still read its buffers
         delete G;
     });
 }
@@ -1253,7 +1274,7 @@ int pg_aggregate_pull(pg_groups h, const float* in_dev, uint64_t in_rows, uint64
         const Base b = base_of(G);
         check_dims(dim, ld_in, ld_out);
         if (in_rows != b.in_rows_local)
-            fail(kConfig, "aggregate_pull: input rows != source count of the grouping's base");
+            fail_shape("aggregate_pull: input rows != source count of the grouping's base");
         run_aggregate(G, false, 0, b.D, in_dev, ld_in, out_dev, ld_out, dim, flags,
                       static_cast<cudaStream_t>(stream));
     });
@@ -1265,7 +1286,7 @@ int pg_backward_aggregate(pg_groups h, const float* y_dev, uint64_t y_rows, uint
         Groups& G = *R_(h);
         if (!G.path) fail(kConfig, "backward_aggregate: grouping is not over an execution path");
         check_dims(dim, ld_in, ld_out);
-        if (y_rows != y_rows_of(G)) fail(kConfig, "backward_aggregate: y_grad rows != parent frontier size");
+        if (y_rows != y_rows_of(G)) fail_shape("backward_aggregate: y_grad rows != parent frontier size");
         run_aggregate(G, true, 0, G.path->D, y_dev, ld_in, x_dev, ld_out, dim, flags,
                       static_cast<cudaStream_t>(stream));
     });
@@ -1278,7 +1299,7 @@ int pg_backward_aggregate_rows(pg_groups h, uint32_t row_begin, uint32_t row_end
         Groups& G = *R_(h);
         if (!G.path) fail(kConfig, "backward_aggregate: grouping is not over an execution path");
         check_dims(dim, ld_in, ld_out);
-        if (y_rows != y_rows_of(G)) fail(kConfig, "backward_aggregate: y_grad rows != parent frontier size");
+        if (y_rows != y_rows_of(G)) fail_shape("backward_aggregate: y_grad rows != parent frontier size");
         if (row_begin > row_end || row_end > G.path->D) fail(kConfig, "backward_aggregate: bad row range");
         if (row_begin == row_end) return;
         run_aggregate(G, true, row_begin, row_end, y_dev, ld_in, x_dev, ld_out, dim, flags,
@@ -1291,7 +1312,7 @@ int pg_aggregate_pull_host(pg_groups h, const float* in_host, uint64_t in_rows, 
     return guard([&] {
         Groups& G = *R_(h);
         if (in_rows != base_of(G).in_rows_local)
-            fail(kConfig, "aggregate_pull: input rows != source count of the grouping's base");
+            fail_shape("aggregate_pull: input rows != source count of the grouping's base");
         run_host(G, false, in_host, in_rows, dim, out_host, flags);
         counters_of(G, dim, flags, counters);
     });
@@ -1302,7 +1323,7 @@ int pg_backward_aggregate_host(pg_groups h, const float* y_host, uint64_t y_rows
     return guard([&] {
         Groups& G = *R_(h);
         if (!G.path) fail(kConfig, "backward_aggregate: grouping is not over an execution path");
-        if (y_rows != y_rows_of(G)) fail(kConfig, "backward_aggregate: y_grad rows != parent frontier size");
+        if (y_rows != y_rows_of(G)) fail_shape("backward_aggregate: y_grad rows != parent frontier size");
         run_host(G, true, y_host, y_rows, dim, x_host, flags);
         counters_of(G, dim, flags, counters);
     });
@@ -1314,13 +1335,14 @@ int pg_groups_remap_sources(pg_groups h, const uint32_t* map, uint64_t map_len, 
         if (!G.path) fail(kConfig, "remap: grouping is not over an execution path");
         Path& p = *G.path;
         DeviceGuard dg(G.device);
+        std::lock_guard<std::recursive_mutex> lk(G.mu);
         cudaStream_t s = lib_stream(G.device);
         if (!map) {
-            G.edges_remap.reset();
+            retire(G.edges_remap);
             G.remap_rows = 0;
             return;
         }
-        if (map_len != p.P) fail(kConfig, "remap: map length != parent frontier size");
+        if (map_len != p.P) fail_shape("remap: map length != parent frontier size");
         for (uint64_t i = 0; i < map_len; ++i)
             if (map[i] >= new_rows) fail(kConfig, "remap: map entry out of range");
         DevBuf<uint32_t> dmap(map_len, s);
@@ -1328,6 +1350,7 @@ int pg_groups_remap_sources(pg_groups h, const uint32_t* map, uint64_t map_len, 
         DevBuf<Edge> out(p.E, s);
         remap_edges(p.edges_parent.get(), p.E, dmap.get(), out.get(), s);
         PG_CUDA(cudaStreamSynchronize(s));
+        retire(G.edges_remap);
         G.edges_remap = std::move(out);
         G.remap_rows = new_rows;
     });
@@ -1338,9 +1361,11 @@ int pg_groups_set_segments(pg_groups h, const uint64_t* cuts, uint32_t nseg) {
         Groups& G = *R_(h);
         if (!G.path) fail(kConfig, "segments: grouping is not over an execution path");
         Path& p = *G.path;
+        DeviceGuard dg(G.device);
+        std::lock_guard<std::recursive_mutex> lk(G.mu);
         if (!cuts || nseg == 0) {
             G.seg_cuts.clear();
-            G.seg_bnd.reset();
+            retire(G.seg_bnd);
             return;
         }
         const uint64_t rows = y_rows_of(G);
@@ -1349,7 +1374,6 @@ int pg_groups_set_segments(pg_groups h, const uint64_t* cuts, uint32_t nseg) {
         for (uint32_t k = 0; k < nseg; ++k)
             if (cuts[k + 1] < cuts[k]) fail(kConfig, "segments: cuts must be non-decreasing");
         (void)rows;
-        DeviceGuard dg(G.device);
         const Edge* edges = G.edges_remap.get() ? G.edges_remap.get() : p.edges_parent.get();
         segment_bounds(p.offsets.get(), edges, p.D, cuts, nseg, G.seg_bnd, lib_stream(G.device));
         G.seg_cuts.assign(cuts, cuts + nseg + 1);
@@ -1364,7 +1388,7 @@ int pg_backward_aggregate_segment(pg_groups h, uint32_t seg, uint32_t row_begin,
         if (!G.path) fail(kConfig, "backward_aggregate: grouping is not over an execution path");
         if (G.seg_cuts.empty() || seg + 1 >= G.seg_cuts.size()) fail(kConfig, "segments: segment index out of range");
         check_dims(dim, ld_in, ld_out);
-        if (y_rows != y_rows_of(G)) fail(kConfig, "backward_aggregate: y_grad rows != parent frontier size");
+        if (y_rows != y_rows_of(G)) fail_shape("backward_aggregate: y_grad rows != parent frontier size");
         if (row_begin > row_end || row_end > G.path->D) fail(kConfig, "backward_aggregate: bad row range");
         if (row_begin == row_end) return;
         run_aggregate(G, true, row_begin, row_end, y_dev, ld_in, x_dev, ld_out, dim, flags,
@@ -1402,7 +1426,7 @@ int pg_path_shard_bounds(pg_path h, uint32_t world, uint32_t* bounds) {
 int pg_gemm_a_bt(const float* a, uint64_t lda, const float* b, uint64_t ldb, float* out, uint64_t ldo, uint64_t n,
                  uint64_t m, uint64_t k, void* stream) {
     return guard([&] {
-        if (lda < k || ldb < k || ldo < m) fail(kConfig, "gemm_a_bt: leading dimension too small");
+        if (lda < k || ldb < k || ldo < m) fail_shape("gemm_a_bt: leading dimension too small");
         gemm(DMat{const_cast<float*>(a), n, k, lda}, DMat{const_cast<float*>(b), m, k, ldb}, DMat{out, n, m, ldo},
              true, static_cast<cudaStream_t>(stream));
     });
@@ -1459,7 +1483,7 @@ int pg_memset_zero(int device, void* dst, uint64_t bytes) {
 int pg_mat_upload(int device, pg_mat dst, const float* host) {
     return guard([&] {
         if (dst.rows && dst.cols && (!dst.data || !host)) fail(kConfig, "pg_mat_upload: null buffer");
-        if (dst.ld < dst.cols) fail(kConfig, "pg_mat_upload: ld < cols");
+        if (dst.ld < dst.cols) fail_shape("pg_mat_upload: ld < cols");
         if (!dst.rows || !dst.cols) return;
         DeviceGuard dg(device);
         cudaStream_t s = lib_stream(device);
@@ -1478,7 +1502,7 @@ int pg_mat_upload(int device, pg_mat dst, const float* host) {
 int pg_mat_download(int device, float* host, pg_mat src) {
     return guard([&] {
         if (src.rows && src.cols && (!src.data || !host)) fail(kConfig, "pg_mat_download: null buffer");
-        if (src.ld < src.cols) fail(kConfig, "pg_mat_download: ld < cols");
+        if (src.ld < src.cols) fail_shape("pg_mat_download: ld < cols");
         if (!src.rows || !src.cols) return;
         DeviceGuard dg(device);
         PG_CUDA(cudaDeviceSynchronize());  // the matrix may have been written on any stream
@@ -1537,7 +1561,7 @@ int pg_aggregate_pull_filtered(pg_groups h, pg_frontiers hf, uint64_t dest_level
         if (!G.graph) fail(kConfig, "aggregate_pull_filtered: needs a grouping of the full graph");
         if (dest_level > F.L || src_level > F.L) fail(kConfig, "aggregate_pull_filtered: level out of range");
         if (F.n != G.graph->n) fail(kConfig, "aggregate_pull_filtered: frontiers are for another graph");
-        if (in_rows != G.graph->n) fail(kConfig, "aggregate_pull_filtered: input rows != vertex count");
+        if (in_rows != G.graph->n) fail_shape("aggregate_pull_filtered: input rows != vertex count");
         check_dims(dim, ld_in, ld_out);
         AggExt ext;
         ext.dst_bits = F.levels[dest_level].bits.get();

@@ -15,13 +15,33 @@ namespace pg {
 // CLI exit codes (error.hpp:10-47, main.cpp:383-406); 5 is new: a CUDA
 // runtime/device failure.
 enum Status : int { kOk = 0, kConfig = 2, kIo = 3, kNumeric = 4, kDevice = 5 };
+// The reference exception type behind a status (error.hpp:10-47), carried
+// across the ABI by pg_last_error_kind (PG_KIND_* in pathgcn_b200.h) so the
+// C++ and Python wrappers rethrow the exact subtype instead of guessing it
+// from the message.
+enum Kind : int { kKindNone = 0, kKindConfig = 1, kKindShape = 2, kKindStaleness = 3, kKindParse = 4,
+                  kKindIo = 5, kKindNumeric = 6, kKindDevice = 7 };
+
+inline int kind_of_status(int code) {
+    return code == kConfig ? kKindConfig : code == kIo ? kKindIo : code == kNumeric ? kKindNumeric
+         : code == kDevice ? kKindDevice : kKindNone;
+}
 
 struct Error : std::runtime_error {
     int code;
-    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+    int kind;
+    uint64_t line = 0;  // ParseError::line_number
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c), kind(kind_of_status(c)) {}
+    Error(int c, int k, const std::string& m, uint64_t ln = 0) : std::runtime_error(m), code(c), kind(k), line(ln) {}
 };
 
 [[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+// ShapeError / StalenessError / ParseError (status 2, error.hpp:18-31)
+[[noreturn]] inline void fail_shape(const std::string& msg) { throw Error(kConfig, kKindShape, msg); }
+[[noreturn]] inline void fail_stale(const std::string& msg) { throw Error(kConfig, kKindStaleness, msg); }
+[[noreturn]] inline void fail_parse(const std::string& msg, uint64_t line) {
+    throw Error(kConfig, kKindParse, msg + " (line " + std::to_string(line) + ")", line);
+}
 
 inline void cuda_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess) fail(kDevice, std::string(what) + ": " + cudaGetErrorString(e));
@@ -172,6 +192,20 @@ struct DevBuf {
     }
     T* get() const { return p; }
 };
+
+// Cached device buffers (schedules, segment bounds, remapped edge streams)
+// are read by kernels on CALLER streams but were allocated on the library
+// stream, so a cudaFreeAsync on that idle stream is not ordered after those
+// kernels. Replacing or destroying one therefore drains the device first
+// (rare: a knob change, a remap, a handle destroy).
+inline void drain_device() { PG_CUDA(cudaDeviceSynchronize()); }
+template <typename T>
+void retire(DevBuf<T>& b) {
+    if (b.p) {
+        drain_device();
+        b.reset();
+    }
+}
 
 inline unsigned grid_for(uint64_t work, unsigned per_block) {
     uint64_t g = (work + per_block - 1) / per_block;

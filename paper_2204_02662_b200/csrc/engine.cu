@@ -616,9 +616,9 @@ dim3 rows_grid(uint64_t rows, uint64_t cols, unsigned tx) {
 
 void gemm(DMat a, DMat b, DMat out, bool b_transposed, cudaStream_t s) {
     const uint64_t K = a.cols;
-    if (b_transposed ? b.cols != K : b.rows != K) fail(kConfig, "gemm: inner dimensions differ");
+    if (b_transposed ? b.cols != K : b.rows != K) fail_shape("gemm: inner dimensions differ");
     const uint64_t n = a.rows, m = b_transposed ? b.rows : b.cols;
-    if (out.rows != n || out.cols != m) fail(kConfig, "gemm: output shape mismatch");
+    if (out.rows != n || out.cols != m) fail_shape("gemm: output shape mismatch");
     if (n == 0 || m == 0) return;
     if (K == 0) {
         PG_CUDA(cudaMemset2DAsync(out.p, out.ld * 4, 0, m * 4, n, s));
@@ -646,8 +646,8 @@ void gemm(DMat a, DMat b, DMat out, bool b_transposed, cudaStream_t s) {
 
 void gemm_at_b(DMat a, const uint32_t* a_rows, DMat b, DMat out, cudaStream_t s) {
     const uint64_t n = b.rows, r = a.cols, c = b.cols;
-    if (!a_rows && a.rows != n) fail(kConfig, "gemm_at_b: row counts differ");
-    if (out.rows != r || out.cols != c) fail(kConfig, "gemm_at_b: output shape mismatch");
+    if (!a_rows && a.rows != n) fail_shape("gemm_at_b: row counts differ");
+    if (out.rows != r || out.cols != c) fail_shape("gemm_at_b: output shape mismatch");
     if (r == 0 || c == 0) return;
     if (n >= (1ull << 31) || r >= (1ull << 31) || c >= (1ull << 31)) fail(kConfig, "gemm_at_b: dimension too large");
     // 64 chains per warp: 4 (or 8) A columns x 16 (or 8) B columns
@@ -656,7 +656,7 @@ void gemm_at_b(DMat a, const uint32_t* a_rows, DMat b, DMat out, cudaStream_t s)
 }
 
 void relu(DMat x, DMat out, cudaStream_t s) {
-    if (x.rows != out.rows || x.cols != out.cols) fail(kConfig, "relu: shape mismatch");
+    if (x.rows != out.rows || x.cols != out.cols) fail_shape("relu: shape mismatch");
     if (x.rows * x.cols == 0) return;
     k_relu<<<rows_grid(x.rows, x.cols, 128), 128, 0, s>>>(x.p, x.ld, out.p, out.ld, x.rows,
                                                          static_cast<uint32_t>(x.cols));
@@ -665,7 +665,7 @@ void relu(DMat x, DMat out, cudaStream_t s) {
 
 void relu_backward_rows(DMat g, DMat pre, const uint32_t* pre_rows, DMat out, cudaStream_t s) {
     if (g.rows != out.rows || g.cols != out.cols || pre.cols != g.cols || (!pre_rows && pre.rows != g.rows))
-        fail(kConfig, "relu_backward: shape mismatch");
+        fail_shape("relu_backward: shape mismatch");
     if (g.rows * g.cols == 0) return;
     k_relu_bwd_rows<<<rows_grid(g.rows, g.cols, 128), 128, 0, s>>>(g.p, g.ld, pre.p, pre.ld, pre_rows, out.p, out.ld,
                                                                    g.rows, static_cast<uint32_t>(g.cols));
@@ -673,8 +673,8 @@ void relu_backward_rows(DMat g, DMat pre, const uint32_t* pre_rows, DMat out, cu
 }
 
 void row_softmax(DMat x, DMat out, cudaStream_t s) {
-    if (x.cols == 0) fail(kConfig, "row_softmax: zero columns");
-    if (x.rows != out.rows || x.cols != out.cols) fail(kConfig, "row_softmax: shape mismatch");
+    if (x.cols == 0) fail_shape("row_softmax: zero columns");
+    if (x.rows != out.rows || x.cols != out.cols) fail_shape("row_softmax: shape mismatch");
     if (x.rows == 0) return;
     k_row_softmax<<<grid_for(x.rows, 128), 128, 0, s>>>(x.p, x.ld, out.p, out.ld, x.rows, x.cols);
     PG_LAUNCH("k_row_softmax");
@@ -682,7 +682,7 @@ void row_softmax(DMat x, DMat out, cudaStream_t s) {
 
 void top_grad_from_probs(DMat probs, DMat ref, const uint32_t* vt, uint64_t k, DMat out, cudaStream_t s) {
     if (probs.rows != ref.rows || probs.cols != ref.cols || out.rows != probs.rows || out.cols != probs.cols)
-        fail(kConfig, "top_grad_from_probs: shapes differ");
+        fail_shape("top_grad_from_probs: shapes differ");
     if (out.rows * out.cols) PG_CUDA(cudaMemset2DAsync(out.p, out.ld * 4, 0, out.cols * 4, out.rows, s));
     if (k == 0 || out.cols == 0) return;
     const float inv = 1.0f / static_cast<float>(k);  // T(1) / static_cast<T>(vt.size())
@@ -726,15 +726,15 @@ void check_chain(const BackwardIO& io, uint64_t n) {
     if (io.L == 0) fail(kConfig, "backward: need at least one layer");
     for (uint64_t l = 0; l < io.L; ++l) {
         if (io.y[l].rows != n || io.y[l].cols != io.w[l].rows)
-            fail(kConfig, "backward: Y^(l) shape does not match W^(l) at layer " + std::to_string(l));
+            fail_shape("backward: Y^(l) shape does not match W^(l) at layer " + std::to_string(l));
         if (io.pre[l].rows != n || io.pre[l].cols != io.w[l].cols)
-            fail(kConfig, "backward: pre-activation shape mismatch at layer " + std::to_string(l));
-        if (l > 0 && io.w[l].rows != io.w[l - 1].cols) fail(kConfig, "backward: weight chain mismatch");
+            fail_shape("backward: pre-activation shape mismatch at layer " + std::to_string(l));
+        if (l > 0 && io.w[l].rows != io.w[l - 1].cols) fail_shape("backward: weight chain mismatch");
         if (io.w_grads[l].rows != io.w[l].rows || io.w_grads[l].cols != io.w[l].cols)
-            fail(kConfig, "backward: W gradient shape mismatch at layer " + std::to_string(l));
+            fail_shape("backward: W gradient shape mismatch at layer " + std::to_string(l));
     }
     if (io.top_grad.rows != n || io.top_grad.cols != io.w[io.L - 1].cols)
-        fail(kConfig, "backward: top gradient shape mismatch");
+        fail_shape("backward: top gradient shape mismatch");
 }
 
 // W' = Y^T g on a forked stream (tuning "wgrad_fork"). The W gradients are
@@ -806,7 +806,7 @@ void backward_full(Groups& G, Frontiers* F, const BackwardIO& io, cudaStream_t s
     Graph& gr = *G.graph;
     const uint64_t n = gr.n, L = io.L;
     check_chain(io, n);
-    if (F && F->L != L) fail(kConfig, "ifelse backward: frontiers were computed for a different depth");
+    if (F && F->L != L) fail_stale("ifelse backward: frontiers were computed for a different depth");
     WGradSide wgs(s);
     std::unique_ptr<Tmp> gcur;
     DMat g = io.top_grad;
@@ -821,7 +821,7 @@ void backward_full(Groups& G, Frontiers* F, const BackwardIO& io, cudaStream_t s
             ext.src_bits = F->levels[L - l - 1].bits.get();
         }
         DMat* xo = io.x_grads ? &io.x_grads[L - 1 - l] : nullptr;
-        if (xo && (xo->rows != n || xo->cols != in_dim)) fail(kConfig, "backward: x_grad shape mismatch");
+        if (xo && (xo->rows != n || xo->cols != in_dim)) fail_shape("backward: x_grad shape mismatch");
         std::unique_ptr<Tmp> gnext;
         if (l > 0 && !xo) {  // fused: the SpMM writes relu_backward(x_grad, pre[l-1])
             gnext = std::make_unique<Tmp>(n, in_dim, s, F != nullptr);
@@ -868,13 +868,13 @@ void forward(Groups& G, DMat x0, const DMat* w, uint64_t L, DMat* y, DMat* pre, 
     if (!G.graph) fail(kConfig, "forward: needs a grouping of the full graph");
     const uint64_t n = G.graph->n;
     DMat cur = x0;
-    if (x0.rows != n) fail(kConfig, "forward: feature rows != vertex count");
+    if (x0.rows != n) fail_shape("forward: feature rows != vertex count");
     for (uint64_t l = 0; l < L; ++l) {
         if (cur.cols != w[l].rows)
-            fail(kConfig, "forward: feature/weight shape mismatch at layer " + std::to_string(l));
+            fail_shape("forward: feature/weight shape mismatch at layer " + std::to_string(l));
         if (y[l].rows != n || y[l].cols != cur.cols || pre[l].rows != n || pre[l].cols != w[l].cols ||
             x[l].rows != n || x[l].cols != w[l].cols)
-            fail(kConfig, "forward: output shape mismatch at layer " + std::to_string(l));
+            fail_shape("forward: output shape mismatch at layer " + std::to_string(l));
         run_aggregate(G, false, 0, G.graph->n, cur.p, cur.ld, y[l].p, y[l].ld, cur.cols, PG_AGG_OVERWRITE, s);
         gemm(y[l], w[l], pre[l], false, s);
         if (l + 1 < L) relu(pre[l], x[l], s);
@@ -890,12 +890,12 @@ void backward_ifelse(Groups& G, Frontiers& F, const BackwardIO& io, cudaStream_t
 void backward_epp(Groups* const* PG, Frontiers& F, const BackwardIO& io, int gather_mode, uint64_t expected_fp,
                   cudaStream_t s) {
     const uint64_t L = io.L;
-    if (F.L != L) fail(kConfig, "epp backward: paths were prepared for a different layer count");
+    if (F.L != L) fail_stale("epp backward: paths were prepared for a different layer count");
     for (uint64_t i = 0; i < L; ++i) {
         if (!PG[i] || !PG[i]->path) fail(kConfig, "epp backward: every grouping must be over an execution path");
-        if (PG[i]->path->layer != L - 1 - i) fail(kConfig, "epp backward: paths were prepared for a different layer count");
+        if (PG[i]->path->layer != L - 1 - i) fail_stale("epp backward: paths were prepared for a different layer count");
         if (PG[i]->path->fingerprint != expected_fp)
-            fail(kConfig, "epp backward: execution paths are stale for this graph/training set");
+            fail_stale("epp backward: execution paths are stale for this graph/training set");
     }
     const uint64_t n = F.n;
     check_chain(io, n);
@@ -907,9 +907,18 @@ void backward_epp(Groups* const* PG, Frontiers& F, const BackwardIO& io, int gat
         for (uint64_t i = 0; i < L; ++i) {
             const uint64_t l = L - 1 - i, in_dim = io.w[l].rows;
             Path& p = *PG[i]->path;
-            if (!p.edges_global.get() && p.E) {
-                p.edges_global = DevBuf<Edge>(p.E, s);
-                remap_edges(p.edges_parent.get(), p.E, F.levels[i].ids.get(), p.edges_global.get(), s);
+            {
+                // long-lived cache: built on the library stream (where it is
+                // freed) and synchronised, under the path's lock
+                std::lock_guard<std::mutex> lk(p.mu);
+                if (!p.edges_global.get() && p.E) {
+                    cudaStream_t ls = lib_stream(p.device);
+                    PG_CUDA(cudaStreamSynchronize(s));  // F's ids are final
+                    DevBuf<Edge> eg(p.E, ls);
+                    remap_edges(p.edges_parent.get(), p.E, F.levels[i].ids.get(), eg.get(), ls);
+                    PG_CUDA(cudaStreamSynchronize(ls));
+                    p.edges_global = std::move(eg);
+                }
             }
             wgs.gemm_at_b(io.y[l], nullptr, g, io.w_grads[l]);
             Tmp yg(n, in_dim, s);
@@ -941,13 +950,13 @@ void backward_epp(Groups* const* PG, Frontiers& F, const BackwardIO& io, int gat
         const uint64_t l = L - 1 - i, in_dim = io.w[l].rows;
         Path& p = *PG[i]->path;
         if (p.P != F.levels[i].size || p.D != F.levels[i + 1].size)
-            fail(kConfig, "epp backward: path does not follow the frontiers");
+            fail_stale("epp backward: path does not follow the frontiers");
         const DMat g = gcur->m;
         wgs.gemm_at_b(io.y[l], F.levels[i].ids.get(), g, io.w_grads[l]);  // gather_rows(Y, in_rows) fused
         Tmp yg(p.P, in_dim, s);
         gemm(g, io.w[l], yg.m, true, s);
         DMat* xo = io.x_grads ? &io.x_grads[i] : nullptr;
-        if (xo && (xo->rows != p.D || xo->cols != in_dim)) fail(kConfig, "backward: x_grad shape mismatch");
+        if (xo && (xo->rows != p.D || xo->cols != in_dim)) fail_shape("backward: x_grad shape mismatch");
         std::unique_ptr<Tmp> gn;
         if (l > 0 && !xo) {  // relu_backward(x_grad, gather_rows(pre, levels[L-l])) in the SpMM epilogue
             gn = std::make_unique<Tmp>(p.D, in_dim, s);

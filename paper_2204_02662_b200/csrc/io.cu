@@ -53,9 +53,7 @@ bool parse_vertex(std::string_view tok, uint32_t& out) {
     return true;
 }
 
-[[noreturn]] void parse_error(const std::string& msg, uint64_t line) {
-    fail(kConfig, msg + " (line " + std::to_string(line) + ")");
-}
+[[noreturn]] void parse_error(const std::string& msg, uint64_t line) { fail_parse(msg, line); }
 
 // getline semantics: lines split at '\n'; a trailing fragment without '\n'
 // is a line; an empty file has none

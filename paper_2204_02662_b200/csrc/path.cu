@@ -481,6 +481,7 @@ __global__ void k_segment_bounds(const uint64_t* __restrict__ offsets, const Edg
 
 void segment_bounds(const uint64_t* offsets, const Edge* edges, uint32_t D, const uint64_t* cuts_host, uint32_t K,
                     DevBuf<uint64_t>& bnd, cudaStream_t s) {
+    retire(bnd);  // the previous bounds may still be read on a caller stream
     bnd = DevBuf<uint64_t>(static_cast<uint64_t>(D) * (K + 1), s);
     if (!D) return;
     DevBuf<uint64_t> cuts(K + 1, s);
@@ -513,6 +514,7 @@ void remap_edges(const Edge* in, uint64_t E, const uint32_t* map, Edge* out, cud
 }
 
 void path_pack_local(Path& p, cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(p.mu);
     if (p.edges_local.get() || p.E == 0 || p.S == p.P) return;
     p.edges_local = DevBuf<Edge>(p.E, s);
     k_pack_local<<<grid_for(p.E, kThreads), kThreads, 0, s>>>(p.nbr_local.get(), p.edges_parent.get(), p.E,

@@ -7,6 +7,7 @@
 
 #include <cstdint>
 #include <memory>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -100,6 +101,7 @@ struct Path {
     DevBuf<Edge> edges_global;    // E (src_local_to_global[nbr], (float)w), lazily (GatherMode::Global)
     DevBuf<uint32_t> order;       // D dests in descending-degree-bucket order (SpMM schedule)
     DegHist hist;                 // degree buckets of `order`
+    std::mutex mu;                // guards the lazily built edge streams (groupings share a path)
 };
 
 // grouping.hpp:14-28 GroupedCsr over a path (or the whole graph).
@@ -143,6 +145,11 @@ struct Groups {
     // automatic L2-sized source segments of a whole-path SpMM (api.cu)
     DevBuf<uint64_t> auto_seg_bnd;
     uint32_t auto_seg_k = 0;
+    // guards every lazily built cache above: aggregate calls on one grouping
+    // may come from several host threads (the reference's aggregate_pull takes
+    // a const GroupedCsr and is re-entrant); recursive because the segmented
+    // whole-path SpMM re-enters run_aggregate
+    std::recursive_mutex mu;
 };
 
 // seg_bnd for cuts[0..K] over the path's edge stream (binary search per

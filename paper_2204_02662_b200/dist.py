@@ -87,6 +87,26 @@ def plan(path_offsets: list, parent_rows: list, world: int, dest_bounds: list | 
     return out
 
 
+def whole_rows(t):
+    """The contiguous (rows, pitch) tensor behind a pitched row view (an
+    ``empty_rows`` matrix, or a column slice of one): NCCL point-to-point and
+    broadcast copy ``numel`` elements from ``data_ptr``, so a view with
+    ``stride(0) > shape[1]`` must be exchanged as whole padded rows. Returns
+    ``t`` itself when it is already contiguous, else None when the pitch is
+    not backed by storage (then the caller packs)."""
+    if t.is_contiguous():
+        return t
+    if t.dim() != 2 or t.stride(1) != 1 or t.stride(0) < t.shape[1]:
+        return None
+    ld = t.stride(0)
+    need = t.storage_offset() + t.shape[0] * ld
+    if t.untyped_storage().nbytes() < need * t.element_size():
+        return None
+    w = t.as_strided((t.shape[0], ld), (ld, 1))
+    assert w.is_contiguous()
+    return w
+
+
 def allgatherv_rows(full, bounds, rank, group=None):
     """Unpadded all-gather-v in place: rank r owns rows [bounds[r],
     bounds[r+1]) of `full` (frontier order); afterwards every rank holds all
@@ -103,15 +123,23 @@ def allgatherv_rows(full, bounds, rank, group=None):
         allgatherv_rows(host, bounds, rank, group)
         full.copy_(host)
         return full
+    w = whole_rows(full)
+    if w is None:  # pitch not backed by storage: exchange a packed copy
+        packed = full.contiguous()
+        allgatherv_rows(packed, bounds, rank, group)
+        full.copy_(packed)
+        return full
+    full_rows = w
     b = [int(x) for x in bounds]
-    mine = full[b[rank]:b[rank + 1]]
+    mine = full_rows[b[rank]:b[rank + 1]]
+    assert mine.is_contiguous()
     ops = []
     for r in range(world):
         if r == rank:
             continue
         if mine.shape[0]:
             ops.append(dist.P2POp(dist.isend, mine, r, group))
-        theirs = full[b[r]:b[r + 1]]
+        theirs = full_rows[b[r]:b[r + 1]]
         if theirs.shape[0]:
             ops.append(dist.P2POp(dist.irecv, theirs, r, group))
     if ops:
@@ -139,9 +167,13 @@ def bcast_rows_async(full, bounds, group=None):
                 dist.broadcast(host[b[s]:b[s + 1]], src=s, group=group)
         full.copy_(host)
         return [None] * world
+    w = whole_rows(full)
+    if w is None:
+        raise ValueError("bcast_rows_async: the row pitch of `full` is not backed by storage (pass a contiguous "
+                         "or empty_rows matrix)")
     works = []
     for s in range(world):
-        works.append(dist.broadcast(full[b[s]:b[s + 1]], src=s, group=group, async_op=True)
+        works.append(dist.broadcast(w[b[s]:b[s + 1]], src=s, group=group, async_op=True)
                      if b[s + 1] > b[s] else None)
     return works
 
@@ -152,6 +184,8 @@ def allgather_rows(shard, out, group=None):
     single-GPU rehearsal of the N>1 path) stages CUDA tensors through host."""
     import torch.distributed as dist
 
+    if not (shard.is_contiguous() and out.is_contiguous()):
+        raise ValueError("allgather_rows: shard and output must be contiguous (NCCL copies numel from data_ptr)")
     if shard.is_cuda and dist.get_backend(group) != "nccl":
         host = out.cpu()
         dist.all_gather_into_tensor(host, shard.cpu(), group=group)
@@ -161,7 +195,7 @@ def allgather_rows(shard, out, group=None):
     return out
 
 
-def backward_epp(prepared, arts, top_grad, weights, plan_, rank, group=None):
+def backward_epp(prepared, arts, top_grad, weights, plan_, rank, group=None, expected_fingerprint=None):
     """engine.hpp:316-346 (Local gather) row-sharded over the ranks of
     ``group``, bit-identical to the single-GPU ``backward_epp``.
 
@@ -180,14 +214,21 @@ def backward_epp(prepared, arts, top_grad, weights, plan_, rank, group=None):
         340-345), then one all-gather-v of the g row shards (NCCL P2P)
         assembles the next layer's g in frontier order.
     ``plan_`` is ``plan(...)`` over the paths (dest bounds per path).
+    ``expected_fingerprint`` (default: recomputed from the graph and training
+    set the paths were prepared from) must match every path's stamp, else
+    StalenessError (engine.hpp:280-283).
     Returns W' per layer (full, identical on every rank)."""
     import torch
 
     from . import pathgcn as pg
 
     L = len(weights)
-    if len(prepared.groups) != L:
+    if len(prepared.groups) != L or prepared.frontiers.L != L:
         raise pg.StalenessError("epp backward: paths were prepared for a different layer count")
+    fp = prepared.current_fingerprint() if expected_fingerprint is None else expected_fingerprint
+    for p in prepared.paths:
+        if p.fingerprint != fp:
+            raise pg.StalenessError("epp backward: execution paths are stale for this graph/training set")
     F = prepared.frontiers
     dev = top_grad.device
     lv = [torch.from_numpy(F.level(k).astype(np.int32)).to(dev) for k in range(L + 1)]
@@ -211,7 +252,7 @@ def backward_epp(prepared, arts, top_grad, weights, plan_, rank, group=None):
             break
         pre = pg.empty_rows(de - db, in_dim, device=dev)
         pg.gather_rows(arts.pre_act[l - 1], lv[i + 1][db:de], pre)
-        g = pg.empty_rows(p.D, in_dim, device=dev)
+        g = pg.empty_rows(p.D, in_dim, device=dev)  # pitched: exchanged as whole padded rows
         pg.relu_backward(x, pre, g[db:de])
         allgatherv_rows(g, plan_[i].dest_bounds, rank, group)
     return w_grads

@@ -73,22 +73,22 @@ def _lib_():
     return _lib.load()
 
 
+# PG_KIND_* (pathgcn_b200.h): the exact reference exception type of a failure
+_KINDS = {1: "ConfigError", 2: "ShapeError", 3: "StalenessError", 4: "ParseError", 5: "IoError",
+          6: "NumericError", 7: "DeviceError"}
+
+
 def _check(rc):
     if rc:
         buf = C.create_string_buffer(2048)
         _lib_().pg_last_error(buf, 2048)
         msg = buf.value.decode(errors="replace")
-        cls = _CODES.get(rc, Error)
-        if cls is ConfigError and ("rows" in msg or "dimension" in msg):
-            cls = ShapeError
-        if cls is ConfigError and "stale" in msg:
-            cls = StalenessError
-        if cls is ConfigError and msg.endswith(")") and "(line " in msg:
-            import re
-
-            m = re.search(r"\(line (\d+)\)$", msg)
-            if m:
-                raise ParseError(msg, int(m.group(1)))
+        line = C.c_uint64(0)
+        kind = _lib_().pg_last_error_kind(C.byref(line))
+        name = _KINDS.get(kind)
+        if name == "ParseError":
+            raise ParseError(msg, int(line.value))
+        cls = globals()[name] if name else _CODES.get(rc, Error)
         raise cls(msg)
 
 
@@ -676,6 +676,15 @@ class PreparedPaths:
     groups: list
     gs: list
     fingerprint: int = 0
+    graph: "CsrGraph | None" = None  # the graph and training set the paths were built from
+    vt: "np.ndarray | None" = None
+
+    def current_fingerprint(self):
+        """path_fingerprint of the graph and training set as they are now
+        (the caller-side expected_fingerprint of engine.hpp:280-283)."""
+        if self.graph is None or self.vt is None:
+            raise ConfigError("PreparedPaths without its graph/training set: pass expected_fingerprint")
+        return path_fingerprint(self.graph, self.vt, self.frontiers.L)
 
 
 def choose_gs(strategy, path: ExecutionPath, dim, workers=8, atomic_penalty=0.25):
@@ -707,7 +716,7 @@ def prepare_paths(g: CsrGraph, vt, layers, agg_dims, gs_strategy="regression", w
         gs = choose_gs(gs_strategy, p, agg_dims[i], workers, atomic_penalty)
         gss.append(gs)
         groups.append(group_neighbors(p, gs))
-    return PreparedPaths(F, paths, groups, gss, stamp)
+    return PreparedPaths(F, paths, groups, gss, stamp, g, vt)
 
 
 # ------------------------------------------------- the chain (engine.hpp) ---
@@ -818,7 +827,9 @@ def backward_epp(prepared: PreparedPaths, arts: EpochArtifacts, top_grad, weight
     L = len(weights)
     if len(prepared.groups) != L or prepared.frontiers.L != L:  # engine.hpp:278-279
         raise StalenessError("epp backward: paths were prepared for a different layer count")
-    fp = prepared.fingerprint if expected_fingerprint is None else expected_fingerprint
+    # engine.hpp:280-283: the stamp on the paths must match the fingerprint of
+    # the CURRENT graph and training set (recomputed here when not given)
+    fp = prepared.current_fingerprint() if expected_fingerprint is None else expected_fingerprint
     hs = (C.c_void_p * max(L, 1))(*[g._h.value for g in prepared.groups])
     wg = _wgrads(weights)
     xg = None

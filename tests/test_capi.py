@@ -27,7 +27,7 @@ def test_library_is_sm100a():
 
 def test_version_and_errors():
     lib = _lib.load()
-    assert lib.pg_version() == 1
+    assert lib.pg_version() == 2
     h = C.c_void_p()
     # null handles are config errors, reported through pg_last_error
     rc = lib.pg_graph_info(None, None, None, None, None)
@@ -35,7 +35,35 @@ def test_version_and_errors():
     buf = C.create_string_buffer(256)
     lib.pg_last_error(buf, 256)
     assert b"null handle" in buf.value
+    line = C.c_uint64(7)
+    assert lib.pg_last_error_kind(C.byref(line)) == 1 and line.value == 0  # PG_KIND_CONFIG
     del h
+
+
+def test_error_kinds_cross_the_abi(tmp_path):
+    """pg_last_error_kind carries the exact error.hpp type (no guessing from
+    the message text): ParseError with its line number, IoError, ShapeError —
+    and a ConfigError whose message mentions "rows" stays a ConfigError."""
+    import paper_2204_02662_b200 as pg
+
+    lib = _lib.load()
+    bad = tmp_path / "bad.txt"
+    bad.write_text("# header\n0 1\n2 x\n")
+    with pytest.raises(pg.ParseError) as ei:
+        pg.load_edge_list_file(str(bad))
+    assert ei.value.line_number == 3 and "(line 3)" in str(ei.value)
+    line = C.c_uint64()
+    assert lib.pg_last_error_kind(C.byref(line)) == 4 and line.value == 3
+    with pytest.raises(pg.IoError):
+        pg.load_edge_list_file(str(tmp_path / "missing.txt"))
+    assert lib.pg_last_error_kind(None) == 5
+    # gemm_a_bt with lda < k: ShapeError (dense_matrix.hpp:80), checked before any device work
+    f = C.POINTER(C.c_float)()
+    rc = lib.pg_gemm_a_bt(f, 2, f, 4, f, 4, 1, 1, 4, None)
+    assert rc == 2 and lib.pg_last_error_kind(None) == 2
+    # a ConfigError mentioning "rows": the kind, not the text, decides
+    rc = lib.pg_training_set_size(0, 0.5, C.byref(C.c_uint64()))
+    assert rc == 2 and lib.pg_last_error_kind(None) == 1
 
 
 def test_host_generators_match_oracle(orc):

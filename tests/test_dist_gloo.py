@@ -57,6 +57,22 @@ def _worker(rank, world, port, result_q):
             fv[pb:pe] = torch.from_numpy(y_full[pb:pe])
             pgd.allgatherv_rows(fv, sh.parent_bounds, rank)
             assert np.array_equal(fv.numpy(), y_full)
+            # the same into a PITCHED view (empty_rows layout, ld > dim): the
+            # exchange must move whole padded rows (NCCL copies numel from
+            # data_ptr), or the tail rows of every peer shard stay stale
+            ld = (dims[i] + 31) // 32 * 32 if dims[i] > 32 else (dims[i] + 3) // 4 * 4
+            buf = torch.full((P, ld + 8), float("nan"), dtype=torch.float32)
+            pv = buf[:, :dims[i]]
+            pv[pb:pe] = torch.from_numpy(y_full[pb:pe])
+            assert not pv.is_contiguous()
+            pgd.allgatherv_rows(pv, sh.parent_bounds, rank)
+            assert np.array_equal(pv.numpy(), y_full)
+            bv = torch.full((P, ld + 8), float("nan"), dtype=torch.float32)[:, :dims[i]]
+            bv[pb:pe] = torch.from_numpy(y_full[pb:pe])
+            for w in pgd.bcast_rows_async(bv, sh.parent_bounds):
+                if w is not None:
+                    w.wait()
+            assert np.array_equal(bv.numpy(), y_full)
             db, de = sh.my_dest_rows(rank)
             offs = p.offsets[db:de + 1]
             src_rows = sh.source_map[p.srcpos[p.neighbors]]  # gather folded + remapped
@@ -125,3 +141,18 @@ def test_balance_bounds_moves_cuts_toward_the_slow_shard():
     cost = lambda b0, b1: float((deg[b0:b1] * rate[b0:b1]).sum())
     cb, t0, t1 = pgd.calibrate_bounds(cost, offs, b, iters=3)
     assert max(t1) <= max(t0)
+
+
+def test_whole_rows_views():
+    """dist.whole_rows: a pitched row view maps to its contiguous padded rows
+    (a row slice of it stays contiguous); views whose pitch is not backed by
+    storage are refused so the caller packs instead."""
+    buf = torch.arange(10 * 12, dtype=torch.float32).reshape(10, 12)
+    v = buf[:, :5]
+    w = pgd.whole_rows(v)
+    assert w.is_contiguous() and w.shape == (10, 12) and w.data_ptr() == v.data_ptr()
+    assert w[3:7].is_contiguous() and torch.equal(w[3:7, :5], v[3:7])
+    assert pgd.whole_rows(buf) is buf
+    # a column slice starting past column 0 of the last row overruns storage
+    assert pgd.whole_rows(buf[:, 8:]) is None
+    assert pgd.whole_rows(buf.t()) is None

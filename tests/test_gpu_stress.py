@@ -212,3 +212,68 @@ def test_concurrent_host_calls_mixed_buffers(pg, orc):
     for t in ts:
         t.join()
     assert not errors, errors
+
+
+def test_concurrent_calls_share_one_grouping(pg, orc):
+    """Host threads calling into ONE grouping at once (the reference's
+    aggregate_pull takes a const GroupedCsr and is re-entrant): device calls
+    over distinct row ranges (each builds and caches its own schedule),
+    whole-path calls (the cached L2-sized source segments) and host-buffer
+    calls (the cached host pipeline cuts), every result bit-exact."""
+    import threading
+
+    import torch
+
+    rng = np.random.default_rng(777)
+    pairs, n_pad = rmat_pairs(orc, 20000, 20000 * 48, 21)
+    vt = orc.sample_training_set(n_pad, 0.6, 5)
+    dg = pg.build_undirected_csr(pairs, n_hint=n_pad, weights="symnorm")
+    og = orc.build_graph(pairs, n_hint=n_pad, symnorm=True)
+    F = pg.compute_frontiers(dg, vt, 2)
+    op = orc.prepare_all_paths(og, orc.compute_frontiers(og, vt, 2))[1]
+    dp = pg.prepare_all_paths(dg, F)[1]
+    dim = 300
+    G = pg.group_neighbors(dp, 8)
+    y = rng.uniform(-1, 1, size=(dp.P, dim)).astype(np.float32)
+    want = orc.aggregate_pull_f32(op.offsets, op.neighbors, op.weights, y[op.srcpos])
+    yd = pg.empty_rows(dp.P, dim)
+    yd.copy_(torch.from_numpy(y))
+    cuts = sorted(set(rng.integers(0, dp.D, 24).tolist()) | {0, dp.D})
+    ranges = [(cuts[i], cuts[i + 1]) for i in range(len(cuts) - 1) if cuts[i + 1] > cuts[i]]
+    errors = []
+
+    def dev_job(rs):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                for rb, re in rs:
+                    x = pg.empty_rows(re - rb, dim)
+                    pg.backward_aggregation(G, yd, x, overwrite=True, rows=(rb, re), stream=st)
+                    st.synchronize()
+                    if not np.array_equal(bits(x.cpu().numpy()), bits(want[rb:re])):
+                        errors.append(("rows", rb, re))
+                x = pg.empty_rows(dp.D, dim)
+                pg.backward_aggregation(G, yd, x, overwrite=True, stream=st)
+                st.synchronize()
+                if not np.array_equal(bits(x.cpu().numpy()), bits(want)):
+                    errors.append("whole")
+        except Exception as e:  # pragma: no cover
+            errors.append(repr(e))
+
+    def host_job():
+        try:
+            for _ in range(2):
+                x = np.full(want.shape, np.nan, np.float32)
+                pg.backward_aggregation(G, y, x, overwrite=True)
+                if not np.array_equal(bits(x), bits(want)):
+                    errors.append("host")
+        except Exception as e:  # pragma: no cover
+            errors.append(repr(e))
+
+    ts = [threading.Thread(target=dev_job, args=(ranges[k::4],)) for k in range(4)]
+    ts += [threading.Thread(target=host_job) for _ in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
