@@ -72,6 +72,40 @@ def agg_dims(cfg):
     return [in_dims[L - 1 - i] for i in range(L)]
 
 
+def grad_input(P, dim, i, seed=GRAD_SEED):
+    """The stage input of path i: y_grad ~ U(-1,1) fp32, P x dim (SURVEY §8d:
+    the zero-mean stress input). tests/golden/make_fullsize_digests.py feeds
+    the reference these very bytes, so the benchmarked x_grad can be checked
+    against the reference's digest (`parity` in the bench line)."""
+    return np.random.default_rng(seed * 1000 + i).uniform(-1.0, 1.0, size=(P, dim)).astype(np.float32)
+
+
+def reference_digest(config):
+    """Committed digests of the reference's own outputs at this config
+    (tests/golden/fullsize_<config>.json), or None."""
+    p = os.path.join(ROOT, "tests", "golden", f"fullsize_{config}.json")
+    try:
+        return json.load(open(p))
+    except Exception:
+        return None
+
+
+def x_grad_parity(x_out, dims, config):
+    """sha256 of each benchmarked path's x_grad vs the reference digest."""
+    import hashlib
+
+    want = reference_digest(config)
+    if want is None:
+        return None
+    res = []
+    for i, x in enumerate(x_out):
+        a = np.ascontiguousarray(x.cpu().numpy()[:, : dims[i]])
+        res.append(hashlib.sha256(a.view(np.uint8).reshape(-1)).hexdigest() == want["paths"][i]["x_grad"]["sha256"])
+    return {"x_grad_equals_reference": res, "all": all(res),
+            "source": f"tests/golden/fullsize_{config}.json (the reference's x_grad of the same inputs, "
+                      f"tests/golden/make_fullsize_digests.py)"}
+
+
 def path_bytes(D, E, dim):
     """Algorithmic bytes of one path's stage (SURVEY §8d B_l): offsets, 4 B
     source index + 4 B fp32 weight per edge, one gathered source row per edge,
@@ -91,21 +125,38 @@ def hbm_peak():
         return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic():
-    """dram read+write bytes per launch of the dominant kernel, from the
-    committed ncu --set full summary (profiles/)."""
+def ncu_capture(config):
+    """The committed ncu --set full summary of THIS config's dominant path
+    (profiles/ncu_full_<config>_rNN*.json, newest first): DRAM read+write
+    bytes per path execution plus the throughput counters that name the
+    binding unit. None when no capture of this config is committed."""
     import glob
 
-    best = None
-    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_full_*.json"))):
+    fs = sorted(glob.glob(os.path.join(ROOT, "profiles", f"ncu_full_{config}_r*.json")))
+    for f in reversed(fs):
         try:
             d = json.load(open(f))
-            best = d
         except Exception:
-            pass
-    if best and "dram_bytes_per_launch" in best:
-        return best["dram_bytes_per_launch"], os.path.basename(f)
-    return None, None
+            continue
+        if "dram_bytes_per_launch" in d:
+            d["_file"] = os.path.relpath(f, ROOT)
+            return d
+    return None
+
+
+def physical_cores():
+    """Physical host cores available to this process (lscpu CORE,SOCKET
+    pairs, capped by the CPU affinity mask): BASELINE.md §3's thread count."""
+    try:
+        out = subprocess.run(["lscpu", "-p=CORE,SOCKET"], capture_output=True, text=True, timeout=10).stdout
+        cores = len({ln for ln in out.splitlines() if ln and not ln.startswith("#")})
+    except Exception:
+        cores = 0
+    try:
+        avail = len(os.sched_getaffinity(0))
+    except Exception:
+        avail = os.cpu_count() or 1
+    return max(1, min(cores or avail, avail))
 
 
 # ------------------------------------------------------------------ clocks --
@@ -194,16 +245,20 @@ def run_reference(args):
     rng = np.random.default_rng(GRAD_SEED)
     ys = [rng.uniform(-1, 1, size=(len(lv[i]), dims[i])).astype(np.float32) for i in range(L)]
     setup_s = time.time() - t0
-    threads = R.max_threads()
+    threads = physical_cores()
     bytes_step = sum(path_bytes(it["D"], it["E"], dims[i]) for i, it in enumerate(items))
+    full_items = R.backward_stage_handles(g, vt, L, sample_stride=1) if args.sample_stride > 1 else items
+    full_bytes = sum(path_bytes(it["D"], it["E"], dims[i]) for i, it in enumerate(full_items))
+    if full_items is not items:
+        R.free_stage_handles(full_items)
     for _ in range(args.warmup):
         for i, it in enumerate(items):
-            R.run_backward_stage(it, ys[i])
+            R.run_backward_stage(it, ys[i], workers=threads)
     times = []
     for _ in range(args.steps):
         s = 0.0
         for i, it in enumerate(items):
-            sec, _ = R.run_backward_stage(it, ys[i])
+            sec, _ = R.run_backward_stage(it, ys[i], workers=threads)
             s += sec
         times.append(s)
     R.free_stage_handles(items)
@@ -217,10 +272,13 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": workload_config(cfg, args, [it["gs"] for it in items]),
         "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
-                         "sample": sample},
+                         "sample": sample, "cores_source": "lscpu physical cores (CORE,SOCKET), affinity-capped"},
         "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "setup_s": round(setup_s, 1),
-        "ms_per_epoch_extrapolated": round(step_s * 1e3 * args.sample_stride, 1),
+        # the sample's share of the epoch's algorithmic bytes, not the stride:
+        # a degree-ordered stride sample keeps ~1/8 of the edges at stride 16
+        "sample_byte_share": round(bytes_step / full_bytes, 5),
+        "ms_per_epoch_extrapolated": round(step_s * 1e3 * full_bytes / bytes_step, 1),
     }
     print(json.dumps(line), flush=True)
 
@@ -229,7 +287,8 @@ def workload_config(cfg, args, gs):
     return {"workload": f"{args.config}-shaped", "V": cfg["V"], "E_directed": cfg["m"], "L": len(cfg["dims"]),
             "f": cfg["f"], "dims": cfg["dims"], "agg_widths": agg_dims(cfg), "train_ratio": round(train_ratio(cfg), 4),
             "weights": "sym-norm", "gs": gs, "gs_strategy": "regression",
-            "l2": "inputs larger than L2 (each step streams the layer-0 y_grad/x_grad, > 1 GB at reddit)",
+            "l2": "no flush between steps; per-step inputs (y_grad + x_grad + edge records) exceed the 126 MB L2 at "
+                  "the reddit and products shapes (> 1 GB); arxiv/cora/pubmed are L2-resident",
             "parallelism": (f"dest-row shards x{args.gpus} (edge-balanced) + per-path NCCL all-gather-v of y_grad rows "
                              f"({os.environ.get('PG_ALLGATHER', 'p2p')})") if args.gpus > 1 else "1 GPU"}
 
@@ -336,8 +395,6 @@ def main():
             del yt
     parent_rows = [p.P for p in paths]
     shards = pgd.plan([None] * L, parent_rows, world, dest_bounds)
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(GRAD_SEED)
     # PG_ALLGATHER=p2p (default): unpadded all-gather-v straight into
     # frontier order; =padded: equal-size all_gather + remapped edge stream
     xmode = os.environ.get("PG_ALLGATHER", "p2p")  # p2p | padded | bcast
@@ -347,16 +404,17 @@ def main():
         ld = pg.padded_ld(dims[i])
         sh = shards[i]
         pb, pe = sh.my_parent_rows(rank)
+        yh = torch.from_numpy(grad_input(p.P, dims[i], i))  # the digests' exact input
         if world > 1 and padded:
             groups[i].remap_sources(sh.source_map, sh.gathered_rows)
             ys = torch.zeros((sh.max_rows, ld), dtype=torch.float32, device=dev)
-            ys[: pe - pb, : dims[i]].uniform_(-1, 1, generator=gen)
+            ys[: pe - pb, : dims[i]].copy_(yh[pb:pe])
             y_shard.append(ys)
             y_full.append(torch.empty((sh.gathered_rows, ld), dtype=torch.float32, device=dev))
             rows.append(sh.my_dest_rows(rank))
         elif world > 1:
             yf = torch.zeros((p.P, ld), dtype=torch.float32, device=dev)
-            yf[pb:pe, : dims[i]].uniform_(-1, 1, generator=gen)
+            yf[pb:pe, : dims[i]].copy_(yh[pb:pe])
             y_shard.append(None)
             y_full.append(yf)
             rows.append(sh.my_dest_rows(rank))
@@ -364,11 +422,12 @@ def main():
                 groups[i].set_segments(sh.parent_bounds)
         else:
             yf = torch.zeros((p.P, ld), dtype=torch.float32, device=dev)
-            yf[:, : dims[i]].uniform_(-1, 1, generator=gen)
+            yf[:, : dims[i]].copy_(yh)
             y_shard.append(yf)
             y_full.append(yf)
             rows.append((0, p.D))
         x_out.append(pg.empty_rows(rows[i][1] - rows[i][0], dims[i], device=dev))
+        del yh
 
     stream = torch.cuda.current_stream()
 
@@ -454,7 +513,12 @@ def main():
     dom_ms = statistics.mean(spmm_ms[dom])
     peak, peak_src = hbm_peak()
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9
-    traffic, traffic_src = ncu_traffic()
+    if (db, de) == (0, p.D):
+        dom_comp = compulsory_bytes(p.D, p.S, p.E, dims[dom])
+    else:
+        dom_comp = None
+    cap = ncu_capture(args.config) if world == 1 else None
+    traffic = cap["dram_bytes_per_launch"] if cap else None
     l2c = None
     try:
         gc = json.load(open(os.path.join(ROOT, "profiles", "gather_ceiling_r01.json")))
@@ -462,20 +526,43 @@ def main():
                "source": "profiles/gather_ceiling_r01.json: " + gc["l2_ceiling_note"]}
     except Exception:
         pass
-    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": traffic if world == 1 else None,
+    # The no-reuse byte count B over-counts DRAM whenever the
+    # gathered rows are reused out of L2: B/t above the HBM peak then only
+    # says the gathers hit L2. The physical picture is the ncu DRAM traffic
+    # of the same path execution (dram_frac) and the unit that binds.
+    l2_resident = achieved > peak
+    roofline = {"bound": "l2-gather" if l2_resident else "hbm", "achieved": round(achieved, 1), "peak": peak,
+                "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                 "kernel": f"k_agg_vec4 (path SG_{p.layer}, width {dims[dom]})",
                 "algorithmic_bytes_per_launch": dom_bytes, "avg_launch_ms": round(dom_ms, 4),
-                "peak_source": peak_src, "traffic_source": traffic_src,
+                "peak_source": peak_src,
+                "frac_note": ("frac = no-reuse algorithmic bytes (SURVEY §8d B_l) / avg launch time / HBM peak; "
+                              "> 1 means the row gathers are served from L2 (L2-resident), see dram_frac"),
                 "frac_vs_8TBps_spec": round(achieved / 8000.0, 4),
+                "compulsory_bytes_per_launch": dom_comp,
+                "compulsory_frac": round(dom_comp / (dom_ms / 1e3) / 1e9 / peak, 4) if dom_comp else None,
                 "l2_gather_ceiling": l2c}
+    if cap:
+        roofline.update({
+            "traffic_source": cap["_file"] + " (ncu --set full of one execution of this path, same kernels)",
+            # DRAM bytes the path really moved, at this run's launch time
+            "dram_frac": round(traffic / (dom_ms / 1e3) / 1e9 / peak, 4),
+            "dram_GBps": round(traffic / (dom_ms / 1e3) / 1e9, 1),
+            "traffic_over_compulsory": round(traffic / dom_comp, 2) if dom_comp else None,
+            "binding_unit": cap.get("binding_unit"),
+            "binding_unit_pct": cap.get("binding_unit_pct"),
+            "l2_hit_rate_pct": cap.get("l2_hit_rate_pct"),
+            "sectors_per_request": cap.get("sectors_per_request"),
+        })
+    else:
+        roofline["traffic_source"] = f"no ncu capture of config {args.config} committed"
 
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32",
         "data": "synthetic: exact-V RMAT(.45/.22/.22/.11, seed 7), sym-norm weights, "
-                "V_t = sample_training_set(V, ratio, 42), y_grad ~ U(-1,1) fp32",
+                "V_t = sample_training_set(V, ratio, 42), y_grad ~ U(-1,1) fp32 (bench.grad_input)",
         "config": workload_config(cfg, args, prep.gs),
         "roofline": roofline,
         "gpu_launches": launches,
@@ -491,6 +578,8 @@ def main():
         "paths": [{"layer": p.layer, "D": p.D, "S": p.S, "E": p.E, "gs": prep.gs[i]} for i, p in enumerate(paths)],
     }
 
+    if world == 1:
+        line["parity"] = x_grad_parity(x_out, dims, args.config)
     if not args.profile and not args.no_e2e:
         line["e2e"] = measure_e2e(pg, pgd, torch, dist, paths, groups, shards, dims, rows, world, rank, dev,
                                   max(3, min(args.steps, 10)), ep_bytes)
@@ -960,20 +1049,24 @@ def cpu_baseline(paths, dims, args):
         arrays.append(x)
     items = R.stage_items_from_arrays(arrays, sample_stride=args.sample_stride)
     del arrays
+    threads = physical_cores()
     rng = np.random.default_rng(GRAD_SEED)
     ys = [rng.uniform(-1, 1, size=(p.P, dims[i])).astype(np.float32) for i, p in enumerate(paths)]
     for i, it in enumerate(items):
-        R.run_backward_stage(it, ys[i])
+        R.run_backward_stage(it, ys[i], workers=threads)
     times = []
     for _ in range(args.cpu_steps):
-        times.append(sum(R.run_backward_stage(it, ys[i])[0] for i, it in enumerate(items)))
+        times.append(sum(R.run_backward_stage(it, ys[i], workers=threads)[0] for i, it in enumerate(items)))
     sec = statistics.median(times)
     b = sum(path_bytes(it["D"], it["E"], dims[i]) for i, it in enumerate(items))
-    out = {"value": round(b / sec / 1e9, 3), "unit": "GB/s", "cores": R.max_threads(), "kind": "reference",
+    full_b = sum(path_bytes(p.D, p.E, dims[i]) for i, p in enumerate(paths))
+    out = {"value": round(b / sec / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
+           "cores_source": "lscpu physical cores (CORE,SOCKET), affinity-capped; OpenMP workers = cores",
            "sample": f"every {args.sample_stride}th destination of each path (D={[it['D'] for it in items]}, "
                      f"E={[it['E'] for it in items]}); median of {args.cpu_steps} after 1 warm-up",
            "ms_per_sample_epoch": round(sec * 1e3, 2),
-           "ms_per_epoch_extrapolated": round(sec * 1e3 * args.sample_stride, 1)}
+           "sample_byte_share": round(b / full_b, 5),
+           "ms_per_epoch_extrapolated": round(sec * 1e3 * full_b / b, 1)}
     R.free_stage_handles(items)
     # the same stage on one host thread (all cores and 1 thread),
     # on a sample 8x sparser so it stays a few seconds
@@ -992,7 +1085,8 @@ def cpu_baseline(paths, dims, args):
     b1 = sum(path_bytes(it["D"], it["E"], dims[i]) for i, it in enumerate(items))
     out["single_thread"] = {"value": round(b1 / t1 / 1e9, 3), "unit": "GB/s", "cores": 1,
                             "sample": f"every {stride1}th destination of each path",
-                            "ms_per_epoch_extrapolated": round(t1 * 1e3 * stride1, 1)}
+                            "sample_byte_share": round(b1 / full_b, 5),
+                            "ms_per_epoch_extrapolated": round(t1 * 1e3 * full_b / b1, 1)}
     R.free_stage_handles(items)
     return out
 

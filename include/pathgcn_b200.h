@@ -274,6 +274,15 @@ int pg_backward_aggregate_segment(pg_groups G, uint32_t seg, uint32_t row_begin,
 /* dense_matrix.hpp:78-95 gemm_a_bt: out[n x m] = a[n x k] * b[m x k]^T */
 int pg_gemm_a_bt(const float* a, uint64_t lda, const float* b, uint64_t ldb, float* out,
                  uint64_t ldo, uint64_t n, uint64_t m, uint64_t k, void* stream);
+/* gemm_a_bt with flags: PG_GEMM_TF32X3 runs it on the tensor cores
+ * (tcgen05.mma kind::tf32, operands split hi + lo, 3 MMAs per K step, fp32
+ * accumulation in TMEM): within the reference's 1e-5 relative / 1e-6
+ * absolute fp32 tolerance of the exact product, NOT bit-exact (the K sum is
+ * re-associated). Needs a 16-byte aligned a with lda % 4 == 0. flags 0 =
+ * pg_gemm_a_bt (bit-exact). */
+#define PG_GEMM_TF32X3 1u
+int pg_gemm_a_bt_ex(const float* a, uint64_t lda, const float* b, uint64_t ldb, float* out,
+                    uint64_t ldo, uint64_t n, uint64_t m, uint64_t k, unsigned flags, void* stream);
 /* dense_matrix.hpp:114-121 relu_backward */
 int pg_relu_backward(const float* grad, uint64_t ldg, const float* pre, uint64_t ldp, float* out,
                      uint64_t ldo, uint64_t rows, uint64_t cols, void* stream);

@@ -126,6 +126,7 @@ SIGNATURES = {
     "pg_groups_set_segments": [H, u64p, u32],
     "pg_backward_aggregate_segment": [H, u32, u32, u32, vp, u64, u64, vp, u64, u64, C.c_uint, vp],
     "pg_gemm_a_bt": [vp, u64, vp, u64, vp, u64, u64, u64, u64, vp],
+    "pg_gemm_a_bt_ex": [vp, u64, vp, u64, vp, u64, u64, u64, u64, C.c_uint, vp],
     "pg_relu_backward": [vp, u64, vp, u64, vp, u64, u64, u64, vp],
     "pg_gather_rows": [vp, u64, vp, u64, vp, u64, u64, vp],
     "pg_path_device_arrays": [H, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)],

@@ -56,8 +56,11 @@ constexpr TuneKey kTuneKeys[] = {
     {"gemm_packed", "PG_GEMM_PACKED", 1},  // gemm / gemm_a_bt: 1 = FFMA2/FADD2 column pairs (k_gemm2), 0 = k_gemm
     {"host_last_seg_pct", "PG_HOST_LAST_SEG_PCT", 40},  // host drop-in: % of the edges in the last (chunked) segment, 0 = 1/K
     {"wgrad_fork", "PG_WGRAD_FORK", 1},  // backward chains: W' GEMMs on a forked stream (1) or in order (0)
+    // chain y_grad = g W^T (gemm_a_bt): 0 = bit-exact FFMA2 kernel, 1 = tcgen05
+    // 3xTF32 tensor-core kernel (fp32 tolerance, not bit-exact)
+    {"gemm_tc", "PG_GEMM_TC", 0},
 };
-static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneWgradFork + 1,
+static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneGemmTc + 1,
               "kTuneKeys and enum TuneKeyId (pg_internal.h) must list the same keys in the same order");
 std::atomic<int64_t> g_tune[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];
 int64_t g_tune_def[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];  // $PG_<KEY> at load, else built-in

@@ -1432,6 +1432,20 @@ int pg_gemm_a_bt(const float* a, uint64_t lda, const float* b, uint64_t ldb, flo
     });
 }
 
+int pg_gemm_a_bt_ex(const float* a, uint64_t lda, const float* b, uint64_t ldb, float* out, uint64_t ldo,
+                    uint64_t n, uint64_t m, uint64_t k, unsigned flags, void* stream) {
+    return guard([&] {
+        if (lda < k || ldb < k || ldo < m) fail_shape("gemm_a_bt: leading dimension too small");
+        if (flags & ~PG_GEMM_TF32X3) fail(kConfig, "gemm_a_bt: unknown flags");
+        const DMat A{const_cast<float*>(a), n, k, lda}, B{const_cast<float*>(b), m, k, ldb}, O{out, n, m, ldo};
+        if (flags & PG_GEMM_TF32X3) {
+            gemm_a_bt_tc(A, B, O, static_cast<cudaStream_t>(stream));
+        } else {
+            gemm(A, B, O, true, static_cast<cudaStream_t>(stream));
+        }
+    });
+}
+
 int pg_relu_backward(const float* grad, uint64_t ldg, const float* pre, uint64_t ldp, float* out, uint64_t ldo,
                      uint64_t rows, uint64_t cols, void* stream) {
     return guard([&] { relu_backward(grad, ldg, pre, ldp, out, ldo, rows, cols, static_cast<cudaStream_t>(stream)); });

@@ -624,6 +624,11 @@ void gemm(DMat a, DMat b, DMat out, bool b_transposed, cudaStream_t s) {
         PG_CUDA(cudaMemset2DAsync(out.p, out.ld * 4, 0, m * 4, n, s));
         return;
     }
+    // y_grad = g W^T on the tensor cores when selected (tolerance, not bits)
+    if (b_transposed && tuning(kTuneGemmTc) == 1 && gemm_a_bt_tc_supported(a)) {
+        gemm_a_bt_tc(a, b, out, s);
+        return;
+    }
     // 64-column tiles waste most of a narrow output (m <= 32: the forward's
     // X W at width 16 runs 1.01 ms packed vs 0.61 ms scalar)
     if (tuning(kTuneGemmPacked) && m > kGT) {

@@ -1,0 +1,446 @@
+// Tensor-core gemm_a_bt (dense_matrix.hpp:78-95: out[n x m] = a[n x K] *
+// b[m x K]^T) on the 5th-generation tensor cores: tcgen05.mma kind::tf32
+// with the fp32 operands split 3 ways (3xTF32) so the product keeps ~fp32
+// accuracy: a = ah + al with ah = a with its low 13 mantissa bits cleared
+// (exactly a TF32 value) and al = a - ah (exact in fp32), likewise b, and
+//   a.b ~= ah.bh + ah.bl + al.bh        (the al.bl term is below 2^-22 |a||b|)
+// accumulated in fp32 in TMEM. This re-associates the K sum, so it is NOT
+// bit-exact with the reference's serial chain: it is selected explicitly
+// (PG_GEMM_TF32X3 / tuning "gemm_tc") and gated by the 1e-5 relative /
+// 1e-6 absolute tolerance against the f64 product (tests/test_gpu_gemm_tc.py).
+// The default gemm_a_bt stays the bit-exact FFMA2 kernel (engine.cu).
+//
+// Persistent, warp-specialised CTA (one per SM, 320 threads):
+//   warp 0      TMA producer: per stage, the raw fp32 A tile(s) [128 x 32]
+//               (cp.async.bulk.tensor, SWIZZLE_128B, out-of-bounds rows and
+//               K columns zero-filled) and the pre-split B image of this
+//               (N tile, k block) (one cp.async.bulk of hi + lo);
+//   warp 1      TMEM allocation + the single MMA-issuing thread: per stage
+//               3 x 4 tcgen05.mma (K = 8 each) per 128-row sub-tile into a
+//               double-buffered TMEM accumulator, tcgen05.commit frees the
+//               stage and, after the last k block, hands the tile to ...
+//   warps 2-5   splitters: ah in place, al into its own buffer (the same
+//               swizzled position: the split is element-wise), then
+//               fence.proxy.async so the tensor core sees the generic writes;
+//   warps 6-9   epilogue: tcgen05.ld 32x32b (warp w reads TMEM lanes
+//               32*(w%4)..), streaming 128-bit stores of the fp32 rows,
+//               overlapped with the next tile's MMAs (second accumulator).
+#include <cuda.h>
+
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "../../include/pathgcn_b200.h"
+#include "pg_internal.h"
+
+namespace pg {
+
+namespace {
+
+constexpr int kTcThreads = 320;
+constexpr int kKB = 32;             // fp32 elements per k block = one 128-byte swizzle row
+constexpr int kTileBytesA = 128 * 128;  // one 128-row x 32-float sub-tile
+constexpr int kMaxN = 256;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "TC_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra.uni TC_DONE;\n\t"
+        "bra.uni TC_WAIT;\n"
+        "TC_DONE:\n\t}" ::"r"(smem_addr(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_addr(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(smem_addr(bar))
+        : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
+
+// SWIZZLE_128B, K-major shared-memory matrix descriptor (tcgen05 format):
+// start address >> 4, LBO = 1 (unused for swizzled K-major), SBO = 1024 B
+// between 8-row groups, version 1 (bits 46-47), layout type 2 = 128B swizzle.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+    d |= static_cast<uint64_t>(1) << 16;
+    d |= static_cast<uint64_t>(1024 >> 4) << 32;
+    d |= static_cast<uint64_t>(1) << 46;
+    d |= static_cast<uint64_t>(2) << 61;
+    return d;
+}
+
+// instruction descriptor, kind::tf32: D f32 (bits 4-5 = 1), A/B TF32 (bits
+// 7-9, 10-12 = 2), both K-major, N >> 3 at bits 17-22, M >> 4 at bits 24-28
+__host__ __device__ constexpr uint32_t tf32_idesc(uint32_t M, uint32_t N) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_addr(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ uint32_t tf32_hi(uint32_t x) { return x & 0xFFFFE000u; }
+
+template <int MT>
+struct TcShape {
+    static constexpr int kABytes = MT * kTileBytesA;  // raw (-> hi) A of one stage; lo the same again
+};
+
+// B image of one (N tile, k block): hi then lo, each N rows x 128 bytes,
+// K-major SWIZZLE_128B (16-byte chunk c of row r at chunk c ^ (r & 7)).
+__global__ void k_tc_pack_b(const float* __restrict__ b, uint64_t ldb, uint32_t m, uint32_t K, uint32_t N,
+                            uint32_t NT, uint32_t KB, float* __restrict__ img) {
+    const uint64_t total = static_cast<uint64_t>(NT) * KB * N * kKB;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t k = static_cast<uint32_t>(i % kKB);
+        const uint32_t r = static_cast<uint32_t>((i / kKB) % N);
+        const uint32_t kb = static_cast<uint32_t>((i / (kKB * static_cast<uint64_t>(N))) % KB);
+        const uint32_t nt = static_cast<uint32_t>(i / (kKB * static_cast<uint64_t>(N) * KB));
+        const uint32_t row = nt * N + r, col = kb * kKB + k;
+        const float v = (row < m && col < K) ? b[row * ldb + col] : 0.f;
+        const uint32_t hb = tf32_hi(__float_as_uint(v));
+        const float hi = __uint_as_float(hb), lo = __fsub_rn(v, hi);
+        const uint64_t stage = (static_cast<uint64_t>(nt) * KB + kb) * (2ull * N * kKB);
+        const uint32_t pos = r * kKB + (((k >> 2) ^ (r & 7)) << 2) + (k & 3);
+        img[stage + pos] = hi;
+        img[stage + static_cast<uint64_t>(N) * kKB + pos] = lo;
+    }
+}
+
+struct TcParams {
+    float* out;
+    uint64_t ldo;
+    uint64_t n, m;
+    uint32_t N;         // N tile (multiple of 8, <= 256)
+    uint32_t NT, KB;    // N tiles, k blocks
+    uint32_t stages;
+    uint32_t acc_stride;  // TMEM columns per accumulator (>= N, multiple of 32)
+    uint64_t row_tiles;
+    const float* bimg;
+    int vec_out;
+};
+
+template <int MT>
+__global__ void __launch_bounds__(kTcThreads, 1) k_gemm_abt_tc(const __grid_constant__ CUtensorMap amap, TcParams P) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    // 1024-byte alignment for the 128B swizzle atoms
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t N = P.N, S = P.stages;
+    const uint32_t bbytes = 2u * N * 128u;
+    const uint32_t stage_bytes = 2u * TcShape<MT>::kABytes + bbytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
+    uint64_t* full = bars;            // [S] TMA landed
+    uint64_t* split = bars + S;       // [S] hi/lo written
+    uint64_t* empty = bars + 2 * S;   // [S] MMAs done reading
+    uint64_t* tfull = bars + 3 * S;   // [2] accumulator ready
+    uint64_t* tempty = bars + 3 * S + 2;  // [2] accumulator drained
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
+
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (uint32_t s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&split[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {  // 512 TMEM columns: two accumulators of MT x acc_stride
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_addr(tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    const uint64_t tiles = P.row_tiles * P.NT;
+    if (warp == 0) {
+        if (lane == 0) {
+            uint32_t q = 0;
+            for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+                const uint32_t nt = static_cast<uint32_t>(t % P.NT);
+                const uint64_t rt = t / P.NT;
+                for (uint32_t kb = 0; kb < P.KB; ++kb, ++q) {
+                    const uint32_t s = q % S, ph = (q / S) & 1;
+                    mbar_wait(&empty[s], ph ^ 1);
+                    unsigned char* st = smem + s * stage_bytes;
+                    mbar_arrive_tx(&full[s], TcShape<MT>::kABytes + bbytes);
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt)
+                        tma_load_2d(st + mt * kTileBytesA, &amap, static_cast<int>(kb * kKB),
+                                    static_cast<int>(rt * 128 * MT + mt * 128), &full[s]);
+                    bulk_load(st + 2 * TcShape<MT>::kABytes,
+                              P.bimg + (static_cast<uint64_t>(nt) * P.KB + kb) * (2ull * N * kKB), bbytes, &full[s]);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t idesc = tf32_idesc(128, N);
+            uint32_t q = 0, it = 0;
+            for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+                const uint32_t buf = it & 1, bph = (it >> 1) & 1;
+                mbar_wait(&tempty[buf], bph ^ 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                for (uint32_t kb = 0; kb < P.KB; ++kb, ++q) {
+                    const uint32_t s = q % S, ph = (q / S) & 1;
+                    mbar_wait(&split[s], ph);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const unsigned char* st = smem + s * stage_bytes;
+                    const uint32_t a_hi = smem_addr(st), a_lo = a_hi + TcShape<MT>::kABytes;
+                    const uint32_t b_hi = a_hi + 2 * TcShape<MT>::kABytes, b_lo = b_hi + N * 128;
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt) {
+                        const uint32_t d = tmem + (buf * MT + mt) * P.acc_stride;
+#pragma unroll
+                        for (int k = 0; k < kKB / 8; ++k) {  // K = 8 per MMA: 32 bytes along the swizzled row
+                            const uint32_t ko = k * 32;
+                            const uint32_t acc0 = (kb | k) ? 1u : 0u;
+                            const uint64_t ah = sw128_desc(a_hi + mt * kTileBytesA + ko);
+                            const uint64_t al = sw128_desc(a_lo + mt * kTileBytesA + ko);
+                            const uint64_t bh = sw128_desc(b_hi + ko), bl = sw128_desc(b_lo + ko);
+                            mma_tf32(d, ah, bh, idesc, acc0);
+                            mma_tf32(d, ah, bl, idesc, 1u);
+                            mma_tf32(d, al, bh, idesc, 1u);
+                        }
+                    }
+                    mma_commit(&empty[s]);  // stage s free once these MMAs have read it
+                }
+                mma_commit(&tfull[buf]);  // accumulator complete
+            }
+        }
+    } else if (warp < 6) {
+        // splitters: 128 threads, 16-byte chunks of the stage's A tile(s)
+        const uint32_t tid = threadIdx.x - 64;
+        uint32_t q = 0;
+        for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+            for (uint32_t kb = 0; kb < P.KB; ++kb, ++q) {
+                const uint32_t s = q % S, ph = (q / S) & 1;
+                mbar_wait(&full[s], ph);
+                uint4* hi = reinterpret_cast<uint4*>(smem + s * stage_bytes);
+                uint4* lo = reinterpret_cast<uint4*>(smem + s * stage_bytes + TcShape<MT>::kABytes);
+#pragma unroll 4
+                for (uint32_t c = tid; c < TcShape<MT>::kABytes / 16; c += 128) {
+                    uint4 v = hi[c];
+                    uint4 h, l;
+                    h.x = tf32_hi(v.x);
+                    h.y = tf32_hi(v.y);
+                    h.z = tf32_hi(v.z);
+                    h.w = tf32_hi(v.w);
+                    l.x = __float_as_uint(__fsub_rn(__uint_as_float(v.x), __uint_as_float(h.x)));
+                    l.y = __float_as_uint(__fsub_rn(__uint_as_float(v.y), __uint_as_float(h.y)));
+                    l.z = __float_as_uint(__fsub_rn(__uint_as_float(v.z), __uint_as_float(h.z)));
+                    l.w = __float_as_uint(__fsub_rn(__uint_as_float(v.w), __uint_as_float(h.w)));
+                    hi[c] = h;
+                    lo[c] = l;
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (tid == 0) mbar_arrive(&split[s]);
+            }
+        }
+    } else {
+        // epilogue: warp w reads TMEM lanes 32*(w%4) .. +31 = rows of the sub-tile
+        const uint32_t quarter = warp & 3;
+        uint32_t it = 0;
+        for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+            const uint32_t buf = it & 1, bph = (it >> 1) & 1;
+            const uint32_t nt = static_cast<uint32_t>(t % P.NT);
+            const uint64_t rt = t / P.NT;
+            mbar_wait(&tfull[buf], bph);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint64_t col0 = static_cast<uint64_t>(nt) * N;
+            for (int mt = 0; mt < MT; ++mt) {
+                const uint64_t row = rt * 128 * MT + mt * 128 + quarter * 32 + lane;
+                const uint32_t tbase = tmem + ((quarter * 32) << 16) + (buf * MT + mt) * P.acc_stride;
+                float* orow = P.out + row * P.ldo + col0;
+                for (uint32_t c = 0; c < N; c += 32) {
+                    uint32_t v[32];
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+                        "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+                        "%30, %31}, [%32];"
+                        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+                          "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+                          "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+                          "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                        : "r"(tbase + c));
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    if (row >= P.n) continue;
+                    const uint64_t cg = col0 + c;
+                    if (P.vec_out && c + 32 <= N && cg + 32 <= P.m) {
+#pragma unroll
+                        for (int j = 0; j < 32; j += 4)
+                            __stcs(reinterpret_cast<float4*>(orow + c + j),
+                                   make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
+                                               __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3])));
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (c + j < N && cg + j < P.m) orow[c + j] = __uint_as_float(v[j]);
+                    }
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[buf]);
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiled encode_fn() {
+    static EncodeTiled fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiled>(p);
+        else
+            cudaGetLastError();
+    });
+    return fn;
+}
+
+template <int MT>
+void launch_tc(const CUtensorMap& amap, const TcParams& p, size_t smem, unsigned grid, cudaStream_t s) {
+    static std::vector<char> attr;  // per device
+    static std::mutex mu;
+    int dev = 0;
+    PG_CUDA(cudaGetDevice(&dev));
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (static_cast<int>(attr.size()) <= dev) attr.resize(dev + 1, 0);
+        if (!attr[dev]) {
+            PG_CUDA(cudaFuncSetAttribute(k_gemm_abt_tc<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
+            attr[dev] = 1;
+        }
+    }
+    k_gemm_abt_tc<MT><<<grid, kTcThreads, smem, s>>>(amap, p);
+    PG_LAUNCH("k_gemm_abt_tc");
+}
+
+}  // namespace
+
+bool gemm_a_bt_tc_supported(DMat a) {
+    return encode_fn() != nullptr && a.ld % 4 == 0 && reinterpret_cast<uintptr_t>(a.p) % 16 == 0 && a.cols > 0 &&
+           a.rows < (1ull << 31) && a.cols < (1ull << 31) && a.ld * 4 < (1ull << 40);
+}
+
+void gemm_a_bt_tc(DMat a, DMat b, DMat out, cudaStream_t s) {
+    const uint64_t n = a.rows, K = a.cols, m = b.rows;
+    if (b.cols != K) fail_shape("gemm_a_bt: column counts differ");
+    if (out.rows != n || out.cols != m) fail_shape("gemm_a_bt: output shape mismatch");
+    if (n == 0 || m == 0) return;
+    if (!gemm_a_bt_tc_supported(a))
+        fail(kConfig, "gemm_a_bt (tensor cores): A needs a 16-byte aligned base and ld % 4 == 0");
+    // N tile: the whole output width when it fits one MMA (<= 256), else
+    // balanced 8-multiples
+    const uint32_t NT = static_cast<uint32_t>((m + kMaxN - 1) / kMaxN);
+    const uint32_t N = static_cast<uint32_t>(((m + NT - 1) / NT + 7) / 8 * 8);
+    const uint32_t KB = static_cast<uint32_t>((K + kKB - 1) / kKB);
+    const uint32_t acc_stride = (N + 31) / 32 * 32;
+    const int MT = acc_stride <= 128 ? 2 : 1;  // two 128-row sub-tiles share each B stage when N is narrow
+    const size_t stage = 2ull * MT * kTileBytesA + 2ull * N * 128;
+    const size_t budget = 232448 - 1024 - 256;
+    const uint32_t S = static_cast<uint32_t>(std::min<size_t>(4, budget / stage));
+    if (S < 2) fail(kConfig, "gemm_a_bt (tensor cores): tile does not fit shared memory");
+    const size_t smem = 1024 + S * stage + (3 * S + 4) * 8 + 16;
+
+    // the pre-split B image (hi, lo), one stage per (N tile, k block)
+    DevBuf<float> img(static_cast<uint64_t>(NT) * KB * 2 * N * kKB, s);
+    {
+        const uint64_t total = static_cast<uint64_t>(NT) * KB * N * kKB;
+        k_tc_pack_b<<<grid_for(total, 256), 256, 0, s>>>(b.p, b.ld, static_cast<uint32_t>(m), static_cast<uint32_t>(K),
+                                                      N, NT, KB, img.get());
+        PG_LAUNCH("k_tc_pack_b");
+    }
+    CUtensorMap amap;
+    std::memset(&amap, 0, sizeof(amap));
+    const cuuint64_t gdim[2] = {K, n};
+    const cuuint64_t gstride[1] = {a.ld * 4};
+    const cuuint32_t box[2] = {kKB, 128};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode_fn()(&amap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, a.p, gdim, gstride, box, estr,
+                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(kDevice, "gemm_a_bt (tensor cores): cuTensorMapEncodeTiled failed");
+    TcParams p{};
+    p.out = out.p;
+    p.ldo = out.ld;
+    p.n = n;
+    p.m = m;
+    p.N = N;
+    p.NT = NT;
+    p.KB = KB;
+    p.stages = S;
+    p.acc_stride = acc_stride;
+    p.row_tiles = (n + 128ull * MT - 1) / (128ull * MT);
+    p.bimg = img.get();
+    p.vec_out = (out.ld % 4 == 0 && reinterpret_cast<uintptr_t>(out.p) % 16 == 0) ? 1 : 0;
+    int dev = 0, sms = 148;
+    PG_CUDA(cudaGetDevice(&dev));
+    PG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const uint64_t tiles = p.row_tiles * NT;
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(tiles, static_cast<uint64_t>(sms)));
+    if (MT == 2)
+        launch_tc<2>(amap, p, smem, grid, s);
+    else
+        launch_tc<1>(amap, p, smem, grid, s);
+}
+
+}  // namespace pg

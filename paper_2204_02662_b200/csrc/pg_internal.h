@@ -271,7 +271,8 @@ enum TuneKeyId {
     kTuneAtbPairs = 19,
     kTuneGemmPacked = 20,
     kTuneHostLastSegPct = 21,
-    kTuneWgradFork = 22
+    kTuneWgradFork = 22,
+    kTuneGemmTc = 23
 };
 
 int64_t tuning(int key);
@@ -299,6 +300,11 @@ inline uint64_t pad_ld(uint64_t c) { return c <= 32 ? (c + 3) & ~3ull : (c + 31)
 
 // dense_matrix.hpp:40-96: out = a * b (b_transposed: a * b^T, gemm_a_bt)
 void gemm(DMat a, DMat b, DMat out, bool b_transposed, cudaStream_t s);
+// dense_matrix.hpp:78-95 on the tensor cores (gemm_tc.cu): tcgen05 kind::tf32
+// with 3xTF32 operand splitting — within fp32 tolerance, NOT bit-exact.
+// supported(): A base 16-byte aligned, ld % 4 == 0, the driver's TMA encoder.
+bool gemm_a_bt_tc_supported(DMat a);
+void gemm_a_bt_tc(DMat a, DMat b, DMat out, cudaStream_t s);
 // dense_matrix.hpp:57-76: out = a[a_rows]^T * b (a_rows nullable: all rows)
 void gemm_at_b(DMat a, const uint32_t* a_rows, DMat b, DMat out, cudaStream_t s);
 void relu(DMat x, DMat out, cudaStream_t s);

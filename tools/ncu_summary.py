@@ -62,9 +62,43 @@ def main():
                 k = hdr.index("gpu__time_duration.sum")
                 dur += float(r[k].replace(",", "")) * (1e-3 if units[k] == "us" else (1e-6 if units[k] == "ns" else 1.0))
         dom = ("+".join(names) + " (one path execution)", tot)
+    # duration-weighted unit throughputs and hit rates over the path's
+    # launches: the unit nearest its peak is the one that binds
+    sel = [r for r in rows[2:] if re.search(a.path_kernels or a.dominant, r[hdr.index("Kernel Name")])]
+
+    def num(r, m):
+        if m not in hdr:
+            return None
+        try:
+            return float(r[hdr.index(m)].replace(",", ""))
+        except ValueError:
+            return None
+
+    def wavg(m):
+        tot = w = 0.0
+        for r in sel:
+            d, v = num(r, "gpu__time_duration.sum"), num(r, m)
+            if d is not None and v is not None:
+                tot += d * v
+                w += d
+        return round(tot / w, 2) if w else None
+
+    units_pct = {"dram": wavg("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+                 "l2 (lts)": wavg("lts__throughput.avg.pct_of_peak_sustained_elapsed"),
+                 "l1tex": wavg("l1tex__throughput.avg.pct_of_peak_sustained_elapsed"),
+                 "sm": wavg("sm__throughput.avg.pct_of_peak_sustained_elapsed")}
+    known = {k: v for k, v in units_pct.items() if v is not None}
+    bind = max(known, key=known.get) if known else None
+    secs = sum(num(r, "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum") or 0 for r in sel)
+    reqs = sum(num(r, "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum") or 0 for r in sel)
     out = {"round": a.round, "command": a.command, "workload": a.workload,
            "dominant_kernel": dom[0] if dom else None, "dram_bytes_per_launch": dom[1] if dom else None,
-           "algorithmic_bytes_per_launch": a.algorithmic_bytes, "kernels": kernels}
+           "algorithmic_bytes_per_launch": a.algorithmic_bytes,
+           "unit_throughput_pct": units_pct, "binding_unit": bind, "binding_unit_pct": known.get(bind),
+           "l2_hit_rate_pct": wavg("lts__t_sector_hit_rate.pct"),
+           "sectors_per_request": round(secs / reqs, 2) if reqs else None,
+           "global_load_requests": int(reqs), "global_load_sectors": int(secs),
+           "kernels": kernels}
     json.dump(out, open(a.out, "w"), indent=1)
     print(json.dumps({k: v for k, v in out.items() if k != "kernels"}))
 
