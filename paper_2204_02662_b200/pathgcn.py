@@ -607,14 +607,20 @@ def backward_aggregation(grouped: GroupedCsr, y_grad, x_grad, mode=DETERMINISTIC
     return x_grad
 
 
-def gemm_a_bt(a, b, out, stream=None):
-    """dense_matrix.hpp:78-95: out = a * b^T (fp32, ascending k, unfused)."""
+PG_GEMM_TF32X3 = 1
+
+
+def gemm_a_bt(a, b, out, stream=None, tensor_cores=False):
+    """dense_matrix.hpp:78-95: out = a * b^T. Default: fp32, ascending k,
+    unfused (bit-exact). tensor_cores=True: tcgen05 kind::tf32 with 3xTF32
+    operand splitting (PG_GEMM_TF32X3) — within the fp32 tolerance, not
+    bit-exact."""
     _dev(a, "a")
     _dev(b, "b", cols=a.shape[1])
     _dev(out, "out", rows=a.shape[0], cols=b.shape[0])
-    _check(_lib_().pg_gemm_a_bt(C.c_void_p(a.data_ptr()), a.stride(0), C.c_void_p(b.data_ptr()), b.stride(0),
-                                C.c_void_p(out.data_ptr()), out.stride(0), a.shape[0], b.shape[0], a.shape[1],
-                                _stream(stream)))
+    _check(_lib_().pg_gemm_a_bt_ex(C.c_void_p(a.data_ptr()), a.stride(0), C.c_void_p(b.data_ptr()), b.stride(0),
+                                   C.c_void_p(out.data_ptr()), out.stride(0), a.shape[0], b.shape[0], a.shape[1],
+                                   PG_GEMM_TF32X3 if tensor_cores else 0, _stream(stream)))
     return out
 
 

@@ -101,7 +101,8 @@ def test_tuning_keys(pg):
     for key in ("vec_u", "chunk_major", "heavy_tma", "host_segs", "host_chunks", "host_trace", "heavy_narrow",
                 "wide_lpd", "src_segs", "ld_cg", "host_chunk_order", "grouped_seg", "heavy_wide_pipe",
                 "host_final_segs", "host_pitch2d", "host_copy_prio", "host_seg_balance",
-                "host_chunk_balance", "atb_split", "atb_pairs", "gemm_packed", "host_last_seg_pct", "wgrad_fork"):
+                "host_chunk_balance", "atb_split", "atb_pairs", "gemm_packed", "host_last_seg_pct", "wgrad_fork",
+                "gemm_tc"):
         pg.set_tuning(key, None)
     import pytest
 
