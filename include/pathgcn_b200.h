@@ -269,6 +269,40 @@ int pg_backward_aggregate_segment(pg_groups G, uint32_t seg, uint32_t row_begin,
                                   const float* y_dev, uint64_t y_rows, uint64_t ld_in, float* x_dev,
                                   uint64_t ld_out, uint64_t dim, unsigned flags, void* stream);
 
+/* ---------------- multi-GPU ----------------
+ * One NCCL rank per device (NCCL is dlopen'ed at first use: the copy already
+ * in the process, else libnccl.so.2). The destinations of each execution
+ * path are sharded by edge count (pg_path_shard_bounds; the parent frontier
+ * of path i is cut where path i-1's destinations are). Rank 0 makes the id
+ * (pg_comm_unique_id) and the caller ships its 128 bytes to every rank over
+ * its own bootstrap channel (MPI, torch.distributed, a file). */
+typedef struct pg_comm_s* pg_comm;
+#define PG_COMM_ID_BYTES 128
+int pg_comm_unique_id(uint8_t* id);
+int pg_comm_init_rank(int device, const uint8_t* id, int world, int rank, pg_comm* out);
+int pg_comm_info(pg_comm c, int* world, int* rank, int* nccl_version);
+int pg_comm_destroy(pg_comm c);
+/* In-place all-gather-v of a pitched row matrix over the communicator: rank
+ * s owns rows [bounds[s], bounds[s+1]) (world+1 cuts); whole ld-float rows
+ * are broadcast in rank order on the library's communication stream,
+ * ordered after and before `stream`. */
+int pg_comm_allgather_rows(pg_comm c, float* rows, uint64_t ld, const uint32_t* bounds, void* stream);
+/* The timed stage (engine.hpp:331-338) row-sharded: this rank holds its
+ * parent rows [parent_bounds[rank], parent_bounds[rank+1]) of y_dev (the
+ * full P x ld frontier-order matrix); the call completes y_dev from the
+ * other ranks (per-owner broadcasts on the communication stream) and
+ * aggregates destination rows [dest_bounds[rank], dest_bounds[rank+1]) into
+ * x_dev. Default: source-segment pass k runs as soon as owner k's rows have
+ * landed (the exchange overlaps the SpMM; passes in owner order are the
+ * serial fp32 order, so every row is bit-identical to one GPU);
+ * PG_SHARD_SINGLE_PASS waits for the whole exchange, then one pass.
+ * Sets the grouping's source segments (pg_groups_set_segments) to the
+ * owner cuts. Asynchronous on `stream`. */
+#define PG_SHARD_SINGLE_PASS 8u
+int pg_backward_aggregate_sharded(pg_comm c, pg_groups G, const uint32_t* parent_bounds,
+                                  const uint32_t* dest_bounds, float* y_dev, uint64_t y_rows, uint64_t ld_in,
+                                  float* x_dev, uint64_t ld_out, uint64_t dim, unsigned flags, void* stream);
+
 /* ---------------- dense helpers of backward_epp ---------------- */
 
 /* dense_matrix.hpp:78-95 gemm_a_bt: out[n x m] = a[n x k] * b[m x k]^T */

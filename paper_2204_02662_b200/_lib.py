@@ -126,6 +126,12 @@ SIGNATURES = {
     "pg_groups_set_segments": [H, u64p, u32],
     "pg_backward_aggregate_segment": [H, u32, u32, u32, vp, u64, u64, vp, u64, u64, C.c_uint, vp],
     "pg_gemm_a_bt": [vp, u64, vp, u64, vp, u64, u64, u64, u64, vp],
+    "pg_comm_unique_id": [vp],
+    "pg_comm_init_rank": [C.c_int, vp, C.c_int, C.c_int, C.POINTER(H)],
+    "pg_comm_info": [H, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)],
+    "pg_comm_destroy": [H],
+    "pg_comm_allgather_rows": [H, vp, u64, u32p, vp],
+    "pg_backward_aggregate_sharded": [H, H, u32p, u32p, vp, u64, u64, vp, u64, u64, C.c_uint, vp],
     "pg_gemm_a_bt_ex": [vp, u64, vp, u64, vp, u64, u64, u64, u64, C.c_uint, vp],
     "pg_relu_backward": [vp, u64, vp, u64, vp, u64, u64, u64, vp],
     "pg_gather_rows": [vp, u64, vp, u64, vp, u64, u64, vp],

@@ -44,7 +44,7 @@ constexpr TuneKey kTuneKeys[] = {
     {"src_segs", "PG_SRC_SEGS", 0},        // whole-path SpMM source segments: 0 = auto (L2-sized), K = forced
     {"ld_cg", "PG_LD_CG", 0},              // row gathers: 0/1 = ld.global.nc (L1), 2 = ld.global.cg (L2 only)
     {"host_chunk_order", "PG_HOST_CHUNK_ORDER", 1},  // host drop-in last pass: 1 = last row chunk first
-    {"grouped_seg", "PG_GROUPED_SEG", 0},  // grouped Fast: 1 = CTA-segmented reduction, 0 = an atomic per extra group
+    {"grouped_seg", "PG_GROUPED_SEG", 0},  // grouped Fast: 0 = atomic-free k_agg_grp, 1 = CTA-segmented + atomics at CTA edges, 2 = an atomic per extra group
     {"heavy_wide_pipe", "PG_HEAVY_WIDE_PIPE", 1},  // heavy wide rows: 1 = software-pipelined k_agg_wide_pipe
     {"host_final_segs", "PG_HOST_FINAL_SEGS", 1},  // host drop-in: trailing source segments of the chunked last pass
     {"host_pitch2d", "PG_HOST_PITCH2D", 0},  // host drop-in: odd widths by 2-D DMA (1) or flat DMA + repack kernel (0)
@@ -550,7 +550,7 @@ void launch_groups(const uint64_t* gbeg, const uint64_t* gend, const uint32_t* g
                    const Edge* edges, uint64_t G, uint32_t chunks, const float* in, uint64_t ld_in, float* out,
                    uint64_t ld_out, uint32_t dim, bool accumulate, cudaStream_t s) {
     const uint64_t items = G * chunks;
-    if (tuning(kTuneGroupedSeg)) {
+    if (tuning(kTuneGroupedSeg) == 1) {
         k_agg_groups_seg<LPD, 8><<<grid_for(items * LPD, 256), 256, 0, s>>>(
             gbeg, gend, gdest, dest_groups, edges, items, chunks, in, static_cast<uint32_t>(ld_in * 4), out, ld_out,
             dim, accumulate, kZeros, 0u);
@@ -1188,6 +1188,359 @@ void launch_heavy_any(const uint64_t* ebeg, const uint64_t* eend, const Edge* ed
                                       accumulate, s, ext);
 }
 
+// ---- CommitMode::Fast, group partitioned, atomic-free (PG_AGG_GROUPED) ----
+// aggregate.hpp:84-115 with the groups as the unit of work and no global
+// atomics. A CTA owns one schedule range: consecutive groups that hold whole
+// destinations (or one slice of a hub destination's groups). Per (range,
+// column chunk):
+//  1. the range's edge records — contiguous, since its groups are — are
+//     staged into shared memory with one cp.async.bulk (TMA bulk copy,
+//     mbarrier completion; windows above kGrpEdgeCap stream from global);
+//  2. a worker = LPD lanes (one float4 column each) takes one group at a
+//     time (groups w, w + W, ...): per batch of U edges, records from shared
+//     memory (broadcast LDS), U 128-bit row gathers in flight, ordered
+//     separately-rounded accumulate into a zero scratch (aggregate.hpp:93),
+//     the group's partial row into shared memory;
+//  3. segmented reduction in group order: the head worker of each
+//     destination's run adds its groups' partials in order and stores the
+//     row once (out = init + sum, + 0) — or, for a hub slice, stores the
+//     slice partial to its scratch slot; k_grp_fixup then adds a hub's
+//     slices in slice order.
+// Deterministic run to run; a destination with one group is bit-equal to
+// the Deterministic kernel (same serial chain); across groups the sum is
+// re-associated (Fast semantics, within the fp32 tolerance). gs sets the
+// work unit and the partial-sum count, so the structure-aware gs selector
+// shapes this schedule.
+constexpr int kGrpEdgeCap = 4096;  // staged records per CTA (32 KB)
+
+template <int LPD>
+__host__ __device__ constexpr int grp_workers() { return 256 / LPD; }
+template <int LPD>
+__host__ __device__ constexpr int grp_gcap() { return 4 * grp_workers<LPD>(); }
+template <int LPD>
+constexpr size_t grp_smem() {
+    return (kGrpEdgeCap + 2) * sizeof(Edge) + static_cast<size_t>(grp_gcap<LPD>()) * LPD * 16 +
+           3ull * grp_gcap<LPD>() * 4 + 16;
+}
+
+template <int LPD, int U>
+__global__ void __launch_bounds__(256, 4) k_agg_grp(const uint4* __restrict__ ranges, uint32_t nranges,
+                                                   const uint64_t* __restrict__ gbeg, const uint64_t* __restrict__ gend,
+                                                   const uint32_t* __restrict__ gdest, const Edge* __restrict__ edges,
+                                                   const float* __restrict__ in, uint32_t ld_in_bytes,
+                                                   float* __restrict__ out, uint64_t ld_out, uint32_t dim,
+                                                   int accumulate, float* __restrict__ scratch, uint64_t ld_scr,
+                                                   float2 zeros, uint32_t zmask) {
+    constexpr int W = grp_workers<LPD>();
+    constexpr int GCAP = grp_gcap<LPD>();
+    extern __shared__ __align__(128) unsigned char smem[];
+    Edge* recs = reinterpret_cast<Edge*>(smem);
+    float4* part = reinterpret_cast<float4*>(smem + (kGrpEdgeCap + 2) * sizeof(Edge));
+    uint32_t* sgb = reinterpret_cast<uint32_t*>(part + GCAP * LPD);
+    uint32_t* sge = sgb + GCAP;
+    uint32_t* sdst = sge + GCAP;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sdst + GCAP + (GCAP & 1));
+
+    const uint32_t ri = blockIdx.x % nranges, ci = blockIdx.x / nranges;
+    const uint4 r = ranges[ri];
+    const uint64_t g0 = static_cast<uint64_t>(r.x) | (static_cast<uint64_t>(r.y) << 32);
+    const uint32_t ng = r.z, slot = r.w;
+    const uint64_t e0 = __ldg(gbeg + g0), e1 = __ldg(gend + g0 + ng - 1);
+    const bool staged = e1 - e0 <= kGrpEdgeCap;
+    const uint64_t ebase = staged ? (e0 & ~1ull) : e0;  // 16-byte aligned window start
+    const unsigned tid = threadIdx.x;
+    if (staged && tid == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (uint32_t lg = tid; lg < ng; lg += 256) {
+        sgb[lg] = static_cast<uint32_t>(__ldg(gbeg + g0 + lg) - ebase);
+        sge[lg] = static_cast<uint32_t>(__ldg(gend + g0 + lg) - ebase);
+        sdst[lg] = __ldg(gdest + g0 + lg);
+    }
+    __syncthreads();
+    if (staged) {
+        if (tid == 0) {
+            // the edge stream is padded (kEdgePad): rounding the end up stays in bounds
+            const uint32_t bytes = static_cast<uint32_t>(((e1 - ebase) * sizeof(Edge) + 15) & ~15ull);
+            mbar_expect_tx(bar, bytes);
+            bulk_g2s(recs, edges + ebase, bytes, bar);
+            mbar_arrive(bar);
+        }
+        mbar_wait(bar, 0);
+    }
+    const Zs z = zs_of(zeros);
+    const unsigned w = tid / LPD, sl = tid % LPD;
+    const uint32_t col = (ci * LPD + sl) * 4;
+    const bool active = col < dim;
+    const char* base = reinterpret_cast<const char*>(in) + (active ? col : 0u) * 4u;
+    asm("mov.b64 %0, %0;" : "+l"(base));
+    const uint32_t srecs = static_cast<uint32_t>(__cvta_generic_to_shared(recs));
+    // a record: from the staged window (LDS, one broadcast per sub-warp) or,
+    // for windows past kGrpEdgeCap, straight from global
+    auto rec = [&](uint32_t i) -> Edge {
+        if (staged) {
+            Edge r;
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "r"(srecs + i * 8u));
+            return r;
+        }
+        return ld_rec(edges + ebase + i);
+    };
+    for (uint32_t lg = w; lg < ng; lg += W) {
+        uint32_t e = sgb[lg];
+        const uint32_t end = sge[lg];
+        Acc acc{0ull, 0ull};  // the group's zero scratch (aggregate.hpp:93)
+        for (; e + U <= end; e += U) {
+            Edge ed[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) ed[u] = rec(e + u);
+            float4 x[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) x[u] = ld_row(base, ed[u].x, ld_in_bytes);
+            const Zs zz = batch_dep<U>(x, z, zmask);
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc_step(acc, __uint_as_float(ed[u].y), x[u], zz);
+        }
+        if (e < end) {
+            const uint32_t n = end - e;
+            Edge ed[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) ed[u] = rec(e + (u < static_cast<int>(n) ? u : n - 1));
+            float4 x[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) x[u] = ld_row(base, ed[u].x, ld_in_bytes);
+            const Zs zz = batch_dep<U>(x, z, zmask);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (u < static_cast<int>(n)) acc_step(acc, __uint_as_float(ed[u].y), x[u], zz);
+        }
+        const float2 l = unpk2(acc.lo), h = unpk2(acc.hi);
+        part[lg * LPD + sl] = make_float4(l.x, l.y, h.x, h.y);
+    }
+    __syncthreads();
+    // segmented reduction over the range's groups, in group order
+    for (uint32_t lg = w; lg < ng; lg += W) {
+        const uint32_t d = sdst[lg];
+        if (lg > 0 && sdst[lg - 1] == d) continue;  // not the head of its destination's run
+        uint32_t last = lg;
+        while (last + 1 < ng && sdst[last + 1] == d) ++last;
+        float4 v = part[lg * LPD + sl];
+        for (uint32_t k = lg + 1; k <= last; ++k) {
+            const float4 p = part[k * LPD + sl];
+            v.x = __fadd_rn(v.x, p.x);
+            v.y = __fadd_rn(v.y, p.y);
+            v.z = __fadd_rn(v.z, p.z);
+            v.w = __fadd_rn(v.w, p.w);
+        }
+        if (!active) continue;
+        const bool full = col + 3 < dim;
+        if (slot != 0xffffffffu) {  // hub slice: its partial, combined by k_grp_fixup
+            float* srow = scratch + slot * ld_scr + col;
+            if (full) {
+                *reinterpret_cast<float4*>(srow) = v;
+            } else {
+                srow[0] = v.x;
+                if (col + 1 < dim) srow[1] = v.y;
+                if (col + 2 < dim) srow[2] = v.z;
+            }
+            continue;
+        }
+        float* orow = out + d * ld_out + col;
+        float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (accumulate) {
+            if (full) o = *reinterpret_cast<const float4*>(orow);
+            else {
+                o.x = orow[0];
+                if (col + 1 < dim) o.y = orow[1];
+                if (col + 2 < dim) o.z = orow[2];
+            }
+        }
+        // out (+)= scratch (aggregate.hpp:102-103), then + 0 (aggregate.hpp:82)
+        o.x = __fadd_rn(__fadd_rn(o.x, v.x), 0.f);
+        o.y = __fadd_rn(__fadd_rn(o.y, v.y), 0.f);
+        o.z = __fadd_rn(__fadd_rn(o.z, v.z), 0.f);
+        o.w = __fadd_rn(__fadd_rn(o.w, v.w), 0.f);
+        if (full) {
+            __stcs(reinterpret_cast<float4*>(orow), o);
+        } else {
+            orow[0] = o.x;
+            if (col + 1 < dim) orow[1] = o.y;
+            if (col + 2 < dim) orow[2] = o.z;
+        }
+    }
+}
+
+// Hub destinations: out[d] = init + slice_0 + slice_1 + ... (slice order),
+// + 0; and the rows of destinations without groups on overwrite.
+template <int LPD>
+__global__ void __launch_bounds__(256) k_grp_fixup(const uint4* __restrict__ hubs, uint32_t nhubs,
+                                                  const uint32_t* __restrict__ empty, uint32_t nempty,
+                                                  uint32_t chunks, const float* __restrict__ scratch, uint64_t ld_scr,
+                                                  float* __restrict__ out, uint64_t ld_out, uint32_t dim,
+                                                  int accumulate) {
+    const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    const uint64_t item = t / LPD;
+    const uint64_t nitems = static_cast<uint64_t>(nhubs + nempty) * chunks;
+    if (item >= nitems) return;
+    const uint32_t hi = static_cast<uint32_t>(item % (nhubs + nempty));
+    const uint32_t ci = static_cast<uint32_t>(item / (nhubs + nempty));
+    const uint32_t col = (ci * LPD + static_cast<uint32_t>(t % LPD)) * 4;
+    if (col >= dim) return;
+    const bool full = col + 3 < dim;
+    if (hi >= nhubs) {  // a destination without groups: overwrite -> +0 row
+        if (accumulate) return;
+        float* orow = out + __ldg(empty + (hi - nhubs)) * ld_out + col;
+        if (full) {
+            *reinterpret_cast<float4*>(orow) = make_float4(0.f, 0.f, 0.f, 0.f);
+        } else {
+            orow[0] = 0.f;
+            if (col + 1 < dim) orow[1] = 0.f;
+            if (col + 2 < dim) orow[2] = 0.f;
+        }
+        return;
+    }
+    const uint4 h = hubs[hi];
+    float* orow = out + static_cast<uint64_t>(h.x) * ld_out + col;
+    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (accumulate) {
+        if (full) o = *reinterpret_cast<const float4*>(orow);
+        else {
+            o.x = orow[0];
+            if (col + 1 < dim) o.y = orow[1];
+            if (col + 2 < dim) o.z = orow[2];
+        }
+    }
+    for (uint32_t k = 0; k < h.z; ++k) {
+        const float* sr = scratch + static_cast<uint64_t>(h.y + k) * ld_scr + col;
+        float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (full) p = *reinterpret_cast<const float4*>(sr);
+        else {
+            p.x = sr[0];
+            if (col + 1 < dim) p.y = sr[1];
+            if (col + 2 < dim) p.z = sr[2];
+        }
+        o.x = __fadd_rn(o.x, p.x);
+        o.y = __fadd_rn(o.y, p.y);
+        o.z = __fadd_rn(o.z, p.z);
+        o.w = __fadd_rn(o.w, p.w);
+    }
+    o.x = __fadd_rn(o.x, 0.f);
+    o.y = __fadd_rn(o.y, 0.f);
+    o.z = __fadd_rn(o.z, 0.f);
+    o.w = __fadd_rn(o.w, 0.f);
+    if (full) {
+        *reinterpret_cast<float4*>(orow) = o;
+    } else {
+        orow[0] = o.x;
+        if (col + 1 < dim) orow[1] = o.y;
+        if (col + 2 < dim) orow[2] = o.z;
+    }
+}
+
+// Host: the schedule over the base CSR's offsets (groups of destination d
+// are [off[d] + j gs, min(off[d] + (j+1) gs, off[d+1])), grouping.cpp:7-27).
+// Ranges close before a destination that would push them past gcap groups
+// or kGrpEdgeCap edges; a destination alone past either limit is a hub,
+// cut into slices within both (one group per slice at least).
+void build_grp_sched(const uint64_t* offsets_dev, uint32_t D, uint32_t gs, uint32_t workers, Groups::GrpSched& sc,
+                     cudaStream_t s) {
+    std::vector<uint64_t> off(static_cast<uint64_t>(D) + 1);
+    PG_CUDA(cudaMemcpyAsync(off.data(), offsets_dev, off.size() * 8, cudaMemcpyDeviceToHost, s));
+    PG_CUDA(cudaStreamSynchronize(s));
+    const uint64_t gcap = 4ull * workers;
+    std::vector<uint4> ranges, hubs;
+    std::vector<uint32_t> empty;
+    uint32_t nslots = 0;
+    uint64_t g = 0, cur_g0 = 0, cur_ng = 0, cur_e = 0;
+    auto close = [&] {
+        if (cur_ng) ranges.push_back(make_uint4(static_cast<uint32_t>(cur_g0), static_cast<uint32_t>(cur_g0 >> 32),
+                                                static_cast<uint32_t>(cur_ng), 0xffffffffu));
+        cur_ng = cur_e = 0;
+    };
+    for (uint32_t d = 0; d < D; ++d) {
+        const uint64_t deg = off[d + 1] - off[d];
+        if (deg == 0) {
+            empty.push_back(d);
+            continue;
+        }
+        const uint64_t k = (deg + gs - 1) / gs;
+        if (k > gcap || deg > static_cast<uint64_t>(kGrpEdgeCap)) {
+            close();
+            const uint32_t first = nslots;
+            uint64_t j = 0;
+            while (j < k) {
+                uint64_t cnt = 0, e = 0;
+                while (j + cnt < k && cnt < gcap) {
+                    const uint64_t ge = std::min<uint64_t>(gs, deg - (j + cnt) * gs);
+                    if (cnt && e + ge > static_cast<uint64_t>(kGrpEdgeCap)) break;
+                    e += ge;
+                    ++cnt;
+                }
+                ranges.push_back(make_uint4(static_cast<uint32_t>(g + j), static_cast<uint32_t>((g + j) >> 32),
+                                            static_cast<uint32_t>(cnt), nslots++));
+                j += cnt;
+            }
+            hubs.push_back(make_uint4(d, first, nslots - first, 0u));
+            g += k;
+            continue;
+        }
+        if (cur_ng + k > gcap || cur_e + deg > static_cast<uint64_t>(kGrpEdgeCap)) close();
+        if (!cur_ng) cur_g0 = g;
+        cur_ng += k;
+        cur_e += deg;
+        g += k;
+    }
+    close();
+    sc.workers = workers;
+    sc.nranges = static_cast<uint32_t>(ranges.size());
+    sc.nhubs = static_cast<uint32_t>(hubs.size());
+    sc.nslots = nslots;
+    sc.nempty = static_cast<uint32_t>(empty.size());
+    sc.ranges = DevBuf<uint4>(ranges.size(), s);
+    sc.hubs = DevBuf<uint4>(hubs.size(), s);
+    sc.empty = DevBuf<uint32_t>(empty.size(), s);
+    if (!ranges.empty())
+        PG_CUDA(cudaMemcpyAsync(sc.ranges.get(), ranges.data(), ranges.size() * 16, cudaMemcpyHostToDevice, s));
+    if (!hubs.empty()) PG_CUDA(cudaMemcpyAsync(sc.hubs.get(), hubs.data(), hubs.size() * 16, cudaMemcpyHostToDevice, s));
+    if (!empty.empty())
+        PG_CUDA(cudaMemcpyAsync(sc.empty.get(), empty.data(), empty.size() * 4, cudaMemcpyHostToDevice, s));
+    PG_CUDA(cudaStreamSynchronize(s));
+}
+
+template <int LPD>
+void launch_grp(Groups& G, const Groups::GrpSched& sc, const Edge* edges, uint32_t chunks, const float* in,
+                uint64_t ld_in, float* out, uint64_t ld_out, uint32_t dim, bool accumulate, cudaStream_t s) {
+    static std::mutex mu;
+    static std::vector<char> attr;
+    constexpr size_t smem = grp_smem<LPD>();
+    int dev = 0;
+    PG_CUDA(cudaGetDevice(&dev));
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (static_cast<int>(attr.size()) <= dev) attr.resize(dev + 1, 0);
+        if (!attr[dev]) {
+            PG_CUDA(cudaFuncSetAttribute(k_agg_grp<LPD, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem)));
+            attr[dev] = 1;
+        }
+    }
+    const uint64_t ld_scr = (static_cast<uint64_t>(dim) + 3) & ~3ull;
+    DevBuf<float> scratch(static_cast<uint64_t>(sc.nslots) * ld_scr, s);
+    if (sc.nranges) {
+        k_agg_grp<LPD, 8><<<sc.nranges * chunks, 256, smem, s>>>(
+            sc.ranges.get(), sc.nranges, G.gbegin.get(), G.gend.get(), G.gdest.get(), edges, in,
+            static_cast<uint32_t>(ld_in * 4), out, ld_out, dim, accumulate, scratch.get(), ld_scr, kZeros, 0u);
+        PG_LAUNCH("k_agg_grp");
+    }
+    const uint64_t fix = static_cast<uint64_t>(sc.nhubs + (accumulate ? 0 : sc.nempty)) * chunks;
+    if (fix) {
+        k_grp_fixup<LPD><<<grid_for(fix * LPD, 256), 256, 0, s>>>(sc.hubs.get(), sc.nhubs, sc.empty.get(),
+                                                                accumulate ? 0u : sc.nempty, chunks, scratch.get(),
+                                                                ld_scr, out, ld_out, dim, accumulate);
+        PG_LAUNCH("k_grp_fixup");
+    }
+}
+
 struct SideStream {
     cudaStream_t s = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
@@ -1381,6 +1734,32 @@ void aggregate_groups(const uint64_t* gbeg, const uint64_t* gend, const uint32_t
         launch_groups<8>(gbeg, gend, gdest, dest_groups, edges, G, 1, in, ld_in, out, ld_out, dim32, true, s);
     else
         launch_groups<4>(gbeg, gend, gdest, dest_groups, edges, G, 1, in, ld_in, out, ld_out, dim32, true, s);
+}
+
+void aggregate_groups_af(Groups& G, const uint64_t* offsets_dev, uint32_t D, const Edge* edges, const float* in,
+                         uint64_t ld_in, float* out, uint64_t ld_out, uint64_t dim, bool accumulate, cudaStream_t s) {
+    if (dim == 0 || D == 0) return;
+    const bool vec = (ld_in % 4 == 0) && (ld_out % 4 == 0) && (reinterpret_cast<uintptr_t>(in) % 16 == 0) &&
+                     (reinterpret_cast<uintptr_t>(out) % 16 == 0) && ld_in >= ((dim + 3) & ~3ull) &&
+                     ld_in < (1ull << 30);
+    if (!vec) fail(kConfig, "grouped aggregation needs 16-byte rows (ld % 4 == 0, aligned base)");
+    const uint32_t dim32 = static_cast<uint32_t>(dim);
+    const uint32_t nq = (dim32 + 3) / 4;
+    const int lpd = nq > 16 ? 32 : nq > 8 ? 16 : nq > 4 ? 8 : 4;
+    const uint32_t workers = 256 / lpd;
+    Groups::GrpSched* sc = nullptr;
+    for (auto& x : G.grp_scheds)
+        if (x->workers == workers) sc = x.get();
+    if (!sc) {
+        G.grp_scheds.push_back(std::make_unique<Groups::GrpSched>());
+        sc = G.grp_scheds.back().get();
+        build_grp_sched(offsets_dev, D, G.gs, workers, *sc, lib_stream(G.device));
+    }
+    const uint32_t chunks = lpd == 32 ? (nq + 31) / 32 : 1;
+    if (lpd == 32) launch_grp<32>(G, *sc, edges, chunks, in, ld_in, out, ld_out, dim32, accumulate, s);
+    else if (lpd == 16) launch_grp<16>(G, *sc, edges, chunks, in, ld_in, out, ld_out, dim32, accumulate, s);
+    else if (lpd == 8) launch_grp<8>(G, *sc, edges, chunks, in, ld_in, out, ld_out, dim32, accumulate, s);
+    else launch_grp<4>(G, *sc, edges, chunks, in, ld_in, out, ld_out, dim32, accumulate, s);
 }
 
 void relu_backward(const float* grad, uint64_t ldg, const float* pre, uint64_t ldp, float* out, uint64_t ldo,

@@ -27,15 +27,25 @@ thread_local std::string g_err;
 thread_local int g_kind = PG_KIND_NONE;
 thread_local uint64_t g_line = 0;
 
+}  // namespace
+
+// the calling thread's last failure (pg_last_error / pg_last_error_kind),
+// shared with the communicator entry points (comm.cu)
+void pg::record_error(const pg::Error& e) {
+    g_err = e.what();
+    g_kind = e.kind;
+    g_line = e.line;
+}
+
+namespace {
+
 template <typename F>
 int guard(F&& f) {
     try {
         f();
         return PG_OK;
     } catch (const pg::Error& e) {
-        g_err = e.what();
-        g_kind = e.kind;
-        g_line = e.line;
+        record_error(e);
         return e.code;
     } catch (const std::bad_alloc&) {
         g_err = "host allocation failed";
@@ -205,8 +215,14 @@ void pg::run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re,
             }
             edges = g.edges.get();
         }
-        aggregate_groups(G.gbegin.get(), G.gend.get(), G.gdest.get(), G.dest_groups.get(), b.D, G.G, edges, in, ld_in,
-                         out, ld_out, dim, accumulate, s);
+        // tuning "grouped_seg": 0 (default) = atomic-free k_agg_grp + hub
+        // fixup; 1 = the CTA-segmented kernel with atomics at CTA edges;
+        // 2 = one atomic commit per extra group (the reference's omp atomic)
+        if (tuning(kTuneGroupedSeg) == 0)
+            aggregate_groups_af(G, b.offsets, b.D, edges, in, ld_in, out, ld_out, dim, accumulate, s);
+        else
+            aggregate_groups(G.gbegin.get(), G.gend.get(), G.gdest.get(), G.dest_groups.get(), b.D, G.G, edges, in,
+                             ld_in, out, ld_out, dim, accumulate, s);
         return;
     }
     if (G.path) {
@@ -1347,7 +1363,7 @@ int pg_groups_remap_sources(pg_groups h, const uint32_t* map, uint64_t map_len, 
             if (map[i] >= new_rows) fail(kConfig, "remap: map entry out of range");
         DevBuf<uint32_t> dmap(map_len, s);
         if (map_len) PG_CUDA(cudaMemcpyAsync(dmap.get(), map, map_len * 4, cudaMemcpyHostToDevice, s));
-        DevBuf<Edge> out(p.E, s);
+        DevBuf<Edge> out = edge_buf(p.E, s);
         remap_edges(p.edges_parent.get(), p.E, dmap.get(), out.get(), s);
         PG_CUDA(cudaStreamSynchronize(s));
         retire(G.edges_remap);

@@ -919,7 +919,7 @@ void backward_epp(Groups* const* PG, Frontiers& F, const BackwardIO& io, int gat
                 if (!p.edges_global.get() && p.E) {
                     cudaStream_t ls = lib_stream(p.device);
                     PG_CUDA(cudaStreamSynchronize(s));  // F's ids are final
-                    DevBuf<Edge> eg(p.E, ls);
+                    DevBuf<Edge> eg = edge_buf(p.E, ls);
                     remap_edges(p.edges_parent.get(), p.E, F.levels[i].ids.get(), eg.get(), ls);
                     PG_CUDA(cudaStreamSynchronize(ls));
                     p.edges_global = std::move(eg);

@@ -259,22 +259,26 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_gemm_abt_tc(const __grid_cons
             for (uint32_t kb = 0; kb < P.KB; ++kb, ++q) {
                 const uint32_t s = q % S, ph = (q / S) & 1;
                 mbar_wait(&full[s], ph);
-                uint4* hi = reinterpret_cast<uint4*>(smem + s * stage_bytes);
-                uint4* lo = reinterpret_cast<uint4*>(smem + s * stage_bytes + TcShape<MT>::kABytes);
+                // shared-window addresses (LDS/STS, not generic LD/ST)
+                const uint32_t hi = smem_addr(smem + s * stage_bytes);
+                const uint32_t lo = hi + TcShape<MT>::kABytes;
 #pragma unroll 4
                 for (uint32_t c = tid; c < TcShape<MT>::kABytes / 16; c += 128) {
-                    uint4 v = hi[c];
-                    uint4 h, l;
-                    h.x = tf32_hi(v.x);
-                    h.y = tf32_hi(v.y);
-                    h.z = tf32_hi(v.z);
-                    h.w = tf32_hi(v.w);
-                    l.x = __float_as_uint(__fsub_rn(__uint_as_float(v.x), __uint_as_float(h.x)));
-                    l.y = __float_as_uint(__fsub_rn(__uint_as_float(v.y), __uint_as_float(h.y)));
-                    l.z = __float_as_uint(__fsub_rn(__uint_as_float(v.z), __uint_as_float(h.z)));
-                    l.w = __float_as_uint(__fsub_rn(__uint_as_float(v.w), __uint_as_float(h.w)));
-                    hi[c] = h;
-                    lo[c] = l;
+                    uint32_t v0, v1, v2, v3;
+                    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(v0), "=r"(v1), "=r"(v2), "=r"(v3)
+                                 : "r"(hi + c * 16));
+                    const uint32_t h0 = tf32_hi(v0), h1 = tf32_hi(v1), h2 = tf32_hi(v2), h3 = tf32_hi(v3);
+                    const uint32_t l0 = __float_as_uint(__fsub_rn(__uint_as_float(v0), __uint_as_float(h0)));
+                    const uint32_t l1 = __float_as_uint(__fsub_rn(__uint_as_float(v1), __uint_as_float(h1)));
+                    const uint32_t l2 = __float_as_uint(__fsub_rn(__uint_as_float(v2), __uint_as_float(h2)));
+                    const uint32_t l3 = __float_as_uint(__fsub_rn(__uint_as_float(v3), __uint_as_float(h3)));
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(hi + c * 16), "r"(h0), "r"(h1),
+                                 "r"(h2), "r"(h3)
+                                 : "memory");
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(lo + c * 16), "r"(l0), "r"(l1),
+                                 "r"(l2), "r"(l3)
+                                 : "memory");
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
                 asm volatile("bar.sync 1, 128;" ::: "memory");

@@ -221,7 +221,7 @@ void graph_assign_weights(Graph& g, int weight_mode, cudaStream_t s) {
 
 void graph_pack_edges(Graph& g, cudaStream_t s) {
     if (g.edges.get() || g.m == 0) return;
-    g.edges = DevBuf<Edge>(g.m, s);
+    g.edges = edge_buf(g.m, s);
     k_pack_edges<<<grid_for(g.m, 256), 256, 0, s>>>(g.nbrs.get(), g.w64.get(), g.m, g.edges.get());
     PG_LAUNCH("k_pack_edges");
 }

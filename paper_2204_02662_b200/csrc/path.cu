@@ -443,7 +443,7 @@ std::unique_ptr<Path> path_extract(const Graph& g, const Frontiers& f, uint64_t 
     const uint64_t E = p->E;
     p->nbr_local = DevBuf<uint32_t>(E, s);
     p->w64 = DevBuf<double>(E, s);
-    p->edges_parent = DevBuf<Edge>(E, s);
+    p->edges_parent = edge_buf(E, s);
     if (D && E) {
         k_fill_path<<<grid_for(static_cast<uint64_t>(D) * 32, kThreads), kThreads, 0, s>>>(
             g.offsets.get(), g.nbrs.get(), g.w64.get(), p->dest.get(), D, pl.bits.get(), pl.prefix.get(),
@@ -516,7 +516,7 @@ void remap_edges(const Edge* in, uint64_t E, const uint32_t* map, Edge* out, cud
 void path_pack_local(Path& p, cudaStream_t s) {
     std::lock_guard<std::mutex> lk(p.mu);
     if (p.edges_local.get() || p.E == 0 || p.S == p.P) return;
-    p.edges_local = DevBuf<Edge>(p.E, s);
+    p.edges_local = edge_buf(p.E, s);
     k_pack_local<<<grid_for(p.E, kThreads), kThreads, 0, s>>>(p.nbr_local.get(), p.edges_parent.get(), p.E,
                                                             p.edges_local.get());
     PG_LAUNCH("k_pack_local");

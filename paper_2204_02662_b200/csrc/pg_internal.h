@@ -34,6 +34,15 @@ struct DeviceGuard {
 
 // Packed edge record streamed by the SpMM: (source row, fp32 weight bits).
 using Edge = uint2;
+// Every edge stream carries kEdgePad zeroed records past its end, so a
+// 16-byte bulk copy (cp.async.bulk) of any record window may round its end
+// up (the grouped kernel stages its CTA's window that way).
+constexpr uint64_t kEdgePad = 2;
+inline DevBuf<Edge> edge_buf(uint64_t E, cudaStream_t s) {
+    DevBuf<Edge> b(E + kEdgePad, s);
+    PG_CUDA(cudaMemsetAsync(b.get() + E, 0, kEdgePad * sizeof(Edge), s));
+    return b;
+}
 
 // Degree-bucket histogram of a schedule (bucket b = floor(log2 deg) + 1).
 struct DegHist {
@@ -145,6 +154,21 @@ struct Groups {
     // automatic L2-sized source segments of a whole-path SpMM (api.cu)
     DevBuf<uint64_t> auto_seg_bnd;
     uint32_t auto_seg_k = 0;
+    // schedule of the atomic-free group-partitioned Fast kernel (aggregate.cu
+    // k_agg_grp), one per worker count (256 / lanes per group): CTA ranges of
+    // consecutive groups that hold whole destinations, each hub destination
+    // (more groups or edges than a CTA takes) cut into slices whose partial
+    // sums are combined in slice order by k_grp_fixup — no global atomics
+    struct GrpSched {
+        uint32_t workers = 0;
+        DevBuf<uint4> ranges;  // {g0 lo, g0 hi, groups, hub slot or ~0u}
+        uint32_t nranges = 0;
+        DevBuf<uint4> hubs;    // {dest, first slot, slices, 0}
+        uint32_t nhubs = 0, nslots = 0;
+        DevBuf<uint32_t> empty;  // destinations without groups (written on overwrite)
+        uint32_t nempty = 0;
+    };
+    std::vector<std::unique_ptr<GrpSched>> grp_scheds;
     // guards every lazily built cache above: aggregate calls on one grouping
     // may come from several host threads (the reference's aggregate_pull takes
     // a const GroupedCsr and is re-entrant); recursive because the segmented
@@ -242,6 +266,15 @@ void run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re, con
 void aggregate_groups(const uint64_t* gbeg, const uint64_t* gend, const uint32_t* gdest, const uint64_t* dest_groups,
                       uint32_t D, uint64_t G, const Edge* edges, const float* in, uint64_t ld_in, float* out,
                       uint64_t ld_out, uint64_t dim, bool accumulate, cudaStream_t s);
+
+// record a failure as the calling thread's pg_last_error / _kind (api.cu)
+void record_error(const Error& e);
+
+// The atomic-free group-partitioned Fast aggregation (default for
+// PG_AGG_GROUPED): builds / reuses G's schedule for this width, then the
+// main kernel and the hub fixup.
+void aggregate_groups_af(Groups& G, const uint64_t* offsets_dev, uint32_t D, const Edge* edges, const float* in,
+                         uint64_t ld_in, float* out, uint64_t ld_out, uint64_t dim, bool accumulate, cudaStream_t s);
 
 // PG_HEAVY_MIN_DEG / pg_set_heavy_min_degree (0 disables; UINT64_MAX restores
 // the width-dependent default)

@@ -258,6 +258,112 @@ def backward_epp(prepared, arts, top_grad, weights, plan_, rank, group=None, exp
     return w_grads
 
 
+# ------------------------------------------------ library communicator ----
+
+class Comm:
+    """The library's communicator (pg_comm, include/pathgcn_b200.h): one
+    NCCL rank on this process's device. The row-sharded stage and the row
+    all-gather run INSIDE the library (comm.cu): per-owner broadcasts on its
+    communication stream, each source-segment pass of the SpMM starting as
+    soon as its owner's rows have landed. torch.distributed only bootstraps
+    the 128-byte NCCL id (``from_process_group``)."""
+
+    SINGLE_PASS = 8  # PG_SHARD_SINGLE_PASS
+
+    def __init__(self, device, world, rank, unique_id: bytes):
+        import ctypes as C
+
+        from . import _lib
+
+        if len(unique_id) != 128:
+            raise ValueError("NCCL unique id must be 128 bytes")
+        self._L = _lib.load()
+        buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        h = C.c_void_p()
+        from .pathgcn import _check
+
+        _check(self._L.pg_comm_init_rank(int(device), buf, int(world), int(rank), C.byref(h)))
+        self._h = h
+        self.world, self.rank, self.device = int(world), int(rank), int(device)
+
+    @staticmethod
+    def unique_id() -> bytes:
+        import ctypes as C
+
+        from . import _lib
+        from .pathgcn import _check
+
+        buf = (C.c_uint8 * 128)()
+        _check(_lib.load().pg_comm_unique_id(buf))
+        return bytes(buf)
+
+    @classmethod
+    def from_process_group(cls, device, group=None):
+        """Rank 0 of ``group`` makes the id; torch.distributed ships it."""
+        import torch.distributed as dist
+
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        return cls(device, world, rank, obj[0])
+
+    def nccl_version(self):
+        import ctypes as C
+
+        from .pathgcn import _check
+
+        v = C.c_int()
+        _check(self._L.pg_comm_info(self._h, None, None, C.byref(v)))
+        return v.value
+
+    def allgather_rows(self, full, bounds, stream=None):
+        """In place: rank s owns rows [bounds[s], bounds[s+1]) of ``full`` (a
+        pitched row matrix, e.g. ``empty_rows``); whole padded rows move."""
+        import ctypes as C
+
+        from .pathgcn import _check, _p, _stream, u32p
+
+        w = whole_rows(full)
+        if w is None:
+            raise ValueError("allgather_rows: the row pitch of `full` is not backed by storage")
+        b = np.ascontiguousarray(bounds, np.uint32)
+        _check(self._L.pg_comm_allgather_rows(self._h, C.c_void_p(w.data_ptr()), w.stride(0), _p(b, u32p),
+                                              _stream(stream)))
+        return full
+
+    def backward_aggregation(self, grouped, y_full, x_rows, parent_bounds, dest_bounds, mode="deterministic",
+                             overwrite=True, single_pass=False, stream=None):
+        """pg_backward_aggregate_sharded: this rank's parent rows of ``y_full``
+        are filled; the call completes it from the other ranks and aggregates
+        this rank's destination rows into ``x_rows``."""
+        import ctypes as C
+
+        from .pathgcn import _check, _dev, _flags, _p, _stream, u32p
+
+        pb = np.ascontiguousarray(parent_bounds, np.uint32)
+        db = np.ascontiguousarray(dest_bounds, np.uint32)
+        p = grouped.base
+        _dev(y_full, "y_grad", rows=p.P)
+        _dev(x_rows, "x_grad", rows=int(db[self.rank + 1] - db[self.rank]), cols=y_full.shape[1])
+        flags = _flags(mode, overwrite) | (self.SINGLE_PASS if single_pass else 0)
+        _check(self._L.pg_backward_aggregate_sharded(self._h, grouped._h, _p(pb, u32p), _p(db, u32p),
+                                                     C.c_void_p(y_full.data_ptr()), y_full.shape[0],
+                                                     y_full.stride(0), C.c_void_p(x_rows.data_ptr()),
+                                                     x_rows.stride(0), y_full.shape[1], flags, _stream(stream)))
+        return x_rows
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._L.pg_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def balance_bounds(offsets, bounds, times):
     """One re-balancing step of the destination-row cuts from measured
     per-shard times: inside current shard r every edge is assumed to cost

@@ -3,7 +3,10 @@ aggregate.hpp:84-115) and the measured gs oracle on the device
 (train.hpp:35-54). Fast re-associates across the groups
 of a destination (atomics), so it is checked against the f64 oracle with the
 conditioning-aware fp32 bound; with gs >= max degree every destination owns
-one group and the result is bit-equal to Deterministic."""
+one group and the result is bit-equal to Deterministic. The default grouped
+kernel (tuning grouped_seg 0) is atomic-free: whole-destination CTA ranges,
+records staged by TMA bulk copy, a segmented reduction in group order and a
+slice-order fixup for hub destinations — deterministic run to run."""
 import numpy as np
 import pytest
 
@@ -23,7 +26,7 @@ def setup(pg, orc, n=2048, m=30000, seed=3, ratio=0.2):
     return g, paths, og, ops
 
 
-@pytest.mark.parametrize("seg", [0, 1])
+@pytest.mark.parametrize("seg", [0, 1, 2])
 @pytest.mark.parametrize("dim", [16, 41, 602])
 def test_grouped_within_tolerance(pg, orc, cuda, dim, seg):
     import torch
@@ -96,3 +99,40 @@ def test_measured_oracle(pg, orc, cuda):
     tmin = min(t for _, t in table)
     assert dict(table)[best] == tmin
     assert pg.choose_gs("oracle:measured", p, 64) in cands
+
+
+@pytest.mark.parametrize("dim", [16, 100, 602])
+def test_grouped_atomic_free_hubs_and_determinism(pg, orc, cuda, dim):
+    """Hub destinations with more groups than a CTA range takes and more
+    edges than its staging window (sliced, combined by the fixup kernel),
+    odd widths, small and large gs: within tolerance of f64, bit-identical
+    across repeated runs (no atomics), and bit-equal to Deterministic when
+    every destination owns one group."""
+    import torch
+
+    g, paths, og, ops = setup(pg, orc, n=16384, m=16384 * 64, seed=5, ratio=0.5)
+    p, op = paths[1], ops[1]
+    assert p.max_degree > 4096  # a hub past the 4096-record staging window
+    y = np.random.default_rng(dim + 1).uniform(-1, 1, size=(p.P, dim)).astype(np.float32)
+    yd = pg.empty_rows(p.P, dim)
+    yd.copy_(torch.from_numpy(y))
+    yu = y[op.srcpos]
+    want64 = orc.aggregate_pull_f64(op.offsets, op.neighbors, op.weights, yu.astype(np.float64))
+    absum = orc.aggregate_pull_f64(op.offsets, op.neighbors, np.abs(op.weights), np.abs(yu).astype(np.float64))
+    det = pg.empty_rows(p.D, dim)
+    pg.backward_aggregation(pg.group_neighbors(p, 1), yd, det, overwrite=True)
+    torch.cuda.synchronize()
+    for gs in (1, 2, 7, 42, 256, 1 << 20):
+        G = pg.group_neighbors(p, gs)
+        runs = []
+        for _ in range(2):
+            x = pg.empty_rows(p.D, dim)
+            x.fill_(float("nan"))
+            pg.backward_aggregation(G, yd, x, mode=pg.GROUPED, overwrite=True)
+            torch.cuda.synchronize()
+            runs.append(x.cpu().numpy())
+        assert np.array_equal(runs[0].view(np.uint32), runs[1].view(np.uint32)), gs
+        err = np.abs(runs[0].astype(np.float64) - want64)
+        assert (err <= 1e-6 + 1e-5 * absum).all(), (gs, float((err / (1e-6 + 1e-5 * absum)).max()))
+        if gs >= p.max_degree:
+            assert np.array_equal(runs[0].view(np.uint32), det.cpu().numpy().view(np.uint32))

@@ -1,0 +1,65 @@
+"""SASS-level properties of the built library (CPU: cuobjdump on the
+sm_100a cubin): the kernels do what DESIGN.md says they do."""
+import os
+import re
+import shutil
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SO = os.path.join(ROOT, "paper_2204_02662_b200", "libpathgcn_b200.so")
+
+
+def _sass():
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(exe) or not os.path.exists(SO):
+        pytest.skip("cuobjdump or the library missing")
+    out = subprocess.run([exe, "-sass", SO], capture_output=True, text=True, timeout=300).stdout
+    funcs, cur = {}, None
+    for line in out.splitlines():
+        m = re.match(r"\s+Function : (\S+)", line)
+        if m:
+            cur = m.group(1)
+            funcs[cur] = []
+        elif cur:
+            funcs[cur].append(line)
+    return funcs
+
+
+# an instruction whose opcode is a global reduction / atomic (the mbarrier
+# SYNCS.ARRIVE.TRANS64.RED of the bulk copy is a shared-memory barrier op)
+GLOBAL_ATOMIC = re.compile(r"^\s*/\*[0-9a-f]+\*/\s+(@!?U?P\w+\s+)?(RED|ATOM|ATOMG)\b", re.M)
+
+
+@pytest.fixture(scope="module")
+def sass():
+    return _sass()
+
+
+def _kernels(sass, pat):
+    ks = {k: "\n".join(v) for k, v in sass.items() if re.search(pat, k)}
+    assert ks, pat
+    return ks
+
+
+def test_grouped_kernel_is_atomic_free_and_stages_records(sass):
+    """k_agg_grp (PG_AGG_GROUPED default): no global RED/ATOM; the record
+    window arrives by TMA bulk copy (UBLKCP) and is read from shared memory
+    (LDS); row gathers are 128-bit (LDG.E.128)."""
+    for name, body in _kernels(sass, r"k_agg_grp").items():
+        assert not GLOBAL_ATOMIC.search(body), name
+        assert "UBLKCP" in body and re.search(r"\bLDS", body), name
+        # staged records are read through the shared window, not generic loads
+        assert not re.search(r"\bLD\.E", body), name
+        assert "LDG.E.128" in body, name
+    for name, body in _kernels(sass, r"k_grp_fixup").items():
+        assert not GLOBAL_ATOMIC.search(body), name
+
+
+def test_tensor_core_gemm_uses_tcgen05(sass):
+    """k_gemm_abt_tc: tcgen05 MMAs (UTCHMMA for kind::tf32), TMEM loads
+    (LDTM), TMA tensor loads (UTMALDG) and bulk copies (UBLKCP)."""
+    for name, body in _kernels(sass, r"k_gemm_abt_tc").items():
+        for op in ("UTCHMMA", "LDTM", "UTMALDG", "UBLKCP"):
+            assert op in body, (name, op)
