@@ -289,8 +289,9 @@ def workload_config(cfg, args, gs):
             "weights": "sym-norm", "gs": gs, "gs_strategy": "regression",
             "l2": "no flush between steps; per-step inputs (y_grad + x_grad + edge records) exceed the 126 MB L2 at "
                   "the reddit and products shapes (> 1 GB); arxiv/cora/pubmed are L2-resident",
-            "parallelism": (f"dest-row shards x{args.gpus} (edge-balanced) + per-path NCCL all-gather-v of y_grad rows "
-                             f"({os.environ.get('PG_ALLGATHER', 'p2p')})") if args.gpus > 1 else "1 GPU"}
+            "parallelism": (f"dest-row shards x{args.gpus} (edge-balanced, calibrated) + per-path NCCL exchange of "
+                             f"y_grad rows ({os.environ.get('PG_ALLGATHER', 'lib')}: lib = inside the C ABI, "
+                             f"pg_backward_aggregate_sharded)") if args.gpus > 1 else "1 GPU"}
 
 
 # ------------------------------------------------------------- our arm ---
@@ -395,9 +396,18 @@ def main():
             del yt
     parent_rows = [p.P for p in paths]
     shards = pgd.plan([None] * L, parent_rows, world, dest_bounds)
-    # PG_ALLGATHER=p2p (default): unpadded all-gather-v straight into
-    # frontier order; =padded: equal-size all_gather + remapped edge stream
-    xmode = os.environ.get("PG_ALLGATHER", "p2p")  # p2p | padded | bcast
+    # PG_ALLGATHER=lib (default): the library's communicator
+    # (pg_backward_aggregate_sharded: per-owner NCCL broadcasts inside the
+    # library, each source-segment pass starting as its owner's rows land);
+    # =p2p: torch.distributed all-gather-v then the row-range SpMM;
+    # =padded: equal-size all_gather + remapped edge stream; =bcast: the same
+    # overlap as lib, driven from Python
+    xmode = os.environ.get("PG_ALLGATHER", "lib")  # lib | p2p | padded | bcast
+    # (one-device rehearsal of N>1 over gloo: NCCL cannot put two ranks on one GPU)
+    one_dev = os.environ.get("PG_BENCH_ONE_DEVICE") == "1"
+    if one_dev and xmode == "lib":
+        xmode = "p2p"
+    comm = pgd.Comm.from_process_group(local) if world > 1 and xmode == "lib" else None
     padded = xmode == "padded"
     y_shard, y_full, x_out, rows = [], [], [], []
     for i, p in enumerate(paths):
@@ -435,7 +445,13 @@ def main():
         for i in range(L):
             if ev is not None:
                 ev[i][0].record(stream)
-            if world > 1 and xmode == "bcast":
+            if comm is not None:
+                # exchange + SpMM in one library call (overlapped inside)
+                if ev is not None:
+                    ev[i][1].record(stream)
+                comm.backward_aggregation(groups[i], y_full[i][:, : dims[i]], x_out[i], shards[i].parent_bounds,
+                                          shards[i].dest_bounds, overwrite=True)
+            elif world > 1 and xmode == "bcast":
                 # rank s's rows arrive by broadcast s (all issued async, in
                 # order); segment s's pass starts as soon as they are in —
                 # the exchange overlaps the SpMM of earlier segments
@@ -582,7 +598,7 @@ def main():
         line["parity"] = x_grad_parity(x_out, dims, args.config)
     if not args.profile and not args.no_e2e:
         line["e2e"] = measure_e2e(pg, pgd, torch, dist, paths, groups, shards, dims, rows, world, rank, dev,
-                                  max(3, min(args.steps, 10)), ep_bytes)
+                                  max(3, min(args.steps, 10)), ep_bytes, comm)
     if not args.profile and world == 1 and (args.train_sweep or args.config == "products"):
         line["train_sweep"] = train_sweep(pg, torch, g, cfg, dims, dev)
     if not args.profile and world == 1 and (args.gs_sweep or args.config == "arxiv"):
@@ -590,7 +606,7 @@ def main():
     if not args.profile and not args.no_chain and world == 1:
         line["chain"] = measure_chain(pg, torch, g, prep, cfg, vt, dev)
     elif not args.profile and not args.no_chain:
-        line["chain"] = measure_chain_sharded(pg, pgd, torch, dist, g, prep, cfg, vt, dev, shards, rank, world)
+        line["chain"] = measure_chain_sharded(pg, pgd, torch, dist, g, prep, cfg, vt, dev, shards, rank, world, comm)
     if not args.profile and not args.no_cpu and world == 1 and rank == 0:
         line["cpu_baseline"] = cpu_baseline(paths, dims, args)
 
@@ -598,6 +614,8 @@ def main():
         dist.barrier()
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     if world > 1:
         dist.destroy_process_group()
 
@@ -790,7 +808,7 @@ def measure_chain(pg, torch, g, prep, cfg, vt, dev, reps=5):
     return out
 
 
-def measure_chain_sharded(pg, pgd, torch, dist, g, prep, cfg, vt, dev, shards, rank, world, reps=5):
+def measure_chain_sharded(pg, pgd, torch, dist, g, prep, cfg, vt, dev, shards, rank, world, comm=None, reps=5):
     """N > 1: the row-sharded backward_epp chain (dist.backward_epp: narrow g
     all-gathered, W' and y_grad recomputed per rank, own destination rows
     aggregated), timed with CUDA events, max over ranks; forward replicated."""
@@ -809,14 +827,14 @@ def measure_chain_sharded(pg, pgd, torch, dist, g, prep, cfg, vt, dev, shards, r
     arts = pg.forward(pg.group_neighbors(g, 1), x0, ws)
     top = pg.empty_rows(n, dims[-1], device=dev)
     top.uniform_(-1e-3, 1e-3, generator=gen)
-    pgd.backward_epp(prep, arts, top, ws, shards, rank)
+    pgd.backward_epp(prep, arts, top, ws, shards, rank, comm=comm)
     torch.cuda.synchronize()
     ts = []
     for _ in range(reps):
         dist.barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        pgd.backward_epp(prep, arts, top, ws, shards, rank)
+        pgd.backward_epp(prep, arts, top, ws, shards, rank, comm=comm)
         b.record()
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b))
@@ -928,7 +946,7 @@ def sweep(pg, torch, step, paths, dims, stream):
         log(f"[sweep] pinned {name} {nbytes / 1e6:.0f} MB: {nbytes * 5 / (a.elapsed_time(b) / 1e3) / 1e9:.1f} GB/s")
 
 
-def measure_e2e(pg, pgd, torch, dist, paths, groups, shards, dims, rows, world, rank, dev, steps, ep_bytes):
+def measure_e2e(pg, pgd, torch, dist, paths, groups, shards, dims, rows, world, rank, dev, steps, ep_bytes, comm=None):
     """Same metric through the public API with HOST buffers: every step
     copies this rank's y_grad rows host->device (pinned), aggregates, and
     reads this rank's x_grad rows back. N=1: the host DenseMatrix drop-in
@@ -1003,6 +1021,13 @@ def measure_e2e(pg, pgd, torch, dist, paths, groups, shards, dims, rows, world, 
 
         def one():
             for i in range(L):
+                if comm is not None:
+                    pb, pe = shards[i].my_parent_rows(rank)
+                    yf[i][pb:pe, : dims[i]].copy_(ys[i], non_blocking=True)
+                    comm.backward_aggregation(groups[i], yf[i][:, : dims[i]], xd[i], shards[i].parent_bounds,
+                                              shards[i].dest_bounds, overwrite=True)
+                    xh[i].copy_(xd[i], non_blocking=True)
+                    continue
                 if padded:
                     yd[i][: ys[i].shape[0], : dims[i]].copy_(ys[i], non_blocking=True)
                     pgd.allgather_rows(yd[i], yf[i])
@@ -1027,7 +1052,9 @@ def measure_e2e(pg, pgd, torch, dist, paths, groups, shards, dims, rows, world, 
     return {"value": round(ep_bytes / sec / 1e9, 2), "unit": "GB/s", "ms_per_step": round(sec * 1e3, 3),
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": steps, **stats,
             "api": "pg_backward_aggregate_host (pinned host buffers)" if world == 1 else
-                   "H2D shard + NCCL all-gather-v + pg_backward_aggregate_rows + D2H shard"}
+                   ("H2D shard + pg_backward_aggregate_sharded (library NCCL exchange overlapped with the SpMM) "
+                    "+ D2H shard" if comm is not None else
+                    "H2D shard + NCCL all-gather-v + pg_backward_aggregate_rows + D2H shard")}
 
 
 def cpu_baseline(paths, dims, args):

@@ -25,6 +25,7 @@
 // reference. All compute runs on the GPU (libpathgcn_b200.so, sm_100a).
 #pragma once
 
+#include <array>
 #include <cstdint>
 #include <memory>
 #include <optional>
@@ -551,6 +552,58 @@ private:
     }
     pg_mat m_{};
     int dev_ = 0;
+};
+
+// ---------------- multi-GPU: the library's NCCL communicator ----------------
+// One rank per device; rank 0's unique_id() is shipped to every rank by the
+// caller's bootstrap (MPI, a file, torch.distributed).
+class Communicator {
+public:
+    using Id = std::array<std::uint8_t, PG_COMM_ID_BYTES>;
+    static Id unique_id() {
+        Id id{};
+        check(pg_comm_unique_id(id.data()));
+        return id;
+    }
+    Communicator(int device, const Id& id, int world, int rank) : dev_(device) {
+        check(pg_comm_init_rank(device, id.data(), world, rank, &h_.h));
+        check(pg_comm_info(h_.h, &world_, &rank_, &nccl_));
+    }
+    int world() const { return world_; }
+    int rank() const { return rank_; }
+    int nccl_version() const { return nccl_; }
+    // edge-balanced destination cuts of a path (pg_path_shard_bounds)
+    std::vector<std::uint32_t> shard_bounds(const DevicePath& p) const {
+        std::vector<std::uint32_t> b(world_ + 1);
+        check(pg_path_shard_bounds(p.raw(), static_cast<std::uint32_t>(world_), b.data()));
+        return b;
+    }
+    // engine.hpp:331-338 row-sharded: y_full holds this rank's parent rows;
+    // x_rows receives destination rows [dest_bounds[rank], dest_bounds[rank+1])
+    void backward_aggregation(const DeviceGroups& grouped, std::span<const std::uint32_t> parent_bounds,
+                              std::span<const std::uint32_t> dest_bounds, DeviceMatrix& y_full, DeviceMatrix& x_rows,
+                              bool single_pass = false) const {
+        if (parent_bounds.size() != static_cast<std::size_t>(world_) + 1 ||
+            dest_bounds.size() != static_cast<std::size_t>(world_) + 1)
+            throw ConfigError("sharded: bounds need world + 1 cuts");
+        if (x_rows.cols() != y_full.cols() ||
+            x_rows.rows() != dest_bounds[rank_ + 1] - dest_bounds[rank_])
+            throw ShapeError("sharded: x_rows shape mismatch");
+        check(pg_backward_aggregate_sharded(h_.h, grouped.raw(), parent_bounds.data(), dest_bounds.data(),
+                                            y_full.raw().data, y_full.rows(), y_full.raw().ld, x_rows.raw().data,
+                                            x_rows.raw().ld, y_full.cols(),
+                                            PG_AGG_OVERWRITE | (single_pass ? PG_SHARD_SINGLE_PASS : 0u), nullptr));
+        check(pg_device_synchronize(dev_));
+    }
+    void allgather_rows(DeviceMatrix& rows, std::span<const std::uint32_t> bounds) const {
+        check(pg_comm_allgather_rows(h_.h, rows.raw().data, rows.raw().ld, bounds.data(), nullptr));
+        check(pg_device_synchronize(dev_));
+    }
+    pg_comm raw() const { return h_.h; }
+
+private:
+    Handle<pg_comm, pg_comm_destroy> h_;
+    int dev_ = 0, world_ = 1, rank_ = 0, nccl_ = 0;
 };
 
 struct DeviceArtifacts {                          // EpochArtifacts (engine.hpp:27-31)

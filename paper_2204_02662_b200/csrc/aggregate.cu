@@ -59,8 +59,11 @@ constexpr TuneKey kTuneKeys[] = {
     // chain y_grad = g W^T (gemm_a_bt): 0 = bit-exact FFMA2 kernel, 1 = tcgen05
     // 3xTF32 tensor-core kernel (fp32 tolerance, not bit-exact)
     {"gemm_tc", "PG_GEMM_TC", 0},
+    // k_agg_vec4 wide rows: 1 = coalesced record window + shuffles, 0 = a
+    // broadcast record load per edge
+    {"rec_window", "PG_REC_WINDOW", 1},
 };
-static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneGemmTc + 1,
+static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneRecWindow + 1,
               "kTuneKeys and enum TuneKeyId (pg_internal.h) must list the same keys in the same order");
 std::atomic<int64_t> g_tune[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];
 int64_t g_tune_def[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];  // $PG_<KEY> at load, else built-in
@@ -250,7 +253,7 @@ __device__ __forceinline__ void acc_store_ext(float* orow, uint32_t col, uint32_
 // of U edges: U edge-record loads, U row gathers (all in flight), then the
 // U ordered accumulate steps. Lanes past dim gather column 0 (in bounds,
 // discarded) so no load is predicated.
-template <int LPD, int U, bool FILT, bool CG = false>
+template <int LPD, int U, bool FILT, bool CG = false, bool RW = false>
 __global__ void __launch_bounds__(256, (U <= 8 ? 4 : 2)) k_agg_vec4(const uint64_t* __restrict__ ebeg, const uint64_t* __restrict__ eend,
                                                  const Edge* __restrict__ edges,
                                                  const uint32_t* __restrict__ order, uint32_t d_begin,
@@ -288,8 +291,32 @@ __global__ void __launch_bounds__(256, (U <= 8 ? 4 : 2)) k_agg_vec4(const uint64
     constexpr int NPL = (U + LPD - 1) / LPD;
     const unsigned sl = static_cast<unsigned>(t % LPD);
     const unsigned submask = LPD >= 32 ? 0xffffffffu : (((1u << LPD) - 1u) << (lane_id() & ~(LPD - 1u)));
+    // Wide rows (RW, LPD >= 16): a record WINDOW — LPD consecutive records,
+    // one per lane, loaded coalesced one window ahead (a 256-byte request per
+    // 32 edges instead of one broadcast record load per edge) and handed out
+    // by shuffles: the L1 sees one request per gathered row.
+    constexpr bool kWin = RW && LPD >= 16 && (LPD % U == 0);
+    uint64_t wbase = e;
+    Edge win = make_uint2(0u, 0u), nwin = make_uint2(0u, 0u);
+    if constexpr (kWin) {
+        if (e + sl < end) win = ld_rec(edges + e + sl);
+        if (e + LPD + sl < end) nwin = ld_rec(edges + e + LPD + sl);
+    }
     auto batch_recs = [&](Edge (&ed)[U], uint32_t n) {
-        if constexpr (LPD <= 8) {
+        if constexpr (kWin) {
+            (void)n;  // records past the destination's end are zero records (row 0, discarded)
+            if (e - wbase == static_cast<uint64_t>(LPD)) {  // window consumed: slide
+                wbase += LPD;
+                win = nwin;
+                nwin = wbase + LPD + sl < end ? ld_rec(edges + wbase + LPD + sl) : make_uint2(0u, 0u);
+            }
+            const unsigned off = static_cast<unsigned>(e - wbase);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                ed[u].x = __shfl_sync(submask, win.x, off + u, LPD);
+                ed[u].y = __shfl_sync(submask, win.y, off + u, LPD);
+            }
+        } else if constexpr (LPD <= 8) {
             Edge mine[NPL];
 #pragma unroll
             for (int i = 0; i < NPL; ++i) {
@@ -1575,6 +1602,10 @@ void launch_vec4(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges, 
             accumulate, kZeros, 0u, cm, ext);
     else if (cg)
         k_agg_vec4<LPD, U, false, true><<<grid_for(items * LPD, 256), 256, 0, s>>>(
+            ebeg, eend, edges, order, d_begin, items, chunks, in, static_cast<uint32_t>(ld_in * 4), out, ld_out, dim,
+            accumulate, kZeros, 0u, cm, ext);
+    else if (LPD >= 16 && tuning(kTuneRecWindow) == 1)
+        k_agg_vec4<LPD, U, false, false, true><<<grid_for(items * LPD, 256), 256, 0, s>>>(
             ebeg, eend, edges, order, d_begin, items, chunks, in, static_cast<uint32_t>(ld_in * 4), out, ld_out, dim,
             accumulate, kZeros, 0u, cm, ext);
     else

@@ -16,6 +16,8 @@
 #include <thread>
 #include <vector>
 
+#include <emmintrin.h>
+
 #include "../../include/pathgcn_b200.h"
 #include "pg_internal.h"
 
@@ -380,6 +382,40 @@ bool host_pinned(const void* p) {
     return at.type == cudaMemoryTypeHost;
 }
 
+// Streaming (non-temporal) copy for the staging pipeline: the destination is
+// written without a read-for-ownership and without displacing the cache
+// (the pinned slot is next read by the DMA engine; a downloaded row is not
+// read back by this call), so each staged byte costs one host-memory read
+// and one write instead of two reads and a write. $PG_STAGE_NT=0: memcpy.
+void stream_copy(char* dst, const char* src, size_t n) {
+    static const bool nt = [] {
+        const char* e = std::getenv("PG_STAGE_NT");
+        return !(e && std::atoi(e) == 0);
+    }();
+    if (!nt || n < 4096) {
+        std::memcpy(dst, src, n);
+        return;
+    }
+    const size_t head = (16 - reinterpret_cast<uintptr_t>(dst) % 16) % 16;
+    std::memcpy(dst, src, head);
+    dst += head;
+    src += head;
+    n -= head;
+    const size_t body = n & ~size_t(63);
+    for (size_t i = 0; i < body; i += 64) {
+        const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i));
+        const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 16));
+        const __m128i c = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 32));
+        const __m128i d = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 48));
+        _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i), a);
+        _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 16), b);
+        _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 32), c);
+        _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 48), d);
+    }
+    std::memcpy(dst + body, src + body, n - body);
+    _mm_sfence();  // the streamed bytes are globally visible before the DMA / the caller reads them
+}
+
 // memcpy split over a small persistent thread pool (the caller takes part)
 class ParallelCopy {
 public:
@@ -397,7 +433,7 @@ public:
     }
     void copy(void* dst, const void* src, size_t n) {
         if (n < (1u << 20) || nthreads_ == 1) {
-            std::memcpy(dst, src, n);
+            stream_copy(static_cast<char*>(dst), static_cast<const char*>(src), n);
             return;
         }
         {
@@ -418,7 +454,7 @@ private:
     void part(unsigned t) {
         const size_t per = ((n_ + nthreads_ - 1) / nthreads_ + 63) & ~size_t(63);  // ceil: parts cover all n_ bytes
         const size_t b = std::min(n_, per * t), e = std::min(n_, per * (t + 1));
-        if (e > b) std::memcpy(dst_ + b, src_ + b, e - b);
+        if (e > b) stream_copy(dst_ + b, src_ + b, e - b);
     }
     void loop(unsigned t) {
         uint64_t seen = 0;

@@ -305,7 +305,8 @@ enum TuneKeyId {
     kTuneGemmPacked = 20,
     kTuneHostLastSegPct = 21,
     kTuneWgradFork = 22,
-    kTuneGemmTc = 23
+    kTuneGemmTc = 23,
+    kTuneRecWindow = 24
 };
 
 int64_t tuning(int key);

@@ -195,7 +195,7 @@ def allgather_rows(shard, out, group=None):
     return out
 
 
-def backward_epp(prepared, arts, top_grad, weights, plan_, rank, group=None, expected_fingerprint=None):
+def backward_epp(prepared, arts, top_grad, weights, plan_, rank, group=None, expected_fingerprint=None, comm=None):
     """engine.hpp:316-346 (Local gather) row-sharded over the ranks of
     ``group``, bit-identical to the single-GPU ``backward_epp``.
 
@@ -216,7 +216,8 @@ def backward_epp(prepared, arts, top_grad, weights, plan_, rank, group=None, exp
     ``plan_`` is ``plan(...)`` over the paths (dest bounds per path).
     ``expected_fingerprint`` (default: recomputed from the graph and training
     set the paths were prepared from) must match every path's stamp, else
-    StalenessError (engine.hpp:280-283).
+    StalenessError (engine.hpp:280-283). ``comm`` (a ``Comm``): the g row
+    exchange runs inside the library (NCCL broadcasts), else torch.distributed.
     Returns W' per layer (full, identical on every rank)."""
     import torch
 
@@ -254,7 +255,10 @@ def backward_epp(prepared, arts, top_grad, weights, plan_, rank, group=None, exp
         pg.gather_rows(arts.pre_act[l - 1], lv[i + 1][db:de], pre)
         g = pg.empty_rows(p.D, in_dim, device=dev)  # pitched: exchanged as whole padded rows
         pg.relu_backward(x, pre, g[db:de])
-        allgatherv_rows(g, plan_[i].dest_bounds, rank, group)
+        if comm is not None:  # the exchange inside the library (NCCL broadcasts)
+            comm.allgather_rows(g, plan_[i].dest_bounds)
+        else:
+            allgatherv_rows(g, plan_[i].dest_bounds, rank, group)
     return w_grads
 
 

@@ -245,6 +245,25 @@ int main() {
         }
         report("missing file -> IoError", io);
     }
+    // the library communicator, one rank (NCCL through the C ABI): the
+    // sharded stage equals the single-GPU stage bit for bit
+    {
+        const auto id = Communicator::unique_id();
+        Communicator comm(0, id, 1, 0);
+        report("communicator: one rank, NCCL loaded", comm.world() == 1 && comm.rank() == 0 && comm.nccl_version() > 0);
+        auto rp = prepare_all_paths(g, f);
+        DeviceGroups gr = group_neighbors(rp[1], 2);
+        const std::size_t dim = 5;
+        MatrixF y(rp[1].parent_rows(), dim), want(rp[1].dest_count(), dim);
+        for (std::size_t i = 0; i < y.data.size(); ++i) y.data[i] = static_cast<float>(std::sin(0.37 * i));
+        backward_aggregation(gr, y, want);
+        DeviceMatrix yd = DeviceMatrix::upload(y), xd(rp[1].dest_count(), dim);
+        const std::vector<std::uint32_t> pb{0, rp[1].parent_rows()}, db = comm.shard_bounds(rp[1]);
+        comm.backward_aggregation(gr, pb, db, yd, xd);
+        const MatrixF got = xd.download();
+        report("sharded stage (1 rank) == backward_aggregation",
+               std::memcmp(got.data.data(), want.data.data(), want.data.size() * 4) == 0);
+    }
     std::printf("%d failure(s)\n", g_fail);
     return g_fail;
 }

@@ -23,6 +23,7 @@ KNOBS = {
     "wide_lpd": (16, 32),
     "src_segs": (0, 1, 2, 3),
     "heavy_tma": (0, 1),
+    "rec_window": (0, 1),
 }
 
 
