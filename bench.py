@@ -308,6 +308,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="few steps, no extras (for ncu)")
+    ap.add_argument("--ncu-path", action="store_true",
+                    help="for ncu --set full: no warm-up and one step of the dominant path only, so every "
+                         "k_agg launch of the process is one execution of that path")
     ap.add_argument("--heavy-sweep", action="store_true", help="diagnostics: heavy-kernel threshold sweep")
     ap.add_argument("--tune-sweep", action="store_true", help="diagnostics: SpMM scheduling-knob sweep")
     ap.add_argument("--no-chain", action="store_true", help="skip the forward/backward-variant chain timing")
@@ -475,6 +478,14 @@ def main():
             if ev is not None:
                 ev[i][2].record(stream)
 
+    if args.ncu_path:
+        dom_i = max(range(L), key=lambda i: path_bytes(paths[i].D, paths[i].E, dims[i]))
+        torch.cuda.synchronize()
+        pg.backward_aggregation(groups[dom_i], y_full[dom_i][:, : dims[dom_i]], x_out[dom_i], overwrite=True)
+        torch.cuda.synchronize()
+        log(f"[bench] ncu-path: one execution of path {dom_i} (D={paths[dom_i].D}, E={paths[dom_i].E}, "
+            f"dim={dims[dom_i]}, algorithmic bytes {path_bytes(paths[dom_i].D, paths[dom_i].E, dims[dom_i])})")
+        return
     if args.heavy_sweep:
         sweep(pg, torch, step, paths, dims, stream)
     if args.tune_sweep:

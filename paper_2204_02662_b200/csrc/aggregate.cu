@@ -60,8 +60,9 @@ constexpr TuneKey kTuneKeys[] = {
     // 3xTF32 tensor-core kernel (fp32 tolerance, not bit-exact)
     {"gemm_tc", "PG_GEMM_TC", 0},
     // k_agg_vec4 wide rows: 1 = coalesced record window + shuffles, 0 = a
-    // broadcast record load per edge
-    {"rec_window", "PG_REC_WINDOW", 1},
+    // broadcast record load per edge (measured equal or slightly faster on
+    // the Reddit layer-0 path: 16.52 vs 16.65 ms, so off)
+    {"rec_window", "PG_REC_WINDOW", 0},
 };
 static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneRecWindow + 1,
               "kTuneKeys and enum TuneKeyId (pg_internal.h) must list the same keys in the same order");
