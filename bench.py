@@ -557,8 +557,14 @@ def main():
     # gathered rows are reused out of L2: B/t above the HBM peak then only
     # says the gathers hit L2. The physical picture is the ncu DRAM traffic
     # of the same path execution (dram_frac) and the unit that binds.
-    l2_resident = achieved > peak
-    roofline = {"bound": "l2-gather" if l2_resident else "hbm", "achieved": round(achieved, 1), "peak": peak,
+    # the bound: the binding unit of the committed ncu capture of this path
+    # (DRAM -> "hbm", L1TEX / L2 -> "l2-gather"), else B/t above the HBM peak
+    # means the gathers are L2 hits
+    if cap and cap.get("binding_unit"):
+        bound = "hbm" if cap["binding_unit"] == "dram" else "l2-gather"
+    else:
+        bound = "l2-gather" if achieved > peak else "hbm"
+    roofline = {"bound": bound, "achieved": round(achieved, 1), "peak": peak,
                 "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                 "kernel": f"k_agg_vec4 (path SG_{p.layer}, width {dims[dom]})",
                 "algorithmic_bytes_per_launch": dom_bytes, "avg_launch_ms": round(dom_ms, 4),

@@ -147,6 +147,7 @@ SIGNATURES = {
     "pg_mat_download": [i32, f32p, PgMat],
     "pg_gemm": [PgMat, PgMat, i32, PgMat, vp],
     "pg_gemm_at_b": [PgMat, vp, PgMat, PgMat, vp],
+    "pg_gemm_at_b_ex": [PgMat, vp, PgMat, PgMat, C.c_uint, vp],
     "pg_relu": [PgMat, PgMat, vp],
     "pg_row_softmax": [PgMat, PgMat, vp],
     "pg_top_grad_from_probs": [PgMat, PgMat, vp, u64, PgMat, vp],

@@ -1604,6 +1604,16 @@ int pg_gemm_at_b(pg_mat a, const uint32_t* a_rows, pg_mat b, pg_mat out, void* s
     return guard([&] { gemm_at_b(dm(a), a_rows, dm(b), dm(out), static_cast<cudaStream_t>(stream)); });
 }
 
+int pg_gemm_at_b_ex(pg_mat a, const uint32_t* a_rows, pg_mat b, pg_mat out, unsigned flags, void* stream) {
+    return guard([&] {
+        if (flags & ~PG_GEMM_TF32X3) fail(kConfig, "gemm_at_b: unknown flags");
+        if (flags & PG_GEMM_TF32X3)
+            gemm_at_b_tc(dm(a), a_rows, dm(b), dm(out), static_cast<cudaStream_t>(stream));
+        else
+            gemm_at_b(dm(a), a_rows, dm(b), dm(out), static_cast<cudaStream_t>(stream));
+    });
+}
+
 int pg_relu(pg_mat x, pg_mat out, void* stream) {
     return guard([&] { relu(dm(x), dm(out), static_cast<cudaStream_t>(stream)); });
 }

@@ -625,7 +625,8 @@ void gemm(DMat a, DMat b, DMat out, bool b_transposed, cudaStream_t s) {
         return;
     }
     // y_grad = g W^T on the tensor cores when selected (tolerance, not bits)
-    if (b_transposed && tuning(kTuneGemmTc) == 1 && gemm_a_bt_tc_supported(a)) {
+    // (below K = 32 the write-bound FFMA2 kernel is faster and exact)
+    if (b_transposed && tuning(kTuneGemmTc) == 1 && K >= 32 && gemm_a_bt_tc_supported(a)) {
         gemm_a_bt_tc(a, b, out, s);
         return;
     }
@@ -655,6 +656,11 @@ void gemm_at_b(DMat a, const uint32_t* a_rows, DMat b, DMat out, cudaStream_t s)
     if (out.rows != r || out.cols != c) fail_shape("gemm_at_b: output shape mismatch");
     if (r == 0 || c == 0) return;
     if (n >= (1ull << 31) || r >= (1ull << 31) || c >= (1ull << 31)) fail(kConfig, "gemm_at_b: dimension too large");
+    // W' on the tensor cores when selected (split-K 3xTF32: tolerance, not bits)
+    if (tuning(kTuneGemmTc) == 1 && gemm_at_b_tc_supported(r, c)) {
+        gemm_at_b_tc(a, a_rows, b, out, s);
+        return;
+    }
     // 64 chains per warp: 4 (or 8) A columns x 16 (or 8) B columns
     if (c <= 8) launch_at_b<8>(a, a_rows, b, out, n, r, c, s);
     else launch_at_b<4>(a, a_rows, b, out, n, r, c, s);

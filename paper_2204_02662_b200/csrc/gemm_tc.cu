@@ -28,6 +28,7 @@
 #include <cuda.h>
 
 #include <cstring>
+#include <type_traits>
 #include <mutex>
 #include <vector>
 
@@ -115,6 +116,7 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
 }
 
 __device__ __forceinline__ uint32_t tf32_hi(uint32_t x) { return x & 0xFFFFE000u; }
+__device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 
 template <int MT>
 struct TcShape {
@@ -340,6 +342,275 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_gemm_abt_tc(const __grid_cons
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
 }
 
+// ---- gemm_at_b on the tensor cores: W' = gather_rows(Y, rows)^T g -----------
+// dense_matrix.hpp:57-76 (+ engine.hpp:323-324's gather folded in):
+//   out[i][j] = sum_r Y[row(r)][i] * g[r][j],  i < in_dim (M), j < out_dim (N),
+// the reduction over the n rows. Split-K: each persistent CTA owns a
+// contiguous row range and accumulates the whole (in_dim x out_dim) tile in
+// TMEM (MT 128-row M tiles x N columns, 3xTF32: ah.bh + ah.bl + al.bh), then
+// writes its partial; k_atb_reduce adds the CTA partials in CTA order
+// (deterministic run to run, re-associated vs the reference's serial chain:
+// fp32 tolerance, not bit-exact).
+// Operands are MN-major (a row of Y / g is contiguous along M / N), in the
+// 128B-swizzled MN-major canonical layout: per 8-row K group, 1024-byte atoms
+// of 32 MN elements x 8 rows (16-byte chunk c of row k at chunk c ^ (k & 7)),
+// atoms along MN at LBO = 1024 B, K groups at SBO. Producers (8 warps) gather
+// the rows with coalesced 128-bit loads (one prefetched K tile ahead), split
+// hi/lo in registers and store both straight into the swizzled slots.
+constexpr int kAtbProducers = 8;
+constexpr int kAtbThreads = 32 * (2 + kAtbProducers);  // MMA/TMEM warp, epilogue-lead, producers
+constexpr int kAtbKT = 16;  // rows per K tile (two 8-row K groups)
+
+__device__ __forceinline__ uint64_t sw128_mn_desc(uint32_t saddr, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+    d |= static_cast<uint64_t>(1024 >> 4) << 16;  // LBO: next 32-element MN atom
+    d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;  // SBO: next 8-row K group
+    d |= static_cast<uint64_t>(1) << 46;
+    d |= static_cast<uint64_t>(2) << 61;
+    return d;
+}
+// kind::tf32, D f32, A and B MN-major (bits 15, 16)
+__host__ __device__ constexpr uint32_t tf32_idesc_mn(uint32_t M, uint32_t N) {
+    return tf32_idesc(M, N) | (1u << 15) | (1u << 16);
+}
+
+struct AtbParams {
+    const float* a;
+    uint64_t lda;
+    const uint32_t* a_rows;  // nullable
+    const float* b;
+    uint64_t ldb;
+    uint64_t n;              // rows (the K extent)
+    uint32_t in_dim, out_dim;
+    uint32_t Npad;           // out_dim rounded up to 32
+    uint32_t stages;
+    uint64_t rows_per_cta;
+    float* part;             // [gridDim.x][in_dim][out_dim]
+};
+
+template <int MT>
+__global__ void __launch_bounds__(kAtbThreads, 1) k_gemm_atb_tc(AtbParams P) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    constexpr uint32_t kAtile = 128u * kAtbKT * 4u;  // one M tile of one K tile, bytes
+    const uint32_t Np = P.Npad, S = P.stages;
+    const uint32_t bbytes = Np * kAtbKT * 4u;
+    const uint32_t stage_bytes = 2u * MT * kAtile + 2u * bbytes;
+    const uint32_t sbo_a = 4u * 1024u, sbo_b = (Np / 32u) * 1024u;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + S;
+    uint64_t* done = bars + 2 * S;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 1);
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (uint32_t s = 0; s < S; ++s) {
+            mbar_init(&full[s], kAtbProducers);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_addr(tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+    const uint64_t r0 = static_cast<uint64_t>(blockIdx.x) * P.rows_per_cta;
+    const uint64_t r1 = min(P.n, r0 + P.rows_per_cta);
+    const uint32_t ntiles = r1 > r0 ? static_cast<uint32_t>((r1 - r0 + kAtbKT - 1) / kAtbKT) : 0u;
+
+    if (warp == 0) {  // the MMA issuer
+        if (lane == 0) {
+            const uint32_t idesc = tf32_idesc_mn(128, Np);
+            for (uint32_t t = 0; t < ntiles; ++t) {
+                const uint32_t s = t % S, ph = (t / S) & 1;
+                mbar_wait(&full[s], ph);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t st = smem_addr(smem + s * stage_bytes);
+                const uint32_t a_hi = st, a_lo = st + MT * kAtile, b_hi = st + 2 * MT * kAtile, b_lo = b_hi + bbytes;
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {
+                    const uint32_t d = tmem + mt * Np;
+#pragma unroll
+                    for (int g = 0; g < kAtbKT / 8; ++g) {
+                        const uint32_t acc0 = (t | g) ? 1u : 0u;
+                        const uint64_t ah = sw128_mn_desc(a_hi + mt * kAtile + g * sbo_a, sbo_a);
+                        const uint64_t al = sw128_mn_desc(a_lo + mt * kAtile + g * sbo_a, sbo_a);
+                        const uint64_t bh = sw128_mn_desc(b_hi + g * sbo_b, sbo_b);
+                        const uint64_t bl = sw128_mn_desc(b_lo + g * sbo_b, sbo_b);
+                        mma_tf32(d, ah, bh, idesc, acc0);
+                        mma_tf32(d, ah, bl, idesc, 1u);
+                        mma_tf32(d, al, bh, idesc, 1u);
+                    }
+                }
+                mma_commit(&empty[s]);
+            }
+            mma_commit(done);
+        }
+    } else if (warp >= 2) {  // producers: gather + split + swizzled store
+        const uint32_t pw = warp - 2;
+        constexpr int RPW = kAtbKT / kAtbProducers;  // rows per producer warp per K tile
+        const uint32_t nq = Np / 4;                   // float4 per B row (padded)
+        float4 ra[2][RPW][MT], rb[2][RPW][2];
+        // register double buffer indexed at compile time (a runtime index
+        // would put ra / rb in local memory)
+        auto load = [&](uint32_t t, auto bufc) {
+            constexpr int buf = decltype(bufc)::value;
+#pragma unroll
+            for (int i = 0; i < RPW; ++i) {
+                const uint64_t r = r0 + static_cast<uint64_t>(t) * kAtbKT + pw * RPW + i;
+                const bool ok = r < r1;
+                const uint64_t ar = ok ? (P.a_rows ? __ldg(P.a_rows + r) : r) : 0;
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {
+                    const uint32_t col = mt * 128 + lane * 4;
+                    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (ok && col < P.in_dim) {
+                        const float* p = P.a + ar * P.lda + col;
+                        if (col + 3 < P.in_dim) v = ldg4(p);
+                        else {
+                            v.x = __ldg(p);
+                            if (col + 1 < P.in_dim) v.y = __ldg(p + 1);
+                            if (col + 2 < P.in_dim) v.z = __ldg(p + 2);
+                        }
+                    }
+                    ra[buf][i][mt] = v;
+                }
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t q = lane + 32 * h;
+                    const uint32_t col = q * 4;
+                    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (ok && q < nq && col < P.out_dim) {
+                        const float* p = P.b + r * P.ldb + col;
+                        if (col + 3 < P.out_dim) v = ldg4(p);
+                        else {
+                            v.x = __ldg(p);
+                            if (col + 1 < P.out_dim) v.y = __ldg(p + 1);
+                            if (col + 2 < P.out_dim) v.z = __ldg(p + 2);
+                        }
+                    }
+                    rb[buf][i][h] = v;
+                }
+            }
+        };
+        auto put = [&](uint32_t hi_addr, uint32_t lo_addr, float4 v) {
+            const uint32_t h0 = tf32_hi(__float_as_uint(v.x)), h1 = tf32_hi(__float_as_uint(v.y));
+            const uint32_t h2 = tf32_hi(__float_as_uint(v.z)), h3 = tf32_hi(__float_as_uint(v.w));
+            const uint32_t l0 = __float_as_uint(__fsub_rn(v.x, __uint_as_float(h0)));
+            const uint32_t l1 = __float_as_uint(__fsub_rn(v.y, __uint_as_float(h1)));
+            const uint32_t l2 = __float_as_uint(__fsub_rn(v.z, __uint_as_float(h2)));
+            const uint32_t l3 = __float_as_uint(__fsub_rn(v.w, __uint_as_float(h3)));
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(hi_addr), "r"(h0), "r"(h1), "r"(h2), "r"(h3)
+                         : "memory");
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(lo_addr), "r"(l0), "r"(l1), "r"(l2), "r"(l3)
+                         : "memory");
+        };
+        auto step = [&](uint32_t t, auto bufc) {
+            constexpr int cb = decltype(bufc)::value;
+            if (t + 1 < ntiles) load(t + 1, std::integral_constant<int, cb ^ 1>{});  // next K tile in flight
+            const uint32_t s = t % S, ph = (t / S) & 1;
+            mbar_wait(&empty[s], ph ^ 1);
+            const uint32_t st = smem_addr(smem + s * stage_bytes);
+            const uint32_t a_hi = st, a_lo = st + MT * kAtile, b_hi = st + 2 * MT * kAtile, b_lo = b_hi + bbytes;
+#pragma unroll
+            for (int i = 0; i < RPW; ++i) {
+                const uint32_t k = pw * RPW + i, g = k >> 3, kr = k & 7;
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {
+                    const uint32_t off = mt * kAtile + g * sbo_a + (lane >> 3) * 1024u + kr * 128u +
+                                         (((lane & 7u) ^ kr) << 4);
+                    put(a_hi + off, a_lo + off, ra[cb][i][mt]);
+                }
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t q = lane + 32 * h;
+                    if (q < nq) {
+                        const uint32_t off = g * sbo_b + (q >> 3) * 1024u + kr * 128u + (((q & 7u) ^ kr) << 4);
+                        put(b_hi + off, b_lo + off, rb[cb][i][h]);
+                    }
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[s]);
+        };
+        if (ntiles) load(0, std::integral_constant<int, 0>{});
+        for (uint32_t t = 0; t < ntiles; t += 2) {
+            step(t, std::integral_constant<int, 0>{});
+            if (t + 1 < ntiles) step(t + 1, std::integral_constant<int, 1>{});
+        }
+    }
+    // epilogue: warps 0-3 read TMEM lane quarters (warp w: lanes 32w..) — the
+    // MMA warp joins after issuing; warps 2-3 after producing
+    if (warp < 4) {
+        mbar_wait(done, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        float* part = P.part + static_cast<uint64_t>(blockIdx.x) * P.in_dim * P.out_dim;
+        for (int mt = 0; mt < MT; ++mt) {
+            const uint32_t i = mt * 128 + warp * 32 + lane;
+            for (uint32_t c = 0; c < Np; c += 32) {
+                uint32_t v[32];
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+                    "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+                    "%30, %31}, [%32];"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                      "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+                      "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+                      "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+                      "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                    : "r"(tmem + ((warp * 32) << 16) + mt * Np + c));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (i < P.in_dim) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (c + j < P.out_dim) part[static_cast<uint64_t>(i) * P.out_dim + c + j] = __uint_as_float(v[j]);
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+}
+
+// out[i][j] = sum over CTAs c (ascending) of part[c][i][j]
+__global__ void k_atb_reduce(const float* __restrict__ part, uint32_t nparts, uint32_t in_dim, uint32_t out_dim,
+                             float* __restrict__ out, uint64_t ldo) {
+    const uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    const uint64_t tot = static_cast<uint64_t>(in_dim) * out_dim;
+    if (e >= tot) return;
+    float acc = 0.f;
+    for (uint32_t c = 0; c < nparts; ++c) acc = __fadd_rn(acc, part[c * tot + e]);
+    out[(e / out_dim) * ldo + e % out_dim] = __fadd_rn(acc, 0.f);
+}
+
+template <int MT>
+void launch_atb(const AtbParams& p, size_t smem, unsigned grid, cudaStream_t s) {
+    static std::vector<char> attr;
+    static std::mutex mu;
+    int dev = 0;
+    PG_CUDA(cudaGetDevice(&dev));
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (static_cast<int>(attr.size()) <= dev) attr.resize(dev + 1, 0);
+        if (!attr[dev]) {
+            PG_CUDA(cudaFuncSetAttribute(k_gemm_atb_tc<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
+            attr[dev] = 1;
+        }
+    }
+    k_gemm_atb_tc<MT><<<grid, kAtbThreads, smem, s>>>(p);
+    PG_LAUNCH("k_gemm_atb_tc");
+}
+
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
 using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -445,6 +716,63 @@ void gemm_a_bt_tc(DMat a, DMat b, DMat out, cudaStream_t s) {
         launch_tc<2>(amap, p, smem, grid, s);
     else
         launch_tc<1>(amap, p, smem, grid, s);
+}
+
+bool gemm_at_b_tc_supported(uint64_t in_dim, uint64_t out_dim) {
+    const uint64_t Np = (out_dim + 31) / 32 * 32;
+    const uint64_t MT = (in_dim + 127) / 128;
+    return in_dim > 0 && out_dim > 0 && Np <= 256 && MT >= 1 && MT <= 5 && MT * Np <= 512;
+}
+
+void gemm_at_b_tc(DMat a, const uint32_t* a_rows, DMat b, DMat out, cudaStream_t s) {
+    const uint64_t n = b.rows, in_dim = a.cols, out_dim = b.cols;
+    if (!a_rows && a.rows != n) fail_shape("gemm_at_b: row counts differ");
+    if (out.rows != in_dim || out.cols != out_dim) fail_shape("gemm_at_b: output shape mismatch");
+    if (in_dim == 0 || out_dim == 0) return;
+    if (!gemm_at_b_tc_supported(in_dim, out_dim))
+        fail(kConfig, "gemm_at_b (tensor cores): needs in_dim <= 640, out_dim <= 256 and in/128 x out/32 <= 16 tiles");
+    if (n == 0) {
+        PG_CUDA(cudaMemset2DAsync(out.p, out.ld * 4, 0, out_dim * 4, in_dim, s));
+        return;
+    }
+    const uint32_t Np = static_cast<uint32_t>((out_dim + 31) / 32 * 32);
+    const int MT = static_cast<int>((in_dim + 127) / 128);
+    const size_t stage = 2ull * MT * 128 * kAtbKT * 4 + 2ull * Np * kAtbKT * 4;
+    const size_t budget = 232448 - 1024 - 256;
+    const uint32_t S = static_cast<uint32_t>(std::min<size_t>(6, budget / stage));
+    if (S < 2) fail(kConfig, "gemm_at_b (tensor cores): tile does not fit shared memory");
+    const size_t smem = 1024 + S * stage + (2 * S + 2) * 8 + 16;
+    int dev = 0, sms = 148;
+    PG_CUDA(cudaGetDevice(&dev));
+    PG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const uint64_t tiles = (n + kAtbKT - 1) / kAtbKT;
+    const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(tiles, static_cast<uint64_t>(sms)));
+    const uint64_t per = (tiles + grid - 1) / grid * kAtbKT;
+    const uint32_t nparts = static_cast<uint32_t>((n + per - 1) / per);
+    DevBuf<float> part(static_cast<uint64_t>(nparts) * in_dim * out_dim, s);
+    AtbParams p{};
+    p.a = a.p;
+    p.lda = a.ld;
+    p.a_rows = a_rows;
+    p.b = b.p;
+    p.ldb = b.ld;
+    p.n = n;
+    p.in_dim = static_cast<uint32_t>(in_dim);
+    p.out_dim = static_cast<uint32_t>(out_dim);
+    p.Npad = Np;
+    p.stages = S;
+    p.rows_per_cta = per;
+    p.part = part.get();
+    switch (MT) {
+        case 1: launch_atb<1>(p, smem, nparts, s); break;
+        case 2: launch_atb<2>(p, smem, nparts, s); break;
+        case 3: launch_atb<3>(p, smem, nparts, s); break;
+        case 4: launch_atb<4>(p, smem, nparts, s); break;
+        default: launch_atb<5>(p, smem, nparts, s); break;
+    }
+    const uint64_t tot = in_dim * out_dim;
+    k_atb_reduce<<<grid_for(tot, 256), 256, 0, s>>>(part.get(), nparts, p.in_dim, p.out_dim, out.p, out.ld);
+    PG_LAUNCH("k_atb_reduce");
 }
 
 }  // namespace pg

@@ -749,11 +749,14 @@ def gemm(a, b, out, stream=None):
     return out
 
 
-def gemm_at_b(a, b, out, a_rows=None, stream=None):
+def gemm_at_b(a, b, out, a_rows=None, stream=None, tensor_cores=False):
     """dense_matrix.hpp:57-76: out = a^T * b; with a_rows (int32/uint32 CUDA
-    tensor of b.rows ids) out = gather_rows(a, a_rows)^T * b."""
+    tensor of b.rows ids) out = gather_rows(a, a_rows)^T * b. Default:
+    bit-exact serial chains. tensor_cores=True: split-K tcgen05 3xTF32
+    (PG_GEMM_TF32X3) — within the fp32 tolerance, not bit-exact."""
     rows = None if a_rows is None else C.c_void_p(a_rows.data_ptr())
-    _check(_lib_().pg_gemm_at_b(_mat(a, "a"), rows, _mat(b, "b"), _mat(out, "out"), _stream(stream)))
+    _check(_lib_().pg_gemm_at_b_ex(_mat(a, "a"), rows, _mat(b, "b"), _mat(out, "out"),
+                                   PG_GEMM_TF32X3 if tensor_cores else 0, _stream(stream)))
     return out
 
 

@@ -107,3 +107,61 @@ def test_chain_with_tc_y_grad_within_tolerance(pg, orc):
         pg.set_tuning("gemm_tc", None)
     for e, t in zip(exact, tc):
         assert np.linalg.norm(t - e) <= 1e-5 * np.linalg.norm(e)
+
+
+def _atb_case(pg, n, rows_y, in_dim, out_dim, seed, gathered=True):
+    import torch
+
+    rng = np.random.default_rng(seed)
+    y = rng.uniform(-1, 1, size=(rows_y, in_dim)).astype(np.float32)
+    g = rng.uniform(-1, 1, size=(n, out_dim)).astype(np.float32)
+    ids = np.sort(rng.choice(rows_y, size=n, replace=False)).astype(np.int32) if gathered else None
+    yd = pg.empty_rows(rows_y, in_dim)
+    yd.copy_(torch.from_numpy(y))
+    gd = pg.empty_rows(n, out_dim)
+    gd.copy_(torch.from_numpy(g))
+    od = pg.empty_rows(in_dim, out_dim)
+    od.fill_(float("nan"))
+    idd = None if ids is None else torch.from_numpy(ids).cuda()
+    pg.gemm_at_b(yd, gd, od, a_rows=idd, tensor_cores=True)
+    torch.cuda.synchronize()
+    ya = (y[ids] if gathered else y).astype(np.float64)
+    exact = ya.T @ g.astype(np.float64)
+    mag = np.abs(ya).T @ np.abs(g).astype(np.float64)
+    return od.cpu().numpy().astype(np.float64), exact, mag
+
+
+@pytest.mark.parametrize("n,rows_y,in_dim,out_dim", [(7, 9, 33, 5), (1000, 1500, 100, 256), (50_000, 60_000, 602, 16),
+                                                     (20_000, 20_000, 16, 41), (5_000, 8_000, 256, 47),
+                                                     (40_000, 50_000, 128, 40), (333, 400, 640, 32)])
+def test_tc_gemm_at_b_tolerance(pg, n, rows_y, in_dim, out_dim):
+    """W' = gather_rows(Y, rows)^T g (dense_matrix.hpp:57-76 + engine.hpp:
+    323-324) on the tensor cores: split-K 3xTF32, CTA partials added in a
+    fixed order."""
+    got, exact, mag = _atb_case(pg, n, rows_y, in_dim, out_dim, seed=n + in_dim)
+    _gate(got, exact, mag)
+
+
+def test_tc_gemm_at_b_products_shape_deterministic(pg):
+    """The products layer-0 W' (1.2M gathered rows, 100 x 256): within
+    tolerance and bit-identical run to run (no atomics in the reduction)."""
+    import torch
+
+    got, exact, mag = _atb_case(pg, 1_198_008, 2_449_029, 100, 256, seed=3)
+    _gate(got, exact, mag)
+    got2, _, _ = _atb_case(pg, 1_198_008, 2_449_029, 100, 256, seed=3)
+    assert np.array_equal(got.view(np.uint64), got2.view(np.uint64))
+
+
+def test_tc_gemm_at_b_ungathered_and_empty(pg):
+    import torch
+
+    got, exact, mag = _atb_case(pg, 3000, 3000, 50, 20, seed=9, gathered=False)
+    _gate(got, exact, mag)
+    a = pg.empty_rows(5, 8)
+    b = pg.empty_rows(0, 4)
+    o = pg.empty_rows(8, 4)
+    o.fill_(1.0)
+    pg.gemm_at_b(a, b, o, a_rows=torch.zeros(0, dtype=torch.int32, device="cuda"), tensor_cores=True)
+    torch.cuda.synchronize()
+    assert (o.cpu().numpy() == 0).all()

@@ -51,5 +51,44 @@ def main():
         torch.cuda.empty_cache()
 
 
+# W' = gather_rows(Y, rows)^T g: (name, n rows of g, rows of Y, in_dim, out_dim)
+ATB = [("products layer0 W'", 1_198_008, 2_449_029, 100, 256), ("products top W'", 195_922, 2_449_029, 256, 47),
+       ("reddit layer0 W'", 232_756, 232_965, 602, 16), ("reddit top W'", 153_756, 232_965, 16, 41),
+       ("arxiv layer0 W'", 113_323, 169_343, 128, 256)]
+
+
+def main_atb():
+    only = [a.split("=", 1)[1] for a in sys.argv if a.startswith("--only=")]
+    for name, n, ry, ind, outd in ATB:
+        if only and not any(o in name for o in only):
+            continue
+        y = pg.empty_rows(ry, ind)
+        y.uniform_(-1, 1)
+        g = pg.empty_rows(n, outd)
+        g.uniform_(-1, 1)
+        ids = torch.sort(torch.randperm(ry, device="cuda")[:n].to(torch.int32))[0]
+        o = pg.empty_rows(ind, outd)
+        res = {}
+        for tc in (False, True):
+            pg.gemm_at_b(y, g, o, a_rows=ids, tensor_cores=tc)
+            torch.cuda.synchronize()
+            ts = []
+            for _ in range(5):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                pg.gemm_at_b(y, g, o, a_rows=ids, tensor_cores=tc)
+                e1.record()
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            res[tc] = statistics.median(ts)
+        byt = n * ind * 4 + n * outd * 4
+        print(f"{name:22s} n={n} {ind}x{outd}: serial chains {res[False]:.3f} ms, tcgen05 split-K 3xTF32 "
+              f"{res[True]:.3f} ms ({res[False] / res[True]:.1f}x); tc {byt / res[True] / 1e6:.0f} GB/s of Y rows + g",
+              flush=True)
+        del y, g, o, ids
+        torch.cuda.empty_cache()
+
+
 if __name__ == "__main__":
     main()
+    main_atb()
