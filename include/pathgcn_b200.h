@@ -243,6 +243,20 @@ int pg_aggregate_pull_host(pg_groups G, const float* in_host, uint64_t in_rows, 
                            float* out_host, unsigned flags, uint64_t* counters);
 int pg_backward_aggregate_host(pg_groups G, const float* y_host, uint64_t y_rows, uint64_t dim,
                                float* x_host, unsigned flags, uint64_t* counters);
+/* aggregate_pull<double> — the reference's default precision
+ * (run_config.hpp:53 Precision::F64): the same operators on f64 rows with the
+ * f64 path weights, Deterministic order (bit-exact with the reference's
+ * f64 build; PG_AGG_FAST gives the same result; PG_AGG_GROUPED is fp32-only).
+ * Device rows need an even ld and a 16-byte aligned base; the host variants
+ * take DenseMatrix<double> rows (ld = cols) and are synchronous. */
+int pg_aggregate_pull_f64(pg_groups G, const double* in_dev, uint64_t in_rows, uint64_t ld_in, double* out_dev,
+                          uint64_t ld_out, uint64_t dim, unsigned flags, void* stream);
+int pg_backward_aggregate_f64(pg_groups G, const double* y_dev, uint64_t y_rows, uint64_t ld_in, double* x_dev,
+                              uint64_t ld_out, uint64_t dim, unsigned flags, void* stream);
+int pg_aggregate_pull_host_f64(pg_groups G, const double* in_host, uint64_t in_rows, uint64_t dim,
+                               double* out_host, unsigned flags, uint64_t* counters);
+int pg_backward_aggregate_host_f64(pg_groups G, const double* y_host, uint64_t y_rows, uint64_t dim,
+                                   double* x_host, unsigned flags, uint64_t* counters);
 /* StageCounters (aggregate.hpp:23-39) of one call, analytically:
  * {edges_traversed, groups_executed, atomic_commits}. */
 int pg_stage_counters(pg_groups G, uint64_t dim, unsigned flags, uint64_t* counters);

@@ -126,6 +126,10 @@ SIGNATURES = {
     "pg_groups_set_segments": [H, u64p, u32],
     "pg_backward_aggregate_segment": [H, u32, u32, u32, vp, u64, u64, vp, u64, u64, C.c_uint, vp],
     "pg_gemm_a_bt": [vp, u64, vp, u64, vp, u64, u64, u64, u64, vp],
+    "pg_aggregate_pull_f64": [H, vp, u64, u64, vp, u64, u64, C.c_uint, vp],
+    "pg_backward_aggregate_f64": [H, vp, u64, u64, vp, u64, u64, C.c_uint, vp],
+    "pg_aggregate_pull_host_f64": [H, f64p, u64, u64, f64p, C.c_uint, u64p],
+    "pg_backward_aggregate_host_f64": [H, f64p, u64, u64, f64p, C.c_uint, u64p],
     "pg_comm_unique_id": [vp],
     "pg_comm_init_rank": [C.c_int, vp, C.c_int, C.c_int, C.POINTER(H)],
     "pg_comm_info": [H, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)],

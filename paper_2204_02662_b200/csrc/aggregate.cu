@@ -1569,6 +1569,69 @@ void launch_grp(Groups& G, const Groups::GrpSched& sc, const Edge* edges, uint32
     }
 }
 
+// ---- aggregate_pull<double> (aggregate.hpp:56-122 with T = double) --------
+// The reference's default precision (run_config.hpp:53 Precision::F64): per
+// destination and column, ascending edge order, acc = fl(acc + fl(w * x))
+// in f64 with w the path's f64 weight unconverted (static_cast<double>),
+// separately rounded (__dmul_rn / __dadd_rn: no contraction, like the
+// default-flag x86-64 build), then acc + 0. A (sub-)warp owns (destination,
+// column chunk), a lane a double2 (one 128-bit gather per edge per lane);
+// U edges in flight. Source id of edge e: src[e * src_stride] (the
+// gather-folded parent position, the local id, or the vertex id).
+template <int LPD, int U>
+__global__ void __launch_bounds__(256) k_agg_f64(const uint64_t* __restrict__ offsets, const uint32_t* __restrict__ src,
+                                                uint32_t src_stride, const double* __restrict__ w,
+                                                const uint32_t* __restrict__ order, uint64_t n_items, uint32_t chunks,
+                                                const double* __restrict__ in, uint64_t ld_in,
+                                                double* __restrict__ out, uint64_t ld_out, uint32_t dim,
+                                                int accumulate) {
+    const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    const uint64_t item = t / LPD;
+    if (item >= n_items) return;
+    const uint64_t nd = n_items / chunks;
+    const uint32_t d = __ldg(order + item % nd);
+    const uint32_t ci = static_cast<uint32_t>(item / nd);  // chunk-major
+    const uint32_t col = (ci * LPD + static_cast<uint32_t>(t % LPD)) * 2;
+    const bool active = col < dim;
+    const bool pair = col + 1 < dim;
+    uint64_t e = __ldg(offsets + d);
+    const uint64_t end = __ldg(offsets + d + 1);
+    const double* icol = in + (active ? col : 0u);
+    double* orow = out + d * ld_out + col;
+    double a0 = 0.0, a1 = 0.0;
+    if (accumulate && active) {
+        a0 = orow[0];
+        if (pair) a1 = orow[1];
+    }
+    for (; e + U <= end; e += U) {
+        uint32_t sr[U];
+        double ww[U];
+        double2 x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            sr[u] = __ldg(src + (e + u) * src_stride);
+            ww[u] = __ldg(w + e + u);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) x[u] = __ldg(reinterpret_cast<const double2*>(icol + sr[u] * ld_in));
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            a0 = __dadd_rn(a0, __dmul_rn(ww[u], x[u].x));
+            a1 = __dadd_rn(a1, __dmul_rn(ww[u], x[u].y));
+        }
+    }
+    for (; e < end; ++e) {
+        const uint32_t s0 = __ldg(src + e * src_stride);
+        const double w0 = __ldg(w + e);
+        const double2 x = __ldg(reinterpret_cast<const double2*>(icol + s0 * ld_in));
+        a0 = __dadd_rn(a0, __dmul_rn(w0, x.x));
+        a1 = __dadd_rn(a1, __dmul_rn(w0, x.y));
+    }
+    if (!active) return;
+    orow[0] = __dadd_rn(a0, 0.0);
+    if (pair) orow[1] = __dadd_rn(a1, 0.0);
+}
+
 struct SideStream {
     cudaStream_t s = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
@@ -1792,6 +1855,34 @@ void aggregate_groups_af(Groups& G, const uint64_t* offsets_dev, uint32_t D, con
     else if (lpd == 16) launch_grp<16>(G, *sc, edges, chunks, in, ld_in, out, ld_out, dim32, accumulate, s);
     else if (lpd == 8) launch_grp<8>(G, *sc, edges, chunks, in, ld_in, out, ld_out, dim32, accumulate, s);
     else launch_grp<4>(G, *sc, edges, chunks, in, ld_in, out, ld_out, dim32, accumulate, s);
+}
+
+void aggregate_f64(const uint64_t* offsets, const uint32_t* src, uint32_t src_stride, const double* w,
+                   const uint32_t* order, uint32_t D, const double* in, uint64_t ld_in, double* out, uint64_t ld_out,
+                   uint64_t dim, bool accumulate, cudaStream_t s) {
+    if (D == 0 || dim == 0) return;
+    if (ld_in % 2 || ld_out % 2 || reinterpret_cast<uintptr_t>(in) % 16 || reinterpret_cast<uintptr_t>(out) % 16)
+        fail(kConfig, "aggregate_pull<double>: rows must be 16-byte aligned (even ld, aligned base)");
+    const uint32_t np = static_cast<uint32_t>((dim + 1) / 2);  // double2 per row
+    const int lpd = np > 16 ? 32 : np > 8 ? 16 : np > 4 ? 8 : 4;
+    const uint32_t chunks = (np + lpd - 1) / lpd;
+    const uint64_t items = static_cast<uint64_t>(D) * chunks;
+    const unsigned grid = grid_for(items * lpd, 256);
+    const int acc = accumulate ? 1 : 0;
+    const uint32_t d32 = static_cast<uint32_t>(dim);
+    if (lpd == 32)
+        k_agg_f64<32, 8><<<grid, 256, 0, s>>>(offsets, src, src_stride, w, order, items, chunks, in, ld_in, out, ld_out,
+                                              d32, acc);
+    else if (lpd == 16)
+        k_agg_f64<16, 8><<<grid, 256, 0, s>>>(offsets, src, src_stride, w, order, items, chunks, in, ld_in, out, ld_out,
+                                              d32, acc);
+    else if (lpd == 8)
+        k_agg_f64<8, 8><<<grid, 256, 0, s>>>(offsets, src, src_stride, w, order, items, chunks, in, ld_in, out, ld_out,
+                                             d32, acc);
+    else
+        k_agg_f64<4, 8><<<grid, 256, 0, s>>>(offsets, src, src_stride, w, order, items, chunks, in, ld_in, out, ld_out,
+                                             d32, acc);
+    PG_LAUNCH("k_agg_f64");
 }
 
 void relu_backward(const float* grad, uint64_t ldg, const float* pre, uint64_t ldp, float* out, uint64_t ldo,

@@ -1359,6 +1359,97 @@ int pg_backward_aggregate_rows(pg_groups h, uint32_t row_begin, uint32_t row_end
     });
 }
 
+// ---- aggregate_pull<double> (the reference's default precision) ----
+namespace {
+// the f64 SpMM over a grouping's base: parent-indexed (the engine.hpp:334
+// gather folded in) or local / vertex-indexed sources
+void run_aggregate_f64(Groups& G, bool parent_indexed, const double* in, uint64_t ld_in, double* out, uint64_t ld_out,
+                       uint64_t dim, unsigned flags, cudaStream_t s) {
+    DeviceGuard dg(G.device);
+    std::lock_guard<std::recursive_mutex> lk(G.mu);
+    const bool accumulate = !(flags & PG_AGG_OVERWRITE);
+    if (G.path) {
+        Path& p = *G.path;
+        const uint32_t* src = parent_indexed ? reinterpret_cast<const uint32_t*>(p.edges_parent.get())
+                                             : p.nbr_local.get();
+        aggregate_f64(p.offsets.get(), src, parent_indexed ? 2u : 1u, p.w64.get(), p.order.get(), p.D, in, ld_in, out,
+                      ld_out, dim, accumulate, s);
+        return;
+    }
+    Graph& g = *G.graph;
+    if (!G.graph_order.get() && g.n)
+        degree_order(g.offsets.get(), g.n, G.graph_order, lib_stream(g.device), &G.graph_hist);
+    aggregate_f64(g.offsets.get(), g.nbrs.get(), 1u, g.w64.get(), G.graph_order.get(), g.n, in, ld_in, out, ld_out,
+                  dim, accumulate, s);
+}
+
+// host DenseMatrix<double> drop-in: copy in (pitched to even ld), run, copy out
+void run_host_f64(Groups& G, bool parent_indexed, const double* in_host, uint64_t in_rows, uint64_t dim,
+                  double* out_host, uint64_t out_rows, unsigned flags) {
+    DeviceGuard dg(G.device);
+    cudaStream_t s = lib_stream(G.device);
+    const uint64_t ld = (dim + 1) & ~1ull;
+    DevBuf<double> din(in_rows * ld, s), dout(out_rows * ld, s);
+    if (in_rows && dim)
+        PG_CUDA(cudaMemcpy2DAsync(din.get(), ld * 8, in_host, dim * 8, dim * 8, in_rows, cudaMemcpyHostToDevice, s));
+    if (!(flags & PG_AGG_OVERWRITE) && out_rows && dim)
+        PG_CUDA(cudaMemcpy2DAsync(dout.get(), ld * 8, out_host, dim * 8, dim * 8, out_rows, cudaMemcpyHostToDevice, s));
+    run_aggregate_f64(G, parent_indexed, din.get(), ld, dout.get(), ld, dim, flags, s);
+    if (out_rows && dim)
+        PG_CUDA(cudaMemcpy2DAsync(out_host, dim * 8, dout.get(), ld * 8, dim * 8, out_rows, cudaMemcpyDeviceToHost, s));
+    PG_CUDA(cudaStreamSynchronize(s));
+}
+}  // namespace
+
+int pg_aggregate_pull_f64(pg_groups h, const double* in_dev, uint64_t in_rows, uint64_t ld_in, double* out_dev,
+                          uint64_t ld_out, uint64_t dim, unsigned flags, void* stream) {
+    return guard([&] {
+        Groups& G = *R_(h);
+        check_dims(dim, ld_in, ld_out);
+        if (in_rows != base_of(G).in_rows_local)
+            fail_shape("aggregate_pull: input rows != source count of the grouping's base");
+        if (flags & PG_AGG_GROUPED) fail(kConfig, "aggregate_pull<double>: the grouped Fast kernel is fp32 only");
+        run_aggregate_f64(G, false, in_dev, ld_in, out_dev, ld_out, dim, flags, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int pg_backward_aggregate_f64(pg_groups h, const double* y_dev, uint64_t y_rows, uint64_t ld_in, double* x_dev,
+                              uint64_t ld_out, uint64_t dim, unsigned flags, void* stream) {
+    return guard([&] {
+        Groups& G = *R_(h);
+        check_dims(dim, ld_in, ld_out);
+        if (!G.path) fail(kConfig, "backward_aggregate: grouping is not over an execution path");
+        if (y_rows != G.path->P) fail_shape("backward_aggregate: y_grad rows != parent frontier size");
+        if (flags & PG_AGG_GROUPED) fail(kConfig, "aggregate_pull<double>: the grouped Fast kernel is fp32 only");
+        run_aggregate_f64(G, true, y_dev, ld_in, x_dev, ld_out, dim, flags, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int pg_aggregate_pull_host_f64(pg_groups h, const double* in_host, uint64_t in_rows, uint64_t dim, double* out_host,
+                               unsigned flags, uint64_t* counters) {
+    return guard([&] {
+        Groups& G = *R_(h);
+        const Base b = base_of(G);
+        if (in_rows != b.in_rows_local)
+            fail_shape("aggregate_pull: input rows != source count of the grouping's base");
+        if (flags & PG_AGG_GROUPED) fail(kConfig, "aggregate_pull<double>: the grouped Fast kernel is fp32 only");
+        run_host_f64(G, false, in_host, in_rows, dim, out_host, b.D, flags);
+        counters_of(G, dim, flags, counters);
+    });
+}
+
+int pg_backward_aggregate_host_f64(pg_groups h, const double* y_host, uint64_t y_rows, uint64_t dim, double* x_host,
+                                   unsigned flags, uint64_t* counters) {
+    return guard([&] {
+        Groups& G = *R_(h);
+        if (!G.path) fail(kConfig, "backward_aggregate: grouping is not over an execution path");
+        if (y_rows != G.path->P) fail_shape("backward_aggregate: y_grad rows != parent frontier size");
+        if (flags & PG_AGG_GROUPED) fail(kConfig, "aggregate_pull<double>: the grouped Fast kernel is fp32 only");
+        run_host_f64(G, true, y_host, y_rows, dim, x_host, G.path->D, flags);
+        counters_of(G, dim, flags, counters);
+    });
+}
+
 int pg_aggregate_pull_host(pg_groups h, const float* in_host, uint64_t in_rows, uint64_t dim, float* out_host,
                            unsigned flags, uint64_t* counters) {
     return guard([&] {

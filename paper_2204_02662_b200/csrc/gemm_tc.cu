@@ -351,12 +351,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_gemm_abt_tc(const __grid_cons
 // writes its partial; k_atb_reduce adds the CTA partials in CTA order
 // (deterministic run to run, re-associated vs the reference's serial chain:
 // fp32 tolerance, not bit-exact).
-// Operands are MN-major (a row of Y / g is contiguous along M / N), in the
-// 128B-swizzled MN-major canonical layout: per 8-row K group, 1024-byte atoms
-// of 32 MN elements x 8 rows (16-byte chunk c of row k at chunk c ^ (k & 7)),
-// atoms along MN at LBO = 1024 B, K groups at SBO. Producers (8 warps) gather
-// the rows with coalesced 128-bit loads (one prefetched K tile ahead), split
-// hi/lo in registers and store both straight into the swizzled slots.
+// Operands are MN-major (a row of Y / g is contiguous along M / N). For
+// 32-bit (tf32) MN-major operands tcgen05 takes the SWIZZLE_128B_BASE32B
+// layout (descriptor layout type 1; CUTLASS Layout_MN_SW128_32B_Atom): atoms
+// of 4 K rows x 32 MN elements (512 B), the 32-byte granule g of row k at
+// g ^ (k & 3), atoms along MN at LBO = 512 B, 4-row K groups at SBO. (The
+// 8-row SWIZZLE_128B MN-major form reads as zeros for tf32 — measured,
+// tools/probes/umma_mn_probe.cu.) Producers (8 warps) gather the rows with
+// coalesced 128-bit loads (one prefetched K tile ahead), split hi/lo in
+// registers and store both straight into the swizzled slots.
 constexpr int kAtbProducers = 8;
 constexpr int kAtbThreads = 32 * (2 + kAtbProducers);  // MMA/TMEM warp, epilogue-lead, producers
 constexpr int kAtbKT = 16;  // rows per K tile (two 8-row K groups)
@@ -364,10 +367,10 @@ constexpr int kAtbKT = 16;  // rows per K tile (two 8-row K groups)
 __device__ __forceinline__ uint64_t sw128_mn_desc(uint32_t saddr, uint32_t sbo) {
     uint64_t d = 0;
     d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
-    d |= static_cast<uint64_t>(1024 >> 4) << 16;  // LBO: next 32-element MN atom
-    d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;  // SBO: next 8-row K group
+    d |= static_cast<uint64_t>(512 >> 4) << 16;             // LBO: next 32-element MN atom
+    d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;  // SBO: next 4-row K group
     d |= static_cast<uint64_t>(1) << 46;
-    d |= static_cast<uint64_t>(2) << 61;
+    d |= static_cast<uint64_t>(1) << 61;                    // SWIZZLE_128B_BASE32B
     return d;
 }
 // kind::tf32, D f32, A and B MN-major (bits 15, 16)
@@ -397,7 +400,7 @@ __global__ void __launch_bounds__(kAtbThreads, 1) k_gemm_atb_tc(AtbParams P) {
     const uint32_t Np = P.Npad, S = P.stages;
     const uint32_t bbytes = Np * kAtbKT * 4u;
     const uint32_t stage_bytes = 2u * MT * kAtile + 2u * bbytes;
-    const uint32_t sbo_a = 4u * 1024u, sbo_b = (Np / 32u) * 1024u;
+    const uint32_t sbo_a = 4u * 512u, sbo_b = (Np / 32u) * 512u;  // K-group strides
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
     uint64_t* full = bars;
     uint64_t* empty = bars + S;
@@ -438,12 +441,12 @@ __global__ void __launch_bounds__(kAtbThreads, 1) k_gemm_atb_tc(AtbParams P) {
                 for (int mt = 0; mt < MT; ++mt) {
                     const uint32_t d = tmem + mt * Np;
 #pragma unroll
-                    for (int g = 0; g < kAtbKT / 8; ++g) {
+                    for (int g = 0; g < kAtbKT / 8; ++g) {  // K = 8 per MMA: two 4-row K groups
                         const uint32_t acc0 = (t | g) ? 1u : 0u;
-                        const uint64_t ah = sw128_mn_desc(a_hi + mt * kAtile + g * sbo_a, sbo_a);
-                        const uint64_t al = sw128_mn_desc(a_lo + mt * kAtile + g * sbo_a, sbo_a);
-                        const uint64_t bh = sw128_mn_desc(b_hi + g * sbo_b, sbo_b);
-                        const uint64_t bl = sw128_mn_desc(b_lo + g * sbo_b, sbo_b);
+                        const uint64_t ah = sw128_mn_desc(a_hi + mt * kAtile + 2 * g * sbo_a, sbo_a);
+                        const uint64_t al = sw128_mn_desc(a_lo + mt * kAtile + 2 * g * sbo_a, sbo_a);
+                        const uint64_t bh = sw128_mn_desc(b_hi + 2 * g * sbo_b, sbo_b);
+                        const uint64_t bl = sw128_mn_desc(b_lo + 2 * g * sbo_b, sbo_b);
                         mma_tf32(d, ah, bh, idesc, acc0);
                         mma_tf32(d, ah, bl, idesc, 1u);
                         mma_tf32(d, al, bh, idesc, 1u);
@@ -521,18 +524,21 @@ __global__ void __launch_bounds__(kAtbThreads, 1) k_gemm_atb_tc(AtbParams P) {
             const uint32_t a_hi = st, a_lo = st + MT * kAtile, b_hi = st + 2 * MT * kAtile, b_lo = b_hi + bbytes;
 #pragma unroll
             for (int i = 0; i < RPW; ++i) {
-                const uint32_t k = pw * RPW + i, g = k >> 3, kr = k & 7;
+                // float4 q of a row (MN elements 4q..4q+3): atom q / 8, 32-byte
+                // granule ((q % 8) / 2) ^ (k % 4), half q % 2
+                const uint32_t k = pw * RPW + i, g = k >> 2, kr = k & 3;
 #pragma unroll
                 for (int mt = 0; mt < MT; ++mt) {
-                    const uint32_t off = mt * kAtile + g * sbo_a + (lane >> 3) * 1024u + kr * 128u +
-                                         (((lane & 7u) ^ kr) << 4);
+                    const uint32_t off = mt * kAtile + g * sbo_a + (lane >> 3) * 512u + kr * 128u +
+                                         ((((lane & 7u) >> 1) ^ kr) << 5) + ((lane & 1u) << 4);
                     put(a_hi + off, a_lo + off, ra[cb][i][mt]);
                 }
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const uint32_t q = lane + 32 * h;
                     if (q < nq) {
-                        const uint32_t off = g * sbo_b + (q >> 3) * 1024u + kr * 128u + (((q & 7u) ^ kr) << 4);
+                        const uint32_t off = g * sbo_b + (q >> 3) * 512u + kr * 128u + ((((q & 7u) >> 1) ^ kr) << 5) +
+                                             ((q & 1u) << 4);
                         put(b_hi + off, b_lo + off, rb[cb][i][h]);
                     }
                 }
@@ -551,6 +557,7 @@ __global__ void __launch_bounds__(kAtbThreads, 1) k_gemm_atb_tc(AtbParams P) {
     // MMA warp joins after issuing; warps 2-3 after producing
     if (warp < 4) {
         mbar_wait(done, 0);
+        __syncwarp();  // warp 0's issuing lane rejoins: tcgen05.ld is .sync.aligned
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         float* part = P.part + static_cast<uint64_t>(blockIdx.x) * P.in_dim * P.out_dim;
         for (int mt = 0; mt < MT; ++mt) {
@@ -709,6 +716,7 @@ void gemm_a_bt_tc(DMat a, DMat b, DMat out, cudaStream_t s) {
     p.vec_out = (out.ld % 4 == 0 && reinterpret_cast<uintptr_t>(out.p) % 16 == 0) ? 1 : 0;
     int dev = 0, sms = 148;
     PG_CUDA(cudaGetDevice(&dev));
+    (void)lib_stream(dev);  // the stream-ordered pool keeps freed temporaries (no re-map per call)
     PG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const uint64_t tiles = p.row_tiles * NT;
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(tiles, static_cast<uint64_t>(sms)));
@@ -744,6 +752,7 @@ void gemm_at_b_tc(DMat a, const uint32_t* a_rows, DMat b, DMat out, cudaStream_t
     const size_t smem = 1024 + S * stage + (2 * S + 2) * 8 + 16;
     int dev = 0, sms = 148;
     PG_CUDA(cudaGetDevice(&dev));
+    (void)lib_stream(dev);  // the stream-ordered pool keeps freed temporaries (no re-map per call)
     PG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const uint64_t tiles = (n + kAtbKT - 1) / kAtbKT;
     const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(tiles, static_cast<uint64_t>(sms)));

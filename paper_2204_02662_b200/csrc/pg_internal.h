@@ -267,6 +267,12 @@ void aggregate_groups(const uint64_t* gbeg, const uint64_t* gend, const uint32_t
                       uint32_t D, uint64_t G, const Edge* edges, const float* in, uint64_t ld_in, float* out,
                       uint64_t ld_out, uint64_t dim, bool accumulate, cudaStream_t s);
 
+// aggregate.hpp:56-122 with T = double (Deterministic order, f64 weights):
+// source of edge e = src[e * src_stride]; destinations in `order`.
+void aggregate_f64(const uint64_t* offsets, const uint32_t* src, uint32_t src_stride, const double* w,
+                   const uint32_t* order, uint32_t D, const double* in, uint64_t ld_in, double* out, uint64_t ld_out,
+                   uint64_t dim, bool accumulate, cudaStream_t s);
+
 // record a failure as the calling thread's pg_last_error / _kind (api.cu)
 void record_error(const Error& e);
 

@@ -507,11 +507,12 @@ def _flags(mode, overwrite=False):
     return f
 
 
-def _dev(t, name, rows=None, cols=None):
+def _dev(t, name, rows=None, cols=None, dtype=None):
     import torch
 
-    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float32:
-        raise ShapeError(f"{name}: expected a float32 CUDA tensor")
+    dtype = dtype or torch.float32
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != dtype:
+        raise ShapeError(f"{name}: expected a {str(dtype).replace('torch.', '')} CUDA tensor")
     if t.dim() != 2 or t.stride(1) != 1:
         raise ShapeError(f"{name}: expected a row-major 2-D tensor")
     if rows is not None and t.shape[0] != rows:
@@ -538,6 +539,12 @@ def aggregate_pull(grouped: GroupedCsr, inp, out, mode=DETERMINISTIC, counters=N
     Input rows are the base's local source ids.
     """
     flags = _flags(mode, overwrite)
+    if _is_f64(inp):  # aggregate_pull<double>, the reference's default precision
+        _pull_f64(grouped, inp, out, flags, stream, backward=False)
+        if counters is not None:
+            for k, v in grouped.counters(inp.shape[1], mode).items():
+                counters[k] = counters.get(k, 0) + v
+        return out
     if isinstance(inp, np.ndarray):
         if inp.dtype != np.float32 or out.dtype != np.float32:
             raise ShapeError("aggregate_pull: float32 matrices expected")
@@ -565,6 +572,39 @@ def aggregate_pull(grouped: GroupedCsr, inp, out, mode=DETERMINISTIC, counters=N
     return out
 
 
+def _is_f64(a):
+    if isinstance(a, np.ndarray):
+        return a.dtype == np.float64
+    import torch
+
+    return isinstance(a, torch.Tensor) and a.dtype == torch.float64
+
+
+def _pull_f64(grouped, inp, out, flags, stream, backward):
+    """aggregate.hpp:56-122 with T = double: numpy (host DenseMatrix<double>
+    drop-in, synchronous) or float64 CUDA tensors (rows with an even pitch)."""
+    import torch
+
+    base = grouped.base
+    rows_in = (base.P if backward else (base.S if isinstance(base, ExecutionPath) else base.n))
+    if isinstance(inp, np.ndarray):
+        x = np.ascontiguousarray(inp, np.float64)
+        if x.shape[0] != rows_in:
+            raise ShapeError("aggregate_pull: input rows != source count of the grouping's base")
+        if out.shape != (grouped.D, x.shape[1]) or out.dtype != np.float64 or not out.flags.c_contiguous:
+            raise ShapeError("aggregate_pull: output must be a C-contiguous float64 D x dim array")
+        fn = _lib_().pg_backward_aggregate_host_f64 if backward else _lib_().pg_aggregate_pull_host_f64
+        c = np.zeros(3, np.uint64)
+        _check(fn(grouped._h, _p(x, f64p), x.shape[0], x.shape[1], _p(out, f64p), flags, _p(c, u64p)))
+        return out
+    _dev(inp, "input", rows=rows_in, dtype=torch.float64)
+    _dev(out, "output", rows=grouped.D, cols=inp.shape[1], dtype=torch.float64)
+    fn = _lib_().pg_backward_aggregate_f64 if backward else _lib_().pg_aggregate_pull_f64
+    _check(fn(grouped._h, C.c_void_p(inp.data_ptr()), inp.shape[0], inp.stride(0), C.c_void_p(out.data_ptr()),
+              out.stride(0), inp.shape[1], flags, _stream(stream)))
+    return out
+
+
 def backward_aggregation(grouped: GroupedCsr, y_grad, x_grad, mode=DETERMINISTIC, overwrite=False, stream=None,
                          rows=None, segment=None):
     """The reference's timed stage engine.hpp:331-338 (gather_rows over
@@ -575,6 +615,10 @@ def backward_aggregation(grouped: GroupedCsr, y_grad, x_grad, mode=DETERMINISTIC
     if not isinstance(path, ExecutionPath):
         raise ConfigError("backward_aggregation: grouping is not over an execution path")
     flags = _flags(mode, overwrite)
+    if _is_f64(y_grad):  # aggregate_pull<double>, the reference's default precision
+        if rows is not None or segment is not None:
+            raise ConfigError("backward_aggregation<double>: whole paths only")
+        return _pull_f64(grouped, y_grad, x_grad, flags, stream, backward=True)
     if isinstance(y_grad, np.ndarray):
         y = np.ascontiguousarray(y_grad, np.float32)
         if x_grad.shape != (path.D, y.shape[1]) or x_grad.dtype != np.float32:
