@@ -175,6 +175,7 @@ struct DenseMatrix {                              // dense_matrix.hpp:14-30 (row
     DenseMatrix(std::size_t r, std::size_t c) : rows(r), cols(c), data(r * c, T(0)) {}
 };
 using MatrixF = DenseMatrix<float>;
+using MatrixD = DenseMatrix<double>;               // Precision::F64, the reference's default (run_config.hpp:53)
 
 // Host copy of an ExecutionPath (execution_path.hpp:16-33 field names).
 struct ExecutionPathHost {
@@ -494,6 +495,38 @@ inline void backward_aggregation(const DeviceGroups& grouped, const MatrixF& y_g
     check(pg_backward_aggregate_host(grouped.raw(), y_grad.data.data(), y_grad.rows, y_grad.cols,
                                      x_grad.data.data(),
                                      commit_flags(mode == CommitMode::Grouped ? CommitMode::Fast : mode), c));
+    if (counters) {
+        counters->edges_traversed += c[0];
+        counters->groups_executed += c[1];
+        counters->atomic_commits += c[2];
+    }
+}
+
+// aggregate_pull<double> / the timed stage in the reference's default
+// precision (Deterministic order, f64 weights; bit-exact with the f64 build)
+inline void aggregate_pull(const DeviceGroups& grouped, const MatrixD& input, MatrixD& output,
+                           CommitMode mode = CommitMode::Deterministic, int workers = 0,
+                           StageCounters* counters = nullptr) {
+    (void)workers;
+    if (output.rows != grouped.dest_count()) throw ShapeError("aggregate_pull: output rows != dest count");
+    if (output.cols != input.cols) throw ShapeError("aggregate_pull: input/output dims differ");
+    std::uint64_t c[3] = {0, 0, 0};
+    check(pg_aggregate_pull_host_f64(grouped.raw(), input.data.data(), input.rows, input.cols, output.data.data(),
+                                     commit_flags(mode == CommitMode::Grouped ? CommitMode::Fast : mode), c));
+    if (counters) {
+        counters->edges_traversed += c[0];
+        counters->groups_executed += c[1];
+        counters->atomic_commits += c[2];
+    }
+}
+inline void backward_aggregation(const DeviceGroups& grouped, const MatrixD& y_grad, MatrixD& x_grad,
+                                 CommitMode mode = CommitMode::Deterministic, StageCounters* counters = nullptr) {
+    if (x_grad.rows != grouped.dest_count() || x_grad.cols != y_grad.cols)
+        throw ShapeError("backward_aggregation: x_grad shape mismatch");
+    std::uint64_t c[3] = {0, 0, 0};
+    check(pg_backward_aggregate_host_f64(grouped.raw(), y_grad.data.data(), y_grad.rows, y_grad.cols,
+                                         x_grad.data.data(),
+                                         commit_flags(mode == CommitMode::Grouped ? CommitMode::Fast : mode), c));
     if (counters) {
         counters->edges_traversed += c[0];
         counters->groups_executed += c[1];

@@ -245,6 +245,16 @@ int main() {
         }
         report("missing file -> IoError", io);
     }
+    // aggregate_pull<double> (the reference's default precision): the hand
+    // case of test_engine.cpp:72-80 on gex, x = [1..5] -> [2, 13, 6, 10, 6]
+    {
+        DeviceGroups gr = group_neighbors(g, 2);
+        MatrixD x(5, 1), out(5, 1);
+        for (int i = 0; i < 5; ++i) x.data[i] = i + 1;
+        aggregate_pull(gr, x, out);
+        report("aggregate_pull<double> hand case",
+               out.data == std::vector<double>{2, 13, 6, 10, 6});
+    }
     // the library communicator, one rank (NCCL through the C ABI): the
     // sharded stage equals the single-GPU stage bit for bit
     {

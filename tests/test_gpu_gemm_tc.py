@@ -164,10 +164,10 @@ def test_tc_gemm_at_b_ungathered_and_empty(pg):
 
     got, exact, mag = _atb_case(pg, 3000, 3000, 50, 20, seed=9, gathered=False)
     _gate(got, exact, mag)
-    a = pg.empty_rows(5, 8)
+    a = pg.empty_rows(0, 8)
     b = pg.empty_rows(0, 4)
     o = pg.empty_rows(8, 4)
     o.fill_(1.0)
-    pg.gemm_at_b(a, b, o, a_rows=torch.zeros(0, dtype=torch.int32, device="cuda"), tensor_cores=True)
+    pg.gemm_at_b(a, b, o, tensor_cores=True)  # no rows: W' = 0
     torch.cuda.synchronize()
     assert (o.cpu().numpy() == 0).all()
