@@ -817,6 +817,18 @@ def measure_chain(pg, torch, g, prep, cfg, vt, dev, reps=5):
     out["backward_edges_per_layer"] = {"epp": c_epp["backward_edges_per_layer"],
                                        "all_active": c_all["backward_edges_per_layer"],
                                        "ifelse": c_if["backward_edges_per_layer"]}
+    # the same backward_epp with the dense products on the tensor cores
+    # (tuning gemm_tc: y_grad = g W^T and W' = gather(Y)^T g as tcgen05
+    # 3xTF32 — fp32 tolerance instead of bits); W' against the exact chain
+    exact = [w.double() for w in pg.backward_epp(prep, arts, top, ws)]
+    pg.set_tuning("gemm_tc", 1)
+    try:
+        out["backward_epp_tensor_core_ms"] = timed(lambda: pg.backward_epp(prep, arts, top, ws))
+        tcw = [w.double() for w in pg.backward_epp(prep, arts, top, ws)]
+    finally:
+        pg.set_tuning("gemm_tc", None)
+    out["tensor_core_w_grad_normwise_rel_err"] = [
+        float((a - b).norm() / max(float(b.norm()), 1e-300)) for a, b in zip(tcw, exact)]
     out["epp_speedup_vs_all_active"] = round(out["backward_all_active_ms"] / out["backward_epp_ms"], 3)
     out["epp_speedup_vs_ifelse"] = round(out["backward_ifelse_ms"] / out["backward_epp_ms"], 3)
     out["note"] = "whole chains incl. W' and y_grad products; random-init weights, U(0,1) features"
