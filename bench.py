@@ -620,6 +620,8 @@ def main():
         line["train_sweep"] = train_sweep(pg, torch, g, cfg, dims, dev)
     if not args.profile and world == 1 and (args.gs_sweep or args.config == "arxiv"):
         line["gs_sweep"] = gs_sweep(pg, prep, dims)
+    if not args.profile and world == 1:
+        line["grouped_fast"] = grouped_fast(pg, torch, prep, y_full, x_out, dims)
     if not args.profile and not args.no_chain and world == 1:
         line["chain"] = measure_chain(pg, torch, g, prep, cfg, vt, dev)
     elif not args.profile and not args.no_chain:
@@ -760,6 +762,39 @@ def gs_sweep(pg, prep, dims, repeats=5):
                     "deterministic_ms": round(det_ms, 4)})
         log(f"[gs_sweep] path {i} dim {dims[i]}: best {best} regression {reg} cost {cost_best} "
             f"det {det_ms:.3f} ms table {[(gs, round(t * 1e3, 3)) for gs, t in table]}")
+    return out
+
+
+def grouped_fast(pg, torch, prep, y_full, x_out, dims, reps=7):
+    """The group-partitioned Fast stage (PG_AGG_GROUPED: the atomic-free
+    k_agg_grp at the paths' regression gs, aggregate.hpp:84-115) beside the
+    Deterministic one on the same inputs: per-path ms (median of reps) and
+    the max deviation from the Deterministic x_grad relative to sum|w y|-free
+    max |x| (Fast re-associates a destination's groups)."""
+    out = []
+    for i, p in enumerate(prep.paths):
+        y = y_full[i][:, : dims[i]]
+        xd = x_out[i]
+        xg = pg.empty_rows(p.D, dims[i])
+
+        def t(fn):
+            fn()
+            torch.cuda.synchronize()
+            ts = []
+            for _ in range(reps):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                fn()
+                b.record()
+                torch.cuda.synchronize()
+                ts.append(a.elapsed_time(b))
+            return statistics.median(ts)
+
+        det = t(lambda: pg.backward_aggregation(prep.groups[i], y, xd, overwrite=True))
+        grp = t(lambda: pg.backward_aggregation(prep.groups[i], y, xg, mode=pg.GROUPED, overwrite=True))
+        dev = float((xg - xd).abs().max() / xd.abs().max().clamp_min(1e-30))
+        out.append({"path": i, "gs": prep.gs[i], "deterministic_ms": round(det, 4), "grouped_fast_ms": round(grp, 4),
+                    "max_rel_dev_vs_deterministic": dev})
     return out
 
 
