@@ -378,9 +378,9 @@ int pg_gemm(pg_mat a, pg_mat b, int b_transposed, pg_mat out, void* stream);
 int pg_gemm_at_b(pg_mat a, const uint32_t* a_rows, pg_mat b, pg_mat out, void* stream);
 /* the same with flags: PG_GEMM_TF32X3 = on the tensor cores, split-K over the
  * rows (CTA partials added in a fixed order, deterministic), 3xTF32 products:
- * within the fp32 tolerance of the exact W', NOT bit-exact. Needs
- * a.cols <= 640 and b.cols <= 256. Tuning "gemm_tc" = 1 routes the chains'
- * W' and y_grad GEMMs here. */
+ * within the fp32 tolerance of the exact W', NOT bit-exact. a and b need
+ * 16-byte aligned rows (ld % 4 == 0). Tuning "gemm_tc" = 1 routes the
+ * chains' W' and y_grad GEMMs here (when aligned). */
 int pg_gemm_at_b_ex(pg_mat a, const uint32_t* a_rows, pg_mat b, pg_mat out, unsigned flags, void* stream);
 /* dense_matrix.hpp:98-104 relu and :116-135 row_softmax (expf bit-exact
  * with glibc 2.39 on FMA x86-64) */

@@ -657,7 +657,8 @@ void gemm_at_b(DMat a, const uint32_t* a_rows, DMat b, DMat out, cudaStream_t s)
     if (r == 0 || c == 0) return;
     if (n >= (1ull << 31) || r >= (1ull << 31) || c >= (1ull << 31)) fail(kConfig, "gemm_at_b: dimension too large");
     // W' on the tensor cores when selected (split-K 3xTF32: tolerance, not bits)
-    if (tuning(kTuneGemmTc) == 1 && gemm_at_b_tc_supported(r, c)) {
+    if (tuning(kTuneGemmTc) == 1 && gemm_at_b_tc_supported(r, c) && a.ld % 4 == 0 && b.ld % 4 == 0 &&
+        reinterpret_cast<uintptr_t>(a.p) % 16 == 0 && reinterpret_cast<uintptr_t>(b.p) % 16 == 0) {
         gemm_at_b_tc(a, a_rows, b, out, s);
         return;
     }

@@ -727,47 +727,36 @@ void gemm_a_bt_tc(DMat a, DMat b, DMat out, cudaStream_t s) {
 }
 
 bool gemm_at_b_tc_supported(uint64_t in_dim, uint64_t out_dim) {
-    const uint64_t Np = (out_dim + 31) / 32 * 32;
-    const uint64_t MT = (in_dim + 127) / 128;
-    return in_dim > 0 && out_dim > 0 && Np <= 256 && MT >= 1 && MT <= 5 && MT * Np <= 512;
+    // any shape: blocks of <= 640 x 256 outputs per launch (gemm_at_b_tc)
+    return in_dim > 0 && out_dim > 0 && in_dim < (1ull << 31) && out_dim < (1ull << 31);
 }
 
-void gemm_at_b_tc(DMat a, const uint32_t* a_rows, DMat b, DMat out, cudaStream_t s) {
-    const uint64_t n = b.rows, in_dim = a.cols, out_dim = b.cols;
-    if (!a_rows && a.rows != n) fail_shape("gemm_at_b: row counts differ");
-    if (out.rows != in_dim || out.cols != out_dim) fail_shape("gemm_at_b: output shape mismatch");
-    if (in_dim == 0 || out_dim == 0) return;
-    if (!gemm_at_b_tc_supported(in_dim, out_dim))
-        fail(kConfig, "gemm_at_b (tensor cores): needs in_dim <= 640, out_dim <= 256 and in/128 x out/32 <= 16 tiles");
-    if (n == 0) {
-        PG_CUDA(cudaMemset2DAsync(out.p, out.ld * 4, 0, out_dim * 4, in_dim, s));
-        return;
-    }
-    const uint32_t Np = static_cast<uint32_t>((out_dim + 31) / 32 * 32);
-    const int MT = static_cast<int>((in_dim + 127) / 128);
+// one launch over output block [i0, i0 + bi) x [j0, j0 + bj) (bi <= 640,
+// MT x Npad <= 512 TMEM columns): sub-views of the same pitched matrices
+void gemm_at_b_tc_block(DMat a, const uint32_t* a_rows, DMat b, DMat out, uint64_t i0, uint64_t bi, uint64_t j0,
+                        uint64_t bj, int sms, cudaStream_t s) {
+    const uint64_t n = b.rows;
+    const uint32_t Np = static_cast<uint32_t>((bj + 31) / 32 * 32);
+    const int MT = static_cast<int>((bi + 127) / 128);
     const size_t stage = 2ull * MT * 128 * kAtbKT * 4 + 2ull * Np * kAtbKT * 4;
     const size_t budget = 232448 - 1024 - 256;
     const uint32_t S = static_cast<uint32_t>(std::min<size_t>(6, budget / stage));
     if (S < 2) fail(kConfig, "gemm_at_b (tensor cores): tile does not fit shared memory");
     const size_t smem = 1024 + S * stage + (2 * S + 2) * 8 + 16;
-    int dev = 0, sms = 148;
-    PG_CUDA(cudaGetDevice(&dev));
-    (void)lib_stream(dev);  // the stream-ordered pool keeps freed temporaries (no re-map per call)
-    PG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const uint64_t tiles = (n + kAtbKT - 1) / kAtbKT;
     const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(tiles, static_cast<uint64_t>(sms)));
     const uint64_t per = (tiles + grid - 1) / grid * kAtbKT;
     const uint32_t nparts = static_cast<uint32_t>((n + per - 1) / per);
-    DevBuf<float> part(static_cast<uint64_t>(nparts) * in_dim * out_dim, s);
+    DevBuf<float> part(static_cast<uint64_t>(nparts) * bi * bj, s);
     AtbParams p{};
-    p.a = a.p;
+    p.a = a.p + i0;
     p.lda = a.ld;
     p.a_rows = a_rows;
-    p.b = b.p;
+    p.b = b.p + j0;
     p.ldb = b.ld;
     p.n = n;
-    p.in_dim = static_cast<uint32_t>(in_dim);
-    p.out_dim = static_cast<uint32_t>(out_dim);
+    p.in_dim = static_cast<uint32_t>(bi);
+    p.out_dim = static_cast<uint32_t>(bj);
     p.Npad = Np;
     p.stages = S;
     p.rows_per_cta = per;
@@ -779,9 +768,36 @@ void gemm_at_b_tc(DMat a, const uint32_t* a_rows, DMat b, DMat out, cudaStream_t
         case 4: launch_atb<4>(p, smem, nparts, s); break;
         default: launch_atb<5>(p, smem, nparts, s); break;
     }
-    const uint64_t tot = in_dim * out_dim;
-    k_atb_reduce<<<grid_for(tot, 256), 256, 0, s>>>(part.get(), nparts, p.in_dim, p.out_dim, out.p, out.ld);
+    const uint64_t tot = bi * bj;
+    k_atb_reduce<<<grid_for(tot, 256), 256, 0, s>>>(part.get(), nparts, p.in_dim, p.out_dim, out.p + i0 * out.ld + j0,
+                                                 out.ld);
     PG_LAUNCH("k_atb_reduce");
+}
+
+void gemm_at_b_tc(DMat a, const uint32_t* a_rows, DMat b, DMat out, cudaStream_t s) {
+    const uint64_t n = b.rows, in_dim = a.cols, out_dim = b.cols;
+    if (!a_rows && a.rows != n) fail_shape("gemm_at_b: row counts differ");
+    if (out.rows != in_dim || out.cols != out_dim) fail_shape("gemm_at_b: output shape mismatch");
+    if (in_dim == 0 || out_dim == 0) return;
+    if (a.ld % 4 || b.ld % 4 || reinterpret_cast<uintptr_t>(a.p) % 16 || reinterpret_cast<uintptr_t>(b.p) % 16)
+        fail(kConfig, "gemm_at_b (tensor cores): Y and g need 16-byte aligned rows (ld % 4 == 0)");
+    if (n == 0) {
+        PG_CUDA(cudaMemset2DAsync(out.p, out.ld * 4, 0, out_dim * 4, in_dim, s));
+        return;
+    }
+    int dev = 0, sms = 148;
+    PG_CUDA(cudaGetDevice(&dev));
+    (void)lib_stream(dev);  // the stream-ordered pool keeps freed temporaries (no re-map per call)
+    PG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    // output blocks: up to 5 M tiles (640 rows) x as many 32-column groups as
+    // the 512 TMEM columns allow (<= 256)
+    for (uint64_t i0 = 0; i0 < in_dim; i0 += 640) {
+        const uint64_t bi = std::min<uint64_t>(640, in_dim - i0);
+        const uint64_t MT = (bi + 127) / 128;
+        const uint64_t nmax = std::min<uint64_t>(256, 512 / MT / 32 * 32);
+        for (uint64_t j0 = 0; j0 < out_dim; j0 += nmax)
+            gemm_at_b_tc_block(a, a_rows, b, out, i0, bi, j0, std::min<uint64_t>(nmax, out_dim - j0), sms, s);
+    }
 }
 
 }  // namespace pg

@@ -347,7 +347,8 @@ bool gemm_a_bt_tc_supported(DMat a);
 void gemm_a_bt_tc(DMat a, DMat b, DMat out, cudaStream_t s);
 // dense_matrix.hpp:57-76 W' = gather_rows(a, a_rows)^T b on the tensor cores
 // (split-K over the rows, 3xTF32, CTA partials added in fixed order):
-// fp32 tolerance, NOT bit-exact. supported(): in_dim <= 640, out_dim <= 256.
+// fp32 tolerance, NOT bit-exact. Any shape (blocks of <= 640 x 256 outputs
+// per launch); Y and g need 16-byte aligned rows.
 bool gemm_at_b_tc_supported(uint64_t in_dim, uint64_t out_dim);
 void gemm_at_b_tc(DMat a, const uint32_t* a_rows, DMat b, DMat out, cudaStream_t s);
 // dense_matrix.hpp:57-76: out = a[a_rows]^T * b (a_rows nullable: all rows)

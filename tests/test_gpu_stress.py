@@ -278,3 +278,79 @@ def test_concurrent_calls_share_one_grouping(pg, orc):
     for t in ts:
         t.join()
     assert not errors, errors
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("PG_STRESS_SEEDS_TOL", "24"))))
+def test_random_tolerance_paths(pg, orc, seed):
+    """Randomised sweep of the tolerance-level kernels: the atomic-free grouped
+    Fast stage (random gs, widths, training fractions; deterministic run to
+    run, within the conditioning-aware fp32 bound of f64, bit-equal to
+    Deterministic when gs >= max degree), the f64 stage (bit-exact vs the
+    f64 oracle) and the tensor-core GEMMs (random shapes, gathered or not)."""
+    import torch
+
+    rng = np.random.default_rng(7000 + seed)
+    n = int(rng.integers(300, 8000))
+    pairs, n_pad = rmat_pairs(orc, n, n * int(rng.choice([4, 16, 48])), 900 + seed)
+    vt = orc.sample_training_set(n_pad, float(rng.choice([0.05, 0.3, 1.0])), seed)
+    dg = pg.build_undirected_csr(pairs, n_hint=n_pad, weights="symnorm")
+    og = orc.build_graph(pairs, n_hint=n_pad, symnorm=True)
+    ops = orc.prepare_all_paths(og, orc.compute_frontiers(og, vt, 2))
+    dps = pg.prepare_all_paths(dg, pg.compute_frontiers(dg, vt, 2))
+    for dp, op in zip(dps, ops):
+        dim = int(rng.choice(WIDTHS))
+        gs = int(rng.choice([1, 2, 5, 17, 64, 300, max(dp.max_degree, 1)]))
+        G = pg.group_neighbors(dp, gs)
+        y = rng.uniform(-1, 1, size=(dp.P, dim)).astype(np.float32)
+        yu = y[op.srcpos]
+        want64 = orc.aggregate_pull_f64(op.offsets, op.neighbors, op.weights, yu.astype(np.float64))
+        absum = orc.aggregate_pull_f64(op.offsets, op.neighbors, np.abs(op.weights), np.abs(yu).astype(np.float64))
+        yd = pg.empty_rows(dp.P, dim)
+        yd.copy_(torch.from_numpy(y))
+        runs = []
+        for _ in range(2):
+            x = pg.empty_rows(dp.D, dim)
+            x.fill_(float("nan"))
+            pg.backward_aggregation(G, yd, x, mode=pg.GROUPED, overwrite=True)
+            torch.cuda.synchronize()
+            runs.append(x.cpu().numpy())
+        assert np.array_equal(bits(runs[0]), bits(runs[1])), (seed, gs, dim)
+        assert (np.abs(runs[0] - want64) <= 1e-6 + 1e-5 * absum).all(), (seed, gs, dim)
+        if gs >= dp.max_degree:
+            det = orc.aggregate_pull_f32(op.offsets, op.neighbors, op.weights, yu)
+            assert np.array_equal(bits(runs[0]), bits(det)), (seed, "one group per destination")
+        # f64 stage, bit-exact
+        x64 = np.zeros((dp.D, dim))
+        pg.backward_aggregation(G, y.astype(np.float64), x64, overwrite=True)
+        assert np.array_equal(x64.view(np.uint64), want64.view(np.uint64)), (seed, dim, "f64")
+    # tensor-core GEMMs on random shapes
+    for _ in range(2):
+        nr, k, m = int(rng.integers(1, 5000)), int(rng.integers(1, 300)), int(rng.integers(1, 700))
+        a = rng.uniform(-1, 1, size=(nr, k)).astype(np.float32)
+        b = rng.uniform(-1, 1, size=(m, k)).astype(np.float32)
+        ad = pg.empty_rows(nr, k)
+        ad.copy_(torch.from_numpy(a))
+        bd = torch.from_numpy(b).cuda()
+        od = pg.empty_rows(nr, m)
+        pg.gemm_a_bt(ad, bd, od, tensor_cores=True)
+        ind, outd = int(rng.integers(1, 641)), int(rng.integers(1, 257))
+        ry = int(rng.integers(1, 4000))
+        rows = rng.integers(0, ry, size=int(rng.integers(0, 4000))).astype(np.int32)
+        yy = rng.uniform(-1, 1, size=(ry, ind)).astype(np.float32)
+        gg = rng.uniform(-1, 1, size=(len(rows), outd)).astype(np.float32)
+        yyd = pg.empty_rows(ry, ind)
+        yyd.copy_(torch.from_numpy(yy))
+        ggd = pg.empty_rows(len(rows), outd)
+        ggd.copy_(torch.from_numpy(gg))
+        wd = pg.empty_rows(ind, outd)
+        if len(rows):
+            pg.gemm_at_b(yyd, ggd, wd, a_rows=torch.from_numpy(rows).cuda(), tensor_cores=True)
+        torch.cuda.synchronize()
+        got, exact = od.cpu().numpy().astype(np.float64), a.astype(np.float64) @ b.astype(np.float64).T
+        mag = np.abs(a).astype(np.float64) @ np.abs(b).astype(np.float64).T
+        assert (np.abs(got - exact) <= 1e-6 + 1e-5 * mag).all(), (seed, nr, k, m)
+        if len(rows):
+            ya = yy[rows].astype(np.float64)
+            got, exact = wd.cpu().numpy().astype(np.float64), ya.T @ gg.astype(np.float64)
+            mag = np.abs(ya).T @ np.abs(gg).astype(np.float64)
+            assert (np.abs(got - exact) <= 1e-6 + 1e-5 * mag).all(), (seed, ind, outd, len(rows))
