@@ -245,12 +245,33 @@ void pg::run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re,
         if (sel.seg < 0 && parent_indexed && !G.edges_remap.get() && !edges_override) {
             const uint32_t K = auto_src_segments(p.P, p.D, p.E, dim);
             if (K > 1) {
-                if (G.auto_seg_k != K) {
+                // cuts: equal source rows (tuning src_seg_balance 0, default) or
+                // rows weighted by edge count (100): a percentage mix
+                const int64_t bal = std::clamp<int64_t>(tuning(kTuneSrcSegBalance), 0, 100);
+                if (G.auto_seg_k != K || G.auto_seg_bal != bal) {
                     std::vector<uint64_t> cuts(K + 1);
                     for (uint32_t k = 0; k <= K; ++k) cuts[k] = static_cast<uint64_t>(p.P) * k / K;
+                    if (bal > 0) {
+                        cudaStream_t ls = lib_stream(p.device);
+                        DevBuf<uint32_t> cnt(p.P, ls);
+                        source_edge_counts(p.edges_parent.get(), p.E, p.P, cnt.get(), ls);
+                        std::vector<uint32_t> hc(p.P);
+                        PG_CUDA(cudaMemcpyAsync(hc.data(), cnt.get(), p.P * 4ull, cudaMemcpyDeviceToHost, ls));
+                        PG_CUDA(cudaStreamSynchronize(ls));
+                        const double tot = static_cast<double>(p.E) * bal / 100.0 +
+                                           static_cast<double>(p.P) * (100 - bal) / 100.0;
+                        double acc = 0;
+                        uint32_t k = 1;
+                        for (uint64_t r = 0; r < p.P && k < K; ++r) {
+                            acc += hc[r] * (bal / 100.0) + (100 - bal) / 100.0;
+                            while (k < K && acc >= tot * k / K) cuts[k++] = r + 1;
+                        }
+                        for (uint32_t j = 1; j <= K; ++j) cuts[j] = std::max(cuts[j], cuts[j - 1]);
+                    }
                     segment_bounds(p.offsets.get(), p.edges_parent.get(), p.D, cuts.data(), K, G.auto_seg_bnd,
                                    lib_stream(p.device));
                     G.auto_seg_k = K;
+                    G.auto_seg_bal = bal;
                 }
                 for (uint32_t k = 0; k < K; ++k) {
                     AggExt ek = ext;

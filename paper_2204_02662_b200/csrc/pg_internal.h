@@ -154,6 +154,7 @@ struct Groups {
     // automatic L2-sized source segments of a whole-path SpMM (api.cu)
     DevBuf<uint64_t> auto_seg_bnd;
     uint32_t auto_seg_k = 0;
+    int64_t auto_seg_bal = 0;
     // schedule of the atomic-free group-partitioned Fast kernel (aggregate.cu
     // k_agg_grp), one per worker count (256 / lanes per group): CTA ranges of
     // consecutive groups that hold whole destinations, each hub destination
@@ -312,7 +313,8 @@ enum TuneKeyId {
     kTuneHostLastSegPct = 21,
     kTuneWgradFork = 22,
     kTuneGemmTc = 23,
-    kTuneRecWindow = 24
+    kTuneRecWindow = 24,
+    kTuneSrcSegBalance = 25
 };
 
 int64_t tuning(int key);

@@ -22,6 +22,7 @@ KNOBS = {
     "heavy_wide_pipe": (0, 1),
     "wide_lpd": (16, 32),
     "src_segs": (0, 1, 2, 3),
+    "src_seg_balance": (0, 50, 100),
     "heavy_tma": (0, 1),
     "rec_window": (0, 1),
 }
