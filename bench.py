@@ -411,6 +411,9 @@ def main():
     if one_dev and xmode == "lib":
         xmode = "p2p"
     comm = pgd.Comm.from_process_group(local) if world > 1 and xmode == "lib" else None
+    if comm is None and world == 1 and os.environ.get("PG_BENCH_FORCE_COMM") == "1":
+        # rehearsal of the N>1 library path on one GPU: a one-rank communicator
+        comm = pgd.Comm(local, 1, 0, pgd.Comm.unique_id())
     padded = xmode == "padded"
     y_shard, y_full, x_out, rows = [], [], [], []
     for i, p in enumerate(paths):
