@@ -13,7 +13,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CHUNKS = 32
-CONFIGS = ("reddit", "products", "arxiv")
+CONFIGS = ("reddit", "products", "arxiv", "pubmed", "cora")
 
 
 def digest_path(config):

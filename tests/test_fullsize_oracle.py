@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.join(HERE, "golden"))
 import fullsize as fs  # noqa: E402
 
-CFGS = ["arxiv"] + (["products", "reddit"] if os.environ.get("PG_FULLSIZE_ORACLE") == "all" else [])
+CFGS = ["cora", "pubmed", "arxiv"] + (["products", "reddit"] if os.environ.get("PG_FULLSIZE_ORACLE") == "all" else [])
 
 
 @pytest.mark.parametrize("config", CFGS)
