@@ -42,7 +42,7 @@ constexpr TuneKey kTuneKeys[] = {
     {"heavy_narrow", "PG_HEAVY_NARROW", 0},  // heavy rows <= 64 floats: 1 = k_agg_narrow_lat, 0 = coop tiles
     {"wide_lpd", "PG_WIDE_LPD", 32},       // wide rows: lanes per (destination, chunk) item, 32 or 16
     {"src_segs", "PG_SRC_SEGS", 0},        // whole-path SpMM source segments: 0 = auto (L2-sized), K = forced
-    {"ld_cg", "PG_LD_CG", 0},              // row gathers: 0/1 = ld.global.nc (L1), 2 = ld.global.cg (L2 only)
+    {"ld_cg", "PG_LD_CG", 0},              // row gathers: 0/1 nc, 2 cg, 3 nc.L1::no_allocate, 4 plain, 5 nc.L1::evict_last, 6 records no_allocate
     {"host_chunk_order", "PG_HOST_CHUNK_ORDER", 1},  // host drop-in last pass: 1 = last row chunk first
     {"grouped_seg", "PG_GROUPED_SEG", 0},  // grouped Fast: 0 = atomic-free k_agg_grp, 1 = CTA-segmented + atomics at CTA edges, 2 = an atomic per extra group
     {"heavy_wide_pipe", "PG_HEAVY_WIDE_PIPE", 1},  // heavy wide rows: 1 = software-pipelined k_agg_wide_pipe
@@ -171,23 +171,40 @@ __device__ __forceinline__ void acc_store(float* orow, uint32_t col, uint32_t di
 
 // 128-bit read-only row gather at base + src * ld_bytes: one IMAD.WIDE.U32
 // per edge (the 32x32->64 multiply-add cannot overflow for ld_bytes < 2^32).
-// CG = true: ld.global.cg (L2 only, no L1 allocation) — for gathers whose
-// L1 reuse does not pay for the L1/TEX wavefront cost
-template <bool CG = false>
+// LDM (tuning "ld_cg") selects the load flavour of the row gathers:
+//   0/1 ld.global.nc (read-only path, L1 allocating; default)
+//   2   ld.global.cg (L2 only)
+//   3   ld.global.nc.L1::no_allocate
+//   4   ld.global (plain)
+//   5   ld.global.nc.L1::evict_last
+// (the records, streamed once, use L1::no_allocate when LDM == 6; rows nc)
+template <int LDM = 0>
 __device__ __forceinline__ float4 ld_row(const char* base, uint32_t src, uint32_t ld_bytes) {
-    if constexpr (CG) {
-        float4 r;
-        const char* p = base + static_cast<uint64_t>(src) * ld_bytes;
-        asm volatile("ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];"
-                     : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
-                     : "l"(p));
-        return r;
-    }
     float4 r;
     const char* p = base + static_cast<uint64_t>(src) * ld_bytes;
-    asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];"
-                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
-                 : "l"(p));
+    if constexpr (LDM == 2)
+        asm volatile("ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+    else if constexpr (LDM == 3)
+        asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                     : "l"(p));
+    else if constexpr (LDM == 4)
+        asm volatile("ld.global.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+    else if constexpr (LDM == 5)
+        asm volatile("ld.global.nc.L1::evict_last.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                     : "l"(p));
+    else
+        asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+    return r;
+}
+template <int LDM = 0>
+__device__ __forceinline__ Edge ld_rec_m(const Edge* p) {
+    Edge r;
+    if constexpr (LDM == 6)
+        asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+    else
+        asm volatile("ld.global.nc.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
     return r;
 }
 __device__ __forceinline__ Edge ld_rec(const Edge* p) {
@@ -256,7 +273,7 @@ __device__ __forceinline__ void acc_store_ext(float* orow, uint32_t col, uint32_
 // of U edges: U edge-record loads, U row gathers (all in flight), then the
 // U ordered accumulate steps. Lanes past dim gather column 0 (in bounds,
 // discarded) so no load is predicated.
-template <int LPD, int U, bool FILT, bool CG = false, bool RW = false>
+template <int LPD, int U, bool FILT, int CG = 0, bool RW = false>
 __global__ void __launch_bounds__(256, (U <= 8 ? 4 : 2)) k_agg_vec4(const uint64_t* __restrict__ ebeg, const uint64_t* __restrict__ eend,
                                                  const Edge* __restrict__ edges,
                                                  const uint32_t* __restrict__ order, uint32_t d_begin,
@@ -324,7 +341,7 @@ __global__ void __launch_bounds__(256, (U <= 8 ? 4 : 2)) k_agg_vec4(const uint64
 #pragma unroll
             for (int i = 0; i < NPL; ++i) {
                 const unsigned k = sl + i * LPD;
-                mine[i] = ld_rec(edges + e + (k < n ? k : n - 1));
+                mine[i] = ld_rec_m<CG>(edges + e + (k < n ? k : n - 1));
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -333,7 +350,7 @@ __global__ void __launch_bounds__(256, (U <= 8 ? 4 : 2)) k_agg_vec4(const uint64
             }
         } else {
 #pragma unroll
-            for (int u = 0; u < U; ++u) ed[u] = ld_rec(edges + e + (u < static_cast<int>(n) ? u : n - 1));
+            for (int u = 0; u < U; ++u) ed[u] = ld_rec_m<CG>(edges + e + (u < static_cast<int>(n) ? u : n - 1));
         }
     };
     for (; e + U <= end; e += U) {
@@ -343,7 +360,7 @@ __global__ void __launch_bounds__(256, (U <= 8 ? 4 : 2)) k_agg_vec4(const uint64
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             if (FILT && !ext_src_on(ext, ed[u].x)) x[u] = make_float4(0.f, 0.f, 0.f, 0.f);  // skipped: +-0 term
-            else x[u] = ld_row<CG>(base, ed[u].x, ld_in_bytes);
+            else x[u] = ld_row<(CG == 6 ? 0 : CG)>(base, ed[u].x, ld_in_bytes);
         }
         const Zs zz = batch_dep<U>(x, z, zmask);
 #pragma unroll
@@ -357,7 +374,7 @@ __global__ void __launch_bounds__(256, (U <= 8 ? 4 : 2)) k_agg_vec4(const uint64
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             if (FILT && !ext_src_on(ext, ed[u].x)) x[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-            else x[u] = ld_row<CG>(base, ed[u].x, ld_in_bytes);
+            else x[u] = ld_row<(CG == 6 ? 0 : CG)>(base, ed[u].x, ld_in_bytes);
         }
         const Zs zz = batch_dep<U>(x, z, zmask);
 #pragma unroll
@@ -1659,25 +1676,35 @@ void launch_vec4(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges, 
                  uint32_t dim, bool accumulate, cudaStream_t s, const AggExt& ext) {
     const uint64_t items = static_cast<uint64_t>(nd) * chunks;
     const int cm = chunks > 1 && tuning(kTuneChunkMajor) ? 1 : 0;
-    // L2-only gathers measured no faster for narrow rows and slower for wide
-    // ones (layer 0 16.7 -> 17.1 ms), so only on request
-    const bool cg = tuning(kTuneLdCg) == 2;
+    // gather load flavour (tuning "ld_cg", see ld_row): measured on the
+    // Reddit layer-0 path, the default read-only L1-allocating load is best
+    const int ldm = static_cast<int>(tuning(kTuneLdCg));
+    const unsigned grid = grid_for(items * LPD, 256);
+    const uint32_t ldb = static_cast<uint32_t>(ld_in * 4);
     if (ext.src_bits || ext.dst_bits)
-        k_agg_vec4<LPD, U, true><<<grid_for(items * LPD, 256), 256, 0, s>>>(
-            ebeg, eend, edges, order, d_begin, items, chunks, in, static_cast<uint32_t>(ld_in * 4), out, ld_out, dim,
-            accumulate, kZeros, 0u, cm, ext);
-    else if (cg)
-        k_agg_vec4<LPD, U, false, true><<<grid_for(items * LPD, 256), 256, 0, s>>>(
-            ebeg, eend, edges, order, d_begin, items, chunks, in, static_cast<uint32_t>(ld_in * 4), out, ld_out, dim,
-            accumulate, kZeros, 0u, cm, ext);
+        k_agg_vec4<LPD, U, true><<<grid, 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks, in, ldb, out,
+                                                      ld_out, dim, accumulate, kZeros, 0u, cm, ext);
     else if (LPD >= 16 && tuning(kTuneRecWindow) == 1)
-        k_agg_vec4<LPD, U, false, false, true><<<grid_for(items * LPD, 256), 256, 0, s>>>(
-            ebeg, eend, edges, order, d_begin, items, chunks, in, static_cast<uint32_t>(ld_in * 4), out, ld_out, dim,
-            accumulate, kZeros, 0u, cm, ext);
+        k_agg_vec4<LPD, U, false, 0, true><<<grid, 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks, in,
+                                                                ldb, out, ld_out, dim, accumulate, kZeros, 0u, cm, ext);
+    else if (ldm == 2)
+        k_agg_vec4<LPD, U, false, 2><<<grid, 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks, in, ldb, out,
+                                                          ld_out, dim, accumulate, kZeros, 0u, cm, ext);
+    else if (ldm == 3)
+        k_agg_vec4<LPD, U, false, 3><<<grid, 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks, in, ldb, out,
+                                                          ld_out, dim, accumulate, kZeros, 0u, cm, ext);
+    else if (ldm == 4)
+        k_agg_vec4<LPD, U, false, 4><<<grid, 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks, in, ldb, out,
+                                                          ld_out, dim, accumulate, kZeros, 0u, cm, ext);
+    else if (ldm == 5)
+        k_agg_vec4<LPD, U, false, 5><<<grid, 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks, in, ldb, out,
+                                                          ld_out, dim, accumulate, kZeros, 0u, cm, ext);
+    else if (ldm == 6)
+        k_agg_vec4<LPD, U, false, 6><<<grid, 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks, in, ldb, out,
+                                                          ld_out, dim, accumulate, kZeros, 0u, cm, ext);
     else
-        k_agg_vec4<LPD, U, false><<<grid_for(items * LPD, 256), 256, 0, s>>>(
-            ebeg, eend, edges, order, d_begin, items, chunks, in, static_cast<uint32_t>(ld_in * 4), out, ld_out, dim,
-            accumulate, kZeros, 0u, cm, ext);
+        k_agg_vec4<LPD, U, false><<<grid, 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks, in, ldb, out,
+                                                       ld_out, dim, accumulate, kZeros, 0u, cm, ext);
     PG_LAUNCH("k_agg_vec4");
 }
 
