@@ -459,17 +459,28 @@ __global__ void __launch_bounds__(kAtbThreads, 1) k_gemm_atb_tc(AtbParams P) {
     } else if (warp >= 2) {  // producers: gather + split + swizzled store
         const uint32_t pw = warp - 2;
         constexpr int RPW = kAtbKT / kAtbProducers;  // rows per producer warp per K tile
-        const uint32_t nq = Np / 4;                   // float4 per B row (padded)
-        float4 ra[2][RPW][MT], rb[2][RPW][2];
-        // register double buffer indexed at compile time (a runtime index
-        // would put ra / rb in local memory)
+        // register ring of DEPTH K tiles in flight per producer warp (a
+        // runtime ring index would put it in local memory, so the loop below
+        // is unrolled by DEPTH); the gathered rows' ids are loaded one tile
+        // ahead of the rows, so no id -> row round trip is exposed
+        constexpr int DEPTH = MT <= 2 ? 4 : 2;
+        const uint32_t nq = Np / 4;  // float4 per B row (padded)
+        float4 ra[DEPTH][RPW][MT], rb[DEPTH][RPW][2];
+        uint64_t nid[RPW];  // Y row ids of the next tile to load
+        auto load_ids = [&](uint32_t t) {
+#pragma unroll
+            for (int i = 0; i < RPW; ++i) {
+                const uint64_t r = r0 + static_cast<uint64_t>(t) * kAtbKT + pw * RPW + i;
+                nid[i] = r < r1 ? (P.a_rows ? __ldg(P.a_rows + r) : r) : 0;
+            }
+        };
         auto load = [&](uint32_t t, auto bufc) {
             constexpr int buf = decltype(bufc)::value;
 #pragma unroll
             for (int i = 0; i < RPW; ++i) {
                 const uint64_t r = r0 + static_cast<uint64_t>(t) * kAtbKT + pw * RPW + i;
                 const bool ok = r < r1;
-                const uint64_t ar = ok ? (P.a_rows ? __ldg(P.a_rows + r) : r) : 0;
+                const uint64_t ar = nid[i];
 #pragma unroll
                 for (int mt = 0; mt < MT; ++mt) {
                     const uint32_t col = mt * 128 + lane * 4;
@@ -517,7 +528,10 @@ __global__ void __launch_bounds__(kAtbThreads, 1) k_gemm_atb_tc(AtbParams P) {
         };
         auto step = [&](uint32_t t, auto bufc) {
             constexpr int cb = decltype(bufc)::value;
-            if (t + 1 < ntiles) load(t + 1, std::integral_constant<int, cb ^ 1>{});  // next K tile in flight
+            if (t + DEPTH - 1 < ntiles) {  // keep DEPTH - 1 tiles in flight beyond this one
+                load(t + DEPTH - 1, std::integral_constant<int, (cb + DEPTH - 1) % DEPTH>{});
+                load_ids(t + DEPTH);
+            }
             const uint32_t s = t % S, ph = (t / S) & 1;
             mbar_wait(&empty[s], ph ^ 1);
             const uint32_t st = smem_addr(smem + s * stage_bytes);
@@ -547,10 +561,23 @@ __global__ void __launch_bounds__(kAtbThreads, 1) k_gemm_atb_tc(AtbParams P) {
             __syncwarp();
             if (lane == 0) mbar_arrive(&full[s]);
         };
-        if (ntiles) load(0, std::integral_constant<int, 0>{});
-        for (uint32_t t = 0; t < ntiles; t += 2) {
+        // prologue: tiles 0 .. DEPTH-2 in flight, the ids of tile DEPTH-1 loaded
+        load_ids(0);
+        if (0 < ntiles) load(0, std::integral_constant<int, 0>{});
+        load_ids(1);
+        if (DEPTH > 2) {
+            if (1 < ntiles) load(1, std::integral_constant<int, 1 % DEPTH>{});
+            load_ids(2);
+        }
+        if (DEPTH > 3) {
+            if (2 < ntiles) load(2, std::integral_constant<int, 2 % DEPTH>{});
+            load_ids(3);
+        }
+        for (uint32_t t = 0; t < ntiles; t += DEPTH) {
             step(t, std::integral_constant<int, 0>{});
-            if (t + 1 < ntiles) step(t + 1, std::integral_constant<int, 1>{});
+            if (t + 1 < ntiles) step(t + 1, std::integral_constant<int, 1 % DEPTH>{});
+            if (DEPTH > 2 && t + 2 < ntiles) step(t + 2, std::integral_constant<int, 2 % DEPTH>{});
+            if (DEPTH > 3 && t + 3 < ntiles) step(t + 3, std::integral_constant<int, 3 % DEPTH>{});
         }
     }
     // epilogue: warps 0-3 read TMEM lane quarters (warp w: lanes 32w..) — the
