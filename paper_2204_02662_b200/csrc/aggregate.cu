@@ -65,8 +65,10 @@ constexpr TuneKey kTuneKeys[] = {
     {"rec_window", "PG_REC_WINDOW", 0},
     // whole-path L2-sized source segments: cuts by rows (0) .. by edges (100)
     {"src_seg_balance", "PG_SRC_SEG_BALANCE", 0},
+    // host drop-in: output size (MB) from which the copy/compute pipeline is used
+    {"host_min_mb", "PG_HOST_MIN_MB", 32},
 };
-static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneSrcSegBalance + 1,
+static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneHostMinMb + 1,
               "kTuneKeys and enum TuneKeyId (pg_internal.h) must list the same keys in the same order");
 std::atomic<int64_t> g_tune[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];
 int64_t g_tune_def[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];  // $PG_<KEY> at load, else built-in

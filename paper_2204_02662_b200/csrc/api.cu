@@ -612,7 +612,10 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
     const uint64_t D = b.D;
     DevBuf<float> fin(packed ? 0 : in_rows * dim, s), din(in_rows * ld, s);
     DevBuf<float> fout(packed ? 0 : D * dim, s), dout(D * ld, s);
-    const bool big = G.path && D >= 16384 && dim * 4 * D >= (32ull << 20);
+    // pipelined (segments / chunks) above an output size floor (tuning
+    // host_min_mb, MB of output rows)
+    const uint64_t floor_mb = static_cast<uint64_t>(std::max<int64_t>(0, tuning(kTuneHostMinMb)));
+    const bool big = G.path && D >= 16384 && dim * 4 * D >= (floor_mb << 20);
     // source segments re-read and re-write the output once per extra pass:
     // only when gathers dominate (E >= 64 D), like the device-side rule
     const uint32_t K = (big && parent_indexed && in_rows >= 4 && b.E >= 64ull * D)

@@ -314,7 +314,8 @@ enum TuneKeyId {
     kTuneWgradFork = 22,
     kTuneGemmTc = 23,
     kTuneRecWindow = 24,
-    kTuneSrcSegBalance = 25
+    kTuneSrcSegBalance = 25,
+    kTuneHostMinMb = 26
 };
 
 int64_t tuning(int key);
