@@ -493,6 +493,8 @@ def main():
         sweep(pg, torch, step, paths, dims, stream)
     if args.tune_sweep:
         tune_sweep(pg, torch, step, L)
+    if os.environ.get("PG_BENCH_SWEEP"):
+        knob_sweep(pg, torch, step, L, x_out, dims, args.config, json.loads(os.environ["PG_BENCH_SWEEP"]))
     for _ in range(max(args.warmup, 1)):
         step()
     torch.cuda.synchronize()
@@ -933,6 +935,21 @@ def tune_sweep(pg, torch, step, L):
     pg.set_tuning("chunk_major")
 
 
+def knob_sweep(pg, torch, step, L, x_out, dims, config, settings):
+    """Diagnostics (stderr): per-path kernel ms for each tuning setting of
+    $PG_BENCH_SWEEP (a JSON list of {knob: value} dicts, applied on top of
+    the defaults), each with its x_grad checked against the reference digest."""
+    for st in settings:
+        for k, v in st.items():
+            pg.set_tuning(k, v)
+        ms = time_steps(torch, step, L, reps=20)
+        par = x_grad_parity(x_out, dims, config)
+        log(f"[sweep] {json.dumps(st)} per-path ms={[round(x, 3) for x in ms]} total={sum(ms):.3f} "
+            f"parity={par['all'] if par else None}")
+        for k in st:
+            pg.set_tuning(k)
+
+
 def sweep(pg, torch, step, paths, dims, stream):
     """Diagnostics (stderr): per-path kernel ms vs the heavy-kernel degree
     threshold, and raw pinned H2D/D2H copy bandwidth."""
@@ -1048,6 +1065,21 @@ def measure_e2e(pg, pgd, torch, dist, paths, groups, shards, dims, rows, world, 
         # VM boxes (host-side stalls, not the pipeline: the device phase
         # trace is flat); the median is reported, the mean kept beside it
         sec = statistics.median(per) / 1e3
+        if os.environ.get("PG_BENCH_E2E_SWEEP"):
+            # diagnostics (stderr): host-pipeline knob settings, each on top of the defaults
+            for st in json.loads(os.environ["PG_BENCH_E2E_SWEEP"]):
+                for k, v in st.items():
+                    pg.set_tuning(k, v)
+                one()
+                pp = []
+                for _ in range(steps):
+                    t1 = time.perf_counter()
+                    one()
+                    pp.append((time.perf_counter() - t1) * 1e3)
+                log(f"[e2e-sweep] {json.dumps(st)} median {statistics.median(pp):.3f} ms "
+                    f"min {min(pp):.3f} per-step {[round(x, 2) for x in pp]}")
+                for k in st:
+                    pg.set_tuning(k)
         stats = {"stat": f"median of {steps} steps", "mean_ms": round(statistics.mean(per), 3),
                  "min_ms": round(min(per), 3), "max_ms": round(max(per), 3)}
         # the same call with PAGEABLE buffers (a reference DenseMatrix is a

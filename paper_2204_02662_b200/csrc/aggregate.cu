@@ -45,16 +45,18 @@ constexpr TuneKey kTuneKeys[] = {
     {"ld_cg", "PG_LD_CG", 0},              // row gathers: 0/1 nc, 2 cg, 3 nc.L1::no_allocate, 4 plain, 5 nc.L1::evict_last, 6 records no_allocate
     {"host_chunk_order", "PG_HOST_CHUNK_ORDER", 1},  // host drop-in last pass: 1 = last row chunk first
     {"grouped_seg", "PG_GROUPED_SEG", 0},  // grouped Fast: 0 = atomic-free k_agg_grp, 1 = CTA-segmented + atomics at CTA edges, 2 = an atomic per extra group
-    {"heavy_wide_pipe", "PG_HEAVY_WIDE_PIPE", 1},  // heavy wide rows: 1 = software-pipelined k_agg_wide_pipe
+    // heavy wide rows: software-pipelined k_agg_wide_pipe with hub items
+    // destination-major (1) or chunk-major (2); 0 = k_agg_wide_lat
+    {"heavy_wide_pipe", "PG_HEAVY_WIDE_PIPE", 1},
     {"host_final_segs", "PG_HOST_FINAL_SEGS", 1},  // host drop-in: trailing source segments of the chunked last pass
     {"host_pitch2d", "PG_HOST_PITCH2D", 0},  // host drop-in: odd widths by 2-D DMA (1) or flat DMA + repack kernel (0)
     {"host_copy_prio", "PG_HOST_COPY_PRIO", 1},  // host drop-in: copy/repack streams at the highest priority (read once)
     {"host_seg_balance", "PG_HOST_SEG_BALANCE", 1},  // host drop-in: source segments of equal rows (0) or equal edges (1)
-    {"host_chunk_balance", "PG_HOST_CHUNK_BALANCE", 0},  // host drop-in: last-pass chunk cuts, % weight of edges vs rows
+    {"host_chunk_balance", "PG_HOST_CHUNK_BALANCE", 30},  // host drop-in: last-pass chunk cuts, % weight of edges vs rows
     {"atb_split", "PG_ATB_SPLIT", 1},  // W' GEMM: 1 = copy warp + chain warp, 0 = one warp does both
     {"atb_pairs", "PG_ATB_PAIRS", 224},  // W' split GEMM: 2 A columns per lane above this many 64-chain blocks (0 = never)
     {"gemm_packed", "PG_GEMM_PACKED", 1},  // gemm / gemm_a_bt: 1 = FFMA2/FADD2 column pairs (k_gemm2), 0 = k_gemm
-    {"host_last_seg_pct", "PG_HOST_LAST_SEG_PCT", 40},  // host drop-in: % of the edges in the last (chunked) segment, 0 = 1/K
+    {"host_last_seg_pct", "PG_HOST_LAST_SEG_PCT", 45},  // host drop-in: % of the edges in the last (chunked) segment, 0 = 1/K
     {"wgrad_fork", "PG_WGRAD_FORK", 1},  // backward chains: W' GEMMs on a forked stream (1) or in order (0)
     // chain y_grad = g W^T (gemm_a_bt): 0 = bit-exact FFMA2 kernel, 1 = tcgen05
     // 3xTF32 tensor-core kernel (fp32 tolerance, not bit-exact)
@@ -67,8 +69,15 @@ constexpr TuneKey kTuneKeys[] = {
     {"src_seg_balance", "PG_SRC_SEG_BALANCE", 0},
     // host drop-in: output size (MB) from which the copy/compute pipeline is used
     {"host_min_mb", "PG_HOST_MIN_MB", 32},
+    // rows of 129..768 floats: 1 = whole-row warps (k_agg_row), 0 = 128-column
+    // chunk items (k_agg_vec4)
+    {"row_kernel", "PG_ROW_KERNEL", 0},
+    {"row_u", "PG_ROW_U", 2},            // k_agg_row: edges per gather batch (2, 3, 4)
+    {"row_seg_mb", "PG_ROW_SEG_MB", 56},  // k_agg_row: per-pass source working set (MB) of the L2-sized segments
+    {"row_heavy", "PG_ROW_HEAVY", 0},    // k_agg_row: hub degree threshold (0 = the default rule)
+    {"vec_block", "PG_VEC_BLOCK", 256},  // k_agg_vec4 wide rows: threads per CTA (256, 512, 1024)
 };
-static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneHostMinMb + 1,
+static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneVecBlock + 1,
               "kTuneKeys and enum TuneKeyId (pg_internal.h) must list the same keys in the same order");
 std::atomic<int64_t> g_tune[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];
 int64_t g_tune_def[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];  // $PG_<KEY> at load, else built-in
@@ -81,6 +90,11 @@ void tune_init() {
     }
 }
 }  // namespace
+
+bool row_kernel_on(uint64_t dim) {
+    const uint64_t nq = (dim + 3) / 4;
+    return nq > 32 && nq <= 192 && tuning(kTuneRowKernel) != 0;
+}
 
 int64_t tuning(int key) {
     std::call_once(g_tune_once, tune_init);
@@ -179,7 +193,8 @@ __device__ __forceinline__ void acc_store(float* orow, uint32_t col, uint32_t di
 //   3   ld.global.nc.L1::no_allocate
 //   4   ld.global (plain)
 //   5   ld.global.nc.L1::evict_last
-// (the records, streamed once, use L1::no_allocate when LDM == 6; rows nc)
+// (the records, streamed once, use L1::no_allocate when LDM == 6 and an
+// L2 evict_first policy when LDM == 7; rows nc)
 template <int LDM = 0>
 __device__ __forceinline__ float4 ld_row(const char* base, uint32_t src, uint32_t ld_bytes) {
     float4 r;
@@ -205,7 +220,12 @@ __device__ __forceinline__ Edge ld_rec_m(const Edge* p) {
     Edge r;
     if constexpr (LDM == 6)
         asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
-    else
+    else if constexpr (LDM == 7) {
+        // streamed once per pass: first out of L2, so the gathered rows stay
+        uint64_t pol;
+        asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+        asm volatile("ld.global.nc.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;" : "=r"(r.x), "=r"(r.y) : "l"(p), "l"(pol));
+    } else
         asm volatile("ld.global.nc.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
     return r;
 }
@@ -275,8 +295,8 @@ __device__ __forceinline__ void acc_store_ext(float* orow, uint32_t col, uint32_
 // of U edges: U edge-record loads, U row gathers (all in flight), then the
 // U ordered accumulate steps. Lanes past dim gather column 0 (in bounds,
 // discarded) so no load is predicated.
-template <int LPD, int U, bool FILT, int CG = 0, bool RW = false>
-__global__ void __launch_bounds__(256, (U <= 8 ? 4 : 2)) k_agg_vec4(const uint64_t* __restrict__ ebeg, const uint64_t* __restrict__ eend,
+template <int LPD, int U, bool FILT, int CG = 0, bool RW = false, int BS = 256>
+__global__ void __launch_bounds__(BS, (BS == 256 ? (U <= 8 ? 4 : 2) : 1024 / BS)) k_agg_vec4(const uint64_t* __restrict__ ebeg, const uint64_t* __restrict__ eend,
                                                  const Edge* __restrict__ edges,
                                                  const uint32_t* __restrict__ order, uint32_t d_begin,
                                                  uint64_t n_items, uint32_t chunks,
@@ -362,7 +382,7 @@ __global__ void __launch_bounds__(256, (U <= 8 ? 4 : 2)) k_agg_vec4(const uint64
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             if (FILT && !ext_src_on(ext, ed[u].x)) x[u] = make_float4(0.f, 0.f, 0.f, 0.f);  // skipped: +-0 term
-            else x[u] = ld_row<(CG == 6 ? 0 : CG)>(base, ed[u].x, ld_in_bytes);
+            else x[u] = ld_row<(CG >= 6 ? 0 : CG)>(base, ed[u].x, ld_in_bytes);
         }
         const Zs zz = batch_dep<U>(x, z, zmask);
 #pragma unroll
@@ -376,7 +396,7 @@ __global__ void __launch_bounds__(256, (U <= 8 ? 4 : 2)) k_agg_vec4(const uint64
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             if (FILT && !ext_src_on(ext, ed[u].x)) x[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-            else x[u] = ld_row<(CG == 6 ? 0 : CG)>(base, ed[u].x, ld_in_bytes);
+            else x[u] = ld_row<(CG >= 6 ? 0 : CG)>(base, ed[u].x, ld_in_bytes);
         }
         const Zs zz = batch_dep<U>(x, z, zmask);
 #pragma unroll
@@ -384,6 +404,115 @@ __global__ void __launch_bounds__(256, (U <= 8 ? 4 : 2)) k_agg_vec4(const uint64
             if (u < static_cast<int>(n)) acc_step(acc, __uint_as_float(ed[u].y), x[u], zz);
     }
     acc_store_ext(orow, col, dim, acc, z, ext, d, row);
+}
+
+// Whole-row warps for wide rows (tuning "row_kernel"): one warp per
+// destination over the whole row, NS float4 slots per lane (slot j = float4
+// columns 32 j + lane). What bounds k_agg_vec4 on the Reddit layer-0 path is
+// the L1 -> register writeback (ncu l1tex__lsu_writeback_active 85 %,
+// data_pipe_lsu_wavefronts 87 %; the L2 -> L1 fill is at 49 %): it costs one
+// cycle per register written per lane, so a 128-column item pays 4 cycles of
+// row data plus 2 of broadcast edge record per edge — a third of the
+// writeback is records. Here one record serves the whole row: for 602
+// columns 5 x 4 + 2 = 22 cycles per edge instead of 5 x (4 + 2) = 30. The
+// per-pass source working set is the whole row, so the path runs as more
+// (L2-sized) source segments. Same fp32 order as k_agg_vec4 (per column,
+// ascending edge, separately rounded multiply and add): bit-identical.
+// Lanes past dim in the last slot re-read the slot's first float4 (same
+// sector, in bounds) and discard it.
+template <int NS, int U>
+__global__ void __launch_bounds__(256, 2) k_agg_row(const uint64_t* __restrict__ ebeg, const uint64_t* __restrict__ eend,
+                                                    const Edge* __restrict__ edges,
+                                                    const uint32_t* __restrict__ order, uint32_t d_begin,
+                                                    uint32_t nd, const float* __restrict__ in, uint32_t ld_in_bytes,
+                                                    float* __restrict__ out, uint64_t ld_out, uint32_t dim,
+                                                    int accumulate, float2 zeros, uint32_t zmask, AggExt ext) {
+    const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (w >= nd) return;
+    const uint32_t lane = lane_id();
+    const Zs z = zs_of(zeros);
+    const uint32_t d = __ldg(order + d_begin + w);
+    uint64_t e = __ldg(ebeg + d);
+    const uint64_t end = __ldg(eend + d);
+    const uint32_t nq = (dim + 3) / 4;
+    // slot j < NS - 1 sits at byte 512 j from the lane's slot-0 column; the
+    // last slot's lanes past dim fall back to the slot's first float4
+    const uint32_t qlast = (NS - 1) * 32 + lane;
+    const uint32_t off_last = (qlast < nq ? qlast : (NS - 1) * 32u) * 16u - lane * 16u;
+    const char* base = reinterpret_cast<const char*>(in) + lane * 16u;
+    asm("mov.b64 %0, %0;" : "+l"(base));
+    const uint32_t row = ext_out_row(ext, d);
+    float* orow = out + row * ld_out;
+    Acc acc[NS];
+#pragma unroll
+    for (int j = 0; j < NS; ++j) acc[j] = acc_load(orow + (j * 32 + lane) * 4, (j * 32 + lane) * 4, dim, accumulate);
+    auto gather = [&](const Edge (&ed)[U], float4 (&x)[U][NS]) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const char* p = base + static_cast<uint64_t>(ed[u].x) * ld_in_bytes;
+#pragma unroll
+            for (int j = 0; j < NS; ++j)
+                x[u][j] = ld_row<0>(p + (j + 1 < NS ? j * 512u : off_last), 0u, 0u);
+        }
+    };
+    auto fold = [&](const float4 (&x)[U][NS]) {
+        uint32_t all = 0;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int j = 0; j < NS; ++j) all ^= __float_as_uint(x[u][j].x);
+        all &= zmask;
+        Zs r = z;
+        r.nz ^= (static_cast<unsigned long long>(all) << 32) | all;
+        return r;
+    };
+    for (; e + U <= end; e += U) {
+        Edge ed[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) ed[u] = ld_rec(edges + e + u);
+        float4 x[U][NS];
+        gather(ed, x);
+        const Zs zz = fold(x);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int j = 0; j < NS; ++j) acc_step(acc[j], __uint_as_float(ed[u].y), x[u][j], zz);
+    }
+    if (e < end) {
+        const uint32_t n = static_cast<uint32_t>(end - e);
+        Edge ed[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) ed[u] = ld_rec(edges + e + (u < static_cast<int>(n) ? u : 0));
+        float4 x[U][NS];
+        gather(ed, x);
+        const Zs zz = fold(x);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (u < static_cast<int>(n))
+#pragma unroll
+                for (int j = 0; j < NS; ++j) acc_step(acc[j], __uint_as_float(ed[u].y), x[u][j], zz);
+    }
+#pragma unroll
+    for (int j = 0; j < NS; ++j)
+        acc_store_ext(orow + (j * 32 + lane) * 4, (j * 32 + lane) * 4, dim, acc[j], z, ext, d, row);
+}
+
+template <int NS>
+void launch_row_ns(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges, const uint32_t* order,
+                   uint32_t d_begin, uint32_t nd, const float* in, uint64_t ld_in, float* out, uint64_t ld_out,
+                   uint32_t dim, bool accumulate, cudaStream_t s, const AggExt& ext, int u) {
+    const unsigned grid = grid_for(static_cast<uint64_t>(nd) * 32, 256);
+    const uint32_t ldb = static_cast<uint32_t>(ld_in * 4);
+    if (u >= 4)
+        k_agg_row<NS, 4><<<grid, 256, 0, s>>>(ebeg, eend, edges, order, d_begin, nd, in, ldb, out, ld_out, dim,
+                                              accumulate, kZeros, 0u, ext);
+    else if (u == 3)
+        k_agg_row<NS, 3><<<grid, 256, 0, s>>>(ebeg, eend, edges, order, d_begin, nd, in, ldb, out, ld_out, dim,
+                                              accumulate, kZeros, 0u, ext);
+    else
+        k_agg_row<NS, 2><<<grid, 256, 0, s>>>(ebeg, eend, edges, order, d_begin, nd, in, ldb, out, ld_out, dim,
+                                              accumulate, kZeros, 0u, ext);
+    PG_LAUNCH("k_agg_row");
 }
 
 // ---- CommitMode::Fast, group partitioned (PG_AGG_GROUPED) ----------------
@@ -787,13 +916,17 @@ __global__ void __launch_bounds__(64) k_agg_wide_pipe(const uint64_t* __restrict
                                                      uint64_t n_items, uint32_t chunks,
                                                      const float* __restrict__ in, uint32_t ld_in_bytes,
                                                      float* __restrict__ out, uint64_t ld_out, uint32_t dim,
-                                                     int accumulate, uint32_t zmask, AggExt ext) {
+                                                     int accumulate, uint32_t zmask, AggExt ext, int chunk_major) {
     static_assert(32 % U == 0, "U divides the 32-record window");
     const uint64_t item = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
     if (item >= n_items) return;
     const unsigned lane = lane_id();
-    const uint32_t d = order[d_begin + item / chunks];
-    const uint32_t col = (static_cast<uint32_t>(item % chunks) * 32 + lane) * 4;
+    // chunk-major: every hub's chunk 0 first, like the concurrent main
+    // kernel, so both gather from the same column chunk of the segment
+    const uint64_t nhub = n_items / chunks;
+    const uint32_t d = order[d_begin + (chunk_major ? item % nhub : item / chunks)];
+    const uint32_t ci = static_cast<uint32_t>(chunk_major ? item / nhub : item % chunks);
+    const uint32_t col = (ci * 32 + lane) * 4;
     const bool active = col < dim;
     const uint64_t eb = ebeg[d], ee = eend[d];
     const uint32_t row = ext_out_row(ext, d);
@@ -1704,6 +1837,20 @@ void launch_vec4(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges, 
     else if (ldm == 6)
         k_agg_vec4<LPD, U, false, 6><<<grid, 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks, in, ldb, out,
                                                           ld_out, dim, accumulate, kZeros, 0u, cm, ext);
+    else if (ldm == 7)
+        k_agg_vec4<LPD, U, false, 7><<<grid, 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks, in, ldb, out,
+                                                          ld_out, dim, accumulate, kZeros, 0u, cm, ext);
+    else if (LPD == 32 && U == 8 && tuning(kTuneVecBlock) == 1024)
+        // 32 destinations of one column chunk per CTA, started together: the
+        // CTA's warps walk their (degree-sorted, similar) lists in step, so
+        // shared sources hit in L1
+        k_agg_vec4<LPD, U, false, 0, false, 1024><<<grid_for(items * LPD, 1024), 1024, 0, s>>>(
+            ebeg, eend, edges, order, d_begin, items, chunks, in, ldb, out, ld_out, dim, accumulate, kZeros, 0u, cm,
+            ext);
+    else if (LPD == 32 && U == 8 && tuning(kTuneVecBlock) == 512)
+        k_agg_vec4<LPD, U, false, 0, false, 512><<<grid_for(items * LPD, 512), 512, 0, s>>>(
+            ebeg, eend, edges, order, d_begin, items, chunks, in, ldb, out, ld_out, dim, accumulate, kZeros, 0u, cm,
+            ext);
     else
         k_agg_vec4<LPD, U, false><<<grid, 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks, in, ldb, out,
                                                        ld_out, dim, accumulate, kZeros, 0u, cm, ext);
@@ -1766,10 +1913,10 @@ void aggregate_det(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges
             // flight per lane, 5 column-chunk warps per 602-wide destination
             const uint32_t chunks = (nq + 31) / 32;
             const uint64_t items = static_cast<uint64_t>(nh) * chunks;
-            if (tuning(kTuneHeavyWidePipe) == 1) {
+            if (tuning(kTuneHeavyWidePipe) >= 1) {
                 k_agg_wide_pipe<16><<<grid_for(items * 32, 64), 64, 0, ss.s>>>(
                     ebeg, eend, edges, order, d_begin, items, chunks, in, static_cast<uint32_t>(ld_in * 4), out,
-                    ld_out, dim32, accumulate, 0u, ext);
+                    ld_out, dim32, accumulate, 0u, ext, tuning(kTuneHeavyWidePipe) == 2 ? 1 : 0);
                 PG_LAUNCH("k_agg_wide_pipe");
             } else {
                 k_agg_wide_lat<32><<<grid_for(items * 32, 256), 256, 0, ss.s>>>(
@@ -1813,6 +1960,17 @@ void aggregate_det(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges
         k_agg_scalar<8><<<grid_for(items * 32, 256), 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks,
                                                                  in, ld_in, out, ld_out, dim32, accumulate, ext);
         PG_LAUNCH("k_agg_scalar");
+        return;
+    }
+    if (nq > 16 && !filt && row_kernel_on(dim32)) {
+        const int u = static_cast<int>(tuning(kTuneRowU));
+        switch ((nq + 31) / 32) {
+            case 2: launch_row_ns<2>(ebeg, eend, edges, order, d_begin, nd, in, ld_in, out, ld_out, dim32, accumulate, s, ext, u); break;
+            case 3: launch_row_ns<3>(ebeg, eend, edges, order, d_begin, nd, in, ld_in, out, ld_out, dim32, accumulate, s, ext, u); break;
+            case 4: launch_row_ns<4>(ebeg, eend, edges, order, d_begin, nd, in, ld_in, out, ld_out, dim32, accumulate, s, ext, u); break;
+            case 5: launch_row_ns<5>(ebeg, eend, edges, order, d_begin, nd, in, ld_in, out, ld_out, dim32, accumulate, s, ext, u); break;
+            default: launch_row_ns<6>(ebeg, eend, edges, order, d_begin, nd, in, ld_in, out, ld_out, dim32, accumulate, s, ext, u); break;
+        }
         return;
     }
     if (nq > 16) {

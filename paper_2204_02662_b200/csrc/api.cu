@@ -1,6 +1,7 @@
 // C ABI of libpathgcn_b200.so (include/pathgcn_b200.h): status codes,
 // handle plumbing, host-side input synthesis with the reference's exact
 // libstdc++ random streams, and the host-buffer drop-ins.
+#include <chrono>
 #include <algorithm>
 #include <atomic>
 #include <cmath>
@@ -173,6 +174,13 @@ void check_dims(uint64_t dim, uint64_t ld_in, uint64_t ld_out) {
 // rule): two when one chunk-major pass would gather from more than ~80 MB
 // (P rows x 512 B) and at most ~400 MB; more passes cost an output
 // read+write each and lost in the measured sweep (K = 3, 4, 6).
+// hub threshold of a (segment) range: the row kernel's own knob, else the
+// measured default rule
+uint64_t heavy_degree(uint64_t dim, uint64_t range_edges) {
+    if (row_kernel_on(dim) && tuning(kTuneRowHeavy) > 0) return static_cast<uint64_t>(tuning(kTuneRowHeavy));
+    return heavy_min_degree(dim, range_edges);
+}
+
 uint32_t auto_src_segments(uint64_t P, uint64_t D, uint64_t E, uint64_t dim) {
     const int64_t forced = tuning(kTuneSrcSegs);
     if (forced > 0) return static_cast<uint32_t>(std::min<int64_t>(forced, 16));
@@ -181,6 +189,12 @@ uint32_t auto_src_segments(uint64_t P, uint64_t D, uint64_t E, uint64_t dim) {
     // when gathers dominate (measured: products' top path, E/D = 4, lost
     // 1.5 -> 2.8 ms with two passes)
     if (E < 64 * D) return 1;
+    if (row_kernel_on(dim)) {
+        // whole-row warps gather whole rows: segments of ~row_seg_mb MB
+        const uint64_t rowb = ((dim + 31) / 32) * 128;
+        const uint64_t tgt = static_cast<uint64_t>(std::max<int64_t>(8, tuning(kTuneRowSegMb))) << 20;
+        return static_cast<uint32_t>(std::min<uint64_t>(16, (P * rowb + tgt - 1) / tgt));
+    }
     const uint64_t w = P * 512;
     return (w > (80ull << 20) && w <= (400ull << 20)) ? 2 : 1;
 }
@@ -295,7 +309,7 @@ void pg::run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re,
         }
         if (rb == 0 && re == p.D) {
             aggregate_det(eb, ee, edges, p.order.get(), p.D, 0, p.D,
-                          p.hist.heavy(heavy_min_degree(dim, p.E / range_div)), in, ld_in, out, ld_out, dim,
+                          p.hist.heavy(heavy_degree(dim, p.E / range_div)), in, ld_in, out, ld_out, dim,
                           accumulate, s, ext);
             return;
         }
@@ -311,7 +325,7 @@ void pg::run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re,
             degree_order(p.offsets.get() + rb, re - rb, rs->order, lib_stream(p.device), &rs->hist);
         }
         aggregate_det(eb + rb, ee + rb, edges, rs->order.get(), re - rb, 0, re - rb,
-                      rs->hist.heavy(heavy_min_degree(dim, rs->hist.edges / range_div)), in, ld_in, out, ld_out, dim,
+                      rs->hist.heavy(heavy_degree(dim, rs->hist.edges / range_div)), in, ld_in, out, ld_out, dim,
                       accumulate, s, ext);
         return;
     }
@@ -338,19 +352,22 @@ void pg::run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re,
             if (k + 1 < K) ek.relu_pre = nullptr;  // the epilogue applies to finished rows only
             const uint64_t* eb = G.auto_seg_bnd.get() + static_cast<uint64_t>(k) * g.n;
             aggregate_det(eb, eb + g.n, g.edges.get(), G.graph_order.get(), g.n, 0, g.n,
-                          G.graph_hist.heavy(heavy_min_degree(dim, g.m / K)), in, ld_in, out, ld_out, dim,
+                          G.graph_hist.heavy(heavy_degree(dim, g.m / K)), in, ld_in, out, ld_out, dim,
                           accumulate || k > 0, s, ek);
         }
         return;
     }
     aggregate_det(g.offsets.get(), g.offsets.get() + 1, g.edges.get(), G.graph_order.get(), g.n, 0, g.n,
-                  G.graph_hist.heavy(heavy_min_degree(dim, g.m)), in, ld_in, out, ld_out, dim, accumulate, s, ext);
+                  G.graph_hist.heavy(heavy_degree(dim, g.m)), in, ld_in, out, ld_out, dim, accumulate, s, ext);
 }
 
 namespace {
 
 struct CopyStreams {
     cudaStream_t h2d = nullptr, d2h = nullptr;
+    // repack streams: the odd-width row repacks run beside the DMA streams,
+    // so a segment's / chunk's copy never queues behind the previous repack
+    cudaStream_t rup = nullptr, rdn = nullptr;
     std::vector<cudaEvent_t> ev;  // sync events
     std::vector<cudaEvent_t> tev;  // timing events (host_trace)
     std::mutex call;              // one host-buffer call at a time per device owns them
@@ -378,6 +395,8 @@ CopyStreams& copy_streams(int device, size_t nev, std::unique_lock<std::mutex>& 
         const int prio = tuning(kTuneHostCopyPrio) ? hi : 0;
         PG_CUDA(cudaStreamCreateWithPriority(&c.h2d, cudaStreamNonBlocking, prio));
         PG_CUDA(cudaStreamCreateWithPriority(&c.d2h, cudaStreamNonBlocking, prio));
+        PG_CUDA(cudaStreamCreateWithPriority(&c.rup, cudaStreamNonBlocking, prio));
+        PG_CUDA(cudaStreamCreateWithPriority(&c.rdn, cudaStreamNonBlocking, prio));
     }
     while (c.ev.size() < nev) {
         cudaEvent_t e;
@@ -601,6 +620,7 @@ struct StagedD2H {
 // size floor (1 and 1 otherwise); "host_trace" = 1 prints phase times.
 void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_rows, uint64_t dim,
               float* out_host, unsigned flags) {
+    const auto t_entry = std::chrono::steady_clock::now();
     const Base b = base_of(G);
     std::lock_guard<std::recursive_mutex> lk(G.mu);  // caches stay put for the whole pipeline
     if (parent_indexed && G.edges_remap.get())
@@ -722,8 +742,11 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
     // rows with a 2-D copy: a repack kernel on the copy stream would queue
     // behind the SpMM's blocks and hold the segment back until the pass ends
     const bool pitch2d = !packed && tuning(kTuneHostPitch2d) != 0;
-    auto upload_rows = [&](float* dst_pitched, float* dst_flat, const float* src, uint64_t rows, bool pageable) {
-        if (!rows) return;
+    // returns the stream the rows are ready on (h2d, or rup after the repack
+    // when `split`: the next segment's DMA does not wait for this repack)
+    auto upload_rows = [&](float* dst_pitched, float* dst_flat, const float* src, uint64_t rows, bool pageable,
+                           cudaEvent_t copied, bool split) -> cudaStream_t {
+        if (!rows) return cs.h2d;
         if (packed) {
             upload(dst_pitched, src, rows * dim * 4, pageable);
         } else if (pitch2d && !pageable) {
@@ -731,18 +754,33 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
                                       cs.h2d));
         } else {
             upload(dst_flat, src, rows * dim * 4, pageable);
-            copy_rows(dst_flat, dim, dst_pitched, ld, rows, dim, cs.h2d);
+            if (!split) {
+                copy_rows(dst_flat, dim, dst_pitched, ld, rows, dim, cs.h2d);
+                return cs.h2d;
+            }
+            PG_CUDA(cudaEventRecord(copied, cs.h2d));
+            PG_CUDA(cudaStreamWaitEvent(cs.rup, copied, 0));
+            copy_rows(dst_flat, dim, dst_pitched, ld, rows, dim, cs.rup);
+            return cs.rup;
         }
+        return cs.h2d;
     };
     if (D && dim && !(flags & PG_AGG_OVERWRITE))  // accumulate: current output goes up first
-        upload_rows(dout.get(), fout.get(), out_host, D, out_pg);
+        upload_rows(dout.get(), fout.get(), out_host, D, out_pg, nullptr, false);
+    // extra sync events after the 2 + K + R of the pipeline: segment k's
+    // flat copy done (before its repack), chunk r repacked (before its D2H)
+    cudaEvent_t* ev_copied = cs.ev.data() + 2 + K + R;
+    cudaEvent_t* ev_packed = cs.ev.data() + 2 + 2 * K + R;
+    // trace events on rup/rdn are not needed: the pass / D2H marks follow them
     // segment k up, then pass k (every destination, segment k's edges) for
     // the K - F segments before the chunked last pass
     for (uint32_t k = 0; k < K; ++k) {
         const uint64_t r0 = rcut[k], r1 = rcut[k + 1];
+        cudaStream_t ready = cs.h2d;
         if (r1 > r0 && dim)
-            upload_rows(din.get() + r0 * ld, fin.get() + r0 * dim, in_host + r0 * dim, r1 - r0, in_pg);
-        PG_CUDA(cudaEventRecord(cs.ev[1 + k], cs.h2d));
+            ready = upload_rows(din.get() + r0 * ld, fin.get() + r0 * dim, in_host + r0 * dim, r1 - r0, in_pg,
+                                ev_copied[k], true);
+        PG_CUDA(cudaEventRecord(cs.ev[1 + k], ready));
         tmark(cs.h2d, "h2d" + std::to_string(k));
         if (k + F < K) {
             PG_CUDA(cudaStreamWaitEvent(s, cs.ev[1 + k], 0));
@@ -787,7 +825,12 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
             continue;
         }
         if (!packed) {
-            copy_rows(dout.get() + rb * ld, ld, fout.get() + rb * dim, dim, re - rb, dim, cs.d2h);
+            // repack on rdn (waits for the chunk), the D2H stream waits for
+            // the repack: chunk r+1's repack overlaps chunk r's DMA
+            PG_CUDA(cudaStreamWaitEvent(cs.rdn, cs.ev[1 + K + r], 0));
+            copy_rows(dout.get() + rb * ld, ld, fout.get() + rb * dim, dim, re - rb, dim, cs.rdn);
+            PG_CUDA(cudaEventRecord(ev_packed[r], cs.rdn));
+            PG_CUDA(cudaStreamWaitEvent(cs.d2h, ev_packed[r], 0));
             src = fout.get() + rb * dim;
         }
         if (down)
@@ -800,10 +843,16 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
     // buffers are freed stream-ordered on s: s waits for both copy streams
     PG_CUDA(cudaEventRecord(cs.ev[1 + K + R], cs.d2h));
     PG_CUDA(cudaStreamWaitEvent(s, cs.ev[1 + K + R], 0));
+    const auto t_queued = std::chrono::steady_clock::now();
     PG_CUDA(cudaStreamSynchronize(s));
     if (trace) {
+        const auto t_done = std::chrono::steady_clock::now();
+        auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        char wb[96];
+        std::snprintf(wb, sizeof(wb), " host: queued=%.2f wall=%.2f |", ms(t_entry, t_queued), ms(t_entry, t_done));
         std::string line = "[host_trace] D=" + std::to_string(D) + " dim=" + std::to_string(dim) +
-                           " K=" + std::to_string(K) + " F=" + std::to_string(F) + " R=" + std::to_string(R) + ":";
+                           " K=" + std::to_string(K) + " F=" + std::to_string(F) + " R=" + std::to_string(R) + ":" +
+                           wb;
         for (size_t i = 1; i < nt; ++i) {
             float ms = 0.f;
             PG_CUDA(cudaEventElapsedTime(&ms, cs.tev[0], cs.tev[i]));

@@ -315,8 +315,15 @@ enum TuneKeyId {
     kTuneGemmTc = 23,
     kTuneRecWindow = 24,
     kTuneSrcSegBalance = 25,
-    kTuneHostMinMb = 26
+    kTuneHostMinMb = 26,
+    kTuneRowKernel = 27,
+    kTuneRowU = 28,
+    kTuneRowSegMb = 29,
+    kTuneRowHeavy = 30,
+    kTuneVecBlock = 31
 };
+// whole-row SpMM warps (k_agg_row) for this width (tuning "row_kernel")
+bool row_kernel_on(uint64_t dim);
 
 int64_t tuning(int key);
 bool set_tuning(const char* name, int64_t value);

@@ -139,6 +139,45 @@ def test_heavy_ring_kernel_bit_exact(pg, orc, dim, heavy_min, kern):
             pg.set_tuning(k)
 
 
+@pytest.mark.parametrize("variant", [{"row_kernel": 1}, {"row_kernel": 1, "row_u": 3, "row_seg_mb": 8},
+                                     {"row_kernel": 1, "row_u": 4, "row_heavy": 64}, {"vec_block": 512},
+                                     {"vec_block": 1024}, {"ld_cg": 7}, {"heavy_wide_pipe": 2}])
+@pytest.mark.parametrize("dim", [130, 300, 602, 700])
+def test_wide_row_schedule_variants_bit_exact(pg, orc, dim, variant):
+    """The measured-and-kept-selectable wide-row schedules:
+    whole-row warps (k_agg_row) with their L2-sized segments and hub
+    threshold, 512/1024-thread CTAs, evict-first record loads, chunk-major hub
+    items — bit-identical to the oracle, accumulate semantics and row ranges
+    included."""
+    torch = torch_mod()
+    pairs, n_pad = rmat_pairs(orc, 4096, 4096 * 24, 21)
+    vt = orc.sample_training_set(4096, 0.5, 8)
+    og, dg, F, ops, dps = build_all(pg, orc, pairs, n_pad, vt, 2)
+    rng = np.random.default_rng(dim)
+    try:
+        for k, v in variant.items():
+            pg.set_tuning(k, v)
+        pg.set_heavy_min_degree(64)
+        for dp, op in zip(dps, ops):
+            y = rng.uniform(-1, 1, size=(dp.P, dim)).astype(np.float32)
+            base = rng.uniform(-1, 1, size=(dp.D, dim)).astype(np.float32)
+            want = orc.aggregate_pull_f32(op.offsets, op.neighbors, op.weights, y[op.srcpos], out=base)
+            x = to_dev(base, pg.padded_ld(dim))
+            G = pg.group_neighbors(dp, 3)
+            pg.backward_aggregation(G, to_dev(y, pg.padded_ld(dim)), x)
+            torch.cuda.synchronize()
+            assert np.array_equal(bits(x.cpu().numpy()), bits(want)), (dim, variant)
+            b = dp.shard_bounds(3)
+            x2 = to_dev(base[b[1]:b[2]], pg.padded_ld(dim))
+            pg.backward_aggregation(G, to_dev(y, pg.padded_ld(dim)), x2, rows=(b[1], b[2]))
+            torch.cuda.synchronize()
+            assert np.array_equal(bits(x2.cpu().numpy()), bits(want[b[1]:b[2]])), (dim, variant, "rows")
+    finally:
+        pg.set_heavy_min_degree(None)
+        for k in variant:
+            pg.set_tuning(k)
+
+
 def test_aggregate_pull_local_and_accumulate(pg, orc):
     torch = torch_mod()
     pairs, n_pad = rmat_pairs(orc, 2048, 2048 * 6, 3)

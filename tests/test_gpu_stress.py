@@ -17,14 +17,18 @@ WIDTHS = (1, 3, 16, 17, 41, 64, 100, 128, 129, 300, 602)
 KNOBS = {
     "vec_u": (4, 8, 16),
     "chunk_major": (0, 1),
-    "ld_cg": (0, 2),
+    "ld_cg": (0, 2, 7),
     "heavy_narrow": (0, 1),
-    "heavy_wide_pipe": (0, 1),
+    "heavy_wide_pipe": (0, 1, 2),
     "wide_lpd": (16, 32),
     "src_segs": (0, 1, 2, 3),
     "src_seg_balance": (0, 50, 100),
     "heavy_tma": (0, 1),
     "rec_window": (0, 1),
+    "row_kernel": (0, 0, 1),
+    "row_u": (2, 3, 4),
+    "row_seg_mb": (8, 56),
+    "vec_block": (256, 256, 512, 1024),
 }
 
 
