@@ -941,13 +941,19 @@ def knob_sweep(pg, torch, step, L, x_out, dims, config, settings):
     the defaults), each with its x_grad checked against the reference digest."""
     for st in settings:
         for k, v in st.items():
-            pg.set_tuning(k, v)
+            if k == "heavy_min":  # pg_set_heavy_min_degree
+                pg.set_heavy_min_degree(v)
+            else:
+                pg.set_tuning(k, v)
         ms = time_steps(torch, step, L, reps=20)
         par = x_grad_parity(x_out, dims, config)
         log(f"[sweep] {json.dumps(st)} per-path ms={[round(x, 3) for x in ms]} total={sum(ms):.3f} "
             f"parity={par['all'] if par else None}")
         for k in st:
-            pg.set_tuning(k)
+            if k == "heavy_min":
+                pg.set_heavy_min_degree(None)
+            else:
+                pg.set_tuning(k)
 
 
 def sweep(pg, torch, step, paths, dims, stream):

@@ -76,8 +76,13 @@ constexpr TuneKey kTuneKeys[] = {
     {"row_seg_mb", "PG_ROW_SEG_MB", 56},  // k_agg_row: per-pass source working set (MB) of the L2-sized segments
     {"row_heavy", "PG_ROW_HEAVY", 0},    // k_agg_row: hub degree threshold (0 = the default rule)
     {"vec_block", "PG_VEC_BLOCK", 256},  // k_agg_vec4 wide rows: threads per CTA (256, 512, 1024)
+    // wide-row hubs: 1 = destination-major front of the main kernel (every
+    // hub chunk starts with the pass, no concurrent side kernel; Reddit
+    // layer 0 16.5 -> 15.8 ms), 0 = k_agg_wide_pipe on a forked stream
+    {"hub_inline", "PG_HUB_INLINE", 1},
+    {"hub_front_min", "PG_HUB_FRONT_MIN", 0},  // hub_inline: degree threshold of the front (0 = the hub rule)
 };
-static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneVecBlock + 1,
+static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneHubFrontMin + 1,
               "kTuneKeys and enum TuneKeyId (pg_internal.h) must list the same keys in the same order");
 std::atomic<int64_t> g_tune[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];
 int64_t g_tune_def[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];  // $PG_<KEY> at load, else built-in
@@ -311,9 +316,20 @@ __global__ void __launch_bounds__(BS, (BS == 256 ? (U <= 8 ? 4 : 2) : 1024 / BS)
     // destination-major (the chunks of one destination on neighbouring warps)
     // or chunk-major (one column chunk of every destination, then the next:
     // the per-pass source working set is S x chunk bytes)
+    // chunk_major >= 2: the first chunk_major - 2 destinations (the hubs at
+    // the head of the degree order) go destination-major ahead of the
+    // chunk-major rest, so every hub chunk starts at the beginning of the pass
     const uint64_t nd = n_items / chunks;
-    const uint32_t di = static_cast<uint32_t>(chunk_major ? item % nd : item / chunks);
-    const uint32_t ci = static_cast<uint32_t>(chunk_major ? item / nd : item % chunks);
+    const uint64_t nf = chunk_major > 1 ? static_cast<uint64_t>(chunk_major - 2) : 0;
+    uint32_t di, ci;
+    if (!chunk_major || item < nf * chunks) {
+        di = static_cast<uint32_t>(item / chunks);
+        ci = static_cast<uint32_t>(item % chunks);
+    } else {
+        const uint64_t r = item - nf * chunks, nr = nd - nf;
+        di = static_cast<uint32_t>(nf + r % nr);
+        ci = static_cast<uint32_t>(r / nr);
+    }
     const uint32_t d = __ldg(order + d_begin + di);
     if (FILT && !ext_dst_on(ext, d)) return;
     const uint32_t q = ci * LPD + static_cast<uint32_t>(t % LPD);
@@ -1808,9 +1824,10 @@ SideStream& side_stream() {
 template <int LPD, int U>
 void launch_vec4(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges, const uint32_t* order, uint32_t d_begin,
                  uint32_t nd, uint32_t chunks, const float* in, uint64_t ld_in, float* out, uint64_t ld_out,
-                 uint32_t dim, bool accumulate, cudaStream_t s, const AggExt& ext) {
+                 uint32_t dim, bool accumulate, cudaStream_t s, const AggExt& ext, uint32_t n_front = 0) {
     const uint64_t items = static_cast<uint64_t>(nd) * chunks;
-    const int cm = chunks > 1 && tuning(kTuneChunkMajor) ? 1 : 0;
+    int cm = chunks > 1 && tuning(kTuneChunkMajor) ? 1 : 0;
+    if (cm && n_front) cm = 2 + static_cast<int>(std::min(n_front, nd));
     // gather load flavour (tuning "ld_cg", see ld_row): measured on the
     // Reddit layer-0 path, the default read-only L1-allocating load is best
     const int ldm = static_cast<int>(tuning(kTuneLdCg));
@@ -1902,7 +1919,10 @@ void aggregate_det(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges
     // heavy wide destinations (k_agg_wide_lat) take no activity filter: the
     // filtered (if-else) traversal keeps them on the main kernel
     const uint32_t nh = vec && !(filt && nq > 16) ? std::min(n_heavy, nd) : 0;
-    if (nh) {
+    // tuning "hub_inline": wide-row hubs stay in the main kernel as its
+    // destination-major front instead of a concurrent side kernel
+    const bool inline_hubs = nh && nq > 16 && !filt && tuning(kTuneHubInline) != 0 && !row_kernel_on(dim32);
+    if (nh && !inline_hubs) {
         // heavy prefix of the degree order on a forked stream, concurrent
         // with the main kernel over the rest; joined back into s
         SideStream& ss = side_stream();
@@ -1987,7 +2007,7 @@ void aggregate_det(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges
                                 accumulate, s, ext);
         else
             launch_vec4<32, 8>(ebeg, eend, edges, order, d_begin, nd, chunks, in, ld_in, out, ld_out, dim32, accumulate,
-                               s, ext);
+                               s, ext, inline_hubs ? nh : 0);
     } else if (nq > 8) {
         launch_vec4<16, 8>(ebeg, eend, edges, order, d_begin, nd, 1, in, ld_in, out, ld_out, dim32, accumulate, s, ext);
     } else if (nq > 4) {

@@ -177,7 +177,12 @@ void check_dims(uint64_t dim, uint64_t ld_in, uint64_t ld_out) {
 // hub threshold of a (segment) range: the row kernel's own knob, else the
 // measured default rule
 uint64_t heavy_degree(uint64_t dim, uint64_t range_edges) {
-    if (row_kernel_on(dim) && tuning(kTuneRowHeavy) > 0) return static_cast<uint64_t>(tuning(kTuneRowHeavy));
+    if (!heavy_min_forced()) {
+        if (row_kernel_on(dim) && tuning(kTuneRowHeavy) > 0) return static_cast<uint64_t>(tuning(kTuneRowHeavy));
+        // wide-row hubs inlined as the main kernel's destination-major front
+        if ((dim + 3) / 4 > 16 && tuning(kTuneHubInline) != 0 && tuning(kTuneHubFrontMin) > 0)
+            return static_cast<uint64_t>(tuning(kTuneHubFrontMin));
+    }
     return heavy_min_degree(dim, range_edges);
 }
 

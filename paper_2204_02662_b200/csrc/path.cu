@@ -306,6 +306,7 @@ uint64_t heavy_min_degree(uint64_t dim, uint64_t range_edges) {
     return t > 12288 ? 0 : std::max<uint64_t>(t, 2048);
 }
 void set_heavy_min_degree(uint64_t v) { g_heavy_min.store(v, std::memory_order_relaxed); }
+bool heavy_min_forced() { return g_heavy_min.load(std::memory_order_relaxed) != UINT64_MAX; }
 
 void degree_order(const uint64_t* offsets, uint32_t D, DevBuf<uint32_t>& order, cudaStream_t s, DegHist* out_hist) {
     order = DevBuf<uint32_t>(D, s);

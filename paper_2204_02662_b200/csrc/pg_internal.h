@@ -287,6 +287,7 @@ void aggregate_groups_af(Groups& G, const uint64_t* offsets_dev, uint32_t D, con
 // the width-dependent default)
 uint64_t heavy_min_degree(uint64_t dim, uint64_t range_edges);
 void set_heavy_min_degree(uint64_t v);
+bool heavy_min_forced();  // pg_set_heavy_min_degree / $PG_HEAVY_MIN_DEG in effect
 // scheduling knobs of the SpMM kernels (pg_set_tuning): never change results
 enum TuneKeyId {
     kTuneHeavyTma = 0,
@@ -320,7 +321,9 @@ enum TuneKeyId {
     kTuneRowU = 28,
     kTuneRowSegMb = 29,
     kTuneRowHeavy = 30,
-    kTuneVecBlock = 31
+    kTuneVecBlock = 31,
+    kTuneHubInline = 32,
+    kTuneHubFrontMin = 33
 };
 // whole-row SpMM warps (k_agg_row) for this width (tuning "row_kernel")
 bool row_kernel_on(uint64_t dim);

@@ -118,6 +118,7 @@ def test_heavy_ring_kernel_bit_exact(pg, orc, dim, heavy_min, kern):
         pg.set_tuning("heavy_narrow", 1 if kern == "narrow" else 0)
         pg.set_tuning("heavy_tma", 1 if kern == "tma" else 0)
         pg.set_tuning("heavy_wide_pipe", 0 if kern == "wide_lat" else 1)
+        pg.set_tuning("hub_inline", 0)  # wide rows: the side kernels, not the inlined front
         for dp, op in zip(dps, ops):
             y = rng.uniform(-1, 1, size=(dp.P, dim)).astype(np.float32)
             base = rng.uniform(-1, 1, size=(dp.D, dim)).astype(np.float32)
@@ -135,13 +136,14 @@ def test_heavy_ring_kernel_bit_exact(pg, orc, dim, heavy_min, kern):
             assert np.array_equal(bits(x2.cpu().numpy()), bits(want[b[1]:b[2]]))
     finally:
         pg.set_heavy_min_degree(None)
-        for k in ("heavy_narrow", "heavy_tma", "heavy_wide_pipe"):
+        for k in ("heavy_narrow", "heavy_tma", "heavy_wide_pipe", "hub_inline"):
             pg.set_tuning(k)
 
 
 @pytest.mark.parametrize("variant", [{"row_kernel": 1}, {"row_kernel": 1, "row_u": 3, "row_seg_mb": 8},
                                      {"row_kernel": 1, "row_u": 4, "row_heavy": 64}, {"vec_block": 512},
-                                     {"vec_block": 1024}, {"ld_cg": 7}, {"heavy_wide_pipe": 2}])
+                                     {"vec_block": 1024}, {"ld_cg": 7}, {"hub_inline": 0, "heavy_wide_pipe": 2},
+                                     {"hub_inline": 0}, {"hub_inline": 1, "hub_front_min": 8}])
 @pytest.mark.parametrize("dim", [130, 300, 602, 700])
 def test_wide_row_schedule_variants_bit_exact(pg, orc, dim, variant):
     """The measured-and-kept-selectable wide-row schedules:
