@@ -298,8 +298,9 @@ __device__ __forceinline__ void acc_store_ext(float* orow, uint32_t col, uint32_
 
 // LPD lanes per (destination, chunk); each lane one float4 column. Per batch
 // of U edges: U edge-record loads, U row gathers (all in flight), then the
-// U ordered accumulate steps. Lanes past dim gather column 0 (in bounds,
-// discarded) so no load is predicated.
+// U ordered accumulate steps. Lanes past dim gather their chunk's first
+// float4 (in bounds, the sector lane 0 reads anyway; discarded) so no load
+// is predicated and no extra sector is fetched.
 template <int LPD, int U, bool FILT, int CG = 0, bool RW = false, int BS = 256>
 __global__ void __launch_bounds__(BS, (BS == 256 ? (U <= 8 ? 4 : 2) : 1024 / BS)) k_agg_vec4(const uint64_t* __restrict__ ebeg, const uint64_t* __restrict__ eend,
                                                  const Edge* __restrict__ edges,
@@ -337,7 +338,7 @@ __global__ void __launch_bounds__(BS, (BS == 256 ? (U <= 8 ? 4 : 2) : 1024 / BS)
     const bool active = col < dim;
     uint64_t e = __ldg(ebeg + d);
     const uint64_t end = __ldg(eend + d);
-    const char* base = reinterpret_cast<const char*>(in) + (active ? col : 0u) * 4u;
+    const char* base = reinterpret_cast<const char*>(in) + (active ? col : ci * LPD * 4u) * 4u;
     asm("mov.b64 %0, %0;" : "+l"(base));  // per-lane 64-bit base: IMAD.WIDE adds it
     const uint32_t row = ext_out_row(ext, d);
     float* orow = out + row * ld_out + col;
@@ -559,7 +560,7 @@ __global__ void __launch_bounds__(256, (U <= 8 ? 4 : 2)) k_agg_groups(
     uint64_t e = __ldg(gbeg + gi);
     const uint64_t end = __ldg(gend + gi);
     const bool multi = __ldg(dest_groups + d + 1) - __ldg(dest_groups + d) > 1;
-    const char* base = reinterpret_cast<const char*>(in) + (active ? col : 0u) * 4u;
+    const char* base = reinterpret_cast<const char*>(in) + (active ? col : ci * LPD * 4u) * 4u;
     asm("mov.b64 %0, %0;" : "+l"(base));
     Acc acc{0ull, 0ull};  // scratch, zero filled (aggregate.hpp:93)
     for (; e + U <= end; e += U) {
@@ -657,7 +658,7 @@ __global__ void __launch_bounds__(256, 4) k_agg_groups_seg(
     if (valid) {
         uint64_t e = __ldg(gbeg + gi);
         const uint64_t end = __ldg(gend + gi);
-        const char* base = reinterpret_cast<const char*>(in) + (active ? col : 0u) * 4u;
+        const char* base = reinterpret_cast<const char*>(in) + (active ? col : ci * LPD * 4u) * 4u;
         asm("mov.b64 %0, %0;" : "+l"(base));
         for (; e + U <= end; e += U) {
             Edge ed[U];
@@ -956,7 +957,7 @@ __global__ void __launch_bounds__(64) k_agg_wide_pipe(const uint64_t* __restrict
             if (col + 2 < dim) acc.z = orow[2];
         }
     }
-    const char* base = reinterpret_cast<const char*>(in) + (active ? col : 0u) * 4u;
+    const char* base = reinterpret_cast<const char*>(in) + (active ? col : ci * 128u) * 4u;
     asm("mov.b64 %0, %0;" : "+l"(base));
     const uint64_t nb = (ee - eb + U - 1) / U;
     // record window: 32 records, one per lane; batch b uses records
@@ -1471,7 +1472,7 @@ __global__ void __launch_bounds__(256, 4) k_agg_grp(const uint4* __restrict__ ra
     const unsigned w = tid / LPD, sl = tid % LPD;
     const uint32_t col = (ci * LPD + sl) * 4;
     const bool active = col < dim;
-    const char* base = reinterpret_cast<const char*>(in) + (active ? col : 0u) * 4u;
+    const char* base = reinterpret_cast<const char*>(in) + (active ? col : ci * LPD * 4u) * 4u;
     asm("mov.b64 %0, %0;" : "+l"(base));
     const uint32_t srecs = static_cast<uint32_t>(__cvta_generic_to_shared(recs));
     // a record: from the staged window (LDS, one broadcast per sub-warp) or,
