@@ -55,7 +55,7 @@ constexpr TuneKey kTuneKeys[] = {
     {"host_chunk_balance", "PG_HOST_CHUNK_BALANCE", 30},  // host drop-in: last-pass chunk cuts, % weight of edges vs rows
     {"atb_split", "PG_ATB_SPLIT", 1},  // W' GEMM: 1 = copy warp + chain warp, 0 = one warp does both
     {"atb_pairs", "PG_ATB_PAIRS", 224},  // W' split GEMM: 2 A columns per lane above this many 64-chain blocks (0 = never)
-    {"gemm_packed", "PG_GEMM_PACKED", 1},  // gemm / gemm_a_bt: 1 = FFMA2/FADD2 column pairs (k_gemm2), 0 = k_gemm
+    {"gemm_packed", "PG_GEMM_PACKED", 2},  // gemm / gemm_a_bt: 2 = k_gemm3 register tiles (m > 64), 1 = k_gemm2 FFMA2 column pairs, 0 = k_gemm
     {"host_last_seg_pct", "PG_HOST_LAST_SEG_PCT", 45},  // host drop-in: % of the edges in the last (chunked) segment, 0 = 1/K
     {"wgrad_fork", "PG_WGRAD_FORK", 1},  // backward chains: W' GEMMs on a forked stream (1) or in order (0)
     // chain y_grad = g W^T (gemm_a_bt): 0 = bit-exact FFMA2 kernel, 1 = tcgen05
@@ -81,8 +81,10 @@ constexpr TuneKey kTuneKeys[] = {
     // layer 0 16.5 -> 15.8 ms), 0 = k_agg_wide_pipe on a forked stream
     {"hub_inline", "PG_HUB_INLINE", 1},
     {"hub_front_min", "PG_HUB_FRONT_MIN", 0},  // hub_inline: degree threshold of the front (0 = the hub rule)
+    {"gemm3_rows", "PG_GEMM3_ROWS", 8},  // k_gemm3 (gemm_packed 2): output rows per thread, 8 or 16
+    {"gemm_beside_wgrad", "PG_GEMM_BESIDE_WGRAD", 1},  // backward chains: y_grad on k_gemm2 while a W' fork runs
 };
-static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneHubFrontMin + 1,
+static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneGemmBesideWgrad + 1,
               "kTuneKeys and enum TuneKeyId (pg_internal.h) must list the same keys in the same order");
 std::atomic<int64_t> g_tune[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];
 int64_t g_tune_def[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];  // $PG_<KEY> at load, else built-in

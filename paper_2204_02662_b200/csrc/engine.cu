@@ -152,6 +152,147 @@ __global__ void __launch_bounds__(256) k_gemm2(const float* __restrict__ a, uint
     }
 }
 
+// Register-tiled variant (tuning "gemm_packed" = 2): each thread owns an
+// 8 x 8 output tile (rows {4ty..4ty+3, 64+4ty..}, column pairs at 4tx and
+// 64+4tx of a 128 x 128 CTA tile), so per k it reads 8 A scalars and 8 B
+// values from shared memory for 32 FFMA2 + 32 FADD2. What bounds k_gemm2 is
+// the L1 -> register writeback (one cycle per register written per lane):
+// its warp-wide row tile loads one broadcast A value per row per k for only
+// 2 output columns a lane (18 registers written per 32 FP instructions);
+// here it is 16 per 64. A goes global -> shared by cp.async (16 B, zero-fill
+// past n / K), double-buffered over 16-k chunks; B arrives k-major
+// (gemm_a_bt transposes W first, a few KB). Same chain per output as k_gemm:
+// ascending k, fl(a*b) by FFMA2 with a runtime -0 addend, FADD2, then + 0.
+constexpr int kG3K = 16;   // k chunk
+constexpr int kG3N = 128;  // columns per CTA tile (16 threads x 8)
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int bytes) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(bytes));
+}
+
+// A rows [i0, i0+TM) x k [k0, k0+16) and B (k-major, ld ldb) rows
+// [k0, k0+16) x columns [j0, j0+128) into stage buffers; zero past n / m / K
+template <int TM>
+__device__ __forceinline__ void g3_load(float (*As)[kG3K + 4], float (*Bs)[kG3N + 4], const float* a, uint64_t lda,
+                                        const float* b, uint64_t ldb, uint64_t n, uint64_t m, uint64_t K,
+                                        uint64_t i0, uint64_t j0, uint64_t k0, int tid) {
+#pragma unroll
+    for (int h = 0; h < TM / 64; ++h) {
+        const int row = (tid >> 2) + 64 * h, kq = (tid & 3) * 4;
+        const uint64_t gi = i0 + row, gk = k0 + kq;
+        const bool in = gi < n && gk < K;
+        const int bytes = in ? (K - gk >= 4 ? 16 : static_cast<int>((K - gk) * 4)) : 0;
+        cp_async16(&As[row][kq], in ? a + gi * lda + gk : a, bytes);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int k = (tid >> 5) + 8 * h, jq = (tid & 31) * 4;
+        const uint64_t gk = k0 + k, gj = j0 + jq;
+        const bool in = gk < K && gj < m;
+        const int bytes = in ? (m - gj >= 4 ? 16 : static_cast<int>((m - gj) * 4)) : 0;
+        cp_async16(&Bs[k][jq], in ? b + gk * ldb + gj : b, bytes);
+    }
+    asm volatile("cp.async.commit_group;");
+}
+
+// thread row r of RM: rows 4 ty + (r % 4) + 64 (r / 4) of the CTA tile
+template <int RM>
+__global__ void __launch_bounds__(256, RM == 8 ? 2 : 1) k_gemm3(const float* __restrict__ a, uint64_t lda,
+                                                                const float* __restrict__ b, uint64_t ldb,
+                                                                float* __restrict__ out, uint64_t ldo, uint64_t n,
+                                                                uint64_t m, uint64_t K, float nz) {
+    constexpr int TM = 16 * RM;
+    // dynamic: 2 x (TM x 20 + 16 x 132) floats = 38.4 KB (RM 8) / 57.3 KB (RM 16)
+    extern __shared__ __align__(16) float g3_smem[];
+    auto As = reinterpret_cast<float(*)[TM][kG3K + 4]>(g3_smem);
+    auto Bs = reinterpret_cast<float(*)[kG3K][kG3N + 4]>(g3_smem + 2 * TM * (kG3K + 4));
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const uint64_t i0 = blockIdx.x * static_cast<uint64_t>(TM), j0 = blockIdx.y * static_cast<uint64_t>(kG3N);
+    unsigned long long nz2, acc[RM][4];
+    asm("mov.b64 %0, {%1,%1};" : "=l"(nz2) : "f"(nz));
+#pragma unroll
+    for (int i = 0; i < RM; ++i)
+#pragma unroll
+        for (int p = 0; p < 4; ++p) asm("mov.b64 %0, {%1,%1};" : "=l"(acc[i][p]) : "f"(0.f));
+    const uint64_t nk = (K + kG3K - 1) / kG3K;
+    g3_load<TM>(As[0], Bs[0], a, lda, b, ldb, n, m, K, i0, j0, 0, tid);
+    for (uint64_t c = 0; c < nk; ++c) {
+        const int cur = static_cast<int>(c & 1);
+        if (c + 1 < nk) {
+            g3_load<TM>(As[cur ^ 1], Bs[cur ^ 1], a, lda, b, ldb, n, m, K, i0, j0, (c + 1) * kG3K, tid);
+            asm volatile("cp.async.wait_group 1;");
+        } else {
+            asm volatile("cp.async.wait_group 0;");
+        }
+        __syncthreads();
+        // zero-filled k past K adds +-0 products after the real ones: only a
+        // -0 chain can change (to +0), which the final fl(acc + 0) does anyway
+#pragma unroll
+        for (int kk = 0; kk < kG3K; kk += 2) {
+            float2 av[RM];
+#pragma unroll
+            for (int i = 0; i < RM; ++i)
+                av[i] = *reinterpret_cast<const float2*>(&As[cur][4 * ty + (i & 3) + 64 * (i >> 2)][kk]);
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const float4 b0 = *reinterpret_cast<const float4*>(&Bs[cur][kk + u][4 * tx]);
+                const float4 b1 = *reinterpret_cast<const float4*>(&Bs[cur][kk + u][64 + 4 * tx]);
+                unsigned long long bp[4];
+                asm("mov.b64 %0, {%1,%2};" : "=l"(bp[0]) : "f"(b0.x), "f"(b0.y));
+                asm("mov.b64 %0, {%1,%2};" : "=l"(bp[1]) : "f"(b0.z), "f"(b0.w));
+                asm("mov.b64 %0, {%1,%2};" : "=l"(bp[2]) : "f"(b1.x), "f"(b1.y));
+                asm("mov.b64 %0, {%1,%2};" : "=l"(bp[3]) : "f"(b1.z), "f"(b1.w));
+#pragma unroll
+                for (int i = 0; i < RM; ++i) {
+                    unsigned long long aa;
+                    asm("mov.b64 %0, {%1,%1};" : "=l"(aa) : "f"(u ? av[i].y : av[i].x));
+#pragma unroll
+                    for (int p = 0; p < 4; ++p) {
+                        unsigned long long pr;
+                        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(pr) : "l"(aa), "l"(bp[p]), "l"(nz2));
+                        asm("add.rn.f32x2 %0, %1, %2;" : "=l"(acc[i][p]) : "l"(acc[i][p]), "l"(pr));
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+    const bool v4 = (ldo & 3) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+#pragma unroll
+    for (int i = 0; i < RM; ++i) {
+        const uint64_t gi = i0 + 4 * ty + (i & 3) + 64 * (i >> 2);
+        if (gi >= n) continue;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint64_t gj = j0 + 64 * h + 4 * tx;
+            if (gj >= m) continue;
+            float v[4];
+            asm("mov.b64 {%0,%1}, %2;" : "=f"(v[0]), "=f"(v[1]) : "l"(acc[i][2 * h]));
+            asm("mov.b64 {%0,%1}, %2;" : "=f"(v[2]), "=f"(v[3]) : "l"(acc[i][2 * h + 1]));
+#pragma unroll
+            for (int q = 0; q < 4; ++q) v[q] = __fadd_rn(v[q], 0.f);
+            float* o = out + gi * ldo + gj;
+            if (v4 && gj + 3 < m) {
+                *reinterpret_cast<float4*>(o) = make_float4(v[0], v[1], v[2], v[3]);
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (gj + q < m) o[q] = v[q];
+            }
+        }
+    }
+}
+
+// W^T for gemm_a_bt's k-major B operand: t[k][j] = b[j][k] (ld_t = m4)
+__global__ void k_transpose(const float* __restrict__ b, uint64_t ldb, float* __restrict__ t, uint64_t ldt,
+                            uint64_t m, uint64_t K) {
+    const uint64_t idx = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (idx >= m * K) return;
+    const uint64_t k = idx / m, j = idx % m;
+    t[k * ldt + j] = b[j * ldb + k];
+}
+
 // ---- out = A[rows]^T * B (dense_matrix.hpp:57-76 gemm_at_b) -----------------
 // out[i][j] = sum over k < n, ascending, of A(k, i) * B(k, j), A(k, i) =
 // a[(rows ? rows[k] : k) * lda + i] (the engine's gather_rows fused in).
@@ -614,7 +755,7 @@ dim3 rows_grid(uint64_t rows, uint64_t cols, unsigned tx) {
 
 }  // namespace
 
-void gemm(DMat a, DMat b, DMat out, bool b_transposed, cudaStream_t s) {
+void gemm(DMat a, DMat b, DMat out, bool b_transposed, cudaStream_t s, int packed) {
     const uint64_t K = a.cols;
     if (b_transposed ? b.cols != K : b.rows != K) fail_shape("gemm: inner dimensions differ");
     const uint64_t n = a.rows, m = b_transposed ? b.rows : b.cols;
@@ -630,9 +771,47 @@ void gemm(DMat a, DMat b, DMat out, bool b_transposed, cudaStream_t s) {
         gemm_a_bt_tc(a, b, out, s);
         return;
     }
+    // register-tiled k_gemm3: A rows by 16-byte cp.async (lda % 4 == 0,
+    // 16-byte aligned), B k-major (gemm_a_bt transposes W into scratch)
+    const bool a16 = (a.ld & 3) == 0 && (reinterpret_cast<uintptr_t>(a.p) & 15) == 0;
+    // (m <= 64: a 128-column tile is mostly waste, k_gemm2's 64 wins: the
+    // products H W1 at m = 47 runs 4.08 ms there vs 5.02 ms here)
+    if (packed < 0) packed = static_cast<int>(tuning(kTuneGemmPacked));
+    if (packed == 2 && m > 2 * kGT && a16 &&
+        (b_transposed || ((b.ld & 3) == 0 && (reinterpret_cast<uintptr_t>(b.p) & 15) == 0))) {
+        volatile float nz = -0.f;
+        const float* bk = b.p;
+        uint64_t ldbk = b.ld;
+        DevBuf<float> bt;
+        int dev = 0;
+        PG_CUDA(cudaGetDevice(&dev));
+        (void)lib_stream(dev);  // the stream-ordered pool keeps the scratch (no re-map per call)
+        if (b_transposed) {
+            ldbk = (m + 3) & ~3ull;
+            bt = DevBuf<float>(K * ldbk, s);
+            k_transpose<<<grid_for(m * K, 256), 256, 0, s>>>(b.p, b.ld, bt.get(), ldbk, m, K);
+            PG_LAUNCH("k_transpose");
+            bk = bt.get();
+        }
+        // 16 x 8 thread tiles (24 registers loaded per 128 FP instructions)
+        // when the rows fill 256-row CTA tiles, else 8 x 8
+        const unsigned gy = static_cast<unsigned>((m + kG3N - 1) / kG3N);
+        auto launch = [&](auto kern, int rm) {
+            const int smem = 2 * (16 * rm * (kG3K + 4) + kG3K * (kG3N + 4)) * 4;
+            PG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));  // per device
+            kern<<<dim3(static_cast<unsigned>((n + 16 * rm - 1) / (16 * rm)), gy), 256, smem, s>>>(
+                a.p, a.ld, bk, ldbk, out.p, out.ld, n, m, K, nz);
+        };
+        if (tuning(kTuneGemm3Rows) == 16)
+            launch(k_gemm3<16>, 16);
+        else
+            launch(k_gemm3<8>, 8);
+        PG_LAUNCH("k_gemm3");
+        return;
+    }
     // 64-column tiles waste most of a narrow output (m <= 32: the forward's
     // X W at width 16 runs 1.01 ms packed vs 0.61 ms scalar)
-    if (tuning(kTuneGemmPacked) && m > kGT) {
+    if (packed && m > kGT) {
         dim3 grid(static_cast<unsigned>((n + kGI - 1) / kGI), static_cast<unsigned>((m + kG2J - 1) / kG2J));
         volatile float nz = -0.f;  // runtime -0: a literal lets ptxas fold the FFMA2 away
         if (b_transposed)
@@ -775,7 +954,13 @@ struct WGradSide {
         if (static_cast<int>(per_dev.size()) <= dev) per_dev.resize(dev + 1);
         PerDev& d = per_dev[dev];
         if (!d.s) {
-            PG_CUDA(cudaStreamCreateWithFlags(&d.s, cudaStreamNonBlocking));
+            // highest priority: the latency-bound W' chains take SMs as soon
+            // as blocks of the bandwidth-bound y_grad GEMM / SpMM retire
+            // (with the register-tiled y_grad GEMM filling every SM they
+            // started late: products backward_epp 19.7 -> 24.2 ms)
+            int lo = 0, hi = 0;
+            PG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            PG_CUDA(cudaStreamCreateWithPriority(&d.s, cudaStreamNonBlocking, hi));
             PG_CUDA(cudaEventCreateWithFlags(&d.fork, cudaEventDisableTiming));
             PG_CUDA(cudaEventCreateWithFlags(&d.done, cudaEventDisableTiming));
         }
@@ -792,6 +977,15 @@ struct WGradSide {
         PG_CUDA(cudaStreamWaitEvent(side, fork, 0));
         pg::gemm_at_b(a, rows, b, out, side);
         used = true;
+    }
+    // y_grad product beside a forked W' chain (tuning "gemm_beside_wgrad",
+    // the EPP chain over compact frontier rows): the register-tiled k_gemm3
+    // fills every SMSP with FP work and the latency-bound W' chains, that
+    // chain's critical path, lose their issue slots (products backward_epp
+    // 18.1 -> 24.3 ms); k_gemm2 leaves them room. The full-graph chains keep
+    // k_gemm3 (products Global EPP 68.8 -> 47.5 ms)
+    int beside_packed() const {
+        return used && tuning(kTuneGemmPacked) == 2 && tuning(kTuneGemmBesideWgrad) ? 1 : -1;
     }
     void retire(std::unique_ptr<Tmp>& g) {
         if (g) keep.push_back(std::move(g));
@@ -966,7 +1160,7 @@ void backward_epp(Groups* const* PG, Frontiers& F, const BackwardIO& io, int gat
         const DMat g = gcur->m;
         wgs.gemm_at_b(io.y[l], F.levels[i].ids.get(), g, io.w_grads[l]);  // gather_rows(Y, in_rows) fused
         Tmp yg(p.P, in_dim, s);
-        gemm(g, io.w[l], yg.m, true, s);
+        gemm(g, io.w[l], yg.m, true, s, wgs.beside_packed());
         DMat* xo = io.x_grads ? &io.x_grads[i] : nullptr;
         if (xo && (xo->rows != p.D || xo->cols != in_dim)) fail_shape("backward: x_grad shape mismatch");
         std::unique_ptr<Tmp> gn;

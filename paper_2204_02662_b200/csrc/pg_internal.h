@@ -323,7 +323,9 @@ enum TuneKeyId {
     kTuneRowHeavy = 30,
     kTuneVecBlock = 31,
     kTuneHubInline = 32,
-    kTuneHubFrontMin = 33
+    kTuneHubFrontMin = 33,
+    kTuneGemm3Rows = 34,
+    kTuneGemmBesideWgrad = 35
 };
 // whole-row SpMM warps (k_agg_row) for this width (tuning "row_kernel")
 bool row_kernel_on(uint64_t dim);
@@ -352,7 +354,8 @@ struct DMat {
 inline uint64_t pad_ld(uint64_t c) { return c <= 32 ? (c + 3) & ~3ull : (c + 31) & ~31ull; }
 
 // dense_matrix.hpp:40-96: out = a * b (b_transposed: a * b^T, gemm_a_bt)
-void gemm(DMat a, DMat b, DMat out, bool b_transposed, cudaStream_t s);
+// packed: -1 = tuning "gemm_packed", else the kernel choice (0 k_gemm, 1 k_gemm2, 2 k_gemm3)
+void gemm(DMat a, DMat b, DMat out, bool b_transposed, cudaStream_t s, int packed = -1);
 // dense_matrix.hpp:78-95 on the tensor cores (gemm_tc.cu): tcgen05 kind::tf32
 // with 3xTF32 operand splitting — within fp32 tolerance, NOT bit-exact.
 // supported(): A base 16-byte aligned, ld % 4 == 0, the driver's TMA encoder.

@@ -124,11 +124,12 @@ def test_dense_kernels(pg, orc, cuda):
     import torch
 
     rng = np.random.default_rng(5)
-    for packed in (1, 0):  # k_gemm2 (FFMA2/FADD2 column pairs) and k_gemm
+    for packed in (2, 1, 0):  # k_gemm3 (8x8 register tiles), k_gemm2 (FFMA2/FADD2 column pairs), k_gemm
         pg.set_tuning("gemm_packed", packed)
         try:
             for n, k, m in ((1, 1, 1), (37, 602, 16), (300, 16, 41), (65, 33, 130), (129, 35, 63), (200, 7, 100),
-                            (70, 5, 33)):
+                            (70, 5, 33), (257, 47, 256), (130, 256, 100), (128, 32, 128), (383, 19, 602),
+                            (64, 3, 129)):
                 a = rng.uniform(-1, 1, (n, k)).astype(np.float32)
                 b = rng.uniform(-1, 1, (k, m)).astype(np.float32)
                 a[0, : min(2, k)] = [0.0, -0.0][: min(2, k)]
@@ -248,7 +249,8 @@ def test_random_chains(pg, orc, cuda, seed):
     case = (n_req, n_req * int(rng.choice([3, 8, 20])), 90 + seed, float(rng.choice([0.05, 0.3, 1.0])), L, f,
             hidden, classes, bool(seed % 2))
     knobs = {"atb_split": int(rng.integers(0, 2)), "atb_pairs": int(rng.choice([1, 224])),
-             "gemm_packed": int(rng.integers(0, 2)), "wgrad_fork": int(rng.integers(0, 2))}
+             "gemm_packed": int(rng.integers(0, 3)), "wgrad_fork": int(rng.integers(0, 2)),
+             "gemm3_rows": int(rng.choice([8, 16])), "gemm_beside_wgrad": int(rng.integers(0, 2))}
     try:
         for k, v in knobs.items():
             pg.set_tuning(k, v)
