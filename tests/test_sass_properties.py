@@ -63,3 +63,23 @@ def test_tensor_core_gemm_uses_tcgen05(sass):
     for name, body in _kernels(sass, r"k_gemm_abt_tc").items():
         for op in ("UTCHMMA", "LDTM", "UTMALDG", "UBLKCP"):
             assert op in body, (name, op)
+
+
+def test_register_tiled_gemm_is_unfused_and_async_staged(sass):
+    """k_gemm3 (the default bit-exact GEMM): products as FFMA2 with a -0
+    addend plus FADD2 (no fused multiply-add into the chain), A / B tiles by
+    cp.async (LDGSTS) into shared memory, read back as LDS.128."""
+    for name, body in _kernels(sass, r"k_gemm3").items():
+        assert re.search(r"\bFFMA2\b", body) and re.search(r"\bFADD2\b", body), name
+        assert "LDGSTS" in body and "LDS.128" in body, name
+        assert not re.search(r"\bFFMA\b", body), name  # no scalar fused chain step
+
+
+def test_default_spmm_gathers_are_128_bit(sass):
+    """k_agg_vec4 (default instantiation) and the whole-row k_agg_row gather
+    rows with 128-bit loads and keep the multiply and the add separate."""
+    for pat in (r"k_agg_vec4ILi32ELi8ELb0ELi0ELb0ELi256E", r"k_agg_rowILi5ELi2E"):
+        for name, body in _kernels(sass, pat).items():
+            assert "LDG.E.128" in body, name
+            assert re.search(r"\bFADD2\b", body), name
+            assert not GLOBAL_ATOMIC.search(body), name
