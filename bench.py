@@ -592,6 +592,10 @@ def main():
             "l2_hit_rate_pct": cap.get("l2_hit_rate_pct"),
             "sectors_per_request": cap.get("sectors_per_request"),
         })
+    elif world > 1:
+        roofline["traffic_source"] = (f"not applicable at N={world}: the committed ncu captures "
+                                      f"(profiles/ncu_full_{args.config}_r*.json) are of the whole single-GPU path, "
+                                      f"this kernel runs one rank's destination shard")
     else:
         roofline["traffic_source"] = f"no ncu capture of config {args.config} committed"
 
