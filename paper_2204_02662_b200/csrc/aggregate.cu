@@ -61,9 +61,10 @@ constexpr TuneKey kTuneKeys[] = {
     // chain y_grad = g W^T (gemm_a_bt): 0 = bit-exact FFMA2 kernel, 1 = tcgen05
     // 3xTF32 tensor-core kernel (fp32 tolerance, not bit-exact)
     {"gemm_tc", "PG_GEMM_TC", 0},
-    // k_agg_vec4 wide rows: 1 = coalesced record window + shuffles, 0 = a
-    // broadcast record load per edge (measured equal or slightly faster on
-    // the Reddit layer-0 path: 16.52 vs 16.65 ms, so off)
+    // k_agg_vec4 wide rows: 1 = coalesced record window + shuffles, 2 = the
+    // window handed out by REDUX into uniform registers, 0 = a broadcast
+    // record load per edge (measured fastest on the Reddit layer-0 path:
+    // 15.65 vs 15.92 (1) / 15.93 (2) ms, so off)
     {"rec_window", "PG_REC_WINDOW", 0},
     // whole-path L2-sized source segments: cuts by rows (0) .. by edges (100)
     {"src_seg_balance", "PG_SRC_SEG_BALANCE", 0},
@@ -374,8 +375,16 @@ __global__ void __launch_bounds__(BS, (BS == 256 ? (U <= 8 ? 4 : 2) : 1024 / BS)
             const unsigned off = static_cast<unsigned>(e - wbase);
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                ed[u].x = __shfl_sync(submask, win.x, off + u, LPD);
-                ed[u].y = __shfl_sync(submask, win.y, off + u, LPD);
+                if constexpr (CG == 8 && LPD == 32) {
+                    // REDUX lands the record in a uniform register: no
+                    // per-lane register write on the L1 -> RF path
+                    const bool me = sl == off + u;
+                    ed[u].x = __reduce_or_sync(0xffffffffu, me ? win.x : 0u);
+                    ed[u].y = __reduce_or_sync(0xffffffffu, me ? win.y : 0u);
+                } else {
+                    ed[u].x = __shfl_sync(submask, win.x, off + u, LPD);
+                    ed[u].y = __shfl_sync(submask, win.y, off + u, LPD);
+                }
             }
         } else if constexpr (LPD <= 8) {
             Edge mine[NPL];
@@ -1839,6 +1848,9 @@ void launch_vec4(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges, 
     if (ext.src_bits || ext.dst_bits)
         k_agg_vec4<LPD, U, true><<<grid, 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks, in, ldb, out,
                                                       ld_out, dim, accumulate, kZeros, 0u, cm, ext);
+    else if (LPD == 32 && tuning(kTuneRecWindow) == 2)
+        k_agg_vec4<LPD, U, false, 8, true><<<grid, 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks, in,
+                                                                ldb, out, ld_out, dim, accumulate, kZeros, 0u, cm, ext);
     else if (LPD >= 16 && tuning(kTuneRecWindow) == 1)
         k_agg_vec4<LPD, U, false, 0, true><<<grid, 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks, in,
                                                                 ldb, out, ld_out, dim, accumulate, kZeros, 0u, cm, ext);

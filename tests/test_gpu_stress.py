@@ -24,7 +24,7 @@ KNOBS = {
     "src_segs": (0, 1, 2, 3),
     "src_seg_balance": (0, 50, 100),
     "heavy_tma": (0, 1),
-    "rec_window": (0, 1),
+    "rec_window": (0, 1, 2),
     "row_kernel": (0, 0, 1),
     "row_u": (2, 3, 4),
     "row_seg_mb": (8, 56),
