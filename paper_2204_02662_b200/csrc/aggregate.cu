@@ -1936,7 +1936,8 @@ void aggregate_det(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges
     const uint32_t nh = vec && !(filt && nq > 16) ? std::min(n_heavy, nd) : 0;
     // tuning "hub_inline": wide-row hubs stay in the main kernel as its
     // destination-major front instead of a concurrent side kernel
-    const bool inline_hubs = nh && nq > 16 && !filt && tuning(kTuneHubInline) != 0 && !row_kernel_on(dim32);
+    const bool inline_hubs =
+        nh && nq > 16 && !filt && !ext.side_hubs && tuning(kTuneHubInline) != 0 && !row_kernel_on(dim32);
     if (nh && !inline_hubs) {
         // heavy prefix of the degree order on a forked stream, concurrent
         // with the main kernel over the rest; joined back into s

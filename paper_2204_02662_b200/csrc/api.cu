@@ -329,9 +329,11 @@ void pg::run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re,
             rs->re = re;
             degree_order(p.offsets.get() + rb, re - rb, rs->order, lib_stream(p.device), &rs->hist);
         }
+        AggExt er = ext;
+        er.side_hubs = true;  // a row range: hub chains on the deeper-pipelined side kernel
         aggregate_det(eb + rb, ee + rb, edges, rs->order.get(), re - rb, 0, re - rb,
                       rs->hist.heavy(heavy_degree(dim, rs->hist.edges / range_div)), in, ld_in, out, ld_out, dim,
-                      accumulate, s, ext);
+                      accumulate, s, er);
         return;
     }
     Graph& g = *G.graph;

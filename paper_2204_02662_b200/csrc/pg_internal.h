@@ -232,6 +232,10 @@ struct AggExt {
     const uint32_t* pre_rows = nullptr;  // prow of destination d (default: the output row)
     const uint32_t* src_bits = nullptr;  // skip edges whose source (edges[e].x) bit is 0
     const uint32_t* dst_bits = nullptr;  // skip destinations whose bit (of d) is 0: row untouched
+    // scheduling only: hubs of wide rows on the concurrent side kernel even
+    // when tuning hub_inline is on (row ranges: a host-pipeline chunk or a
+    // shard is short, and its hub chains would set its length)
+    bool side_hubs = false;
     bool any() const { return out_rows || relu_pre || src_bits || dst_bits; }
 };
 
