@@ -13,6 +13,7 @@
 // from U edges in flight per lane (U independent LDG.128 before the ordered
 // adds). The gather of gradient rows (engine.hpp:334) is folded into the
 // packed edge record (src_pos_in_parent composed at path build).
+#include <deque>
 #include <algorithm>
 #include <atomic>
 #include <cstdlib>
@@ -84,8 +85,12 @@ constexpr TuneKey kTuneKeys[] = {
     {"hub_front_min", "PG_HUB_FRONT_MIN", 0},  // hub_inline: degree threshold of the front (0 = the hub rule)
     {"gemm3_rows", "PG_GEMM3_ROWS", 8},  // k_gemm3 (gemm_packed 2): output rows per thread, 8 or 16
     {"gemm_beside_wgrad", "PG_GEMM_BESIDE_WGRAD", 1},  // backward chains: y_grad on k_gemm2 while a W' fork runs
+    // host drop-in: hub chunk of the last pass on its own stream, concurrent
+    // with the other chunks (measured 25.7 vs 23.4 ms: it takes the GPU from
+    // the first chunks and delays the first D2H by 2.3 ms, so off)
+    {"host_hub_chunk_side", "PG_HOST_HUB_CHUNK_SIDE", 0},
 };
-static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneGemmBesideWgrad + 1,
+static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneHostHubChunkSide + 1,
               "kTuneKeys and enum TuneKeyId (pg_internal.h) must list the same keys in the same order");
 std::atomic<int64_t> g_tune[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];
 int64_t g_tune_def[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];  // $PG_<KEY> at load, else built-in
@@ -1819,17 +1824,32 @@ struct SideStream {
     cudaEvent_t fork = nullptr, join = nullptr;
 };
 
-SideStream& side_stream() {
-    static thread_local std::vector<SideStream> per_dev;
+// one side stream per (device, calling stream): two calls running
+// concurrently on different streams (the host pipeline's hub chunk beside
+// the other chunks) must not queue their hub kernels behind each other
+SideStream& side_stream(cudaStream_t caller) {
+    struct Entry {
+        int dev;
+        cudaStream_t caller;
+        SideStream ss;
+    };
+    static thread_local std::deque<Entry> per;  // stable references
     int dev = 0;
     PG_CUDA(cudaGetDevice(&dev));
-    if (static_cast<int>(per_dev.size()) <= dev) per_dev.resize(dev + 1);
-    SideStream& ss = per_dev[dev];
-    if (!ss.s) {
-        PG_CUDA(cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking));
-        PG_CUDA(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming));
-        PG_CUDA(cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming));
-    }
+    for (auto& e : per)
+        if (e.dev == dev && e.caller == caller) return e.ss;
+    // bounded: past 16 (device, stream) pairs every new caller shares the
+    // device's first side stream (still correct, only serialised)
+    int same_dev = 0;
+    for (auto& e : per) same_dev += e.dev == dev;
+    if (same_dev >= 16)
+        for (auto& e : per)
+            if (e.dev == dev) return e.ss;
+    per.push_back(Entry{dev, caller, SideStream{}});
+    SideStream& ss = per.back().ss;
+    PG_CUDA(cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking));
+    PG_CUDA(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming));
+    PG_CUDA(cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming));
     return ss;
 }
 
@@ -1941,7 +1961,7 @@ void aggregate_det(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges
     if (nh && !inline_hubs) {
         // heavy prefix of the degree order on a forked stream, concurrent
         // with the main kernel over the rest; joined back into s
-        SideStream& ss = side_stream();
+        SideStream& ss = side_stream(s);
         PG_CUDA(cudaEventRecord(ss.fork, s));
         PG_CUDA(cudaStreamWaitEvent(ss.s, ss.fork, 0));
         if (nq > 16) {

@@ -375,6 +375,7 @@ struct CopyStreams {
     // repack streams: the odd-width row repacks run beside the DMA streams,
     // so a segment's / chunk's copy never queues behind the previous repack
     cudaStream_t rup = nullptr, rdn = nullptr;
+    cudaStream_t hub = nullptr;  // the last pass's hub chunk, concurrent with the other chunks
     std::vector<cudaEvent_t> ev;  // sync events
     std::vector<cudaEvent_t> tev;  // timing events (host_trace)
     std::mutex call;              // one host-buffer call at a time per device owns them
@@ -404,6 +405,7 @@ CopyStreams& copy_streams(int device, size_t nev, std::unique_lock<std::mutex>& 
         PG_CUDA(cudaStreamCreateWithPriority(&c.d2h, cudaStreamNonBlocking, prio));
         PG_CUDA(cudaStreamCreateWithPriority(&c.rup, cudaStreamNonBlocking, prio));
         PG_CUDA(cudaStreamCreateWithPriority(&c.rdn, cudaStreamNonBlocking, prio));
+        PG_CUDA(cudaStreamCreateWithPriority(&c.hub, cudaStreamNonBlocking, prio));
     }
     while (c.ev.size() < nev) {
         cudaEvent_t e;
@@ -808,16 +810,32 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
     // Every chunk is queued before any D2H, so a host that blocks on a
     // staged (pageable) download never starves the SpMM stream.
     const bool reverse = tuning(kTuneHostChunkOrder) == 1;
+    // The hub chunk (chunk 0: the head of the degree order, latency-bound
+    // chains) on its own stream from the start of the last pass (tuning
+    // "host_hub_chunk_side"), concurrent with the others: it is ready before
+    // its turn in the D2H order instead of holding the last copy back
+    // (Reddit: the D2H sat idle 0.9 ms waiting for it)
+    const bool hub_side = reverse && cuts.size() > 2 && tuning(kTuneHostHubChunkSide) != 0 && cuts[0] < cuts[1];
+    if (hub_side) {
+        PG_CUDA(cudaEventRecord(cs.ev[0], s));
+        PG_CUDA(cudaStreamWaitEvent(cs.hub, cs.ev[0], 0));
+        run_aggregate(G, parent_indexed, cuts[0], cuts[1], din.get(), ld, dout.get(), ld, dim, last_flags, cs.hub,
+                      last);
+        PG_CUDA(cudaEventRecord(cs.ev[1 + K], cs.hub));
+        tmark(cs.hub, "chunk0");
+    }
     std::vector<size_t> order;
     for (size_t ri = 0; ri + 1 < cuts.size(); ++ri) {
         const size_t r = reverse ? cuts.size() - 2 - ri : ri;
         if (cuts[r] == cuts[r + 1]) continue;
         order.push_back(r);
+        if (hub_side && r == 0) continue;
         run_aggregate(G, parent_indexed, cuts[r], cuts[r + 1], din.get(), ld, dout.get() + cuts[r] * ld, ld, dim,
                       last_flags, s, last);
         PG_CUDA(cudaEventRecord(cs.ev[1 + K + r], s));
         tmark(s, "chunk" + std::to_string(r));
     }
+    if (hub_side) PG_CUDA(cudaStreamWaitEvent(s, cs.ev[1 + K], 0));  // s joins the hub stream
     std::unique_ptr<StagedD2H> down;
     if (out_pg) down = std::make_unique<StagedD2H>(StagedD2H{*sg, cs.d2h});
     for (const size_t r : order) {

@@ -329,7 +329,8 @@ enum TuneKeyId {
     kTuneHubInline = 32,
     kTuneHubFrontMin = 33,
     kTuneGemm3Rows = 34,
-    kTuneGemmBesideWgrad = 35
+    kTuneGemmBesideWgrad = 35,
+    kTuneHostHubChunkSide = 36
 };
 // whole-row SpMM warps (k_agg_row) for this width (tuning "row_kernel")
 bool row_kernel_on(uint64_t dim);
