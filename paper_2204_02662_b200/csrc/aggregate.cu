@@ -89,8 +89,11 @@ constexpr TuneKey kTuneKeys[] = {
     // with the other chunks (measured 25.7 vs 23.4 ms: it takes the GPU from
     // the first chunks and delays the first D2H by 2.3 ms, so off)
     {"host_hub_chunk_side", "PG_HOST_HUB_CHUNK_SIDE", 0},
+    // k_agg_vec4 wide rows: > 0 = source-window lockstep CTAs (k_agg_vec4w),
+    // the value = edges per warp per window
+    {"vec_window", "PG_VEC_WINDOW", 0},
 };
-static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneHostHubChunkSide + 1,
+static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneVecWindow + 1,
               "kTuneKeys and enum TuneKeyId (pg_internal.h) must list the same keys in the same order");
 std::atomic<int64_t> g_tune[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];
 int64_t g_tune_def[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];  // $PG_<KEY> at load, else built-in
@@ -528,6 +531,92 @@ __global__ void __launch_bounds__(256, 2) k_agg_row(const uint64_t* __restrict__
 #pragma unroll
     for (int j = 0; j < NS; ++j)
         acc_store_ext(orow + (j * 32 + lane) * 4, (j * 32 + lane) * 4, dim, acc[j], z, ext, d, row);
+}
+
+// Source-window lockstep (tuning "vec_window"): the 16 warps of a 512-thread
+// CTA are 16 consecutive (degree-sorted, similar) destinations of one column
+// chunk. They walk the CTA's source range in nwin windows, each warp taking
+// only its edges below the window end, with a CTA barrier between windows,
+// so the rows the destinations share are gathered within one window and hit
+// in L1 (32 such destinations share 31 % of their sources on Reddit layer
+// 0). Same per-column ascending-edge order: bit-identical.
+template <int U>
+__global__ void __launch_bounds__(512, 2) k_agg_vec4w(const uint64_t* __restrict__ ebeg,
+                                                     const uint64_t* __restrict__ eend,
+                                                     const Edge* __restrict__ edges,
+                                                     const uint32_t* __restrict__ order, uint32_t d_begin,
+                                                     uint64_t n_items, uint32_t chunks,
+                                                     const float* __restrict__ in, uint32_t ld_in_bytes,
+                                                     float* __restrict__ out, uint64_t ld_out, uint32_t dim,
+                                                     int accumulate, float2 zeros, uint32_t zmask, int chunk_major,
+                                                     uint32_t win_edges, AggExt ext) {
+    __shared__ uint32_t s_lo, s_hi, s_cnt;
+    const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    const uint64_t item = t >> 5;
+    const bool valid = item < n_items;
+    if (threadIdx.x == 0) {
+        s_lo = 0xffffffffu;
+        s_hi = 0u;
+        s_cnt = 0u;
+    }
+    __syncthreads();
+    const Zs z = zs_of(zeros);
+    const uint64_t nd = n_items / chunks;
+    const uint64_t nf = chunk_major > 1 ? static_cast<uint64_t>(chunk_major - 2) : 0;
+    uint32_t di = 0, ci = 0;
+    if (!chunk_major || item < nf * chunks) {
+        di = static_cast<uint32_t>(item / chunks);
+        ci = static_cast<uint32_t>(item % chunks);
+    } else {
+        const uint64_t r = item - nf * chunks, nr = nd - nf;
+        di = static_cast<uint32_t>(nf + r % nr);
+        ci = static_cast<uint32_t>(r / nr);
+    }
+    const uint32_t lane = lane_id();
+    const uint32_t d = valid ? __ldg(order + d_begin + di) : 0u;
+    const uint32_t col = (ci * 32 + lane) * 4;
+    const bool active = valid && col < dim;
+    uint64_t e = valid ? __ldg(ebeg + d) : 0, end = valid ? __ldg(eend + d) : 0;
+    if (lane == 0 && e < end) {
+        atomicMin(&s_lo, __ldg(&edges[e].x));
+        atomicMax(&s_hi, __ldg(&edges[end - 1].x));
+        atomicMax(&s_cnt, end - e < 0xffffffffull ? static_cast<uint32_t>(end - e) : 0xffffffffu);
+    }
+    const char* base = reinterpret_cast<const char*>(in) + (active ? col : ci * 128u) * 4u;
+    asm("mov.b64 %0, %0;" : "+l"(base));
+    const uint32_t row = valid ? ext_out_row(ext, d) : 0u;
+    float* orow = out + row * ld_out + col;
+    Acc acc = acc_load(orow, col, active ? dim : 0u, accumulate);
+    __syncthreads();
+    const uint32_t lo = s_lo, hi = s_hi;
+    const uint32_t nwin = s_cnt ? min(64u, max(1u, s_cnt / max(1u, win_edges))) : 0u;
+    const uint64_t span = static_cast<uint64_t>(hi) - lo + 1;
+    for (uint32_t w = 0; w < nwin; ++w) {
+        const uint64_t wend = lo + span * (w + 1) / nwin;  // exclusive
+        while (e < end) {
+            Edge ed[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) ed[u] = ld_rec(edges + e + (e + u < end ? u : 0));
+            // the window's edges are a prefix of the batch (sources ascend)
+            uint32_t n_ok = 0;
+#pragma unroll
+            for (int u = 0; u < U; ++u) n_ok += (e + u < end && ed[u].x < wend) ? 1u : 0u;
+            if (!n_ok) break;
+            float4 x[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                x[u] = u < static_cast<int>(n_ok) ? ld_row<0>(base, ed[u].x, ld_in_bytes)
+                                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+            const Zs zz = batch_dep<U>(x, z, zmask);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (u < static_cast<int>(n_ok)) acc_step(acc, __uint_as_float(ed[u].y), x[u], zz);
+            e += n_ok;
+            if (n_ok < U) break;
+        }
+        __syncthreads();
+    }
+    if (valid) acc_store_ext(orow, col, dim, acc, z, ext, d, row);
 }
 
 template <int NS>
@@ -1892,6 +1981,10 @@ void launch_vec4(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges, 
     else if (ldm == 7)
         k_agg_vec4<LPD, U, false, 7><<<grid, 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks, in, ldb, out,
                                                           ld_out, dim, accumulate, kZeros, 0u, cm, ext);
+    else if (LPD == 32 && U == 8 && tuning(kTuneVecWindow) > 0)
+        k_agg_vec4w<8><<<grid_for(items * LPD, 512), 512, 0, s>>>(
+            ebeg, eend, edges, order, d_begin, items, chunks, in, ldb, out, ld_out, dim, accumulate, kZeros, 0u, cm,
+            static_cast<uint32_t>(tuning(kTuneVecWindow)), ext);
     else if (LPD == 32 && U == 8 && tuning(kTuneVecBlock) == 1024)
         // 32 destinations of one column chunk per CTA, started together: the
         // CTA's warps walk their (degree-sorted, similar) lists in step, so

@@ -330,7 +330,8 @@ enum TuneKeyId {
     kTuneHubFrontMin = 33,
     kTuneGemm3Rows = 34,
     kTuneGemmBesideWgrad = 35,
-    kTuneHostHubChunkSide = 36
+    kTuneHostHubChunkSide = 36,
+    kTuneVecWindow = 37
 };
 // whole-row SpMM warps (k_agg_row) for this width (tuning "row_kernel")
 bool row_kernel_on(uint64_t dim);
