@@ -85,15 +85,19 @@ constexpr TuneKey kTuneKeys[] = {
     {"hub_front_min", "PG_HUB_FRONT_MIN", 0},  // hub_inline: degree threshold of the front (0 = the hub rule)
     {"gemm3_rows", "PG_GEMM3_ROWS", 8},  // k_gemm3 (gemm_packed 2): output rows per thread, 8 or 16
     {"gemm_beside_wgrad", "PG_GEMM_BESIDE_WGRAD", 1},  // backward chains: y_grad on k_gemm2 while a W' fork runs
-    // host drop-in: hub chunk of the last pass on its own stream, concurrent
-    // with the other chunks (measured 25.7 vs 23.4 ms: it takes the GPU from
-    // the first chunks and delays the first D2H by 2.3 ms, so off)
+    // host drop-in last pass: 1 = the hub rows (degree >= host_hub_min) of
+    // every chunk first on their own stream, 2 = the whole hub chunk on its
+    // own stream, 0 = off. Measured (profiles/e2e_hub_split_sweep_r02.log):
+    // 27.2 / 25.7 vs 23.2 ms — latency-bound hub chains run 2.5x slower
+    // beside the other chunks than alone, so the split costs more than the
+    // 0.9 ms of D2H idle it was to remove
     {"host_hub_chunk_side", "PG_HOST_HUB_CHUNK_SIDE", 0},
     // k_agg_vec4 wide rows: > 0 = source-window lockstep CTAs (k_agg_vec4w),
     // the value = edges per warp per window
     {"vec_window", "PG_VEC_WINDOW", 0},
+    {"host_hub_min", "PG_HOST_HUB_MIN", 16384},  // host_hub_chunk_side 1: degree of the hub rows split off
 };
-static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneVecWindow + 1,
+static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneHostHubMin + 1,
               "kTuneKeys and enum TuneKeyId (pg_internal.h) must list the same keys in the same order");
 std::atomic<int64_t> g_tune[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];
 int64_t g_tune_def[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];  // $PG_<KEY> at load, else built-in
@@ -1936,7 +1940,9 @@ SideStream& side_stream(cudaStream_t caller) {
             if (e.dev == dev) return e.ss;
     per.push_back(Entry{dev, caller, SideStream{}});
     SideStream& ss = per.back().ss;
-    PG_CUDA(cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking));
+    int prio = 0;  // the caller's priority (a high-priority caller's hubs stay high)
+    if (caller) PG_CUDA(cudaStreamGetPriority(caller, &prio));
+    PG_CUDA(cudaStreamCreateWithPriority(&ss.s, cudaStreamNonBlocking, prio));
     PG_CUDA(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming));
     PG_CUDA(cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming));
     return ss;

@@ -207,6 +207,26 @@ uint32_t auto_src_segments(uint64_t P, uint64_t D, uint64_t E, uint64_t dim) {
 // Core launch over the grouping's base: which edge stream and which schedule.
 }  // namespace
 
+// degree-ordered schedule of path rows [rb, re) of a grouping (cached; the
+// caller holds G.mu)
+Groups::RowSched* pg::row_sched(Groups& G, uint32_t rb, uint32_t re) {
+    Path& p = *G.path;
+    for (auto& x : G.row_scheds)
+        if (x.rb == rb && x.re == re) return &x;
+    G.row_scheds.emplace_back();
+    Groups::RowSched* rs = &G.row_scheds.back();
+    rs->rb = rb;
+    rs->re = re;
+    degree_order(p.offsets.get() + rb, re - rb, rs->order, lib_stream(p.device), &rs->hist);
+    return rs;
+}
+
+// destinations of a row range with degree >= min_degree (a prefix of its
+// degree order)
+uint32_t pg::range_heavy(Groups& G, uint32_t rb, uint32_t re, uint64_t min_degree) {
+    return row_sched(G, rb, re)->hist.heavy(min_degree);
+}
+
 void pg::run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re, const float* in, uint64_t ld_in,
                    float* out, uint64_t ld_out, uint64_t dim, unsigned flags, cudaStream_t s, SegSel sel,
                    const AggExt& ext, const Edge* edges_override) {
@@ -319,21 +339,24 @@ void pg::run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re,
             return;
         }
         // row range: schedule of rows [rb, re) relative to rb (cached)
-        Groups::RowSched* rs = nullptr;
-        for (auto& x : G.row_scheds)
-            if (x.rb == rb && x.re == re) rs = &x;
-        if (!rs) {
-            G.row_scheds.emplace_back();
-            rs = &G.row_scheds.back();
-            rs->rb = rb;
-            rs->re = re;
-            degree_order(p.offsets.get() + rb, re - rb, rs->order, lib_stream(p.device), &rs->hist);
-        }
+        Groups::RowSched* rs = row_sched(G, rb, re);
         AggExt er = ext;
         er.side_hubs = true;  // a row range: hub chains on the deeper-pipelined side kernel
-        aggregate_det(eb + rb, ee + rb, edges, rs->order.get(), re - rb, 0, re - rb,
-                      rs->hist.heavy(heavy_degree(dim, rs->hist.edges / range_div)), in, ld_in, out, ld_out, dim,
-                      accumulate, s, er);
+        const uint32_t nh = rs->hist.heavy(heavy_degree(dim, rs->hist.edges / range_div));
+        const uint32_t nd = re - rb;
+        if (ext.part) {
+            const uint32_t np = std::min(rs->hist.heavy(std::max<uint64_t>(1, ext.part_min_degree)), nd);
+            if (ext.part == 1) {  // the hub prefix only, all of it on the side kernel
+                if (np) aggregate_det(eb + rb, ee + rb, edges, rs->order.get(), nd, 0, np, np, in, ld_in, out, ld_out,
+                                      dim, accumulate, s, er);
+            } else if (np < nd) {  // the rest; its own heavy ones (past the prefix) still on the side kernel
+                aggregate_det(eb + rb, ee + rb, edges, rs->order.get(), nd, np, nd, nh > np ? nh - np : 0, in, ld_in,
+                              out, ld_out, dim, accumulate, s, er);
+            }
+            return;
+        }
+        aggregate_det(eb + rb, ee + rb, edges, rs->order.get(), nd, 0, nd, nh, in, ld_in, out, ld_out, dim, accumulate,
+                      s, er);
         return;
     }
     Graph& g = *G.graph;
@@ -718,7 +741,7 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
     std::unique_lock<std::mutex> cs_lock;
     // sync events: 1 + K + R + 1 used; trace events: up to 1 + K + (K - F)
     // + 2 R (start, uploads, whole passes, chunks, downloads)
-    CopyStreams& cs = copy_streams(G.device, 4 + 2 * K + 2 * R, cs_lock);
+    CopyStreams& cs = copy_streams(G.device, 4 + 2 * K + 3 * R, cs_lock);
     size_t nt = 0;  // trace events used
     auto mark = [&](cudaStream_t st) {
         if (trace && nt < cs.tev.size()) PG_CUDA(cudaEventRecord(cs.tev[nt++], st));
@@ -810,15 +833,42 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
     // Every chunk is queued before any D2H, so a host that blocks on a
     // staged (pageable) download never starves the SpMM stream.
     const bool reverse = tuning(kTuneHostChunkOrder) == 1;
-    // The hub chunk (chunk 0: the head of the degree order, latency-bound
-    // chains) on its own stream from the start of the last pass (tuning
-    // "host_hub_chunk_side"), concurrent with the others: it is ready before
-    // its turn in the D2H order instead of holding the last copy back
-    // (Reddit: the D2H sat idle 0.9 ms waiting for it)
-    const bool hub_side = reverse && cuts.size() > 2 && tuning(kTuneHostHubChunkSide) != 0 && cuts[0] < cuts[1];
-    if (hub_side) {
+    // Hub split (tuning "host_hub_chunk_side" = 1): the hub prefix of every
+    // chunk's degree order (latency-bound chains, a handful of small CTAs on
+    // the side kernel) goes first on its own stream; the rest of each chunk
+    // runs on s. A chunk's D2H waits for its own part on s and, only when it
+    // has hubs, for its hub part. The chunks without hubs (the low-degree
+    // tail, copied first) no longer queue behind the hub chains, and the hub
+    // chunk is finished long before its turn in the D2H order.
+    // Mode 2: the whole hub chunk (chunk 0) on its own stream instead.
+    const int hub_mode = reverse && cuts.size() > 2 ? static_cast<int>(tuning(kTuneHostHubChunkSide)) : 0;
+    std::vector<uint32_t> nh(cuts.size() - 1, 0);
+    bool any_hub = false;
+    const uint64_t hub_min = static_cast<uint64_t>(std::max<int64_t>(1, tuning(kTuneHostHubMin)));
+    if (hub_mode == 1) {
+        for (size_t r = 0; r + 1 < cuts.size(); ++r) {
+            if (cuts[r] == cuts[r + 1]) continue;
+            nh[r] = range_heavy(G, cuts[r], cuts[r + 1], hub_min);
+            any_hub |= nh[r] > 0;
+        }
+    }
+    cudaEvent_t* ev_hub = cs.ev.data() + 2 + 2 * K + 2 * R;  // per chunk: its hub part done
+    if (any_hub || hub_mode == 2) {
         PG_CUDA(cudaEventRecord(cs.ev[0], s));
         PG_CUDA(cudaStreamWaitEvent(cs.hub, cs.ev[0], 0));
+    }
+    if (any_hub) {
+        for (size_t r = 0; r + 1 < cuts.size(); ++r) {  // destination order: the real hubs first
+            if (!nh[r]) continue;
+            AggExt hx;
+            hx.part = 1;
+            hx.part_min_degree = hub_min;
+            run_aggregate(G, parent_indexed, cuts[r], cuts[r + 1], din.get(), ld, dout.get() + cuts[r] * ld, ld, dim,
+                          last_flags, cs.hub, last, hx);
+            PG_CUDA(cudaEventRecord(ev_hub[r], cs.hub));
+        }
+        tmark(cs.hub, "hubs");
+    } else if (hub_mode == 2 && cuts[0] < cuts[1]) {
         run_aggregate(G, parent_indexed, cuts[0], cuts[1], din.get(), ld, dout.get(), ld, dim, last_flags, cs.hub,
                       last);
         PG_CUDA(cudaEventRecord(cs.ev[1 + K], cs.hub));
@@ -829,18 +879,28 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
         const size_t r = reverse ? cuts.size() - 2 - ri : ri;
         if (cuts[r] == cuts[r + 1]) continue;
         order.push_back(r);
-        if (hub_side && r == 0) continue;
+        if (hub_mode == 2 && !any_hub && r == 0) continue;
+        AggExt cx;
+        cx.part = any_hub && nh[r] ? 2 : 0;
+        cx.part_min_degree = hub_min;
         run_aggregate(G, parent_indexed, cuts[r], cuts[r + 1], din.get(), ld, dout.get() + cuts[r] * ld, ld, dim,
-                      last_flags, s, last);
+                      last_flags, s, last, cx);
         PG_CUDA(cudaEventRecord(cs.ev[1 + K + r], s));
         tmark(s, "chunk" + std::to_string(r));
     }
-    if (hub_side) PG_CUDA(cudaStreamWaitEvent(s, cs.ev[1 + K], 0));  // s joins the hub stream
+    if (any_hub || hub_mode == 2) {  // s joins the hub stream (buffers are freed on s)
+        PG_CUDA(cudaEventRecord(cs.ev[0], cs.hub));
+        PG_CUDA(cudaStreamWaitEvent(s, cs.ev[0], 0));
+    }
     std::unique_ptr<StagedD2H> down;
     if (out_pg) down = std::make_unique<StagedD2H>(StagedD2H{*sg, cs.d2h});
     for (const size_t r : order) {
         const uint32_t rb = cuts[r], re = cuts[r + 1];
         PG_CUDA(cudaStreamWaitEvent(cs.d2h, cs.ev[1 + K + r], 0));
+        if (any_hub && nh[r]) {  // the chunk's hub rows come from the hub stream
+            PG_CUDA(cudaStreamWaitEvent(cs.d2h, ev_hub[r], 0));
+            PG_CUDA(cudaStreamWaitEvent(cs.rdn, ev_hub[r], 0));
+        }
         if (!dim) continue;
         const float* src = dout.get() + rb * ld;
         if (!packed && pitch2d && !down) {

@@ -236,6 +236,10 @@ struct AggExt {
     // when tuning hub_inline is on (row ranges: a host-pipeline chunk or a
     // shard is short, and its hub chains would set its length)
     bool side_hubs = false;
+    // scheduling only, row ranges: 0 every destination, 1 only the hub
+    // prefix of the range's degree order, 2 all but that prefix
+    int part = 0;
+    uint64_t part_min_degree = 0;  // the hub prefix of part 1 / 2: degree >= this
     bool any() const { return out_rows || relu_pre || src_bits || dst_bits; }
 };
 
@@ -261,6 +265,10 @@ struct SegSel {
 // graph: vertex ids), destination rows [rb, re) with their cached degree
 // schedule; flags = PG_AGG_* of the C ABI. edges_override replaces the
 // path's edge stream (same destinations and order, other source ids).
+// degree-ordered schedule of path rows [rb, re) (cached on the grouping;
+// caller holds G.mu) and the hub count of that range's SpMM call
+Groups::RowSched* row_sched(Groups& G, uint32_t rb, uint32_t re);
+uint32_t range_heavy(Groups& G, uint32_t rb, uint32_t re, uint64_t min_degree);
 void run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re, const float* in, uint64_t ld_in,
                    float* out, uint64_t ld_out, uint64_t dim, unsigned flags, cudaStream_t s, SegSel sel = {},
                    const AggExt& ext = AggExt{}, const Edge* edges_override = nullptr);
@@ -331,7 +339,8 @@ enum TuneKeyId {
     kTuneGemm3Rows = 34,
     kTuneGemmBesideWgrad = 35,
     kTuneHostHubChunkSide = 36,
-    kTuneVecWindow = 37
+    kTuneVecWindow = 37,
+    kTuneHostHubMin = 38
 };
 // whole-row SpMM warps (k_agg_row) for this width (tuning "row_kernel")
 bool row_kernel_on(uint64_t dim);

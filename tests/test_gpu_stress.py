@@ -95,7 +95,8 @@ HOST_KNOBS = {
     "host_last_seg_pct": (0, 30, 40, 70),
     "host_chunks": (1, 3, 8, 16),
     "host_chunk_order": (0, 1),
-    "host_hub_chunk_side": (0, 1),
+    "host_hub_chunk_side": (0, 1, 2),
+    "host_hub_min": (1, 64, 16384),
 }
 
 
