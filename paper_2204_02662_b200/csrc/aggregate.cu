@@ -96,8 +96,9 @@ constexpr TuneKey kTuneKeys[] = {
     // the value = edges per warp per window
     {"vec_window", "PG_VEC_WINDOW", 0},
     {"host_hub_min", "PG_HOST_HUB_MIN", 16384},  // host_hub_chunk_side 1: degree of the hub rows split off
+    {"grouped_src_segs", "PG_GROUPED_SRC_SEGS", 1},  // grouped Fast (k_agg_grp): L2-sized source segments for wide rows
 };
-static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneHostHubMin + 1,
+static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneGroupedSrcSegs + 1,
               "kTuneKeys and enum TuneKeyId (pg_internal.h) must list the same keys in the same order");
 std::atomic<int64_t> g_tune[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];
 int64_t g_tune_def[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];  // $PG_<KEY> at load, else built-in
@@ -1538,7 +1539,9 @@ __global__ void __launch_bounds__(256, 4) k_agg_grp(const uint4* __restrict__ ra
                                                    const float* __restrict__ in, uint32_t ld_in_bytes,
                                                    float* __restrict__ out, uint64_t ld_out, uint32_t dim,
                                                    int accumulate, float* __restrict__ scratch, uint64_t ld_scr,
-                                                   float2 zeros, uint32_t zmask) {
+                                                   float2 zeros, uint32_t zmask,
+                                                   const uint64_t* __restrict__ seg_lo,
+                                                   const uint64_t* __restrict__ seg_hi) {
     constexpr int W = grp_workers<LPD>();
     constexpr int GCAP = grp_gcap<LPD>();
     extern __shared__ __align__(128) unsigned char smem[];
@@ -1562,9 +1565,15 @@ __global__ void __launch_bounds__(256, 4) k_agg_grp(const uint4* __restrict__ ra
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     for (uint32_t lg = tid; lg < ng; lg += 256) {
-        sgb[lg] = static_cast<uint32_t>(__ldg(gbeg + g0 + lg) - ebase);
-        sge[lg] = static_cast<uint32_t>(__ldg(gend + g0 + lg) - ebase);
-        sdst[lg] = __ldg(gdest + g0 + lg);
+        uint64_t gb = __ldg(gbeg + g0 + lg), ge = __ldg(gend + g0 + lg);
+        const uint32_t dd = __ldg(gdest + g0 + lg);
+        if (seg_lo) {  // an L2-sized source segment: the group's part of it (maybe empty)
+            gb = max(gb, __ldg(seg_lo + dd));
+            ge = max(gb, min(ge, __ldg(seg_hi + dd)));
+        }
+        sgb[lg] = static_cast<uint32_t>(gb - ebase);
+        sge[lg] = static_cast<uint32_t>(ge - ebase);
+        sdst[lg] = dd;
     }
     __syncthreads();
     if (staged) {
@@ -1817,7 +1826,8 @@ void build_grp_sched(const uint64_t* offsets_dev, uint32_t D, uint32_t gs, uint3
 
 template <int LPD>
 void launch_grp(Groups& G, const Groups::GrpSched& sc, const Edge* edges, uint32_t chunks, const float* in,
-                uint64_t ld_in, float* out, uint64_t ld_out, uint32_t dim, bool accumulate, cudaStream_t s) {
+                uint64_t ld_in, float* out, uint64_t ld_out, uint32_t dim, bool accumulate, cudaStream_t s,
+                const uint64_t* seg_lo, const uint64_t* seg_hi) {
     static std::mutex mu;
     static std::vector<char> attr;
     constexpr size_t smem = grp_smem<LPD>();
@@ -1837,7 +1847,8 @@ void launch_grp(Groups& G, const Groups::GrpSched& sc, const Edge* edges, uint32
     if (sc.nranges) {
         k_agg_grp<LPD, 8><<<sc.nranges * chunks, 256, smem, s>>>(
             sc.ranges.get(), sc.nranges, G.gbegin.get(), G.gend.get(), G.gdest.get(), edges, in,
-            static_cast<uint32_t>(ld_in * 4), out, ld_out, dim, accumulate, scratch.get(), ld_scr, kZeros, 0u);
+            static_cast<uint32_t>(ld_in * 4), out, ld_out, dim, accumulate, scratch.get(), ld_scr, kZeros, 0u, seg_lo,
+            seg_hi);
         PG_LAUNCH("k_agg_grp");
     }
     const uint64_t fix = static_cast<uint64_t>(sc.nhubs + (accumulate ? 0 : sc.nempty)) * chunks;
@@ -2176,7 +2187,8 @@ void aggregate_groups(const uint64_t* gbeg, const uint64_t* gend, const uint32_t
 }
 
 void aggregate_groups_af(Groups& G, const uint64_t* offsets_dev, uint32_t D, const Edge* edges, const float* in,
-                         uint64_t ld_in, float* out, uint64_t ld_out, uint64_t dim, bool accumulate, cudaStream_t s) {
+                         uint64_t ld_in, float* out, uint64_t ld_out, uint64_t dim, bool accumulate, cudaStream_t s,
+                         const uint64_t* seg_lo, const uint64_t* seg_hi) {
     if (dim == 0 || D == 0) return;
     const bool vec = (ld_in % 4 == 0) && (ld_out % 4 == 0) && (reinterpret_cast<uintptr_t>(in) % 16 == 0) &&
                      (reinterpret_cast<uintptr_t>(out) % 16 == 0) && ld_in >= ((dim + 3) & ~3ull) &&
@@ -2195,10 +2207,11 @@ void aggregate_groups_af(Groups& G, const uint64_t* offsets_dev, uint32_t D, con
         build_grp_sched(offsets_dev, D, G.gs, workers, *sc, lib_stream(G.device));
     }
     const uint32_t chunks = lpd == 32 ? (nq + 31) / 32 : 1;
-    if (lpd == 32) launch_grp<32>(G, *sc, edges, chunks, in, ld_in, out, ld_out, dim32, accumulate, s);
-    else if (lpd == 16) launch_grp<16>(G, *sc, edges, chunks, in, ld_in, out, ld_out, dim32, accumulate, s);
-    else if (lpd == 8) launch_grp<8>(G, *sc, edges, chunks, in, ld_in, out, ld_out, dim32, accumulate, s);
-    else launch_grp<4>(G, *sc, edges, chunks, in, ld_in, out, ld_out, dim32, accumulate, s);
+    if (lpd == 32) launch_grp<32>(G, *sc, edges, chunks, in, ld_in, out, ld_out, dim32, accumulate, s, seg_lo, seg_hi);
+    else if (lpd == 16)
+        launch_grp<16>(G, *sc, edges, chunks, in, ld_in, out, ld_out, dim32, accumulate, s, seg_lo, seg_hi);
+    else if (lpd == 8) launch_grp<8>(G, *sc, edges, chunks, in, ld_in, out, ld_out, dim32, accumulate, s, seg_lo, seg_hi);
+    else launch_grp<4>(G, *sc, edges, chunks, in, ld_in, out, ld_out, dim32, accumulate, s, seg_lo, seg_hi);
 }
 
 void aggregate_f64(const uint64_t* offsets, const uint32_t* src, uint32_t src_stride, const double* w,

@@ -227,6 +227,37 @@ uint32_t pg::range_heavy(Groups& G, uint32_t rb, uint32_t re, uint64_t min_degre
     return row_sched(G, rb, re)->hist.heavy(min_degree);
 }
 
+namespace {
+// Per-destination bounds of K L2-sized source segments of a path (cached on
+// the grouping): cuts at equal source rows (tuning src_seg_balance 0,
+// default) or rows weighted by edge count (100), a percentage mix.
+void auto_segment_bounds(Groups& G, Path& p, uint32_t K) {
+    const int64_t bal = std::clamp<int64_t>(tuning(kTuneSrcSegBalance), 0, 100);
+    if (G.auto_seg_k == K && G.auto_seg_bal == bal) return;
+    std::vector<uint64_t> cuts(K + 1);
+    for (uint32_t k = 0; k <= K; ++k) cuts[k] = static_cast<uint64_t>(p.P) * k / K;
+    if (bal > 0) {
+        cudaStream_t ls = lib_stream(p.device);
+        DevBuf<uint32_t> cnt(p.P, ls);
+        source_edge_counts(p.edges_parent.get(), p.E, p.P, cnt.get(), ls);
+        std::vector<uint32_t> hc(p.P);
+        PG_CUDA(cudaMemcpyAsync(hc.data(), cnt.get(), p.P * 4ull, cudaMemcpyDeviceToHost, ls));
+        PG_CUDA(cudaStreamSynchronize(ls));
+        const double tot = static_cast<double>(p.E) * bal / 100.0 + static_cast<double>(p.P) * (100 - bal) / 100.0;
+        double acc = 0;
+        uint32_t k = 1;
+        for (uint64_t r = 0; r < p.P && k < K; ++r) {
+            acc += hc[r] * (bal / 100.0) + (100 - bal) / 100.0;
+            while (k < K && acc >= tot * k / K) cuts[k++] = r + 1;
+        }
+        for (uint32_t j = 1; j <= K; ++j) cuts[j] = std::max(cuts[j], cuts[j - 1]);
+    }
+    segment_bounds(p.offsets.get(), p.edges_parent.get(), p.D, cuts.data(), K, G.auto_seg_bnd, lib_stream(p.device));
+    G.auto_seg_k = K;
+    G.auto_seg_bal = bal;
+}
+}  // namespace
+
 void pg::run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re, const float* in, uint64_t ld_in,
                    float* out, uint64_t ld_out, uint64_t dim, unsigned flags, cudaStream_t s, SegSel sel,
                    const AggExt& ext, const Edge* edges_override) {
@@ -259,9 +290,28 @@ void pg::run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re,
         // tuning "grouped_seg": 0 (default) = atomic-free k_agg_grp + hub
         // fixup; 1 = the CTA-segmented kernel with atomics at CTA edges;
         // 2 = one atomic commit per extra group (the reference's omp atomic)
-        if (tuning(kTuneGroupedSeg) == 0)
-            aggregate_groups_af(G, b.offsets, b.D, edges, in, ld_in, out, ld_out, dim, accumulate, s);
-        else
+        if (tuning(kTuneGroupedSeg) == 0) {
+            // L2-sized source segments for wide rows, like the Deterministic
+            // path (tuning grouped_src_segs): each pass takes every group's
+            // part of one segment. Partials per segment re-associate the sum
+            // further, inside Fast mode's tolerance like its per-group partials.
+            // (groups below 32 edges lose: each pass re-stages whole windows
+            // for little work per group; Reddit layer 0 gs 8: 38 -> 58 ms,
+            // gs 128: 22.3 -> 20.5 ms)
+            const uint32_t K = G.path && parent_indexed && !G.edges_remap.get() && !edges_override &&
+                                       tuning(kTuneGroupedSrcSegs) && G.gs >= 32
+                                   ? auto_src_segments(G.path->P, G.path->D, G.path->E, dim)
+                                   : 1;
+            if (K > 1) {
+                auto_segment_bounds(G, *G.path, K);
+                for (uint32_t k = 0; k < K; ++k)
+                    aggregate_groups_af(G, b.offsets, b.D, edges, in, ld_in, out, ld_out, dim, accumulate || k > 0, s,
+                                        G.auto_seg_bnd.get() + static_cast<uint64_t>(k) * b.D,
+                                        G.auto_seg_bnd.get() + static_cast<uint64_t>(k + 1) * b.D);
+            } else {
+                aggregate_groups_af(G, b.offsets, b.D, edges, in, ld_in, out, ld_out, dim, accumulate, s);
+            }
+        } else
             aggregate_groups(G.gbegin.get(), G.gend.get(), G.gdest.get(), G.dest_groups.get(), b.D, G.G, edges, in,
                              ld_in, out, ld_out, dim, accumulate, s);
         return;
@@ -284,34 +334,7 @@ void pg::run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re,
         if (sel.seg < 0 && parent_indexed && !G.edges_remap.get() && !edges_override) {
             const uint32_t K = auto_src_segments(p.P, p.D, p.E, dim);
             if (K > 1) {
-                // cuts: equal source rows (tuning src_seg_balance 0, default) or
-                // rows weighted by edge count (100): a percentage mix
-                const int64_t bal = std::clamp<int64_t>(tuning(kTuneSrcSegBalance), 0, 100);
-                if (G.auto_seg_k != K || G.auto_seg_bal != bal) {
-                    std::vector<uint64_t> cuts(K + 1);
-                    for (uint32_t k = 0; k <= K; ++k) cuts[k] = static_cast<uint64_t>(p.P) * k / K;
-                    if (bal > 0) {
-                        cudaStream_t ls = lib_stream(p.device);
-                        DevBuf<uint32_t> cnt(p.P, ls);
-                        source_edge_counts(p.edges_parent.get(), p.E, p.P, cnt.get(), ls);
-                        std::vector<uint32_t> hc(p.P);
-                        PG_CUDA(cudaMemcpyAsync(hc.data(), cnt.get(), p.P * 4ull, cudaMemcpyDeviceToHost, ls));
-                        PG_CUDA(cudaStreamSynchronize(ls));
-                        const double tot = static_cast<double>(p.E) * bal / 100.0 +
-                                           static_cast<double>(p.P) * (100 - bal) / 100.0;
-                        double acc = 0;
-                        uint32_t k = 1;
-                        for (uint64_t r = 0; r < p.P && k < K; ++r) {
-                            acc += hc[r] * (bal / 100.0) + (100 - bal) / 100.0;
-                            while (k < K && acc >= tot * k / K) cuts[k++] = r + 1;
-                        }
-                        for (uint32_t j = 1; j <= K; ++j) cuts[j] = std::max(cuts[j], cuts[j - 1]);
-                    }
-                    segment_bounds(p.offsets.get(), p.edges_parent.get(), p.D, cuts.data(), K, G.auto_seg_bnd,
-                                   lib_stream(p.device));
-                    G.auto_seg_k = K;
-                    G.auto_seg_bal = bal;
-                }
+                auto_segment_bounds(G, p, K);
                 for (uint32_t k = 0; k < K; ++k) {
                     AggExt ek = ext;
                     if (k + 1 < K) ek.relu_pre = nullptr;  // the epilogue applies to finished rows only

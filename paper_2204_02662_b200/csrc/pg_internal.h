@@ -292,8 +292,11 @@ void record_error(const Error& e);
 // The atomic-free group-partitioned Fast aggregation (default for
 // PG_AGG_GROUPED): builds / reuses G's schedule for this width, then the
 // main kernel and the hub fixup.
+// seg_lo / seg_hi (per destination, optional): only each group's edges in
+// [seg_lo[d], seg_hi[d]) — one L2-sized source segment pass
 void aggregate_groups_af(Groups& G, const uint64_t* offsets_dev, uint32_t D, const Edge* edges, const float* in,
-                         uint64_t ld_in, float* out, uint64_t ld_out, uint64_t dim, bool accumulate, cudaStream_t s);
+                         uint64_t ld_in, float* out, uint64_t ld_out, uint64_t dim, bool accumulate, cudaStream_t s,
+                         const uint64_t* seg_lo = nullptr, const uint64_t* seg_hi = nullptr);
 
 // PG_HEAVY_MIN_DEG / pg_set_heavy_min_degree (0 disables; UINT64_MAX restores
 // the width-dependent default)
@@ -340,7 +343,8 @@ enum TuneKeyId {
     kTuneGemmBesideWgrad = 35,
     kTuneHostHubChunkSide = 36,
     kTuneVecWindow = 37,
-    kTuneHostHubMin = 38
+    kTuneHostHubMin = 38,
+    kTuneGroupedSrcSegs = 39
 };
 // whole-row SpMM warps (k_agg_row) for this width (tuning "row_kernel")
 bool row_kernel_on(uint64_t dim);

@@ -136,3 +136,36 @@ def test_grouped_atomic_free_hubs_and_determinism(pg, orc, cuda, dim):
         assert (err <= 1e-6 + 1e-5 * absum).all(), (gs, float((err / (1e-6 + 1e-5 * absum)).max()))
         if gs >= p.max_degree:
             assert np.array_equal(runs[0].view(np.uint32), det.cpu().numpy().view(np.uint32))
+
+
+@pytest.mark.parametrize("dim", [41, 602])
+def test_grouped_source_segments_within_tolerance(pg, orc, cuda, dim):
+    """The atomic-free grouped kernel over L2-sized source segments (tuning
+    grouped_src_segs, forced here with src_segs = 3): each pass takes every
+    group's part of one segment and adds its partials to the output — a
+    further re-association, still inside the Fast-mode bound."""
+    import torch
+
+    g, paths, og, ops = setup(pg, orc, m=60000)
+    try:
+        pg.set_tuning("src_segs", 3)
+        for p, op in zip(paths, ops):
+            y = np.random.default_rng(dim + 5).uniform(-1, 1, size=(p.P, dim)).astype(np.float32)
+            yd = pg.empty_rows(p.P, dim)
+            yd.copy_(torch.from_numpy(y))
+            yu = y[op.srcpos]
+            want64 = orc.aggregate_pull_f64(op.offsets, op.neighbors, op.weights, yu.astype(np.float64))
+            absum = orc.aggregate_pull_f64(op.offsets, op.neighbors, np.abs(op.weights),
+                                           np.abs(yu).astype(np.float64))
+            for gs in (32, 64, max(p.max_degree, 32)):
+                for segs in (1, 0):
+                    pg.set_tuning("grouped_src_segs", segs)
+                    x = pg.empty_rows(p.D, dim)
+                    x.fill_(7.0)
+                    pg.backward_aggregation(pg.group_neighbors(p, gs), yd, x, mode=pg.GROUPED, overwrite=True)
+                    torch.cuda.synchronize()
+                    err = np.abs(x.cpu().numpy().astype(np.float64) - want64)
+                    assert (err <= 1e-6 + 1e-5 * absum).all(), (gs, segs, dim, float(err.max()))
+    finally:
+        pg.set_tuning("src_segs")
+        pg.set_tuning("grouped_src_segs")
