@@ -97,8 +97,12 @@ constexpr TuneKey kTuneKeys[] = {
     {"vec_window", "PG_VEC_WINDOW", 0},
     {"host_hub_min", "PG_HOST_HUB_MIN", 16384},  // host_hub_chunk_side 1: degree of the hub rows split off
     {"grouped_src_segs", "PG_GROUPED_SRC_SEGS", 1},  // grouped Fast (k_agg_grp): L2-sized source segments for wide rows
+    {"narrow_u", "PG_NARROW_U", 8},  // rows <= 16 floats: edges per gather batch of a 4-lane destination (8, 16)
+    // W' split GEMM copy warp: 0 = a row per lane, 4 slots / 2 in flight;
+    // 1 = the same 7 / 5; 2 = lanes sharing rows (fewer L1 wavefronts)
+    {"atb_depth", "PG_ATB_DEPTH", 0},
 };
-static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneGroupedSrcSegs + 1,
+static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneAtbDepth + 1,
               "kTuneKeys and enum TuneKeyId (pg_internal.h) must list the same keys in the same order");
 std::atomic<int64_t> g_tune[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];
 int64_t g_tune_def[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];  // $PG_<KEY> at load, else built-in
@@ -2158,6 +2162,8 @@ void aggregate_det(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges
         launch_vec4<16, 8>(ebeg, eend, edges, order, d_begin, nd, 1, in, ld_in, out, ld_out, dim32, accumulate, s, ext);
     } else if (nq > 4) {
         launch_vec4<8, 8>(ebeg, eend, edges, order, d_begin, nd, 1, in, ld_in, out, ld_out, dim32, accumulate, s, ext);
+    } else if (tuning(kTuneNarrowU) == 16) {
+        launch_vec4<4, 16>(ebeg, eend, edges, order, d_begin, nd, 1, in, ld_in, out, ld_out, dim32, accumulate, s, ext);
     } else {
         launch_vec4<4, 8>(ebeg, eend, edges, order, d_begin, nd, 1, in, ld_in, out, ld_out, dim32, accumulate, s, ext);
     }

@@ -444,20 +444,25 @@ __global__ void __launch_bounds__(32) k_gemm_at_b_w(const float* __restrict__ a,
 // Copy warp + chain warp variant (tuning "atb_split", default): warp 1
 // issues every cp.async of a 64-row stage (2 rows per lane, the same 16-byte
 // copies and id pipeline as above) and warp 0 only walks the chains
-// (LDS a + LDS.64 b + FFMA2 + FADD2 per row); kAtbSlots stage slots are
+// (LDS a + LDS.64 b + FFMA2 + FADD2 per row); SL stage slots are
 // handed over with named barriers (FULL: copy warp waits for its group and
 // arrives; EMPTY: chain warp arrives after reading). 64-row stages keep
 // the barrier cost per row small.
-constexpr int kAtbSlots = 4, kAtbLag = 2, kAtbKC = 64;
+// SL slots, LAG stages in flight ahead of the chain warp (tuning
+// "atb_depth": 0 = 4 / 2, 1 = 7 / 5). A block's copy pipeline is its
+// memory-level parallelism: LAG x 64 gathered rows per latency. At 4 / 2 the
+// products layer-0 W' (1.2M rows per chain) ran at ~34 cycles per row, the
+// 128 rows in flight per block over a ~1 us gather latency.
+constexpr int kAtbKC = 64;
 
 // TI A columns x TC B columns per block; CH A columns per lane (CH = 2:
 // 128 chains per block for shapes with more chains than SMs)
-template <int TI, int CH>
+template <int TI, int CH, int SL, int LAG>
 struct AtbSplitSmem {
     static constexpr int TC = 2 * 32 / (TI / CH);
-    float sa[kAtbSlots][kAtbKC][TI];
-    float sb[kAtbSlots][kAtbKC][TC];
-    uint32_t sid[kAtbLag + 2][kAtbKC];
+    float sa[SL][kAtbKC][TI];
+    float sb[SL][kAtbKC][TC];
+    uint32_t sid[LAG + 2][kAtbKC];
 };
 
 __device__ __forceinline__ void named_sync(int id, int count) {
@@ -467,13 +472,13 @@ __device__ __forceinline__ void named_arrive(int id, int count) {
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
-template <int TI, int V, int CH>
+template <int TI, int V, int CH, int SL = 4, int LAG = 2, bool kAtbCoopCopy = false>
 __global__ void __launch_bounds__(64) k_gemm_at_b_split(const float* __restrict__ a, uint64_t lda,
                                                        const uint32_t* __restrict__ rows, const float* __restrict__ b,
                                                        uint64_t ldb, float* __restrict__ out, uint64_t ldo,
                                                        uint32_t n, uint32_t r, uint32_t c, float nz) {
-    using Sm = AtbSplitSmem<TI, CH>;
-    constexpr int LPI = 32 / (TI / CH), TC = Sm::TC, KC = kAtbKC, SL = kAtbSlots, LAG = kAtbLag, NI = LAG + 2;
+    using Sm = AtbSplitSmem<TI, CH, SL, LAG>;
+    constexpr int LPI = 32 / (TI / CH), TC = Sm::TC, KC = kAtbKC, NI = LAG + 2;
     constexpr int AV = (V == 4 && TI % 4 == 0) ? 4 : 1;
     constexpr int BV = V == 4 ? 4 : 1;
     constexpr int NA = TI / AV, NB = TC / BV;
@@ -552,6 +557,33 @@ __global__ void __launch_bounds__(64) k_gemm_at_b_split(const float* __restrict_
         if (ts < ntiles) {
             if (ts >= static_cast<uint32_t>(SL)) named_sync(empty_bar(ts), 64);
             const int slot = ts % SL;
+            if (kAtbCoopCopy) {
+                // lanes share rows: a warp-wide copy touches 32 / NA (A) and
+                // 32 / NB (B) rows instead of 32 — one L1 wavefront per row
+                // line, 3x fewer than one row per lane
+                const bool tail = ts * KC + KC > n;
+#pragma unroll
+                for (int q = lane; q < KC * NA; q += 32) {
+                    const int kk = q / NA, qa = q % NA;
+                    const bool out_row = tail && ts * KC + kk >= n;
+                    uint32_t id;
+                    if (!rows)
+                        id = ts * KC + kk;
+                    else if (ts <= static_cast<uint32_t>(LAG))
+                        id = fetch_id(ts, kk);
+                    else
+                        id = sm.sid[ts % NI][kk];
+                    const float* ar = out_row ? a : a_col + static_cast<uint64_t>(id) * lda;
+                    cp_async_skip<AV * 4>(&sm.sa[slot][kk][qa * AV], ar + qa * AV, a_skip[qa] || out_row);
+                }
+#pragma unroll
+                for (int q = lane; q < KC * NB; q += 32) {
+                    const int kk = q / NB, qb = q % NB;
+                    const bool out_row = tail && ts * KC + kk >= n;
+                    const float* br = out_row ? b : b + static_cast<uint64_t>(kk) * ldb + j0 + ts * b_stage;
+                    cp_async_skip<BV * 4>(&sm.sb[slot][kk][qb * BV], br + qb * BV, b_skip[qb] || out_row);
+                }
+            } else {
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const int kk = lane + 32 * h;
@@ -563,6 +595,7 @@ __global__ void __launch_bounds__(64) k_gemm_at_b_split(const float* __restrict_
                 else
                     id = sm.sid[ts % NI][kk];
                 copy_row(ts, slot, kk, id);
+            }
             }
             if (rows) {  // ids of stage ts + LAG + 1 ride with this group
 #pragma unroll
@@ -605,15 +638,29 @@ void launch_at_b(DMat a, const uint32_t* rows, DMat b, DMat out, uint64_t n, uin
     if (tuning(kTuneAtbSplit)) {
         // two A columns per lane once one-per-lane blocks outnumber the SMs
         // ~1.5x: fewer chain warps sharing SMSPs (products layer 0: 400 -> 200)
+        const bool deep = tuning(kTuneAtbDepth) == 1;
+        const bool coop = tuning(kTuneAtbDepth) == 2;
         if (gemm_at_b_chain_pairs(r, c)) {
             constexpr int TI2 = 2 * TI;
             dim3 g2(static_cast<unsigned>((r + TI2 - 1) / TI2), grid.y);
-            if (v4)
+            if (v4 && coop)
+                k_gemm_at_b_split<TI2, 4, 2, 4, 2, true><<<g2, 64, 0, s>>>(a.p, a.ld, rows, b.p, b.ld, out.p, out.ld,
+                                                                          n32, r32, c32, nz);
+            else if (v4 && deep)
+                k_gemm_at_b_split<TI2, 4, 2, 7, 5><<<g2, 64, 0, s>>>(a.p, a.ld, rows, b.p, b.ld, out.p, out.ld, n32,
+                                                                    r32, c32, nz);
+            else if (v4)
                 k_gemm_at_b_split<TI2, 4, 2><<<g2, 64, 0, s>>>(a.p, a.ld, rows, b.p, b.ld, out.p, out.ld, n32, r32, c32,
                                                               nz);
             else
                 k_gemm_at_b_split<TI2, 1, 2><<<g2, 64, 0, s>>>(a.p, a.ld, rows, b.p, b.ld, out.p, out.ld, n32, r32, c32,
                                                               nz);
+        } else if (v4 && coop) {
+            k_gemm_at_b_split<TI, 4, 1, 4, 2, true><<<grid, 64, 0, s>>>(a.p, a.ld, rows, b.p, b.ld, out.p, out.ld, n32,
+                                                                       r32, c32, nz);
+        } else if (v4 && deep) {
+            k_gemm_at_b_split<TI, 4, 1, 7, 5><<<grid, 64, 0, s>>>(a.p, a.ld, rows, b.p, b.ld, out.p, out.ld, n32, r32,
+                                                                 c32, nz);
         } else if (v4) {
             k_gemm_at_b_split<TI, 4, 1><<<grid, 64, 0, s>>>(a.p, a.ld, rows, b.p, b.ld, out.p, out.ld, n32, r32, c32, nz);
         } else {

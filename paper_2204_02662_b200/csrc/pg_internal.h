@@ -344,7 +344,9 @@ enum TuneKeyId {
     kTuneHostHubChunkSide = 36,
     kTuneVecWindow = 37,
     kTuneHostHubMin = 38,
-    kTuneGroupedSrcSegs = 39
+    kTuneGroupedSrcSegs = 39,
+    kTuneNarrowU = 40,
+    kTuneAtbDepth = 41
 };
 // whole-row SpMM warps (k_agg_row) for this width (tuning "row_kernel")
 bool row_kernel_on(uint64_t dim);
