@@ -19,8 +19,11 @@ SHAPES = [("products layer0 y_grad", "a_bt", 2_177_454, 100, 256), ("products to
           ("reddit layer0 y_grad", "a_bt", 232_898, 602, 16), ("arxiv layer0 y_grad", "a_bt", 131_584, 128, 256),
           ("products forward X W0", "ab", 2_449_029, 256, 100), ("arxiv forward X W0", "ab", 169_343, 256, 128),
           ("products forward H W1", "ab", 2_449_029, 47, 256)]
-# unfused multiply + add on the FP32 pipe: 2 FP32x2 instructions per 2 multiply-adds per lane
-FP32_UNFUSED_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
+# unfused multiply + add on the FP32 pipe: the pipe retires 32 fp32 lane-ops per
+# SMSP per cycle (an FFMA2 / FADD2 occupies it two cycles: ncu
+# sm__pipe_fma_cycles_active ~1.84x sm__inst_executed_pipe_fma), and an
+# unfused multiply-add is 2 lane-ops: 64 multiply-adds = 128 flops per SM-cycle
+FP32_UNFUSED_TFLOPS = 148 * 128 * 1.965e9 / 1e12
 
 
 def timed(fn, reps=10):
