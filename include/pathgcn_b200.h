@@ -96,9 +96,17 @@ int pg_set_heavy_min_degree(uint64_t min_degree);
  * the last, chunked segment; 0 = 1/K), "host_chunk_balance" (chunk cuts: %
  * weight of edges vs rows), "host_copy_prio" (copy/repack streams at the
  * highest priority), "host_pitch2d" (measured slower,
- * off) and "host_trace" (1: phase times on stderr). A negative value
- * restores the default ($PG_<KEY> at load, else built-in). Unknown key ->
- * PG_ERR_CONFIG. */
+ * off) and "host_trace" (1: phase times on stderr). Round-2 knobs (each
+ * measured; DESIGN.md §4 gives the numbers): "hub_inline" (1, default: wide-
+ * row hubs as the main SpMM's destination-major front; 0: side kernel),
+ * "hub_front_min", "rec_window" (0 / 1 shuffles / 2 REDUX), "row_kernel" +
+ * "row_u" + "row_seg_mb" + "row_heavy" (whole-row warps), "vec_block" (256 /
+ * 512 / 1024), "vec_window" (source-window lockstep CTAs), "narrow_u",
+ * "grouped_src_segs" (grouped Fast over L2-sized segments), "gemm_packed"
+ * (2, default: register-tiled k_gemm3; 1: k_gemm2; 0: k_gemm), "gemm3_rows",
+ * "gemm_beside_wgrad", "atb_depth", "host_hub_chunk_side" + "host_hub_min".
+ * A negative value restores the default ($PG_<KEY> at load, else built-in).
+ * Unknown key -> PG_ERR_CONFIG. */
 int pg_set_tuning(const char* key, int64_t value);
 
 /* ---------------- graph load ---------------- */
