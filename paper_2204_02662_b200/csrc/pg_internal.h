@@ -240,6 +240,9 @@ struct AggExt {
     // prefix of the range's degree order, 2 all but that prefix
     int part = 0;
     uint64_t part_min_degree = 0;  // the hub prefix of part 1 / 2: degree >= this
+    // scheduling only: the call's average edges per destination (0 unknown);
+    // very short lists (< 8) gather 4 edges per batch instead of 8
+    uint64_t avg_degree = 0;
     bool any() const { return out_rows || relu_pre || src_bits || dst_bits; }
 };
 

@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 
 WIDTHS = (1, 3, 16, 17, 41, 64, 100, 128, 129, 300, 602)
 KNOBS = {
-    "vec_u": (4, 8, 16),
+    "vec_u": (0, 4, 8, 16),
     "chunk_major": (0, 1),
     "ld_cg": (0, 2, 7),
     "heavy_narrow": (0, 1),
