@@ -101,8 +101,9 @@ constexpr TuneKey kTuneKeys[] = {
     // W' split GEMM copy warp: 0 = a row per lane, 4 slots / 2 in flight;
     // 1 = the same 7 / 5; 2 = lanes sharing rows (fewer L1 wavefronts)
     {"atb_depth", "PG_ATB_DEPTH", 0},
+    {"host_first_chunk_pct", "PG_HOST_FIRST_CHUNK_PCT", 100},  // host drop-in: size of the first-computed chunk, % of the others
 };
-static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneAtbDepth + 1,
+static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneHostFirstChunkPct + 1,
               "kTuneKeys and enum TuneKeyId (pg_internal.h) must list the same keys in the same order");
 std::atomic<int64_t> g_tune[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];
 int64_t g_tune_def[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];  // $PG_<KEY> at load, else built-in

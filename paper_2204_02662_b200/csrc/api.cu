@@ -711,7 +711,7 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
     // segments give the first pass most of the edges while only its small
     // slice of rows has arrived
     const int bal = K > 1 ? static_cast<int>(tuning(kTuneHostSegBalance) != 0) : 0;
-    const int bal_key = bal ? 1 + static_cast<int>(tuning(kTuneHostLastSegPct)) : 0;
+    const int bal_key = bal ? (1 + static_cast<int>(tuning(kTuneHostLastSegPct))) * 16 + static_cast<int>(F) : 0;
     if (K > 1 && (G.host_seg_rows != in_rows || G.host_seg_k != K || G.host_seg_bal != bal_key)) {
         std::vector<uint64_t> rc(K + 1);
         for (uint32_t k = 0; k <= K; ++k) rc[k] = in_rows * k / K;
@@ -721,12 +721,14 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
             std::vector<uint32_t> hc(in_rows);
             PG_CUDA(cudaMemcpyAsync(hc.data(), cnt.get(), in_rows * 4, cudaMemcpyDeviceToHost, s));
             PG_CUDA(cudaStreamSynchronize(s));
-            // edge fraction of the last segment (host_last_seg_pct, 0 = 1/K);
-            // the first K-1 share the rest equally
+            // edge fraction of the last pass's F segments (host_last_seg_pct,
+            // 0 = F/K), shared equally; the first K-F share the rest equally
             const int64_t pct = tuning(kTuneHostLastSegPct);
-            const double last = pct > 0 ? std::clamp<double>(pct / 100.0, 0.01, 0.99) : 1.0 / K;
+            const double last = pct > 0 ? std::clamp<double>(pct / 100.0, 0.01, 0.99) : static_cast<double>(F) / K;
             std::vector<double> tgt(K);
-            for (uint32_t j = 1; j < K; ++j) tgt[j] = (1.0 - last) * j / (K - 1) * static_cast<double>(b.E);
+            for (uint32_t j = 1; j < K; ++j)
+                tgt[j] = (j <= K - F ? (1.0 - last) * j / (K - F) : (1.0 - last) + last * (j - (K - F)) / F) *
+                         static_cast<double>(b.E);
             uint64_t acc = 0, k = 1;
             for (uint64_t r = 0; r < in_rows && k < K; ++r) {
                 acc += hc[r];
@@ -748,22 +750,27 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
         // crosses r / R: edge-balanced chunks (alpha = 1) isolate the hub
         // rows (frontier order: hubs first) into tiny, latency-bound chunks
         const int alpha = static_cast<int>(std::clamp<int64_t>(tuning(kTuneHostChunkBalance), 0, 100));
-        if (G.host_chunks.size() != R + 1 || G.host_chunk_alpha != alpha) {
+        // the last chunk (computed first under the reverse order) at
+        // host_first_chunk_pct % of the others: the first D2H starts sooner
+        const int64_t fpct = std::clamp<int64_t>(tuning(kTuneHostFirstChunkPct), 10, 100);
+        const int key = alpha * 1000 + static_cast<int>(fpct);
+        if (G.host_chunks.size() != R + 1 || G.host_chunk_alpha != key) {
             std::vector<uint64_t> off(D + 1);
             PG_CUDA(cudaMemcpyAsync(off.data(), G.path->offsets.get(), off.size() * 8, cudaMemcpyDeviceToHost, s));
             PG_CUDA(cudaStreamSynchronize(s));
             G.host_chunks.assign(1, 0);
             const double E = std::max<double>(1.0, static_cast<double>(off[D]));
+            const double total = (R - 1) + fpct / 100.0;
             uint64_t row = 0;
             for (uint32_t r = 1; r < R; ++r) {
-                const double target = static_cast<double>(r) / R;
+                const double target = static_cast<double>(r) / total;
                 while (row < D && (alpha * (off[row] / E) + (100 - alpha) * (static_cast<double>(row) / D)) / 100.0 <
                                       target)
                     ++row;
                 G.host_chunks.push_back(std::max(G.host_chunks.back(), static_cast<uint32_t>(row)));
             }
             G.host_chunks.push_back(static_cast<uint32_t>(D));
-            G.host_chunk_alpha = alpha;
+            G.host_chunk_alpha = key;
         }
         cuts = G.host_chunks;
     }
@@ -912,8 +919,17 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
         AggExt cx;
         cx.part = any_hub && nh[r] ? 2 : 0;
         cx.part_min_degree = hub_min;
-        run_aggregate(G, parent_indexed, cuts[r], cuts[r + 1], din.get(), ld, dout.get() + cuts[r] * ld, ld, dim,
-                      last_flags, s, last, cx);
+        if (K > 1 && F > 1) {
+            // the chunk's F final segments one by one, in source order: each
+            // launch gathers from one segment's rows (L2-sized when K is)
+            for (uint32_t k = K - F; k < K; ++k)
+                run_aggregate(G, parent_indexed, cuts[r], cuts[r + 1], din.get(), ld, dout.get() + cuts[r] * ld, ld,
+                              dim, k == K - F ? last_flags : (last_flags & ~PG_AGG_OVERWRITE), s,
+                              SegSel{G.host_seg_bnd.get(), static_cast<int>(k), K}, cx);
+        } else {
+            run_aggregate(G, parent_indexed, cuts[r], cuts[r + 1], din.get(), ld, dout.get() + cuts[r] * ld, ld, dim,
+                          last_flags, s, last, cx);
+        }
         PG_CUDA(cudaEventRecord(cs.ev[1 + K + r], s));
         tmark(s, "chunk" + std::to_string(r));
     }

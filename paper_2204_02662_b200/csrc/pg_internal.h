@@ -349,7 +349,8 @@ enum TuneKeyId {
     kTuneHostHubMin = 38,
     kTuneGroupedSrcSegs = 39,
     kTuneNarrowU = 40,
-    kTuneAtbDepth = 41
+    kTuneAtbDepth = 41,
+    kTuneHostFirstChunkPct = 42
 };
 // whole-row SpMM warps (k_agg_row) for this width (tuning "row_kernel")
 bool row_kernel_on(uint64_t dim);
