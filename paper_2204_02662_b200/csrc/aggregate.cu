@@ -102,8 +102,14 @@ constexpr TuneKey kTuneKeys[] = {
     // 1 = the same 7 / 5; 2 = lanes sharing rows (fewer L1 wavefronts)
     {"atb_depth", "PG_ATB_DEPTH", 0},
     {"host_first_chunk_pct", "PG_HOST_FIRST_CHUNK_PCT", 100},  // host drop-in: size of the first-computed chunk, % of the others
+    // host drop-in: the last pass as ONE launch whose items count per row
+    // chunk, each chunk's D2H waiting on its counter (cuStreamWaitValue32):
+    // the pass itself runs 9.8 vs 11.7 ms, but the hub front's chains hold
+    // warp slots and the later chunks finish late (e2e 23.3-24.0 vs 22.8 ms,
+    // profiles/e2e_seq_sweep_r02.log), so off
+    {"host_seq", "PG_HOST_SEQ", 0},
 };
-static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneHostFirstChunkPct + 1,
+static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneHostSeq + 1,
               "kTuneKeys and enum TuneKeyId (pg_internal.h) must list the same keys in the same order");
 std::atomic<int64_t> g_tune[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];
 int64_t g_tune_def[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];  // $PG_<KEY> at load, else built-in
@@ -630,6 +636,107 @@ __global__ void __launch_bounds__(512, 2) k_agg_vec4w(const uint64_t* __restrict
         __syncthreads();
     }
     if (valid) acc_store_ext(orow, col, dim, acc, z, ext, d, row);
+}
+
+// One launch over a SEQUENCE of destination runs (the host drop-in's last
+// pass, tuning "host_seq"): run s covers items [item0, item0 + nd*chunks)
+// of destinations dlist[dofs .. dofs+nd), destination-major (the hub front)
+// or column-chunk-major, and each finished item bumps counters[counter] after
+// a system-scope fence, so a copy stream can wait (cuStreamWaitValue32) for a
+// row chunk's last item and start its D2H while the launch goes on: no
+// per-chunk launch tails. The body is k_agg_vec4's (LPD 32, U 8): the same
+// per-column ascending-edge order, bit-identical.
+template <int U>
+__global__ void __launch_bounds__(256, 4) k_agg_vec4_seq(const uint64_t* __restrict__ ebeg,
+                                                        const uint64_t* __restrict__ eend,
+                                                        const Edge* __restrict__ edges,
+                                                        const uint32_t* __restrict__ dlist, SeqTable tab,
+                                                        uint64_t n_items, uint32_t chunks,
+                                                        const float* __restrict__ in, uint32_t ld_in_bytes,
+                                                        float* __restrict__ out, uint64_t ld_out, uint32_t dim,
+                                                        int accumulate, float2 zeros, uint32_t zmask,
+                                                        unsigned* __restrict__ counters) {
+    __shared__ uint32_t s_cnt[8];  // the completion counter of each warp's item (~0u: none)
+    const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    const uint64_t item = t >> 5;
+    const uint32_t lane = lane_id(), wib = threadIdx.x >> 5;
+    uint32_t si = 0;
+    while (si + 1 < tab.nseg && item >= tab.seg[si + 1].item0) ++si;
+    const SeqSeg sg = tab.seg[si];
+    const uint64_t local = item - sg.item0;
+    // (items past a run's nd * chunks are the CTA-alignment padding)
+    if (item < n_items && local < static_cast<uint64_t>(sg.nd) * chunks) {  // no early return: the CTA meets below
+        const uint32_t di = static_cast<uint32_t>(sg.dest_major ? local / chunks : local % sg.nd);
+        const uint32_t ci = static_cast<uint32_t>(sg.dest_major ? local % chunks : local / sg.nd);
+        const Zs z = zs_of(zeros);
+        const uint32_t d = __ldg(dlist + sg.dofs + di);
+        const uint32_t col = (ci * 32 + lane) * 4;
+        const bool active = col < dim;
+        uint64_t e = __ldg(ebeg + d);
+        const uint64_t end = __ldg(eend + d);
+        const char* base = reinterpret_cast<const char*>(in) + (active ? col : ci * 128u) * 4u;
+        asm("mov.b64 %0, %0;" : "+l"(base));
+        float* orow = out + d * ld_out + col;
+        Acc acc = acc_load(orow, col, dim, accumulate);
+        for (; e + U <= end; e += U) {
+            Edge ed[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) ed[u] = ld_rec(edges + e + u);
+            float4 x[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) x[u] = ld_row<0>(base, ed[u].x, ld_in_bytes);
+            const Zs zz = batch_dep<U>(x, z, zmask);
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc_step(acc, __uint_as_float(ed[u].y), x[u], zz);
+        }
+        if (e < end) {
+            const uint32_t n = static_cast<uint32_t>(end - e);
+            Edge ed[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) ed[u] = ld_rec(edges + e + (u < static_cast<int>(n) ? u : n - 1));
+            float4 x[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                x[u] = u < static_cast<int>(n) ? ld_row<0>(base, ed[u].x, ld_in_bytes) : make_float4(0.f, 0.f, 0.f, 0.f);
+            const Zs zz = batch_dep<U>(x, z, zmask);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (u < static_cast<int>(n)) acc_step(acc, __uint_as_float(ed[u].y), x[u], zz);
+        }
+        if (active) {
+            asm("add.rn.f32x2 %0, %1, %2;" : "=l"(acc.lo) : "l"(acc.lo), "l"(z.pz));
+            asm("add.rn.f32x2 %0, %1, %2;" : "=l"(acc.hi) : "l"(acc.hi), "l"(z.pz));
+            const float2 l = unpk2(acc.lo), h = unpk2(acc.hi);
+            if (col + 3 < dim) {
+                *reinterpret_cast<float4*>(orow) = make_float4(l.x, l.y, h.x, h.y);
+            } else {
+                orow[0] = l.x;
+                if (col + 1 < dim) orow[1] = l.y;
+                if (col + 2 < dim) orow[2] = h.x;
+            }
+        }
+        if (lane == 0) s_cnt[wib] = sg.counter;
+    } else if (lane == 0) {
+        s_cnt[wib] = ~0u;
+    }
+    // every thread's stores ordered before the CTA's completion marks (one
+    // atomic per distinct counter per CTA, not per warp: the counters of a
+    // chunk are hit by every CTA of its items)
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t nw = blockDim.x >> 5;
+        for (uint32_t w = 0; w < nw; ++w) {
+            const uint32_t c = s_cnt[w];
+            if (c == ~0u) continue;
+            bool seen = false;
+            for (uint32_t v = 0; v < w; ++v) seen |= s_cnt[v] == c;
+            if (seen) continue;
+            uint32_t k = 0;
+            for (uint32_t v = w; v < nw; ++v) k += s_cnt[v] == c;
+            atomicAdd(counters + c, k);
+        }
+    }
 }
 
 template <int NS>
@@ -2055,6 +2162,16 @@ __global__ void k_gather_rows(const float* __restrict__ src, uint64_t lds, const
 }
 
 }  // namespace
+
+void aggregate_seq(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges, const uint32_t* dlist,
+                   const SeqTable& tab, uint64_t n_items, uint32_t chunks, const float* in, uint64_t ld_in, float* out,
+                   uint64_t ld_out, uint32_t dim, bool accumulate, unsigned* counters, cudaStream_t s) {
+    if (!n_items) return;
+    k_agg_vec4_seq<8><<<grid_for(n_items * 32, 256), 256, 0, s>>>(ebeg, eend, edges, dlist, tab, n_items, chunks, in,
+                                                                 static_cast<uint32_t>(ld_in * 4), out, ld_out, dim,
+                                                                 accumulate, kZeros, 0u, counters);
+    PG_LAUNCH("k_agg_vec4_seq");
+}
 
 void aggregate_det(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges, const uint32_t* order, uint32_t D,
                    uint32_t d_begin, uint32_t d_end, uint32_t n_heavy, const float* in, uint64_t ld_in,

@@ -428,6 +428,9 @@ struct CopyStreams {
     // so a segment's / chunk's copy never queues behind the previous repack
     cudaStream_t rup = nullptr, rdn = nullptr;
     cudaStream_t hub = nullptr;  // the last pass's hub chunk, concurrent with the other chunks
+    // per-chunk completion counters of the sequenced last pass: plain
+    // cudaMalloc memory (stream memory operations reject pool allocations)
+    unsigned* counters = nullptr;
     std::vector<cudaEvent_t> ev;  // sync events
     std::vector<cudaEvent_t> tev;  // timing events (host_trace)
     std::mutex call;              // one host-buffer call at a time per device owns them
@@ -458,6 +461,7 @@ CopyStreams& copy_streams(int device, size_t nev, std::unique_lock<std::mutex>& 
         PG_CUDA(cudaStreamCreateWithPriority(&c.rup, cudaStreamNonBlocking, prio));
         PG_CUDA(cudaStreamCreateWithPriority(&c.rdn, cudaStreamNonBlocking, prio));
         PG_CUDA(cudaStreamCreateWithPriority(&c.hub, cudaStreamNonBlocking, prio));
+        PG_CUDA(cudaMalloc(&c.counters, 64 * sizeof(unsigned)));
     }
     while (c.ev.size() < nev) {
         cudaEvent_t e;
@@ -474,6 +478,30 @@ CopyStreams& copy_streams(int device, size_t nev, std::unique_lock<std::mutex>& 
 // ~10 GB/s. Instead they go through library-owned pinned slots: a few host
 // threads memcpy pageable <-> slot while the copy engine moves the previous
 // slot, so the link still streams.
+// cuStreamWaitValue32 (driver API, loaded at first use): a stream waits
+// until a 32-bit word in device memory reaches a value
+using WaitValueFn = int (*)(cudaStream_t, unsigned long long, unsigned int, unsigned int);
+WaitValueFn wait_value_fn() {
+    static WaitValueFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<WaitValueFn>(p);
+        else
+            cudaGetLastError();
+    });
+    return fn;
+}
+constexpr unsigned kWaitValueGeq = 0;  // CU_STREAM_WAIT_VALUE_GEQ
+
+__global__ void k_add_offset(const uint32_t* __restrict__ src, uint32_t n, uint32_t off, uint32_t* __restrict__ dst) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = src[i] + off;
+}
+
 bool host_pinned(const void* p) {
     cudaPointerAttributes at{};
     if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
@@ -910,8 +938,77 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
         PG_CUDA(cudaEventRecord(cs.ev[1 + K], cs.hub));
         tmark(cs.hub, "chunk0");
     }
+    // Sequenced last pass (tuning "host_seq"): ONE launch over every chunk,
+    // the hub front of chunk 0 first (its long chains start with the pass),
+    // then chunks R-1 .. 1, then the rest of chunk 0, each finished item
+    // counted per chunk; chunk r's D2H stream waits on its counter
+    // (cuStreamWaitValue32) instead of a per-chunk launch boundary.
+    const uint32_t nq_h = static_cast<uint32_t>((dim + 3) / 4);
+    const bool seq = tuning(kTuneHostSeq) != 0 && reverse && R > 1 && (K == 1 || F == 1) && hub_mode == 0 &&
+                     nq_h > 16 && !row_kernel_on(dim) && wait_value_fn() && ld % 4 == 0 && G.path;
+    DevBuf<uint32_t> seq_dlist;
+    unsigned* seq_counters = nullptr;
+    std::vector<uint32_t> seq_target(cuts.size() - 1, 0);
     std::vector<size_t> order;
-    for (size_t ri = 0; ri + 1 < cuts.size(); ++ri) {
+    if (seq) {
+        const uint32_t nrc = static_cast<uint32_t>(cuts.size() - 1);
+        const uint32_t chunks = (nq_h + 31) / 32;
+        seq_dlist = DevBuf<uint32_t>(D, s);
+        seq_counters = cs.counters;  // R <= 16 <= 64
+        PG_CUDA(cudaMemsetAsync(seq_counters, 0, nrc * sizeof(unsigned), s));
+        // the waiting streams must see THIS call's zeroed counters, not the
+        // final counts a previous call of the same shape left behind
+        PG_CUDA(cudaEventRecord(cs.ev[0], s));
+        PG_CUDA(cudaStreamWaitEvent(cs.rdn, cs.ev[0], 0));
+        PG_CUDA(cudaStreamWaitEvent(cs.d2h, cs.ev[0], 0));
+        const uint64_t rdiv = K > 1 ? K : 1;  // the last pass covers one of K segments
+        SeqTable tab;
+        std::vector<uint32_t> dofs(nrc, 0);
+        uint32_t pos = 0, nh0 = 0;
+        auto put = [&](uint32_t r) {  // chunk r's degree-ordered rows, absolute ids
+            Groups::RowSched* rs = row_sched(G, cuts[r], cuts[r + 1]);
+            const uint32_t nd = cuts[r + 1] - cuts[r];
+            k_add_offset<<<(nd + 255) / 256, 256, 0, s>>>(rs->order.get(), nd, cuts[r], seq_dlist.get() + pos);
+            PG_LAUNCH("k_add_offset");
+            dofs[r] = pos;
+            pos += nd;
+            if (r == 0) nh0 = std::min(nd, rs->hist.heavy(heavy_degree(dim, rs->hist.edges / rdiv)));
+        };
+        for (uint32_t r = 0; r < nrc; ++r)
+            if (cuts[r] < cuts[r + 1]) put(r);
+        uint64_t item = 0;
+        // runs start on CTA boundaries (8 items): a CTA marks its items done
+        // together, so a run sharing a CTA with the next one (a hub chain)
+        // would wait for it; the padding items do nothing
+        auto run = [&](uint32_t r, uint32_t off, uint32_t nd, uint32_t dest_major) {
+            if (!nd) return;
+            tab.seg[tab.nseg++] = SeqSeg{item, nd, dofs[r] + off, dest_major, r};
+            item += (static_cast<uint64_t>(nd) * chunks + 7) & ~7ull;
+        };
+        // the first chunk of the D2H order first (the copies start as soon
+        // as possible), then the hub front (its chains have until chunk 0's
+        // turn), then the other chunks in D2H order, then chunk 0's rest
+        uint32_t first = nrc - 1;
+        while (first > 0 && cuts[first] == cuts[first + 1]) --first;
+        if (first > 0) run(first, 0, cuts[first + 1] - cuts[first], 0);
+        if (cuts[0] < cuts[1]) run(0, 0, nh0, 1);  // the hub front
+        for (uint32_t r = first; r-- > 1;) {
+            if (cuts[r] == cuts[r + 1]) continue;
+            run(r, 0, cuts[r + 1] - cuts[r], 0);
+        }
+        if (cuts[0] < cuts[1]) run(0, nh0, cuts[1] - cuts[0] - nh0, 0);
+        for (uint32_t r = 0; r < nrc; ++r) seq_target[r] = (cuts[r + 1] - cuts[r]) * chunks;
+        const uint64_t* eb = K > 1 ? G.host_seg_bnd.get() + static_cast<uint64_t>(K - 1) * D : G.path->offsets.get();
+        const uint64_t* ee = K > 1 ? G.host_seg_bnd.get() + static_cast<uint64_t>(K) * D : G.path->offsets.get() + 1;
+        aggregate_seq(eb, ee, G.path->edges_parent.get(), seq_dlist.get(), tab, item, chunks, din.get(), ld, dout.get(),
+                      ld, static_cast<uint32_t>(dim), !(last_flags & PG_AGG_OVERWRITE), seq_counters, s);
+        tmark(s, "seqpass");
+        for (size_t ri = 0; ri + 1 < cuts.size(); ++ri) {
+            const size_t r = cuts.size() - 2 - ri;
+            if (cuts[r] < cuts[r + 1]) order.push_back(r);
+        }
+    }
+    for (size_t ri = 0; !seq && ri + 1 < cuts.size(); ++ri) {
         const size_t r = reverse ? cuts.size() - 2 - ri : ri;
         if (cuts[r] == cuts[r + 1]) continue;
         order.push_back(r);
@@ -941,7 +1038,15 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
     if (out_pg) down = std::make_unique<StagedD2H>(StagedD2H{*sg, cs.d2h});
     for (const size_t r : order) {
         const uint32_t rb = cuts[r], re = cuts[r + 1];
-        PG_CUDA(cudaStreamWaitEvent(cs.d2h, cs.ev[1 + K + r], 0));
+        if (seq) {  // the chunk's items all counted: its rows are final
+            cudaStream_t w = packed || (pitch2d && !down) ? cs.d2h : cs.rdn;
+            const int rc = wait_value_fn()(w, reinterpret_cast<unsigned long long>(seq_counters + r), seq_target[r],
+                                           kWaitValueGeq);
+            if (rc != 0) fail(kDevice, "cuStreamWaitValue32 failed (CUresult " + std::to_string(rc) + ")");
+            tmark(w, "rdy" + std::to_string(r));
+        } else {
+            PG_CUDA(cudaStreamWaitEvent(cs.d2h, cs.ev[1 + K + r], 0));
+        }
         if (any_hub && nh[r]) {  // the chunk's hub rows come from the hub stream
             PG_CUDA(cudaStreamWaitEvent(cs.d2h, ev_hub[r], 0));
             PG_CUDA(cudaStreamWaitEvent(cs.rdn, ev_hub[r], 0));
@@ -957,7 +1062,7 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
         if (!packed) {
             // repack on rdn (waits for the chunk), the D2H stream waits for
             // the repack: chunk r+1's repack overlaps chunk r's DMA
-            PG_CUDA(cudaStreamWaitEvent(cs.rdn, cs.ev[1 + K + r], 0));
+            if (!seq) PG_CUDA(cudaStreamWaitEvent(cs.rdn, cs.ev[1 + K + r], 0));
             copy_rows(dout.get() + rb * ld, ld, fout.get() + rb * dim, dim, re - rb, dim, cs.rdn);
             PG_CUDA(cudaEventRecord(ev_packed[r], cs.rdn));
             PG_CUDA(cudaStreamWaitEvent(cs.d2h, ev_packed[r], 0));

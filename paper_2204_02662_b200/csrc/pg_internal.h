@@ -268,6 +268,24 @@ struct SegSel {
 // graph: vertex ids), destination rows [rb, re) with their cached degree
 // schedule; flags = PG_AGG_* of the C ABI. edges_override replaces the
 // path's edge stream (same destinations and order, other source ids).
+// A launch over a sequence of destination runs with per-run completion
+// counters (aggregate_seq, k_agg_vec4_seq): run s = items [item0, item0 +
+// nd * chunks) of destinations dlist[dofs, dofs + nd), destination-major or
+// column-chunk-major; each finished item adds 1 to counters[counter].
+struct SeqSeg {
+    uint64_t item0;
+    uint32_t nd, dofs, dest_major, counter;
+};
+constexpr int kSeqMax = 24;
+struct SeqTable {
+    SeqSeg seg[kSeqMax];
+    uint32_t nseg = 0;
+};
+// wide rows (ld % 4 == 0, 16-byte aligned), LPD 32: the k_agg_vec4 body
+void aggregate_seq(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges, const uint32_t* dlist,
+                   const SeqTable& tab, uint64_t n_items, uint32_t chunks, const float* in, uint64_t ld_in, float* out,
+                   uint64_t ld_out, uint32_t dim, bool accumulate, unsigned* counters, cudaStream_t s);
+
 // degree-ordered schedule of path rows [rb, re) (cached on the grouping;
 // caller holds G.mu) and the hub count of that range's SpMM call
 Groups::RowSched* row_sched(Groups& G, uint32_t rb, uint32_t re);
@@ -350,7 +368,8 @@ enum TuneKeyId {
     kTuneGroupedSrcSegs = 39,
     kTuneNarrowU = 40,
     kTuneAtbDepth = 41,
-    kTuneHostFirstChunkPct = 42
+    kTuneHostFirstChunkPct = 42,
+    kTuneHostSeq = 43
 };
 // whole-row SpMM warps (k_agg_row) for this width (tuning "row_kernel")
 bool row_kernel_on(uint64_t dim);
