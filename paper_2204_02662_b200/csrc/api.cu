@@ -948,6 +948,7 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
                      nq_h > 16 && !row_kernel_on(dim) && wait_value_fn() && ld % 4 == 0 && G.path;
     DevBuf<uint32_t> seq_dlist;
     unsigned* seq_counters = nullptr;
+    bool seq_side_hubs = false;
     std::vector<uint32_t> seq_target(cuts.size() - 1, 0);
     std::vector<size_t> order;
     if (seq) {
@@ -965,6 +966,7 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
         SeqTable tab;
         std::vector<uint32_t> dofs(nrc, 0);
         uint32_t pos = 0, nh0 = 0;
+        uint64_t thr0 = 0;
         auto put = [&](uint32_t r) {  // chunk r's degree-ordered rows, absolute ids
             Groups::RowSched* rs = row_sched(G, cuts[r], cuts[r + 1]);
             const uint32_t nd = cuts[r + 1] - cuts[r];
@@ -972,7 +974,10 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
             PG_LAUNCH("k_add_offset");
             dofs[r] = pos;
             pos += nd;
-            if (r == 0) nh0 = std::min(nd, rs->hist.heavy(heavy_degree(dim, rs->hist.edges / rdiv)));
+            if (r == 0) {
+                thr0 = heavy_degree(dim, rs->hist.edges / rdiv);
+                nh0 = std::min(nd, rs->hist.heavy(thr0));
+            }
         };
         for (uint32_t r = 0; r < nrc; ++r)
             if (cuts[r] < cuts[r + 1]) put(r);
@@ -988,16 +993,30 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
         // the first chunk of the D2H order first (the copies start as soon
         // as possible), then the hub front (its chains have until chunk 0's
         // turn), then the other chunks in D2H order, then chunk 0's rest
+        // host_seq 2: chunk 0's hubs on the side kernel (deeper-pipelined
+        // chains, a few small CTAs) on the hub stream instead of the front
+        seq_side_hubs = tuning(kTuneHostSeq) == 2 && nh0 > 0;
         uint32_t first = nrc - 1;
         while (first > 0 && cuts[first] == cuts[first + 1]) --first;
+        if (seq_side_hubs) {
+            PG_CUDA(cudaEventRecord(cs.ev[0], s));
+            PG_CUDA(cudaStreamWaitEvent(cs.hub, cs.ev[0], 0));
+            AggExt hx;
+            hx.part = 1;
+            hx.part_min_degree = thr0;
+            run_aggregate(G, parent_indexed, cuts[0], cuts[1], din.get(), ld, dout.get(), ld, dim, last_flags, cs.hub,
+                          last, hx);
+            PG_CUDA(cudaEventRecord(ev_hub[0], cs.hub));
+        }
         if (first > 0) run(first, 0, cuts[first + 1] - cuts[first], 0);
-        if (cuts[0] < cuts[1]) run(0, 0, nh0, 1);  // the hub front
+        if (cuts[0] < cuts[1] && !seq_side_hubs) run(0, 0, nh0, 1);  // the hub front
         for (uint32_t r = first; r-- > 1;) {
             if (cuts[r] == cuts[r + 1]) continue;
             run(r, 0, cuts[r + 1] - cuts[r], 0);
         }
         if (cuts[0] < cuts[1]) run(0, nh0, cuts[1] - cuts[0] - nh0, 0);
         for (uint32_t r = 0; r < nrc; ++r) seq_target[r] = (cuts[r + 1] - cuts[r]) * chunks;
+        if (seq_side_hubs) seq_target[0] -= nh0 * chunks;
         const uint64_t* eb = K > 1 ? G.host_seg_bnd.get() + static_cast<uint64_t>(K - 1) * D : G.path->offsets.get();
         const uint64_t* ee = K > 1 ? G.host_seg_bnd.get() + static_cast<uint64_t>(K) * D : G.path->offsets.get() + 1;
         aggregate_seq(eb, ee, G.path->edges_parent.get(), seq_dlist.get(), tab, item, chunks, din.get(), ld, dout.get(),
@@ -1030,7 +1049,7 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
         PG_CUDA(cudaEventRecord(cs.ev[1 + K + r], s));
         tmark(s, "chunk" + std::to_string(r));
     }
-    if (any_hub || hub_mode == 2) {  // s joins the hub stream (buffers are freed on s)
+    if (any_hub || hub_mode == 2 || seq_side_hubs) {  // s joins the hub stream (buffers are freed on s)
         PG_CUDA(cudaEventRecord(cs.ev[0], cs.hub));
         PG_CUDA(cudaStreamWaitEvent(s, cs.ev[0], 0));
     }
@@ -1044,6 +1063,10 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
                                            kWaitValueGeq);
             if (rc != 0) fail(kDevice, "cuStreamWaitValue32 failed (CUresult " + std::to_string(rc) + ")");
             tmark(w, "rdy" + std::to_string(r));
+            if (seq_side_hubs && r == 0) {  // and chunk 0's hub rows from the hub stream
+                PG_CUDA(cudaStreamWaitEvent(cs.d2h, ev_hub[0], 0));
+                PG_CUDA(cudaStreamWaitEvent(cs.rdn, ev_hub[0], 0));
+            }
         } else {
             PG_CUDA(cudaStreamWaitEvent(cs.d2h, cs.ev[1 + K + r], 0));
         }
