@@ -631,6 +631,8 @@ def main():
         line["gs_sweep"] = gs_sweep(pg, prep, dims)
     if not args.profile and world == 1:
         line["grouped_fast"] = grouped_fast(pg, torch, prep, y_full, x_out, dims)
+    if not args.profile and world == 1 and os.environ.get("PG_BENCH_NO_SHARDS") != "1":
+        line["shard_projection"] = shard_projection(pg, torch, paths, groups, y_full, dims, ep_bytes)
     if not args.profile and not args.no_chain and world == 1:
         line["chain"] = measure_chain(pg, torch, g, prep, cfg, vt, dev)
     elif not args.profile and not args.no_chain:
@@ -937,6 +939,46 @@ def tune_sweep(pg, torch, step, L):
             log(f"[tune] vec_u={vu} chunk_major={cm} per-path ms={[round(x, 3) for x in ms]} total={sum(ms):.3f}")
     pg.set_tuning("vec_u")
     pg.set_tuning("chunk_major")
+
+
+def shard_projection(pg, torch, paths, groups, y_full, dims, ep_bytes, nvlink_gbs=700.0):
+    """Single-GPU PROJECTION of the N-GPU epoch (no multi-GPU box here): for
+    N = 2, 4, 8 the library's destination-row shards of every path
+    (edge-balanced, ExecutionPath.shard_bounds) are run ONE AT A TIME on this
+    GPU through the same row-range call a rank makes, and the slowest rank's
+    time is taken per path; the y_grad exchange (each rank receives the
+    (N-1)/N of the parent rows it does not own) is modelled at nvlink_gbs and
+    either hidden under the SpMM (the library overlaps it per owner) or added
+    (no overlap). A projection, not a measurement: reported so the shard
+    balance and the compute side of the scaling are on record."""
+    out = {"note": ("projection from single-GPU shard timings (each rank's rows run alone through the row-range "
+                    f"call) + the y_grad exchange modelled at {nvlink_gbs:.0f} GB/s per GPU; not a multi-GPU "
+                    "measurement"), "per_n": []}
+    for world in (2, 4, 8):
+        rank_max, xch = [], []
+        for i, p in enumerate(paths):
+            b = p.shard_bounds(world)
+            y = y_full[i][:, : dims[i]]
+            ts = []
+            for r in range(world):
+                x = pg.empty_rows(int(b[r + 1] - b[r]), dims[i])
+                pg.backward_aggregation(groups[i], y, x, overwrite=True, rows=(int(b[r]), int(b[r + 1])))
+                a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                for _ in range(3):
+                    pg.backward_aggregation(groups[i], y, x, overwrite=True, rows=(int(b[r]), int(b[r + 1])))
+                z.record()
+                torch.cuda.synchronize()
+                ts.append(a.elapsed_time(z) / 3)
+            rank_max.append(max(ts))
+            xch.append(p.P * dims[i] * 4 * (world - 1) / world / (nvlink_gbs * 1e9) * 1e3)
+        overlap = sum(max(a, b) for a, b in zip(rank_max, xch))
+        serial = sum(a + b for a, b in zip(rank_max, xch))
+        out["per_n"].append({"n_gpus": world, "spmm_rank_max_ms": [round(x, 4) for x in rank_max],
+                             "exchange_model_ms": [round(x, 4) for x in xch],
+                             "epoch_ms_overlapped": round(overlap, 4), "epoch_ms_serial": round(serial, 4),
+                             "GBps_overlapped": round(ep_bytes / (overlap / 1e3) / 1e9, 1)})
+    return out
 
 
 def knob_sweep(pg, torch, step, L, x_out, dims, config, settings):
