@@ -939,10 +939,10 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
         tmark(cs.hub, "chunk0");
     }
     // Sequenced last pass (tuning "host_seq"): ONE launch over every chunk,
-    // the hub front of chunk 0 first (its long chains start with the pass),
-    // then chunks R-1 .. 1, then the rest of chunk 0, each finished item
-    // counted per chunk; chunk r's D2H stream waits on its counter
-    // (cuStreamWaitValue32) instead of a per-chunk launch boundary.
+    // each finished item counted per chunk; chunk r's D2H stream waits on its
+    // counter (cuStreamWaitValue32) instead of a per-chunk launch boundary.
+    // Run order below: the first chunk of the D2H order, chunk 0's hub front,
+    // the other chunks in D2H order, chunk 0's rest.
     const uint32_t nq_h = static_cast<uint32_t>((dim + 3) / 4);
     const bool seq = tuning(kTuneHostSeq) != 0 && reverse && R > 1 && (K == 1 || F == 1) && hub_mode == 0 &&
                      nq_h > 16 && !row_kernel_on(dim) && wait_value_fn() && ld % 4 == 0 && G.path;
@@ -992,9 +992,9 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
         };
         // the first chunk of the D2H order first (the copies start as soon
         // as possible), then the hub front (its chains have until chunk 0's
-        // turn), then the other chunks in D2H order, then chunk 0's rest
+        // turn), then the other chunks in D2H order, then chunk 0's rest.
         // host_seq 2: chunk 0's hubs on the side kernel (deeper-pipelined
-        // chains, a few small CTAs) on the hub stream instead of the front
+        // chains, a few small CTAs) on the hub stream instead of the front.
         seq_side_hubs = tuning(kTuneHostSeq) == 2 && nh0 > 0;
         uint32_t first = nrc - 1;
         while (first > 0 && cuts[first] == cuts[first + 1]) --first;
