@@ -47,7 +47,9 @@ constexpr TuneKey kTuneKeys[] = {
     {"host_chunk_order", "PG_HOST_CHUNK_ORDER", 1},  // host drop-in last pass: 1 = last row chunk first
     {"grouped_seg", "PG_GROUPED_SEG", 0},  // grouped Fast: 0 = atomic-free k_agg_grp, 1 = CTA-segmented + atomics at CTA edges, 2 = an atomic per extra group
     // heavy wide rows: software-pipelined k_agg_wide_pipe with hub items
-    // destination-major (1) or chunk-major (2); 0 = k_agg_wide_lat
+    // destination-major (1) or chunk-major (2); 3 = whole-row TMA ring
+    // (k_agg_hub_ring: measured slower, its ~80 KB ring holds only 32 rows in
+    // flight per hub, profiles/e2e_hub_ring_sweep_r02.log); 0 = k_agg_wide_lat
     {"heavy_wide_pipe", "PG_HEAVY_WIDE_PIPE", 1},
     {"host_final_segs", "PG_HOST_FINAL_SEGS", 1},  // host drop-in: trailing source segments of the chunked last pass
     {"host_pitch2d", "PG_HOST_PITCH2D", 0},  // host drop-in: odd widths by 2-D DMA (1) or flat DMA + repack kernel (0)
@@ -1409,6 +1411,103 @@ __global__ void __launch_bounds__(64) k_agg_heavy(const uint64_t* __restrict__ e
     if (active) acc_store(orow, col, dim, acc, z);
 }
 
+// Wide-row hubs on a whole-row TMA ring (tuning heavy_wide_pipe = 3): one
+// CTA per hub destination, a producer warp that bulk-copies WHOLE rows (one
+// cp.async.bulk of ld bytes per edge, every column chunk at once) into a
+// kRingStages-deep shared-memory ring, and one consumer warp per 128-column
+// chunk folding the staged rows in edge order (per column, ascending edge,
+// fl(w*x) then fl(acc + .): bit-identical). A hub is a serial chain per
+// column: its time is rows x the slower of the copy issue (~28 SM cycles per
+// bulk op) and the fold; k_agg_wide_pipe gathers the same row five times
+// (once per chunk warp) with 32 loads in flight per warp instead.
+constexpr int kRingStages = 4;
+constexpr int kRingRows = 8;  // rows per stage
+
+__global__ void __launch_bounds__(288) k_agg_hub_ring(const uint64_t* __restrict__ ebeg,
+                                                     const uint64_t* __restrict__ eend,
+                                                     const Edge* __restrict__ edges,
+                                                     const uint32_t* __restrict__ order, uint32_t d_begin,
+                                                     const float* __restrict__ in, uint32_t ld_in_bytes,
+                                                     float* __restrict__ out, uint64_t ld_out, uint32_t dim,
+                                                     int accumulate, float2 zeros, AggExt ext) {
+    constexpr int NS = kRingStages, T = kRingRows;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const uint32_t nwc = (blockDim.x >> 5) - 1;  // consumer warps = 128-column chunks
+    unsigned char* buf = smem;                   // NS x T rows of ld_in_bytes
+    float* wbuf = reinterpret_cast<float*>(smem + static_cast<size_t>(NS) * T * ld_in_bytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>(wbuf + NS * T);
+    uint64_t* empty = full + NS;
+    const uint32_t d = order[d_begin + blockIdx.x];
+    const uint64_t eb = ebeg[d], ee = eend[d];
+    const uint64_t ntiles = (ee - eb + T - 1) / T;
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < NS; ++st) {
+            mbar_init(&full[st], 32);
+            mbar_init(&empty[st], nwc);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == nwc) {  // producer
+        for (uint64_t t = 0; t < ntiles; ++t) {
+            const int st = static_cast<int>(t % NS);
+            const uint32_t ph = static_cast<uint32_t>((t / NS) & 1);
+            mbar_wait(&empty[st], ph ^ 1u);
+            const uint64_t e0 = eb + t * T;
+            const uint32_t n = static_cast<uint32_t>(min(static_cast<uint64_t>(T), ee - e0));
+            if (lane == 0) mbar_expect_tx(&full[st], n * ld_in_bytes);
+            __syncwarp();
+            if (lane < n) {
+                const Edge ed = __ldg(edges + e0 + lane);
+                wbuf[st * T + lane] = __uint_as_float(ed.y);
+                bulk_g2s(buf + (static_cast<size_t>(st) * T + lane) * ld_in_bytes,
+                         reinterpret_cast<const char*>(in) + static_cast<uint64_t>(ed.x) * ld_in_bytes, ld_in_bytes,
+                         &full[st]);
+            }
+            mbar_arrive(&full[st]);
+        }
+        return;
+    }
+    const Zs z = zs_of(zeros);
+    const uint32_t col = (warp * 32 + lane) * 4;
+    const bool active = col < dim;
+    const uint32_t row = ext_out_row(ext, d);
+    float* orow = out + row * ld_out + col;
+    Acc acc = acc_load(orow, col, dim, accumulate && active);
+    for (uint64_t t = 0; t < ntiles; ++t) {
+        const int st = static_cast<int>(t % NS);
+        const uint32_t ph = static_cast<uint32_t>((t / NS) & 1);
+        mbar_wait(&full[st], ph);
+        const uint32_t n = static_cast<uint32_t>(min(static_cast<uint64_t>(T), ee - (eb + t * T)));
+        if (active) {
+            const unsigned char* sb = buf + static_cast<size_t>(st) * T * ld_in_bytes + col * 4;
+            const float* sw = wbuf + st * T;
+#pragma unroll
+            for (int j = 0; j < T; ++j)
+                if (j < static_cast<int>(n))
+                    acc_step(acc, sw[j], *reinterpret_cast<const float4*>(sb + static_cast<size_t>(j) * ld_in_bytes),
+                             z);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+    }
+    if (active) acc_store_ext(orow, col, dim, acc, z, ext, d, row);
+}
+
+void launch_hub_ring(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges, const uint32_t* order,
+                     uint32_t d_begin, uint32_t nh, const float* in, uint64_t ld_in, float* out, uint64_t ld_out,
+                     uint32_t dim, bool accumulate, cudaStream_t s, const AggExt& ext) {
+    const uint32_t nq = (dim + 3) / 4, chunks = (nq + 31) / 32;
+    const size_t smem = static_cast<size_t>(kRingStages) * kRingRows * ld_in * 4 + kRingStages * kRingRows * 4 +
+                        2 * kRingStages * 8;
+    PG_CUDA(cudaFuncSetAttribute(k_agg_hub_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    k_agg_hub_ring<<<nh, 32 * (chunks + 1), smem, s>>>(ebeg, eend, edges, order, d_begin, in,
+                                                       static_cast<uint32_t>(ld_in * 4), out, ld_out, dim, accumulate,
+                                                       kZeros, ext);
+    PG_LAUNCH("k_agg_hub_ring");
+}
+
 template <int CHQ>
 void launch_heavy(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges, const uint32_t* order, uint32_t d_begin, uint32_t nh,
                   uint32_t nq, const float* in, uint64_t ld_in, float* out, uint64_t ld_out, uint32_t dim,
@@ -2204,7 +2303,14 @@ void aggregate_det(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges
             // flight per lane, 5 column-chunk warps per 602-wide destination
             const uint32_t chunks = (nq + 31) / 32;
             const uint64_t items = static_cast<uint64_t>(nh) * chunks;
-            if (tuning(kTuneHeavyWidePipe) >= 1) {
+            // whole-row TMA ring: rows up to 8 chunks (1024 floats) and a
+            // ring that fits the 227-KB shared memory
+            if (tuning(kTuneHeavyWidePipe) == 3 && chunks <= 8 &&
+                static_cast<uint64_t>(kRingStages) * kRingRows * ld_in * 4 <= (200u << 10) &&
+                (reinterpret_cast<uintptr_t>(in) & 15) == 0) {
+                launch_hub_ring(ebeg, eend, edges, order, d_begin, nh, in, ld_in, out, ld_out, dim32, accumulate, ss.s,
+                                ext);
+            } else if (tuning(kTuneHeavyWidePipe) >= 1) {
                 k_agg_wide_pipe<16><<<grid_for(items * 32, 64), 64, 0, ss.s>>>(
                     ebeg, eend, edges, order, d_begin, items, chunks, in, static_cast<uint32_t>(ld_in * 4), out,
                     ld_out, dim32, accumulate, 0u, ext, tuning(kTuneHeavyWidePipe) == 2 ? 1 : 0);
