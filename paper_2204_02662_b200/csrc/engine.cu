@@ -155,11 +155,10 @@ __global__ void __launch_bounds__(256) k_gemm2(const float* __restrict__ a, uint
 // Register-tiled variant (tuning "gemm_packed" = 2): each thread owns an
 // 8 x 8 output tile (rows {4ty..4ty+3, 64+4ty..}, column pairs at 4tx and
 // 64+4tx of a 128 x 128 CTA tile), so per k it reads 8 A scalars and 8 B
-// values from shared memory for 32 FFMA2 + 32 FADD2. What bounds k_gemm2 is
-// the L1 -> register writeback (one cycle per register written per lane):
-// its warp-wide row tile loads one broadcast A value per row per k for only
-// 2 output columns a lane (18 registers written per 32 FP instructions);
-// here it is 16 per 64. A goes global -> shared by cp.async (16 B, zero-fill
+// values from shared memory for 32 FFMA2 + 32 FADD2 (k_gemm2's warp-wide
+// row tile loads one broadcast A value per row per k for only 2 output
+// columns a lane: 18 registers per 32 FP instructions, FMA pipe 58 % busy;
+// here 16 per 64 and the FMA pipe 88 % busy, ncu profiles/ncu_gemm_r02.json). A goes global -> shared by cp.async (16 B, zero-fill
 // past n / K), double-buffered over 16-k chunks; B arrives k-major
 // (gemm_a_bt transposes W first, a few KB). Same chain per output as k_gemm:
 // ascending k, fl(a*b) by FFMA2 with a runtime -0 addend, FADD2, then + 0.
