@@ -43,7 +43,7 @@ constexpr TuneKey kTuneKeys[] = {
     {"heavy_narrow", "PG_HEAVY_NARROW", 0},  // heavy rows <= 64 floats: 1 = k_agg_narrow_lat, 0 = coop tiles
     {"wide_lpd", "PG_WIDE_LPD", 32},       // wide rows: lanes per (destination, chunk) item, 32 or 16
     {"src_segs", "PG_SRC_SEGS", 0},        // whole-path SpMM source segments: 0 = auto (L2-sized), K = forced
-    {"ld_cg", "PG_LD_CG", 0},              // row gathers: 0/1 nc, 2 cg, 3 nc.L1::no_allocate, 4 plain, 5 nc.L1::evict_last, 6 records no_allocate
+    {"ld_cg", "PG_LD_CG", 0},              // row gathers: 0/1 nc, 2 cg, 3 nc.L1::no_allocate, 4 plain, 5 nc.L1::evict_last, 6 records no_allocate, 7 records L2 evict_first, 9 rows L2 evict_last
     {"host_chunk_order", "PG_HOST_CHUNK_ORDER", 1},  // host drop-in last pass: 1 = last row chunk first
     {"grouped_seg", "PG_GROUPED_SEG", 0},  // grouped Fast: 0 = atomic-free k_agg_grp, 1 = CTA-segmented + atomics at CTA edges, 2 = an atomic per extra group
     // heavy wide rows: software-pipelined k_agg_wide_pipe with hub items
@@ -245,6 +245,13 @@ __device__ __forceinline__ float4 ld_row(const char* base, uint32_t src, uint32_
         asm volatile("ld.global.nc.L1::evict_last.v4.f32 {%0, %1, %2, %3}, [%4];"
                      : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
                      : "l"(p));
+    else if constexpr (LDM == 9) {  // rows kept in L2 ahead of the streamed records / outputs
+        uint64_t pol;
+        asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+        asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+                     : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                     : "l"(p), "l"(pol));
+    }
     else
         asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
     return r;
@@ -436,7 +443,7 @@ __global__ void __launch_bounds__(BS, (BS == 256 ? (U <= 8 ? 4 : 2) : 1024 / BS)
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             if (FILT && !ext_src_on(ext, ed[u].x)) x[u] = make_float4(0.f, 0.f, 0.f, 0.f);  // skipped: +-0 term
-            else x[u] = ld_row<(CG >= 6 ? 0 : CG)>(base, ed[u].x, ld_in_bytes);
+            else x[u] = ld_row<(CG >= 6 && CG <= 8 ? 0 : CG)>(base, ed[u].x, ld_in_bytes);
         }
         const Zs zz = batch_dep<U>(x, z, zmask);
 #pragma unroll
@@ -453,7 +460,7 @@ __global__ void __launch_bounds__(BS, (BS == 256 ? (U <= 8 ? 4 : 2) : 1024 / BS)
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             if ((FILT && !ext_src_on(ext, ed[u].x)) || u >= static_cast<int>(n)) x[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-            else x[u] = ld_row<(CG >= 6 ? 0 : CG)>(base, ed[u].x, ld_in_bytes);
+            else x[u] = ld_row<(CG >= 6 && CG <= 8 ? 0 : CG)>(base, ed[u].x, ld_in_bytes);
         }
         const Zs zz = batch_dep<U>(x, z, zmask);
 #pragma unroll
@@ -2211,6 +2218,9 @@ void launch_vec4(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges, 
                                                           ld_out, dim, accumulate, kZeros, 0u, cm, ext);
     else if (ldm == 7)
         k_agg_vec4<LPD, U, false, 7><<<grid, 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks, in, ldb, out,
+                                                          ld_out, dim, accumulate, kZeros, 0u, cm, ext);
+    else if (ldm == 9)
+        k_agg_vec4<LPD, U, false, 9><<<grid, 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks, in, ldb, out,
                                                           ld_out, dim, accumulate, kZeros, 0u, cm, ext);
     else if (LPD == 32 && U == 8 && tuning(kTuneVecWindow) > 0)
         k_agg_vec4w<8><<<grid_for(items * LPD, 512), 512, 0, s>>>(
