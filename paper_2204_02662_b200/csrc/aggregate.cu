@@ -110,8 +110,13 @@ constexpr TuneKey kTuneKeys[] = {
     // warp slots and the later chunks finish late (e2e 23.3-24.0 vs 22.8 ms,
     // profiles/e2e_seq_sweep_r02.log), so off
     {"host_seq", "PG_HOST_SEQ", 0},
+    // W': 1 / 2 = 4 chain + 4 copy warps per block, one chain warp per SMSP
+    // (6 / 10 ring slots). Alone it is faster (products 10.6 -> 7.7 ms), but
+    // holding whole SMs it slows the forked chains it overlaps (products
+    // backward_epp 17.0 -> 28.6 ms, profiles/atb_quad_sweep_r02.log): off
+    {"atb_quad", "PG_ATB_QUAD", 0},
 };
-static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneHostSeq + 1,
+static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneAtbQuad + 1,
               "kTuneKeys and enum TuneKeyId (pg_internal.h) must list the same keys in the same order");
 std::atomic<int64_t> g_tune[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];
 int64_t g_tune_def[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];  // $PG_<KEY> at load, else built-in

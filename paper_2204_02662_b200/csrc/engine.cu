@@ -618,6 +618,121 @@ __global__ void __launch_bounds__(64) k_gemm_at_b_split(const float* __restrict_
         named_sync(empty_bar(ts), 64);
 }
 
+// Four chain warps + four copy warps per block, one block per SM (tuning
+// "atb_quad"). The FP32 pipe holds an FFMA2 / FADD2 two cycles, so a chain
+// warp's row costs 4 pipe cycles at best and two chain warps on one SMSP
+// halve each other: here every SMSP runs exactly one chain warp (warps 0-3),
+// and four copy warps (warps 4-7, each a quarter of every 64-row stage) keep
+// enough gathered rows in flight — one copy warp per block capped the ring at
+// ~128 rows per gather latency. Chain warp w owns the tile's B columns
+// [w*TCW, (w+1)*TCW): lane = (A column ti, B column pair tj). Same chain per
+// output (ascending rows, fl(a*b) by FFMA2 with a -0 addend, FADD2, + 0):
+// bit-identical.
+template <int TI, int TCW, int SL, int LAG>
+struct AtbQuadSmem {
+    float sa[SL][kAtbKC][TI];
+    float sb[SL][kAtbKC][4 * TCW];
+    uint32_t sid[LAG + 2][kAtbKC];
+};
+
+template <int TI, int TCW, int SL, int LAG>
+__global__ void __launch_bounds__(256) k_gemm_at_b_quad(const float* __restrict__ a, uint64_t lda,
+                                                       const uint32_t* __restrict__ rows, const float* __restrict__ b,
+                                                       uint64_t ldb, float* __restrict__ out, uint64_t ldo,
+                                                       uint32_t n, uint32_t r, uint32_t c, float nz) {
+    constexpr int KC = kAtbKC, NI = LAG + 2, TC = 4 * TCW, NT = 256, RPW = KC / 4;  // rows per copy warp
+    constexpr int NA = TI / 4, NB = TC / 4;  // 16-byte pieces per row
+    static_assert(TI % 4 == 0 && TC % 4 == 0 && TI * (TCW / 2) <= 32, "tile");
+    using Sm = AtbQuadSmem<TI, TCW, SL, LAG>;
+    extern __shared__ __align__(16) unsigned char atbq_smem[];
+    Sm& sm = *reinterpret_cast<Sm*>(atbq_smem);
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t i0 = blockIdx.x * TI, j0 = blockIdx.y * TC;
+    const uint32_t ntiles = (n + KC - 1) / KC;
+    auto full_bar = [](uint32_t ts) { return 1 + static_cast<int>(ts % SL); };
+    auto empty_bar = [](uint32_t ts) { return 1 + SL + static_cast<int>(ts % SL); };
+    if (warp < 4) {  // chain warp: B columns [warp*TCW, +TCW) of the tile
+        constexpr int NP = TCW / 2;
+        const bool on = lane < TI * NP;
+        const unsigned ti = on ? lane / NP : 0, tj = warp * TCW + (on ? lane % NP : 0) * 2;
+        unsigned long long nz2, acc;
+        asm("mov.b64 %0, {%1,%1};" : "=l"(nz2) : "f"(nz));
+        asm("mov.b64 %0, {%1,%1};" : "=l"(acc) : "f"(0.f));
+        for (uint32_t ts = 0; ts < ntiles; ++ts) {
+            const int slot = ts % SL;
+            named_sync(full_bar(ts), NT);
+            const float* pa = &sm.sa[slot][0][ti];
+            const unsigned long long* pb = reinterpret_cast<const unsigned long long*>(&sm.sb[slot][0][tj]);
+#pragma unroll
+            for (int kk = 0; kk < KC; ++kk) {
+                unsigned long long aa, p;
+                asm("mov.b64 %0, {%1,%1};" : "=l"(aa) : "f"(pa[kk * TI]));
+                asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p) : "l"(aa), "l"(pb[kk * (TC / 2)]), "l"(nz2));
+                asm("add.rn.f32x2 %0, %1, %2;" : "=l"(acc) : "l"(acc), "l"(p));
+            }
+            named_arrive(empty_bar(ts), NT);
+        }
+        if (!on) return;
+        float lo, hi;
+        asm("mov.b64 {%0,%1}, %2;" : "=f"(lo), "=f"(hi) : "l"(acc));
+        const uint64_t i = i0 + ti, j = j0 + tj;
+        if (i < r && j < c) out[i * ldo + j] = __fadd_rn(lo, 0.f);
+        if (i < r && j + 1 < c) out[i * ldo + j + 1] = __fadd_rn(hi, 0.f);
+        return;
+    }
+    // copy warp cw: rows [cw*RPW, (cw+1)*RPW) of every stage, 16-byte pieces,
+    // lanes sharing rows
+    const unsigned cw = warp - 4;
+    const float* a_col = a + i0;
+    const uint64_t b_stage = static_cast<uint64_t>(KC) * ldb;
+    auto fetch_id = [&](uint32_t ts, int kk) -> uint32_t {
+        const uint32_t k = ts * KC + kk;
+        return k < n ? (rows ? __ldg(rows + k) : k) : 0u;
+    };
+    for (uint32_t ts = 0; ts < ntiles + LAG; ++ts) {
+        if (ts < ntiles) {
+            if (ts >= static_cast<uint32_t>(SL)) named_sync(empty_bar(ts), NT);
+            const int slot = ts % SL;
+            const bool tail = ts * KC + KC > n;
+#pragma unroll
+            for (int q = lane; q < RPW * NA; q += 32) {
+                const int kk = cw * RPW + q / NA, qa = q % NA;
+                const bool skip = (tail && ts * KC + kk >= n) || i0 + qa * 4 >= r;
+                uint32_t id;
+                if (!rows)
+                    id = ts * KC + kk;
+                else if (ts <= static_cast<uint32_t>(LAG))
+                    id = fetch_id(ts, kk);
+                else
+                    id = sm.sid[ts % NI][kk];
+                cp_async_skip<16>(&sm.sa[slot][kk][qa * 4], skip ? a : a_col + static_cast<uint64_t>(id) * lda + qa * 4,
+                                  skip);
+            }
+#pragma unroll
+            for (int q = lane; q < RPW * NB; q += 32) {
+                const int kk = cw * RPW + q / NB, qb = q % NB;
+                const bool skip = (tail && ts * KC + kk >= n) || j0 + qb * 4 >= c;
+                cp_async_skip<16>(&sm.sb[slot][kk][qb * 4],
+                                  skip ? b : b + static_cast<uint64_t>(kk) * ldb + j0 + ts * b_stage + qb * 4, skip);
+            }
+            if (rows && lane < RPW) {  // ids of stage ts + LAG + 1 ride with this group
+                const int kk = cw * RPW + lane;
+                const uint32_t ka = (ts + LAG + 1) * KC + kk;
+                const bool skip = ka >= n;
+                cp_async_skip<4>(&sm.sid[(ts + LAG + 1) % NI][kk], skip ? rows : rows + ka, skip);
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        if (ts >= static_cast<uint32_t>(LAG)) {
+            asm volatile("cp.async.wait_group %0;" ::"n"(LAG) : "memory");
+            __syncwarp();
+            named_arrive(full_bar(ts - LAG), NT);
+        }
+    }
+    for (uint32_t ts = ntiles > static_cast<uint32_t>(SL) ? ntiles : SL; ts < ntiles + SL; ++ts)
+        named_sync(empty_bar(ts), NT);
+}
+
 // one-column-per-lane blocks (64 chains each) beyond ~1.5 per SM: use 2
 bool gemm_at_b_chain_pairs(uint64_t r, uint64_t c) {
     if (!tuning(kTuneAtbSplit) || tuning(kTuneAtbPairs) == 0) return false;
@@ -885,6 +1000,63 @@ void gemm_at_b(DMat a, const uint32_t* a_rows, DMat b, DMat out, cudaStream_t s)
     if (tuning(kTuneGemmTc) == 1 && gemm_at_b_tc_supported(r, c) && a.ld % 4 == 0 && b.ld % 4 == 0 &&
         reinterpret_cast<uintptr_t>(a.p) % 16 == 0 && reinterpret_cast<uintptr_t>(b.p) % 16 == 0) {
         gemm_at_b_tc(a, a_rows, b, out, s);
+        return;
+    }
+    // one chain warp per SMSP (k_gemm_at_b_quad, tuning atb_quad): the tile
+    // shape whose block count comes closest to one block per SM
+    const bool v4 = a.ld % 4 == 0 && b.ld % 4 == 0 && reinterpret_cast<uintptr_t>(a.p) % 16 == 0 &&
+                    reinterpret_cast<uintptr_t>(b.p) % 16 == 0;
+    // (wide outputs only: at c = 16 / 41 the 32-column tiles leave chain
+    // warps idle and the split kernel wins, Reddit 1.92 vs 1.32 ms)
+    if (tuning(kTuneAtbQuad) && tuning(kTuneAtbSplit) && v4 && c >= 64) {
+        int dev = 0, sms = 148;
+        PG_CUDA(cudaGetDevice(&dev));
+        PG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        struct Cand {
+            int ti, tcw;
+        };
+        const Cand cands[] = {{8, 8}, {16, 4}, {8, 4}, {4, 8}, {4, 4}};
+        int best = -1;
+        uint64_t best_blocks = 0;
+        const uint64_t sm64 = static_cast<uint64_t>(sms);
+        for (int k = 0; k < 5; ++k) {
+            const uint64_t bl =
+                ((r + cands[k].ti - 1) / cands[k].ti) * ((c + 4 * cands[k].tcw - 1) / (4 * cands[k].tcw));
+            const bool better = best < 0 ? true
+                                : bl <= sm64 ? (best_blocks > sm64 || bl > best_blocks)
+                                             : (best_blocks > sm64 && bl < best_blocks);
+            if (better) {
+                best = k;
+                best_blocks = bl;
+            }
+        }
+        volatile float nz = -0.f;
+        const uint32_t n32 = static_cast<uint32_t>(n), r32 = static_cast<uint32_t>(r), c32 = static_cast<uint32_t>(c);
+        const Cand cd = cands[best];
+        const dim3 grid(static_cast<unsigned>((r + cd.ti - 1) / cd.ti),
+                        static_cast<unsigned>((c + 4 * cd.tcw - 1) / (4 * cd.tcw)));
+        auto go = [&](auto kern, size_t smem) {
+            PG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+            kern<<<grid, 256, smem, s>>>(a.p, a.ld, a_rows, b.p, b.ld, out.p, out.ld, n32, r32, c32, nz);
+        };
+        auto pick = [&](auto qs, auto ql) {  // slots / stages in flight
+            constexpr int QS = decltype(qs)::value, QL = decltype(ql)::value;
+            if (cd.ti == 8 && cd.tcw == 8)
+                go(k_gemm_at_b_quad<8, 8, QS, QL>, sizeof(AtbQuadSmem<8, 8, QS, QL>));
+            else if (cd.ti == 16)
+                go(k_gemm_at_b_quad<16, 4, QS, QL>, sizeof(AtbQuadSmem<16, 4, QS, QL>));
+            else if (cd.ti == 8)
+                go(k_gemm_at_b_quad<8, 4, QS, QL>, sizeof(AtbQuadSmem<8, 4, QS, QL>));
+            else if (cd.tcw == 8)
+                go(k_gemm_at_b_quad<4, 8, QS, QL>, sizeof(AtbQuadSmem<4, 8, QS, QL>));
+            else
+                go(k_gemm_at_b_quad<4, 4, QS, QL>, sizeof(AtbQuadSmem<4, 4, QS, QL>));
+        };
+        if (tuning(kTuneAtbQuad) == 2)
+            pick(std::integral_constant<int, 10>{}, std::integral_constant<int, 8>{});
+        else
+            pick(std::integral_constant<int, 6>{}, std::integral_constant<int, 4>{});
+        PG_LAUNCH("k_gemm_at_b_quad");
         return;
     }
     // 64 chains per warp: 4 (or 8) A columns x 16 (or 8) B columns

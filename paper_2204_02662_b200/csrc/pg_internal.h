@@ -369,7 +369,8 @@ enum TuneKeyId {
     kTuneNarrowU = 40,
     kTuneAtbDepth = 41,
     kTuneHostFirstChunkPct = 42,
-    kTuneHostSeq = 43
+    kTuneHostSeq = 43,
+    kTuneAtbQuad = 44
 };
 // whole-row SpMM warps (k_agg_row) for this width (tuning "row_kernel")
 bool row_kernel_on(uint64_t dim);

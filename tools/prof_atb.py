@@ -26,8 +26,9 @@ def main():
         g.uniform_(-1, 1)
         ids = torch.sort(torch.randperm(ry, device="cuda")[:n].to(torch.int32))[0]
         res, outs = {}, {}
-        for depth in (0, 1, 2):
-            pg.set_tuning("atb_depth", depth)
+        for depth in (0, 1, 2, 3, 4):
+            pg.set_tuning("atb_depth", depth if depth < 3 else 0)
+            pg.set_tuning("atb_quad", 0 if depth < 3 else depth - 2)
             o = pg.empty_rows(ind, outd)
             pg.gemm_at_b(y, g, o, a_rows=ids)
             torch.cuda.synchronize()
@@ -42,9 +43,11 @@ def main():
             res[depth] = statistics.median(ts)
             outs[depth] = o
         pg.set_tuning("atb_depth", None)
+        pg.set_tuning("atb_quad", None)
         same = all(torch.equal(outs[0].view(torch.int32), o.view(torch.int32)) for o in outs.values())
         print(f"{name:22s} n={n} {ind}x{outd}: row per lane 4/2 {res[0]:.3f} ms, 7/5 {res[1]:.3f} ms, "
-              f"rows shared by lanes {res[2]:.3f} ms ({res[2] * 1e6 * 1.95 / n:.1f} cycles per row); "
+              f"rows shared by lanes {res[2]:.3f} ms, 4 chain + 4 copy warps per block 6/4 {res[3]:.3f} ms, "
+              f"10/8 {res[4]:.3f} ms ({res[4] * 1e6 * 1.95 / n:.1f} cycles per row); "
               f"bit-identical: {same}", flush=True)
         del y, g, ids, outs
         torch.cuda.empty_cache()
