@@ -49,7 +49,9 @@ constexpr TuneKey kTuneKeys[] = {
     // heavy wide rows: software-pipelined k_agg_wide_pipe with hub items
     // destination-major (1) or chunk-major (2); 3 = whole-row TMA ring
     // (k_agg_hub_ring: measured slower, its ~80 KB ring holds only 32 rows in
-    // flight per hub, profiles/e2e_hub_ring_sweep_r02.log); 0 = k_agg_wide_lat
+    // flight per hub, profiles/e2e_hub_ring_sweep_r02.log); 4 = cooperative
+    // 64-row tiles (k_agg_heavy_coop<32>: slower still, 64 KB + 256 threads
+    // per hub chunk, profiles/e2e_hub_coop_sweep_r02.log); 0 = k_agg_wide_lat
     {"heavy_wide_pipe", "PG_HEAVY_WIDE_PIPE", 1},
     {"host_final_segs", "PG_HOST_FINAL_SEGS", 1},  // host drop-in: trailing source segments of the chunked last pass
     {"host_pitch2d", "PG_HOST_PITCH2D", 0},  // host drop-in: odd widths by 2-D DMA (1) or flat DMA + repack kernel (0)
@@ -1693,7 +1695,21 @@ __global__ void __launch_bounds__(256) k_agg_heavy_coop(const uint64_t* __restri
                 const uint32_t n = static_cast<uint32_t>(min(static_cast<uint64_t>(T), ee - (eb + t * T)));
                 const float4* sb = tile + b * T * CHQ + lane;
                 const float* sw = wt + b * T;
-                for (uint32_t j = 0; j < n; ++j) acc_step(acc, sw[j], sb[j * CHQ], z);
+                // 8 rows' loads ahead of their chain steps (the serial chain
+                // is the hub's critical path, not the LDS latency)
+                uint32_t j = 0;
+                for (; j + 8 <= n; j += 8) {
+                    float pw[8];
+                    float4 px[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        pw[u] = sw[j + u];
+                        px[u] = sb[(j + u) * CHQ];
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) acc_step(acc, pw[u], px[u], z);
+                }
+                for (; j < n; ++j) acc_step(acc, sw[j], sb[j * CHQ], z);
             }
             if (t + 1 < ntiles) stash(b ^ 1);
             __syncthreads();
@@ -2336,7 +2352,13 @@ void aggregate_det(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges
             const uint64_t items = static_cast<uint64_t>(nh) * chunks;
             // whole-row TMA ring: rows up to 8 chunks (1024 floats) and a
             // ring that fits the 227-KB shared memory
-            if (tuning(kTuneHeavyWidePipe) == 3 && chunks <= 8 &&
+            if (tuning(kTuneHeavyWidePipe) == 4) {
+                // cooperative tiles: all eight warps of a (hub, 128-column
+                // chunk) CTA gather 64-row tiles into shared memory while
+                // warp 0 folds the previous one
+                launch_heavy_coop<32, false>(ebeg, eend, edges, order, d_begin, nh, nq, in, ld_in, out, ld_out, dim32,
+                                             accumulate, ss.s, ext);
+            } else if (tuning(kTuneHeavyWidePipe) == 3 && chunks <= 8 &&
                 static_cast<uint64_t>(kRingStages) * kRingRows * ld_in * 4 <= (200u << 10) &&
                 (reinterpret_cast<uintptr_t>(in) & 15) == 0) {
                 launch_hub_ring(ebeg, eend, edges, order, d_begin, nh, in, ld_in, out, ld_out, dim32, accumulate, ss.s,

@@ -144,7 +144,8 @@ def test_heavy_ring_kernel_bit_exact(pg, orc, dim, heavy_min, kern):
                                      {"row_kernel": 1, "row_u": 4, "row_heavy": 64}, {"vec_block": 512},
                                      {"vec_block": 1024}, {"ld_cg": 7}, {"hub_inline": 0, "heavy_wide_pipe": 2},
                                      {"hub_inline": 0}, {"hub_inline": 1, "hub_front_min": 8}, {"rec_window": 2},
-                                     {"vec_window": 4}, {"hub_inline": 0, "heavy_wide_pipe": 3}])
+                                     {"vec_window": 4}, {"hub_inline": 0, "heavy_wide_pipe": 3},
+                                     {"hub_inline": 0, "heavy_wide_pipe": 4}])
 @pytest.mark.parametrize("dim", [130, 300, 602, 700])
 def test_wide_row_schedule_variants_bit_exact(pg, orc, dim, variant):
     """The measured-and-kept-selectable wide-row schedules:
