@@ -117,8 +117,12 @@ constexpr TuneKey kTuneKeys[] = {
     // holding whole SMs it slows the forked chains it overlaps (products
     // backward_epp 17.0 -> 28.6 ms, profiles/atb_quad_sweep_r02.log): off
     {"atb_quad", "PG_ATB_QUAD", 0},
+    // host drop-in below host_min_mb: D2H-overlap chunks (0/1 = off; the
+    // Reddit top path split in 2 computes 0.94 vs 0.62 ms, so no gain:
+    // profiles/e2e_small_chunks_sweep_r02.log)
+    {"host_small_chunks", "PG_HOST_SMALL_CHUNKS", 0},
 };
-static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneAtbQuad + 1,
+static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneHostSmallChunks + 1,
               "kTuneKeys and enum TuneKeyId (pg_internal.h) must list the same keys in the same order");
 std::atomic<int64_t> g_tune[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];
 int64_t g_tune_def[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];  // $PG_<KEY> at load, else built-in

@@ -729,7 +729,14 @@ void run_host(Groups& G, bool parent_indexed, const float* in_host, uint64_t in_
     // only when gathers dominate (E >= 64 D), like the device-side rule
     const uint32_t K = (big && parent_indexed && in_rows >= 4 && b.E >= 64ull * D)
                            ? static_cast<uint32_t>(std::clamp<int64_t>(tuning(kTuneHostSegs), 1, 8)) : 1;
-    const uint32_t R = big ? static_cast<uint32_t>(std::clamp<int64_t>(tuning(kTuneHostChunks), 1, 16)) : 1;
+    // below the floor, paths with >= 4 MB of output still overlap their D2H
+    // with a few destination chunks (tuning host_small_chunks; no source
+    // segments: the input is small)
+    const bool small_pipe = !big && G.path && D >= 16384 && dim * 4 * D >= (4ull << 20) &&
+                            tuning(kTuneHostSmallChunks) > 1;
+    const uint32_t R = big ? static_cast<uint32_t>(std::clamp<int64_t>(tuning(kTuneHostChunks), 1, 16))
+                       : small_pipe ? static_cast<uint32_t>(std::clamp<int64_t>(tuning(kTuneHostSmallChunks), 1, 16))
+                                    : 1;
     // the last F segments form the chunked last pass (its D2H overlaps the
     // next chunk); the K - F before it are whole-row passes under the H2D
     const uint32_t F = static_cast<uint32_t>(std::clamp<int64_t>(tuning(kTuneHostFinalSegs), 1, K));

@@ -370,7 +370,8 @@ enum TuneKeyId {
     kTuneAtbDepth = 41,
     kTuneHostFirstChunkPct = 42,
     kTuneHostSeq = 43,
-    kTuneAtbQuad = 44
+    kTuneAtbQuad = 44,
+    kTuneHostSmallChunks = 45
 };
 // whole-row SpMM warps (k_agg_row) for this width (tuning "row_kernel")
 bool row_kernel_on(uint64_t dim);

@@ -104,7 +104,8 @@ def test_tuning_keys(pg):
                 "host_chunk_balance", "atb_split", "atb_pairs", "gemm_packed", "host_last_seg_pct", "wgrad_fork",
                 "gemm_tc", "rec_window", "src_seg_balance", "host_min_mb", "row_kernel", "row_u", "row_seg_mb",
                 "row_heavy", "vec_block", "hub_inline", "hub_front_min", "gemm3_rows", "gemm_beside_wgrad", "host_hub_chunk_side", "vec_window", "host_hub_min", "grouped_src_segs", "narrow_u", "atb_depth",
-                "host_first_chunk_pct", "host_seq", "atb_quad"):
+                "host_first_chunk_pct", "host_seq", "atb_quad",
+                "host_small_chunks"):
         pg.set_tuning(key, None)
     import pytest
 

@@ -98,6 +98,7 @@ HOST_KNOBS = {
     "host_hub_chunk_side": (0, 1, 2),
     "host_first_chunk_pct": (100, 50, 10),
     "host_seq": (0, 1, 2),
+    "host_small_chunks": (0, 2),
     "host_hub_min": (1, 64, 16384),
 }
 
