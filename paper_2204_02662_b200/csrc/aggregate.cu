@@ -121,8 +121,11 @@ constexpr TuneKey kTuneKeys[] = {
     // Reddit top path split in 2 computes 0.94 vs 0.62 ms, so no gain:
     // profiles/e2e_small_chunks_sweep_r02.log)
     {"host_small_chunks", "PG_HOST_SMALL_CHUNKS", 0},
+    // wide rows: 256-bit row gathers, two 128-column items per warp
+    // (k_agg_vec8): 1 on, 0 off, 2 auto (from 2^21 edges per call)
+    {"vec8", "PG_VEC8", 2},
 };
-static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneHostSmallChunks + 1,
+static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneVec8 + 1,
               "kTuneKeys and enum TuneKeyId (pg_internal.h) must list the same keys in the same order");
 std::atomic<int64_t> g_tune[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];
 int64_t g_tune_def[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];  // $PG_<KEY> at load, else built-in
@@ -479,6 +482,93 @@ __global__ void __launch_bounds__(BS, (BS == 256 ? (U <= 8 ? 4 : 2) : 1024 / BS)
             if (u < static_cast<int>(n)) acc_step(acc, __uint_as_float(ed[u].y), x[u], zz);
     }
     acc_store_ext(orow, col, dim, acc, z, ext, d, row);
+}
+
+// 256-bit row gathers (tuning "vec8"): sm_100 has LDG.E.ENL2.256, one
+// 32-byte load per lane. 16 lanes cover a 128-column chunk (8 floats each),
+// so a warp carries TWO (destination, chunk) items — the same items, chunk
+// order and per-column fp32 chains as k_agg_vec4<32, 2U>, with half the
+// load instructions per gathered byte and one record load (two addresses)
+// per edge pair instead of one broadcast per edge. Needs a 32-byte aligned
+// input and an 8-float row pitch.
+__device__ __forceinline__ void ld_row8(const char* base, uint32_t src, uint32_t ld_bytes, float4& a, float4& b) {
+    const char* p = base + static_cast<uint64_t>(src) * ld_bytes;
+    asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+                 : "l"(p));
+}
+template <int U>
+__global__ void __launch_bounds__(256, 4) k_agg_vec8(const uint64_t* __restrict__ ebeg, const uint64_t* __restrict__ eend,
+                                                     const Edge* __restrict__ edges,
+                                                     const uint32_t* __restrict__ order, uint32_t d_begin,
+                                                     uint64_t n_items, uint32_t chunks,
+                                                     const float* __restrict__ in, uint32_t ld_in_bytes,
+                                                     float* __restrict__ out, uint64_t ld_out, uint32_t dim,
+                                                     int accumulate, float2 zeros, uint32_t zmask, int chunk_major,
+                                                     AggExt ext) {
+    constexpr int LPD = 16;
+    const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    const uint64_t item = t / LPD;
+    if (item >= n_items) return;
+    const Zs z = zs_of(zeros);
+    const uint64_t nd = n_items / chunks;
+    const uint64_t nf = chunk_major > 1 ? static_cast<uint64_t>(chunk_major - 2) : 0;
+    uint32_t di, ci;
+    if (!chunk_major || item < nf * chunks) {
+        di = static_cast<uint32_t>(item / chunks);
+        ci = static_cast<uint32_t>(item % chunks);
+    } else {
+        const uint64_t r = item - nf * chunks, nr = nd - nf;
+        di = static_cast<uint32_t>(nf + r % nr);
+        ci = static_cast<uint32_t>(r / nr);
+    }
+    const uint32_t d = __ldg(order + d_begin + di);
+    const uint32_t col = ci * 128u + static_cast<uint32_t>(t % LPD) * 8u;
+    const bool active = col < dim;
+    uint64_t e = __ldg(ebeg + d);
+    const uint64_t end = __ldg(eend + d);
+    const char* base = reinterpret_cast<const char*>(in) + (active ? col : ci * 128u) * 4u;
+    asm("mov.b64 %0, %0;" : "+l"(base));
+    const uint32_t row = ext_out_row(ext, d);
+    float* orow = out + row * ld_out + col;
+    Acc a0 = acc_load(orow, col, dim, accumulate), a1 = acc_load(orow + 4, col + 4, dim, accumulate);
+    for (; e + U <= end; e += U) {
+        Edge ed[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) ed[u] = ld_rec(edges + e + u);
+        float4 x[2 * U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) ld_row8(base, ed[u].x, ld_in_bytes, x[2 * u], x[2 * u + 1]);
+        const Zs zz = batch_dep<2 * U>(x, z, zmask);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const float w = __uint_as_float(ed[u].y);
+            acc_step(a0, w, x[2 * u], zz);
+            acc_step(a1, w, x[2 * u + 1], zz);
+        }
+    }
+    if (e < end) {
+        const uint32_t n = static_cast<uint32_t>(end - e);
+        Edge ed[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) ed[u] = ld_rec(edges + e + (u < static_cast<int>(n) ? u : n - 1));
+        float4 x[2 * U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (u < static_cast<int>(n)) ld_row8(base, ed[u].x, ld_in_bytes, x[2 * u], x[2 * u + 1]);
+            else x[2 * u] = x[2 * u + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        const Zs zz = batch_dep<2 * U>(x, z, zmask);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (u < static_cast<int>(n)) {
+                const float w = __uint_as_float(ed[u].y);
+                acc_step(a0, w, x[2 * u], zz);
+                acc_step(a1, w, x[2 * u + 1], zz);
+            }
+    }
+    acc_store_ext(orow, col, dim, a0, z, ext, d, row);
+    acc_store_ext(orow + 4, col + 4, dim, a1, z, ext, d, row);
 }
 
 // Whole-row warps for wide rows (tuning "row_kernel"): one warp per
@@ -2221,6 +2311,15 @@ SideStream& side_stream(cudaStream_t caller) {
     return ss;
 }
 
+// 256-bit gathers: 1 on, 0 off, 2 (default) from 2^21 edges per call. On
+// small calls (arxiv, 0.6-1.1M edges: 0.24 -> 0.36 ms) the longest lists —
+// twice the columns per lane — set the length; on the large ones the halved
+// load count wins (Reddit layer 0 15.65 -> 15.15 ms, products 4.77 -> 4.13)
+bool vec8_on(const AggExt& ext) {
+    const int64_t v = tuning(kTuneVec8);
+    return v == 1 || (v == 2 && ext.n_edges >= (1ull << 21));
+}
+
 template <int LPD, int U>
 void launch_vec4(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges, const uint32_t* order, uint32_t d_begin,
                  uint32_t nd, uint32_t chunks, const float* in, uint64_t ld_in, float* out, uint64_t ld_out,
@@ -2236,6 +2335,10 @@ void launch_vec4(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges, 
     if (ext.src_bits || ext.dst_bits)
         k_agg_vec4<LPD, U, true><<<grid, 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks, in, ldb, out,
                                                       ld_out, dim, accumulate, kZeros, 0u, cm, ext);
+    else if (LPD == 32 && U <= 8 && vec8_on(ext) && ldb % 32 == 0 && reinterpret_cast<uintptr_t>(in) % 32 == 0)
+        k_agg_vec8<(U >= 2 ? U / 2 : 1)><<<grid_for(items * 16, 256), 256, 0, s>>>(
+            ebeg, eend, edges, order, d_begin, items, chunks, in, ldb, out, ld_out, dim, accumulate, kZeros, 0u, cm,
+            ext);
     else if (LPD == 32 && tuning(kTuneRecWindow) == 2)
         k_agg_vec4<LPD, U, false, 8, true><<<grid, 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks, in,
                                                                 ldb, out, ld_out, dim, accumulate, kZeros, 0u, cm, ext);

@@ -358,6 +358,7 @@ void pg::run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re,
         if (rb == 0 && re == p.D) {
             AggExt ew = ext;
             ew.avg_degree = p.E / range_div / std::max<uint64_t>(1, p.D);
+            ew.n_edges = p.E / range_div;
             aggregate_det(eb, ee, edges, p.order.get(), p.D, 0, p.D,
                           p.hist.heavy(heavy_degree(dim, p.E / range_div)), in, ld_in, out, ld_out, dim,
                           accumulate, s, ew);
@@ -368,6 +369,7 @@ void pg::run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re,
         AggExt er = ext;
         er.side_hubs = true;  // a row range: hub chains on the deeper-pipelined side kernel
         er.avg_degree = rs->hist.edges / range_div / std::max<uint64_t>(1, re - rb);
+        er.n_edges = rs->hist.edges / range_div;
         const uint32_t nh = rs->hist.heavy(heavy_degree(dim, rs->hist.edges / range_div));
         const uint32_t nd = re - rb;
         if (ext.part) {
@@ -407,6 +409,7 @@ void pg::run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re,
             AggExt ek = ext;
             if (k + 1 < K) ek.relu_pre = nullptr;  // the epilogue applies to finished rows only
             ek.avg_degree = g.m / K / std::max<uint64_t>(1, g.n);
+            ek.n_edges = g.m / K;
             const uint64_t* eb = G.auto_seg_bnd.get() + static_cast<uint64_t>(k) * g.n;
             aggregate_det(eb, eb + g.n, g.edges.get(), G.graph_order.get(), g.n, 0, g.n,
                           G.graph_hist.heavy(heavy_degree(dim, g.m / K)), in, ld_in, out, ld_out, dim,
@@ -416,6 +419,7 @@ void pg::run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re,
     }
     AggExt ew = ext;
     ew.avg_degree = g.m / std::max<uint64_t>(1, g.n);
+    ew.n_edges = g.m;
     aggregate_det(g.offsets.get(), g.offsets.get() + 1, g.edges.get(), G.graph_order.get(), g.n, 0, g.n,
                   G.graph_hist.heavy(heavy_degree(dim, g.m)), in, ld_in, out, ld_out, dim, accumulate, s, ew);
 }

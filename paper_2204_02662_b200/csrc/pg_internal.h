@@ -243,6 +243,9 @@ struct AggExt {
     // scheduling only: the call's average edges per destination (0 unknown);
     // very short lists (< 8) gather 4 edges per batch instead of 8
     uint64_t avg_degree = 0;
+    // scheduling only: the call's edge count (0 unknown); 256-bit gathers
+    // (tuning vec8 auto) from 2^21 edges on
+    uint64_t n_edges = 0;
     bool any() const { return out_rows || relu_pre || src_bits || dst_bits; }
 };
 
@@ -371,7 +374,8 @@ enum TuneKeyId {
     kTuneHostFirstChunkPct = 42,
     kTuneHostSeq = 43,
     kTuneAtbQuad = 44,
-    kTuneHostSmallChunks = 45
+    kTuneHostSmallChunks = 45,
+    kTuneVec8 = 46
 };
 // whole-row SpMM warps (k_agg_row) for this width (tuning "row_kernel")
 bool row_kernel_on(uint64_t dim);

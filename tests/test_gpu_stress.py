@@ -29,6 +29,7 @@ KNOBS = {
     "row_u": (2, 3, 4),
     "row_seg_mb": (8, 56),
     "vec_block": (256, 256, 512, 1024),
+    "vec8": (0, 1, 2, 2),
     "hub_inline": (0, 1, 1),
     "hub_front_min": (0, 0, 16, 256),
 }

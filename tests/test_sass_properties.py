@@ -83,3 +83,16 @@ def test_default_spmm_gathers_are_128_bit(sass):
             assert "LDG.E.128" in body, name
             assert re.search(r"\bFADD2\b", body), name
             assert not GLOBAL_ATOMIC.search(body), name
+
+
+def test_wide_spmm_gathers_are_256_bit(sass):
+    """k_agg_vec8 (the wide-row default from 2^21 edges per call): every
+    row gather one 256-bit load per lane and edge (LDG.E.ENL2.256), the unfused
+    FFMA2 + FADD2 chain step, no spills, no global atomics."""
+    for name, body in _kernels(sass, r"k_agg_vec8ILi4E").items():
+        # U = 4 gathers in the batch loop + 4 in the remainder batch (the
+        # two LDG.E.128 left are the accumulate-mode output loads)
+        assert len(re.findall(r"LDG\.E\.ENL2\.256", body)) >= 8, name
+        assert re.search(r"\bFFMA2\b", body) and re.search(r"\bFADD2\b", body), name
+        assert not re.search(r"\b(STL|LDL)\b", body), name
+        assert not GLOBAL_ATOMIC.search(body), name
