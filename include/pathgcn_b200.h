@@ -104,7 +104,10 @@ int pg_set_heavy_min_degree(uint64_t min_degree);
  * 512 / 1024), "vec_window" (source-window lockstep CTAs), "narrow_u",
  * "grouped_src_segs" (grouped Fast over L2-sized segments), "gemm_packed"
  * (2, default: register-tiled k_gemm3; 1: k_gemm2; 0: k_gemm), "gemm3_rows",
- * "gemm_beside_wgrad", "atb_depth", "host_hub_chunk_side" + "host_hub_min".
+ * "gemm_beside_wgrad", "atb_depth", "host_hub_chunk_side" + "host_hub_min",
+ * "host_first_chunk_pct", "host_seq", "atb_quad", "host_small_chunks",
+ * "vec8" (2, default: 256-bit row gathers for rows wider than 64 columns
+ * from 2^21 edges per call; 1: every width; 0: off).
  * A negative value restores the default ($PG_<KEY> at load, else built-in).
  * Unknown key -> PG_ERR_CONFIG. */
 int pg_set_tuning(const char* key, int64_t value);

@@ -122,7 +122,8 @@ constexpr TuneKey kTuneKeys[] = {
     // profiles/e2e_small_chunks_sweep_r02.log)
     {"host_small_chunks", "PG_HOST_SMALL_CHUNKS", 0},
     // wide rows: 256-bit row gathers, two 128-column items per warp
-    // (k_agg_vec8): 1 on, 0 off, 2 auto (from 2^21 edges per call)
+    // (k_agg_vec8): 1 on, 0 off, 2 auto (rows wider than 64 columns, from
+    // 2^21 edges per call)
     {"vec8", "PG_VEC8", 2},
 };
 static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneVec8 + 1,
@@ -485,19 +486,21 @@ __global__ void __launch_bounds__(BS, (BS == 256 ? (U <= 8 ? 4 : 2) : 1024 / BS)
 }
 
 // 256-bit row gathers (tuning "vec8"): sm_100 has LDG.E.ENL2.256, one
-// 32-byte load per lane. 16 lanes cover a 128-column chunk (8 floats each),
-// so a warp carries TWO (destination, chunk) items — the same items, chunk
-// order and per-column fp32 chains as k_agg_vec4<32, 2U>, with half the
-// load instructions per gathered byte and one record load (two addresses)
-// per edge pair instead of one broadcast per edge. Needs a 32-byte aligned
-// input and an 8-float row pitch.
+// 32-byte load per lane. LPD lanes of 8 floats own a (destination, chunk):
+// LPD = 16 covers a 128-column chunk, so a warp carries TWO items of
+// k_agg_vec4<32>'s — the same items, chunk order and per-column fp32
+// chains, with half the load instructions per gathered byte and one record
+// load (two addresses) per edge pair instead of one broadcast per edge;
+// LPD = 2 / 4 / 8 are k_agg_vec4<4 / 8 / 16>'s narrow rows (widths <= 16 /
+// 32 / 64) with the batch's records spread over the sub-warp and shuffled.
+// Needs a 32-byte aligned input and an 8-float row pitch.
 __device__ __forceinline__ void ld_row8(const char* base, uint32_t src, uint32_t ld_bytes, float4& a, float4& b) {
     const char* p = base + static_cast<uint64_t>(src) * ld_bytes;
     asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
                  : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
                  : "l"(p));
 }
-template <int U>
+template <int LPD, int U, bool FILT>
 __global__ void __launch_bounds__(256, 4) k_agg_vec8(const uint64_t* __restrict__ ebeg, const uint64_t* __restrict__ eend,
                                                      const Edge* __restrict__ edges,
                                                      const uint32_t* __restrict__ order, uint32_t d_begin,
@@ -506,7 +509,6 @@ __global__ void __launch_bounds__(256, 4) k_agg_vec8(const uint64_t* __restrict_
                                                      float* __restrict__ out, uint64_t ld_out, uint32_t dim,
                                                      int accumulate, float2 zeros, uint32_t zmask, int chunk_major,
                                                      AggExt ext) {
-    constexpr int LPD = 16;
     const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     const uint64_t item = t / LPD;
     if (item >= n_items) return;
@@ -523,22 +525,48 @@ __global__ void __launch_bounds__(256, 4) k_agg_vec8(const uint64_t* __restrict_
         ci = static_cast<uint32_t>(r / nr);
     }
     const uint32_t d = __ldg(order + d_begin + di);
-    const uint32_t col = ci * 128u + static_cast<uint32_t>(t % LPD) * 8u;
+    if (FILT && !ext_dst_on(ext, d)) return;
+    constexpr uint32_t kChunk = 8u * LPD;
+    const unsigned sl = static_cast<unsigned>(t % LPD);
+    const uint32_t col = ci * kChunk + sl * 8u;
     const bool active = col < dim;
     uint64_t e = __ldg(ebeg + d);
     const uint64_t end = __ldg(eend + d);
-    const char* base = reinterpret_cast<const char*>(in) + (active ? col : ci * 128u) * 4u;
+    const char* base = reinterpret_cast<const char*>(in) + (active ? col : ci * kChunk) * 4u;
     asm("mov.b64 %0, %0;" : "+l"(base));
     const uint32_t row = ext_out_row(ext, d);
     float* orow = out + row * ld_out + col;
     Acc a0 = acc_load(orow, col, dim, accumulate), a1 = acc_load(orow + 4, col + 4, dim, accumulate);
+    constexpr int NPL = (U + LPD - 1) / LPD;
+    const unsigned submask = LPD >= 32 ? 0xffffffffu : (((1u << LPD) - 1u) << (lane_id() & ~(LPD - 1u)));
+    auto batch_recs = [&](Edge (&ed)[U], uint32_t n) {
+        if constexpr (LPD <= 8) {
+            Edge mine[NPL];
+#pragma unroll
+            for (int i = 0; i < NPL; ++i) {
+                const unsigned k = sl + i * LPD;
+                mine[i] = ld_rec(edges + e + (k < n ? k : n - 1));
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                ed[u].x = __shfl_sync(submask, mine[u / LPD].x, u % LPD, LPD);
+                ed[u].y = __shfl_sync(submask, mine[u / LPD].y, u % LPD, LPD);
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < U; ++u) ed[u] = ld_rec(edges + e + (u < static_cast<int>(n) ? u : n - 1));
+        }
+    };
+    auto gather = [&](const Edge& ed, float4& xa, float4& xb) {
+        if (FILT && !ext_src_on(ext, ed.x)) xa = xb = make_float4(0.f, 0.f, 0.f, 0.f);  // skipped: +-0 term
+        else ld_row8(base, ed.x, ld_in_bytes, xa, xb);
+    };
     for (; e + U <= end; e += U) {
         Edge ed[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) ed[u] = ld_rec(edges + e + u);
+        batch_recs(ed, U);
         float4 x[2 * U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) ld_row8(base, ed[u].x, ld_in_bytes, x[2 * u], x[2 * u + 1]);
+        for (int u = 0; u < U; ++u) gather(ed[u], x[2 * u], x[2 * u + 1]);
         const Zs zz = batch_dep<2 * U>(x, z, zmask);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -550,12 +578,11 @@ __global__ void __launch_bounds__(256, 4) k_agg_vec8(const uint64_t* __restrict_
     if (e < end) {
         const uint32_t n = static_cast<uint32_t>(end - e);
         Edge ed[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) ed[u] = ld_rec(edges + e + (u < static_cast<int>(n) ? u : n - 1));
+        batch_recs(ed, n);
         float4 x[2 * U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            if (u < static_cast<int>(n)) ld_row8(base, ed[u].x, ld_in_bytes, x[2 * u], x[2 * u + 1]);
+            if (u < static_cast<int>(n)) gather(ed[u], x[2 * u], x[2 * u + 1]);
             else x[2 * u] = x[2 * u + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
         const Zs zz = batch_dep<2 * U>(x, z, zmask);
@@ -2315,9 +2342,11 @@ SideStream& side_stream(cudaStream_t caller) {
 // small calls (arxiv, 0.6-1.1M edges: 0.24 -> 0.36 ms) the longest lists —
 // twice the columns per lane — set the length; on the large ones the halved
 // load count wins (Reddit layer 0 15.65 -> 15.15 ms, products 4.77 -> 4.13)
-bool vec8_on(const AggExt& ext) {
+// Narrow rows (2 / 4 / 8 lanes of 8 floats) only when forced: the Reddit top
+// path (width 16, 75.6M edges) runs 0.61 -> 0.94 ms with them.
+bool vec8_on(const AggExt& ext, int lpd) {
     const int64_t v = tuning(kTuneVec8);
-    return v == 1 || (v == 2 && ext.n_edges >= (1ull << 21));
+    return v == 1 || (v == 2 && lpd == 32 && ext.n_edges >= (1ull << 21));
 }
 
 template <int LPD, int U>
@@ -2332,13 +2361,24 @@ void launch_vec4(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges, 
     const int ldm = static_cast<int>(tuning(kTuneLdCg));
     const unsigned grid = grid_for(items * LPD, 256);
     const uint32_t ldb = static_cast<uint32_t>(ld_in * 4);
+    if constexpr (U <= 8 && LPD >= 4) {
+        if (vec8_on(ext, LPD) && ldb % 32 == 0 && reinterpret_cast<uintptr_t>(in) % 32 == 0) {
+            constexpr int U8 = U / 2;
+            const unsigned g8 = grid_for(items * (LPD / 2), 256);
+            if (ext.src_bits || ext.dst_bits)
+                k_agg_vec8<LPD / 2, U8, true><<<g8, 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks, in,
+                                                                 ldb, out, ld_out, dim, accumulate, kZeros, 0u, cm, ext);
+            else
+                k_agg_vec8<LPD / 2, U8, false><<<g8, 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks,
+                                                                  in, ldb, out, ld_out, dim, accumulate, kZeros, 0u,
+                                                                  cm, ext);
+            PG_LAUNCH("k_agg_vec8");
+            return;
+        }
+    }
     if (ext.src_bits || ext.dst_bits)
         k_agg_vec4<LPD, U, true><<<grid, 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks, in, ldb, out,
                                                       ld_out, dim, accumulate, kZeros, 0u, cm, ext);
-    else if (LPD == 32 && U <= 8 && vec8_on(ext) && ldb % 32 == 0 && reinterpret_cast<uintptr_t>(in) % 32 == 0)
-        k_agg_vec8<(U >= 2 ? U / 2 : 1)><<<grid_for(items * 16, 256), 256, 0, s>>>(
-            ebeg, eend, edges, order, d_begin, items, chunks, in, ldb, out, ld_out, dim, accumulate, kZeros, 0u, cm,
-            ext);
     else if (LPD == 32 && tuning(kTuneRecWindow) == 2)
         k_agg_vec4<LPD, U, false, 8, true><<<grid, 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks, in,
                                                                 ldb, out, ld_out, dim, accumulate, kZeros, 0u, cm, ext);

@@ -183,6 +183,39 @@ def test_wide_row_schedule_variants_bit_exact(pg, orc, dim, variant):
             pg.set_tuning(k)
 
 
+@pytest.mark.parametrize("vec8", [0, 1])
+@pytest.mark.parametrize("dim", [8, 16, 20, 24, 32, 40, 64, 100, 128, 136])
+def test_vec8_widths_bit_exact(pg, orc, dim, vec8):
+    """256-bit row gathers (k_agg_vec8, forced on small graphs with vec8 = 1)
+    at every lane-count instantiation — 2 / 4 / 8 lanes per narrow row,
+    16 per 128-column chunk — and the pitches it refuses (20 columns: a
+    16-byte pitch, back to k_agg_vec4): bit-identical to the oracle, with
+    accumulate semantics and row ranges."""
+    torch = torch_mod()
+    pairs, n_pad = rmat_pairs(orc, 4096, 4096 * 24, 23)
+    vt = orc.sample_training_set(4096, 0.5, 8)
+    og, dg, F, ops, dps = build_all(pg, orc, pairs, n_pad, vt, 2)
+    rng = np.random.default_rng(dim)
+    try:
+        pg.set_tuning("vec8", vec8)
+        for dp, op in zip(dps, ops):
+            y = rng.uniform(-1, 1, size=(dp.P, dim)).astype(np.float32)
+            base = rng.uniform(-1, 1, size=(dp.D, dim)).astype(np.float32)
+            want = orc.aggregate_pull_f32(op.offsets, op.neighbors, op.weights, y[op.srcpos], out=base)
+            x = to_dev(base, pg.padded_ld(dim))
+            G = pg.group_neighbors(dp, 3)
+            pg.backward_aggregation(G, to_dev(y, pg.padded_ld(dim)), x)
+            torch.cuda.synchronize()
+            assert np.array_equal(bits(x.cpu().numpy()), bits(want)), (dim, vec8)
+            b = dp.shard_bounds(3)
+            x2 = to_dev(base[b[1]:b[2]], pg.padded_ld(dim))
+            pg.backward_aggregation(G, to_dev(y, pg.padded_ld(dim)), x2, rows=(b[1], b[2]))
+            torch.cuda.synchronize()
+            assert np.array_equal(bits(x2.cpu().numpy()), bits(want[b[1]:b[2]])), (dim, vec8, "rows")
+    finally:
+        pg.set_tuning("vec8")
+
+
 def test_aggregate_pull_local_and_accumulate(pg, orc):
     torch = torch_mod()
     pairs, n_pad = rmat_pairs(orc, 2048, 2048 * 6, 3)

@@ -251,7 +251,8 @@ def test_random_chains(pg, orc, cuda, seed):
     knobs = {"atb_split": int(rng.integers(0, 2)), "atb_pairs": int(rng.choice([1, 224])),
              "atb_depth": int(rng.integers(0, 3)), "atb_quad": int(rng.integers(0, 3)),
              "gemm_packed": int(rng.integers(0, 3)), "wgrad_fork": int(rng.integers(0, 2)),
-             "gemm3_rows": int(rng.choice([8, 16])), "gemm_beside_wgrad": int(rng.integers(0, 2))}
+             "gemm3_rows": int(rng.choice([8, 16])), "gemm_beside_wgrad": int(rng.integers(0, 2)),
+             "vec8": int(rng.integers(0, 3))}
     try:
         for k, v in knobs.items():
             pg.set_tuning(k, v)
