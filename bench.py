@@ -631,6 +631,8 @@ def main():
         line["gs_sweep"] = gs_sweep(pg, prep, dims)
     if not args.profile and world == 1:
         line["grouped_fast"] = grouped_fast(pg, torch, prep, y_full, x_out, dims)
+    if not args.profile and world == 1 and os.environ.get("PG_BENCH_NO_F64") != "1":
+        line["f64"] = f64_stage(pg, torch, prep, y_full, dims)
     if not args.profile and world == 1 and os.environ.get("PG_BENCH_NO_SHARDS") != "1":
         line["shard_projection"] = shard_projection(pg, torch, paths, groups, y_full, dims, ep_bytes)
     if not args.profile and not args.no_chain and world == 1:
@@ -807,6 +809,47 @@ def grouped_fast(pg, torch, prep, y_full, x_out, dims, reps=7):
         out.append({"path": i, "gs": prep.gs[i], "deterministic_ms": round(det, 4), "grouped_fast_ms": round(grp, 4),
                     "max_rel_dev_vs_deterministic": dev})
     return out
+
+
+def f64_stage(pg, torch, prep, y_full, dims, reps=5):
+    """aggregate_pull<double> (Precision::F64, the reference's default,
+    run_config.hpp:53) on the same paths: f64 y_grad (the f32 inputs
+    widened), per-path ms (median of reps, device events), the f64 epoch's
+    algorithmic bytes 8(D+1) + 12E + 8 dim (E + D) per path over its time,
+    and the max deviation of the result from the f32 stage's (same order,
+    so only the f32 rounding shows)."""
+    ms, gbs, devs = [], [], []
+    tot_b = 0
+    for i, p in enumerate(prep.paths):
+        dim = dims[i]
+        ld = (dim + 15) // 16 * 16 if dim > 16 else dim + (dim & 1)  # 128-B rows, like the f32 pitch
+        yb = torch.zeros((p.P, ld), dtype=torch.float64, device="cuda")
+        yb[:, :dim] = y_full[i][:, :dim].double()
+        y = yb[:, :dim]
+        x = torch.zeros((p.D, ld), dtype=torch.float64, device="cuda")[:, :dim]
+        pg.backward_aggregation(prep.groups[i], y, x, overwrite=True)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            pg.backward_aggregation(prep.groups[i], y, x, overwrite=True)
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        t = statistics.median(ts)
+        nb = 8 * (p.D + 1) + 12 * p.E + 8 * dim * (p.E + p.D)
+        tot_b += nb
+        ms.append(round(t, 4))
+        gbs.append(round(nb / t / 1e6, 1))
+        x32 = pg.empty_rows(p.D, dim)
+        pg.backward_aggregation(prep.groups[i], y_full[i][:, :dim], x32, overwrite=True)
+        torch.cuda.synchronize()
+        devs.append(float((x - x32.double()).abs().max() / x.abs().max().clamp_min(1e-300)))
+        del yb, y, x, x32
+    return {"per_path_ms": ms, "ms_per_epoch": round(sum(ms), 4), "algorithmic_GBps_per_path": gbs,
+            "algorithmic_GBps": round(tot_b / sum(ms) / 1e6, 1), "max_rel_dev_vs_f32": devs,
+            "api": "pg_backward_aggregate_f64 (float64 device tensors)"}
 
 
 def measure_chain(pg, torch, g, prep, cfg, vt, dev, reps=5):

@@ -125,8 +125,10 @@ constexpr TuneKey kTuneKeys[] = {
     // (k_agg_vec8): 1 on, 0 off, 2 auto (rows wider than 64 columns, from
     // 2^21 edges per call)
     {"vec8", "PG_VEC8", 2},
+    // aggregate_pull<double>: hub-kernel degree threshold (0 = by the call's bytes)
+    {"f64_hub_min", "PG_F64_HUB_MIN", 0},
 };
-static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneVec8 + 1,
+static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneF64HubMin + 1,
               "kTuneKeys and enum TuneKeyId (pg_internal.h) must list the same keys in the same order");
 std::atomic<int64_t> g_tune[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];
 int64_t g_tune_def[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];  // $PG_<KEY> at load, else built-in
@@ -2248,24 +2250,47 @@ void launch_grp(Groups& G, const Groups::GrpSched& sc, const Edge* edges, uint32
 // column chunk), a lane a double2 (one 128-bit gather per edge per lane);
 // U edges in flight. Source id of edge e: src[e * src_stride] (the
 // gather-folded parent position, the local id, or the vertex id).
+// The f64 twin of batch_dep: the first weight of a batch XOR a runtime-zero
+// function of all its gathered rows (zmask = 0), so the chain's first DMUL
+// waits for every gather and ptxas issues them all back to back.
+template <int N>
+__device__ __forceinline__ double f64_batch_dep(double w0, const double2 (&x)[N], unsigned long long zmask) {
+    unsigned long long all = 0;
+#pragma unroll
+    for (int u = 0; u < N; ++u) all ^= static_cast<unsigned long long>(__double_as_longlong(x[u].x));
+    return __longlong_as_double(static_cast<long long>(static_cast<unsigned long long>(__double_as_longlong(w0)) ^
+                                                       (all & zmask)));
+}
+
 template <int LPD, int U>
-__global__ void __launch_bounds__(256) k_agg_f64(const uint64_t* __restrict__ offsets, const uint32_t* __restrict__ src,
+__global__ void __launch_bounds__(256) k_agg_f64(const uint64_t* __restrict__ ebeg, const uint64_t* __restrict__ eend,
+                                                const uint32_t* __restrict__ src,
                                                 uint32_t src_stride, const double* __restrict__ w,
                                                 const uint32_t* __restrict__ order, uint64_t n_items, uint32_t chunks,
-                                                const double* __restrict__ in, uint64_t ld_in,
+                                                uint32_t n_front, const double* __restrict__ in, uint64_t ld_in,
                                                 double* __restrict__ out, uint64_t ld_out, uint32_t dim,
-                                                int accumulate) {
+                                                int accumulate, unsigned long long zmask) {
     const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     const uint64_t item = t / LPD;
     if (item >= n_items) return;
+    // chunk-major, except the first n_front destinations (the longest lists,
+    // at the head of the degree order): destination-major ahead of the rest,
+    // so every chunk of them starts at the beginning of the pass
     const uint64_t nd = n_items / chunks;
-    const uint32_t d = __ldg(order + item % nd);
-    const uint32_t ci = static_cast<uint32_t>(item / nd);  // chunk-major
+    uint32_t d, ci;
+    if (item < static_cast<uint64_t>(n_front) * chunks) {
+        d = __ldg(order + item / chunks);
+        ci = static_cast<uint32_t>(item % chunks);
+    } else {
+        const uint64_t r = item - static_cast<uint64_t>(n_front) * chunks, nr = nd - n_front;
+        d = __ldg(order + n_front + r % nr);
+        ci = static_cast<uint32_t>(r / nr);
+    }
     const uint32_t col = (ci * LPD + static_cast<uint32_t>(t % LPD)) * 2;
     const bool active = col < dim;
     const bool pair = col + 1 < dim;
-    uint64_t e = __ldg(offsets + d);
-    const uint64_t end = __ldg(offsets + d + 1);
+    uint64_t e = __ldg(ebeg + d);
+    const uint64_t end = __ldg(eend + d);
     const double* icol = in + (active ? col : 0u);
     double* orow = out + d * ld_out + col;
     double a0 = 0.0, a1 = 0.0;
@@ -2284,22 +2309,207 @@ __global__ void __launch_bounds__(256) k_agg_f64(const uint64_t* __restrict__ of
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) x[u] = __ldg(reinterpret_cast<const double2*>(icol + sr[u] * ld_in));
+        ww[0] = f64_batch_dep<U>(ww[0], x, zmask);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             a0 = __dadd_rn(a0, __dmul_rn(ww[u], x[u].x));
             a1 = __dadd_rn(a1, __dmul_rn(ww[u], x[u].y));
         }
     }
-    for (; e < end; ++e) {
-        const uint32_t s0 = __ldg(src + e * src_stride);
-        const double w0 = __ldg(w + e);
-        const double2 x = __ldg(reinterpret_cast<const double2*>(icol + s0 * ld_in));
-        a0 = __dadd_rn(a0, __dmul_rn(w0, x.x));
-        a1 = __dadd_rn(a1, __dmul_rn(w0, x.y));
+    if (e < end) {  // remainder (< U edges) as one batch: all gathers in flight
+        const uint32_t n = static_cast<uint32_t>(end - e);
+        uint32_t sr[U];
+        double ww[U];
+        double2 x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t eu = e + (u < static_cast<int>(n) ? u : 0);
+            sr[u] = __ldg(src + eu * src_stride);
+            ww[u] = __ldg(w + eu);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            x[u] = u < static_cast<int>(n) ? __ldg(reinterpret_cast<const double2*>(icol + sr[u] * ld_in))
+                                           : make_double2(0.0, 0.0);
+        ww[0] = f64_batch_dep<U>(ww[0], x, zmask);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (u < static_cast<int>(n)) {
+                a0 = __dadd_rn(a0, __dmul_rn(ww[u], x[u].x));
+                a1 = __dadd_rn(a1, __dmul_rn(ww[u], x[u].y));
+            }
     }
     if (!active) return;
     orow[0] = __dadd_rn(a0, 0.0);
     if (pair) orow[1] = __dadd_rn(a1, 0.0);
+}
+
+// Wide f64 rows with 256-bit gathers (ld.global.nc.v4.f64, one 32-byte load
+// per lane and edge): 16 lanes of 4 doubles own a 64-double chunk, two items
+// per warp, so a record load (source id + f64 weight) serves two items.
+// Same items (chunk-major), per-column chains and bits as k_agg_f64<32>.
+// Needs a 32-byte aligned input and a 4-double row pitch.
+__device__ __forceinline__ void ld_row4d(const double* p, double2& a, double2& b) {
+    asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y)
+                 : "l"(p));
+}
+template <int U>
+__global__ void __launch_bounds__(256) k_agg_f64v(const uint64_t* __restrict__ ebeg, const uint64_t* __restrict__ eend,
+                                                 const uint32_t* __restrict__ src, uint32_t src_stride,
+                                                 const double* __restrict__ w, const uint32_t* __restrict__ order,
+                                                 uint64_t n_items, uint32_t chunks, const double* __restrict__ in,
+                                                 uint64_t ld_in, double* __restrict__ out, uint64_t ld_out,
+                                                 uint32_t dim, int accumulate, unsigned long long zmask) {
+    constexpr int LPD = 16;
+    const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    const uint64_t item = t / LPD;
+    if (item >= n_items) return;
+    const uint64_t nd = n_items / chunks;
+    const uint32_t d = __ldg(order + item % nd);
+    const uint32_t ci = static_cast<uint32_t>(item / nd);  // chunk-major
+    const uint32_t col = ci * 64u + static_cast<uint32_t>(t % LPD) * 4u;
+    const bool active = col < dim;
+    uint64_t e = __ldg(ebeg + d);
+    const uint64_t end = __ldg(eend + d);
+    const double* icol = in + (active ? col : ci * 64u);
+    double* orow = out + d * ld_out + col;
+    double a[4] = {0.0, 0.0, 0.0, 0.0};
+    if (accumulate && active)
+        for (int k = 0; k < 4; ++k)
+            if (col + k < dim) a[k] = orow[k];
+    auto step = [&](double wv, const double2& x0, const double2& x1) {
+        a[0] = __dadd_rn(a[0], __dmul_rn(wv, x0.x));
+        a[1] = __dadd_rn(a[1], __dmul_rn(wv, x0.y));
+        a[2] = __dadd_rn(a[2], __dmul_rn(wv, x1.x));
+        a[3] = __dadd_rn(a[3], __dmul_rn(wv, x1.y));
+    };
+    for (; e + U <= end; e += U) {
+        uint32_t sr[U];
+        double ww[U];
+        double2 x[2 * U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            sr[u] = __ldg(src + (e + u) * src_stride);
+            ww[u] = __ldg(w + e + u);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) ld_row4d(icol + sr[u] * ld_in, x[2 * u], x[2 * u + 1]);
+        ww[0] = f64_batch_dep<2 * U>(ww[0], x, zmask);
+#pragma unroll
+        for (int u = 0; u < U; ++u) step(ww[u], x[2 * u], x[2 * u + 1]);
+    }
+    if (e < end) {
+        const uint32_t n = static_cast<uint32_t>(end - e);
+        uint32_t sr[U];
+        double ww[U];
+        double2 x[2 * U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t eu = e + (u < static_cast<int>(n) ? u : 0);
+            sr[u] = __ldg(src + eu * src_stride);
+            ww[u] = __ldg(w + eu);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (u < static_cast<int>(n)) ld_row4d(icol + sr[u] * ld_in, x[2 * u], x[2 * u + 1]);
+            else x[2 * u] = x[2 * u + 1] = make_double2(0.0, 0.0);
+        }
+        ww[0] = f64_batch_dep<2 * U>(ww[0], x, zmask);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (u < static_cast<int>(n)) step(ww[u], x[2 * u], x[2 * u + 1]);
+    }
+    if (!active) return;
+    for (int k = 0; k < 4; ++k)
+        if (col + k < dim) orow[k] = __dadd_rn(a[k], 0.0);
+}
+
+// aggregate_pull<double> hub destinations (the longest lists): a CTA per
+// (hub, CW-column chunk). All 256 threads gather a tile of T edges' row
+// slices into shared memory (double-buffered: tile t+1's rows in flight
+// while tile t folds); CW owner threads then run each column's serial
+// chain over the tile in edge order — the reference's order, so the same
+// bits as k_agg_f64, with the gathers no longer one latency per batch of 8.
+template <int CW>
+__global__ void __launch_bounds__(256) k_agg_f64_hub(const uint64_t* __restrict__ ebeg,
+                                                    const uint64_t* __restrict__ eend,
+                                                    const uint32_t* __restrict__ src, uint32_t src_stride,
+                                                    const double* __restrict__ w, const uint32_t* __restrict__ order,
+                                                    uint32_t chunks, const double* __restrict__ in, uint64_t ld_in,
+                                                    double* __restrict__ out, uint64_t ld_out, uint32_t dim,
+                                                    int accumulate) {
+    constexpr int H = CW / 2;             // double2 per row slice
+    constexpr int T = 16384 / (CW * 8);   // edges per tile (16 KB of rows)
+    constexpr int PER = T * H / 256;      // double2 gathers per thread per tile
+    __shared__ __align__(16) double2 tile[2][T * H];
+    __shared__ double wt[2][T];
+    const uint32_t d = order[blockIdx.x / chunks];
+    const uint32_t c0 = (blockIdx.x % chunks) * CW;
+    const uint64_t eb = ebeg[d], ee = eend[d];
+    const uint64_t ntiles = (ee - eb + T - 1) / T;
+    const unsigned tid = threadIdx.x;
+    double2 r[PER];
+    double rw[PER];
+    auto rows = [&](uint64_t t) {
+        const uint64_t e0 = eb + t * T;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const unsigned idx = tid + 256u * k;
+            const unsigned j = idx / H, q = idx % H;
+            const uint32_t col = c0 + 2 * q;
+            if (e0 + j < ee) {
+                const uint32_t sr = __ldg(src + (e0 + j) * src_stride);
+                r[k] = col < dim ? __ldg(reinterpret_cast<const double2*>(in + static_cast<uint64_t>(sr) * ld_in + col))
+                                 : make_double2(0.0, 0.0);
+                rw[k] = __ldg(w + e0 + j);
+            } else {
+                r[k] = make_double2(0.0, 0.0);
+                rw[k] = 0.0;
+            }
+        }
+    };
+    auto stash = [&](int b) {
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const unsigned idx = tid + 256u * k;
+            tile[b][idx] = r[k];
+            if (idx % H == 0) wt[b][idx / H] = rw[k];
+        }
+    };
+    const uint32_t col = c0 + tid;
+    const bool owner = tid < CW && col < dim;
+    double* orow = out + static_cast<uint64_t>(d) * ld_out + col;
+    double acc = owner && accumulate ? *orow : 0.0;
+    if (ntiles) {
+        rows(0);
+        stash(0);
+    }
+    __syncthreads();
+    for (uint64_t t = 0; t < ntiles; ++t) {
+        const int b = static_cast<int>(t & 1);
+        if (t + 1 < ntiles) rows(t + 1);
+        if (owner) {
+            const uint32_t n = static_cast<uint32_t>(min(static_cast<uint64_t>(T), ee - (eb + t * T)));
+            const double* sb = reinterpret_cast<const double*>(tile[b]) + tid;
+            const double* sw = wt[b];
+            uint32_t j = 0;
+            for (; j + 8 <= n; j += 8) {
+                double pw[8], px[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    pw[u] = sw[j + u];
+                    px[u] = sb[(j + u) * CW];
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, __dmul_rn(pw[u], px[u]));
+            }
+            for (; j < n; ++j) acc = __dadd_rn(acc, __dmul_rn(sw[j], sb[j * CW]));
+        }
+        if (t + 1 < ntiles) stash(b ^ 1);
+        __syncthreads();
+    }
+    if (owner) *orow = __dadd_rn(acc, 0.0);
 }
 
 struct SideStream {
@@ -2652,32 +2862,66 @@ void aggregate_groups_af(Groups& G, const uint64_t* offsets_dev, uint32_t D, con
     else launch_grp<4>(G, *sc, edges, chunks, in, ld_in, out, ld_out, dim32, accumulate, s, seg_lo, seg_hi);
 }
 
-void aggregate_f64(const uint64_t* offsets, const uint32_t* src, uint32_t src_stride, const double* w,
-                   const uint32_t* order, uint32_t D, const double* in, uint64_t ld_in, double* out, uint64_t ld_out,
-                   uint64_t dim, bool accumulate, cudaStream_t s) {
+void aggregate_f64(const uint64_t* ebeg, const uint64_t* eend, const uint32_t* src, uint32_t src_stride,
+                   const double* w, const uint32_t* order, uint32_t D, uint32_t n_hub, uint32_t n_front,
+                   const double* in, uint64_t ld_in, double* out, uint64_t ld_out, uint64_t dim, bool accumulate,
+                   cudaStream_t s, uint64_t n_edges) {
     if (D == 0 || dim == 0) return;
     if (ld_in % 2 || ld_out % 2 || reinterpret_cast<uintptr_t>(in) % 16 || reinterpret_cast<uintptr_t>(out) % 16)
         fail(kConfig, "aggregate_pull<double>: rows must be 16-byte aligned (even ld, aligned base)");
-    const uint32_t np = static_cast<uint32_t>((dim + 1) / 2);  // double2 per row
-    const int lpd = np > 16 ? 32 : np > 8 ? 16 : np > 4 ? 8 : 4;
-    const uint32_t chunks = (np + lpd - 1) / lpd;
-    const uint64_t items = static_cast<uint64_t>(D) * chunks;
-    const unsigned grid = grid_for(items * lpd, 256);
-    const int acc = accumulate ? 1 : 0;
     const uint32_t d32 = static_cast<uint32_t>(dim);
-    if (lpd == 32)
-        k_agg_f64<32, 8><<<grid, 256, 0, s>>>(offsets, src, src_stride, w, order, items, chunks, in, ld_in, out, ld_out,
-                                              d32, acc);
-    else if (lpd == 16)
-        k_agg_f64<16, 8><<<grid, 256, 0, s>>>(offsets, src, src_stride, w, order, items, chunks, in, ld_in, out, ld_out,
-                                              d32, acc);
-    else if (lpd == 8)
-        k_agg_f64<8, 8><<<grid, 256, 0, s>>>(offsets, src, src_stride, w, order, items, chunks, in, ld_in, out, ld_out,
-                                             d32, acc);
-    else
-        k_agg_f64<4, 8><<<grid, 256, 0, s>>>(offsets, src, src_stride, w, order, items, chunks, in, ld_in, out, ld_out,
-                                             d32, acc);
-    PG_LAUNCH("k_agg_f64");
+    const int acc = accumulate ? 1 : 0;
+    n_hub = std::min(n_hub, D);
+    SideStream* ss = nullptr;
+    if (n_hub) {  // the hubs on the forked side stream, concurrent with the rest
+        ss = &side_stream(s);
+        PG_CUDA(cudaEventRecord(ss->fork, s));
+        PG_CUDA(cudaStreamWaitEvent(ss->s, ss->fork, 0));
+        if (dim <= 16) {
+            k_agg_f64_hub<16><<<n_hub, 256, 0, ss->s>>>(ebeg, eend, src, src_stride, w, order, 1u, in, ld_in, out,
+                                                       ld_out, d32, acc);
+        } else {
+            const uint32_t ch = static_cast<uint32_t>((dim + 31) / 32);
+            k_agg_f64_hub<32><<<static_cast<unsigned>(n_hub) * ch, 256, 0, ss->s>>>(
+                ebeg, eend, src, src_stride, w, order, ch, in, ld_in, out, ld_out, d32, acc);
+        }
+        PG_LAUNCH("k_agg_f64_hub");
+        PG_CUDA(cudaEventRecord(ss->join, ss->s));
+    }
+    const uint32_t nd = D - n_hub;
+    if (nd) {
+        const uint32_t* ord = order + n_hub;
+        const uint32_t np = static_cast<uint32_t>((dim + 1) / 2);  // double2 per row
+        const int lpd = np > 16 ? 32 : np > 8 ? 16 : np > 4 ? 8 : 4;
+        const uint32_t chunks = (np + lpd - 1) / lpd;
+        const uint32_t nf = chunks > 1 ? std::min(n_front > n_hub ? n_front - n_hub : 0u, nd) : 0u;
+        const uint64_t items = static_cast<uint64_t>(nd) * chunks;
+        const unsigned grid = grid_for(items * lpd, 256);
+        const int64_t v8 = tuning(kTuneVec8);
+        if (lpd == 32 && (v8 == 1 || (v8 == 2 && n_edges >= (1ull << 21))) && ld_in % 4 == 0 &&
+            reinterpret_cast<uintptr_t>(in) % 32 == 0) {
+            // 256-bit gathers for rows wider than 32 doubles, on the f32
+            // rule (tuning vec8; arxiv's 0.6M-edge top path: 0.27 vs 0.29 ms
+            // without; Reddit layer 0 40.7 -> 38.6 ms, products 11.9 -> 8.3)
+            const uint64_t it = static_cast<uint64_t>(nd) * ((dim + 63) / 64);
+            k_agg_f64v<4><<<grid_for(it * 16, 256), 256, 0, s>>>(ebeg, eend, src, src_stride, w, ord, it,
+                                                                 static_cast<uint32_t>((dim + 63) / 64), in, ld_in,
+                                                                 out, ld_out, d32, acc, 0ull);
+        } else if (lpd == 32)
+            k_agg_f64<32, 8><<<grid, 256, 0, s>>>(ebeg, eend, src, src_stride, w, ord, items, chunks, nf, in, ld_in,
+                                                  out, ld_out, d32, acc, 0ull);
+        else if (lpd == 16)
+            k_agg_f64<16, 8><<<grid, 256, 0, s>>>(ebeg, eend, src, src_stride, w, ord, items, chunks, nf, in, ld_in,
+                                                  out, ld_out, d32, acc, 0ull);
+        else if (lpd == 8)
+            k_agg_f64<8, 8><<<grid, 256, 0, s>>>(ebeg, eend, src, src_stride, w, ord, items, chunks, nf, in, ld_in,
+                                                 out, ld_out, d32, acc, 0ull);
+        else
+            k_agg_f64<4, 8><<<grid, 256, 0, s>>>(ebeg, eend, src, src_stride, w, ord, items, chunks, nf, in, ld_in,
+                                                 out, ld_out, d32, acc, 0ull);
+        PG_LAUNCH("k_agg_f64");
+    }
+    if (ss) PG_CUDA(cudaStreamWaitEvent(s, ss->join, 0));
 }
 
 void relu_backward(const float* grad, uint64_t ldg, const float* pre, uint64_t ldp, float* out, uint64_t ldo,

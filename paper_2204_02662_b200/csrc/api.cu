@@ -1705,6 +1705,21 @@ int pg_backward_aggregate_rows(pg_groups h, uint32_t row_begin, uint32_t row_end
 namespace {
 // the f64 SpMM over a grouping's base: parent-indexed (the engine.hpp:334
 // gather folded in) or local / vertex-indexed sources
+// aggregate_pull<double> hubs: rows of <= 32 doubles whose lists are longer
+// than this go to k_agg_f64_hub (k_agg_f64 pays one gather round trip per
+// batch of 8 edges of a list). Measured on the Reddit top path (width 16,
+// 75.6M edges): no hub kernel 4.65 ms, lists >= 10.6K 2.21, >= 4096 1.39,
+// >= 1024 1.98. Wide rows keep every list in k_agg_f64 (layer 0, width 602:
+// 46.6 ms, 62.9 with the hubs >= 4096 on the hub kernel, 100 with >= 1024),
+// and chunk-major without a destination-major front (the front cost
+// 42.9 -> 54.2 ms). Tuning "f64_hub_min" > 0 forces the threshold.
+constexpr uint64_t kNoHubs = 0;  // DegHist::heavy(0) = no destinations
+uint64_t f64_hub_degree(uint64_t dim) {
+    const int64_t forced = tuning(kTuneF64HubMin);
+    if (forced > 0) return static_cast<uint64_t>(forced);
+    return dim <= 32 ? 4096 : kNoHubs;
+}
+
 void run_aggregate_f64(Groups& G, bool parent_indexed, const double* in, uint64_t ld_in, double* out, uint64_t ld_out,
                        uint64_t dim, unsigned flags, cudaStream_t s) {
     DeviceGuard dg(G.device);
@@ -1714,15 +1729,31 @@ void run_aggregate_f64(Groups& G, bool parent_indexed, const double* in, uint64_
         Path& p = *G.path;
         const uint32_t* src = parent_indexed ? reinterpret_cast<const uint32_t*>(p.edges_parent.get())
                                              : p.nbr_local.get();
-        aggregate_f64(p.offsets.get(), src, parent_indexed ? 2u : 1u, p.w64.get(), p.order.get(), p.D, in, ld_in, out,
-                      ld_out, dim, accumulate, s);
+        const uint32_t stride = parent_indexed ? 2u : 1u;
+        // the f32 path's L2-sized source segments (a 32-lane double2 chunk
+        // is 512 B, the f32 chunk's size): accumulate passes in source order
+        const uint32_t K = parent_indexed ? auto_src_segments(p.P, p.D, p.E, dim) : 1u;
+        if (K > 1) {
+            auto_segment_bounds(G, p, K);
+            for (uint32_t k = 0; k < K; ++k) {
+                const uint64_t* eb = G.auto_seg_bnd.get() + static_cast<uint64_t>(k) * p.D;
+                aggregate_f64(eb, eb + p.D, src, stride, p.w64.get(), p.order.get(), p.D,
+                              p.hist.heavy(f64_hub_degree(dim)), 0u, in, ld_in,
+                              out, ld_out, dim, accumulate || k > 0, s, p.E / K);
+            }
+            return;
+        }
+        aggregate_f64(p.offsets.get(), p.offsets.get() + 1, src, stride, p.w64.get(), p.order.get(), p.D,
+                      p.hist.heavy(f64_hub_degree(dim)), 0u, in, ld_in, out, ld_out,
+                      dim, accumulate, s, p.E);
         return;
     }
     Graph& g = *G.graph;
     if (!G.graph_order.get() && g.n)
         degree_order(g.offsets.get(), g.n, G.graph_order, lib_stream(g.device), &G.graph_hist);
-    aggregate_f64(g.offsets.get(), g.nbrs.get(), 1u, g.w64.get(), G.graph_order.get(), g.n, in, ld_in, out, ld_out,
-                  dim, accumulate, s);
+    aggregate_f64(g.offsets.get(), g.offsets.get() + 1, g.nbrs.get(), 1u, g.w64.get(), G.graph_order.get(), g.n,
+                  G.graph_hist.heavy(f64_hub_degree(dim)), 0u, in, ld_in, out,
+                  ld_out, dim, accumulate, s, g.m);
 }
 
 // host DenseMatrix<double> drop-in: copy in (pitched to even ld), run, copy out
@@ -1730,7 +1761,9 @@ void run_host_f64(Groups& G, bool parent_indexed, const double* in_host, uint64_
                   double* out_host, uint64_t out_rows, unsigned flags) {
     DeviceGuard dg(G.device);
     cudaStream_t s = lib_stream(G.device);
-    const uint64_t ld = (dim + 1) & ~1ull;
+    // 128-byte device rows past 16 columns (256-bit gathers need a 4-double
+    // pitch), else 16-byte
+    const uint64_t ld = dim > 16 ? (dim + 15) & ~15ull : (dim + 1) & ~1ull;
     DevBuf<double> din(in_rows * ld, s), dout(out_rows * ld, s);
     if (in_rows && dim)
         PG_CUDA(cudaMemcpy2DAsync(din.get(), ld * 8, in_host, dim * 8, dim * 8, in_rows, cudaMemcpyHostToDevice, s));

@@ -305,10 +305,14 @@ void aggregate_groups(const uint64_t* gbeg, const uint64_t* gend, const uint32_t
                       uint64_t ld_out, uint64_t dim, bool accumulate, cudaStream_t s);
 
 // aggregate.hpp:56-122 with T = double (Deterministic order, f64 weights):
-// source of edge e = src[e * src_stride]; destinations in `order`.
-void aggregate_f64(const uint64_t* offsets, const uint32_t* src, uint32_t src_stride, const double* w,
-                   const uint32_t* order, uint32_t D, const double* in, uint64_t ld_in, double* out, uint64_t ld_out,
-                   uint64_t dim, bool accumulate, cudaStream_t s);
+// destination d sums edges [ebeg[d], eend[d]) (whole lists or one source
+// segment), source of edge e = src[e * src_stride]; destinations in the
+// descending-degree `order`: its first n_hub on the hub kernel (forked side
+// stream), its first n_front (multi-chunk rows) started destination-major.
+void aggregate_f64(const uint64_t* ebeg, const uint64_t* eend, const uint32_t* src, uint32_t src_stride,
+                   const double* w, const uint32_t* order, uint32_t D, uint32_t n_hub, uint32_t n_front,
+                   const double* in, uint64_t ld_in, double* out, uint64_t ld_out, uint64_t dim, bool accumulate,
+                   cudaStream_t s, uint64_t n_edges);
 
 // record a failure as the calling thread's pg_last_error / _kind (api.cu)
 void record_error(const Error& e);
@@ -375,7 +379,8 @@ enum TuneKeyId {
     kTuneHostSeq = 43,
     kTuneAtbQuad = 44,
     kTuneHostSmallChunks = 45,
-    kTuneVec8 = 46
+    kTuneVec8 = 46,
+    kTuneF64HubMin = 47
 };
 // whole-row SpMM warps (k_agg_row) for this width (tuning "row_kernel")
 bool row_kernel_on(uint64_t dim);

@@ -15,8 +15,27 @@ def bits64(a):
     return np.ascontiguousarray(a, np.float64).view(np.uint64)
 
 
+@pytest.mark.parametrize("knobs", [{}, {"f64_hub_min": 24}, {"f64_hub_min": 24, "src_segs": 2},
+                                   {"src_segs": 3}, {"vec8": 0}, {"pitch4": 1, "vec8": 1},
+                                   {"pitch4": 1, "vec8": 1, "src_segs": 2}, {"pitch4": 1}])
 @pytest.mark.parametrize("dim", [1, 2, 3, 16, 41, 100, 257])
-def test_f64_stage_bit_exact(pg, orc, cuda, dim):
+def test_f64_stage_bit_exact(pg, orc, cuda, dim, knobs):
+    """Default schedule, the hub kernel forced down to 24-edge lists
+    (k_agg_f64_hub: tile-staged gathers, per-column serial fold), forced
+    source-segment passes, and the 256-bit k_agg_f64v (4-double pitch,
+    vec8 forced on): all bit-identical to the f64 oracle."""
+    knobs = dict(knobs)
+    pitch4 = knobs.pop("pitch4", 0)
+    for k, v in knobs.items():
+        pg.set_tuning(k, v)
+    try:
+        _f64_stage(pg, orc, dim, pitch4)
+    finally:
+        for k in knobs:
+            pg.set_tuning(k)
+
+
+def _f64_stage(pg, orc, dim, pitch4=0):
     import torch
 
     pairs, n_pad = rmat_pairs(orc, 4096, 4096 * 24, 11)
@@ -34,7 +53,8 @@ def test_f64_stage_bit_exact(pg, orc, cuda, dim):
         pg.backward_aggregation(G, y, xh, overwrite=True)
         assert np.array_equal(bits64(xh), bits64(want))
         # device, pitched rows (even ld) and accumulate semantics
-        ld = dim + (dim & 1) + 2
+        # pitch4: a 4-double pitch (the 256-bit k_agg_f64v path past 32 columns)
+        ld = (dim + 3) // 4 * 4 if pitch4 else dim + (dim & 1) + 2
         yd = torch.zeros((p.P, ld), dtype=torch.float64, device="cuda")[:, :dim]
         yd.copy_(torch.from_numpy(y))
         xd = torch.ones((p.D, ld), dtype=torch.float64, device="cuda")[:, :dim]
