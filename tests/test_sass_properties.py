@@ -96,3 +96,15 @@ def test_wide_spmm_gathers_are_256_bit(sass):
         assert re.search(r"\bFFMA2\b", body) and re.search(r"\bFADD2\b", body), name
         assert not re.search(r"\b(STL|LDL)\b", body), name
         assert not GLOBAL_ATOMIC.search(body), name
+
+
+def test_f64_wide_gathers_are_256_bit_and_unfused(sass):
+    """k_agg_f64v (aggregate_pull<double>, rows > 32 doubles): 256-bit row
+    gathers; every multiply and add separately rounded (DMUL + DADD, no DFMA
+    — the reference's default-flag x86-64 build does not contract)."""
+    for name, body in _kernels(sass, r"k_agg_f64v?ILi").items():
+        assert re.search(r"\bDMUL\b", body) and re.search(r"\bDADD\b", body), name
+        assert not re.search(r"\bDFMA\b", body), name
+        assert not re.search(r"\b(STL|LDL)\b", body), name
+    for name, body in _kernels(sass, r"k_agg_f64vILi4E").items():
+        assert len(re.findall(r"LDG\.E\.ENL2\.256", body)) >= 8, name
