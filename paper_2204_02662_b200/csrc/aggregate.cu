@@ -127,8 +127,10 @@ constexpr TuneKey kTuneKeys[] = {
     {"vec8", "PG_VEC8", 2},
     // aggregate_pull<double>: hub-kernel degree threshold (0 = by the call's bytes)
     {"f64_hub_min", "PG_F64_HUB_MIN", 0},
+    // grouped Fast (k_agg_grp): 1 = groups handed to workers dynamically
+    {"grp_dynamic", "PG_GRP_DYNAMIC", 0},
 };
-static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneF64HubMin + 1,
+static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneGrpDynamic + 1,
               "kTuneKeys and enum TuneKeyId (pg_internal.h) must list the same keys in the same order");
 std::atomic<int64_t> g_tune[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];
 int64_t g_tune_def[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];  // $PG_<KEY> at load, else built-in
@@ -1922,8 +1924,9 @@ __global__ void __launch_bounds__(256, 4) k_agg_grp(const uint4* __restrict__ ra
                                                    int accumulate, float* __restrict__ scratch, uint64_t ld_scr,
                                                    float2 zeros, uint32_t zmask,
                                                    const uint64_t* __restrict__ seg_lo,
-                                                   const uint64_t* __restrict__ seg_hi) {
+                                                   const uint64_t* __restrict__ seg_hi, int dyn) {
     constexpr int W = grp_workers<LPD>();
+    __shared__ uint32_t next_group;  // dyn: groups handed out in order, one at a time
     constexpr int GCAP = grp_gcap<LPD>();
     extern __shared__ __align__(128) unsigned char smem[];
     Edge* recs = reinterpret_cast<Edge*>(smem);
@@ -1945,6 +1948,7 @@ __global__ void __launch_bounds__(256, 4) k_agg_grp(const uint4* __restrict__ ra
         mbar_init(bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    if (tid == 0) next_group = W;
     for (uint32_t lg = tid; lg < ng; lg += 256) {
         uint64_t gb = __ldg(gbeg + g0 + lg), ge = __ldg(gend + g0 + lg);
         const uint32_t dd = __ldg(gdest + g0 + lg);
@@ -1984,7 +1988,18 @@ __global__ void __launch_bounds__(256, 4) k_agg_grp(const uint4* __restrict__ ra
         }
         return ld_rec(edges + ebase + i);
     };
-    for (uint32_t lg = w; lg < ng; lg += W) {
+    const unsigned submask = LPD >= 32 ? 0xffffffffu : (((1u << LPD) - 1u) << (lane_id() & ~(LPD - 1u)));
+    // the next group of this worker: static round robin, or (dyn) the CTA's
+    // next unclaimed group — a worker that drew short groups takes more, so
+    // the reduction barrier waits less (the partials, their order and the
+    // result do not depend on which worker computed a group)
+    auto next = [&](uint32_t lg) -> uint32_t {
+        if (!dyn) return lg + W;
+        uint32_t nl = 0;
+        if (sl == 0) nl = atomicAdd(&next_group, 1u);
+        return __shfl_sync(submask, nl, 0, LPD);
+    };
+    for (uint32_t lg = w; lg < ng; lg = next(lg)) {
         uint32_t e = sgb[lg];
         const uint32_t end = sge[lg];
         Acc acc{0ull, 0ull};  // the group's zero scratch (aggregate.hpp:93)
@@ -2229,7 +2244,7 @@ void launch_grp(Groups& G, const Groups::GrpSched& sc, const Edge* edges, uint32
         k_agg_grp<LPD, 8><<<sc.nranges * chunks, 256, smem, s>>>(
             sc.ranges.get(), sc.nranges, G.gbegin.get(), G.gend.get(), G.gdest.get(), edges, in,
             static_cast<uint32_t>(ld_in * 4), out, ld_out, dim, accumulate, scratch.get(), ld_scr, kZeros, 0u, seg_lo,
-            seg_hi);
+            seg_hi, static_cast<int>(tuning(kTuneGrpDynamic)));
         PG_LAUNCH("k_agg_grp");
     }
     const uint64_t fix = static_cast<uint64_t>(sc.nhubs + (accumulate ? 0 : sc.nempty)) * chunks;

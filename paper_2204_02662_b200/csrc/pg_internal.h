@@ -380,7 +380,8 @@ enum TuneKeyId {
     kTuneAtbQuad = 44,
     kTuneHostSmallChunks = 45,
     kTuneVec8 = 46,
-    kTuneF64HubMin = 47
+    kTuneF64HubMin = 47,
+    kTuneGrpDynamic = 48
 };
 // whole-row SpMM warps (k_agg_row) for this width (tuning "row_kernel")
 bool row_kernel_on(uint64_t dim);

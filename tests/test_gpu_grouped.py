@@ -132,6 +132,17 @@ def test_grouped_atomic_free_hubs_and_determinism(pg, orc, cuda, dim):
             torch.cuda.synchronize()
             runs.append(x.cpu().numpy())
         assert np.array_equal(runs[0].view(np.uint32), runs[1].view(np.uint32)), gs
+        # groups handed to workers dynamically (tuning grp_dynamic): the
+        # partials and their reduction order are the same, so the same bits
+        try:
+            for dyn in (0, 1):
+                pg.set_tuning("grp_dynamic", dyn)
+                x = pg.empty_rows(p.D, dim)
+                pg.backward_aggregation(G, yd, x, mode=pg.GROUPED, overwrite=True)
+                torch.cuda.synchronize()
+                assert np.array_equal(x.cpu().numpy().view(np.uint32), runs[0].view(np.uint32)), (gs, dyn)
+        finally:
+            pg.set_tuning("grp_dynamic")
         err = np.abs(runs[0].astype(np.float64) - want64)
         assert (err <= 1e-6 + 1e-5 * absum).all(), (gs, float((err / (1e-6 + 1e-5 * absum)).max()))
         if gs >= p.max_degree:
