@@ -129,8 +129,10 @@ constexpr TuneKey kTuneKeys[] = {
     {"f64_hub_min", "PG_F64_HUB_MIN", 0},
     // grouped Fast (k_agg_grp): 1 = groups handed to workers dynamically
     {"grp_dynamic", "PG_GRP_DYNAMIC", 0},
+    // k_agg_vec8 wide rows: edges per batch per half-warp (0 = 4; 3, 6)
+    {"vec8_u", "PG_VEC8_U", 0},
 };
-static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneGrpDynamic + 1,
+static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneVec8U + 1,
               "kTuneKeys and enum TuneKeyId (pg_internal.h) must list the same keys in the same order");
 std::atomic<int64_t> g_tune[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];
 int64_t g_tune_def[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];  // $PG_<KEY> at load, else built-in
@@ -505,7 +507,7 @@ __device__ __forceinline__ void ld_row8(const char* base, uint32_t src, uint32_t
                  : "l"(p));
 }
 template <int LPD, int U, bool FILT>
-__global__ void __launch_bounds__(256, 4) k_agg_vec8(const uint64_t* __restrict__ ebeg, const uint64_t* __restrict__ eend,
+__global__ void __launch_bounds__(256, (U <= 3 ? 5 : U == 4 ? 4 : 3)) k_agg_vec8(const uint64_t* __restrict__ ebeg, const uint64_t* __restrict__ eend,
                                                      const Edge* __restrict__ edges,
                                                      const uint32_t* __restrict__ order, uint32_t d_begin,
                                                      uint64_t n_items, uint32_t chunks,
@@ -2590,6 +2592,22 @@ void launch_vec4(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges, 
         if (vec8_on(ext, LPD) && ldb % 32 == 0 && reinterpret_cast<uintptr_t>(in) % 32 == 0) {
             constexpr int U8 = U / 2;
             const unsigned g8 = grid_for(items * (LPD / 2), 256);
+            const int64_t vu8 = tuning(kTuneVec8U);
+            if constexpr (LPD == 32 && U == 8) {
+                // edges per batch per half-warp (tuning vec8_u; 0 = 4)
+                if (vu8 == 3 && !(ext.src_bits || ext.dst_bits)) {
+                    k_agg_vec8<16, 3, false><<<g8, 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks, in,
+                                                                ldb, out, ld_out, dim, accumulate, kZeros, 0u, cm, ext);
+                    PG_LAUNCH("k_agg_vec8");
+                    return;
+                }
+                if (vu8 == 6 && !(ext.src_bits || ext.dst_bits)) {
+                    k_agg_vec8<16, 6, false><<<g8, 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks, in,
+                                                                ldb, out, ld_out, dim, accumulate, kZeros, 0u, cm, ext);
+                    PG_LAUNCH("k_agg_vec8");
+                    return;
+                }
+            }
             if (ext.src_bits || ext.dst_bits)
                 k_agg_vec8<LPD / 2, U8, true><<<g8, 256, 0, s>>>(ebeg, eend, edges, order, d_begin, items, chunks, in,
                                                                  ldb, out, ld_out, dim, accumulate, kZeros, 0u, cm, ext);
