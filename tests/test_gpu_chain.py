@@ -174,15 +174,23 @@ def test_dense_kernels(pg, orc, cuda):
     out = pg.empty_rows(*x.shape)
     pg.relu(dev(torch, pg, x), out)
     assert same(host(out), orc.relu_f32(x))
+    # past 32768 rows: each thread takes 8 rows per step (the last step partial)
+    x = rng.uniform(-2, 2, (32768 * 8 + 32768 * 3 + 5, 21)).astype(np.float32)
+    out = pg.empty_rows(*x.shape)
+    pg.relu(dev(torch, pg, x), out)
+    assert same(host(out), orc.relu_f32(x))
 
 
 def test_row_softmax_bit_exact(pg, orc, cuda):
-    """expf emulation == glibc expf: wide-range logits incl. underflow."""
+    """expf emulation == glibc expf: wide-range logits incl. underflow; the
+    shared-memory-tiled kernel (<= 95 columns, a partial last tile of rows)
+    and the thread-per-row one past it."""
     import torch
 
     rng = np.random.default_rng(9)
-    for cols, scale in ((41, 1.0), (7, 30.0), (3, 200.0), (47, 0.01), (1, 5.0)):
-        x = (rng.standard_normal((4096, cols)) * scale).astype(np.float32)
+    for cols, scale in ((41, 1.0), (7, 30.0), (3, 200.0), (47, 0.01), (1, 5.0), (95, 3.0), (96, 3.0),
+                        (130, 1.0)):
+        x = (rng.standard_normal((4099, cols)) * scale).astype(np.float32)
         out = pg.empty_rows(*x.shape)
         pg.row_softmax(dev(torch, pg, x), out)
         torch.cuda.synchronize()
