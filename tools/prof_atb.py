@@ -2,6 +2,7 @@
 configs' shapes for each setting of tuning atb_depth, CUDA-event timed,
 outputs compared bit for bit across settings.
   python tools/prof_atb.py"""
+import json
 import os
 import statistics
 import sys
@@ -18,6 +19,13 @@ ATB = [("products layer0 W'", 1_198_008, 2_449_029, 100, 256), ("products top W'
        ("arxiv layer0 W'", 113_323, 169_343, 128, 256)]
 
 
+# tuning settings compared (atb_pairs 0: one A column per lane; 1: two;
+# atb_depth 0 = 4/2, 1 = 7/5, 2 = rows shared by lanes 4/2)
+SETTINGS = json.loads(os.environ.get("ATB_SETTINGS", "null")) or [
+    {}, {"atb_depth": 1}, {"atb_depth": 2}, {"atb_pairs": 0}, {"atb_pairs": 0, "atb_depth": 1},
+    {"atb_pairs": 0, "atb_depth": 2}, {"atb_quad": 1}, {"atb_quad": 2}]
+
+
 def main():
     for name, n, ry, ind, outd in ATB:
         y = pg.empty_rows(ry, ind)
@@ -26,9 +34,9 @@ def main():
         g.uniform_(-1, 1)
         ids = torch.sort(torch.randperm(ry, device="cuda")[:n].to(torch.int32))[0]
         res, outs = {}, {}
-        for depth in (0, 1, 2, 3, 4):
-            pg.set_tuning("atb_depth", depth if depth < 3 else 0)
-            pg.set_tuning("atb_quad", 0 if depth < 3 else depth - 2)
+        for si, st in enumerate(SETTINGS):
+            for k, v in st.items():
+                pg.set_tuning(k, v)
             o = pg.empty_rows(ind, outd)
             pg.gemm_at_b(y, g, o, a_rows=ids)
             torch.cuda.synchronize()
@@ -40,15 +48,15 @@ def main():
                 e1.record()
                 torch.cuda.synchronize()
                 ts.append(e0.elapsed_time(e1))
-            res[depth] = statistics.median(ts)
-            outs[depth] = o
-        pg.set_tuning("atb_depth", None)
-        pg.set_tuning("atb_quad", None)
+            res[si] = statistics.median(ts)
+            outs[si] = o
+            for k in st:
+                pg.set_tuning(k, None)
         same = all(torch.equal(outs[0].view(torch.int32), o.view(torch.int32)) for o in outs.values())
-        print(f"{name:22s} n={n} {ind}x{outd}: row per lane 4/2 {res[0]:.3f} ms, 7/5 {res[1]:.3f} ms, "
-              f"rows shared by lanes {res[2]:.3f} ms, 4 chain + 4 copy warps per block 6/4 {res[3]:.3f} ms, "
-              f"10/8 {res[4]:.3f} ms ({res[4] * 1e6 * 1.95 / n:.1f} cycles per row); "
-              f"bit-identical: {same}", flush=True)
+        print(f"{name:22s} n={n} {ind}x{outd}: bit-identical {same}", flush=True)
+        for si, st in enumerate(SETTINGS):
+            print(f"    {json.dumps(st):48s} {res[si]:8.3f} ms  ({res[si] * 1e6 * 1.95 / n:5.1f} cycles per row)",
+                  flush=True)
         del y, g, ids, outs
         torch.cuda.empty_cache()
 
