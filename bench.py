@@ -571,7 +571,10 @@ def main():
         bound = "l2-gather" if achieved > peak else "hbm"
     roofline = {"bound": bound, "achieved": round(achieved, 1), "peak": peak,
                 "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                "kernel": f"k_agg_vec4 (path SG_{p.layer}, width {dims[dom]})",
+                # the library's default kernel for this call (tuning vec8 auto:
+                # rows wider than 64 columns from 2^21 edges per call)
+                "kernel": (f"{'k_agg_vec8' if dims[dom] > 64 and p.E >= (1 << 21) else 'k_agg_vec4'} "
+                           f"(path SG_{p.layer}, width {dims[dom]})"),
                 "algorithmic_bytes_per_launch": dom_bytes, "avg_launch_ms": round(dom_ms, 4),
                 "peak_source": peak_src,
                 "frac_note": ("frac = no-reuse algorithmic bytes (SURVEY §8d B_l) / avg launch time / HBM peak; "
