@@ -115,8 +115,10 @@ constexpr TuneKey kTuneKeys[] = {
     // W': 1 / 2 = 4 chain + 4 copy warps per block, one chain warp per SMSP
     // (6 / 10 ring slots). Alone it is faster (products 10.6 -> 7.7 ms), but
     // holding whole SMs it slows the forked chains it overlaps (products
-    // backward_epp 17.0 -> 28.6 ms, profiles/atb_quad_sweep_r02.log): off
-    {"atb_quad", "PG_ATB_QUAD", 0},
+    // backward_epp 17.0 -> 28.6 ms, profiles/atb_quad_sweep_r02.log); 3
+    // (default) = only for W' over whole matrices (no row gather: the
+    // all-active / if-else / Global EPP chains, products 47 -> 39 ms)
+    {"atb_quad", "PG_ATB_QUAD", 3},
     // host drop-in below host_min_mb: D2H-overlap chunks (0/1 = off; the
     // Reddit top path split in 2 computes 0.94 vs 0.62 ms, so no gain:
     // profiles/e2e_small_chunks_sweep_r02.log)

@@ -1074,7 +1074,12 @@ void gemm_at_b(DMat a, const uint32_t* a_rows, DMat b, DMat out, cudaStream_t s)
                     reinterpret_cast<uintptr_t>(b.p) % 16 == 0;
     // (wide outputs only: at c = 16 / 41 the 32-column tiles leave chain
     // warps idle and the split kernel wins, Reddit 1.92 vs 1.32 ms)
-    if (tuning(kTuneAtbQuad) && tuning(kTuneAtbSplit) && v4 && c >= 64) {
+    // atb_quad 3 (default): only for W' over whole matrices (no row
+    // gather: the all-active / if-else / Global EPP chains, products 47 ->
+    // 39 ms); beside the Local EPP chain's SpMM it lost (16.7 -> 28.6 ms)
+    const int64_t quad = tuning(kTuneAtbQuad);
+    const bool quad_on = quad == 1 || quad == 2 || (quad == 3 && !a_rows);
+    if (quad_on && tuning(kTuneAtbSplit) && v4 && c >= 64) {
         int dev = 0, sms = 148;
         PG_CUDA(cudaGetDevice(&dev));
         PG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));

@@ -257,7 +257,7 @@ def test_random_chains(pg, orc, cuda, seed):
     case = (n_req, n_req * int(rng.choice([3, 8, 20])), 90 + seed, float(rng.choice([0.05, 0.3, 1.0])), L, f,
             hidden, classes, bool(seed % 2))
     knobs = {"atb_split": int(rng.integers(0, 2)), "atb_pairs": int(rng.choice([1, 224])),
-             "atb_depth": int(rng.integers(0, 3)), "atb_quad": int(rng.integers(0, 3)),
+             "atb_depth": int(rng.integers(0, 3)), "atb_quad": int(rng.integers(0, 4)),
              "gemm_packed": int(rng.integers(0, 3)), "wgrad_fork": int(rng.integers(0, 2)),
              "gemm3_rows": int(rng.choice([8, 16])), "gemm_beside_wgrad": int(rng.integers(0, 2)),
              "vec8": int(rng.integers(0, 3))}
