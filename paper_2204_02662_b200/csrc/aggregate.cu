@@ -133,8 +133,10 @@ constexpr TuneKey kTuneKeys[] = {
     {"grp_dynamic", "PG_GRP_DYNAMIC", 0},
     // k_agg_vec8 wide rows: edges per batch per half-warp (0 = 4; 3, 6)
     {"vec8_u", "PG_VEC8_U", 0},
+    // row-range calls (host pipeline chunks, shards): 1 = hubs on the side kernel, 0 = inline front
+    {"range_side_hubs", "PG_RANGE_SIDE_HUBS", 1},
 };
-static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneVec8U + 1,
+static_assert(sizeof(kTuneKeys) / sizeof(kTuneKeys[0]) == kTuneRangeSideHubs + 1,
               "kTuneKeys and enum TuneKeyId (pg_internal.h) must list the same keys in the same order");
 std::atomic<int64_t> g_tune[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];
 int64_t g_tune_def[sizeof(kTuneKeys) / sizeof(kTuneKeys[0])];  // $PG_<KEY> at load, else built-in

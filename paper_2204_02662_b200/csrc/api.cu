@@ -367,7 +367,9 @@ void pg::run_aggregate(Groups& G, bool parent_indexed, uint32_t rb, uint32_t re,
         // row range: schedule of rows [rb, re) relative to rb (cached)
         Groups::RowSched* rs = row_sched(G, rb, re);
         AggExt er = ext;
-        er.side_hubs = true;  // a row range: hub chains on the deeper-pipelined side kernel
+        // a row range: hub chains on the deeper-pipelined side kernel
+        // (tuning range_side_hubs 0: as the main kernel's front instead)
+        er.side_hubs = tuning(kTuneRangeSideHubs) != 0;
         er.avg_degree = rs->hist.edges / range_div / std::max<uint64_t>(1, re - rb);
         er.n_edges = rs->hist.edges / range_div;
         const uint32_t nh = rs->hist.heavy(heavy_degree(dim, rs->hist.edges / range_div));

@@ -382,7 +382,8 @@ enum TuneKeyId {
     kTuneVec8 = 46,
     kTuneF64HubMin = 47,
     kTuneGrpDynamic = 48,
-    kTuneVec8U = 49
+    kTuneVec8U = 49,
+    kTuneRangeSideHubs = 50
 };
 // whole-row SpMM warps (k_agg_row) for this width (tuning "row_kernel")
 bool row_kernel_on(uint64_t dim);

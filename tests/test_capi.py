@@ -105,7 +105,7 @@ def test_tuning_keys(pg):
                 "gemm_tc", "rec_window", "src_seg_balance", "host_min_mb", "row_kernel", "row_u", "row_seg_mb",
                 "row_heavy", "vec_block", "hub_inline", "hub_front_min", "gemm3_rows", "gemm_beside_wgrad", "host_hub_chunk_side", "vec_window", "host_hub_min", "grouped_src_segs", "narrow_u", "atb_depth",
                 "host_first_chunk_pct", "host_seq", "atb_quad",
-                "host_small_chunks", "vec8", "f64_hub_min", "grp_dynamic", "vec8_u"):
+                "host_small_chunks", "vec8", "f64_hub_min", "grp_dynamic", "vec8_u", "range_side_hubs"):
         pg.set_tuning(key, None)
     import pytest
 
