@@ -30,6 +30,9 @@ KNOBS = {
     "row_seg_mb": (8, 56),
     "vec_block": (256, 256, 512, 1024),
     "vec8": (0, 1, 2, 2),
+    "vec8_u": (0, 0, 3, 6),
+    "range_side_hubs": (1, 1, 0),
+    "grp_dynamic": (0, 1),
     "hub_inline": (0, 1, 1),
     "hub_front_min": (0, 0, 16, 256),
 }
