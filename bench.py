@@ -996,31 +996,45 @@ def shard_projection(pg, torch, paths, groups, y_full, dims, ep_bytes, nvlink_gb
     (N-1)/N of the parent rows it does not own) is modelled at nvlink_gbs and
     either hidden under the SpMM (the library overlaps it per owner) or added
     (no overlap). A projection, not a measurement: reported so the shard
-    balance and the compute side of the scaling are on record."""
+    balance and the compute side of the scaling are on record. The cuts are
+    the ones an N-GPU run uses: edge-balanced, then calibrated on the
+    measured shard times (dist.calibrate_bounds; $PG_CALIBRATE_SHARDS=0:
+    edge-balanced only)."""
+    from paper_2204_02662_b200 import dist as pgd
+
+    calibrate = os.environ.get("PG_CALIBRATE_SHARDS", "1") == "1"
     out = {"note": ("projection from single-GPU shard timings (each rank's rows run alone through the row-range "
                     f"call) + the y_grad exchange modelled at {nvlink_gbs:.0f} GB/s per GPU; not a multi-GPU "
-                    "measurement"), "per_n": []}
+                    "measurement"), "cuts": "edge-balanced, calibrated" if calibrate else "edge-balanced",
+           "per_n": []}
     for world in (2, 4, 8):
-        rank_max, xch = [], []
+        rank_max, xch, edge_bal = [], [], []
         for i, p in enumerate(paths):
-            b = p.shard_bounds(world)
             y = y_full[i][:, : dims[i]]
-            ts = []
-            for r in range(world):
-                x = pg.empty_rows(int(b[r + 1] - b[r]), dims[i])
-                pg.backward_aggregation(groups[i], y, x, overwrite=True, rows=(int(b[r]), int(b[r + 1])))
+
+            def time_shard(b0, b1, i=i, y=y):
+                x = pg.empty_rows(b1 - b0, dims[i])
+                pg.backward_aggregation(groups[i], y, x, overwrite=True, rows=(b0, b1))
                 a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record()
                 for _ in range(3):
-                    pg.backward_aggregation(groups[i], y, x, overwrite=True, rows=(int(b[r]), int(b[r + 1])))
+                    pg.backward_aggregation(groups[i], y, x, overwrite=True, rows=(b0, b1))
                 z.record()
                 torch.cuda.synchronize()
-                ts.append(a.elapsed_time(z) / 3)
+                return a.elapsed_time(z) / 3
+
+            b = p.shard_bounds(world)
+            if calibrate:
+                _, t0, ts = pgd.calibrate_bounds(time_shard, p.export()["offsets"], b, iters=2)
+                edge_bal.append(round(max(t0), 4))
+            else:
+                ts = [time_shard(int(b[r]), int(b[r + 1])) for r in range(world)]
             rank_max.append(max(ts))
             xch.append(p.P * dims[i] * 4 * (world - 1) / world / (nvlink_gbs * 1e9) * 1e3)
         overlap = sum(max(a, b) for a, b in zip(rank_max, xch))
         serial = sum(a + b for a, b in zip(rank_max, xch))
         out["per_n"].append({"n_gpus": world, "spmm_rank_max_ms": [round(x, 4) for x in rank_max],
+                             "spmm_rank_max_ms_edge_balanced": edge_bal or None,
                              "exchange_model_ms": [round(x, 4) for x in xch],
                              "epoch_ms_overlapped": round(overlap, 4), "epoch_ms_serial": round(serial, 4),
                              "GBps_overlapped": round(ep_bytes / (overlap / 1e3) / 1e9, 1)})
