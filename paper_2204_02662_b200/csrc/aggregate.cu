@@ -51,7 +51,9 @@ constexpr TuneKey kTuneKeys[] = {
     // (k_agg_hub_ring: measured slower, its ~80 KB ring holds only 32 rows in
     // flight per hub, profiles/e2e_hub_ring_sweep_r02.log); 4 = cooperative
     // 64-row tiles (k_agg_heavy_coop<32>: slower still, 64 KB + 256 threads
-    // per hub chunk, profiles/e2e_hub_coop_sweep_r02.log); 0 = k_agg_wide_lat
+    // per hub chunk, profiles/e2e_hub_coop_sweep_r02.log); 5 = float2 lanes,
+    // 64 rows in flight per chain (k_agg_wide_pipe2: e2e 23.2-23.5 vs 23.0-23.2
+    // ms, profiles/hub_pipe2_sweep_r02.log); 0 = k_agg_wide_lat
     {"heavy_wide_pipe", "PG_HEAVY_WIDE_PIPE", 1},
     {"host_final_segs", "PG_HOST_FINAL_SEGS", 1},  // host drop-in: trailing source segments of the chunked last pass
     {"host_pitch2d", "PG_HOST_PITCH2D", 0},  // host drop-in: odd widths by 2-D DMA (1) or flat DMA + repack kernel (0)
@@ -1386,6 +1388,97 @@ __global__ void __launch_bounds__(64) k_agg_wide_pipe(const uint64_t* __restrict
 
 
 // Scalar fallback for unaligned rows (ld or base not 16-byte aligned).
+// k_agg_wide_pipe with a float2 per lane (tuning heavy_wide_pipe 5): a hub
+// item covers 64 columns, so the same registers hold twice the rows — U = 32
+// per batch, two batches (64 rows) in flight per chain — and a hub has twice
+// the items. A hub's time is its serial chain: edges x gather latency /
+// rows in flight.
+__device__ __forceinline__ float2 ld_row2(const char* base, uint32_t src, uint32_t ld_bytes) {
+    float2 r;
+    const char* p = base + static_cast<uint64_t>(src) * ld_bytes;
+    asm volatile("ld.global.nc.v2.f32 {%0, %1}, [%2];" : "=f"(r.x), "=f"(r.y) : "l"(p));
+    return r;
+}
+template <int U>
+__global__ void __launch_bounds__(64) k_agg_wide_pipe2(const uint64_t* __restrict__ ebeg,
+                                                      const uint64_t* __restrict__ eend,
+                                                      const Edge* __restrict__ edges,
+                                                      const uint32_t* __restrict__ order, uint32_t d_begin,
+                                                      uint64_t n_items, uint32_t chunks,
+                                                      const float* __restrict__ in, uint32_t ld_in_bytes,
+                                                      float* __restrict__ out, uint64_t ld_out, uint32_t dim,
+                                                      int accumulate, uint32_t zmask, AggExt ext) {
+    static_assert(32 % U == 0, "U divides the 32-record window");
+    const uint64_t item = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+    if (item >= n_items) return;
+    const unsigned lane = lane_id();
+    const uint32_t d = order[d_begin + item / chunks];
+    const uint32_t ci = static_cast<uint32_t>(item % chunks);
+    const uint32_t col = (ci * 32 + lane) * 2;
+    const bool active = col < dim;
+    const uint64_t eb = ebeg[d], ee = eend[d];
+    const uint32_t row = ext_out_row(ext, d);
+    float* orow = out + row * ld_out + col;
+    float2 acc = make_float2(0.f, 0.f);
+    if (accumulate && active) {
+        acc.x = orow[0];
+        if (col + 1 < dim) acc.y = orow[1];
+    }
+    const char* base = reinterpret_cast<const char*>(in) + (active ? col : ci * 64u) * 4u;
+    asm("mov.b64 %0, %0;" : "+l"(base));
+    const uint64_t nb = (ee - eb + U - 1) / U;
+    Edge win = eb + lane < ee ? __ldg(edges + eb + lane) : make_uint2(0u, 0u);
+    Edge nwin = eb + 32 + lane < ee ? __ldg(edges + eb + 32 + lane) : make_uint2(0u, 0u);
+    float2 xa[U], xb[U];
+    float wa[U], wb[U];
+    auto gather = [&](uint64_t b, float2 (&x)[U], float (&w)[U]) {
+        const int s0 = static_cast<int>((b * U) & 31);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t src = __shfl_sync(0xffffffffu, win.x, s0 + u);
+            w[u] = __uint_as_float(__shfl_sync(0xffffffffu, win.y, s0 + u));  // 0 past the end
+            x[u] = ld_row2(base, src, ld_in_bytes);
+        }
+        if (s0 + U == 32) {  // window consumed: slide
+            win = nwin;
+            const uint64_t e = eb + (b + 1) * U + 32 + lane;
+            nwin = e < ee ? __ldg(edges + e) : make_uint2(0u, 0u);
+        }
+    };
+    auto fold = [&](const float2 (&x)[U], const float (&w)[U]) {
+        uint32_t all = 0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) all ^= __float_as_uint(x[u].x);
+        all &= zmask;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const float wu = __uint_as_float(__float_as_uint(w[u]) ^ all);
+            acc.x = __fadd_rn(acc.x, __fmul_rn(wu, x[u].x));
+            acc.y = __fadd_rn(acc.y, __fmul_rn(wu, x[u].y));
+        }
+    };
+    if (nb) gather(0, xa, wa);
+    for (uint64_t b = 0; b < nb; b += 2) {
+        if (b + 1 < nb) gather(b + 1, xb, wb);  // in flight while batch b folds
+        fold(xa, wa);
+        if (b + 1 < nb) {
+            if (b + 2 < nb) gather(b + 2, xa, wa);
+            fold(xb, wb);
+        }
+    }
+    if (!active) return;
+    acc.x = __fadd_rn(acc.x, 0.f);
+    acc.y = __fadd_rn(acc.y, 0.f);
+    if (ext.relu_pre) {
+        const uint32_t prow = ext.pre_rows ? __ldg(ext.pre_rows + d) : row;
+        const float* pr = ext.relu_pre + static_cast<uint64_t>(prow) * ext.ld_pre + col;
+        acc.x = pr[0] > 0.f ? acc.x : 0.f;
+        if (col + 1 < dim) acc.y = pr[1] > 0.f ? acc.y : 0.f;
+    }
+    orow[0] = acc.x;
+    if (col + 1 < dim) orow[1] = acc.y;
+}
+
 template <int U>
 __global__ void __launch_bounds__(256) k_agg_scalar(const uint64_t* __restrict__ ebeg, const uint64_t* __restrict__ eend,
                                                    const Edge* __restrict__ edges,
@@ -2757,6 +2850,13 @@ void aggregate_det(const uint64_t* ebeg, const uint64_t* eend, const Edge* edges
                 (reinterpret_cast<uintptr_t>(in) & 15) == 0) {
                 launch_hub_ring(ebeg, eend, edges, order, d_begin, nh, in, ld_in, out, ld_out, dim32, accumulate, ss.s,
                                 ext);
+            } else if (tuning(kTuneHeavyWidePipe) == 5 && ld_in % 2 == 0 && (reinterpret_cast<uintptr_t>(in) & 7) == 0) {
+                const uint32_t ch2 = (dim32 + 63) / 64;
+                const uint64_t it2 = static_cast<uint64_t>(nh) * ch2;
+                k_agg_wide_pipe2<32><<<grid_for(it2 * 32, 64), 64, 0, ss.s>>>(
+                    ebeg, eend, edges, order, d_begin, it2, ch2, in, static_cast<uint32_t>(ld_in * 4), out, ld_out,
+                    dim32, accumulate, 0u, ext);
+                PG_LAUNCH("k_agg_wide_pipe2");
             } else if (tuning(kTuneHeavyWidePipe) >= 1) {
                 k_agg_wide_pipe<16><<<grid_for(items * 32, 64), 64, 0, ss.s>>>(
                     ebeg, eend, edges, order, d_begin, items, chunks, in, static_cast<uint32_t>(ld_in * 4), out,

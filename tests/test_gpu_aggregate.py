@@ -148,7 +148,8 @@ def test_heavy_ring_kernel_bit_exact(pg, orc, dim, heavy_min, kern):
                                      {"hub_inline": 0, "heavy_wide_pipe": 4}, {"vec8": 1},
                                      {"vec8": 1, "vec_u": 4}, {"vec8": 1, "hub_inline": 0},
                                      {"vec8": 1, "vec8_u": 3}, {"vec8": 1, "vec8_u": 6},
-                                     {"range_side_hubs": 0}, {"range_side_hubs": 0, "vec8": 1}])
+                                     {"range_side_hubs": 0}, {"range_side_hubs": 0, "vec8": 1},
+                                     {"hub_inline": 0, "heavy_wide_pipe": 5}])
 @pytest.mark.parametrize("dim", [130, 300, 602, 700])
 def test_wide_row_schedule_variants_bit_exact(pg, orc, dim, variant):
     """The measured-and-kept-selectable wide-row schedules:

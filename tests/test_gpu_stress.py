@@ -19,7 +19,7 @@ KNOBS = {
     "chunk_major": (0, 1),
     "ld_cg": (0, 2, 7),
     "heavy_narrow": (0, 1),
-    "heavy_wide_pipe": (0, 1, 2, 3, 4),
+    "heavy_wide_pipe": (0, 1, 2, 3, 4, 5),
     "wide_lpd": (16, 32),
     "src_segs": (0, 1, 2, 3),
     "src_seg_balance": (0, 50, 100),
